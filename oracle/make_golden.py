@@ -1,0 +1,238 @@
+"""Generate golden vectors by running the REFERENCE in place (this container only).
+
+    PYTHONDONTWRITEBYTECODE=1 python oracle/make_golden.py
+
+Imports `splatlod` from /root/reference/pkg/src (read-only) and writes
+tests/golden/*.npz.  The per-tile member lists are internal to
+`splatlod.raster.rasterize` (src/raster.py:421-438); they are captured by
+wrapping `splatlod.raster._composite_tile`, which rasterize looks up in its
+module globals for every tile (src/raster.py:430).
+
+Files:
+  cases.npz    small projection/raster cases mirroring tests/test_raster.py
+               (random_scene, face_on_camera, SH degrees 0..3, culling, empty,
+               modulation, alpha_min=0, dilation 0, odd resolutions).
+  config1.npz  BASELINE config 1 (SURVEY.md 8d recipe): deep_street 10k,
+               2 LOD levels, 4 chunks, 8 views at 128x128, stateless blend.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
+sys.path.insert(0, REF)
+
+import splatlod.raster as R  # noqa: E402
+from splatlod.blending import blend_factor, compose_active, nearest_two_chunks  # noqa: E402
+from splatlod.chunks import (ChunkBuildConfig, build_chunk_active_sets, chunk_radii,  # noqa: E402
+                             kmeans_positions, visibility_filter_chunk)
+from splatlod.lod import (LodBuildConfig, build_levels, mean_focal,  # noqa: E402
+                          project_selection)
+from splatlod.scene import Camera, ChunkPlan, LodLevel, Scene  # noqa: E402
+from splatlod.synthetic import deep_street, face_on_camera, random_scene  # noqa: E402
+from splatlod.thresholds import default_grid, greedy_search  # noqa: E402
+
+_captured = []
+_orig_composite = R._composite_tile
+
+
+def _capture(tile_x, tile_y, members, *args, **kw):
+    _captured.append((tile_x, tile_y, np.array(members)))
+    return _orig_composite(tile_x, tile_y, members, *args, **kw)
+
+
+R._composite_tile = _capture
+
+
+def rasterize_with_lists(batch, cam, cfg, need_image=True, record_max_weight=True):
+    """Run the reference rasterize and return its output plus its per-tile
+    lists as (tile_offsets (T+1), tile_src (P)) in tile-major order."""
+    _captured.clear()
+    out = R.rasterize(batch, cam, cfg, need_image=need_image, record_max_weight=record_max_weight)
+    w, h = cam.resolution
+    tx, ty = -(-w // 16), -(-h // 16)
+    T = tx * ty
+    lists = [np.zeros(0, np.int64)] * T
+    if len(batch):
+        order = np.lexsort((batch.source_index, batch.depth))
+        src_sorted = batch.source_index[order]
+        for (x, y, members) in _captured:
+            lists[y * tx + x] = src_sorted[members]
+    offs = np.zeros(T + 1, np.int64)
+    offs[1:] = np.cumsum([len(l) for l in lists])
+    tile_src = np.concatenate(lists) if offs[-1] else np.zeros(0, np.int64)
+    return out, offs, tile_src
+
+
+def cam_arrays(cam: Camera, prefix: str, d: dict):
+    d[prefix + "R"] = cam.rotation_matrix
+    d[prefix + "pos"] = cam.position
+    d[prefix + "focal"] = cam.focal
+    d[prefix + "pp"] = cam.principal_point
+    d[prefix + "res"] = np.array(cam.resolution, np.int64)
+    d[prefix + "near"] = np.array(cam.near_plane)
+    d[prefix + "quat"] = cam.orientation
+
+
+def scene_arrays(scene: Scene, prefix: str, d: dict):
+    d[prefix + "means"] = scene.means
+    d[prefix + "scales"] = scene.scales
+    d[prefix + "rotations"] = scene.rotations
+    d[prefix + "opacities"] = scene.opacities
+    d[prefix + "sh"] = scene.sh_coeffs
+    d[prefix + "fv"] = scene.filter_variance
+    d[prefix + "deg"] = np.array(scene.sh_degree)
+
+
+def batch_arrays(b, prefix, d):
+    d[prefix + "n_inputs"] = np.array(b.n_inputs)
+    d[prefix + "src"] = b.source_index
+    d[prefix + "mean2d"] = b.mean2d
+    d[prefix + "cov2d"] = b.cov2d
+    d[prefix + "conic"] = b.conic
+    d[prefix + "extent"] = b.extent
+    d[prefix + "depth"] = b.depth
+    d[prefix + "opacity"] = b.opacity_eff
+    d[prefix + "color"] = b.color
+
+
+def out_arrays(out, offs, tile_src, prefix, d):
+    if out.image is not None:
+        d[prefix + "image"] = out.image
+    d[prefix + "tile_count"] = out.per_tile_count
+    d[prefix + "visible"] = out.per_pixel_visible
+    if out.per_gaussian_max_weight is not None:
+        d[prefix + "maxw"] = out.per_gaussian_max_weight
+    d[prefix + "tile_offsets"] = offs
+    d[prefix + "tile_src"] = tile_src
+
+
+def cfg_arrays(cfg, prefix, d):
+    d[prefix + "cfg"] = np.array([cfg.alpha_clamp, cfg.alpha_min, cfg.t_min, cfg.dilation2d])
+
+
+def make_cases():
+    d = {}
+    cases = []
+    face = face_on_camera()
+    # (name, scene, camera, cfg, indices, modulation)
+    for seed in range(3):
+        cases.append((f"rand{seed}_amin0", random_scene(seed, 300), face,
+                      R.RasterConfig(alpha_min=0.0), None, None))
+    cases.append(("rand21_default", random_scene(21, 400), face, R.RasterConfig(), None, None))
+    cases.append(("rand6_behind", random_scene(6, 200, box_min=(-3, -3, -6), box_max=(3, 3, 12)),
+                  face, R.RasterConfig(), None, None))
+    cases.append(("rand5_nodil", random_scene(5, 400), face, R.RasterConfig(dilation2d=0.0),
+                  None, None))
+    for deg in (0, 2, 3):
+        cases.append((f"sh{deg}", random_scene(30 + deg, 350, sh_degree=deg), face,
+                      R.RasterConfig(), None, None))
+    sc = random_scene(40, 900, box_min=(-3, -3, -2), box_max=(3, 3, 12))
+    rng = np.random.default_rng(3)
+    idx = np.sort(rng.choice(900, 500, replace=False))
+    cases.append(("subset_mod", sc, face, R.RasterConfig(), idx, rng.uniform(0, 1, 500)))
+    cases.append(("empty", Scene.empty(1), face, R.RasterConfig(), None, None))
+    far = random_scene(41, 50, box_min=(100, 100, 2), box_max=(120, 120, 12))
+    cases.append(("all_culled", far, face, R.RasterConfig(), None, None))
+    odd = Camera((0.0, 0.0, 0.0), (1.0, 0.0, 0.0, 0.0), (60.0, 55.0), (50.0, 35.0), (100, 70),
+                 near_plane=0.05)
+    cases.append(("odd_res", random_scene(42, 700), odd, R.RasterConfig(), None, None))
+    yaw = Camera((0.3, -0.2, -1.0), (0.9659258262890683, 0.0, 0.25881904510252074, 0.0),
+                 (48.0, 48.0), (40.0, 32.0), (80, 64), near_plane=0.05)
+    cases.append(("yawed", random_scene(43, 800, box_min=(-6, -3, -2), box_max=(6, 3, 12)), yaw,
+                  R.RasterConfig(), None, None))
+    big = random_scene(44, 60, box_min=(-1, -1, 3), box_max=(1, 1, 4))
+    big = Scene(big.means, big.scales * 4.0, big.rotations, big.opacities, big.sh_coeffs,
+                np.full(60, 0.05), 1)
+    cases.append(("huge_filtered", big, face, R.RasterConfig(), None, None))
+    names = []
+    for (name, scene, cam, cfg, idx, mod) in cases:
+        p = name + "/"
+        names.append(name)
+        scene_arrays(scene, p, d)
+        cam_arrays(cam, p, d)
+        cfg_arrays(cfg, p, d)
+        if idx is not None:
+            d[p + "idx"] = np.asarray(idx, np.int64)
+        if mod is not None:
+            d[p + "mod"] = np.asarray(mod, np.float64)
+        b = R.project_scene(scene, cam, cfg, indices=idx, modulation=mod)
+        batch_arrays(b, p + "b_", d)
+        out, offs, tsrc = rasterize_with_lists(b, cam, cfg)
+        out_arrays(out, offs, tsrc, p + "o_", d)
+    d["names"] = np.array(names)
+    return d
+
+
+def make_config1():
+    t0 = time.time()
+    scene, cams = deep_street(seed=7, n_fine=4380, n_views=8, resolution=(128, 128),
+                              focal=104.0, length=200.0)
+    assert len(scene) == 10000, len(scene)
+    cfg = LodBuildConfig(importance_views=tuple(cams), reference_focal=mean_focal(cams))
+    base = LodLevel.base(scene)
+    grid = list(default_grid(base, cams, 12))
+    accepted, _ = greedy_search(base, cams, cfg, grid, max_levels=1)
+    levels, _ = build_levels(scene, accepted, cfg)
+    positions = np.stack([c.position for c in cams])
+    centers, assign = kmeans_positions(positions, 4, seed=0)
+    radii = chunk_radii(centers, positions)
+    plan = build_chunk_active_sets(levels, centers, radii, assign)
+    ccfg = ChunkBuildConfig(d1=accepted[0], kmeans_seed=0, perturb_count=4, perturb_seed=0,
+                            vis_threshold=cfg.gamma)
+    filtered = []
+    for j in range(plan.n_chunks):
+        cams_j = [cams[i] for i in np.flatnonzero(assign == j)]
+        filtered.append(visibility_filter_chunk(plan, j, levels, cams_j, ccfg, cfg.raster))
+    plan = ChunkPlan(centers, radii, tuple(filtered), assign)
+    print("config1 build", round(time.time() - t0, 1), "s; d1", accepted,
+          "levels", [len(l) for l in levels],
+          "sets", [[len(s) for s in ch] for ch in plan.active_sets])
+    d = {"thresholds": np.array(accepted, np.float64)}
+    for l, lv in enumerate(levels):
+        scene_arrays(lv.scene, f"L{l}/", d)
+        d[f"L{l}/depth_threshold"] = np.array(lv.depth_threshold)
+    d["n_levels"] = np.array(len(levels))
+    d["centers"] = plan.centers
+    d["radii"] = plan.radii
+    for j in range(plan.n_chunks):
+        for l in range(plan.n_levels):
+            d[f"set/{j}/{l}"] = plan.active_sets[j][l]
+    rc = R.RasterConfig()
+    cfg_arrays(rc, "", d)
+    for v, cam in enumerate(cams):
+        p = f"v{v}/"
+        cam_arrays(cam, p, d)
+        f, o = nearest_two_chunks(plan, cam.position)
+        t_bar, t = blend_factor(cam.position, plan.centers[f], plan.centers[o])
+        d[p + "pair"] = np.array([f, o])
+        d[p + "t"] = np.array([t_bar, t])
+        sel = compose_active(plan, levels, f, o, t)
+        for l in range(len(levels)):
+            d[p + f"sel{l}"] = sel.sets[l]
+            d[p + f"mod{l}"] = sel.modulations[l]
+        batch = project_selection(levels, sel.sets, cam, rc, modulations=sel.modulations)
+        batch_arrays(batch, p + "b_", d)
+        out, offs, tsrc = rasterize_with_lists(batch, cam, rc)
+        out_arrays(out, offs, tsrc, p + "o_", d)
+    return d
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    t0 = time.time()
+    np.savez_compressed(os.path.join(OUT, "cases.npz"), **make_cases())
+    print("cases", round(time.time() - t0, 1), "s")
+    np.savez_compressed(os.path.join(OUT, "config1.npz"), **make_config1())
+    for f in sorted(os.listdir(OUT)):
+        print(f, os.path.getsize(os.path.join(OUT, f)) // 1024, "KiB")
+
+
+if __name__ == "__main__":
+    main()
