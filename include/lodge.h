@@ -1,0 +1,204 @@
+/*
+ * lodge.h -- C ABI of the B200-native LODGE per-frame renderer (liblodge.so).
+ *
+ * Drop-in boundary for the reference `splatlod` render path.
+ * The reference is pure Python; its "FFI" is the Python API re-exported by
+ * src/__init__.py:3-21.  Each entry point below replaces one group of those
+ * functions; paper_2505_23158_b200/ binds them with ctypes.
+ *
+ * Conventions
+ *   - Every pointer argument named *_dev is a CUDA device pointer on the
+ *     context's device.  The library never frees caller memory.
+ *   - All work is asynchronous on the context stream (lodge_set_stream);
+ *     entry points that return a host-visible size say so explicitly.
+ *   - Status: 0 ok, <0 one of LODGE_ERR_*; lodge_last_error() returns a
+ *     thread-local message.  A context is not thread-safe; use one per GPU.
+ *   - Results are deterministic bit-for-bit run to run: ordered compaction,
+ *     stable radix sorts, order-independent atomicMax on float bits.
+ */
+#ifndef LODGE_H
+#define LODGE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LODGE_OK 0
+#define LODGE_ERR_BAD_ARG (-1)
+#define LODGE_ERR_CUDA (-2)
+#define LODGE_ERR_OOM (-3)
+#define LODGE_ERR_CAPACITY (-4)
+
+#define LODGE_MAX_LEVELS 8
+
+typedef struct lodge_ctx lodge_ctx;
+
+/* Camera (src/scene.py:80-121).  R is Camera.rotation_matrix (world ->
+ * camera, row-major), computed on the host exactly as the reference does. */
+typedef struct {
+  double R[9];
+  double pos[3];
+  double fx, fy, cx, cy;
+  int32_t w, h;
+  double near_plane;
+} lodge_camera;
+
+/* RasterConfig (src/raster.py:39-56); `threads` has no device meaning. */
+typedef struct {
+  double alpha_clamp, alpha_min, t_min, dilation2d;
+} lodge_raster_params;
+
+/* One LOD level resident on the device (src/scene.py:124-226).
+ * geom: n records of 12 values [mean xyz, scale xyz, rot wxyz, opacity,
+ *       filter_variance], fp64 (96 B) or fp32 (48 B) per LODGE_GEOM_FP32.
+ * sh:   (n, 3, (deg+1)^2) coefficients, fp64 or fp32 per LODGE_SH_FP32.
+ * Arithmetic is fp64 either way (fp32 storage is the asset's native
+ * precision, src/assets.py:240-254). */
+#define LODGE_GEOM_FP32 1
+#define LODGE_SH_FP32 2
+typedef struct {
+  int64_t n;
+  int32_t sh_degree;
+  int32_t flags;
+  const void *geom_dev;
+  const void *sh_dev;
+} lodge_level;
+
+/* Chunk plan (src/scene.py:229-272): K centres (fp64, K x 3) and K*L sorted
+ * uint32 index sets, set (j, l) = data[offsets[j*L+l] .. offsets[j*L+l+1]). */
+typedef struct {
+  int32_t K, L;
+  const double *centers_dev;
+  const int64_t *offsets_dev;
+  const uint32_t *data_dev;
+  int64_t max_set[LODGE_MAX_LEVELS]; /* host-side: max_j |set(j,l)| */
+} lodge_chunks;
+
+/* Compositing precision.  FAST: fp32 FMA/MUFU compositing with an fp64
+ * guard band that re-decides the q<=9 and alpha>=alpha_min cut-offs exactly;
+ * EXACT: fp64 compositing that reproduces the reference's blocked
+ * transmittance product (src/raster.py:346-373). Projection is fp64 in both. */
+#define LODGE_PREC_FAST 0
+#define LODGE_PREC_EXACT 1
+
+/* Render flags */
+#define LODGE_NEED_IMAGE 1
+#define LODGE_RECORD_MAX 2
+
+/* Device outputs of one frame (src/raster.py:119-127).  image is float
+ * (FAST) or double (EXACT), (h, w, 3); tile_count (tiles_y*tiles_x) int32;
+ * visible (h*w) int32; maxw (n_inputs) float (FAST) or double (EXACT),
+ * zeroed by the library.  Any pointer may be NULL if its flag is off. */
+typedef struct {
+  void *image_dev;
+  int32_t *tile_count_dev;
+  int32_t *visible_dev;
+  void *maxw_dev;
+} lodge_frame_out;
+
+/* Per-frame scalars written by the device (lodge_render_frame /
+ * lodge_rasterize): read back after the stream completes. */
+typedef struct {
+  int32_t f, o;          /* chunk pair (o = -1: single chunk) */
+  double t_bar, t;       /* blend factor */
+  uint32_t U;            /* active inputs (n_inputs of the batch) */
+  uint32_t U_level[LODGE_MAX_LEVELS];
+  uint32_t M;            /* survivors after culling */
+  uint32_t P;            /* tile-splat pairs */
+  uint32_t overflow;     /* 1 if P exceeded the pair capacity */
+  uint32_t guard_hits;   /* FAST: pixel-splat decisions re-checked in fp64 */
+} lodge_frame_stats;
+
+/* ---- context ---------------------------------------------------------- */
+int lodge_create(int32_t device, lodge_ctx **out);
+void lodge_destroy(lodge_ctx *ctx);
+const char *lodge_last_error(void);
+int lodge_set_stream(lodge_ctx *ctx, void *cuda_stream);
+/* Reserve workspace: survivors M and pairs P.  Grown automatically by the
+ * synchronous entry points; the async frame path reports overflow. */
+int lodge_reserve(lodge_ctx *ctx, int64_t max_splats, int64_t max_pairs);
+int lodge_set_precision(lodge_ctx *ctx, int32_t precision);
+
+/* ---- chunk selection: nearest_two_chunks + blend_factor ---------------
+ * replaces src/blending.py:77-99.  n positions (fp64 x3) -> f, o, t_bar, t.
+ * Bit-exact with the reference's fp64 arithmetic. */
+int lodge_select(lodge_ctx *ctx, const double *centers_dev, int32_t K,
+                 const double *positions_dev, int32_t n, int32_t *f_dev, int32_t *o_dev,
+                 double *t_bar_dev, double *t_dev);
+
+/* blend_factor for explicit centres (src/blending.py:87-99): in_dev holds n
+ * rows [position xyz, m_f xyz, m_o xyz]; out_dev n rows [|m_f-m_o|^2, t_bar,
+ * t].  The caller raises when the first column is <= 0. */
+int lodge_blend_factor(lodge_ctx *ctx, const double *in_dev, int32_t n, double *out_dev);
+
+/* ---- compose_active: union of two chunks' sets with modulation ---------
+ * replaces src/blending.py:102-129.  Synchronous (returns sizes).
+ * out_idx_dev[l] / out_tag_dev[l] need |A_l|+|B_l| slots; tag 3 = both,
+ * 1 = primary only (mod t), 2 = other only (mod 1-t).  o = -1: single chunk. */
+int lodge_compose(lodge_ctx *ctx, const lodge_chunks *chunks, int32_t f, int32_t o,
+                  uint32_t **out_idx_dev, uint8_t **out_tag_dev, int64_t *out_sizes);
+
+/* ---- project_scene for one level (compat path) ------------------------
+ * replaces src/raster.py:188-291.  idx_dev: n int64 indices (NULL = all);
+ * mod_dev: n fp64 modulation (NULL = none).  Writes the survivors in input
+ * order as the reference's Splat2DBatch fields (fp64, int64 source index).
+ * Synchronous; returns M in *out_m. */
+typedef struct {
+  int64_t *src_dev;     /* (M,) */
+  double *mean2d_dev;   /* (M,2) */
+  double *cov2d_dev;    /* (M,2,2) */
+  double *conic_dev;    /* (M,3) */
+  double *extent_dev;   /* (M,2) */
+  double *depth_dev;    /* (M,) */
+  double *opacity_dev;  /* (M,) */
+  double *color_dev;    /* (M,3) */
+} lodge_batch;
+int lodge_project(lodge_ctx *ctx, const lodge_level *level, const int64_t *idx_dev, int64_t n,
+                  const double *mod_dev, const lodge_camera *cam,
+                  const lodge_raster_params *rp, int32_t shade, lodge_batch *out,
+                  int64_t *out_m);
+
+/* ---- rasterize a Splat2DBatch (compat path) ----------------------------
+ * replaces src/raster.py:380-449.  batch fields as above (cov2d unused),
+ * M rows, n_inputs for the max-weight output.  Synchronous; *stats filled.
+ * Optionally returns the sorted per-tile lists: tile_offsets_dev (T+1
+ * int64) and tile_src_dev (source indices, capacity list_cap). */
+int lodge_rasterize(lodge_ctx *ctx, const lodge_batch *batch, int64_t M, int64_t n_inputs,
+                    const lodge_camera *cam, const lodge_raster_params *rp, int32_t flags,
+                    const lodge_frame_out *out, int64_t *tile_offsets_dev,
+                    int64_t *tile_src_dev, int64_t list_cap, lodge_frame_stats *stats);
+
+/* ---- fused per-frame path ------------------------------------------------
+ * One camera view rendered end to end on the device: (select ->) union +
+ * modulation -> projection -> depth sort -> binning -> tile sort ->
+ * compositing.  No host synchronisation.  pair: if NULL, the nearest two
+ * chunks are selected on the device for cam->pos (stateless CLI blend mode,
+ * src/cli.py:236-242); else {f, o} with t = *t_override (render_blend_state).
+ * cam_dev is a device copy of the camera (its w,h must equal width,height,
+ * which size the grids); out->maxw_dev must hold the chunk plan's maximum
+ * union size (sum over levels of 2 * max_set).
+ * stats_dev: device lodge_frame_stats (may be NULL). */
+int lodge_render_frame(lodge_ctx *ctx, const lodge_level *levels, int32_t n_levels,
+                       const lodge_chunks *chunks, const lodge_camera *cam_dev, int32_t width,
+                       int32_t height, const lodge_raster_params *rp, const int32_t *pair,
+                       const double *t_override, int32_t flags, const lodge_frame_out *out,
+                       lodge_frame_stats *stats_dev);
+
+/* Inspection of the last frame (async, on the context stream).
+ * lodge_frame_lists: the sorted per-tile lists as source indices (T+1 int64
+ * offsets, up to cap int64 sources; T = tiles of the frame).
+ * lodge_frame_union: level l's union (uint32 indices, uint8 tags), up to cap. */
+int lodge_frame_lists(lodge_ctx *ctx, int32_t T, int64_t *tile_offsets_dev,
+                      int64_t *tile_src_dev, int64_t cap);
+int lodge_frame_union(lodge_ctx *ctx, int32_t level, uint32_t *idx_dev, uint8_t *tag_dev,
+                      int64_t cap);
+
+/* Number of kernels the last lodge_render_frame enqueued. */
+int32_t lodge_last_launch_count(lodge_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

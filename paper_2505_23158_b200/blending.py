@@ -1,0 +1,165 @@
+"""Drop-in runtime chunk selection and two-chunk opacity blending
+(reference src/blending.py).
+
+nearest_two_chunks / blend_factor / compose_active run as liblodge kernels
+(K0 select, K1 union with blend tags, fp64 in the reference's operation
+order); stream_step is the reference's O(1) host state machine restated on
+top of them.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .device import context, plan_for, ptr
+from .lod import project_selection_device
+from .raster import output_to_host, rasterize_device
+from .types import ActiveSelection, BlendState, RasterConfig, StreamEvent
+
+
+def nearest_two_chunks(plan, position) -> tuple:
+    """Ids of the two closest chunk centres; ties go to the lower id (src/blending.py:77-84)."""
+    ctx = context()
+    dp = plan_for(plan, ctx.device)
+    pos = torch.from_numpy(np.ascontiguousarray(position, np.float64).reshape(3)).to(ctx.device)
+    out_i = torch.empty(2, dtype=torch.int32, device=ctx.device)
+    out_d = torch.empty(2, dtype=torch.float64, device=ctx.device)
+    N.check(N.lib().lodge_select(ctx.bind(), ptr(dp.centers), dp.K, ptr(pos), 1, ptr(out_i[0:1]),
+                                 ptr(out_i[1:2]), ptr(out_d[0:1]), ptr(out_d[1:2])),
+            "lodge_select")
+    f, o = (int(v) for v in out_i.cpu().tolist())
+    return f, (None if o < 0 else o)
+
+
+def select_batch(plan, positions, device=None):
+    """nearest_two_chunks + blend_factor for n positions at once (device arrays)."""
+    ctx = context(device)
+    dp = plan_for(plan, ctx.device)
+    pos = torch.as_tensor(np.ascontiguousarray(positions, np.float64).reshape(-1, 3),
+                          device=ctx.device)
+    n = pos.shape[0]
+    f = torch.empty(n, dtype=torch.int32, device=ctx.device)
+    o = torch.empty(n, dtype=torch.int32, device=ctx.device)
+    tb = torch.empty(n, dtype=torch.float64, device=ctx.device)
+    t = torch.empty(n, dtype=torch.float64, device=ctx.device)
+    N.check(N.lib().lodge_select(ctx.bind(), ptr(dp.centers), dp.K, ptr(pos), n, ptr(f), ptr(o),
+                                 ptr(tb), ptr(t)), "lodge_select")
+    return f, o, tb, t
+
+
+def blend_factor(position, m_f, m_o) -> tuple:
+    """t_bar = (c - m_o).(m_f - m_o) / |m_f - m_o|^2, t = clamp (src/blending.py:87-99)."""
+    ctx = context()
+    row = np.concatenate([np.asarray(position, float).reshape(3), np.asarray(m_f, float).reshape(3),
+                          np.asarray(m_o, float).reshape(3)])
+    inp = torch.from_numpy(row).to(ctx.device)
+    out = torch.empty(3, dtype=torch.float64, device=ctx.device)
+    N.check(N.lib().lodge_blend_factor(ctx.bind(), ptr(inp), 1, ptr(out)), "lodge_blend_factor")
+    d2, t_bar, t = (float(v) for v in out.cpu().tolist())
+    if d2 <= 0:
+        raise ValueError("blend_factor needs distinct chunk centers")
+    return t_bar, t
+
+
+def compose_active(plan, levels: Sequence, m_f_id: int, m_o_id: Optional[int],
+                   t: float) -> ActiveSelection:
+    """Union of two chunks' active sets with opacity modulation (src/blending.py:102-129)."""
+    if not 0 <= m_f_id < plan.n_chunks:
+        raise ValueError(f"chunk {m_f_id} is not in the plan")
+    if m_o_id is None:
+        sets = plan.active_sets[m_f_id]
+        return ActiveSelection(tuple(sets), tuple(np.ones(len(s)) for s in sets))
+    if not 0 <= m_o_id < plan.n_chunks:
+        raise ValueError(f"chunk {m_o_id} is not in the plan")
+    if m_o_id == m_f_id:
+        raise ValueError("blending needs two distinct chunks")
+    sets, tags = compose_device(plan, m_f_id, m_o_id)
+    mods = tuple(np.where(tg == 3, 1.0, np.where(tg == 1, t, 1.0 - t)) for tg in tags)
+    return ActiveSelection(tuple(sets), mods)
+
+
+def compose_device(plan, f: int, o: int, device=None):
+    """K1 on the device; returns per-level (sorted int64 union, uint8 tags) on the host."""
+    ctx = context(device)
+    dp = plan_for(plan, ctx.device)
+    L = dp.L
+    cap = [int(2 * dp.max_set[l]) for l in range(L)]
+    idx = [torch.empty(max(c, 1), dtype=torch.int32, device=ctx.device) for c in cap]
+    tag = [torch.empty(max(c, 1), dtype=torch.uint8, device=ctx.device) for c in cap]
+    idx_p = (C.c_void_p * L)(*[t.data_ptr() for t in idx])
+    tag_p = (C.c_void_p * L)(*[t.data_ptr() for t in tag])
+    sizes = (C.c_int64 * L)()
+    N.check(N.lib().lodge_compose(ctx.bind(), C.byref(dp.struct), f, -1 if o is None else o,
+                                  idx_p, tag_p, sizes), "lodge_compose")
+    sets, tags = [], []
+    for l in range(L):
+        n = int(sizes[l])
+        sets.append(idx[l][:n].cpu().numpy().view(np.uint32).astype(np.int64))
+        tags.append(tag[l][:n].cpu().numpy())
+    return sets, tags
+
+
+def render_selection(levels, selection, camera, raster_cfg: RasterConfig = RasterConfig(),
+                     need_image: bool = True):
+    """project_selection + rasterize, device-resident in between (src/blending.py:132-137)."""
+    db = project_selection_device(levels, selection.sets, camera, raster_cfg,
+                                  modulations=selection.modulations, shade=need_image)
+    res = rasterize_device(db, camera, raster_cfg, need_image, True)
+    return output_to_host(res, raster_cfg)
+
+
+def _state_for(plan, resident: tuple, position) -> BlendState:
+    c = np.asarray(position, float)
+    if len(resident) == 1:
+        return BlendState(resident, resident[0], 1.0, 1.0)
+    dist = [float(np.linalg.norm(plan.centers[j] - c)) for j in resident]
+    order = sorted(range(2), key=lambda i: (dist[i], resident[i]))
+    f, o = resident[order[0]], resident[order[1]]
+    t_bar, t = blend_factor(c, plan.centers[f], plan.centers[o])
+    return BlendState((f, o), f, t_bar, t)
+
+
+def stream_step(state, plan, position):
+    """Residency state machine (src/blending.py:151-194), host control plane."""
+    c = np.asarray(position, dtype=np.float64)
+    pos_t = tuple(float(v) for v in c)
+    events = []
+    n1, n2 = nearest_two_chunks(plan, c)
+    if state is None:
+        resident = (n1,) if n2 is None else (n1, n2)
+        for j in resident:
+            events.append(StreamEvent("load", j, pos_t))
+        return _state_for(plan, resident, c), events
+    resident = state.loaded_chunks
+    if n1 not in resident:
+        for j in resident:
+            events.append(StreamEvent("unload", j, pos_t))
+        resident = (n1,) if n2 is None else (n1, n2)
+        for j in resident:
+            events.append(StreamEvent("load", j, pos_t))
+        new_state = _state_for(plan, resident, c)
+        if new_state.primary_id != state.primary_id:
+            events.append(StreamEvent("swap_primary", new_state.primary_id, pos_t))
+        return new_state, events
+    new_state = _state_for(plan, resident, c)
+    if new_state.primary_id != state.primary_id:
+        events.append(StreamEvent("swap_primary", new_state.primary_id, pos_t))
+    sec = new_state.secondary_id
+    if (sec is not None and new_state.t_bar >= 1.0 and n2 is not None and n2 != sec
+            and n2 != new_state.primary_id):
+        events.append(StreamEvent("unload", sec, pos_t))
+        events.append(StreamEvent("load", n2, pos_t))
+        new_state = _state_for(plan, (new_state.primary_id, n2), c)
+    return new_state, events
+
+
+def render_blend_state(state, plan, levels, camera, raster_cfg: RasterConfig = RasterConfig(),
+                       need_image: bool = True):
+    """Render from a residency state (src/blending.py:197-203)."""
+    selection = compose_active(plan, levels, state.primary_id, state.secondary_id, state.t)
+    return render_selection(levels, selection, camera, raster_cfg, need_image)

@@ -1,0 +1,220 @@
+// Internal device-side definitions shared by the liblodge kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/lodge.h"
+
+#define LODGE_TILE 16
+#define LODGE_SUPPORT_Q 9.0
+#define FULL_MASK 0xffffffffu
+
+namespace lodge {
+
+// ---------------------------------------------------------------------------
+// Per-frame device state (one per in-flight frame).
+// ---------------------------------------------------------------------------
+struct FrameState {
+  lodge_frame_stats stats;            // f, o, t_bar, t, U, M, P, overflow ...
+  uint32_t epoch;                     // look-back epoch base for this frame
+  uint32_t n_pairs;                   // min(P, P_cap): pairs actually stored
+  uint32_t tickets[32];               // virtual block-id tickets, zeroed per frame
+  uint32_t hist_depth[8][256];        // onesweep digit histograms (depth keys)
+  uint32_t off_depth[8][256];         // their exclusive scans
+  uint32_t off_tile[2][256];          // digit offsets for the two tile passes
+};
+
+enum Ticket {
+  TK_COMPACT = 0,
+  TK_DUP = 1,
+  TK_DEPTH0 = 2,   // .. TK_DEPTH0 + 7
+  TK_TILE0 = 10,   // .. TK_TILE0 + 1
+  TK_UNION0 = 12,  // .. TK_UNION0 + LODGE_MAX_LEVELS - 1
+};
+
+// Splat payload for compositing (64 B, one per survivor).  mean2d is kept in
+// fp64 so the tile-local fp32 offset is exact to fp32 rounding; q_eff is the
+// per-splat cut-off on the quadratic form that encodes both q > 9 and
+// alpha < alpha_min, tol its fp32 error bound (guard band).
+struct __align__(16) Payload {
+  double mx, my;
+  float A, B2, C, o;    // conic (A, 2B, C), effective opacity
+  float r, g, b;        // colour
+  uint32_t src;         // concatenated input index
+  float q_eff, tol;
+  uint32_t pad0, pad1;
+};
+static_assert(sizeof(Payload) == 64, "payload must be 64 B");
+
+// fp64 copy of the compositing inputs (guard band and EXACT mode).
+struct __align__(16) Precise {
+  double A, B, C, o;
+  double r, g, b, pad;
+};
+static_assert(sizeof(Precise) == 64, "precise record must be 64 B");
+
+// Workspace pointers handed to kernels.
+struct Work {
+  uint64_t *key_depth[2];   // M_cap each (ping-pong)
+  uint32_t *val_depth[2];   // M_cap each
+  uint64_t *rect;           // M_cap packed x0|x1<<16|y0<<32|y1<<48
+  Payload *payload;         // M_cap
+  Precise *precise;         // M_cap
+  uint64_t *pairs[2];       // P_cap each
+  int32_t *tile_diff;       // (tiles_x+1)*(tiles_y+1) 2-D difference array
+  uint32_t *tile_start;     // T+1
+  uint64_t *status;         // look-back status words (epoch | flags | value)
+  uint32_t *union_idx;      // slots
+  uint8_t *union_tag;       // slots
+  int64_t M_cap, P_cap, status_cap, slot_cap;
+};
+
+// Status word: [63:32] epoch, [31:30] flag, [29:0] value.
+enum : uint32_t { ST_EMPTY = 0, ST_AGG = 1, ST_PREFIX = 2 };
+__device__ __forceinline__ uint64_t st_pack(uint32_t epoch, uint32_t flag, uint32_t v) {
+  return ((uint64_t)epoch << 32) | ((uint64_t)flag << 30) | (uint64_t)(v & 0x3fffffffu);
+}
+__device__ __forceinline__ void st_store(uint64_t *p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t st_load(const uint64_t *p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Single-counter decoupled look-back (one warp).  Returns the exclusive
+// prefix of partition `part`.  `agg` must be warp-uniform; lane 0 publishes.
+__device__ __forceinline__ uint32_t lookback_warp(uint64_t *status, uint32_t part, uint32_t agg,
+                                                  uint32_t epoch) {
+  const int lane = threadIdx.x & 31;
+  if (part == 0) {
+    if (lane == 0) st_store(status, st_pack(epoch, ST_PREFIX, agg));
+    return 0;
+  }
+  if (lane == 0) st_store(status + part, st_pack(epoch, ST_AGG, agg));
+  uint32_t prefix = 0;
+  int64_t window_end = (int64_t)part - 1;  // inclusive, walk backwards
+  while (true) {
+    int64_t q = window_end - lane;
+    uint32_t flag = ST_PREFIX, val = 0;
+    if (q >= 0) {
+      uint64_t s;
+      do {
+        s = st_load(status + q);
+        flag = ((uint32_t)(s >> 32) == epoch) ? (uint32_t)((s >> 30) & 3u) : ST_EMPTY;
+      } while (flag == ST_EMPTY);
+      val = (uint32_t)(s & 0x3fffffffu);
+    }
+    // lanes beyond q<0 act as an implicit zero prefix
+    uint32_t pmask = __ballot_sync(FULL_MASK, flag == ST_PREFIX);
+    int first = __ffs(pmask) - 1;  // nearest partition holding a prefix
+    // no prefix in the window: every lane holds an aggregate, take all 32
+    uint32_t contrib = (pmask == 0u || lane <= first) ? val : 0u;
+    for (int o = 16; o > 0; o >>= 1) contrib += __shfl_xor_sync(FULL_MASK, contrib, o);
+    prefix += contrib;
+    if (pmask) break;
+    window_end -= 32;
+  }
+  if (lane == 0) st_store(status + part, st_pack(epoch, ST_PREFIX, prefix + agg));
+  return prefix;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Virtual block id from an atomic ticket: partitions are processed in the
+// order blocks start, so a block only ever waits on running blocks.
+__device__ __forceinline__ uint32_t take_ticket(uint32_t *ticket, uint32_t *s_tmp) {
+  if (threadIdx.x == 0) *s_tmp = atomicAdd(ticket, 1u);
+  __syncthreads();
+  return *s_tmp;
+}
+
+// Block-ordered compaction of partition `part`: returns this thread's output
+// slot (or -1); one look-back per block.
+__device__ __forceinline__ int64_t compact_slot(bool keep, uint64_t *status, uint32_t epoch,
+                                                uint32_t part, uint32_t *s_warp,
+                                                uint32_t *s_base) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const uint32_t bal = __ballot_sync(FULL_MASK, keep);
+  if (lane == 0) s_warp[warp] = __popc(bal);
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t v = lane < nwarps ? s_warp[lane] : 0;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const uint32_t total = __shfl_sync(FULL_MASK, inc, 31);
+    const uint32_t pre = lookback_warp(status, part, total, epoch);
+    if (lane < nwarps) s_warp[lane] = inc - v;
+    if (lane == 0) *s_base = pre;
+  }
+  __syncthreads();
+  if (!keep) return -1;
+  return (int64_t)(*s_base) + s_warp[warp] + __popc(bal & lanemask_lt());
+}
+
+__host__ __device__ __forceinline__ uint32_t union_status_stride(uint32_t max_slots) {
+  return (max_slots + 255u) / 256u + 1u;
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+}  // namespace lodge
+
+// ---------------------------------------------------------------------------
+// Host-side launchers (implemented in the k_*.cu files)
+// ---------------------------------------------------------------------------
+namespace lodge {
+struct LevelSlots {
+  int32_t n_levels;
+  uint32_t slot_base[LODGE_MAX_LEVELS + 1];  // slots per level = 2*max_set
+};
+
+void launch_begin_frame(FrameState *fs, cudaStream_t s);
+void launch_select(const double *centers, int32_t K, const double *pos, int32_t n, int32_t *f,
+                   int32_t *o, double *tb, double *t, cudaStream_t s);
+void launch_blend_factor(const double *in, int32_t n, double *out, cudaStream_t s);
+void launch_select_frame(const double *centers, int32_t K, const lodge_camera *cam,
+                         const int32_t *pair, const double *t_override, int32_t have_pair,
+                         int32_t pair_f, int32_t pair_o, double t_val, FrameState *fs,
+                         cudaStream_t s);
+void launch_union(const lodge_chunks &ch, const LevelSlots &ls, FrameState *fs, uint64_t *status,
+                  uint32_t *union_idx, uint8_t *union_tag, cudaStream_t s);
+int launch_project_frame(const lodge_level *levels, const LevelSlots &ls, const Work &w,
+                         FrameState *fs, const lodge_camera *cam_dev,
+                         const lodge_raster_params &rp, int32_t shade, int32_t exact,
+                         cudaStream_t s);
+int launch_project_compat(const lodge_level &level, const int64_t *idx, int64_t n,
+                          const double *mod, const Work &w, FrameState *fs,
+                          const lodge_camera *cam_dev, const lodge_raster_params &rp,
+                          int32_t shade, const lodge_batch *out, cudaStream_t s);
+void launch_import_batch(const lodge_batch &b, int64_t M, const Work &w, FrameState *fs,
+                         const lodge_camera *cam_dev, const lodge_raster_params &rp,
+                         int32_t exact, cudaStream_t s);
+void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
+                       cudaStream_t s);
+void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32_t tiles_x,
+                       int32_t tiles_y, cudaStream_t s);
+void launch_duplicate(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_cap,
+                      cudaStream_t s);
+void launch_tile_sort(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
+                      int32_t *launches, cudaStream_t s);
+void launch_composite(const Work &w, FrameState *fs, const lodge_camera *cam_dev, int32_t W,
+                      int32_t H, const lodge_raster_params &rp, int32_t flags, int32_t exact,
+                      const lodge_frame_out &out, uint32_t n_inputs_cap, cudaStream_t s);
+void launch_export_lists(const Work &w, FrameState *fs, int32_t T, int64_t *tile_offsets,
+                         int64_t *tile_src, int64_t cap, cudaStream_t s);
+}  // namespace lodge

@@ -1,0 +1,199 @@
+// K3/K5: tile binning.  Restates reference src/raster.py:409-425:
+//   per_tile_count = bincount(tile ids)           (k_tile_setup)
+//   duplication of each depth-sorted splat over its tile rectangle,
+//   row-major, pairs in global depth order       (k_duplicate)
+//   run starts of each tile in the sorted pairs  (tile_start, from counts)
+// Counts come from a 2-D difference array filled by K2 (four atomics per
+// splat instead of one per pair), integrated here; the duplication kernel
+// uses a single-pass look-back scan and block-cooperative emission so one
+// huge splat (all 8160 tiles at 1080p) does not serialise a thread.
+#include "internal.cuh"
+
+namespace lodge {
+
+// Single block.  diff: (ty+1) x (tx+1).  Produces tile_count (int32, may be
+// NULL), tile_start (T+1), the two tile-digit offset tables, P, n_pairs, and
+// re-zeroes diff for the next frame.
+__global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t tiles_x,
+                                                     int32_t tiles_y, int32_t *tile_count,
+                                                     uint32_t *tile_start, FrameState *fs,
+                                                     int64_t P_cap) {
+  extern __shared__ int32_t sd[];  // (tx+1)*(ty+1)
+  __shared__ uint32_t h0[256], h1[256];
+  __shared__ uint32_t s_sum[1024];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int stride = tiles_x + 1;
+  const int nd = stride * (tiles_y + 1);
+  for (int i = tid; i < nd; i += nt) {
+    sd[i] = diff[i];
+    diff[i] = 0;
+  }
+  for (int i = tid; i < 256; i += nt) h0[i] = h1[i] = 0;
+  __syncthreads();
+  for (int y = tid; y < tiles_y; y += nt) {  // prefix along x
+    int32_t run = 0;
+    for (int x = 0; x < tiles_x; ++x) {
+      run += sd[y * stride + x];
+      sd[y * stride + x] = run;
+    }
+  }
+  __syncthreads();
+  for (int x = tid; x < tiles_x; x += nt) {  // prefix along y
+    int32_t run = 0;
+    for (int y = 0; y < tiles_y; ++y) {
+      run += sd[y * stride + x];
+      sd[y * stride + x] = run;
+    }
+  }
+  __syncthreads();
+  const int T = tiles_x * tiles_y;
+  const int per = (T + nt - 1) / nt;
+  const int b = tid * per, e = min(T, b + per);
+  uint32_t loc = 0;
+  for (int t = b; t < e; ++t) {
+    const uint32_t c = (uint32_t)sd[(t / tiles_x) * stride + (t % tiles_x)];
+    loc += c;
+    if (tile_count) tile_count[t] = (int32_t)c;
+    atomicAdd(&h0[t & 255], c);
+    atomicAdd(&h1[(t >> 8) & 255], c);
+  }
+  s_sum[tid] = loc;
+  __syncthreads();
+  // exclusive scan over threads (Hillis-Steele on 1024 entries)
+  for (int o = 1; o < nt; o <<= 1) {
+    uint32_t v = (tid >= o) ? s_sum[tid - o] : 0u;
+    __syncthreads();
+    s_sum[tid] += v;
+    __syncthreads();
+  }
+  uint32_t run = s_sum[tid] - loc;
+  for (int t = b; t < e; ++t) {
+    tile_start[t] = run;
+    run += (uint32_t)sd[(t / tiles_x) * stride + (t % tiles_x)];
+  }
+  if (tid == nt - 1) {
+    const uint32_t P = s_sum[nt - 1];
+    tile_start[T] = P;
+    fs->stats.P = P;
+    fs->stats.overflow = (int64_t)P > P_cap ? 1u : 0u;
+    fs->n_pairs = (int64_t)P < P_cap ? P : (uint32_t)P_cap;
+  }
+  __syncthreads();
+  if (tid < 32) {  // digit offsets for the two onesweep passes over tile ids
+    for (int p = 0; p < 2; ++p) {
+      uint32_t *h = p ? h1 : h0;
+      uint32_t acc = 0;
+      for (int c = 0; c < 256; c += 32) {
+        const uint32_t v = h[c + tid];
+        uint32_t inc = v;
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
+          if (tid >= o) inc += t;
+        }
+        fs->off_tile[p][c + tid] = acc + inc - v;
+        acc += __shfl_sync(FULL_MASK, inc, 31);
+      }
+    }
+  }
+}
+
+constexpr int DUP_THREADS = 256;
+
+// One thread per depth-sorted splat for counting; block-cooperative emission.
+__global__ void __launch_bounds__(DUP_THREADS) k_duplicate(const uint32_t *__restrict__ order,
+                                                           const uint64_t *__restrict__ rect,
+                                                           int32_t tiles_x, uint64_t *pairs,
+                                                           int64_t P_cap, uint64_t *status,
+                                                           FrameState *fs) {
+  __shared__ uint32_t s_off[DUP_THREADS + 1];
+  __shared__ uint32_t s_m[DUP_THREADS];
+  __shared__ uint64_t s_rect[DUP_THREADS];
+  __shared__ uint32_t s_w[DUP_THREADS / 32];
+  __shared__ uint32_t s_part, s_base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_part = atomicAdd(&fs->tickets[TK_DUP], 1u);
+  __syncthreads();
+  const uint32_t part = s_part;
+  const uint32_t M = fs->stats.M;
+  const uint32_t r = part * DUP_THREADS + tid;
+  if (part * DUP_THREADS >= M) return;
+  uint32_t cnt = 0;
+  if (r < M) {
+    const uint32_t m = order[r];
+    const uint64_t rc = rect[m];
+    const uint32_t x0 = rc & 0xffff, x1 = (rc >> 16) & 0xffff, y0 = (rc >> 32) & 0xffff,
+                   y1 = rc >> 48;
+    cnt = (x1 - x0 + 1) * (y1 - y0 + 1);
+    s_m[tid] = m;
+    s_rect[tid] = rc;
+  }
+  // block exclusive scan of counts
+  uint32_t inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t wv = lane < DUP_THREADS / 32 ? s_w[lane] : 0u;
+    uint32_t winc = wv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(FULL_MASK, winc, o);
+      if (lane >= o) winc += t;
+    }
+    const uint32_t total = __shfl_sync(FULL_MASK, winc, 31);
+    if (lane < DUP_THREADS / 32) s_w[lane] = winc - wv;
+    const uint32_t pre = lookback_warp(status, part, total, fs->epoch + TK_DUP);
+    if (lane == 0) {
+      s_base = pre;
+      s_off[DUP_THREADS] = total;
+    }
+  }
+  __syncthreads();
+  s_off[tid] = s_w[warp] + inc - cnt;
+  __syncthreads();
+  const uint32_t total = s_off[DUP_THREADS];
+  const uint64_t base = s_base;
+  for (uint32_t j = tid; j < total; j += DUP_THREADS) {
+    // owner: last s with s_off[s] <= j
+    int lo = 0, hi = DUP_THREADS - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_off[mid] <= j) lo = mid;
+      else hi = mid - 1;
+    }
+    const uint64_t rc = s_rect[lo];
+    const uint32_t x0 = rc & 0xffff, x1 = (rc >> 16) & 0xffff, y0 = (rc >> 32) & 0xffff;
+    const uint32_t w = x1 - x0 + 1;
+    const uint32_t local = j - s_off[lo];
+    const uint32_t ty = y0 + local / w, tx = x0 + local % w;
+    const uint64_t dst = base + j;
+    if ((int64_t)dst < P_cap)
+      pairs[dst] = ((uint64_t)(ty * (uint32_t)tiles_x + tx) << 32) | s_m[lo];
+  }
+}
+
+void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32_t tiles_x,
+                       int32_t tiles_y, cudaStream_t s) {
+  const size_t sm = (size_t)(tiles_x + 1) * (tiles_y + 1) * 4;
+  static size_t attr = 0;
+  if (sm > 48 * 1024 && sm > attr) {
+    cudaFuncSetAttribute(k_tile_setup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = sm;
+  }
+  k_tile_setup<<<1, 1024, sm, s>>>(w.tile_diff, tiles_x, tiles_y, tile_count, w.tile_start, fs,
+                                   w.P_cap);
+}
+
+void launch_duplicate(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_cap,
+                      cudaStream_t s) {
+  if (M_cap <= 0) return;
+  const unsigned grid = (unsigned)((M_cap + DUP_THREADS - 1) / DUP_THREADS);
+  k_duplicate<<<grid, DUP_THREADS, 0, s>>>(w.val_depth[0], w.rect, tiles_x, w.pairs[0], w.P_cap,
+                                           w.status, fs);
+}
+
+}  // namespace lodge

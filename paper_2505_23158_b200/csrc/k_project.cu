@@ -1,0 +1,487 @@
+// K2: EWA projection with the Eq. 3 smoothing-filter opacity factor, 2-D
+// dilation, culling and SH colour; one thread per active Gaussian, fp64
+// arithmetic in the reference's operation order (compiled with
+// -fmad=false; every fma() below is one OpenBLAS places).  Survivors are
+// compacted in input order by a single-pass decoupled look-back scan, so the
+// concatenated source index order is preserved (tie order).
+//
+// Restates reference src/raster.py:188-291 (project_scene),
+// src/raster.py:176-185 (filter_opacity_factor), src/raster.py:136-173
+// (eval_sh), src/scene.py:23-42 (quat_to_matrix), src/raster.py:303-313
+// (_tile_ranges) and src/lod.py:216-227 (project_selection, level-major).
+#include "internal.cuh"
+
+namespace lodge {
+
+__device__ __constant__ double c_SH_C0 = 0.28209479177387814;
+__device__ __constant__ double c_SH_C1 = 0.4886025119029199;
+__device__ __constant__ double c_SH_C2[5] = {1.0925484305920792, -1.0925484305920792,
+                                            0.31539156525252005, -1.0925484305920792,
+                                            0.5462742152960396};
+__device__ __constant__ double c_SH_C3[7] = {-0.5900435899266435, 2.890611442640554,
+                                            -0.4570457994644658, 0.3731763325901154,
+                                            -0.4570457994644658, 1.445305721320277,
+                                            -0.5900435899266435};
+
+struct Proj {
+  double mx, my, z, ex, ey, op;
+  double c00, c01, c10, c11, det;
+  bool ok;
+};
+
+template <typename GT>
+__device__ __forceinline__ void load_geom(const GT *__restrict__ g, double v[12]);
+
+template <>
+__device__ __forceinline__ void load_geom<double>(const double *__restrict__ g, double v[12]) {
+  const double2 *p = reinterpret_cast<const double2 *>(g);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    double2 t = __ldg(p + i);
+    v[2 * i] = t.x;
+    v[2 * i + 1] = t.y;
+  }
+}
+
+template <>
+__device__ __forceinline__ void load_geom<float>(const float *__restrict__ g, double v[12]) {
+  const float4 *p = reinterpret_cast<const float4 *>(g);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    float4 t = __ldg(p + i);
+    v[4 * i] = t.x;
+    v[4 * i + 1] = t.y;
+    v[4 * i + 2] = t.z;
+    v[4 * i + 3] = t.w;
+  }
+}
+
+// v: [mean3, scale3, rot4 wxyz, opacity, fv]
+__device__ __forceinline__ Proj project_core(const double v[12], const lodge_camera &cam,
+                                             const lodge_raster_params &rp, double mod,
+                                             bool has_mod) {
+  Proj p;
+  p.ok = false;
+  const double *W = cam.R;
+  const double d0 = v[0] - cam.pos[0], d1 = v[1] - cam.pos[1], d2 = v[2] - cam.pos[2];
+  const double x = fma(d2, W[2], fma(d1, W[1], d0 * W[0]));
+  const double y = fma(d2, W[5], fma(d1, W[4], d0 * W[3]));
+  const double z = fma(d2, W[8], fma(d1, W[7], d0 * W[6]));
+  p.z = z;
+  if (!(z > cam.near_plane)) return p;
+  const double fx = cam.fx, fy = cam.fy;
+  p.mx = ((fx * x) / z) + cam.cx;
+  p.my = ((fy * y) / z) + cam.cy;
+  const double qw = v[6], qx = v[7], qy = v[8], qz = v[9];
+  double r[9];
+  r[0] = 1 - 2 * ((qy * qy) + (qz * qz));
+  r[1] = 2 * ((qx * qy) - (qw * qz));
+  r[2] = 2 * ((qx * qz) + (qw * qy));
+  r[3] = 2 * ((qx * qy) + (qw * qz));
+  r[4] = 1 - 2 * ((qx * qx) + (qz * qz));
+  r[5] = 2 * ((qy * qz) - (qw * qx));
+  r[6] = 2 * ((qx * qz) - (qw * qy));
+  r[7] = 2 * ((qy * qz) + (qw * qx));
+  r[8] = 1 - 2 * ((qx * qx) + (qy * qy));
+  const double s2[3] = {v[3] * v[3], v[4] * v[4], v[5] * v[5]};
+  const double fv = v[11];
+  double cw[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) acc = acc + (r[3 * i + j] * s2[j]) * r[3 * k + j];
+      cw[3 * i + k] = acc;
+    }
+  cw[0] = cw[0] + fv;
+  cw[4] = cw[4] + fv;
+  cw[8] = cw[8] + fv;
+  double cc[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc = acc + (W[3 * i + j] * cw[3 * j + k]) * W[3 * l + k];
+      cc[3 * i + l] = acc;
+    }
+  const double lim_x = 1.3 * 0.5 * (double)cam.w / fx;
+  const double lim_y = 1.3 * 0.5 * (double)cam.h / fy;
+  double tx = x / z, ty = y / z;
+  tx = tx < -lim_x ? -lim_x : (tx > lim_x ? lim_x : tx);
+  ty = ty < -lim_y ? -lim_y : (ty > lim_y ? lim_y : ty);
+  const double jx = tx * z, jy = ty * z;
+  const double inv_z = 1.0 / z;
+  const double J00 = fx * inv_z, J02 = ((-fx * jx) * inv_z) * inv_z;
+  const double J11 = fy * inv_z, J12 = ((-fy * jy) * inv_z) * inv_z;
+  // cov2d = einsum("nij,njk,nlk->nil", J, cc, J); J01 = J10 = 0 terms add
+  // exact zeros, so only the (j,k) in {i,2}x{l,2} terms are kept, in order.
+  const double Jr[2][3] = {{J00, 0.0, J02}, {0.0, J11, J12}};
+  double c2[4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        if (j != i && j != 2) continue;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          if (k != l && k != 2) continue;
+          acc = acc + (Jr[i][j] * cc[3 * j + k]) * Jr[l][k];
+        }
+      }
+      c2[2 * i + l] = acc;
+    }
+  double det_raw = c2[0] * c2[3] - c2[1] * c2[2];
+  det_raw = det_raw > 0.0 ? det_raw : 0.0;
+  c2[0] = c2[0] + rp.dilation2d;
+  c2[3] = c2[3] + rp.dilation2d;
+  const double det = c2[0] * c2[3] - c2[1] * c2[2];
+  const double ra = s2[0] / (s2[0] + fv), rb = s2[1] / (s2[1] + fv), rc = s2[2] / (s2[2] + fv);
+  double op = v[10] * sqrt((ra * rb) * rc);
+  if (rp.dilation2d > 0) op = op * sqrt(det_raw / det);
+  if (has_mod) op = op * mod;
+  const double e0 = c2[0] > 0.0 ? c2[0] : 0.0, e1 = c2[3] > 0.0 ? c2[3] : 0.0;
+  const double ex = 3.0 * sqrt(e0), ey = 3.0 * sqrt(e1);
+  bool ok = det > 1e-12;
+  ok = ok && (p.mx + ex > 0) && (p.mx - ex < (double)cam.w);
+  ok = ok && (p.my + ey > 0) && (p.my - ey < (double)cam.h);
+  p.ex = ex;
+  p.ey = ey;
+  p.op = op;
+  p.c00 = c2[0];
+  p.c01 = c2[1];
+  p.c10 = c2[2];
+  p.c11 = c2[3];
+  p.det = det;
+  p.ok = ok;
+  return p;
+}
+
+template <typename ST>
+__device__ __forceinline__ void eval_sh_dev(const ST *__restrict__ k, int terms, int degree,
+                                            const double v[12], const lodge_camera &cam,
+                                            double rgb[3]) {
+  const double dd0 = v[0] - cam.pos[0], dd1 = v[1] - cam.pos[1], dd2 = v[2] - cam.pos[2];
+  const double nrm = sqrt((dd0 * dd0 + dd1 * dd1) + dd2 * dd2);
+  const double xs = dd0 / nrm, ys = dd1 / nrm, zs = dd2 / nrm;
+  double b2[5], b3[7];
+  const double c1y = c_SH_C1 * ys, c1z = c_SH_C1 * zs, c1x = c_SH_C1 * xs;
+  if (degree >= 2) {
+    const double xx = xs * xs, yy = ys * ys, zz = zs * zs;
+    const double xy = xs * ys, yz = ys * zs, xz = xs * zs;
+    b2[0] = c_SH_C2[0] * xy;
+    b2[1] = c_SH_C2[1] * yz;
+    b2[2] = c_SH_C2[2] * (((2 * zz) - xx) - yy);
+    b2[3] = c_SH_C2[3] * xz;
+    b2[4] = c_SH_C2[4] * (xx - yy);
+    if (degree >= 3) {
+      b3[0] = c_SH_C3[0] * (ys * ((3 * xx) - yy));
+      b3[1] = c_SH_C3[1] * (xy * zs);
+      b3[2] = c_SH_C3[2] * (ys * (((4 * zz) - xx) - yy));
+      b3[3] = c_SH_C3[3] * (zs * (((2 * zz) - (3 * xx)) - (3 * yy)));
+      b3[4] = c_SH_C3[4] * (xs * (((4 * zz) - xx) - yy));
+      b3[5] = c_SH_C3[5] * (zs * (xx - yy));
+      b3[6] = c_SH_C3[6] * (xs * (xx - (3 * yy)));
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const ST *kc = k + c * terms;
+    double out = c_SH_C0 * (double)__ldg(kc);
+    if (degree >= 1) {
+      out = out - c1y * (double)__ldg(kc + 1);
+      out = out + c1z * (double)__ldg(kc + 2);
+      out = out - c1x * (double)__ldg(kc + 3);
+      if (degree >= 2)
+        for (int q = 0; q < 5; ++q) out = out + b2[q] * (double)__ldg(kc + 4 + q);
+      if (degree >= 3)
+        for (int q = 0; q < 7; ++q) out = out + b3[q] * (double)__ldg(kc + 9 + q);
+    }
+    out = out + 0.5;
+    rgb[c] = (out > 0.0 || out != out) ? out : 0.0;
+  }
+}
+
+// Compositing payload from fp64 batch values (shared by K2 and the compat
+// import).  q_eff folds both skip tests of src/raster.py:356 into one cut-off
+// on q; tol bounds |q_fp32 - q_fp64| near that cut-off.
+__device__ __forceinline__ void make_payload(double mx, double my, double A, double B, double C,
+                                             double o, const double rgb[3], uint32_t src,
+                                             const lodge_raster_params &rp, Payload &pl,
+                                             Precise &pr) {
+  pl.mx = mx;
+  pl.my = my;
+  pl.A = (float)A;
+  pl.B2 = (float)(2.0 * B);
+  pl.C = (float)C;
+  pl.o = (float)o;
+  pl.r = (float)rgb[0];
+  pl.g = (float)rgb[1];
+  pl.b = (float)rgb[2];
+  pl.src = src;
+  double q_eff;
+  if (rp.alpha_min <= 0.0) q_eff = LODGE_SUPPORT_Q;
+  else if (!(o >= rp.alpha_min)) q_eff = -INFINITY;  // alpha <= o < alpha_min everywhere
+  else q_eff = fmin(LODGE_SUPPORT_Q, 2.0 * log(o / rp.alpha_min));
+  const double lmid = 0.5 * (A + C);
+  const double rad = sqrt(0.25 * (A - C) * (A - C) + B * B);
+  const double lmax = lmid + rad, lmin = lmid - rad;
+  double tol;
+  if (!(lmin > 0.0) || !(q_eff > -INFINITY)) {
+    tol = (q_eff > -INFINITY) ? INFINITY : 0.0;
+  } else {
+    const double qr = fmax(q_eff, 0.0) + 1.0;
+    const double cond = lmax / lmin;
+    tol = 5.96e-8 * (48.0 * cond * qr + 96.0 * sqrt(lmax * cond * qr) + 4.0 * qr) + 1e-9 * qr;
+  }
+  pl.q_eff = (float)q_eff;
+  pl.tol = (float)tol;
+  pl.pad0 = pl.pad1 = 0;
+  pr.A = A;
+  pr.B = B;
+  pr.C = C;
+  pr.o = o;
+  pr.r = rgb[0];
+  pr.g = rgb[1];
+  pr.b = rgb[2];
+  pr.pad = 0.0;
+}
+
+__device__ __forceinline__ uint64_t tile_rect(double mx, double my, double ex, double ey,
+                                              int32_t tiles_x, int32_t tiles_y) {
+  // floor((m -/+ e) / 16), clipped (src/raster.py:303-313)
+  int64_t x0 = (int64_t)floor((mx - ex) / 16.0), x1 = (int64_t)floor((mx + ex) / 16.0);
+  int64_t y0 = (int64_t)floor((my - ey) / 16.0), y1 = (int64_t)floor((my + ey) / 16.0);
+  x0 = x0 < 0 ? 0 : (x0 > tiles_x - 1 ? tiles_x - 1 : x0);
+  x1 = x1 < 0 ? 0 : (x1 > tiles_x - 1 ? tiles_x - 1 : x1);
+  y0 = y0 < 0 ? 0 : (y0 > tiles_y - 1 ? tiles_y - 1 : y0);
+  y1 = y1 < 0 ? 0 : (y1 > tiles_y - 1 ? tiles_y - 1 : y1);
+  return (uint64_t)x0 | ((uint64_t)x1 << 16) | ((uint64_t)y0 << 32) | ((uint64_t)y1 << 48);
+}
+
+__device__ __forceinline__ void add_tile_diff(int32_t *diff, uint64_t rc, int32_t tiles_x) {
+  const int32_t x0 = (int32_t)(rc & 0xffff), x1 = (int32_t)((rc >> 16) & 0xffff);
+  const int32_t y0 = (int32_t)((rc >> 32) & 0xffff), y1 = (int32_t)(rc >> 48);
+  const int32_t stride = tiles_x + 1;
+  atomicAdd(diff + y0 * stride + x0, 1);
+  atomicAdd(diff + y0 * stride + x1 + 1, -1);
+  atomicAdd(diff + (y1 + 1) * stride + x0, -1);
+  atomicAdd(diff + (y1 + 1) * stride + x1 + 1, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Frame mode: inputs come from the K1 union (tags), outputs are the internal
+// compositing representation.
+// ---------------------------------------------------------------------------
+struct ProjLevels {
+  const void *geom[LODGE_MAX_LEVELS];
+  const void *sh[LODGE_MAX_LEVELS];
+  int32_t degree[LODGE_MAX_LEVELS];
+  uint32_t slot_base[LODGE_MAX_LEVELS + 1];
+  int32_t L;
+};
+
+template <typename GT, typename ST>
+__global__ void __launch_bounds__(256) k_project_frame(ProjLevels lv, Work w, FrameState *fs,
+                                                       const lodge_camera *__restrict__ cam_p,
+                                                       lodge_raster_params rp, int32_t shade) {
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_base;
+  __shared__ lodge_camera cam;
+  if (threadIdx.x == 0) cam = *cam_p;
+  const uint32_t part = take_ticket(&fs->tickets[TK_COMPACT], &s_base);
+  const uint32_t slot = part * blockDim.x + threadIdx.x;
+  // map slot -> level
+  int l = 0;
+  while (l + 1 < lv.L && slot >= lv.slot_base[l + 1]) ++l;
+  const uint32_t pos = slot - lv.slot_base[l];
+  bool valid = slot < lv.slot_base[lv.L] && pos < fs->stats.U_level[l];
+  uint32_t cat_off = 0;  // concatenated index offset of level l
+  for (int k = 0; k < l; ++k) cat_off += fs->stats.U_level[k];
+  Proj p;
+  p.ok = false;
+  double v[12];
+  uint32_t gidx = 0;
+  if (valid) {
+    gidx = w.union_idx[slot];
+    const uint8_t tag = w.union_tag[slot];
+    const double t = fs->stats.t;
+    const double mod = (tag == 3) ? 1.0 : (tag == 1 ? t : 1.0 - t);
+    load_geom<GT>(reinterpret_cast<const GT *>(lv.geom[l]) + (size_t)gidx * 12, v);
+    p = project_core(v, cam, rp, mod, true);
+  }
+  const bool keep = valid && p.ok;
+  const uint32_t epoch = fs->epoch + TK_COMPACT;
+  const int64_t m = compact_slot(keep, w.status, epoch, part, s_warp, &s_base);
+  if (m < 0) return;
+  double rgb[3] = {0.0, 0.0, 0.0};
+  if (shade) {
+    const int deg = lv.degree[l];
+    const int terms = (deg + 1) * (deg + 1);
+    eval_sh_dev<ST>(reinterpret_cast<const ST *>(lv.sh[l]) + (size_t)gidx * 3 * terms, terms, deg,
+                    v, cam, rgb);
+  }
+  const double inv_det = 1.0 / p.det;
+  const double A = p.c11 * inv_det, B = (-p.c01) * inv_det, C = p.c00 * inv_det;
+  Payload pl;
+  Precise pr;
+  make_payload(p.mx, p.my, A, B, C, p.op, rgb, cat_off + pos, rp, pl, pr);
+  w.payload[m] = pl;
+  w.precise[m] = pr;
+  const int32_t tiles_x = (cam.w + 15) / 16, tiles_y = (cam.h + 15) / 16;
+  const uint64_t rc = tile_rect(p.mx, p.my, p.ex, p.ey, tiles_x, tiles_y);
+  w.rect[m] = rc;
+  add_tile_diff(w.tile_diff, rc, tiles_x);
+  w.key_depth[0][m] = (uint64_t)__double_as_longlong(p.z);
+  w.val_depth[0][m] = (uint32_t)m;
+  atomicMax(&fs->stats.M, (uint32_t)(m + 1));
+}
+
+// ---------------------------------------------------------------------------
+// Compat mode: one level, explicit indices/modulation, exports Splat2DBatch.
+// ---------------------------------------------------------------------------
+template <typename GT, typename ST>
+__global__ void __launch_bounds__(256) k_project_compat(const GT *geom, const ST *sh, int32_t deg,
+                                                        const int64_t *idx, int64_t n,
+                                                        const double *mod, Work w, FrameState *fs,
+                                                        const lodge_camera *__restrict__ cam_p,
+                                                        lodge_raster_params rp, int32_t shade,
+                                                        lodge_batch out) {
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_base;
+  __shared__ lodge_camera cam;
+  if (threadIdx.x == 0) cam = *cam_p;
+  const uint32_t part = take_ticket(&fs->tickets[TK_COMPACT], &s_base);
+  const int64_t e = (int64_t)part * blockDim.x + threadIdx.x;
+  Proj p;
+  p.ok = false;
+  double v[12];
+  int64_t g = 0;
+  if (e < n) {
+    g = idx ? idx[e] : e;
+    load_geom<GT>(geom + (size_t)g * 12, v);
+    p = project_core(v, cam, rp, mod ? mod[e] : 1.0, mod != nullptr);
+  }
+  const int64_t m = compact_slot(e < n && p.ok, w.status, fs->epoch + TK_COMPACT, part, s_warp,
+                                 &s_base);
+  if (m < 0) return;
+  double rgb[3] = {0.0, 0.0, 0.0};
+  if (shade) {
+    const int terms = (deg + 1) * (deg + 1);
+    eval_sh_dev<ST>(sh + (size_t)g * 3 * terms, terms, deg, v, cam, rgb);
+  }
+  const double inv_det = 1.0 / p.det;
+  out.src_dev[m] = e;
+  out.mean2d_dev[2 * m] = p.mx;
+  out.mean2d_dev[2 * m + 1] = p.my;
+  out.cov2d_dev[4 * m] = p.c00;
+  out.cov2d_dev[4 * m + 1] = p.c01;
+  out.cov2d_dev[4 * m + 2] = p.c10;
+  out.cov2d_dev[4 * m + 3] = p.c11;
+  out.conic_dev[3 * m] = p.c11 * inv_det;
+  out.conic_dev[3 * m + 1] = (-p.c01) * inv_det;
+  out.conic_dev[3 * m + 2] = p.c00 * inv_det;
+  out.extent_dev[2 * m] = p.ex;
+  out.extent_dev[2 * m + 1] = p.ey;
+  out.depth_dev[m] = p.z;
+  out.opacity_dev[m] = p.op;
+  out.color_dev[3 * m] = rgb[0];
+  out.color_dev[3 * m + 1] = rgb[1];
+  out.color_dev[3 * m + 2] = rgb[2];
+  atomicMax(&fs->stats.M, (uint32_t)(m + 1));
+}
+
+// Compat rasterize: import a host-made Splat2DBatch into the internal form.
+__global__ void __launch_bounds__(256) k_import_batch(lodge_batch b, int64_t M, Work w,
+                                                      FrameState *fs,
+                                                      const lodge_camera *__restrict__ cam_p,
+                                                      lodge_raster_params rp) {
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  const lodge_camera &cam = *cam_p;
+  const double mx = b.mean2d_dev[2 * m], my = b.mean2d_dev[2 * m + 1];
+  const double rgb[3] = {b.color_dev[3 * m], b.color_dev[3 * m + 1], b.color_dev[3 * m + 2]};
+  Payload pl;
+  Precise pr;
+  make_payload(mx, my, b.conic_dev[3 * m], b.conic_dev[3 * m + 1], b.conic_dev[3 * m + 2],
+               b.opacity_dev[m], rgb, (uint32_t)b.src_dev[m], rp, pl, pr);
+  w.payload[m] = pl;
+  w.precise[m] = pr;
+  const int32_t tiles_x = (cam.w + 15) / 16, tiles_y = (cam.h + 15) / 16;
+  const uint64_t rc = tile_rect(mx, my, b.extent_dev[2 * m], b.extent_dev[2 * m + 1], tiles_x,
+                                tiles_y);
+  w.rect[m] = rc;
+  add_tile_diff(w.tile_diff, rc, tiles_x);
+  // lexsort((src, depth)): the depth sort is stable, so feed rows in
+  // source-index order via the values; the batch's src order is ascending
+  // for project_scene outputs, otherwise the host pre-sorts (see raster.py).
+  w.key_depth[0][m] = (uint64_t)__double_as_longlong(b.depth_dev[m]);
+  w.val_depth[0][m] = (uint32_t)m;
+  if (m == 0) fs->stats.M = (uint32_t)M;
+}
+
+template <typename GT, typename ST>
+static void launch_pf(const ProjLevels &lv, const Work &w, FrameState *fs,
+                      const lodge_camera *cam, const lodge_raster_params &rp, int32_t shade,
+                      uint32_t nslots, cudaStream_t s) {
+  k_project_frame<GT, ST><<<(nslots + 255) / 256, 256, 0, s>>>(lv, w, fs, cam, rp, shade);
+}
+
+int launch_project_frame(const lodge_level *levels, const LevelSlots &ls, const Work &w,
+                         FrameState *fs, const lodge_camera *cam_dev,
+                         const lodge_raster_params &rp, int32_t shade, int32_t, cudaStream_t s) {
+  ProjLevels lv;
+  lv.L = ls.n_levels;
+  const int32_t fl = levels[0].flags;
+  for (int l = 0; l < lv.L; ++l) {
+    if (levels[l].flags != fl) return -1;  // one storage precision per store
+    lv.geom[l] = levels[l].geom_dev;
+    lv.sh[l] = levels[l].sh_dev;
+    lv.degree[l] = levels[l].sh_degree;
+  }
+  for (int l = 0; l <= LODGE_MAX_LEVELS; ++l) lv.slot_base[l] = l <= lv.L ? ls.slot_base[l] : 0;
+  const uint32_t nslots = ls.slot_base[lv.L];
+  if (nslots == 0) return 0;
+  const bool g32 = fl & LODGE_GEOM_FP32, s32 = fl & LODGE_SH_FP32;
+  if (g32 && s32) launch_pf<float, float>(lv, w, fs, cam_dev, rp, shade, nslots, s);
+  else if (g32) launch_pf<float, double>(lv, w, fs, cam_dev, rp, shade, nslots, s);
+  else if (s32) launch_pf<double, float>(lv, w, fs, cam_dev, rp, shade, nslots, s);
+  else launch_pf<double, double>(lv, w, fs, cam_dev, rp, shade, nslots, s);
+  return 0;
+}
+
+int launch_project_compat(const lodge_level &level, const int64_t *idx, int64_t n,
+                          const double *mod, const Work &w, FrameState *fs,
+                          const lodge_camera *cam_dev, const lodge_raster_params &rp,
+                          int32_t shade, const lodge_batch *out, cudaStream_t s) {
+  if (n <= 0) return 0;
+  const unsigned grid = (unsigned)((n + 255) / 256);
+  const bool g32 = level.flags & LODGE_GEOM_FP32, s32 = level.flags & LODGE_SH_FP32;
+#define LP(GT, ST)                                                                         \
+  k_project_compat<GT, ST><<<grid, 256, 0, s>>>((const GT *)level.geom_dev,                \
+                                                (const ST *)level.sh_dev, level.sh_degree, \
+                                                idx, n, mod, w, fs, cam_dev, rp, shade, *out)
+  if (g32 && s32) LP(float, float);
+  else if (g32) LP(float, double);
+  else if (s32) LP(double, float);
+  else LP(double, double);
+#undef LP
+  return 0;
+}
+
+void launch_import_batch(const lodge_batch &b, int64_t M, const Work &w, FrameState *fs,
+                         const lodge_camera *cam_dev, const lodge_raster_params &rp, int32_t,
+                         cudaStream_t s) {
+  if (M <= 0) return;
+  k_import_batch<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(b, M, w, fs, cam_dev, rp);
+}
+
+}  // namespace lodge

@@ -1,0 +1,415 @@
+// C ABI of liblodge (include/lodge.h): context, workspace, entry points.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "internal.cuh"
+
+using namespace lodge;
+
+static thread_local std::string g_err;
+
+static int set_err(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                  \
+  do {                                                                            \
+    cudaError_t _e = (call);                                                      \
+    if (_e != cudaSuccess)                                                        \
+      return set_err(_e == cudaErrorMemoryAllocation ? LODGE_ERR_OOM : LODGE_ERR_CUDA, \
+                     std::string(#call) + ": " + cudaGetErrorString(_e));         \
+  } while (0)
+
+struct lodge_ctx {
+  int device = 0;
+  cudaStream_t stream = 0;
+  int32_t precision = LODGE_PREC_FAST;
+  FrameState *fs = nullptr;
+  lodge_camera *cam_dev = nullptr;   // scratch for the synchronous entry points
+  lodge_camera *cam_host = nullptr;  // pinned staging
+  lodge_frame_stats *stats_host = nullptr;  // pinned
+  Work w{};
+  int64_t tiles_cap = 0;  // capacity of tile_start (T+1) and diff
+  int32_t launches = 0;
+  LevelSlots last_slots{};  // slot layout of the last union
+};
+
+static int ensure_M(lodge_ctx *c, int64_t need) {
+  Work &w = c->w;
+  if (need <= w.M_cap && w.payload) return 0;
+  int64_t ncap = std::max<int64_t>(std::max<int64_t>(need, w.M_cap + w.M_cap / 2), 4096);
+  cudaFree(w.key_depth[0]); cudaFree(w.key_depth[1]);
+  cudaFree(w.val_depth[0]); cudaFree(w.val_depth[1]);
+  cudaFree(w.rect); cudaFree(w.payload); cudaFree(w.precise);
+  w.M_cap = 0;
+  CK(cudaMalloc(&w.key_depth[0], 8 * ncap));
+  CK(cudaMalloc(&w.key_depth[1], 8 * ncap));
+  CK(cudaMalloc(&w.val_depth[0], 4 * ncap));
+  CK(cudaMalloc(&w.val_depth[1], 4 * ncap));
+  CK(cudaMalloc(&w.rect, 8 * ncap));
+  CK(cudaMalloc(&w.payload, sizeof(Payload) * ncap));
+  CK(cudaMalloc(&w.precise, sizeof(Precise) * ncap));
+  w.M_cap = ncap;
+  return 0;
+}
+
+static int ensure_status(lodge_ctx *c, int64_t words) {
+  Work &w = c->w;
+  if (words <= w.status_cap && w.status) return 0;
+  int64_t ncap = std::max<int64_t>(words, w.status_cap + w.status_cap / 2);
+  ncap = std::max<int64_t>(ncap, 1 << 16);
+  if (w.status) cudaFree(w.status);
+  w.status = nullptr;
+  w.status_cap = 0;
+  CK(cudaMalloc(&w.status, 8 * ncap));
+  CK(cudaMemset(w.status, 0, 8 * ncap));  // epoch 0 is never used
+  w.status_cap = ncap;
+  return 0;
+}
+
+static int ensure_P(lodge_ctx *c, int64_t need) {
+  Work &w = c->w;
+  if (need <= w.P_cap && w.pairs[0]) return 0;
+  int64_t ncap = std::max<int64_t>(std::max<int64_t>(need, w.P_cap + w.P_cap / 2), 1 << 16);
+  cudaFree(w.pairs[0]); cudaFree(w.pairs[1]);
+  w.pairs[0] = w.pairs[1] = nullptr;
+  w.P_cap = 0;
+  CK(cudaMalloc(&w.pairs[0], 8 * ncap));
+  CK(cudaMalloc(&w.pairs[1], 8 * ncap));
+  w.P_cap = ncap;
+  return ensure_status(c, (ncap + 4095) / 4096 * 256);
+}
+
+static int ensure_tiles(lodge_ctx *c, int32_t W, int32_t H) {
+  const int64_t tx = (W + 15) / 16, ty = (H + 15) / 16;
+  const int64_t need = (tx + 1) * (ty + 1) + 1;
+  if (need <= c->tiles_cap && c->w.tile_diff) return 0;
+  cudaFree(c->w.tile_diff); cudaFree(c->w.tile_start);
+  c->tiles_cap = 0;
+  CK(cudaMalloc(&c->w.tile_diff, 4 * need));
+  CK(cudaMemset(c->w.tile_diff, 0, 4 * need));
+  CK(cudaMalloc(&c->w.tile_start, 4 * need));
+  c->tiles_cap = need;
+  return 0;
+}
+
+static int ensure_slots(lodge_ctx *c, int64_t need) {
+  Work &w = c->w;
+  if (need <= w.slot_cap && w.union_idx) return 0;
+  int64_t ncap = std::max<int64_t>(need, 4096);
+  cudaFree(w.union_idx); cudaFree(w.union_tag);
+  w.slot_cap = 0;
+  CK(cudaMalloc(&w.union_idx, 4 * ncap));
+  CK(cudaMalloc(&w.union_tag, ncap));
+  w.slot_cap = ncap;
+  return 0;
+}
+
+static int check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return set_err(LODGE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return 0;
+}
+
+static int check_cam(const lodge_camera *cam) {
+  if (!cam) return set_err(LODGE_ERR_BAD_ARG, "camera is NULL");
+  if (cam->w <= 0 || cam->h <= 0) return set_err(LODGE_ERR_BAD_ARG, "camera resolution must be positive");
+  if (cam->w > 16 * 65535 || cam->h > 16 * 65535) return set_err(LODGE_ERR_BAD_ARG, "resolution too large");
+  if (!(cam->fx > 0) || !(cam->fy > 0)) return set_err(LODGE_ERR_BAD_ARG, "focal must be positive");
+  return 0;
+}
+
+static int check_tile_smem(int32_t W, int32_t H) {
+  const int64_t tx = (W + 15) / 16, ty = (H + 15) / 16;
+  if ((tx + 1) * (ty + 1) * 4 > 200 * 1024)
+    return set_err(LODGE_ERR_BAD_ARG, "resolution exceeds the tile-count table (max ~4K)");
+  return 0;
+}
+
+extern "C" {
+
+const char *lodge_last_error(void) { return g_err.c_str(); }
+
+int lodge_create(int32_t device, lodge_ctx **out) {
+  if (!out) return set_err(LODGE_ERR_BAD_ARG, "out is NULL");
+  int n = 0;
+  CK(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return set_err(LODGE_ERR_BAD_ARG, "no such CUDA device");
+  CK(cudaSetDevice(device));
+  lodge_ctx *c = new lodge_ctx();
+  c->device = device;
+  CK(cudaMalloc(&c->fs, sizeof(FrameState)));
+  CK(cudaMemset(c->fs, 0, sizeof(FrameState)));
+  CK(cudaMalloc(&c->cam_dev, sizeof(lodge_camera)));
+  CK(cudaMallocHost(&c->cam_host, sizeof(lodge_camera)));
+  CK(cudaMallocHost(&c->stats_host, sizeof(lodge_frame_stats)));
+  int rc = ensure_status(c, 1 << 16);
+  if (rc) return rc;
+  *out = c;
+  return 0;
+}
+
+void lodge_destroy(lodge_ctx *c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  Work &w = c->w;
+  void *ptrs[] = {w.key_depth[0], w.key_depth[1], w.val_depth[0], w.val_depth[1], w.rect,
+                  w.payload, w.precise, w.pairs[0], w.pairs[1], w.tile_diff, w.tile_start,
+                  w.status, w.union_idx, w.union_tag, c->fs, c->cam_dev};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  if (c->cam_host) cudaFreeHost(c->cam_host);
+  if (c->stats_host) cudaFreeHost(c->stats_host);
+  delete c;
+}
+
+int lodge_set_stream(lodge_ctx *c, void *stream) {
+  if (!c) return set_err(LODGE_ERR_BAD_ARG, "ctx is NULL");
+  c->stream = (cudaStream_t)stream;
+  return 0;
+}
+
+int lodge_set_precision(lodge_ctx *c, int32_t p) {
+  if (!c) return set_err(LODGE_ERR_BAD_ARG, "ctx is NULL");
+  if (p != LODGE_PREC_FAST && p != LODGE_PREC_EXACT)
+    return set_err(LODGE_ERR_BAD_ARG, "precision must be LODGE_PREC_FAST or LODGE_PREC_EXACT");
+  c->precision = p;
+  return 0;
+}
+
+int lodge_reserve(lodge_ctx *c, int64_t max_splats, int64_t max_pairs) {
+  if (!c) return set_err(LODGE_ERR_BAD_ARG, "ctx is NULL");
+  CK(cudaSetDevice(c->device));
+  int rc = ensure_M(c, max_splats);
+  if (rc) return rc;
+  rc = ensure_P(c, max_pairs);
+  if (rc) return rc;
+  return ensure_status(c, std::max<int64_t>((max_splats + 4095) / 4096 * 256,
+                                            (max_splats + 255) / 256 * 2));
+}
+
+int lodge_select(lodge_ctx *c, const double *centers, int32_t K, const double *pos, int32_t n,
+                 int32_t *f, int32_t *o, double *tb, double *t) {
+  if (!c || !centers || !pos || !f || !o || !tb || !t)
+    return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  if (K < 1) return set_err(LODGE_ERR_BAD_ARG, "a chunk plan needs at least one chunk");
+  launch_select(centers, K, pos, n, f, o, tb, t, c->stream);
+  return check_launch("lodge_select");
+}
+
+int lodge_blend_factor(lodge_ctx *c, const double *in, int32_t n, double *out) {
+  if (!c || !in || !out) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  launch_blend_factor(in, n, out, c->stream);
+  return check_launch("lodge_blend_factor");
+}
+
+int lodge_compose(lodge_ctx *c, const lodge_chunks *ch, int32_t f, int32_t o,
+                  uint32_t **out_idx, uint8_t **out_tag, int64_t *out_sizes) {
+  if (!c || !ch || !out_idx || !out_tag || !out_sizes) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  if (f < 0 || f >= ch->K) return set_err(LODGE_ERR_BAD_ARG, "chunk " + std::to_string(f) + " is not in the plan");
+  if (o >= ch->K || o < -1) return set_err(LODGE_ERR_BAD_ARG, "chunk " + std::to_string(o) + " is not in the plan");
+  if (o == f) return set_err(LODGE_ERR_BAD_ARG, "blending needs two distinct chunks");
+  if (ch->L < 1 || ch->L > LODGE_MAX_LEVELS) return set_err(LODGE_ERR_BAD_ARG, "bad level count");
+  CK(cudaSetDevice(c->device));
+  LevelSlots ls;
+  ls.n_levels = ch->L;
+  ls.slot_base[0] = 0;
+  for (int l = 0; l < ch->L; ++l) ls.slot_base[l + 1] = ls.slot_base[l] + (uint32_t)(2 * ch->max_set[l]);
+  int rc = ensure_slots(c, ls.slot_base[ch->L]);
+  if (rc) return rc;
+  rc = ensure_status(c, (int64_t)ch->L * union_status_stride(ls.slot_base[ch->L]));
+  if (rc) return rc;
+  launch_begin_frame(c->fs, c->stream);
+  launch_select_frame(ch->centers_dev, ch->K, c->cam_dev, nullptr, nullptr, 1, f, o, 1.0, c->fs,
+                      c->stream);
+  launch_union(*ch, ls, c->fs, c->w.status, c->w.union_idx, c->w.union_tag, c->stream);
+  rc = check_launch("lodge_compose");
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(c->stats_host, &c->fs->stats, sizeof(lodge_frame_stats),
+                     cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int l = 0; l < ch->L; ++l) {
+    out_sizes[l] = c->stats_host->U_level[l];
+    if (out_idx[l] && out_sizes[l])
+      CK(cudaMemcpyAsync(out_idx[l], c->w.union_idx + ls.slot_base[l], 4 * out_sizes[l],
+                         cudaMemcpyDeviceToDevice, c->stream));
+    if (out_tag[l] && out_sizes[l])
+      CK(cudaMemcpyAsync(out_tag[l], c->w.union_tag + ls.slot_base[l], out_sizes[l],
+                         cudaMemcpyDeviceToDevice, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int lodge_project(lodge_ctx *c, const lodge_level *level, const int64_t *idx, int64_t n,
+                  const double *mod, const lodge_camera *cam, const lodge_raster_params *rp,
+                  int32_t shade, lodge_batch *out, int64_t *out_m) {
+  if (!c || !level || !rp || !out || !out_m) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  int rc = check_cam(cam);
+  if (rc) return rc;
+  if (level->sh_degree < 0 || level->sh_degree > 3)
+    return set_err(LODGE_ERR_BAD_ARG, "sh degree must be in 0..3, got " + std::to_string(level->sh_degree));
+  if (n > 0x3fffffff) return set_err(LODGE_ERR_BAD_ARG, "too many inputs");
+  *out_m = 0;
+  if (n <= 0) return 0;
+  CK(cudaSetDevice(c->device));
+  rc = ensure_status(c, (n + 255) / 256 + 1);
+  if (rc) return rc;
+  *c->cam_host = *cam;
+  CK(cudaMemcpyAsync(c->cam_dev, c->cam_host, sizeof(lodge_camera), cudaMemcpyHostToDevice, c->stream));
+  launch_begin_frame(c->fs, c->stream);
+  launch_project_compat(*level, idx, n, mod, c->w, c->fs, c->cam_dev, *rp, shade, out, c->stream);
+  rc = check_launch("lodge_project");
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(c->stats_host, &c->fs->stats, sizeof(lodge_frame_stats),
+                     cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *out_m = c->stats_host->M;
+  return 0;
+}
+
+int lodge_rasterize(lodge_ctx *c, const lodge_batch *b, int64_t M, int64_t n_inputs,
+                    const lodge_camera *cam, const lodge_raster_params *rp, int32_t flags,
+                    const lodge_frame_out *out, int64_t *tile_offsets, int64_t *tile_src,
+                    int64_t list_cap, lodge_frame_stats *stats) {
+  if (!c || !b || !rp || !out) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  int rc = check_cam(cam);
+  if (rc) return rc;
+  rc = check_tile_smem(cam->w, cam->h);
+  if (rc) return rc;
+  if (M < 0 || M > 0x3fffffff || n_inputs < M) return set_err(LODGE_ERR_BAD_ARG, "bad batch size");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  const int32_t tiles_x = (cam->w + 15) / 16, tiles_y = (cam->h + 15) / 16;
+  const int32_t T = tiles_x * tiles_y;
+  if ((rc = ensure_M(c, std::max<int64_t>(M, 1))) || (rc = ensure_tiles(c, cam->w, cam->h)) ||
+      (rc = ensure_status(c, (M + 4095) / 4096 * 256 + (M + 255) / 256 + 256)) ||
+      (rc = ensure_P(c, 1)))
+    return rc;
+  *c->cam_host = *cam;
+  CK(cudaMemcpyAsync(c->cam_dev, c->cam_host, sizeof(lodge_camera), cudaMemcpyHostToDevice, s));
+  const bool exact = c->precision == LODGE_PREC_EXACT;
+  if ((flags & LODGE_RECORD_MAX) && out->maxw_dev && n_inputs > 0)
+    CK(cudaMemsetAsync(out->maxw_dev, 0, (exact ? 8 : 4) * (size_t)n_inputs, s));
+  int32_t nl = 0;
+  launch_begin_frame(c->fs, s);
+  launch_import_batch(*b, M, c->w, c->fs, c->cam_dev, *rp, exact, s);
+  launch_depth_sort(c->w, c->fs, M, &nl, s);
+  launch_tile_setup(c->w, c->fs, out->tile_count_dev, tiles_x, tiles_y, s);
+  rc = check_launch("lodge_rasterize: setup");
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(c->stats_host, &c->fs->stats, sizeof(lodge_frame_stats), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const uint32_t P = c->stats_host->P;
+  if ((int64_t)P > c->w.P_cap) {  // grow, then clear the overflow the setup recorded
+    rc = ensure_P(c, P);
+    if (rc) return rc;
+    const uint32_t fix[2] = {P, 0u};
+    CK(cudaMemcpy(&c->fs->n_pairs, &fix[0], 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(&c->fs->stats.overflow, &fix[1], 4, cudaMemcpyHostToDevice));
+  }
+  const Work &w = c->w;
+  launch_duplicate(w, c->fs, tiles_x, M, s);
+  launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s);
+  launch_composite(w, c->fs, c->cam_dev, cam->w, cam->h, *rp, flags, exact, *out, 0, s);
+  if (tile_offsets && tile_src) launch_export_lists(w, c->fs, T, tile_offsets, tile_src, list_cap, s);
+  rc = check_launch("lodge_rasterize");
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(c->stats_host, &c->fs->stats, sizeof(lodge_frame_stats), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (stats) *stats = *c->stats_host;
+  return 0;
+}
+
+int lodge_render_frame(lodge_ctx *c, const lodge_level *levels, int32_t n_levels,
+                       const lodge_chunks *ch, const lodge_camera *cam_dev, int32_t W, int32_t H,
+                       const lodge_raster_params *rp, const int32_t *pair,
+                       const double *t_override, int32_t flags, const lodge_frame_out *out,
+                       lodge_frame_stats *stats_dev) {
+  if (!c || !levels || !ch || !cam_dev || !rp || !out) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  if (n_levels != ch->L || n_levels < 1 || n_levels > LODGE_MAX_LEVELS)
+    return set_err(LODGE_ERR_BAD_ARG, "level count does not match the chunk plan");
+  if (W <= 0 || H <= 0) return set_err(LODGE_ERR_BAD_ARG, "camera resolution must be positive");
+  int rc = check_tile_smem(W, H);
+  if (rc) return rc;
+  int32_t pf = 0, po = -1;
+  double tv = 1.0;
+  if (pair) {
+    pf = pair[0];
+    po = pair[1];
+    if (pf < 0 || pf >= ch->K) return set_err(LODGE_ERR_BAD_ARG, "chunk " + std::to_string(pf) + " is not in the plan");
+    if (po < -1 || po >= ch->K) return set_err(LODGE_ERR_BAD_ARG, "chunk " + std::to_string(po) + " is not in the plan");
+    if (po == pf) return set_err(LODGE_ERR_BAD_ARG, "blending needs two distinct chunks");
+    tv = t_override ? *t_override : 1.0;
+  }
+  for (int l = 0; l < n_levels; ++l)
+    if (levels[l].sh_degree < 0 || levels[l].sh_degree > 3)
+      return set_err(LODGE_ERR_BAD_ARG, "sh degree must be in 0..3");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  LevelSlots ls;
+  ls.n_levels = n_levels;
+  ls.slot_base[0] = 0;
+  for (int l = 0; l < n_levels; ++l) ls.slot_base[l + 1] = ls.slot_base[l] + (uint32_t)(2 * ch->max_set[l]);
+  const int64_t U_cap = ls.slot_base[n_levels];
+  const int32_t tiles_x = (W + 15) / 16, tiles_y = (H + 15) / 16;
+  if ((rc = ensure_slots(c, U_cap)) || (rc = ensure_M(c, std::max<int64_t>(U_cap, 1))) ||
+      (rc = ensure_tiles(c, W, H)) || (rc = ensure_P(c, 1)) ||
+      (rc = ensure_status(c, (c->w.M_cap + 4095) / 4096 * 256 + (U_cap + 255) / 256 + 256)))
+    return rc;
+  const bool exact = c->precision == LODGE_PREC_EXACT;
+  const Work &w = c->w;
+  c->last_slots = ls;
+  int32_t nl = 0;
+  launch_begin_frame(c->fs, s); ++nl;
+  launch_select_frame(ch->centers_dev, ch->K, cam_dev, nullptr, nullptr, pair != nullptr, pf, po,
+                      tv, c->fs, s); ++nl;
+  launch_union(*ch, ls, c->fs, w.status, w.union_idx, w.union_tag, s); nl += 2;
+  if ((flags & LODGE_RECORD_MAX) && out->maxw_dev)
+    CK(cudaMemsetAsync(out->maxw_dev, 0, (exact ? 8 : 4) * (size_t)U_cap, s));
+  rc = launch_project_frame(levels, ls, w, c->fs, cam_dev, *rp, (flags & LODGE_NEED_IMAGE) ? 1 : 0,
+                            exact, s);
+  if (rc) return set_err(LODGE_ERR_BAD_ARG, "all levels must share one storage precision");
+  ++nl;
+  launch_depth_sort(w, c->fs, U_cap, &nl, s);
+  launch_tile_setup(w, c->fs, out->tile_count_dev, tiles_x, tiles_y, s); ++nl;
+  launch_duplicate(w, c->fs, tiles_x, U_cap, s); ++nl;
+  launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s);
+  launch_composite(w, c->fs, cam_dev, W, H, *rp, flags, exact, *out, 0, s); ++nl;
+  if (stats_dev)
+    CK(cudaMemcpyAsync(stats_dev, &c->fs->stats, sizeof(lodge_frame_stats), cudaMemcpyDeviceToDevice, s));
+  c->launches = nl;
+  return check_launch("lodge_render_frame");
+}
+
+int lodge_frame_lists(lodge_ctx *c, int32_t T, int64_t *tile_offsets, int64_t *tile_src,
+                      int64_t cap) {
+  if (!c || !tile_offsets || !tile_src) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  if (!c->w.pairs[0] || T + 1 > c->tiles_cap) return set_err(LODGE_ERR_BAD_ARG, "no frame rendered at this size");
+  launch_export_lists(c->w, c->fs, T, tile_offsets, tile_src, cap, c->stream);
+  return check_launch("lodge_frame_lists");
+}
+
+int lodge_frame_union(lodge_ctx *c, int32_t level, uint32_t *idx, uint8_t *tag, int64_t cap) {
+  if (!c || !idx || !tag) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  if (level < 0 || level >= c->last_slots.n_levels) return set_err(LODGE_ERR_BAD_ARG, "bad level");
+  const int64_t n = std::min<int64_t>(cap, c->last_slots.slot_base[level + 1] - c->last_slots.slot_base[level]);
+  if (n > 0) {
+    CK(cudaMemcpyAsync(idx, c->w.union_idx + c->last_slots.slot_base[level], 4 * n,
+                       cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(tag, c->w.union_tag + c->last_slots.slot_base[level], n,
+                       cudaMemcpyDeviceToDevice, c->stream));
+  }
+  return 0;
+}
+
+int32_t lodge_last_launch_count(lodge_ctx *c) { return c ? c->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,123 @@
+"""Device-resident per-frame renderer: the fused hot path.
+
+A Renderer owns the level store and chunk plan on one GPU and renders camera
+views end to end with lodge_render_frame: chunk selection -> union +
+modulation -> projection -> depth sort -> binning -> tile sort ->
+compositing, with no host synchronisation inside a frame.  Outputs stay in
+HBM (image, per_tile_count, per_pixel_visible, per_gaussian_max_weight) until
+the caller reads them.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .device import (CAMERA_BYTES, DeviceLevel, DevicePlan, camera_bytes, context,
+                     params_struct, ptr)
+from .types import TILE_SIZE, RasterConfig
+
+STATS_BYTES = C.sizeof(N.FrameStats)
+
+
+@dataclass
+class Frame:
+    """Device outputs of one view (reference TileRenderOutput fields)."""
+
+    width: int
+    height: int
+    image: Optional[torch.Tensor]        # (H, W, 3) fp32 (fast) / fp64 (exact)
+    tile_count: torch.Tensor             # (tiles_y, tiles_x) int32
+    visible: torch.Tensor                # (H, W) int32
+    maxw: Optional[torch.Tensor]         # (U_cap,) fp32 / fp64; first stats.U valid
+    stats: torch.Tensor                  # lodge_frame_stats bytes
+
+    def read_stats(self) -> N.FrameStats:
+        raw = self.stats.cpu().numpy().tobytes()
+        return N.FrameStats.from_buffer_copy(raw)
+
+
+class Renderer:
+    def __init__(self, levels: Sequence, plan, device=None, storage: str = "fp32",
+                 precision: str = "fast", raster_cfg: RasterConfig = RasterConfig()):
+        self.ctx = context(device)
+        self.device = self.ctx.device
+        self.levels = []
+        for lv in levels:
+            if isinstance(lv, DeviceLevel):
+                self.levels.append(lv)
+            else:
+                self.levels.append(DeviceLevel(getattr(lv, "scene", lv), self.device, storage))
+        self.plan = plan if isinstance(plan, DevicePlan) else DevicePlan(plan, self.device)
+        if self.plan.L != len(self.levels):
+            raise ValueError("chunk plan and level list disagree on the level count")
+        self._level_arr = (N.Level * len(self.levels))(*[l.struct for l in self.levels])
+        self.precision = precision
+        self.cfg = raster_cfg
+        self._rp = params_struct(raster_cfg)
+        self.U_cap = self.plan.union_capacity
+
+    # ------------------------------------------------------------------
+    def reserve(self, max_pairs: int):
+        N.check(N.lib().lodge_reserve(self.ctx.bind(self.precision), self.U_cap, int(max_pairs)),
+                "lodge_reserve")
+
+    def alloc_frame(self, width: int, height: int, need_image=True, record_max=True) -> Frame:
+        tx, ty = -(-width // TILE_SIZE), -(-height // TILE_SIZE)
+        fdt = torch.float64 if self.precision == "exact" else torch.float32
+        d = self.device
+        return Frame(width, height,
+                     torch.empty((height, width, 3), dtype=fdt, device=d) if need_image else None,
+                     torch.empty((ty, tx), dtype=torch.int32, device=d),
+                     torch.empty((height, width), dtype=torch.int32, device=d),
+                     torch.empty(max(self.U_cap, 1), dtype=fdt, device=d) if record_max else None,
+                     torch.zeros(STATS_BYTES, dtype=torch.uint8, device=d))
+
+    def upload_cameras(self, cameras) -> torch.Tensor:
+        """(V, sizeof(lodge_camera)) uint8 device tensor of camera structs."""
+        host = np.stack([camera_bytes(c) for c in cameras])
+        return torch.from_numpy(host).to(self.device)
+
+    def render(self, cam_row: torch.Tensor, frame: Frame, pair=None, t: float = None,
+               need_image: bool = True, record_max: bool = True) -> Frame:
+        """Enqueue one frame on the current stream.  cam_row: one row of
+        upload_cameras().  pair=None: nearest two chunks chosen on device."""
+        out = N.FrameOut()
+        out.image_dev = frame.image.data_ptr() if (need_image and frame.image is not None) else None
+        out.tile_count_dev = frame.tile_count.data_ptr()
+        out.visible_dev = frame.visible.data_ptr()
+        out.maxw_dev = frame.maxw.data_ptr() if (record_max and frame.maxw is not None) else None
+        flags = (N.NEED_IMAGE if need_image else 0) | (N.RECORD_MAX if record_max else 0)
+        pr = None
+        tv = None
+        if pair is not None:
+            f, o = pair
+            pr = (C.c_int32 * 2)(int(f), -1 if o is None else int(o))
+            tv = C.c_double(1.0 if t is None else float(t))
+        N.check(N.lib().lodge_render_frame(
+            self.ctx.bind(self.precision), self._level_arr, len(self.levels), C.byref(self.plan.struct),
+            ptr(cam_row), frame.width, frame.height, C.byref(self._rp), pr,
+            None if tv is None else C.byref(tv), flags, C.byref(out), ptr(frame.stats)),
+            "lodge_render_frame")
+        return frame
+
+    def last_launch_count(self) -> int:
+        return int(N.lib().lodge_last_launch_count(self.ctx.ptr))
+
+    def render_camera(self, camera, need_image=True, record_max=True, pair=None, t=None):
+        """Convenience: one host camera -> host outputs (image fp64, counts int64)."""
+        w, h = (int(v) for v in camera.resolution)
+        fr = self.alloc_frame(w, h, need_image, record_max)
+        cams = self.upload_cameras([camera])
+        self.render(cams[0], fr, pair=pair, t=t, need_image=need_image, record_max=record_max)
+        st = fr.read_stats()
+        if st.overflow:
+            self.reserve(int(st.P))
+            self.render(cams[0], fr, pair=pair, t=t, need_image=need_image, record_max=record_max)
+            st = fr.read_stats()
+        return fr, st

@@ -1,0 +1,190 @@
+"""GPU parity: liblodge kernels against the reference-generated golden vectors
+and the pinned CPU oracle.  Marked gpu (run on a B200 via gpurun).
+
+Bars:
+  bit-exact  chunk selection (f, o, t_bar, t), active sets, modulations,
+             projected batch fields, per_tile_count, sorted per-tile lists;
+  EXACT      image <= 1e-12, per_pixel_visible exact, max weights rtol 1e-12
+             (fp64; only exp() differs from NumPy's by an ulp);
+  FAST       image max-abs <= 1e-3 per channel and PSNR >= 60 dB,
+             per_pixel_visible within 1 on <= 0.1% of pixels.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2505_23158_b200 as L  # noqa: E402
+from paper_2505_23158_b200 import device as D  # noqa: E402
+from paper_2505_23158_b200.raster import (DeviceBatch, project_scene_device,  # noqa: E402
+                                          rasterize_device)
+
+from .golden_util import batch, camera, cfg, config1_levels, config1_sets, load, scene  # noqa: E402
+
+CASES = load("cases.npz")
+CASE_NAMES = [str(n) for n in CASES["names"]]
+BATCH_FIELDS = [("source_index", "src"), ("mean2d", "mean2d"), ("cov2d", "cov2d"),
+                ("conic", "conic"), ("extent", "extent"), ("depth", "depth"),
+                ("opacity_eff", "opacity"), ("color", "color")]
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    yield
+    D.set_default_precision("exact")
+
+
+def psnr(a, b):
+    mse = float(np.mean((np.asarray(a, float) - np.asarray(b, float)) ** 2))
+    return float("inf") if mse == 0 else -10.0 * np.log10(mse)
+
+
+def host_batch(d, p):
+    g = batch(d, p)
+    return L.Splat2DBatch(g["n_inputs"], g["src"], g["mean2d"], g["cov2d"], g["conic"],
+                          g["extent"], g["depth"], g["opacity"], g["color"])
+
+
+def lists_of(res):
+    return res["tile_offsets"].cpu().numpy(), res["tile_src"].cpu().numpy()
+
+
+def check_exact(res, d, p):
+    out = L.raster.output_to_host(res, L.RasterConfig())
+    assert np.array_equal(out.per_tile_count, d[p + "tile_count"])
+    offs, tsrc = lists_of(res)
+    assert np.array_equal(offs, d[p + "tile_offsets"])
+    assert np.array_equal(tsrc, d[p + "tile_src"])
+    assert np.array_equal(out.per_pixel_visible, d[p + "visible"])
+    np.testing.assert_allclose(out.image, d[p + "image"], atol=1e-12, rtol=0)
+    np.testing.assert_allclose(out.per_gaussian_max_weight, d[p + "maxw"], rtol=1e-12, atol=1e-300)
+
+
+def check_fast(res, d, p):
+    out = L.raster.output_to_host(res, L.RasterConfig())
+    assert np.array_equal(out.per_tile_count, d[p + "tile_count"])
+    offs, tsrc = lists_of(res)
+    assert np.array_equal(offs, d[p + "tile_offsets"])
+    assert np.array_equal(tsrc, d[p + "tile_src"])
+    ref = d[p + "image"]
+    err = np.abs(out.image - ref).max() if ref.size else 0.0
+    assert err <= 1e-3, err
+    assert psnr(out.image, ref) >= 60.0
+    dv = np.abs(out.per_pixel_visible - d[p + "visible"])
+    assert dv.max(initial=0) <= 1 and np.count_nonzero(dv) <= max(1, dv.size // 1000)
+    np.testing.assert_allclose(out.per_gaussian_max_weight, d[p + "maxw"], atol=2e-3)
+
+
+@pytest.mark.parametrize("name", CASE_NAMES)
+def test_case_projection_bit_exact(name):
+    d, p = CASES, name + "/"
+    sc, cam, rc = scene(d, p), camera(d, p), cfg(d, p)
+    idx = d[p + "idx"] if p + "idx" in d else None
+    mod = d[p + "mod"] if p + "mod" in d else None
+    got = L.project_scene(sc, cam, rc, indices=idx, modulation=mod)
+    assert got.n_inputs == int(d[p + "b_n_inputs"])
+    for gk, rk in BATCH_FIELDS:
+        ref = d[p + "b_" + rk]
+        assert np.array_equal(getattr(got, gk).reshape(ref.shape), ref), gk
+
+
+@pytest.mark.parametrize("name", CASE_NAMES)
+@pytest.mark.parametrize("prec", ["exact", "fast"])
+def test_case_raster(name, prec):
+    d, p = CASES, name + "/"
+    cam, rc = camera(d, p), cfg(d, p)
+    ctx = D.context()
+    db = DeviceBatch.from_host(host_batch(d, p + "b_"), ctx.device)
+    res = rasterize_device(db, cam, rc, True, True, precision=prec, lists=True)
+    (check_exact if prec == "exact" else check_fast)(res, d, p + "o_")
+
+
+@pytest.fixture(scope="module")
+def c1():
+    return load("config1.npz")
+
+
+@pytest.fixture(scope="module")
+def c1_objects(c1):
+    levels = [L.LodLevel(l, float(c1[f"L{l}/depth_threshold"]),
+                         L.Scene(s.means, s.scales, s.rotations, s.opacities, s.sh_coeffs,
+                                 s.filter_variance, s.sh_degree),
+                         np.arange(len(s.means)))
+              for l, s in enumerate(config1_levels(c1))]
+    sets = config1_sets(c1)
+    plan = L.ChunkPlan(c1["centers"], c1["radii"], tuple(tuple(ch) for ch in sets))
+    return levels, plan
+
+
+@pytest.mark.parametrize("v", range(8))
+def test_config1_select_and_compose(c1, c1_objects, v):
+    levels, plan = c1_objects
+    p = f"v{v}/"
+    cam = camera(c1, p)
+    f, o = L.nearest_two_chunks(plan, cam.position)
+    assert (f, o) == tuple(int(x) for x in c1[p + "pair"])
+    tb, t = L.blend_factor(cam.position, plan.centers[f], plan.centers[o])
+    assert tb == c1[p + "t"][0] and t == c1[p + "t"][1]
+    sel = L.compose_active(plan, levels, f, o, t)
+    for l in range(len(levels)):
+        assert np.array_equal(sel.sets[l], c1[p + f"sel{l}"])
+        assert np.array_equal(sel.modulations[l], c1[p + f"mod{l}"])
+
+
+@pytest.mark.parametrize("v", range(8))
+@pytest.mark.parametrize("prec", ["exact", "fast"])
+def test_config1_render_selection(c1, c1_objects, v, prec):
+    levels, plan = c1_objects
+    p = f"v{v}/"
+    cam = camera(c1, p)
+    sets = [c1[p + f"sel{l}"] for l in range(len(levels))]
+    mods = [c1[p + f"mod{l}"] for l in range(len(levels))]
+    db = L.lod.project_selection_device(levels, sets, cam, L.RasterConfig(), mods)
+    hb = db.to_host()
+    for gk, rk in BATCH_FIELDS:
+        ref = c1[p + "b_" + rk]
+        assert np.array_equal(getattr(hb, gk).reshape(ref.shape), ref), gk
+    res = rasterize_device(db, cam, L.RasterConfig(), True, True, precision=prec, lists=True)
+    (check_exact if prec == "exact" else check_fast)(res, c1, p + "o_")
+
+
+@pytest.mark.parametrize("prec", ["exact", "fast"])
+def test_config1_fused_frame(c1, c1_objects, prec):
+    """lodge_render_frame (device-side select -> ... -> composite) vs golden."""
+    levels, plan = c1_objects
+    r = L.Renderer(levels, plan, storage="fp64", precision=prec)
+    for v in range(8):
+        p = f"v{v}/"
+        cam = camera(c1, p)
+        fr, st = r.render_camera(cam)
+        assert (st.f, st.o) == tuple(int(x) for x in c1[p + "pair"])
+        assert st.t == c1[p + "t"][1]
+        assert st.U == int(c1[p + "b_n_inputs"]) and st.M == len(c1[p + "b_src"])
+        tc = fr.tile_count.cpu().numpy()
+        assert np.array_equal(tc, c1[p + "o_tile_count"])
+        img = fr.image.double().cpu().numpy()
+        vis = fr.visible.cpu().numpy()
+        mw = fr.maxw[:st.U].double().cpu().numpy()
+        if prec == "exact":
+            np.testing.assert_allclose(img, c1[p + "o_image"], atol=1e-12, rtol=0)
+            assert np.array_equal(vis, c1[p + "o_visible"])
+            np.testing.assert_allclose(mw, c1[p + "o_maxw"], rtol=1e-12, atol=1e-300)
+        else:
+            assert np.abs(img - c1[p + "o_image"]).max() <= 1e-3
+            assert psnr(img, c1[p + "o_image"]) >= 60
+
+
+def test_fused_frame_deterministic(c1_objects, c1):
+    levels, plan = c1_objects
+    r = L.Renderer(levels, plan, storage="fp32", precision="fast")
+    cam = camera(c1, "v3/")
+    a, _ = r.render_camera(cam)
+    img0, vis0, mw0 = a.image.clone(), a.visible.clone(), a.maxw.clone()
+    for _ in range(3):
+        b, _ = r.render_camera(cam)
+        assert torch.equal(b.image, img0) and torch.equal(b.visible, vis0)
+        assert torch.equal(b.maxw, mw0)
