@@ -1,0 +1,455 @@
+#!/usr/bin/env python
+"""LODGE per-frame render throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lodge|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
+
+Workload (config 5 on config 3): a 4096-view camera sweep at
+1920x1080 along a synthetic 20M-Gaussian, 5-LOD, 64-chunk corridor
+(fixtures/scenes.py).  Views are block-cyclic over ranks, 16 consecutive
+views per block; one step = one block per rank, every view rendered end to
+end on the device (chunk selection, union + blend weights, projection, depth
+sort, binning, tile sort, compositing, outputs resident in HBM).  Weak
+scaling; the store is replicated on every GPU; NCCL gathers metrics only.
+
+--impl reference times the reference algorithm on the host cores: the CPU
+restatement in oracle/ (the reference is Python and cannot run on the GPU
+box), rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frames/sec at 1080p (1/2/4/8 B200, views sharded) vs CPU ref; % of HBM roofline"
+UNIT = "frames/s"
+SWEEP_VIEWS = 4096
+BLOCK = 16
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="lodge", choices=["lodge", "reference"])
+    ap.add_argument("--config", default="config3")
+    ap.add_argument("--precision", default="fast", choices=["fast", "exact"])
+    ap.add_argument("--views-per-step", type=int, default=BLOCK)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-views", type=int, default=1, help="views in the CPU baseline sample")
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def workload_name(cfg_name):
+    return {"config3": "config5 sweep over config3: 4096 views, 1920x1080, 20M Gaussians, "
+                       "5 LODs, 64 chunks, SH3, chunk opacity blending",
+            "config2": "config2 scene (1M Gaussians, 3 LODs, 16 chunks, SH3) swept at 1920x1080",
+            "street1080": "46k-Gaussian street, 2 LODs, 4 chunks, SH1, 1920x1080"}[cfg_name]
+
+
+def my_views(rank, world, n_steps_total, block):
+    """Block-cyclic view assignment: block b of `block` consecutive sweep views
+    goes to rank b % world; step s of this rank uses its s-th block (cyclic)."""
+    n_blocks = SWEEP_VIEWS // block
+    mine = [b for b in range(n_blocks) if b % world == rank]
+    return [[mine[s % len(mine)] * block + v for v in range(block)] for s in range(n_steps_total)]
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes per stage
+# ---------------------------------------------------------------------------
+def stage_bytes(U, AB, M, P, W, H, sh_terms, geom_bytes=48, sh_elem=4):
+    sh_b = 3 * sh_terms * sh_elem
+    return {
+        "select": 0.0,
+        "union": 4.0 * AB + 5.0 * U,
+        "project": U * (5.0 + geom_bytes) + M * (sh_b + 8 + 4 + 8 + 64 + 64),
+        "depth_sort": M * (8.0 + 8 * 24.0),
+        "tile_setup": 0.0,
+        "duplicate": M * 12.0 + P * 8.0,
+        "tile_sort": 2 * 16.0 * P,
+        "composite": P * 8.0 + M * 64.0 + W * H * 16.0 + U * 4.0,
+    }
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def load_traffic(kernel_stage):
+    """dram bytes per launch from a committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(kernel_stage)
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle restatement of the reference algorithm)
+# ---------------------------------------------------------------------------
+def cpu_render_view(cfg, cam, O):
+    f, o, tb, t = O.select(cfg.centers, cam.position)
+    oc = O.camera_from(cam)
+    rc = O.cfg_struct(_raster_cfg())
+    parts = []
+    for l in range(cfg.L):
+        b = cfg.set(o, l).astype(np.int64) if o is not None else np.zeros(0, np.int64)
+        idx, mod, _ = O.union(cfg.set(f, l).astype(np.int64), b, t)
+        g, s, _ = cfg.levels[l]
+        parts.append(O.project_f32(g, s, cfg.degree, idx, oc, rc, mod))
+    batch = O.concat(parts)
+    w, h = cam.resolution
+    return O.rasterize(batch, w, h, rc, lists=False), batch
+
+
+def _raster_cfg():
+    from paper_2505_23158_b200.types import RasterConfig
+    return RasterConfig()
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    from fixtures import scenes
+    from oracle import oracle as O
+    O.lib()
+    cfg = scenes.build(args.config)
+    sweep = cfg.sweep(SWEEP_VIEWS)
+    views = [v for blk in my_views(0, 1, args.warmup + args.steps, BLOCK) for v in blk[:1]]
+    for v in views[:args.warmup]:
+        cpu_render_view(cfg, sweep[v], O)
+    times = []
+    for v in views[args.warmup:]:
+        t0 = time.perf_counter()
+        cpu_render_view(cfg, sweep[v], O)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    fps = len(times) / total
+    cores = O.num_threads()
+    line = {"metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": workload_name(args.config), "views_per_step": 1},
+            "cpu_baseline": {"value": fps, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"1 sweep view per step ({len(times)} views), oracle/ C "
+                                       f"restatement with OpenMP on {cores} threads, "
+                                       f"{cpu_model()}"},
+            "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_lodge(args):
+    import torch
+    import torch.distributed as dist
+
+    from fixtures import scenes
+    import paper_2505_23158_b200 as LG
+    from paper_2505_23158_b200 import _native as N
+    from paper_2505_23158_b200.device import DeviceLevel, DevicePlan
+    from paper_2505_23158_b200.renderer import STATS_BYTES
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    t_setup = time.time()
+    cfg = scenes.build(args.config)
+    levels = [DeviceLevel.from_tensors(torch.from_numpy(g).to(dev), torch.from_numpy(s).to(dev),
+                                       cfg.degree) for g, s, _ in cfg.levels]
+    plan = DevicePlan.from_arrays(cfg.centers, cfg.offsets, cfg.data, cfg.L, dev)
+    r = LG.Renderer(levels, plan, device=dev, storage="fp32", precision=args.precision)
+    store_gb = sum(l.nbytes() for l in levels) / 1e9
+    B = args.views_per_step
+    schedule = my_views(rank, world, args.warmup + args.steps, B)
+    sweep = cfg.sweep(SWEEP_VIEWS)
+    W, H = sweep[0].resolution
+    flat = sorted({v for blk in schedule for v in blk})
+    pos = {v: i for i, v in enumerate(flat)}
+    cams = r.upload_cameras([sweep[v] for v in flat])
+    frames = [r.alloc_frame(W, H) for _ in range(B)]
+    n_timed = args.steps * B
+    stats_all = torch.zeros((n_timed, STATS_BYTES), dtype=torch.uint8, device=dev)
+
+    def read_stats(t):
+        raw = t.cpu().numpy()
+        return [N.FrameStats.from_buffer_copy(raw[i].tobytes()) for i in range(raw.shape[0])]
+
+    # sizing: every scheduled view once, then reserve pairs for the largest
+    sizing = torch.zeros((len(flat), STATS_BYTES), dtype=torch.uint8, device=dev)
+    r.reserve(64 << 20)
+    for i, v in enumerate(flat):
+        fr = frames[0]
+        r.render(cams[pos[v]], fr)
+        sizing[i].copy_(fr.stats)
+    torch.cuda.synchronize()
+    st_sz = read_stats(sizing)
+    P_max = max(s.P for s in st_sz)
+    r.reserve(int(P_max * 1.05) + 4096)
+    launches_per_frame = r.last_launch_count()
+    for s in range(args.warmup):
+        for j, v in enumerate(schedule[s]):
+            r.render(cams[pos[v]], frames[j])
+    torch.cuda.synchronize()
+    setup_s = time.time() - t_setup
+
+    # ---- timed region ----------------------------------------------------
+    clocks = Clocks(local)
+    N.check(N.lib().lodge_profile(r.ctx.ptr, 1, n_timed), "lodge_profile")
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    k = 0
+    for s in range(args.warmup, args.warmup + args.steps):
+        for j, v in enumerate(schedule[s]):
+            r.render(cams[pos[v]], frames[j])
+            stats_all[k].copy_(frames[j].stats, non_blocking=True)
+            k += 1
+    e1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    stage_ms = (C.c_double * N.N_STAGES)()
+    nprof = C.c_int32()
+    N.check(N.lib().lodge_profile_read(r.ctx.ptr, stage_ms, C.byref(nprof)), "profile_read")
+    N.check(N.lib().lodge_profile(r.ctx.ptr, 0, 0), "lodge_profile")
+    stats = read_stats(stats_all)
+    overflow = sum(s.overflow for s in stats)
+    ms_max = ms
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    total_frames = n_timed * world
+    value = total_frames / (ms_max / 1000.0)
+
+    # ---- per-stage roofline ----------------------------------------------
+    U = np.mean([s.U for s in stats])
+    M = np.mean([s.M for s in stats])
+    P = np.mean([s.P for s in stats])
+    def set_total(j):  # sum over levels of |set(j, l)|
+        return int(cfg.offsets[(j + 1) * cfg.L] - cfg.offsets[j * cfg.L]) if j >= 0 else 0
+
+    AB = np.mean([set_total(s.f) + set_total(s.o) for s in stats])
+    sb = stage_bytes(U, AB, M, P, W, H, (cfg.degree + 1) ** 2)
+    peak, peak_kind = load_peaks()
+    stages = {}
+    for i, name in enumerate(N.STAGES):
+        per = stage_ms[i] / max(nprof.value, 1)
+        gbs = sb[name] / (per / 1000.0) / 1e9 if per > 0 else 0.0
+        stages[name] = {"ms_per_frame": round(per, 5), "bytes_per_frame": round(sb[name]),
+                        "GB_s": round(gbs, 1), "frac": round(gbs / peak, 4)}
+    hbm_stages = ["union", "project", "depth_sort", "duplicate", "tile_sort"]
+    dom = max(N.STAGES, key=lambda k: stages[k]["ms_per_frame"])
+    dom_hbm = max(hbm_stages, key=lambda k: stages[k]["ms_per_frame"])
+    rf_stage = dom if dom in hbm_stages else dom_hbm
+    rs = stages[rf_stage]
+    roofline = {"bound": "hbm", "kernel": rf_stage, "achieved": rs["GB_s"], "peak": peak,
+                "unit": "GB/s", "frac": rs["frac"], "peak_kind": peak_kind,
+                "traffic": load_traffic(rf_stage),
+                "bytes_per_launch": rs["bytes_per_frame"], "ms_per_launch": rs["ms_per_frame"],
+                "dominant_stage": dom,
+                "note": "composite is FP32/MUFU-bound, not HBM; see stages" if dom == "composite"
+                else ""}
+
+    # ---- end to end through the public API --------------------------------
+    e2e = None
+    if not args.no_e2e:
+        cam_host = torch.empty((B, cams.shape[1]), dtype=torch.uint8).pin_memory()
+        cam_dev = torch.empty((B, cams.shape[1]), dtype=torch.uint8, device=dev)
+        img8 = torch.empty((B, H, W, 3), dtype=torch.uint8, device=dev)
+        img8_host = torch.empty((B, H, W, 3), dtype=torch.uint8).pin_memory()
+        st_host = torch.empty((B, STATS_BYTES), dtype=torch.uint8).pin_memory()
+        cams_host = cams.cpu()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for s in range(args.warmup, args.warmup + args.steps):
+            for j, v in enumerate(schedule[s]):
+                cam_host[j].copy_(cams_host[pos[v]])
+            cam_dev.copy_(cam_host, non_blocking=True)
+            for j in range(B):
+                r.render(cam_dev[j], frames[j])
+                r.to_srgb8(frames[j], img8[j])
+            img8_host.copy_(img8, non_blocking=True)
+            st_host.copy_(torch.stack([f.stats for f in frames]), non_blocking=True)
+        f1.record()
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": total_frames / (ems / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": int(B * cams.shape[1]),
+               "d2h_bytes_per_step": int(B * (H * W * 3 + STATS_BYTES)),
+               "path": "Renderer.render + to_srgb8 (8-bit sRGB like splatlod render), pinned "
+                       "host camera upload and image/stats read-back every step"}
+
+    # ---- gather per-rank metrics over NCCL ---------------------------------
+    per_rank = torch.tensor([ms, float(n_timed), P, float(overflow)], dtype=torch.float64,
+                            device=dev)
+    if world > 1:
+        gathered = [torch.zeros_like(per_rank) for _ in range(world)]
+        dist.all_gather(gathered, per_rank)
+        overflow = int(sum(float(g[3]) for g in gathered))
+
+    # ---- CPU baseline (rank 0, N=1): oracle on a bounded sample ------------
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        O.lib()
+        v = schedule[args.warmup][0]
+        cam = sweep[v]
+        t0 = time.perf_counter()
+        for _ in range(args.cpu_views):
+            ref, batch = cpu_render_view(cfg, cam, O)
+        dt = (time.perf_counter() - t0) / args.cpu_views
+        cpu = {"value": 1.0 / dt, "unit": UNIT, "cores": O.num_threads(), "kind": "port",
+               "sample": f"{args.cpu_views} view(s) of the same sweep (z={cam.position[2]:.2f}), "
+                         f"oracle/ C restatement, OpenMP {O.num_threads()} threads, "
+                         f"{cpu_model()}, {dt:.1f} s/view"}
+        fr = frames[0]
+        r.render(cams[pos[v]], fr)
+        st = fr.read_stats()
+        img = fr.image.double().cpu().numpy()
+        err = float(np.abs(img - ref["image"]).max())
+        mse = float(np.mean((img - ref["image"]) ** 2))
+        parity = {"view": int(v), "tile_count_exact": bool(np.array_equal(
+            fr.tile_count.cpu().numpy(), ref["per_tile_count"])), "P": int(st.P),
+            "P_oracle": int(ref["P"]), "M": int(st.M), "M_oracle": int(len(batch["src"])),
+            "image_max_abs": err, "psnr_db": (math.inf if mse == 0 else -10 * math.log10(mse))}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64 projection / f32 compositing (fp64 guard band)", "data": "synthetic",
+            "config": {"workload": workload_name(args.config), "resolution": [W, H],
+                       "views_per_step_per_gpu": B, "frames_timed": total_frames,
+                       "precision": args.precision, "store": "fp32 records, replicated",
+                       "store_gb": round(store_gb, 2),
+                       "l2": "inputs larger than L2: per-frame working set "
+                             f"~{(sb['project'] + sb['tile_sort'] + sb['composite']) / 1e9:.1f} GB"
+                             " >> 126 MB L2; no explicit flush",
+                       "mean_U": round(U), "mean_M": round(M), "mean_P": round(P),
+                       "levels": cfg.n_gaussians(), "chunks": cfg.K,
+                       "pairs_per_s": P * value, "gaussians_per_s": U * value,
+                       "overflow_frames": int(overflow), "setup_s": round(setup_s, 1)},
+            "e2e": e2e, "gpu_launches": int(launches_per_frame * total_frames),
+            "roofline": roofline, "stages": stages, "cpu_baseline": cpu, "clocks": clk,
+            "parity_sample": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_lodge(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

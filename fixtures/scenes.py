@@ -1,0 +1,204 @@
+"""Bench/test fixture configs (SURVEY.md 8d recipes) built with fixtures/synth.c.
+
+    cfg = build("config3")     # 20M Gaussians, 5 LODs, 64 chunks, SH3
+    cfg.levels  -> [(geom fp32 (n,12), sh fp32 (n,3,16), depth_threshold)]
+    cfg.plan    -> centers (K,3), radii (K,), offsets (K*L+1), data uint32
+    cfg.sweep(n)-> n trajectory cameras along the corridor (config 5)
+
+Levels use the pruning proxy of the recipe (keep the top fraction by
+opacity * max(scale)^2, ties by index) with the Eq. 3 filter variance
+d / f_ref; chunks are 1-D Lloyd k-means over the rig positions (quantile
+initialisation), radii to the nearest other centre, radius-offset distance
+bands (src/chunks.py:101-135).  Visibility filtering is off (documented in
+DESIGN.md).  Inputs for both bench arms; not part of the render path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import time
+from dataclasses import dataclass, field
+from types import SimpleNamespace
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "libsynth.so")
+_lib = None
+
+CONFIGS = {
+    # name: n_fine, length, sh_degree, thresholds, keep fractions, K, rig views
+    "street1080": dict(n_fine=42000, length=200.0, degree=1, d=(10.0,), keep=(0.31,), K=4,
+                       views=64),
+    "config2": dict(n_fine=994_380, length=200.0, degree=3, d=(10.0, 28.0), keep=(0.31, 0.13),
+                    K=16, views=64),
+    "config3": dict(n_fine=19_994_380, length=2000.0, degree=3, d=(10.0, 28.0, 47.0, 63.0),
+                    keep=(0.31, 0.13, 0.076, 0.049), K=64, views=256),
+}
+WIDTH, HEIGHT, FOCAL = 1920, 1080, 1560.0
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB):
+            subprocess.run(["make", "-s", "-C", _HERE], check=True)
+        L = C.CDLL(_LIB)
+        P = C.c_void_p
+        L.synth_count.argtypes = [C.c_int64]
+        L.synth_count.restype = C.c_int64
+        L.synth_street.argtypes = [C.c_uint64, C.c_int64, C.c_double, C.c_int32, P, P]
+        L.synth_prune_key.argtypes = [P, C.c_int64, P]
+        L.synth_gather_level.argtypes = [P, P, C.c_int32, P, C.c_int64, C.c_float, P, P]
+        L.synth_bands.argtypes = [P, C.c_int64, P, C.c_int32, P, P, P, P, P]
+        L.synth_threads.restype = C.c_int32
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def camera(z: float, width=WIDTH, height=HEIGHT, focal=FOCAL, x=0.0, y=0.5):
+    """Identity-orientation trajectory camera (pkg/scripts/make_deep_street.py:34-36)."""
+    return SimpleNamespace(position=np.array([x, y, z], np.float64),
+                           orientation=np.array([1.0, 0.0, 0.0, 0.0]),
+                           rotation_matrix=np.eye(3), focal=np.array([focal, focal]),
+                           principal_point=np.array([width / 2, height / 2]),
+                           resolution=(width, height), near_plane=0.05)
+
+
+def kmeans_1d(positions: np.ndarray, k: int, iters: int = 50):
+    """Lloyd iterations from quantile seeds (deterministic)."""
+    pts = np.asarray(positions, np.float64)
+    seeds = np.round(np.linspace(0, len(pts) - 1, k)).astype(np.int64)
+    centers = pts[seeds].copy()
+    assign = None
+    for _ in range(iters):
+        d = np.linalg.norm(pts[:, None, :] - centers[None, :, :], axis=2)
+        new = np.argmin(d, axis=1)
+        if assign is not None and np.array_equal(new, assign):
+            break
+        assign = new
+        for j in range(k):
+            m = pts[assign == j]
+            if len(m):
+                centers[j] = m.mean(axis=0)
+    return centers, assign
+
+
+def chunk_radii(centers):
+    d = np.linalg.norm(centers[:, None, :] - centers[None, :, :], axis=2)
+    np.fill_diagonal(d, np.inf)
+    return d.min(axis=1)
+
+
+@dataclass
+class Config:
+    name: str
+    levels: list           # [(geom, sh, depth_threshold)]
+    degree: int
+    centers: np.ndarray
+    radii: np.ndarray
+    offsets: np.ndarray    # (K*L+1,) int64
+    data: np.ndarray       # uint32
+    rig_z: np.ndarray
+    length: float
+    timings: dict = field(default_factory=dict)
+
+    @property
+    def K(self):
+        return self.centers.shape[0]
+
+    @property
+    def L(self):
+        return len(self.levels)
+
+    def set(self, j, l):
+        return self.data[self.offsets[j * self.L + l]:self.offsets[j * self.L + l + 1]]
+
+    def sweep(self, n: int):
+        """Config 5 path: z from 4 to 0.65*length, identity orientation."""
+        return [camera(float(z)) for z in np.linspace(4.0, 0.65 * self.length, n)]
+
+    def rig_camera(self, i: int):
+        return camera(float(self.rig_z[i]))
+
+    def n_gaussians(self):
+        return [len(g) for g, _, _ in self.levels]
+
+    def store_bytes(self):
+        return sum(g.nbytes + s.nbytes for g, s, _ in self.levels)
+
+
+def build(name: str, seed: int = 7, verbose: bool = False) -> Config:
+    spec = CONFIGS[name]
+    L = lib()
+    t0 = time.time()
+    deg = spec["degree"]
+    terms = (deg + 1) ** 2
+    n = int(L.synth_count(spec["n_fine"]))
+    geom = np.empty((n, 12), np.float32)
+    sh = np.empty((n, 3, terms), np.float32)
+    L.synth_street(seed, spec["n_fine"], spec["length"], deg, _p(geom), _p(sh))
+    t1 = time.time()
+    levels = [(geom, sh, 0.0)]
+    if spec["d"]:
+        key = np.empty(n, np.float32)
+        L.synth_prune_key(_p(geom), n, _p(key))
+        order = np.argsort(-key, kind="stable")
+        for d, keep in zip(spec["d"], spec["keep"]):
+            idx = np.sort(order[:int(round(keep * n))]).astype(np.int64)
+            g = np.empty((len(idx), 12), np.float32)
+            s = np.empty((len(idx), 3, terms), np.float32)
+            L.synth_gather_level(_p(geom), _p(sh), terms, _p(idx), len(idx), float(d / FOCAL),
+                                 _p(g), _p(s))
+            levels.append((g, s, float(d)))
+    t2 = time.time()
+    rig_z = np.linspace(2.0, 0.7 * spec["length"], spec["views"])
+    positions = np.stack([np.zeros_like(rig_z), np.full_like(rig_z, 0.5), rig_z], axis=1)
+    centers, _ = kmeans_1d(positions, spec["K"])
+    radii = chunk_radii(centers) if spec["K"] > 1 else np.array([1.0])
+    K, nl = spec["K"], len(levels)
+    ds = [0.0] + list(spec["d"])
+    counts = np.zeros((nl, K), np.int64)
+    per_level = []
+    for l, (g, _, _) in enumerate(levels):
+        lo = np.array([0.0 if l == 0 else ds[l] + radii[j] for j in range(K)])
+        hi = np.array([np.inf if l + 1 == nl else ds[l + 1] + radii[j] for j in range(K)])
+        c = np.zeros(K, np.int64)
+        L.synth_bands(_p(g), len(g), _p(centers), K, _p(lo), _p(hi), _p(c), None, None)
+        offs = np.zeros(K + 1, np.int64)
+        offs[1:] = np.cumsum(c)
+        out = np.empty(int(offs[-1]), np.uint32)
+        L.synth_bands(_p(g), len(g), _p(centers), K, _p(lo), _p(hi), None, _p(offs), _p(out))
+        counts[l] = c
+        per_level.append((offs, out))
+    sizes = counts.T.reshape(-1)  # (j, l) order
+    offsets = np.zeros(K * nl + 1, np.int64)
+    offsets[1:] = np.cumsum(sizes)
+    data = np.empty(int(offsets[-1]), np.uint32)
+    for j in range(K):
+        for l in range(nl):
+            o, arr = per_level[l]
+            data[offsets[j * nl + l]:offsets[j * nl + l + 1]] = arr[o[j]:o[j + 1]]
+    t3 = time.time()
+    cfg = Config(name, levels, deg, centers, radii, offsets, data, rig_z, spec["length"],
+                 {"scene_s": t1 - t0, "levels_s": t2 - t1, "chunks_s": t3 - t2,
+                  "threads": int(L.synth_threads())})
+    if verbose:
+        print(f"[fixtures] {name}: levels {cfg.n_gaussians()} sets {len(data)} "
+              f"({cfg.timings})", flush=True)
+    return cfg
+
+
+def scene_objects(cfg: Config, l: int):
+    """fp64 Scene-like view of level l (for the oracle / drop-in API)."""
+    g, s, _ = cfg.levels[l]
+    g64 = g.astype(np.float64)
+    return SimpleNamespace(means=g64[:, 0:3], scales=g64[:, 3:6], rotations=g64[:, 6:10],
+                           opacities=g64[:, 10], filter_variance=g64[:, 11],
+                           sh_coeffs=s.astype(np.float64), sh_degree=cfg.degree)

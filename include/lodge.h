@@ -195,6 +195,20 @@ int lodge_frame_lists(lodge_ctx *ctx, int32_t T, int64_t *tile_offsets_dev,
 int lodge_frame_union(lodge_ctx *ctx, int32_t level, uint32_t *idx_dev, uint8_t *tag_dev,
                       int64_t cap);
 
+/* Stage profiling: when enabled, lodge_render_frame records CUDA events on
+ * the context stream at the boundaries of its LODGE_N_STAGES stages (select,
+ * union, project, depth sort, tile setup, duplicate, tile sort, composite)
+ * for up to `max_frames` frames.  lodge_profile_read synchronises those
+ * events and returns the summed milliseconds per stage and the frame count,
+ * then clears the record. */
+#define LODGE_N_STAGES 8
+int lodge_profile(lodge_ctx *ctx, int32_t enable, int32_t max_frames);
+int lodge_profile_read(lodge_ctx *ctx, double *stage_ms, int32_t *frames);
+
+/* Linear [0,1] RGB (fp32, n pixels) -> 8-bit sRGB, round(srgb(x) * 255)
+ * (reference src/images.py:10-17).  Async. */
+int lodge_to_srgb8(lodge_ctx *ctx, const float *image_dev, int64_t n_pixels, uint8_t *out_dev);
+
 /* Number of kernels the last lodge_render_frame enqueued. */
 int32_t lodge_last_launch_count(lodge_ctx *ctx);
 

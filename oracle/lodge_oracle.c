@@ -451,3 +451,70 @@ int32_t orc_num_threads(void) {
   return 1;
 #endif
 }
+
+/* ---------------------------------------------------------------------- */
+/* project_scene over fp32 AoS storage (the asset record layout,           */
+/* src/assets.py:240-254: [mean3, scale3, rot4, opacity, fv] + sh), values  */
+/* widened to fp64 exactly as the device's fp32 store does.  Parallel over  */
+/* contiguous input chunks (each restated by orc_project), concatenated in  */
+/* input order, so the result is independent of the thread count.          */
+/* ---------------------------------------------------------------------- */
+int64_t orc_project_f32(const float *geom, const float *sh, int32_t degree, const int64_t *idx,
+                        int64_t n, const double *mod, const orc_camera *cam,
+                        const orc_raster_cfg *cfg, int32_t shade, int64_t *src, double *mean2d,
+                        double *cov2d_out, double *conic, double *extent, double *depth,
+                        double *opacity, double *color, int32_t *rect) {
+  const int terms = (degree + 1) * (degree + 1);
+  const int64_t chunk = 8192;
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  int64_t *mc = (int64_t *)calloc((size_t)(nchunks > 0 ? nchunks : 1), sizeof(int64_t));
+  if (!mc) return -1;
+  int failed = 0;
+  /* pass 1: survivors per chunk (outputs staged in place, compacted later) */
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t b = c * chunk, k = (b + chunk < n ? chunk : n - b);
+    double *buf = (double *)malloc(sizeof(double) * (size_t)k * (12 + 3 * terms));
+    int64_t *lidx = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+    if (!buf || !lidx) { failed = 1; free(buf); free(lidx); continue; }
+    double *mu = buf, *sc = mu + 3 * k, *ro = sc + 3 * k, *op = ro + 4 * k, *fv = op + k,
+           *shd = fv + k;
+    for (int64_t i = 0; i < k; ++i) {
+      const float *g = geom + 12 * idx[b + i];
+      for (int d = 0; d < 3; ++d) { mu[3 * i + d] = g[d]; sc[3 * i + d] = g[3 + d]; }
+      for (int d = 0; d < 4; ++d) ro[4 * i + d] = g[6 + d];
+      op[i] = g[10];
+      fv[i] = g[11];
+      const float *s = sh + (int64_t)3 * terms * idx[b + i];
+      for (int d = 0; d < 3 * terms; ++d) shd[(int64_t)3 * terms * i + d] = s[d];
+      lidx[i] = i;
+    }
+    mc[c] = orc_project(mu, sc, ro, op, fv, shd, degree, lidx, k, mod ? mod + b : NULL, cam, cfg,
+                        shade, src + b, mean2d + 2 * b, cov2d_out ? cov2d_out + 4 * b : NULL,
+                        conic + 3 * b, extent + 2 * b, depth + b, opacity + b, color + 3 * b,
+                        rect ? rect + 4 * b : NULL);
+    for (int64_t i = 0; i < mc[c]; ++i) src[b + i] += b;
+    free(buf);
+    free(lidx);
+  }
+  if (failed) { free(mc); return -1; }
+  /* pass 2: compact the chunks in input order */
+  int64_t m = 0;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t b = c * chunk, k = mc[c];
+    if (m != b && k > 0) {
+      memmove(src + m, src + b, sizeof(int64_t) * k);
+      memmove(mean2d + 2 * m, mean2d + 2 * b, sizeof(double) * 2 * k);
+      if (cov2d_out) memmove(cov2d_out + 4 * m, cov2d_out + 4 * b, sizeof(double) * 4 * k);
+      memmove(conic + 3 * m, conic + 3 * b, sizeof(double) * 3 * k);
+      memmove(extent + 2 * m, extent + 2 * b, sizeof(double) * 2 * k);
+      memmove(depth + m, depth + b, sizeof(double) * k);
+      memmove(opacity + m, opacity + b, sizeof(double) * k);
+      memmove(color + 3 * m, color + 3 * b, sizeof(double) * 3 * k);
+      if (rect) memmove(rect + 4 * m, rect + 4 * b, sizeof(int32_t) * 4 * k);
+    }
+    m += k;
+  }
+  free(mc);
+  return m;
+}

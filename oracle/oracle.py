@@ -64,6 +64,10 @@ def lib():
                                     C.c_int32, _D, _I64, _I64, _D, _I64, _I64, C.c_int64]
         L.orc_rasterize.restype = C.c_int64
         L.orc_num_threads.restype = C.c_int32
+        L.orc_project_f32.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, _I64, C.c_int64, _D,
+                                      C.POINTER(Camera), C.POINTER(RasterCfg), C.c_int32,
+                                      _I64, _D, _D, _D, _D, _D, _D, _D, _I32]
+        L.orc_project_f32.restype = C.c_int64
         _lib = L
     return _lib
 
@@ -150,6 +154,32 @@ def project(scene, indices, camera: Camera, cfg: RasterCfg, modulation=None, sha
                           _p(out["conic"], _D), _p(out["extent"], _D), _p(out["depth"], _D),
                           _p(out["opacity"], _D), _p(out["color"], _D), _p(out["rect"], _I32))
     res = {k: v[:m].copy() for k, v in out.items()}
+    res["n_inputs"] = n
+    return res
+
+
+def project_f32(geom, sh, degree, indices, camera: Camera, cfg: RasterCfg, modulation=None,
+                shade=True):
+    """project_scene over fp32 AoS records (N,12) + SH (N,3,terms), widened to
+    fp64 (the device's fp32 store); OpenMP over input chunks, order kept."""
+    geom = np.ascontiguousarray(geom, np.float32)
+    sh = np.ascontiguousarray(sh, np.float32)
+    idx = np.ascontiguousarray(indices, np.int64)
+    n = idx.shape[0]
+    mod = None if modulation is None else np.ascontiguousarray(modulation, np.float64)
+    out = {"src": np.empty(n, np.int64), "mean2d": np.empty((n, 2)), "cov2d": np.empty((n, 2, 2)),
+           "conic": np.empty((n, 3)), "extent": np.empty((n, 2)), "depth": np.empty(n),
+           "opacity": np.empty(n), "color": np.empty((n, 3)), "rect": np.empty((n, 4), np.int32)}
+    m = lib().orc_project_f32(C.c_void_p(geom.ctypes.data), C.c_void_p(sh.ctypes.data),
+                              int(degree), _p(idx, _I64), n, _p(mod, _D), C.byref(camera),
+                              C.byref(cfg), int(bool(shade)), _p(out["src"], _I64),
+                              _p(out["mean2d"], _D), _p(out["cov2d"], _D), _p(out["conic"], _D),
+                              _p(out["extent"], _D), _p(out["depth"], _D),
+                              _p(out["opacity"], _D), _p(out["color"], _D),
+                              _p(out["rect"], _I32))
+    if m < 0:
+        raise MemoryError("oracle project_f32: allocation failed")
+    res = {k: v[:m] for k, v in out.items()}
     res["n_inputs"] = n
     return res
 

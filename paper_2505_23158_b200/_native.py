@@ -96,8 +96,14 @@ EXPORTS = {
                             C.POINTER(FrameOut), C.c_void_p], C.c_int),
     "lodge_frame_lists": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
     "lodge_frame_union": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
+    "lodge_profile": ([C.c_void_p, C.c_int32, C.c_int32], C.c_int),
+    "lodge_profile_read": ([C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int32)], C.c_int),
+    "lodge_to_srgb8": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p], C.c_int),
     "lodge_last_launch_count": ([C.c_void_p], C.c_int32),
 }
+N_STAGES = 8
+STAGES = ("select", "union", "project", "depth_sort", "tile_setup", "duplicate", "tile_sort",
+          "composite")
 
 _lib = None
 _lock = threading.Lock()

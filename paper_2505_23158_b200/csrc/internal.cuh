@@ -42,7 +42,7 @@ struct __align__(16) Payload {
   float r, g, b;        // colour
   uint32_t src;         // concatenated input index
   float q_eff, tol;
-  uint32_t pad0, pad1;
+  float bx, by;         // half-widths of a box containing every pixel that can be non-skipped
 };
 static_assert(sizeof(Payload) == 64, "payload must be 64 B");
 
@@ -61,6 +61,10 @@ struct Work {
   Payload *payload;         // M_cap
   Precise *precise;         // M_cap
   uint64_t *pairs[2];       // P_cap each
+  uint64_t *rect_sorted;    // M_cap: rectangles in depth order
+  uint32_t *splat_off;      // M_cap + 1: pair offset of each depth-ordered splat
+  uint32_t *chunk_first;    // P_cap / EMIT_CHUNK + 2: owner of each emission chunk
+  uint32_t *tile_order;     // T: tiles, heaviest first (composite schedule)
   int32_t *tile_diff;       // (tiles_x+1)*(tiles_y+1) 2-D difference array
   uint32_t *tile_start;     // T+1
   uint64_t *status;         // look-back status words (epoch | flags | value)

@@ -16,11 +16,12 @@ namespace lodge {
 // re-zeroes diff for the next frame.
 __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t tiles_x,
                                                      int32_t tiles_y, int32_t *tile_count,
-                                                     uint32_t *tile_start, FrameState *fs,
-                                                     int64_t P_cap) {
+                                                     uint32_t *tile_start, uint32_t *tile_order,
+                                                     FrameState *fs, int64_t P_cap) {
   extern __shared__ int32_t sd[];  // (tx+1)*(ty+1)
   __shared__ uint32_t h0[256], h1[256];
   __shared__ uint32_t s_sum[1024];
+  __shared__ uint32_t s_bk[33];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int stride = tiles_x + 1;
   const int nd = stride * (tiles_y + 1);
@@ -71,12 +72,36 @@ __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t tile
     tile_start[t] = run;
     run += (uint32_t)sd[(t / tiles_x) * stride + (t % tiles_x)];
   }
+  // composite schedule: tiles by descending log2(count) so the longest lists
+  // start first (order affects scheduling only, never results)
+  if (tid < 33) s_bk[tid] = 0;
+  __syncthreads();
+  for (int t = b; t < e; ++t) {
+    const uint32_t c = (uint32_t)sd[(t / tiles_x) * stride + (t % tiles_x)];
+    atomicAdd(&s_bk[c ? 32 - __clz(c) : 0], 1u);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t acc = 0;
+    for (int k = 32; k >= 0; --k) {
+      const uint32_t v = s_bk[k];
+      s_bk[k] = acc;
+      acc += v;
+    }
+  }
+  __syncthreads();
+  for (int t = b; t < e; ++t) {
+    const uint32_t c = (uint32_t)sd[(t / tiles_x) * stride + (t % tiles_x)];
+    tile_order[atomicAdd(&s_bk[c ? 32 - __clz(c) : 0], 1u)] = (uint32_t)t;
+  }
   if (tid == nt - 1) {
     const uint32_t P = s_sum[nt - 1];
     tile_start[T] = P;
     fs->stats.P = P;
     fs->stats.overflow = (int64_t)P > P_cap ? 1u : 0u;
-    fs->n_pairs = (int64_t)P < P_cap ? P : (uint32_t)P_cap;
+    // on overflow nothing is duplicated or sorted (the digit offsets assume
+    // all P pairs); the host grows the buffers and renders the frame again
+    fs->n_pairs = (int64_t)P <= P_cap ? P : 0u;
   }
   __syncthreads();
   if (tid < 32) {  // digit offsets for the two onesweep passes over tile ids
@@ -98,23 +123,23 @@ __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t tile
 }
 
 constexpr int DUP_THREADS = 256;
+constexpr int EMIT_ITEMS = 8;
+constexpr int EMIT_CHUNK = DUP_THREADS * EMIT_ITEMS;  // pairs per emission CTA
 
-// One thread per depth-sorted splat for counting; block-cooperative emission.
-__global__ void __launch_bounds__(DUP_THREADS) k_duplicate(const uint32_t *__restrict__ order,
+// Pass 1, one thread per depth-sorted splat: tile count, exclusive scan of
+// the counts in depth order (single-pass look-back), the splat's rectangle
+// and id in depth order, and for every EMIT_CHUNK boundary inside the
+// splat's pair range the splat that owns it (the emission CTAs' splitters).
+__global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__restrict__ order,
                                                            const uint64_t *__restrict__ rect,
-                                                           int32_t tiles_x, uint64_t *pairs,
-                                                           int64_t P_cap, uint64_t *status,
-                                                           FrameState *fs) {
-  __shared__ uint32_t s_off[DUP_THREADS + 1];
-  __shared__ uint32_t s_m[DUP_THREADS];
-  __shared__ uint64_t s_rect[DUP_THREADS];
+                                                           Work w, FrameState *fs) {
   __shared__ uint32_t s_w[DUP_THREADS / 32];
   __shared__ uint32_t s_part, s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_part = atomicAdd(&fs->tickets[TK_DUP], 1u);
   __syncthreads();
   const uint32_t part = s_part;
-  const uint32_t M = fs->stats.M;
+  const uint32_t M = fs->stats.overflow ? 0u : fs->stats.M;
   const uint32_t r = part * DUP_THREADS + tid;
   if (part * DUP_THREADS >= M) return;
   uint32_t cnt = 0;
@@ -124,10 +149,8 @@ __global__ void __launch_bounds__(DUP_THREADS) k_duplicate(const uint32_t *__res
     const uint32_t x0 = rc & 0xffff, x1 = (rc >> 16) & 0xffff, y0 = (rc >> 32) & 0xffff,
                    y1 = rc >> 48;
     cnt = (x1 - x0 + 1) * (y1 - y0 + 1);
-    s_m[tid] = m;
-    s_rect[tid] = rc;
+    w.rect_sorted[r] = rc;
   }
-  // block exclusive scan of counts
   uint32_t inc = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -137,7 +160,7 @@ __global__ void __launch_bounds__(DUP_THREADS) k_duplicate(const uint32_t *__res
   if (lane == 31) s_w[warp] = inc;
   __syncthreads();
   if (warp == 0) {
-    uint32_t wv = lane < DUP_THREADS / 32 ? s_w[lane] : 0u;
+    const uint32_t wv = lane < DUP_THREADS / 32 ? s_w[lane] : 0u;
     uint32_t winc = wv;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -146,33 +169,59 @@ __global__ void __launch_bounds__(DUP_THREADS) k_duplicate(const uint32_t *__res
     }
     const uint32_t total = __shfl_sync(FULL_MASK, winc, 31);
     if (lane < DUP_THREADS / 32) s_w[lane] = winc - wv;
-    const uint32_t pre = lookback_warp(status, part, total, fs->epoch + TK_DUP);
-    if (lane == 0) {
-      s_base = pre;
-      s_off[DUP_THREADS] = total;
-    }
+    const uint32_t pre = lookback_warp(w.status, part, total, fs->epoch + TK_DUP);
+    if (lane == 0) s_base = pre;
   }
   __syncthreads();
-  s_off[tid] = s_w[warp] + inc - cnt;
+  if (r >= M) return;
+  const uint32_t off = s_base + s_w[warp] + inc - cnt;
+  w.splat_off[r] = off;
+  if (r == M - 1) w.splat_off[M] = off + cnt;
+  for (uint32_t c = (off + EMIT_CHUNK - 1) / EMIT_CHUNK; c * EMIT_CHUNK < off + cnt; ++c)
+    w.chunk_first[c] = r;
+}
+
+// Pass 2, EMIT_CHUNK pairs per CTA regardless of splat sizes: the owners of
+// the chunk's pairs are a contiguous depth-order range [chunk_first[c],
+// chunk_first[c+1]] staged in shared memory; each pair finds its owner by a
+// binary search there and writes (tile << 32 | splat) coalesced.
+__global__ void __launch_bounds__(DUP_THREADS) k_dup_emit(const uint32_t *__restrict__ order,
+                                                          int32_t tiles_x, Work w,
+                                                          FrameState *fs) {
+  __shared__ uint32_t s_off[EMIT_CHUNK + 2];
+  __shared__ uint64_t s_rect[EMIT_CHUNK + 1];
+  __shared__ uint32_t s_m[EMIT_CHUNK + 1];
+  const uint32_t P = fs->n_pairs;
+  const uint32_t M = fs->stats.M;
+  const uint32_t c = blockIdx.x;
+  const uint32_t j0 = c * EMIT_CHUNK;
+  if (j0 >= P) return;
+  const uint32_t j1 = min(j0 + (uint32_t)EMIT_CHUNK, P);
+  const uint32_t r0 = w.chunk_first[c];
+  const uint32_t r1 = (j1 < P) ? w.chunk_first[c + 1] : M - 1;
+  const uint32_t nr = r1 - r0 + 1;
+  for (uint32_t k = threadIdx.x; k < nr; k += DUP_THREADS) {
+    s_off[k] = w.splat_off[r0 + k];
+    s_rect[k] = w.rect_sorted[r0 + k];
+    s_m[k] = order[r0 + k];
+  }
   __syncthreads();
-  const uint32_t total = s_off[DUP_THREADS];
-  const uint64_t base = s_base;
-  for (uint32_t j = tid; j < total; j += DUP_THREADS) {
-    // owner: last s with s_off[s] <= j
-    int lo = 0, hi = DUP_THREADS - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
+#pragma unroll
+  for (int it = 0; it < EMIT_ITEMS; ++it) {
+    const uint32_t j = j0 + it * DUP_THREADS + threadIdx.x;
+    if (j >= j1) break;
+    uint32_t lo = 0, hi = nr - 1;
+    while (lo < hi) {  // last k with s_off[k] <= j
+      const uint32_t mid = (lo + hi + 1) >> 1;
       if (s_off[mid] <= j) lo = mid;
       else hi = mid - 1;
     }
     const uint64_t rc = s_rect[lo];
     const uint32_t x0 = rc & 0xffff, x1 = (rc >> 16) & 0xffff, y0 = (rc >> 32) & 0xffff;
-    const uint32_t w = x1 - x0 + 1;
+    const uint32_t wdt = x1 - x0 + 1;
     const uint32_t local = j - s_off[lo];
-    const uint32_t ty = y0 + local / w, tx = x0 + local % w;
-    const uint64_t dst = base + j;
-    if ((int64_t)dst < P_cap)
-      pairs[dst] = ((uint64_t)(ty * (uint32_t)tiles_x + tx) << 32) | s_m[lo];
+    const uint32_t ty = y0 + local / wdt, tx = x0 + local % wdt;
+    w.pairs[0][j] = ((uint64_t)(ty * (uint32_t)tiles_x + tx) << 32) | s_m[lo];
   }
 }
 
@@ -184,16 +233,17 @@ void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32
     cudaFuncSetAttribute(k_tile_setup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = sm;
   }
-  k_tile_setup<<<1, 1024, sm, s>>>(w.tile_diff, tiles_x, tiles_y, tile_count, w.tile_start, fs,
-                                   w.P_cap);
+  k_tile_setup<<<1, 1024, sm, s>>>(w.tile_diff, tiles_x, tiles_y, tile_count, w.tile_start,
+                                   w.tile_order, fs, w.P_cap);
 }
 
 void launch_duplicate(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_cap,
                       cudaStream_t s) {
   if (M_cap <= 0) return;
   const unsigned grid = (unsigned)((M_cap + DUP_THREADS - 1) / DUP_THREADS);
-  k_duplicate<<<grid, DUP_THREADS, 0, s>>>(w.val_depth[0], w.rect, tiles_x, w.pairs[0], w.P_cap,
-                                           w.status, fs);
+  k_dup_count<<<grid, DUP_THREADS, 0, s>>>(w.val_depth[0], w.rect, w, fs);
+  const unsigned egrid = (unsigned)((w.P_cap + EMIT_CHUNK - 1) / EMIT_CHUNK);
+  k_dup_emit<<<egrid, DUP_THREADS, 0, s>>>(w.val_depth[0], tiles_x, w, fs);
 }
 
 }  // namespace lodge

@@ -215,6 +215,7 @@ __device__ __forceinline__ void eval_sh_dev(const ST *__restrict__ k, int terms,
 // on q; tol bounds |q_fp32 - q_fp64| near that cut-off.
 __device__ __forceinline__ void make_payload(double mx, double my, double A, double B, double C,
                                              double o, const double rgb[3], uint32_t src,
+                                             double ex, double ey,
                                              const lodge_raster_params &rp, Payload &pl,
                                              Precise &pr) {
   pl.mx = mx;
@@ -244,7 +245,13 @@ __device__ __forceinline__ void make_payload(double mx, double my, double A, dou
   }
   pl.q_eff = (float)q_eff;
   pl.tol = (float)tol;
-  pl.pad0 = pl.pad1 = 0;
+  // {q <= Q} lies in |dx| <= sqrt(Q/9) * ex, |dy| <= sqrt(Q/9) * ey (ex = 3 sqrt(cov00));
+  // Q = q_eff + tol bounds every pixel the fp64 reference may keep.  Generous
+  // relative/absolute margins cover the rounding of cov2d and of the bounds.
+  const double Q = fmin(fmax(q_eff, 0.0) + tol, LODGE_SUPPORT_Q * 1.001);
+  const double sc = (q_eff > -INFINITY) ? sqrt(Q / 9.0) * 1.0001 : 0.0;
+  pl.bx = (q_eff > -INFINITY) ? (float)(sc * ex + 1e-3) : -1.0f;
+  pl.by = (q_eff > -INFINITY) ? (float)(sc * ey + 1e-3) : -1.0f;
   pr.A = A;
   pr.B = B;
   pr.C = C;
@@ -333,7 +340,7 @@ __global__ void __launch_bounds__(256) k_project_frame(ProjLevels lv, Work w, Fr
   const double A = p.c11 * inv_det, B = (-p.c01) * inv_det, C = p.c00 * inv_det;
   Payload pl;
   Precise pr;
-  make_payload(p.mx, p.my, A, B, C, p.op, rgb, cat_off + pos, rp, pl, pr);
+  make_payload(p.mx, p.my, A, B, C, p.op, rgb, cat_off + pos, p.ex, p.ey, rp, pl, pr);
   w.payload[m] = pl;
   w.precise[m] = pr;
   const int32_t tiles_x = (cam.w + 15) / 16, tiles_y = (cam.h + 15) / 16;
@@ -412,7 +419,8 @@ __global__ void __launch_bounds__(256) k_import_batch(lodge_batch b, int64_t M, 
   Payload pl;
   Precise pr;
   make_payload(mx, my, b.conic_dev[3 * m], b.conic_dev[3 * m + 1], b.conic_dev[3 * m + 2],
-               b.opacity_dev[m], rgb, (uint32_t)b.src_dev[m], rp, pl, pr);
+               b.opacity_dev[m], rgb, (uint32_t)b.src_dev[m], b.extent_dev[2 * m],
+               b.extent_dev[2 * m + 1], rp, pl, pr);
   w.payload[m] = pl;
   w.precise[m] = pr;
   const int32_t tiles_x = (cam.w + 15) / 16, tiles_y = (cam.h + 15) / 16;

@@ -37,6 +37,14 @@ struct lodge_ctx {
   int64_t tiles_cap = 0;  // capacity of tile_start (T+1) and diff
   int32_t launches = 0;
   LevelSlots last_slots{};  // slot layout of the last union
+  // stage profiling
+  bool prof = false;
+  int32_t prof_cap = 0, prof_frames = 0;
+  cudaEvent_t *prof_ev = nullptr;  // prof_cap * (LODGE_N_STAGES + 1)
+  void mark(int k) {
+    if (prof && prof_frames < prof_cap)
+      cudaEventRecord(prof_ev[prof_frames * (LODGE_N_STAGES + 1) + k], stream);
+  }
 };
 
 static int ensure_M(lodge_ctx *c, int64_t need) {
@@ -46,7 +54,10 @@ static int ensure_M(lodge_ctx *c, int64_t need) {
   cudaFree(w.key_depth[0]); cudaFree(w.key_depth[1]);
   cudaFree(w.val_depth[0]); cudaFree(w.val_depth[1]);
   cudaFree(w.rect); cudaFree(w.payload); cudaFree(w.precise);
+  cudaFree(w.rect_sorted); cudaFree(w.splat_off);
   w.M_cap = 0;
+  CK(cudaMalloc(&w.rect_sorted, 8 * ncap));
+  CK(cudaMalloc(&w.splat_off, 4 * (ncap + 1)));
   CK(cudaMalloc(&w.key_depth[0], 8 * ncap));
   CK(cudaMalloc(&w.key_depth[1], 8 * ncap));
   CK(cudaMalloc(&w.val_depth[0], 4 * ncap));
@@ -76,11 +87,12 @@ static int ensure_P(lodge_ctx *c, int64_t need) {
   Work &w = c->w;
   if (need <= w.P_cap && w.pairs[0]) return 0;
   int64_t ncap = std::max<int64_t>(std::max<int64_t>(need, w.P_cap + w.P_cap / 2), 1 << 16);
-  cudaFree(w.pairs[0]); cudaFree(w.pairs[1]);
+  cudaFree(w.pairs[0]); cudaFree(w.pairs[1]); cudaFree(w.chunk_first);
   w.pairs[0] = w.pairs[1] = nullptr;
   w.P_cap = 0;
   CK(cudaMalloc(&w.pairs[0], 8 * ncap));
   CK(cudaMalloc(&w.pairs[1], 8 * ncap));
+  CK(cudaMalloc(&w.chunk_first, 4 * (ncap / 2048 + 4)));
   w.P_cap = ncap;
   return ensure_status(c, (ncap + 4095) / 4096 * 256);
 }
@@ -89,11 +101,12 @@ static int ensure_tiles(lodge_ctx *c, int32_t W, int32_t H) {
   const int64_t tx = (W + 15) / 16, ty = (H + 15) / 16;
   const int64_t need = (tx + 1) * (ty + 1) + 1;
   if (need <= c->tiles_cap && c->w.tile_diff) return 0;
-  cudaFree(c->w.tile_diff); cudaFree(c->w.tile_start);
+  cudaFree(c->w.tile_diff); cudaFree(c->w.tile_start); cudaFree(c->w.tile_order);
   c->tiles_cap = 0;
   CK(cudaMalloc(&c->w.tile_diff, 4 * need));
   CK(cudaMemset(c->w.tile_diff, 0, 4 * need));
   CK(cudaMalloc(&c->w.tile_start, 4 * need));
+  CK(cudaMalloc(&c->w.tile_order, 4 * need));
   c->tiles_cap = need;
   return 0;
 }
@@ -162,7 +175,8 @@ void lodge_destroy(lodge_ctx *c) {
   Work &w = c->w;
   void *ptrs[] = {w.key_depth[0], w.key_depth[1], w.val_depth[0], w.val_depth[1], w.rect,
                   w.payload, w.precise, w.pairs[0], w.pairs[1], w.tile_diff, w.tile_start,
-                  w.status, w.union_idx, w.union_tag, c->fs, c->cam_dev};
+                  w.status, w.union_idx, w.union_tag, c->fs, c->cam_dev, w.rect_sorted,
+                  w.splat_off, w.chunk_first, w.tile_order};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c->cam_host) cudaFreeHost(c->cam_host);
@@ -368,21 +382,31 @@ int lodge_render_frame(lodge_ctx *c, const lodge_level *levels, int32_t n_levels
   const Work &w = c->w;
   c->last_slots = ls;
   int32_t nl = 0;
+  c->mark(0);
   launch_begin_frame(c->fs, s); ++nl;
   launch_select_frame(ch->centers_dev, ch->K, cam_dev, nullptr, nullptr, pair != nullptr, pf, po,
                       tv, c->fs, s); ++nl;
+  c->mark(1);
   launch_union(*ch, ls, c->fs, w.status, w.union_idx, w.union_tag, s); nl += 2;
+  c->mark(2);
   if ((flags & LODGE_RECORD_MAX) && out->maxw_dev)
     CK(cudaMemsetAsync(out->maxw_dev, 0, (exact ? 8 : 4) * (size_t)U_cap, s));
   rc = launch_project_frame(levels, ls, w, c->fs, cam_dev, *rp, (flags & LODGE_NEED_IMAGE) ? 1 : 0,
                             exact, s);
   if (rc) return set_err(LODGE_ERR_BAD_ARG, "all levels must share one storage precision");
   ++nl;
+  c->mark(3);
   launch_depth_sort(w, c->fs, U_cap, &nl, s);
+  c->mark(4);
   launch_tile_setup(w, c->fs, out->tile_count_dev, tiles_x, tiles_y, s); ++nl;
+  c->mark(5);
   launch_duplicate(w, c->fs, tiles_x, U_cap, s); ++nl;
+  c->mark(6);
   launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s);
+  c->mark(7);
   launch_composite(w, c->fs, cam_dev, W, H, *rp, flags, exact, *out, 0, s); ++nl;
+  c->mark(8);
+  if (c->prof && c->prof_frames < c->prof_cap) ++c->prof_frames;
   if (stats_dev)
     CK(cudaMemcpyAsync(stats_dev, &c->fs->stats, sizeof(lodge_frame_stats), cudaMemcpyDeviceToDevice, s));
   c->launches = nl;
@@ -408,6 +432,55 @@ int lodge_frame_union(lodge_ctx *c, int32_t level, uint32_t *idx, uint8_t *tag, 
                        cudaMemcpyDeviceToDevice, c->stream));
   }
   return 0;
+}
+
+int lodge_profile(lodge_ctx *c, int32_t enable, int32_t max_frames) {
+  if (!c) return set_err(LODGE_ERR_BAD_ARG, "ctx is NULL");
+  CK(cudaSetDevice(c->device));
+  if (enable && max_frames > c->prof_cap) {
+    if (c->prof_ev) {
+      for (int i = 0; i < c->prof_cap * (LODGE_N_STAGES + 1); ++i) cudaEventDestroy(c->prof_ev[i]);
+      delete[] c->prof_ev;
+    }
+    c->prof_ev = new cudaEvent_t[(size_t)max_frames * (LODGE_N_STAGES + 1)];
+    for (int i = 0; i < max_frames * (LODGE_N_STAGES + 1); ++i) CK(cudaEventCreate(&c->prof_ev[i]));
+    c->prof_cap = max_frames;
+  }
+  c->prof = enable != 0;
+  c->prof_frames = 0;
+  return 0;
+}
+
+int lodge_profile_read(lodge_ctx *c, double *stage_ms, int32_t *frames) {
+  if (!c || !stage_ms || !frames) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  for (int k = 0; k < LODGE_N_STAGES; ++k) stage_ms[k] = 0.0;
+  for (int f = 0; f < c->prof_frames; ++f) {
+    cudaEvent_t *e = c->prof_ev + f * (LODGE_N_STAGES + 1);
+    CK(cudaEventSynchronize(e[LODGE_N_STAGES]));
+    for (int k = 0; k < LODGE_N_STAGES; ++k) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e[k], e[k + 1]));
+      stage_ms[k] += ms;
+    }
+  }
+  *frames = c->prof_frames;
+  c->prof_frames = 0;
+  return 0;
+}
+
+__global__ void k_srgb8(const float *img, int64_t n, uint8_t *out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * n) return;
+  const double x = fmin(fmax((double)img[i], 0.0), 1.0);
+  const double e = x <= 0.0031308 ? 12.92 * x : 1.055 * pow(x, 1.0 / 2.4) - 0.055;
+  out[i] = (uint8_t)rint(e * 255.0);  // np.round: half to even
+}
+
+int lodge_to_srgb8(lodge_ctx *c, const float *img, int64_t n, uint8_t *out) {
+  if (!c || !img || !out) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  if (n <= 0) return 0;
+  k_srgb8<<<(unsigned)((3 * n + 255) / 256), 256, 0, c->stream>>>(img, n, out);
+  return check_launch("lodge_to_srgb8");
 }
 
 int32_t lodge_last_launch_count(lodge_ctx *c) { return c ? c->launches : 0; }

@@ -199,6 +199,27 @@ class DevicePlan:
         for l in range(L):
             self.struct.max_set[l] = int(self.max_set[l])
 
+    @classmethod
+    def from_arrays(cls, centers, offsets, data, L: int, device: torch.device):
+        """From flat arrays: centers (K,3) fp64, offsets (K*L+1) int64, data uint32
+        with set (j, l) = data[offsets[j*L+l]:offsets[j*L+l+1]] (sorted)."""
+        self = cls.__new__(cls)
+        centers = np.ascontiguousarray(centers, np.float64)
+        self.K, self.L = centers.shape[0], int(L)
+        self.centers = torch.from_numpy(centers).to(device)
+        self.offsets = torch.from_numpy(np.ascontiguousarray(offsets, np.int64)).to(device)
+        data = np.ascontiguousarray(data, np.uint32)
+        self.data = torch.from_numpy(data.view(np.int32)).to(device)
+        self.max_set = np.diff(np.asarray(offsets)).reshape(self.K, self.L).max(axis=0)
+        self.struct = N.Chunks()
+        self.struct.K, self.struct.L = self.K, self.L
+        self.struct.centers_dev = self.centers.data_ptr()
+        self.struct.offsets_dev = self.offsets.data_ptr()
+        self.struct.data_dev = self.data.data_ptr() if data.size else self.offsets.data_ptr()
+        for l in range(self.L):
+            self.struct.max_set[l] = int(self.max_set[l])
+        return self
+
     @property
     def union_capacity(self) -> int:
         return int(2 * self.max_set.sum())

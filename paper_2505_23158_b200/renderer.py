@@ -106,6 +106,14 @@ class Renderer:
             "lodge_render_frame")
         return frame
 
+    def to_srgb8(self, frame: Frame, out: torch.Tensor) -> torch.Tensor:
+        """8-bit sRGB of the frame's image on the device (src/images.py:10-17)."""
+        if frame.image is None or frame.image.dtype != torch.float32:
+            raise ValueError("to_srgb8 needs a FAST-precision frame with an image")
+        N.check(N.lib().lodge_to_srgb8(self.ctx.bind(self.precision), ptr(frame.image),
+                                       frame.width * frame.height, ptr(out)), "lodge_to_srgb8")
+        return out
+
     def last_launch_count(self) -> int:
         return int(N.lib().lodge_last_launch_count(self.ctx.ptr))
 
