@@ -17,7 +17,8 @@ namespace lodge {
 struct FrameState {
   lodge_frame_stats stats;            // f, o, t_bar, t, U, M, P, overflow ...
   uint32_t epoch;                     // look-back epoch base for this frame
-  uint32_t n_pairs;                   // min(P, P_cap): pairs actually stored
+  uint32_t n_pairs;                   // P, or 0 on overflow: pairs actually stored
+  uint32_t n_sort;                    // keys in the depth sort (U fused, M compat)
   uint32_t tickets[32];               // virtual block-id tickets, zeroed per frame
   uint32_t hist_depth[8][256];        // onesweep digit histograms (depth keys)
   uint32_t off_depth[8][256];         // their exclusive scans

@@ -274,14 +274,25 @@ __device__ __forceinline__ uint64_t tile_rect(double mx, double my, double ex, d
   return (uint64_t)x0 | ((uint64_t)x1 << 16) | ((uint64_t)y0 << 32) | ((uint64_t)y1 << 48);
 }
 
-__device__ __forceinline__ void add_tile_diff(int32_t *diff, uint64_t rc, int32_t tiles_x) {
+// Warp-aggregated atomic: lanes hitting the same counter combine first (the
+// corners of border-clipped splats are shared by many splats).  Called by
+// the whole warp; inactive lanes pass idx = -1.
+__device__ __forceinline__ void warp_add(int32_t *base, int32_t idx, int32_t v) {
+  const uint32_t peers = __match_any_sync(FULL_MASK, idx);
+  if (idx >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1)
+    atomicAdd(base + idx, v * __popc(peers));
+}
+
+// 2-D difference-array update for a tile rectangle (whole warp; valid flag).
+__device__ __forceinline__ void add_tile_diff(int32_t *diff, uint64_t rc, int32_t tiles_x,
+                                              bool valid) {
   const int32_t x0 = (int32_t)(rc & 0xffff), x1 = (int32_t)((rc >> 16) & 0xffff);
   const int32_t y0 = (int32_t)((rc >> 32) & 0xffff), y1 = (int32_t)(rc >> 48);
   const int32_t stride = tiles_x + 1;
-  atomicAdd(diff + y0 * stride + x0, 1);
-  atomicAdd(diff + y0 * stride + x1 + 1, -1);
-  atomicAdd(diff + (y1 + 1) * stride + x0, -1);
-  atomicAdd(diff + (y1 + 1) * stride + x1 + 1, 1);
+  warp_add(diff, valid ? y0 * stride + x0 : -1, 1);
+  warp_add(diff, valid ? y0 * stride + x1 + 1 : -1, -1);
+  warp_add(diff, valid ? (y1 + 1) * stride + x0 : -1, -1);
+  warp_add(diff, valid ? (y1 + 1) * stride + x1 + 1 : -1, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -296,23 +307,27 @@ struct ProjLevels {
   int32_t L;
 };
 
+// Outputs are written at the dense concatenated input index g (level-major
+// union position, the reference's Splat2DBatch.concat source index), with no
+// compaction: culled inputs get depth key ~0, so the stable depth sort over
+// all U inputs orders the M survivors by (depth, g) -- exactly
+// np.lexsort((source_index, depth)) -- and leaves the culled ones after them.
 template <typename GT, typename ST>
-__global__ void __launch_bounds__(256) k_project_frame(ProjLevels lv, Work w, FrameState *fs,
+__global__ void __launch_bounds__(256, 2) k_project_frame(ProjLevels lv, Work w, FrameState *fs,
                                                        const lodge_camera *__restrict__ cam_p,
                                                        lodge_raster_params rp, int32_t shade) {
-  __shared__ uint32_t s_warp[32];
-  __shared__ uint32_t s_base;
   __shared__ lodge_camera cam;
   if (threadIdx.x == 0) cam = *cam_p;
-  const uint32_t part = take_ticket(&fs->tickets[TK_COMPACT], &s_base);
-  const uint32_t slot = part * blockDim.x + threadIdx.x;
+  __syncthreads();
+  const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
   // map slot -> level
   int l = 0;
   while (l + 1 < lv.L && slot >= lv.slot_base[l + 1]) ++l;
   const uint32_t pos = slot - lv.slot_base[l];
-  bool valid = slot < lv.slot_base[lv.L] && pos < fs->stats.U_level[l];
+  const bool valid = slot < lv.slot_base[lv.L] && pos < fs->stats.U_level[l];
   uint32_t cat_off = 0;  // concatenated index offset of level l
   for (int k = 0; k < l; ++k) cat_off += fs->stats.U_level[k];
+  const uint32_t g = cat_off + pos;
   Proj p;
   p.ok = false;
   double v[12];
@@ -326,9 +341,18 @@ __global__ void __launch_bounds__(256) k_project_frame(ProjLevels lv, Work w, Fr
     p = project_core(v, cam, rp, mod, true);
   }
   const bool keep = valid && p.ok;
-  const uint32_t epoch = fs->epoch + TK_COMPACT;
-  const int64_t m = compact_slot(keep, w.status, epoch, part, s_warp, &s_base);
-  if (m < 0) return;
+  const uint32_t nkeep = __popc(__ballot_sync(FULL_MASK, keep));
+  if ((threadIdx.x & 31) == 0 && nkeep) atomicAdd(&fs->stats.M, nkeep);
+  const int32_t tiles_x = (cam.w + 15) / 16, tiles_y = (cam.h + 15) / 16;
+  const uint64_t rc = keep ? tile_rect(p.mx, p.my, p.ex, p.ey, tiles_x, tiles_y) : 0ull;
+  add_tile_diff(w.tile_diff, rc, tiles_x, keep);
+  if (!valid) return;
+  w.val_depth[0][g] = g;
+  if (!keep) {
+    w.key_depth[0][g] = ~0ull;
+    return;
+  }
+  const uint64_t m = g;
   double rgb[3] = {0.0, 0.0, 0.0};
   if (shade) {
     const int deg = lv.degree[l];
@@ -340,16 +364,11 @@ __global__ void __launch_bounds__(256) k_project_frame(ProjLevels lv, Work w, Fr
   const double A = p.c11 * inv_det, B = (-p.c01) * inv_det, C = p.c00 * inv_det;
   Payload pl;
   Precise pr;
-  make_payload(p.mx, p.my, A, B, C, p.op, rgb, cat_off + pos, p.ex, p.ey, rp, pl, pr);
+  make_payload(p.mx, p.my, A, B, C, p.op, rgb, g, p.ex, p.ey, rp, pl, pr);
   w.payload[m] = pl;
   w.precise[m] = pr;
-  const int32_t tiles_x = (cam.w + 15) / 16, tiles_y = (cam.h + 15) / 16;
-  const uint64_t rc = tile_rect(p.mx, p.my, p.ex, p.ey, tiles_x, tiles_y);
   w.rect[m] = rc;
-  add_tile_diff(w.tile_diff, rc, tiles_x);
   w.key_depth[0][m] = (uint64_t)__double_as_longlong(p.z);
-  w.val_depth[0][m] = (uint32_t)m;
-  atomicMax(&fs->stats.M, (uint32_t)(m + 1));
 }
 
 // ---------------------------------------------------------------------------
@@ -412,8 +431,15 @@ __global__ void __launch_bounds__(256) k_import_batch(lodge_batch b, int64_t M, 
                                                       const lodge_camera *__restrict__ cam_p,
                                                       lodge_raster_params rp) {
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= M) return;
   const lodge_camera &cam = *cam_p;
+  const int32_t tiles_x = (cam.w + 15) / 16, tiles_y = (cam.h + 15) / 16;
+  const bool valid = m < M;
+  const uint64_t rc = valid ? tile_rect(b.mean2d_dev[2 * m], b.mean2d_dev[2 * m + 1],
+                                        b.extent_dev[2 * m], b.extent_dev[2 * m + 1], tiles_x,
+                                        tiles_y)
+                            : 0ull;
+  add_tile_diff(w.tile_diff, rc, tiles_x, valid);
+  if (!valid) return;
   const double mx = b.mean2d_dev[2 * m], my = b.mean2d_dev[2 * m + 1];
   const double rgb[3] = {b.color_dev[3 * m], b.color_dev[3 * m + 1], b.color_dev[3 * m + 2]};
   Payload pl;
@@ -423,17 +449,16 @@ __global__ void __launch_bounds__(256) k_import_batch(lodge_batch b, int64_t M, 
                b.extent_dev[2 * m + 1], rp, pl, pr);
   w.payload[m] = pl;
   w.precise[m] = pr;
-  const int32_t tiles_x = (cam.w + 15) / 16, tiles_y = (cam.h + 15) / 16;
-  const uint64_t rc = tile_rect(mx, my, b.extent_dev[2 * m], b.extent_dev[2 * m + 1], tiles_x,
-                                tiles_y);
   w.rect[m] = rc;
-  add_tile_diff(w.tile_diff, rc, tiles_x);
   // lexsort((src, depth)): the depth sort is stable, so feed rows in
   // source-index order via the values; the batch's src order is ascending
   // for project_scene outputs, otherwise the host pre-sorts (see raster.py).
   w.key_depth[0][m] = (uint64_t)__double_as_longlong(b.depth_dev[m]);
   w.val_depth[0][m] = (uint32_t)m;
-  if (m == 0) fs->stats.M = (uint32_t)M;
+  if (m == 0) {
+    fs->stats.M = (uint32_t)M;
+    fs->n_sort = (uint32_t)M;
+  }
 }
 
 template <typename GT, typename ST>

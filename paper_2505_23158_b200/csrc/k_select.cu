@@ -177,6 +177,7 @@ __global__ void k_union_sizes(int32_t L, FrameState *fs) {
   uint32_t U = 0;
   for (int l = 0; l < L; ++l) U += fs->stats.U_level[l];
   fs->stats.U = U;
+  fs->n_sort = U;  // fused path: every input is a depth-sort key (culled -> ~0)
 }
 
 void launch_union(const lodge_chunks &ch, const LevelSlots &ls, FrameState *fs, uint64_t *status,

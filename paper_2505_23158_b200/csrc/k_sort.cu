@@ -20,11 +20,11 @@ constexpr int OS_WSTRIDE = 257;                 // per-warp digit counters (+1 p
 
 static size_t onesweep_smem(bool vals) {
   return (size_t)OS_TILE * 8 + (vals ? (size_t)OS_TILE * 4 : 0) +
-         (size_t)(8 * OS_WSTRIDE + 256 + 256 + 32) * 4;
+         (size_t)(8 * OS_WSTRIDE + 256 + 256 + 32) * 4 + (size_t)OS_TILE * 2;
 }
 
 template <bool VALS>
-__global__ void __launch_bounds__(OS_THREADS) k_onesweep(
+__global__ void __launch_bounds__(OS_THREADS, VALS ? 2 : 3) k_onesweep(
     const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
     const uint32_t *__restrict__ vin, uint32_t *__restrict__ vout, const uint32_t *n_ptr,
     int shift, const uint32_t *__restrict__ digit_off, uint64_t *status, FrameState *fs,
@@ -46,27 +46,28 @@ __global__ void __launch_bounds__(OS_THREADS) k_onesweep(
   const uint32_t base = part * OS_TILE;
   if (base >= n) return;
 
+  // keys live in registers; ranks go to shared memory and digits are
+  // recomputed from the keys, keeping the kernel at >= 2-3 CTAs per SM
+  uint16_t *s_rank = reinterpret_cast<uint16_t *>(s_misc + 32);
   uint64_t k[OS_ITEMS];
-  uint32_t v[OS_ITEMS];
-  uint32_t d[OS_ITEMS];
-  uint32_t r[OS_ITEMS];
+  uint32_t vmask = 0;
 #pragma unroll
   for (int i = 0; i < OS_ITEMS; ++i) {
     const uint32_t idx = base + warp * (OS_ITEMS * 32) + i * 32 + lane;
     const bool valid = idx < n;
+    vmask |= valid ? (1u << i) : 0u;
     k[i] = valid ? kin[idx] : ~0ull;
-    if (VALS) v[i] = valid ? vin[idx] : 0u;
-    d[i] = valid ? (uint32_t)((k[i] >> shift) & 255u) : 256u;
   }
   uint32_t *wh = s_whist + warp * OS_WSTRIDE;
 #pragma unroll
   for (int i = 0; i < OS_ITEMS; ++i) {
-    const uint32_t peers = __match_any_sync(FULL_MASK, d[i]);
-    const uint32_t cnt = wh[d[i]];
+    const uint32_t di = ((vmask >> i) & 1u) ? (uint32_t)((k[i] >> shift) & 255u) : 256u;
+    const uint32_t peers = __match_any_sync(FULL_MASK, di);
+    const uint32_t cnt = wh[di];
     __syncwarp();
-    if (lane == __ffs(peers) - 1) wh[d[i]] = cnt + __popc(peers);
+    if (lane == __ffs(peers) - 1) wh[di] = cnt + __popc(peers);
     __syncwarp();
-    r[i] = cnt + __popc(peers & lanemask_lt());
+    s_rank[warp * (OS_ITEMS * 32) + i * 32 + lane] = (uint16_t)(cnt + __popc(peers & lanemask_lt()));
   }
   __syncthreads();
 
@@ -116,10 +117,12 @@ __global__ void __launch_bounds__(OS_THREADS) k_onesweep(
 
 #pragma unroll
   for (int i = 0; i < OS_ITEMS; ++i) {
-    if (d[i] < 256u) {
-      const uint32_t lp = s_dstart[d[i]] + wh[d[i]] + r[i];
+    if ((vmask >> i) & 1u) {
+      const uint32_t li = warp * (OS_ITEMS * 32) + i * 32 + lane;
+      const uint32_t di = (uint32_t)((k[i] >> shift) & 255u);
+      const uint32_t lp = s_dstart[di] + wh[di] + s_rank[li];
       s_keys[lp] = k[i];
-      if (VALS) s_vals[lp] = v[i];
+      if (VALS) s_vals[lp] = vin[base + li];
     }
   }
   __syncthreads();
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(256) k_depth_hist(const uint64_t *__restrict__
   __shared__ uint32_t h[8][256];
   for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
   __syncthreads();
-  const uint32_t n = fs->stats.M;
+  const uint32_t n = fs->n_sort;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint64_t k = keys[i];
 #pragma unroll
@@ -194,7 +197,7 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
     const int a = p & 1;
     k_onesweep<true><<<grid, OS_THREADS, sm, s>>>(w.key_depth[a], w.key_depth[a ^ 1],
                                                   w.val_depth[a], w.val_depth[a ^ 1],
-                                                  &fs->stats.M, 8 * p, fs->off_depth[p],
+                                                  &fs->n_sort, 8 * p, fs->off_depth[p],
                                                   w.status, fs, TK_DEPTH0 + p);
     ++*launches;
   }
