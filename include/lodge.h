@@ -212,6 +212,12 @@ int lodge_to_srgb8(lodge_ctx *ctx, const float *image_dev, int64_t n_pixels, uin
 /* Number of kernels the last lodge_render_frame enqueued. */
 int32_t lodge_last_launch_count(lodge_ctx *ctx);
 
+/* Compositing work counters of the last frame (synchronous; all zero unless
+ * liblodge was built with -DLODGE_COUNTERS): [0] per-warp list entries,
+ * [1] warp iterations, [2] iterations with a pixel inside the cut-off,
+ * [3] pixel evaluations inside the cut-off, [4] warp-batches. */
+int lodge_debug_counters(lodge_ctx *ctx, uint64_t *out8);
+
 #ifdef __cplusplus
 }
 #endif

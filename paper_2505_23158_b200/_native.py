@@ -100,6 +100,7 @@ EXPORTS = {
     "lodge_profile_read": ([C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int32)], C.c_int),
     "lodge_to_srgb8": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p], C.c_int),
     "lodge_last_launch_count": ([C.c_void_p], C.c_int32),
+    "lodge_debug_counters": ([C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
 }
 N_STAGES = 8
 STAGES = ("select", "union", "project", "depth_sort", "tile_setup", "duplicate", "tile_sort",

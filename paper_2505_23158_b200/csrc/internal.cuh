@@ -23,6 +23,7 @@ struct FrameState {
   uint32_t hist_depth[8][256];        // onesweep digit histograms (depth keys)
   uint32_t off_depth[8][256];         // their exclusive scans
   uint32_t off_tile[2][256];          // digit offsets for the two tile passes
+  unsigned long long counters[8];     // LODGE_COUNTERS builds: compositing work counters
 };
 
 enum Ticket {

@@ -1,21 +1,22 @@
 // K6: per-tile front-to-back alpha compositing (reference
 // src/raster.py:327-377 _composite_tile and :440-449 combine).
 //
-// One CTA of 128 threads per 16x16 tile (heaviest tiles first); each warp
-// owns an 8x8 pixel block, each thread two pixels (rows ly and ly+4).  The
-// tile's sorted member list is consumed in batches of 256 members through a
-// two-stage TMA pipeline: for batch b+1 each thread issues cp.async.bulk
-// copies of two members' 64 B payloads (plus the 64 B fp64 records in EXACT
-// mode) into the idle shared-memory stage, completing on that stage's
-// mbarrier, while the warps composite batch b.  After a stage lands, each
-// member's mean is converted once to tile-local fp32 in place.  Each warp
-// then compacts (8 ballots) the members whose pixel box meets its 8x8 block
-// -- the others give its pixels weight 0 -- and walks only those, in list
-// order.  Warp votes stop a warp when all its pixels have T < t_min and the
-// CTA when all pixels have (the reference's per-block break is the same
-// per-pixel rule).  Per-member max weights reduce in-warp with redux.sync,
-// per CTA with shared-memory atomics, then one global atomicMax on the float
-// bits per member and batch.
+// One CTA per 16x16 tile (heaviest tiles first).  FAST: 64 threads, 4 pixels
+// per thread, each warp owning a 16x8 pixel block; EXACT: 128 threads, 2
+// pixels per thread, 16x4 blocks.  The tile's sorted member list is consumed
+// in batches of 256 members through a two-stage TMA pipeline: for batch b+1
+// each thread issues cp.async.bulk copies of its members' 64 B payloads
+// (plus the 64 B fp64 records in EXACT mode) into the idle shared-memory
+// stage, completing on that stage's mbarrier, while the warps composite batch
+// b.  After a stage lands each member's mean is converted once to tile-local
+// fp32 in place.  Each warp then compacts (8 ballots) the members whose
+// ellipse can reach one of its pixel centres -- the minimum of the quadratic
+// form over the block's centre rectangle against the member's cut-off -- and
+// walks only those, in list order.  Warp votes stop a warp when all its
+// pixels have T < t_min and the CTA when all pixels have (the reference's
+// per-block break is the same per-pixel rule).  Per-member max weights reduce
+// in-warp with redux.sync, per CTA with shared-memory atomics, then one global
+// atomicMax on the float bits per member and batch.
 //
 // FAST: fp32 FMA/MUFU, branch-free.  Both skip tests of src/raster.py:356
 // are folded into one per-splat cut-off q_eff on the quadratic form; pixels
@@ -29,9 +30,14 @@
 
 namespace lodge {
 
-constexpr int CB = 256;      // members per batch
-constexpr int CT = 128;      // threads per CTA (4 warps x 8x8 pixels, 2 per thread)
-constexpr int NW = CT / 32;
+template <bool EXACT>
+struct CC {
+  static constexpr int CB = EXACT ? 256 : 128;  // members per batch (divides 1024)
+  static constexpr int PX = EXACT ? 2 : 4;  // pixels per thread
+  static constexpr int CT = 256 / PX;       // threads per CTA
+  static constexpr int NW = CT / 32;        // warps; warp w owns rows [w*ROWS, (w+1)*ROWS)
+  static constexpr int ROWS = 2 * PX;
+};
 
 __device__ __forceinline__ double q_ref64(double A, double B, double C, double dx, double dy) {
   // cn0*dx*dx + 2.0*cn1*dx*dy + cn2*dy*dy, NumPy left-to-right
@@ -49,6 +55,28 @@ __device__ __forceinline__ bool ref_decide(double gx, double gy, double mx, doub
   a = fmin(a, rp.alpha_clamp);
   alpha = a;
   return (a < rp.alpha_min) || (q > LODGE_SUPPORT_Q);  // skipped
+}
+
+// Can the ellipse {q <= cut} reach a pixel centre in [xlo,xhi] x [ylo,yhi]
+// (tile-local)?  Exact minimum of the convex quadratic form over the
+// rectangle (interior, else the four edges), with a margin for fp32 rounding.
+__device__ __forceinline__ bool ellipse_meets_block(float mx, float my, float A, float B2, float C,
+                                                    float cut, float tol, float xlo, float xhi,
+                                                    float ylo, float yhi) {
+  if (!(cut > -INFINITY)) return false;
+  if (mx >= xlo && mx <= xhi && my >= ylo && my <= yhi) return true;
+  const float ex0 = xlo - mx, ex1 = xhi - mx, ey0 = ylo - my, ey1 = yhi - my;
+  float qmin = INFINITY;
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const float dx = s ? ex1 : ex0;  // vertical edge: minimise over dy
+    const float dy = fminf(fmaxf(-B2 * dx / (2.f * C), ey0), ey1);
+    qmin = fminf(qmin, A * dx * dx + B2 * dx * dy + C * dy * dy);
+    const float dy2 = s ? ey1 : ey0;  // horizontal edge: minimise over dx
+    const float dx2 = fminf(fmaxf(-B2 * dy2 / (2.f * A), ex0), ex1);
+    qmin = fminf(qmin, A * dx2 * dx2 + B2 * dx2 * dy2 + C * dy2 * dy2);
+  }
+  return !(qmin > cut + tol + 1e-3f * (1.f + fabsf(cut)));  // NaN -> meets
 }
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
@@ -83,12 +111,13 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 
 template <bool EXACT>
 struct CompSmem {
-  Payload pl[2][CB];                           // TMA destinations (64 B each)
+  static constexpr int CB = CC<EXACT>::CB;
+  Payload pl[2][CB];                         // TMA destinations (64 B each)
   Precise pr[EXACT ? 2 : 1][EXACT ? CB : 1];  // EXACT: fp64 records
   uint32_t m[2][CB];                           // member splat ids (guard re-check)
   unsigned long long maxw[EXACT ? CB : 1];
   uint32_t maxw32[CB];
-  uint8_t wlist[NW * CB];
+  uint8_t wlist[CC<EXACT>::NW * CB];
   uint64_t bar[2];
 };
 
@@ -99,13 +128,13 @@ struct CompParams {
 };
 
 template <bool EXACT>
-__global__ void __launch_bounds__(CT) k_composite(const uint64_t *__restrict__ pairs,
-                                                  const uint32_t *__restrict__ tile_start,
-                                                  const uint32_t *__restrict__ tile_order,
-                                                  const Payload *__restrict__ payload,
-                                                  const Precise *__restrict__ precise,
-                                                  FrameState *fs, const CompParams cpar,
-                                                  void *image, int32_t *visible, void *maxw) {
+__global__ void __launch_bounds__(CC<EXACT>::CT) k_composite(
+    const uint64_t *__restrict__ pairs, const uint32_t *__restrict__ tile_start,
+    const uint32_t *__restrict__ tile_order, const Payload *__restrict__ payload,
+    const Precise *__restrict__ precise, FrameState *fs, const CompParams cpar, void *image,
+    int32_t *visible, void *maxw) {
+  constexpr int PX = CC<EXACT>::PX, CT = CC<EXACT>::CT, ROWS = CC<EXACT>::ROWS;
+  constexpr int CB = CC<EXACT>::CB;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   CompSmem<EXACT> &S = *reinterpret_cast<CompSmem<EXACT> *>(smem_raw);
   const lodge_raster_params &rp = cpar.rp;
@@ -113,21 +142,25 @@ __global__ void __launch_bounds__(CT) k_composite(const uint64_t *__restrict__ p
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t t = tile_order ? tile_order[blockIdx.x] : blockIdx.x;
   const int tx = t % cpar.tiles_x, ty = t / cpar.tiles_x;
-  const int lx = (warp & 1) * 8 + (lane & 7), ly0 = (warp >> 1) * 8 + (lane >> 3);
-  const float wx_lo = (float)((warp & 1) * 8) + 0.5f, wx_hi = wx_lo + 7.0f;
-  const float wy_lo = (float)((warp >> 1) * 8) + 0.5f, wy_hi = wy_lo + 7.0f;
-  const int px = tx * 16 + lx, py0 = ty * 16 + ly0, py1 = py0 + 4;
-  const bool in0 = px < cpar.W && py0 < cpar.H, in1 = px < cpar.W && py1 < cpar.H;
+  const int lx = lane & 15, ly0 = warp * ROWS + (lane >> 4);  // pixel p at row ly0 + 2p
+  const float wx_lo = 0.5f, wx_hi = 15.5f;
+  const float wy_lo = (float)(warp * ROWS) + 0.5f, wy_hi = wy_lo + (float)(ROWS - 1);
+  const int px = tx * 16 + lx, py0 = ty * 16 + ly0;
   const bool need_image = cpar.flags & LODGE_NEED_IMAGE;
   const bool record_max = (cpar.flags & LODGE_RECORD_MAX) && maxw != nullptr;
   const uint32_t s = tile_start[t];
   uint32_t e = tile_start[t + 1];
   if (fs->stats.overflow) e = s;
 
-  const float fpx = (float)lx + 0.5f, fpy0 = (float)ly0 + 0.5f, fpy1 = fpy0 + 4.0f;
-  const double gx = (double)px + 0.5, gy0 = (double)py0 + 0.5, gy1 = gy0 + 4.0;
+  const float fpx = (float)lx + 0.5f, fpy0 = (float)ly0 + 0.5f;
+  const double gx = (double)px + 0.5, gy0 = (double)py0 + 0.5;
   const double ox = (double)(tx * 16), oy = (double)(ty * 16);
   constexpr uint32_t REC = EXACT ? 128u : 64u;  // bytes staged per member
+
+  uint32_t alive = 0;  // bit p: pixel p composites (T_before >= t_min)
+#pragma unroll
+  for (int p = 0; p < PX; ++p)
+    if (px < cpar.W && py0 + 2 * p < cpar.H) alive |= 1u << p;
 
   if (tid == 0) {
     mbar_init(&S.bar[0], 1);
@@ -152,15 +185,28 @@ __global__ void __launch_bounds__(CT) k_composite(const uint64_t *__restrict__ p
     }
   };
 
-  // FAST state (two pixels)
-  float T0 = 1.f, T1 = 1.f, r0 = 0.f, g0 = 0.f, b0 = 0.f, r1 = 0.f, g1 = 0.f, b1 = 0.f;
-  // EXACT state: per pixel trans, block cumprod, image, block image
-  double tr0 = 1.0, cp0 = 1.0, tr1 = 1.0, cp1 = 1.0;
-  double ir0 = 0, ig0 = 0, ib0 = 0, br0 = 0, bg0 = 0, bb0 = 0;
-  double ir1 = 0, ig1 = 0, ib1 = 0, br1 = 0, bg1 = 0, bb1 = 0;
-  int32_t vis0 = 0, vis1 = 0;
+  float T[PX], cr[PX], cg[PX], cb[PX];                 // FAST
+  double tr[EXACT ? PX : 1], cp[EXACT ? PX : 1];      // EXACT transmittance
+  double ir[EXACT ? PX : 1], ig[EXACT ? PX : 1], ib[EXACT ? PX : 1];
+  double br[EXACT ? PX : 1], bg[EXACT ? PX : 1], bb[EXACT ? PX : 1];
+  int32_t vis[PX];
+#pragma unroll
+  for (int p = 0; p < PX; ++p) {
+    T[p] = 1.f;
+    cr[p] = cg[p] = cb[p] = 0.f;
+    vis[p] = 0;
+  }
+  if (EXACT) {
+#pragma unroll
+    for (int p = 0; p < (EXACT ? PX : 1); ++p) {
+      tr[p] = cp[p] = 1.0;
+      ir[p] = ig[p] = ib[p] = br[p] = bg[p] = bb[p] = 0.0;
+    }
+  }
   uint32_t guard = 0;
-  bool alive0 = in0, alive1 = in1;
+#ifdef LODGE_COUNTERS
+  unsigned long long c_list = 0, c_iter = 0, c_hit = 0, c_px = 0, c_batch = 0;
+#endif
   uint32_t phase0 = 0u, phase1 = 0u;
 
   if (s < e) issue(s, 0);
@@ -170,25 +216,29 @@ __global__ void __launch_bounds__(CT) k_composite(const uint64_t *__restrict__ p
     if (b + CB < e) issue(b + CB, k ^ 1);  // next batch in flight while this one composites
     if (EXACT && b > s && ((b - s) & 1023u) == 0) {
       // block boundary of the reference's 1024-member cumprod
-      tr0 = __dmul_rn(cp0, tr0); cp0 = 1.0;
-      tr1 = __dmul_rn(cp1, tr1); cp1 = 1.0;
-      ir0 = __dadd_rn(ir0, br0); ig0 = __dadd_rn(ig0, bg0); ib0 = __dadd_rn(ib0, bb0);
-      ir1 = __dadd_rn(ir1, br1); ig1 = __dadd_rn(ig1, bg1); ib1 = __dadd_rn(ib1, bb1);
-      br0 = bg0 = bb0 = br1 = bg1 = bb1 = 0.0;
+#pragma unroll
+      for (int p = 0; p < (EXACT ? PX : 1); ++p) {
+        tr[p] = __dmul_rn(cp[p], tr[p]);
+        cp[p] = 1.0;
+        ir[p] = __dadd_rn(ir[p], br[p]);
+        ig[p] = __dadd_rn(ig[p], bg[p]);
+        ib[p] = __dadd_rn(ib[p], bb[p]);
+        br[p] = bg[p] = bb[p] = 0.0;
+      }
     }
     if (k == 0) { mbar_wait(&S.bar[0], phase0); phase0 ^= 1u; }
     else { mbar_wait(&S.bar[1], phase1); phase1 ^= 1u; }
     Payload *PL = S.pl[k];
-    // tile-local fp32 mean, written over the fp64 mean (kept in S.m -> global
-    // payload for the rare fp64 re-check); zero the batch's max slots
+    // tile-local fp32 mean, written over the fp64 mean in FAST mode (the
+    // fp64 mean stays in global memory for the rare re-check)
 #pragma unroll
     for (int h = 0; h < CB / CT; ++h) {
       const int j = tid + h * CT;
       if (j < n) {
-        Payload &p = PL[j];
+        Payload &pj = PL[j];
         if (!EXACT) {
-          const float mxl = (float)(p.mx - ox), myl = (float)(p.my - oy);
-          reinterpret_cast<float2 *>(&p.mx)[0] = make_float2(mxl, myl);
+          const float mxl = (float)(pj.mx - ox), myl = (float)(pj.my - oy);
+          reinterpret_cast<float2 *>(&pj.mx)[0] = make_float2(mxl, myl);
           S.maxw32[j] = 0u;
         } else {
           S.maxw[j] = 0ull;
@@ -196,26 +246,28 @@ __global__ void __launch_bounds__(CT) k_composite(const uint64_t *__restrict__ p
       }
     }
     __syncthreads();
-    // per-warp member list: members whose box meets this warp's 8x8 pixels
+    // per-warp member list: members whose ellipse can reach a pixel centre
     uint8_t *wl = S.wlist + warp * CB;
     int cnt = 0;
-    if (__any_sync(FULL_MASK, alive0 || alive1)) {
+    if (__any_sync(FULL_MASK, alive != 0u)) {
       for (int q0 = 0; q0 < n; q0 += 32) {
         const int j = q0 + lane;
         bool hit = false;
         if (j < n) {
-          const Payload &p = PL[j];
+          const Payload &pj = PL[j];
           float mxl, myl;
           if (EXACT) {
-            mxl = (float)(p.mx - ox);
-            myl = (float)(p.my - oy);
+            mxl = (float)(pj.mx - ox);
+            myl = (float)(pj.my - oy);
           } else {
-            const float2 mm = reinterpret_cast<const float2 *>(&p.mx)[0];
+            const float2 mm = reinterpret_cast<const float2 *>(&pj.mx)[0];
             mxl = mm.x;
             myl = mm.y;
           }
-          hit = !(mxl + p.bx < wx_lo || mxl - p.bx > wx_hi || myl + p.by < wy_lo ||
-                  myl - p.by > wy_hi);
+          hit = !(mxl + pj.bx < wx_lo || mxl - pj.bx > wx_hi || myl + pj.by < wy_lo ||
+                  myl - pj.by > wy_hi) &&
+                ellipse_meets_block(mxl, myl, pj.A, pj.B2, pj.C, pj.q_eff, pj.tol, wx_lo, wx_hi,
+                                    wy_lo, wy_hi);
         }
         const uint32_t hm = __ballot_sync(FULL_MASK, hit);
         if (hit) wl[cnt + __popc(hm & lanemask_lt())] = (uint8_t)j;
@@ -223,45 +275,40 @@ __global__ void __launch_bounds__(CT) k_composite(const uint64_t *__restrict__ p
       }
     }
     __syncwarp();
+#ifdef LODGE_COUNTERS
+    c_list += cnt;
+    c_batch += 1;
+#endif
     for (int i = 0; i < cnt; ++i) {
-      if (!__any_sync(FULL_MASK, alive0 || alive1)) break;
+      if (!__any_sync(FULL_MASK, alive != 0u)) break;
+#ifdef LODGE_COUNTERS
+      c_iter += 1;
+#endif
       const int j = wl[i];
-      const Payload &p = PL[j];
+      const Payload &pj = PL[j];
       if (EXACT) {
         const Precise &d = S.pr[k][j];
-        double w0 = 0.0, w1 = 0.0;
-        if (alive0) {
+        double wmax = 0.0;
+#pragma unroll
+        for (int p = 0; p < PX; ++p) {
+          if (!((alive >> p) & 1u)) continue;
           double a;
-          const bool sk = ref_decide(gx, gy0, p.mx, p.my, d, rp, a);
+          const bool sk = ref_decide(gx, gy0 + 2.0 * p, pj.mx, pj.my, d, rp, a);
           if (sk) a = 0.0;
-          const double before = __dmul_rn(cp0, tr0);
-          cp0 = __dmul_rn(cp0, __dsub_rn(1.0, a));
-          w0 = __dmul_rn(before, a);
+          const double before = __dmul_rn(cp[p], tr[p]);
+          cp[p] = __dmul_rn(cp[p], __dsub_rn(1.0, a));
+          const double w = __dmul_rn(before, a);
           if (need_image) {
-            br0 = __dadd_rn(br0, __dmul_rn(w0, d.r));
-            bg0 = __dadd_rn(bg0, __dmul_rn(w0, d.g));
-            bb0 = __dadd_rn(bb0, __dmul_rn(w0, d.b));
+            br[p] = __dadd_rn(br[p], __dmul_rn(w, d.r));
+            bg[p] = __dadd_rn(bg[p], __dmul_rn(w, d.g));
+            bb[p] = __dadd_rn(bb[p], __dmul_rn(w, d.b));
           }
-          vis0 += sk ? 0 : 1;
-          alive0 = __dmul_rn(cp0, tr0) >= rp.t_min;
-        }
-        if (alive1) {
-          double a;
-          const bool sk = ref_decide(gx, gy1, p.mx, p.my, d, rp, a);
-          if (sk) a = 0.0;
-          const double before = __dmul_rn(cp1, tr1);
-          cp1 = __dmul_rn(cp1, __dsub_rn(1.0, a));
-          w1 = __dmul_rn(before, a);
-          if (need_image) {
-            br1 = __dadd_rn(br1, __dmul_rn(w1, d.r));
-            bg1 = __dadd_rn(bg1, __dmul_rn(w1, d.g));
-            bb1 = __dadd_rn(bb1, __dmul_rn(w1, d.b));
-          }
-          vis1 += sk ? 0 : 1;
-          alive1 = __dmul_rn(cp1, tr1) >= rp.t_min;
+          vis[p] += sk ? 0 : 1;
+          if (!(__dmul_rn(cp[p], tr[p]) >= rp.t_min)) alive &= ~(1u << p);
+          wmax = fmax(wmax, w);
         }
         if (record_max) {
-          unsigned long long wb = (unsigned long long)__double_as_longlong(fmax(w0, w1));
+          unsigned long long wb = (unsigned long long)__double_as_longlong(wmax);
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
             const unsigned long long ob = __shfl_xor_sync(FULL_MASK, wb, o);
@@ -270,43 +317,68 @@ __global__ void __launch_bounds__(CT) k_composite(const uint64_t *__restrict__ p
           if (lane == 0 && wb) atomicMax(&S.maxw[j], wb);
         }
       } else {
-        const float2 mm = reinterpret_cast<const float2 *>(&p.mx)[0];
-        const float4 cn = *reinterpret_cast<const float4 *>(&p.A);    // A, 2B, C, o
-        const float2 qt = *reinterpret_cast<const float2 *>(&p.q_eff);  // q_eff, tol
-        const float dx = fpx - mm.x, dy0 = fpy0 - mm.y, dy1 = fpy1 - mm.y;
-        const float adx = cn.x * dx, bdx = cn.y * dx;
-        const float q0 = fmaf(adx, dx, fmaf(bdx, dy0, cn.z * dy0 * dy0));
-        const float q1 = fmaf(adx, dx, fmaf(bdx, dy1, cn.z * dy1 * dy1));
-        const float d0 = q0 - qt.x, d1 = q1 - qt.x;
-        bool keep0 = alive0 && d0 < -qt.y, keep1 = alive1 && d1 < -qt.y;
-        float a0 = fminf(cn.w * ex2_approx(fmaxf(q0, 0.f) * -0.72134752044448170f), cpar.clamp_f);
-        float a1 = fminf(cn.w * ex2_approx(fmaxf(q1, 0.f) * -0.72134752044448170f), cpar.clamp_f);
-        const bool inb0 = alive0 && fabsf(d0) <= qt.y, inb1 = alive1 && fabsf(d1) <= qt.y;
-        if (__any_sync(FULL_MASK, inb0 || inb1)) {
+        const float2 mm = reinterpret_cast<const float2 *>(&pj.mx)[0];
+        const float4 cn = *reinterpret_cast<const float4 *>(&pj.A);    // A, 2B, C, o
+        const float2 qt = *reinterpret_cast<const float2 *>(&pj.q_eff);  // q_eff, tol
+        const float dx = fpx - mm.x;
+        const float adx2 = cn.x * dx * dx, bdx = cn.y * dx;
+        float q[PX], a[PX];
+        uint32_t keep = 0, inb = 0;
+#pragma unroll
+        for (int p = 0; p < PX; ++p) {
+          const float dy = (fpy0 + 2.f * p) - mm.y;
+          q[p] = fmaf(dy, fmaf(cn.z, dy, bdx), adx2);
+          const float d = q[p] - qt.x;
+          keep |= (d < -qt.y) ? (1u << p) : 0u;
+          inb |= (fabsf(d) <= qt.y) ? (1u << p) : 0u;
+          a[p] = fminf(cn.w * ex2_approx(fmaxf(q[p], 0.f) * -0.72134752044448170f),
+                       cpar.clamp_f);
+        }
+        keep &= alive;
+        inb &= alive;
+#ifdef LODGE_COUNTERS
+        {
+          const uint32_t h = (keep | inb);
+          c_hit += __any_sync(FULL_MASK, h != 0u) ? 1 : 0;
+          c_px += __popc(h);
+        }
+#endif
+        if (__any_sync(FULL_MASK, inb != 0u)) {
           // guard band: re-decide in fp64 with the reference's op order (rare)
-          if (inb0 || inb1) {
+          if (inb) {
             const uint32_t m = S.m[k][j];
             const Payload pg = payload[m];
             const Precise pr = precise[m];
-            double a;
-            if (inb0) { keep0 = !ref_decide(gx, gy0, pg.mx, pg.my, pr, rp, a); a0 = (float)a; ++guard; }
-            if (inb1) { keep1 = !ref_decide(gx, gy1, pg.mx, pg.my, pr, rp, a); a1 = (float)a; ++guard; }
+#pragma unroll
+            for (int p = 0; p < PX; ++p) {
+              if ((inb >> p) & 1u) {
+                double ad;
+                if (!ref_decide(gx, gy0 + 2.0 * p, pg.mx, pg.my, pr, rp, ad)) keep |= 1u << p;
+                a[p] = (float)ad;
+                ++guard;
+              }
+            }
           }
         }
-        const float w0 = keep0 ? T0 * a0 : 0.f, w1 = keep1 ? T1 * a1 : 0.f;
-        if (need_image) {
-          const float4 c = *reinterpret_cast<const float4 *>(&p.r);
-          r0 = fmaf(w0, c.x, r0); g0 = fmaf(w0, c.y, g0); b0 = fmaf(w0, c.z, b0);
-          r1 = fmaf(w1, c.x, r1); g1 = fmaf(w1, c.y, g1); b1 = fmaf(w1, c.z, b1);
+        float wmax = 0.f;
+        float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (need_image) c = *reinterpret_cast<const float4 *>(&pj.r);
+#pragma unroll
+        for (int p = 0; p < PX; ++p) {
+          const bool kp = (keep >> p) & 1u;
+          const float w = kp ? T[p] * a[p] : 0.f;
+          if (need_image) {
+            cr[p] = fmaf(w, c.x, cr[p]);
+            cg[p] = fmaf(w, c.y, cg[p]);
+            cb[p] = fmaf(w, c.z, cb[p]);
+          }
+          T[p] = kp ? T[p] * (1.f - a[p]) : T[p];
+          vis[p] += kp ? 1 : 0;
+          if (!(T[p] >= cpar.tmin_f)) alive &= ~(1u << p);
+          wmax = fmaxf(wmax, w);
         }
-        T0 = keep0 ? T0 * (1.f - a0) : T0;
-        T1 = keep1 ? T1 * (1.f - a1) : T1;
-        vis0 += keep0;
-        vis1 += keep1;
-        alive0 = alive0 && T0 >= cpar.tmin_f;
-        alive1 = alive1 && T1 >= cpar.tmin_f;
         if (record_max) {
-          const unsigned wb = __reduce_max_sync(FULL_MASK, __float_as_uint(fmaxf(w0, w1)));
+          const unsigned wb = __reduce_max_sync(FULL_MASK, __float_as_uint(wmax));
           if (lane == 0 && wb) atomicMax(&S.maxw32[j], wb);
         }
       }
@@ -327,7 +399,7 @@ __global__ void __launch_bounds__(CT) k_composite(const uint64_t *__restrict__ p
       }
     }
     // also the WAR barrier: buffer k is re-filled by the next-but-one issue
-    if (__syncthreads_count(alive0 || alive1) == 0) {
+    if (__syncthreads_count(alive != 0u) == 0) {
       if (b + CB < e) {  // drain the stage already in flight before exiting
         if (k == 0) mbar_wait(&S.bar[1], phase1);
         else mbar_wait(&S.bar[0], phase0);
@@ -336,27 +408,39 @@ __global__ void __launch_bounds__(CT) k_composite(const uint64_t *__restrict__ p
     }
   }
   if (!EXACT && guard) atomicAdd(&fs->stats.guard_hits, guard);
+#ifdef LODGE_COUNTERS
+  if (lane == 0) {  // per warp: list entries, iterations, iterations with a hit, batches
+    atomicAdd(&fs->counters[0], c_list);
+    atomicAdd(&fs->counters[1], c_iter);
+    atomicAdd(&fs->counters[2], c_hit);
+    atomicAdd(&fs->counters[4], c_batch);
+  }
+  atomicAdd(&fs->counters[3], c_px);  // pixel evaluations inside the cut-off
+  if (tid == 0) {
+    atomicMax(&fs->counters[5], c_batch);
+    if (c_batch > 16) atomicAdd(&fs->counters[6], 1ull);
+  }
+#endif
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const bool in = h ? in1 : in0;
-    if (!in) continue;
-    const size_t pix = (size_t)(h ? py1 : py0) * cpar.W + px;
-    if (visible) visible[pix] = h ? vis1 : vis0;
+  for (int p = 0; p < PX; ++p) {
+    const int py = py0 + 2 * p;
+    if (!(px < cpar.W && py < cpar.H)) continue;
+    const size_t pix = (size_t)py * cpar.W + px;
+    if (visible) visible[pix] = vis[p];
     if (!(need_image && image)) continue;
     if (EXACT) {
-      double ir = h ? ir1 : ir0, ig = h ? ig1 : ig0, ib = h ? ib1 : ib0;
-      ir = __dadd_rn(ir, h ? br1 : br0);
-      ig = __dadd_rn(ig, h ? bg1 : bg0);
-      ib = __dadd_rn(ib, h ? bb1 : bb0);
+      const int pe = EXACT ? p : 0;
+      const double r = __dadd_rn(ir[pe], br[pe]), g = __dadd_rn(ig[pe], bg[pe]),
+                   b2 = __dadd_rn(ib[pe], bb[pe]);
       double *im = reinterpret_cast<double *>(image) + 3 * pix;
-      im[0] = fmin(fmax(ir, 0.0), 1.0);
-      im[1] = fmin(fmax(ig, 0.0), 1.0);
-      im[2] = fmin(fmax(ib, 0.0), 1.0);
+      im[0] = fmin(fmax(r, 0.0), 1.0);
+      im[1] = fmin(fmax(g, 0.0), 1.0);
+      im[2] = fmin(fmax(b2, 0.0), 1.0);
     } else {
       float *im = reinterpret_cast<float *>(image) + 3 * pix;
-      im[0] = fminf(fmaxf(h ? r1 : r0, 0.f), 1.f);
-      im[1] = fminf(fmaxf(h ? g1 : g0, 0.f), 1.f);
-      im[2] = fminf(fmaxf(h ? b1 : b0, 0.f), 1.f);
+      im[0] = fminf(fmaxf(cr[p], 0.f), 1.f);
+      im[1] = fminf(fmaxf(cg[p], 0.f), 1.f);
+      im[2] = fminf(fmaxf(cb[p], 0.f), 1.f);
     }
   }
 }
@@ -381,9 +465,9 @@ static void launch_comp(const Work &w, FrameState *fs, int32_t W, int32_t H,
   cp.tiles_x = tiles_x;
   cp.W = W;
   cp.H = H;
-  k_composite<EXACT><<<T, CT, sm, s>>>(w.pairs[0], w.tile_start, w.tile_order, w.payload,
-                                       w.precise, fs, cp, out.image_dev, out.visible_dev,
-                                       out.maxw_dev);
+  k_composite<EXACT><<<T, CC<EXACT>::CT, sm, s>>>(w.pairs[0], w.tile_start, w.tile_order,
+                                                   w.payload, w.precise, fs, cp, out.image_dev,
+                                                   out.visible_dev, out.maxw_dev);
 }
 
 void launch_composite(const Work &w, FrameState *fs, const lodge_camera *, int32_t W, int32_t H,

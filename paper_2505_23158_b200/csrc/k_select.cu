@@ -207,6 +207,7 @@ __global__ void k_begin_frame(FrameState *fs) {
     fs->stats.guard_hits = 0;
   }
   if (i < 32) fs->tickets[i] = 0;
+  if (i < 8) fs->counters[i] = 0;
   for (int k = i; k < 8 * 256; k += blockDim.x) (&fs->hist_depth[0][0])[k] = 0;
 }
 

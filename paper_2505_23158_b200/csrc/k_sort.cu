@@ -88,14 +88,28 @@ __global__ void __launch_bounds__(OS_THREADS, VALS ? 2 : 3) k_onesweep(
     st_store(st + dg, st_pack(epoch, ST_PREFIX, tot));
   } else {
     st_store(st + dg, st_pack(epoch, ST_AGG, tot));
+    // look back LB partitions per round trip (independent loads), consuming
+    // aggregates from the nearest until an inclusive prefix; an empty slot
+    // restarts the window at that partition
+    constexpr int LB = 8;
     int64_t q = (int64_t)part - 1;
-    while (q >= 0) {
-      const uint64_t s = st_load(status + (size_t)q * 256 + dg);
-      const uint32_t flag = ((uint32_t)(s >> 32) == epoch) ? (uint32_t)((s >> 30) & 3u) : 0u;
-      if (flag == ST_EMPTY) continue;
-      excl += (uint32_t)(s & 0x3fffffffu);
-      if (flag == ST_PREFIX) break;
-      --q;
+    bool done = false;
+    while (!done) {
+      uint64_t sv[LB];
+#pragma unroll
+      for (int i = 0; i < LB; ++i)
+        sv[i] = (q - i >= 0) ? st_load(status + (size_t)(q - i) * 256 + dg)
+                             : st_pack(epoch, ST_PREFIX, 0u);
+#pragma unroll
+      for (int i = 0; i < LB; ++i) {
+        if (done) break;
+        const uint32_t flag =
+            ((uint32_t)(sv[i] >> 32) == epoch) ? (uint32_t)((sv[i] >> 30) & 3u) : 0u;
+        if (flag == ST_EMPTY) break;  // retry from partition q
+        excl += (uint32_t)(sv[i] & 0x3fffffffu);
+        --q;
+        if (flag == ST_PREFIX) done = true;
+      }
     }
     st_store(st + dg, st_pack(epoch, ST_PREFIX, excl + tot));
   }

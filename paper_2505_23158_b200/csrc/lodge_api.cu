@@ -485,4 +485,11 @@ int lodge_to_srgb8(lodge_ctx *c, const float *img, int64_t n, uint8_t *out) {
 
 int32_t lodge_last_launch_count(lodge_ctx *c) { return c ? c->launches : 0; }
 
+int lodge_debug_counters(lodge_ctx *c, uint64_t *out8) {
+  if (!c || !out8) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(out8, c->fs->counters, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
 }  // extern "C"
