@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
 // Pass 2, EMIT_CHUNK pairs per CTA regardless of splat sizes: the owners of
 // the chunk's pairs are a contiguous depth-order range [chunk_first[c],
 // chunk_first[c+1]] staged in shared memory; each pair finds its owner by a
-// binary search there and writes (tile << 32 | splat) coalesced.
+// binary search there and writes (tile << 32 | splat) coalesced, in depth
+// order (the tile passes in k_sort.cu then sort them stably by tile).
 __global__ void __launch_bounds__(DUP_THREADS) k_dup_emit(const uint32_t *__restrict__ order,
                                                           int32_t tiles_x, Work w,
                                                           FrameState *fs) {
@@ -200,10 +201,10 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_emit(const uint32_t *__rest
   const uint32_t r0 = w.chunk_first[c];
   const uint32_t r1 = (j1 < P) ? w.chunk_first[c + 1] : M - 1;
   const uint32_t nr = r1 - r0 + 1;
-  for (uint32_t k = threadIdx.x; k < nr; k += DUP_THREADS) {
-    s_off[k] = w.splat_off[r0 + k];
-    s_rect[k] = w.rect_sorted[r0 + k];
-    s_m[k] = order[r0 + k];
+  for (uint32_t q = threadIdx.x; q < nr; q += DUP_THREADS) {
+    s_off[q] = w.splat_off[r0 + q];
+    s_rect[q] = w.rect_sorted[r0 + q];
+    s_m[q] = order[r0 + q];
   }
   __syncthreads();
 #pragma unroll
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_emit(const uint32_t *__rest
     const uint32_t j = j0 + it * DUP_THREADS + threadIdx.x;
     if (j >= j1) break;
     uint32_t lo = 0, hi = nr - 1;
-    while (lo < hi) {  // last k with s_off[k] <= j
+    while (lo < hi) {  // last q with s_off[q] <= j
       const uint32_t mid = (lo + hi + 1) >> 1;
       if (s_off[mid] <= j) lo = mid;
       else hi = mid - 1;

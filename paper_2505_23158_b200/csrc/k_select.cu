@@ -117,17 +117,70 @@ struct UnionArgs {
   int32_t L;
   uint32_t status_stride;  // look-back words per level
   uint32_t slot_base[LODGE_MAX_LEVELS + 1];
+  uint32_t part_base[LODGE_MAX_LEVELS + 1];  // CTA-count table offsets per level
 };
 
-// grid.y = level.  Element t of the stable merge S = merge(A, B) (A first on
-// ties) is located by a merge-path search on diagonal t; the B copy of a
-// value present in both sets is dropped, and survivors are compacted in S
-// order (ordered look-back), which yields np.union1d(A, B) with its tags.
-__global__ void __launch_bounds__(256) k_union(UnionArgs a, FrameState *fs, uint64_t *status,
-                                               uint32_t *union_idx, uint8_t *union_tag) {
-  __shared__ uint32_t s_warp[32];
-  __shared__ uint32_t s_base;
-  const int l = blockIdx.y;
+// One CTA = 256 consecutive diagonals of level l's stable merge S =
+// merge(A, B) (A first on ties).  The CTA's window of A and B is found by two
+// merge-path searches and staged in shared memory; each thread then locates
+// its element by a short search there.  The B copy of a value present in
+// both sets is dropped (keep = false).  Compacting the kept elements in S
+// order yields np.union1d(A, B) with its tags (count -> scan -> write, so no
+// look-back chain serialises the CTAs).  Returns false if the CTA is idle.
+struct UnionLevel {
+  const uint32_t *A, *B;
+  uint32_t na, nb;
+};
+
+__device__ __forceinline__ UnionLevel union_level(const UnionArgs &a, const FrameState *fs, int l) {
+  const int32_t f = fs->stats.f, o = fs->stats.o;
+  UnionLevel u;
+  const int64_t fa = a.offsets[(int64_t)f * a.L + l];
+  u.na = (uint32_t)(a.offsets[(int64_t)f * a.L + l + 1] - fa);
+  u.A = a.data + fa;
+  u.nb = 0;
+  u.B = u.A;
+  if (o >= 0) {
+    const int64_t fb = a.offsets[(int64_t)o * a.L + l];
+    u.nb = (uint32_t)(a.offsets[(int64_t)o * a.L + l + 1] - fb);
+    u.B = a.data + fb;
+  }
+  return u;
+}
+
+// Flattened CTA index -> (level, part) over a.part_base.
+__device__ __forceinline__ int union_level_of(const UnionArgs &a, uint32_t g, uint32_t &part) {
+  int l = 0;
+  while (l + 1 < a.L && g >= a.part_base[l + 1]) ++l;
+  part = g - a.part_base[l];
+  return l;
+}
+
+// Merge-path splits for every CTA boundary of every level, all in parallel:
+// splits[part_base[l] + l + p] = #A among the first min(256 p, n_l) merged
+// elements, p = 0 .. ceil(n_l / 256).
+__global__ void k_union_split(UnionArgs a, FrameState *fs, uint32_t *splits) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= a.part_base[a.L] + a.L) return;
+  int l = 0;
+  while (l + 1 < a.L && g >= a.part_base[l + 1] + l + 1) ++l;
+  const uint32_t p = g - a.part_base[l] - l;
+  const UnionLevel u = union_level(a, fs, l);
+  const uint32_t n = u.na + u.nb;
+  if (p > (n + 255u) / 256u) return;
+  const uint32_t d = min(p * 256u, n);
+  uint32_t lo = d > u.nb ? d - u.nb : 0u, hi = d < u.na ? d : u.na;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(u.A + mid) <= __ldg(u.B + (d - 1 - mid))) lo = mid + 1;
+    else hi = mid;
+  }
+  splits[g] = lo;
+}
+
+__device__ __forceinline__ bool union_block(const UnionArgs &a, const FrameState *fs, int l,
+                                            uint32_t part, const uint32_t *splits, bool &keep,
+                                            uint32_t &v, uint8_t &tag) {
   const int32_t f = fs->stats.f, o = fs->stats.o;
   const int64_t fa = a.offsets[(int64_t)f * a.L + l];
   const uint32_t na = (uint32_t)(a.offsets[(int64_t)f * a.L + l + 1] - fa);
@@ -139,37 +192,112 @@ __global__ void __launch_bounds__(256) k_union(UnionArgs a, FrameState *fs, uint
     nb = (uint32_t)(a.offsets[(int64_t)o * a.L + l + 1] - fb);
     B = a.data + fb;
   }
-  const uint32_t part = take_ticket(&fs->tickets[TK_UNION0 + l], &s_base);
+  __shared__ uint32_t s_a[258], s_b[258];  // A[i0-1 .. i1], B[j0 .. j1]
   const uint32_t n = na + nb;
-  if (part * 256u >= n) return;  // block-uniform
-  const uint32_t t = part * 256u + threadIdx.x;
-  bool keep = false;
-  uint32_t v = 0;
-  uint8_t tag = 0;
+  if (part * 256u >= n) return false;  // block-uniform
+  const uint32_t d0 = part * 256u, d1 = min(d0 + 256u, n);
+  const uint32_t *sp = splits + a.part_base[l] + l + part;
+  const uint32_t i0 = sp[0], i1 = sp[1], j0 = d0 - i0, j1 = d1 - i1;
+  // stage A[i0-1 .. i1] (one element back for the duplicate test, one ahead
+  // for the tie test) and B[j0 .. j1]
+  for (uint32_t q = threadIdx.x; q < i1 - i0 + 2; q += 256) {
+    const int64_t ia = (int64_t)i0 - 1 + q;
+    s_a[q] = (ia >= 0 && ia < na) ? __ldg(A + ia) : 0xffffffffu;
+  }
+  for (uint32_t q = threadIdx.x; q < j1 - j0 + 1; q += 256)
+    s_b[q] = (j0 + q < nb) ? __ldg(B + j0 + q) : 0xffffffffu;
+  __syncthreads();
+  const uint32_t t = d0 + threadIdx.x;
+  keep = false;
+  v = 0;
+  tag = 0;
   if (t < n) {
-    uint32_t lo = t > nb ? t - nb : 0u, hi = t < na ? t : na;
-    while (lo < hi) {  // i = #A among the first t merged elements
+    // merge-path search inside the staged window (local diagonal t - d0)
+    const uint32_t dl = t - d0;
+    uint32_t lo = dl > (j1 - j0) ? dl - (j1 - j0) : 0u, hi = min(dl, i1 - i0);
+    while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;
-      if (__ldg(A + mid) <= __ldg(B + (t - 1 - mid))) lo = mid + 1;
+      if (s_a[mid + 1] <= s_b[dl - 1 - mid]) lo = mid + 1;
       else hi = mid;
     }
-    const uint32_t i = lo, j = t - lo;
-    if (i < na && (j >= nb || __ldg(A + i) <= __ldg(B + j))) {
-      v = __ldg(A + i);
-      tag = (j < nb && __ldg(B + j) == v) ? 3 : 1;
+    const uint32_t i = i0 + lo, j = j0 + (dl - lo);  // global positions
+    const uint32_t av = s_a[lo + 1], bv = s_b[dl - lo];
+    if (i < na && (j >= nb || av <= bv)) {
+      v = av;
+      tag = (j < nb && bv == v) ? 3 : 1;
       keep = true;
     } else {
-      v = __ldg(B + j);
-      keep = !(i > 0 && __ldg(A + i - 1) == v);
+      v = bv;
+      keep = !(i > 0 && s_a[lo] == v);
       tag = 2;
     }
   }
-  const int64_t m = compact_slot(keep, status + (size_t)l * a.status_stride,
-                                 fs->epoch + TK_UNION0 + l, part, s_warp, &s_base);
-  if (m < 0) return;
+  return true;
+}
+
+// flattened grid over all levels' CTAs: kept elements per CTA.
+__global__ void __launch_bounds__(256) k_union_count(UnionArgs a, FrameState *fs,
+                                                     const uint32_t *splits, uint32_t *cnt) {
+  uint32_t part;
+  const int l = union_level_of(a, blockIdx.x, part);
+  bool keep;
+  uint32_t v;
+  uint8_t tag;
+  if (!union_block(a, fs, l, part, splits, keep, v, tag)) return;
+  const uint32_t c = __syncthreads_count(keep);
+  if (threadIdx.x == 0) cnt[a.part_base[l] + part] = c;
+}
+
+// grid L x 1024 threads: exclusive scan of the CTA counts of level l, U_l.
+__global__ void __launch_bounds__(1024) k_union_scan(UnionArgs a, FrameState *fs, uint32_t *cnt) {
+  __shared__ uint32_t s_sum[1024];
+  const int l = blockIdx.x;
+  const int32_t f = fs->stats.f, o = fs->stats.o;
+  uint32_t n = (uint32_t)(a.offsets[(int64_t)f * a.L + l + 1] - a.offsets[(int64_t)f * a.L + l]);
+  if (o >= 0) n += (uint32_t)(a.offsets[(int64_t)o * a.L + l + 1] - a.offsets[(int64_t)o * a.L + l]);
+  const uint32_t np = (n + 255u) / 256u;
+  uint32_t *c = cnt + a.part_base[l];
+  const uint32_t per = (np + 1023u) / 1024u, b = threadIdx.x * per, e = min(np, b + per);
+  uint32_t loc = 0;
+  for (uint32_t q = b; q < e; ++q) loc += c[q];
+  s_sum[threadIdx.x] = loc;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const uint32_t t = threadIdx.x >= off ? s_sum[threadIdx.x - off] : 0u;
+    __syncthreads();
+    s_sum[threadIdx.x] += t;
+    __syncthreads();
+  }
+  uint32_t run = s_sum[threadIdx.x] - loc;
+  for (uint32_t q = b; q < e; ++q) {
+    const uint32_t x = c[q];
+    c[q] = run;
+    run += x;
+  }
+  if (threadIdx.x == 1023) fs->stats.U_level[l] = s_sum[1023];
+}
+
+// flattened grid: recompute the CTA's merge and write the kept elements in order.
+__global__ void __launch_bounds__(256) k_union_write(UnionArgs a, FrameState *fs,
+                                                     const uint32_t *splits, const uint32_t *cnt,
+                                                     uint32_t *union_idx, uint8_t *union_tag) {
+  __shared__ uint32_t s_w[8];
+  uint32_t part;
+  const int l = union_level_of(a, blockIdx.x, part);
+  bool keep;
+  uint32_t v;
+  uint8_t tag;
+  if (!union_block(a, fs, l, part, splits, keep, v, tag)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t bal = __ballot_sync(FULL_MASK, keep);
+  if (lane == 0) s_w[warp] = __popc(bal);
+  __syncthreads();
+  uint32_t pre = cnt[a.part_base[l] + part];
+  for (int w = 0; w < warp; ++w) pre += s_w[w];
+  if (!keep) return;
+  const uint32_t m = pre + __popc(bal & lanemask_lt());
   union_idx[a.slot_base[l] + m] = v;
   union_tag[a.slot_base[l] + m] = tag;
-  atomicMax(&fs->stats.U_level[l], (uint32_t)(m + 1));
 }
 
 __global__ void k_union_sizes(int32_t L, FrameState *fs) {
@@ -190,9 +318,19 @@ void launch_union(const lodge_chunks &ch, const LevelSlots &ls, FrameState *fs, 
   for (int l = 0; l <= LODGE_MAX_LEVELS; ++l) a.slot_base[l] = (l <= ch.L) ? ls.slot_base[l] : 0;
   for (int l = 0; l < ch.L; ++l) max_slots = max(max_slots, ls.slot_base[l + 1] - ls.slot_base[l]);
   a.status_stride = union_status_stride(max_slots);
-  if (max_slots > 0) {
-    dim3 grid((max_slots + 255) / 256, ch.L);
-    k_union<<<grid, 256, 0, s>>>(a, fs, status, union_idx, union_tag);
+  a.part_base[0] = 0;
+  for (int l = 0; l < ch.L; ++l)
+    a.part_base[l + 1] = a.part_base[l] + (ls.slot_base[l + 1] - ls.slot_base[l] + 255) / 256;
+  // scratch in the look-back buffer: CTA counts, then the merge-path splits
+  // (count words have zero flag bits, so no look-back ever reads them as ready)
+  uint32_t *cnt = reinterpret_cast<uint32_t *>(status);
+  uint32_t *splits = cnt + a.part_base[ch.L];
+  const uint32_t nparts = a.part_base[ch.L];
+  if (max_slots > 0 && nparts > 0) {
+    k_union_split<<<(nparts + ch.L + 255) / 256, 256, 0, s>>>(a, fs, splits);
+    k_union_count<<<nparts, 256, 0, s>>>(a, fs, splits, cnt);
+    k_union_scan<<<ch.L, 1024, 0, s>>>(a, fs, cnt);
+    k_union_write<<<nparts, 256, 0, s>>>(a, fs, splits, cnt, union_idx, union_tag);
   }
   k_union_sizes<<<1, 32, 0, s>>>(ch.L, fs);
 }

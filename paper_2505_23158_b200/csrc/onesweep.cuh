@@ -1,0 +1,146 @@
+// One onesweep partition (shared by the radix passes in k_sort.cu and the
+// emission-fused first tile pass in k_bin.cu).
+#pragma once
+#include "internal.cuh"
+
+namespace lodge {
+
+constexpr int OS_THREADS = 256;
+constexpr int OS_WSTRIDE = 257;  // per-warp digit counters (+1 bucket for invalid items)
+
+// Lanes holding the same 9-bit digit (bit 8 marks invalid items), from nine
+// ballots: cheaper than MATCH.ANY, whose latency dominated the ranking.
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
+  uint32_t peers = FULL_MASK;
+#pragma unroll
+  for (int b = 0; b < 9; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const uint32_t bal = __ballot_sync(FULL_MASK, bit);
+    peers &= bit ? bal : ~bal;
+  }
+  return peers;
+}
+
+template <int ITEMS, bool VALS>
+struct OSmem {
+  uint64_t keys[OS_THREADS * ITEMS];
+  uint32_t vals[VALS ? OS_THREADS * ITEMS : 1];
+  uint32_t whist[2][OS_THREADS / 32][OS_WSTRIDE];  // two ranking chains per warp
+  uint32_t dstart[256];
+  uint32_t gbase[256];
+  uint32_t misc[32];
+  uint16_t rank[OS_THREADS * ITEMS];
+};
+
+// Keys are in registers in warp-contiguous order: item i of lane l in warp w
+// is partition element w*(ITEMS*32) + i*32 + l (the first half of a warp's
+// items forms ranking chain 0, the second half chain 1, so the two chains
+// are independent and the element order is (warp, chain, item, lane)).
+// vmask marks valid items; cnt_valid = number of valid elements, which are
+// the partition's first cnt_valid.  Writes keys (and vget(li) values) to
+// their digit-sorted global positions digit_off[d] + prefix + local rank.
+template <int ITEMS, bool VALS, typename VGet>
+__device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS> &S, uint64_t (&k)[ITEMS],
+                                                   uint32_t vmask, uint32_t part,
+                                                   uint32_t cnt_valid, int shift,
+                                                   const uint32_t *__restrict__ digit_off,
+                                                   uint64_t *status, uint32_t epoch,
+                                                   uint64_t *__restrict__ kout,
+                                                   uint32_t *__restrict__ vout, VGet vget) {
+  static_assert(ITEMS % 2 == 0, "two ranking chains");
+  constexpr int H = ITEMS / 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 2 * (OS_THREADS / 32) * OS_WSTRIDE; i += OS_THREADS)
+    (&S.whist[0][0][0])[i] = 0;
+  __syncthreads();
+  uint32_t *wh0 = S.whist[0][warp], *wh1 = S.whist[1][warp];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const uint32_t d0 = ((vmask >> i) & 1u) ? (uint32_t)((k[i] >> shift) & 255u) : 256u;
+    const uint32_t d1 = ((vmask >> (i + H)) & 1u) ? (uint32_t)((k[i + H] >> shift) & 255u) : 256u;
+    const uint32_t p0 = digit_peers(d0);
+    const uint32_t p1 = digit_peers(d1);
+    const uint32_t c0 = wh0[d0], c1 = wh1[d1];
+    const uint32_t lt = lanemask_lt();
+    __syncwarp();
+    if ((p0 & lt) == 0u) wh0[d0] = c0 + __popc(p0);  // lowest peer lane updates
+    if ((p1 & lt) == 0u) wh1[d1] = c1 + __popc(p1);
+    __syncwarp();
+    S.rank[warp * (ITEMS * 32) + i * 32 + lane] = (uint16_t)(c0 + __popc(p0 & lt));
+    S.rank[warp * (ITEMS * 32) + (i + H) * 32 + lane] = (uint16_t)(c1 + __popc(p1 & lt));
+  }
+  __syncthreads();
+  // per digit: exclusive offsets over (warp, chain) and the partition total
+  const uint32_t dg = tid;  // 256 threads == 256 digits
+  uint32_t tot = 0;
+#pragma unroll
+  for (int w = 0; w < OS_THREADS / 32; ++w) {
+    const uint32_t a = S.whist[0][w][dg], b = S.whist[1][w][dg];
+    S.whist[0][w][dg] = tot;
+    S.whist[1][w][dg] = tot + a;
+    tot += a + b;
+  }
+  // publish aggregate, then look back LB partitions per round trip
+  uint64_t *st = status + (size_t)part * 256;
+  uint32_t excl = 0;
+  if (part == 0) {
+    st_store(st + dg, st_pack(epoch, ST_PREFIX, tot));
+  } else {
+    st_store(st + dg, st_pack(epoch, ST_AGG, tot));
+    constexpr int LB = 8;
+    int64_t q = (int64_t)part - 1;
+    bool done = false;
+    while (!done) {
+      uint64_t sv[LB];
+#pragma unroll
+      for (int i = 0; i < LB; ++i)
+        sv[i] = (q - i >= 0) ? st_load(status + (size_t)(q - i) * 256 + dg)
+                             : st_pack(epoch, ST_PREFIX, 0u);
+#pragma unroll
+      for (int i = 0; i < LB; ++i) {
+        if (done) break;
+        const uint32_t flag =
+            ((uint32_t)(sv[i] >> 32) == epoch) ? (uint32_t)((sv[i] >> 30) & 3u) : 0u;
+        if (flag == ST_EMPTY) break;  // retry from partition q
+        excl += (uint32_t)(sv[i] & 0x3fffffffu);
+        --q;
+        if (flag == ST_PREFIX) done = true;
+      }
+    }
+    st_store(st + dg, st_pack(epoch, ST_PREFIX, excl + tot));
+  }
+  S.gbase[dg] = digit_off[dg] + excl;
+  uint32_t inc = tot;  // partition-local exclusive scan of the digit totals
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) S.misc[1 + warp] = inc;
+  __syncthreads();
+  uint32_t wpre = 0;
+#pragma unroll
+  for (int w = 0; w < OS_THREADS / 32; ++w) wpre += (w < warp) ? S.misc[1 + w] : 0u;
+  S.dstart[dg] = wpre + inc - tot;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    if ((vmask >> i) & 1u) {
+      const uint32_t li = warp * (ITEMS * 32) + i * 32 + lane;
+      const uint32_t di = (uint32_t)((k[i] >> shift) & 255u);
+      const uint32_t lp = S.dstart[di] + S.whist[i < H ? 0 : 1][warp][di] + S.rank[li];
+      S.keys[lp] = k[i];
+      if (VALS) S.vals[lp] = vget(li);
+    }
+  }
+  __syncthreads();
+  for (uint32_t j = tid; j < cnt_valid; j += OS_THREADS) {
+    const uint64_t key = S.keys[j];
+    const uint32_t dd = (uint32_t)((key >> shift) & 255u);
+    const uint32_t out = S.gbase[dd] + (j - S.dstart[dd]);
+    kout[out] = key;
+    if (VALS) vout[out] = S.vals[j];
+  }
+}
+
+}  // namespace lodge
