@@ -69,11 +69,11 @@ def workload_name(cfg_name):
 
 
 def my_views(rank, world, n_steps_total, block):
-    """Block-cyclic view assignment: block b of `block` consecutive sweep views
-    goes to rank b % world; step s of this rank uses its s-th block (cyclic)."""
-    n_blocks = SWEEP_VIEWS // block
-    mine = [b for b in range(n_blocks) if b % world == rank]
-    return [[mine[s % len(mine)] * block + v for v in range(block)] for s in range(n_steps_total)]
+    """Block-cyclic view assignment (paper_2505_23158_b200/shard.py): block b
+    of `block` consecutive sweep views goes to rank b % world; step s of this
+    rank uses its s-th block (cyclic)."""
+    from paper_2505_23158_b200.shard import step_schedule
+    return step_schedule(SWEEP_VIEWS, world, rank, n_steps_total, block)
 
 
 # ---------------------------------------------------------------------------
@@ -382,13 +382,19 @@ def run_lodge(args):
                "path": "Renderer.render + to_srgb8 (8-bit sRGB like splatlod render), pinned "
                        "host camera upload and image/stats read-back every step"}
 
-    # ---- gather per-rank metrics over NCCL ---------------------------------
+    # ---- gather per-rank metrics and per-view results over NCCL ------------
+    from paper_2505_23158_b200 import shard
     per_rank = torch.tensor([ms, float(n_timed), P, float(overflow)], dtype=torch.float64,
                             device=dev)
-    if world > 1:
-        gathered = [torch.zeros_like(per_rank) for _ in range(world)]
-        dist.all_gather(gathered, per_rank)
-        overflow = int(sum(float(g[3]) for g in gathered))
+    gathered = shard.gather_rows(per_rank)
+    overflow = int(gathered[:, 3].sum().item())
+    last = schedule[args.warmup + args.steps - 1]
+    view_ids = torch.tensor(last, dtype=torch.int64, device=dev)
+    sums = torch.stack([frames[j].image.double().sum().reshape(1) for j in range(len(last))])
+    g_ids, g_sums = shard.gather_views(view_ids, sums, max_per_rank=B)
+    gathered_views = {"views": int(g_ids.numel()), "image_checksum": float(g_sums.sum().item()),
+                      "how": "per-view image sums of each rank's last step, all_gather "
+                             + ("NCCL" if world > 1 else "(single rank)")}
 
     # ---- CPU baseline (rank 0, N=1): oracle on a bounded sample ------------
     cpu = None
@@ -436,7 +442,7 @@ def run_lodge(args):
                        "overflow_frames": int(overflow), "setup_s": round(setup_s, 1)},
             "e2e": e2e, "gpu_launches": int(launches_per_frame * total_frames),
             "roofline": roofline, "stages": stages, "cpu_baseline": cpu, "clocks": clk,
-            "parity_sample": parity,
+            "parity_sample": parity, "gathered": gathered_views,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -33,7 +33,10 @@ namespace lodge {
 template <bool EXACT>
 struct CC {
   static constexpr int CB = EXACT ? 256 : 128;  // members per batch (divides 1024)
-  static constexpr int PX = EXACT ? 2 : 4;  // pixels per thread
+#ifndef LODGE_COMP_PX
+#define LODGE_COMP_PX 4
+#endif
+  static constexpr int PX = EXACT ? 2 : LODGE_COMP_PX;  // pixels per thread
   static constexpr int CT = 256 / PX;       // threads per CTA
   static constexpr int NW = CT / 32;        // warps; warp w owns rows [w*ROWS, (w+1)*ROWS)
   static constexpr int ROWS = 2 * PX;
