@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--views-per-step", type=int, default=BLOCK)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--streams", type=int, default=2,
+                    help="frames in flight per GPU (one liblodge context + stream each)")
     ap.add_argument("--cpu-views", type=int, default=1, help="views in the CPU baseline sample")
     return ap.parse_args()
 
@@ -247,7 +249,8 @@ def run_lodge(args):
     levels = [DeviceLevel.from_tensors(torch.from_numpy(g).to(dev), torch.from_numpy(s).to(dev),
                                        cfg.degree) for g, s, _ in cfg.levels]
     plan = DevicePlan.from_arrays(cfg.centers, cfg.offsets, cfg.data, cfg.L, dev)
-    r = LG.Renderer(levels, plan, device=dev, storage="fp32", precision=args.precision)
+    r = LG.Renderer(levels, plan, device=dev, storage="fp32", precision=args.precision,
+                    n_streams=args.streams)
     store_gb = sum(l.nbytes() for l in levels) / 1e9
     B = args.views_per_step
     schedule = my_views(rank, world, args.warmup + args.steps, B)
@@ -267,10 +270,12 @@ def run_lodge(args):
     # sizing: every scheduled view once, then reserve pairs for the largest
     sizing = torch.zeros((len(flat), STATS_BYTES), dtype=torch.uint8, device=dev)
     r.reserve(64 << 20)
+    torch.cuda.synchronize()
     for i, v in enumerate(flat):
         fr = frames[0]
-        r.render(cams[pos[v]], fr)
-        sizing[i].copy_(fr.stats)
+        r.render(cams[pos[v]], fr, slot=0)
+        with torch.cuda.stream(r.stream_of(0)):
+            sizing[i].copy_(fr.stats)
     torch.cuda.synchronize()
     st_sz = read_stats(sizing)
     P_max = max(s.P for s in st_sz)
@@ -278,35 +283,43 @@ def run_lodge(args):
     launches_per_frame = r.last_launch_count()
     for s in range(args.warmup):
         for j, v in enumerate(schedule[s]):
-            r.render(cams[pos[v]], frames[j])
+            r.render(cams[pos[v]], frames[j], slot=j % r.n_streams)
     torch.cuda.synchronize()
     setup_s = time.time() - t_setup
 
     # ---- timed region ----------------------------------------------------
+    # frame j of a step runs on slot j % n_streams (own context + stream); the
+    # region is bracketed by events on the current stream that every slot
+    # stream waits on / is waited for.
+    S = r.n_streams
     clocks = Clocks(local)
-    N.check(N.lib().lodge_profile(r.ctx.ptr, 1, n_timed), "lodge_profile")
+    r.profile(True, n_timed)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks.start()
+    cur = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
+    e0.record(cur)
+    for q in range(S):
+        r.stream_of(q).wait_event(e0)
     k = 0
     for s in range(args.warmup, args.warmup + args.steps):
         for j, v in enumerate(schedule[s]):
-            r.render(cams[pos[v]], frames[j])
-            stats_all[k].copy_(frames[j].stats, non_blocking=True)
+            r.render(cams[pos[v]], frames[j], slot=j % S)
+            with torch.cuda.stream(r.stream_of(j % S)):
+                stats_all[k].copy_(frames[j].stats, non_blocking=True)
             k += 1
-    e1.record()
+    for q in range(S):
+        cur.wait_stream(r.stream_of(q))
+    e1.record(cur)
     torch.cuda.synchronize()
     clk = clocks.stop()
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    stage_ms = (C.c_double * N.N_STAGES)()
-    nprof = C.c_int32()
-    N.check(N.lib().lodge_profile_read(r.ctx.ptr, stage_ms, C.byref(nprof)), "profile_read")
-    N.check(N.lib().lodge_profile(r.ctx.ptr, 0, 0), "lodge_profile")
+    stage_ms, nprof_frames = r.profile_read()
+    r.profile(False)
     stats = read_stats(stats_all)
     overflow = sum(s.overflow for s in stats)
     ms_max = ms
@@ -329,7 +342,7 @@ def run_lodge(args):
     peak, peak_kind = load_peaks()
     stages = {}
     for i, name in enumerate(N.STAGES):
-        per = stage_ms[i] / max(nprof.value, 1)
+        per = stage_ms[i] / max(nprof_frames, 1)
         gbs = sb[name] / (per / 1000.0) / 1e9 if per > 0 else 0.0
         stages[name] = {"ms_per_frame": round(per, 5), "bytes_per_frame": round(sb[name]),
                         "GB_s": round(gbs, 1), "frac": round(gbs / peak, 4)}
@@ -349,27 +362,45 @@ def run_lodge(args):
     # ---- end to end through the public API --------------------------------
     e2e = None
     if not args.no_e2e:
-        cam_host = torch.empty((B, cams.shape[1]), dtype=torch.uint8).pin_memory()
-        cam_dev = torch.empty((B, cams.shape[1]), dtype=torch.uint8, device=dev)
+        # double-buffered pinned camera upload (the host refills a buffer only
+        # after its previous copy completed), renders on the slot streams, then
+        # the 8-bit images + stats read back on the current stream each step
+        cam_host = [torch.empty((B, cams.shape[1]), dtype=torch.uint8).pin_memory()
+                    for _ in range(2)]
+        cam_dev = [torch.empty((B, cams.shape[1]), dtype=torch.uint8, device=dev)
+                   for _ in range(2)]
+        copied = [torch.cuda.Event(), torch.cuda.Event()]
         img8 = torch.empty((B, H, W, 3), dtype=torch.uint8, device=dev)
         img8_host = torch.empty((B, H, W, 3), dtype=torch.uint8).pin_memory()
         st_host = torch.empty((B, STATS_BYTES), dtype=torch.uint8).pin_memory()
+        st_dev = torch.empty((B, STATS_BYTES), dtype=torch.uint8, device=dev)
         cams_host = cams.cpu()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        cur = torch.cuda.current_stream(dev)
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record()
-        for s in range(args.warmup, args.warmup + args.steps):
+        f0.record(cur)
+        for si, s in enumerate(range(args.warmup, args.warmup + args.steps)):
+            par = si & 1
+            if si >= 2:
+                copied[par].synchronize()
             for j, v in enumerate(schedule[s]):
-                cam_host[j].copy_(cams_host[pos[v]])
-            cam_dev.copy_(cam_host, non_blocking=True)
+                cam_host[par][j].copy_(cams_host[pos[v]])
+            cam_dev[par].copy_(cam_host[par], non_blocking=True)
+            copied[par].record(cur)
+            for q in range(S):
+                r.stream_of(q).wait_stream(cur)
             for j in range(B):
-                r.render(cam_dev[j], frames[j])
-                r.to_srgb8(frames[j], img8[j])
+                r.render(cam_dev[par][j], frames[j], slot=j % S)
+                r.to_srgb8(frames[j], img8[j], slot=j % S)
+                with torch.cuda.stream(r.stream_of(j % S)):
+                    st_dev[j].copy_(frames[j].stats, non_blocking=True)
+            for q in range(S):
+                cur.wait_stream(r.stream_of(q))
             img8_host.copy_(img8, non_blocking=True)
-            st_host.copy_(torch.stack([f.stats for f in frames]), non_blocking=True)
-        f1.record()
+            st_host.copy_(st_dev, non_blocking=True)
+        f1.record(cur)
         torch.cuda.synchronize()
         ems = f0.elapsed_time(f1)
         if world > 1:
@@ -413,7 +444,8 @@ def run_lodge(args):
                          f"oracle/ C restatement, OpenMP {O.num_threads()} threads, "
                          f"{cpu_model()}, {dt:.1f} s/view"}
         fr = frames[0]
-        r.render(cams[pos[v]], fr)
+        r.render(cams[pos[v]], fr, slot=0)
+        torch.cuda.synchronize()
         st = fr.read_stats()
         img = fr.image.double().cpu().numpy()
         err = float(np.abs(img - ref["image"]).max())

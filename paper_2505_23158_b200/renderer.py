@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .device import (CAMERA_BYTES, DeviceLevel, DevicePlan, camera_bytes, context,
+from .device import (CAMERA_BYTES, Context, DeviceLevel, DevicePlan, camera_bytes, context,
                      params_struct, ptr)
 from .types import TILE_SIZE, RasterConfig
 
@@ -43,10 +43,23 @@ class Frame:
 
 
 class Renderer:
+    """n_streams > 1 keeps that many frames in flight: each slot owns a
+    liblodge context (workspace + frame state) and a CUDA stream, so the
+    latency-bound stages of one frame overlap the bandwidth-bound stages of
+    another.  render(..., slot=k) enqueues on slot k's stream."""
+
     def __init__(self, levels: Sequence, plan, device=None, storage: str = "fp32",
-                 precision: str = "fast", raster_cfg: RasterConfig = RasterConfig()):
+                 precision: str = "fast", raster_cfg: RasterConfig = RasterConfig(),
+                 n_streams: int = 1):
         self.ctx = context(device)
         self.device = self.ctx.device
+        if n_streams < 1:
+            raise ValueError("n_streams must be >= 1")
+        self._slots = [(self.ctx, None)]
+        for _ in range(n_streams - 1):
+            self._slots.append((Context(self.device), torch.cuda.Stream(self.device)))
+        if n_streams > 1:  # slot 0 gets its own stream too
+            self._slots[0] = (self.ctx, torch.cuda.Stream(self.device))
         self.levels = []
         for lv in levels:
             if isinstance(lv, DeviceLevel):
@@ -63,9 +76,42 @@ class Renderer:
         self.U_cap = self.plan.union_capacity
 
     # ------------------------------------------------------------------
+    @property
+    def n_streams(self) -> int:
+        return len(self._slots)
+
+    def stream_of(self, slot: int = 0):
+        """torch stream of a slot (the current stream for a single-slot renderer)."""
+        s = self._slots[slot][1]
+        return s if s is not None else torch.cuda.current_stream(self.device)
+
+    def _bind(self, slot: int):
+        ctx, s = self._slots[slot]
+        if s is None:
+            return ctx.bind(self.precision)
+        with torch.cuda.stream(s):
+            return ctx.bind(self.precision)
+
     def reserve(self, max_pairs: int):
-        N.check(N.lib().lodge_reserve(self.ctx.bind(self.precision), self.U_cap, int(max_pairs)),
-                "lodge_reserve")
+        for k in range(self.n_streams):
+            N.check(N.lib().lodge_reserve(self._bind(k), self.U_cap, int(max_pairs)),
+                    "lodge_reserve")
+
+    def profile(self, enable: bool, max_frames: int = 0):
+        for ctx, _ in self._slots:
+            N.check(N.lib().lodge_profile(ctx.ptr, int(enable), int(max_frames)), "lodge_profile")
+
+    def profile_read(self):
+        """Summed per-stage milliseconds and frame count over all slots."""
+        tot = np.zeros(N.N_STAGES)
+        frames = 0
+        for ctx, _ in self._slots:
+            ms = (C.c_double * N.N_STAGES)()
+            n = C.c_int32()
+            N.check(N.lib().lodge_profile_read(ctx.ptr, ms, C.byref(n)), "lodge_profile_read")
+            tot += np.array(ms[:])
+            frames += n.value
+        return tot, frames
 
     def alloc_frame(self, width: int, height: int, need_image=True, record_max=True) -> Frame:
         tx, ty = -(-width // TILE_SIZE), -(-height // TILE_SIZE)
@@ -84,9 +130,10 @@ class Renderer:
         return torch.from_numpy(host).to(self.device)
 
     def render(self, cam_row: torch.Tensor, frame: Frame, pair=None, t: float = None,
-               need_image: bool = True, record_max: bool = True) -> Frame:
-        """Enqueue one frame on the current stream.  cam_row: one row of
-        upload_cameras().  pair=None: nearest two chunks chosen on device."""
+               need_image: bool = True, record_max: bool = True, slot: int = 0) -> Frame:
+        """Enqueue one frame on slot `slot`'s stream (the current stream for a
+        single-slot renderer).  cam_row: one row of upload_cameras().
+        pair=None: nearest two chunks chosen on device."""
         out = N.FrameOut()
         out.image_dev = frame.image.data_ptr() if (need_image and frame.image is not None) else None
         out.tile_count_dev = frame.tile_count.data_ptr()
@@ -100,17 +147,17 @@ class Renderer:
             pr = (C.c_int32 * 2)(int(f), -1 if o is None else int(o))
             tv = C.c_double(1.0 if t is None else float(t))
         N.check(N.lib().lodge_render_frame(
-            self.ctx.bind(self.precision), self._level_arr, len(self.levels), C.byref(self.plan.struct),
+            self._bind(slot), self._level_arr, len(self.levels), C.byref(self.plan.struct),
             ptr(cam_row), frame.width, frame.height, C.byref(self._rp), pr,
             None if tv is None else C.byref(tv), flags, C.byref(out), ptr(frame.stats)),
             "lodge_render_frame")
         return frame
 
-    def to_srgb8(self, frame: Frame, out: torch.Tensor) -> torch.Tensor:
+    def to_srgb8(self, frame: Frame, out: torch.Tensor, slot: int = 0) -> torch.Tensor:
         """8-bit sRGB of the frame's image on the device (src/images.py:10-17)."""
         if frame.image is None or frame.image.dtype != torch.float32:
             raise ValueError("to_srgb8 needs a FAST-precision frame with an image")
-        N.check(N.lib().lodge_to_srgb8(self.ctx.bind(self.precision), ptr(frame.image),
+        N.check(N.lib().lodge_to_srgb8(self._bind(slot), ptr(frame.image),
                                        frame.width * frame.height, ptr(out)), "lodge_to_srgb8")
         return out
 
