@@ -9,6 +9,8 @@
 // src/raster.py:176-185 (filter_opacity_factor), src/raster.py:136-173
 // (eval_sh), src/scene.py:23-42 (quat_to_matrix), src/raster.py:303-313
 // (_tile_ranges) and src/lod.py:216-227 (project_selection, level-major).
+#include <type_traits>
+
 #include "internal.cuh"
 
 namespace lodge {
@@ -165,10 +167,96 @@ __device__ __forceinline__ Proj project_core(const double v[12], const lodge_cam
   return p;
 }
 
+// Coefficients of one record, (3, (DEG+1)^2), loaded with 16-byte vector
+// loads when the record size allows it (fp32 SH1/SH3, fp64 SH1/SH3).
+template <typename ST, int DEG>
+__device__ __forceinline__ void load_sh(const ST *__restrict__ k, ST (&co)[3 * (DEG + 1) * (DEG + 1)]) {
+  constexpr int N = 3 * (DEG + 1) * (DEG + 1);
+  constexpr int PER = 16 / sizeof(ST);
+  if constexpr ((N * sizeof(ST)) % 16 == 0) {
+    using V = typename std::conditional<sizeof(ST) == 4, float4, double2>::type;
+    const V *p = reinterpret_cast<const V *>(k);
+#pragma unroll
+    for (int i = 0; i < N / PER; ++i) {
+      const V t = __ldg(p + i);
+      const ST *ts = reinterpret_cast<const ST *>(&t);
+#pragma unroll
+      for (int e = 0; e < PER; ++e) co[i * PER + e] = ts[e];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) co[i] = __ldg(k + i);
+  }
+}
+
+// eval_sh (src/raster.py:136-173) with compile-time degree.
+template <typename ST, int DEG>
+__device__ __forceinline__ void eval_sh_t(const ST *__restrict__ k, double xs, double ys,
+                                          double zs, double rgb[3]) {
+  constexpr int T = (DEG + 1) * (DEG + 1);
+  ST co[3 * T];
+  load_sh<ST, DEG>(k, co);
+  double b2[5], b3[7];
+  const double c1y = c_SH_C1 * ys, c1z = c_SH_C1 * zs, c1x = c_SH_C1 * xs;
+  if (DEG >= 2) {
+    const double xx = xs * xs, yy = ys * ys, zz = zs * zs;
+    const double xy = xs * ys, yz = ys * zs, xz = xs * zs;
+    b2[0] = c_SH_C2[0] * xy;
+    b2[1] = c_SH_C2[1] * yz;
+    b2[2] = c_SH_C2[2] * (((2 * zz) - xx) - yy);
+    b2[3] = c_SH_C2[3] * xz;
+    b2[4] = c_SH_C2[4] * (xx - yy);
+    if (DEG >= 3) {
+      b3[0] = c_SH_C3[0] * (ys * ((3 * xx) - yy));
+      b3[1] = c_SH_C3[1] * (xy * zs);
+      b3[2] = c_SH_C3[2] * (ys * (((4 * zz) - xx) - yy));
+      b3[3] = c_SH_C3[3] * (zs * (((2 * zz) - (3 * xx)) - (3 * yy)));
+      b3[4] = c_SH_C3[4] * (xs * (((4 * zz) - xx) - yy));
+      b3[5] = c_SH_C3[5] * (zs * (xx - yy));
+      b3[6] = c_SH_C3[6] * (xs * (xx - (3 * yy)));
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const ST *kc = co + c * T;
+    double out = c_SH_C0 * (double)kc[0];
+    if (DEG >= 1) {
+      out = out - c1y * (double)kc[1];
+      out = out + c1z * (double)kc[2];
+      out = out - c1x * (double)kc[3];
+      if (DEG >= 2) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) out = out + b2[q] * (double)kc[4 + q];
+      }
+      if (DEG >= 3) {
+#pragma unroll
+        for (int q = 0; q < 7; ++q) out = out + b3[q] * (double)kc[9 + q];
+      }
+    }
+    out = out + 0.5;
+    rgb[c] = (out > 0.0 || out != out) ? out : 0.0;
+  }
+}
+
 template <typename ST>
 __device__ __forceinline__ void eval_sh_dev(const ST *__restrict__ k, int terms, int degree,
                                             const double v[12], const lodge_camera &cam,
                                             double rgb[3]) {
+  const double dd0 = v[0] - cam.pos[0], dd1 = v[1] - cam.pos[1], dd2 = v[2] - cam.pos[2];
+  const double nrm = sqrt((dd0 * dd0 + dd1 * dd1) + dd2 * dd2);
+  const double xs = dd0 / nrm, ys = dd1 / nrm, zs = dd2 / nrm;
+  switch (degree) {
+    case 0: eval_sh_t<ST, 0>(k, xs, ys, zs, rgb); return;
+    case 1: eval_sh_t<ST, 1>(k, xs, ys, zs, rgb); return;
+    case 2: eval_sh_t<ST, 2>(k, xs, ys, zs, rgb); return;
+    default: eval_sh_t<ST, 3>(k, xs, ys, zs, rgb); return;
+  }
+}
+
+template <typename ST>
+__device__ __forceinline__ void eval_sh_dev_scalar(const ST *__restrict__ k, int terms, int degree,
+                                                   const double v[12], const lodge_camera &cam,
+                                                   double rgb[3]) {
   const double dd0 = v[0] - cam.pos[0], dd1 = v[1] - cam.pos[1], dd2 = v[2] - cam.pos[2];
   const double nrm = sqrt((dd0 * dd0 + dd1 * dd1) + dd2 * dd2);
   const double xs = dd0 / nrm, ys = dd1 / nrm, zs = dd2 / nrm;
