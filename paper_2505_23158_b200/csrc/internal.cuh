@@ -63,6 +63,7 @@ struct Work {
   Payload *payload;         // M_cap
   Precise *precise;         // M_cap
   uint64_t *pairs[2];       // P_cap each
+  const uint32_t *list;     // per-tile lists (splat ids) of the last tile sort, in pairs[0|1]
   uint64_t *rect_sorted;    // M_cap: rectangles in depth order
   uint32_t *splat_off;      // M_cap + 1: pair offset of each depth-ordered splat
   uint32_t *chunk_first;    // P_cap / EMIT_CHUNK + 2: owner of each emission chunk
@@ -216,7 +217,7 @@ void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32
                        int32_t tiles_y, cudaStream_t s);
 void launch_duplicate(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_cap,
                       cudaStream_t s);
-void launch_tile_sort(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
+void launch_tile_sort(Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
                       int32_t *launches, cudaStream_t s);
 void launch_composite(const Work &w, FrameState *fs, const lodge_camera *cam_dev, int32_t W,
                       int32_t H, const lodge_raster_params &rp, int32_t flags, int32_t exact,

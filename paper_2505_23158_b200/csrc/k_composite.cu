@@ -132,7 +132,7 @@ struct CompParams {
 
 template <bool EXACT>
 __global__ void __launch_bounds__(CC<EXACT>::CT) k_composite(
-    const uint64_t *__restrict__ pairs, const uint32_t *__restrict__ tile_start,
+    const uint32_t *__restrict__ list, const uint32_t *__restrict__ tile_start,
     const uint32_t *__restrict__ tile_order, const Payload *__restrict__ payload,
     const Precise *__restrict__ precise, FrameState *fs, const CompParams cpar, void *image,
     int32_t *visible, void *maxw) {
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT) k_composite(
     for (int h = 0; h < CB / CT; ++h) {
       const int j = tid + h * CT;
       if (j < n) {
-        const uint32_t m = (uint32_t)pairs[bb + j];
+        const uint32_t m = list[bb + j];
         S.m[k][j] = m;
         bulk_g2s(&S.pl[k][j], payload + m, 64, &S.bar[k]);
         if (EXACT) bulk_g2s(&S.pr[k][j], precise + m, 64, &S.bar[k]);
@@ -468,7 +468,7 @@ static void launch_comp(const Work &w, FrameState *fs, int32_t W, int32_t H,
   cp.tiles_x = tiles_x;
   cp.W = W;
   cp.H = H;
-  k_composite<EXACT><<<T, CC<EXACT>::CT, sm, s>>>(w.pairs[0], w.tile_start, w.tile_order,
+  k_composite<EXACT><<<T, CC<EXACT>::CT, sm, s>>>(w.list, w.tile_start, w.tile_order,
                                                    w.payload, w.precise, fs, cp, out.image_dev,
                                                    out.visible_dev, out.maxw_dev);
 }
@@ -481,19 +481,19 @@ void launch_composite(const Work &w, FrameState *fs, const lodge_camera *, int32
 }
 
 // Compat / inspection: export the sorted per-tile lists as source indices.
-__global__ void k_export_lists(const uint64_t *pairs, const uint32_t *tile_start,
+__global__ void k_export_lists(const uint32_t *list, const uint32_t *tile_start,
                                const Payload *payload, FrameState *fs, int32_t T,
                                int64_t *tile_offsets, int64_t *tile_src, int64_t cap) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i <= T) tile_offsets[i] = tile_start[i];
   const uint32_t P = fs->n_pairs;
-  if (i < P && i < cap) tile_src[i] = payload[(uint32_t)pairs[i]].src;
+  if (i < P && i < cap) tile_src[i] = payload[list[i]].src;
 }
 
 void launch_export_lists(const Work &w, FrameState *fs, int32_t T, int64_t *tile_offsets,
                          int64_t *tile_src, int64_t cap, cudaStream_t s) {
   const int64_t n = cap > (int64_t)T + 1 ? cap : (int64_t)T + 1;
-  k_export_lists<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w.pairs[0], w.tile_start, w.payload,
+  k_export_lists<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w.list, w.tile_start, w.payload,
                                                              fs, T, tile_offsets, tile_src, cap);
 }
 

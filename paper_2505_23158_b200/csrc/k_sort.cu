@@ -11,6 +11,8 @@
 // chains per warp (ILP), per-digit decoupled look-back across partitions
 // (virtual partition ids from an atomic ticket for forward progress), then a
 // shared-memory staged, digit-run-coalesced scatter.
+#include <algorithm>
+
 #include "internal.cuh"
 #include "onesweep.cuh"
 
@@ -19,14 +21,16 @@ namespace lodge {
 constexpr int OS_ITEMS = 16;
 constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096 keys per partition
 
-template <bool VALS>
+// Key maps applied at the scatter (see launch_tile_sort).
+enum : int { MAP_ID = 0, MAP_PACK = 1, MAP_LOW = 2 };
+
+template <bool VALS, typename KI, typename KO, int MAP>
 __global__ void __launch_bounds__(OS_THREADS, VALS ? 2 : 3) k_onesweep(
-    const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
-    const uint32_t *__restrict__ vin, uint32_t *__restrict__ vout, const uint32_t *n_ptr,
-    int shift, const uint32_t *__restrict__ digit_off, uint64_t *status, FrameState *fs,
-    int tk) {
+    const KI *__restrict__ kin, KO *__restrict__ kout, const uint32_t *__restrict__ vin,
+    uint32_t *__restrict__ vout, const uint32_t *n_ptr, int shift, int nb, int sb,
+    const uint32_t *__restrict__ digit_off, uint64_t *status, FrameState *fs, int tk) {
   extern __shared__ __align__(16) uint8_t smem[];
-  OSmem<OS_ITEMS, VALS> &S = *reinterpret_cast<OSmem<OS_ITEMS, VALS> *>(smem);
+  OSmem<OS_ITEMS, VALS, KI> &S = *reinterpret_cast<OSmem<OS_ITEMS, VALS, KI> *>(smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) S.misc[0] = atomicAdd(&fs->tickets[tk], 1u);
   __syncthreads();
@@ -34,17 +38,26 @@ __global__ void __launch_bounds__(OS_THREADS, VALS ? 2 : 3) k_onesweep(
   const uint32_t n = *n_ptr;
   const uint32_t base = part * OS_TILE;
   if (base >= n) return;
-  uint64_t k[OS_ITEMS];
+  KI k[OS_ITEMS];
   uint32_t vmask = 0;
 #pragma unroll
   for (int i = 0; i < OS_ITEMS; ++i) {
     const uint32_t idx = base + warp * (OS_ITEMS * 32) + i * 32 + lane;
     const bool valid = idx < n;
     vmask |= valid ? (1u << i) : 0u;
-    k[i] = valid ? kin[idx] : ~0ull;
+    k[i] = valid ? kin[idx] : (KI)~(KI)0;
   }
+  const uint32_t lowmask = sb >= 32 ? 0xffffffffu : ((1u << sb) - 1u);
+  auto kmap = [&](KI key) -> KO {
+    if (MAP == MAP_PACK)  // (tile << 32 | splat) -> (tile >> 8) << sb | splat
+      return (KO)((((uint32_t)((uint64_t)key >> 40)) << sb) | (uint32_t)key);
+    else if (MAP == MAP_LOW)  // -> splat
+      return (KO)((uint32_t)key & lowmask);
+    else
+      return (KO)key;
+  };
   onesweep_partition<OS_ITEMS, VALS>(S, k, vmask, part, min((uint32_t)OS_TILE, n - base), shift,
-                                     digit_off, status, fs->epoch + tk, kout, vout,
+                                     nb, digit_off, status, fs->epoch + tk, kout, kmap, vout,
                                      [&](uint32_t li) { return vin[base + li]; });
 }
 
@@ -84,19 +97,20 @@ __global__ void k_depth_scan(FrameState *fs) {
   }
 }
 
-static void set_smem_once() {
+template <bool VALS, typename KI, typename KO, int MAP>
+static size_t os_kernel_smem() {
   static bool done = false;
-  if (done) return;
-  cudaFuncSetAttribute(k_onesweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(OSmem<OS_ITEMS, true>));
-  cudaFuncSetAttribute(k_onesweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(OSmem<OS_ITEMS, false>));
-  done = true;
+  const size_t sm = sizeof(OSmem<OS_ITEMS, VALS, KI>);
+  if (!done) {
+    cudaFuncSetAttribute(k_onesweep<VALS, KI, KO, MAP>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    done = true;
+  }
+  return sm;
 }
 
 void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
                        cudaStream_t s) {
-  set_smem_once();
   if (M_cap <= 0) return;
   int hist_blocks = (int)((M_cap + 1023) / 1024);
   if (hist_blocks > 148 * 4) hist_blocks = 148 * 4;
@@ -104,28 +118,69 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
   k_depth_scan<<<1, 256, 0, s>>>(fs);
   *launches += 2;
   const unsigned grid = (unsigned)((M_cap + OS_TILE - 1) / OS_TILE);
-  const size_t sm = sizeof(OSmem<OS_ITEMS, true>);
+  const size_t sm = os_kernel_smem<true, uint64_t, uint64_t, MAP_ID>();
   for (int p = 0; p < 8; ++p) {
     const int a = p & 1;
-    k_onesweep<true><<<grid, OS_THREADS, sm, s>>>(w.key_depth[a], w.key_depth[a ^ 1],
-                                                  w.val_depth[a], w.val_depth[a ^ 1],
-                                                  &fs->n_sort, 8 * p, fs->off_depth[p],
-                                                  w.status, fs, TK_DEPTH0 + p);
+    k_onesweep<true, uint64_t, uint64_t, MAP_ID><<<grid, OS_THREADS, sm, s>>>(
+        w.key_depth[a], w.key_depth[a ^ 1], w.val_depth[a], w.val_depth[a ^ 1], &fs->n_sort,
+        8 * p, 8, 32, fs->off_depth[p], w.status, fs, TK_DEPTH0 + p);
     ++*launches;
   }
 }
 
-// The two tile-digit passes: pairs[0] -> pairs[1] (tile & 255) -> pairs[0] (tile >> 8).
-void launch_tile_sort(const Work &w, FrameState *fs, int32_t, int32_t, int32_t *launches,
-                      cudaStream_t s) {
-  set_smem_once();
+static int bit_width(uint64_t v) {
+  int b = 0;
+  while (v) { ++b; v >>= 1; }
+  return b;
+}
+
+// The tile-digit passes over the emitted (tile << 32 | splat) pairs, which
+// leave the bare u32 splat ids of the per-tile lists in w.list:
+//   T <= 256  one pass pairs[0] -> list (u32 in pairs[1])
+//   else      pass 1 on tile & 255, pairs[0] -> pairs[1] packed as
+//             (tile >> 8) << sb | splat in u32 when it fits (sb = the bits a
+//             splat id of this workspace needs), else kept u64;
+//             pass 2 on tile >> 8 -> list (u32 in pairs[0]).
+// Tile ranges come from tile_start, so the lists need no tile bits.
+void launch_tile_sort(Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
+                      int32_t *launches, cudaStream_t s) {
   const unsigned grid = (unsigned)((w.P_cap + OS_TILE - 1) / OS_TILE);
-  for (int p = 0; p < 2; ++p) {
-    k_onesweep<false><<<grid, OS_THREADS, sizeof(OSmem<OS_ITEMS, false>), s>>>(
-        w.pairs[p], w.pairs[p ^ 1], nullptr, nullptr, &fs->n_pairs, 32 + 8 * p, fs->off_tile[p],
-        w.status, fs, TK_TILE0 + p);
+  const uint32_t T = (uint32_t)tiles_x * (uint32_t)tiles_y;
+  const int lo_bits = std::min(8, std::max(1, bit_width(T - 1)));
+  uint32_t *u32_1 = reinterpret_cast<uint32_t *>(w.pairs[1]);
+  uint32_t *u32_0 = reinterpret_cast<uint32_t *>(w.pairs[0]);
+  if (T <= 256) {
+    const size_t sm = os_kernel_smem<false, uint64_t, uint32_t, MAP_LOW>();
+    k_onesweep<false, uint64_t, uint32_t, MAP_LOW><<<grid, OS_THREADS, sm, s>>>(
+        w.pairs[0], u32_1, nullptr, nullptr, &fs->n_pairs, 32, lo_bits, 32, fs->off_tile[0],
+        w.status, fs, TK_TILE0);
     ++*launches;
+    w.list = u32_1;
+    return;
   }
+  const int hi_bits = bit_width((T - 1) >> 8);
+  const int sb = std::max(1, bit_width((uint64_t)std::max<int64_t>(w.M_cap, 1) - 1));
+  if (hi_bits + sb <= 32) {
+    const size_t sm1 = os_kernel_smem<false, uint64_t, uint32_t, MAP_PACK>();
+    k_onesweep<false, uint64_t, uint32_t, MAP_PACK><<<grid, OS_THREADS, sm1, s>>>(
+        w.pairs[0], u32_1, nullptr, nullptr, &fs->n_pairs, 32, 8, sb, fs->off_tile[0], w.status,
+        fs, TK_TILE0);
+    const size_t sm2 = os_kernel_smem<false, uint32_t, uint32_t, MAP_LOW>();
+    k_onesweep<false, uint32_t, uint32_t, MAP_LOW><<<grid, OS_THREADS, sm2, s>>>(
+        u32_1, u32_0, nullptr, nullptr, &fs->n_pairs, sb, hi_bits, sb, fs->off_tile[1], w.status,
+        fs, TK_TILE0 + 1);
+  } else {
+    const size_t sm1 = os_kernel_smem<false, uint64_t, uint64_t, MAP_ID>();
+    k_onesweep<false, uint64_t, uint64_t, MAP_ID><<<grid, OS_THREADS, sm1, s>>>(
+        w.pairs[0], w.pairs[1], nullptr, nullptr, &fs->n_pairs, 32, 8, 32, fs->off_tile[0],
+        w.status, fs, TK_TILE0);
+    const size_t sm2 = os_kernel_smem<false, uint64_t, uint32_t, MAP_LOW>();
+    k_onesweep<false, uint64_t, uint32_t, MAP_LOW><<<grid, OS_THREADS, sm2, s>>>(
+        w.pairs[1], u32_0, nullptr, nullptr, &fs->n_pairs, 40, hi_bits, 32, fs->off_tile[1],
+        w.status, fs, TK_TILE0 + 1);
+  }
+  *launches += 2;
+  w.list = u32_0;
 }
 
 }  // namespace lodge

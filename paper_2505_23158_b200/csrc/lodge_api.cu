@@ -89,6 +89,7 @@ static int ensure_P(lodge_ctx *c, int64_t need) {
   int64_t ncap = std::max<int64_t>(std::max<int64_t>(need, w.P_cap + w.P_cap / 2), 1 << 16);
   cudaFree(w.pairs[0]); cudaFree(w.pairs[1]); cudaFree(w.chunk_first);
   w.pairs[0] = w.pairs[1] = nullptr;
+  w.list = nullptr;
   w.P_cap = 0;
   CK(cudaMalloc(&w.pairs[0], 8 * ncap));
   CK(cudaMalloc(&w.pairs[1], 8 * ncap));
@@ -329,7 +330,7 @@ int lodge_rasterize(lodge_ctx *c, const lodge_batch *b, int64_t M, int64_t n_inp
     CK(cudaMemcpy(&c->fs->n_pairs, &fix[0], 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(&c->fs->stats.overflow, &fix[1], 4, cudaMemcpyHostToDevice));
   }
-  const Work &w = c->w;
+  Work &w = c->w;
   launch_duplicate(w, c->fs, tiles_x, M, s);
   launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s);
   launch_composite(w, c->fs, c->cam_dev, cam->w, cam->h, *rp, flags, exact, *out, 0, s);
@@ -379,7 +380,7 @@ int lodge_render_frame(lodge_ctx *c, const lodge_level *levels, int32_t n_levels
       (rc = ensure_status(c, (c->w.M_cap + 4095) / 4096 * 256 + (U_cap + 255) / 256 + 256)))
     return rc;
   const bool exact = c->precision == LODGE_PREC_EXACT;
-  const Work &w = c->w;
+  Work &w = c->w;
   c->last_slots = ls;
   int32_t nl = 0;
   c->mark(0);
@@ -416,7 +417,7 @@ int lodge_render_frame(lodge_ctx *c, const lodge_level *levels, int32_t n_levels
 int lodge_frame_lists(lodge_ctx *c, int32_t T, int64_t *tile_offsets, int64_t *tile_src,
                       int64_t cap) {
   if (!c || !tile_offsets || !tile_src) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
-  if (!c->w.pairs[0] || T + 1 > c->tiles_cap) return set_err(LODGE_ERR_BAD_ARG, "no frame rendered at this size");
+  if (!c->w.list || T + 1 > c->tiles_cap) return set_err(LODGE_ERR_BAD_ARG, "no frame rendered at this size");
   launch_export_lists(c->w, c->fs, T, tile_offsets, tile_src, cap, c->stream);
   return check_launch("lodge_frame_lists");
 }

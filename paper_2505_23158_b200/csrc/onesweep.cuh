@@ -1,5 +1,7 @@
-// One onesweep partition (shared by the radix passes in k_sort.cu and the
-// emission-fused first tile pass in k_bin.cu).
+// One onesweep partition (the radix passes of k_sort.cu).  Input keys KI are
+// ranked on an 8-bit digit (k >> shift) & 255 of which only the low nb bits
+// can be non-zero (fewer ballots per item); the scatter writes kmap(key),
+// which lets a pass narrow the key it hands to the next one.
 #pragma once
 #include "internal.cuh"
 
@@ -8,22 +10,26 @@ namespace lodge {
 constexpr int OS_THREADS = 256;
 constexpr int OS_WSTRIDE = 257;  // per-warp digit counters (+1 bucket for invalid items)
 
-// Lanes holding the same 9-bit digit (bit 8 marks invalid items), from nine
+// Lanes holding the same digit d (d = 256 marks invalid items) from nb + 1
 // ballots: cheaper than MATCH.ANY, whose latency dominated the ranking.
-__device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d, int nb) {
   uint32_t peers = FULL_MASK;
 #pragma unroll
-  for (int b = 0; b < 9; ++b) {
-    const bool bit = (d >> b) & 1u;
-    const uint32_t bal = __ballot_sync(FULL_MASK, bit);
-    peers &= bit ? bal : ~bal;
+  for (int b = 0; b < 8; ++b) {
+    if (b < nb) {
+      const bool bit = (d >> b) & 1u;
+      const uint32_t bal = __ballot_sync(FULL_MASK, bit);
+      peers &= bit ? bal : ~bal;
+    }
   }
-  return peers;
+  const bool inv = d >> 8;
+  const uint32_t bal = __ballot_sync(FULL_MASK, inv);
+  return peers & (inv ? bal : ~bal);
 }
 
-template <int ITEMS, bool VALS>
+template <int ITEMS, bool VALS, typename KI = uint64_t>
 struct OSmem {
-  uint64_t keys[OS_THREADS * ITEMS];
+  KI keys[OS_THREADS * ITEMS];
   uint32_t vals[VALS ? OS_THREADS * ITEMS : 1];
   uint32_t whist[2][OS_THREADS / 32][OS_WSTRIDE];  // two ranking chains per warp
   uint32_t dstart[256];
@@ -39,13 +45,13 @@ struct OSmem {
 // vmask marks valid items; cnt_valid = number of valid elements, which are
 // the partition's first cnt_valid.  Writes keys (and vget(li) values) to
 // their digit-sorted global positions digit_off[d] + prefix + local rank.
-template <int ITEMS, bool VALS, typename VGet>
-__device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS> &S, uint64_t (&k)[ITEMS],
+template <int ITEMS, bool VALS, typename KI, typename KO, typename KMap, typename VGet>
+__device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI> &S, KI (&k)[ITEMS],
                                                    uint32_t vmask, uint32_t part,
-                                                   uint32_t cnt_valid, int shift,
+                                                   uint32_t cnt_valid, int shift, int nb,
                                                    const uint32_t *__restrict__ digit_off,
                                                    uint64_t *status, uint32_t epoch,
-                                                   uint64_t *__restrict__ kout,
+                                                   KO *__restrict__ kout, KMap kmap,
                                                    uint32_t *__restrict__ vout, VGet vget) {
   static_assert(ITEMS % 2 == 0, "two ranking chains");
   constexpr int H = ITEMS / 2;
@@ -58,8 +64,8 @@ __device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS> &S, uint64
   for (int i = 0; i < H; ++i) {
     const uint32_t d0 = ((vmask >> i) & 1u) ? (uint32_t)((k[i] >> shift) & 255u) : 256u;
     const uint32_t d1 = ((vmask >> (i + H)) & 1u) ? (uint32_t)((k[i + H] >> shift) & 255u) : 256u;
-    const uint32_t p0 = digit_peers(d0);
-    const uint32_t p1 = digit_peers(d1);
+    const uint32_t p0 = digit_peers(d0, nb);
+    const uint32_t p1 = digit_peers(d1, nb);
     const uint32_t c0 = wh0[d0], c1 = wh1[d1];
     const uint32_t lt = lanemask_lt();
     __syncwarp();
@@ -135,10 +141,10 @@ __device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS> &S, uint64
   }
   __syncthreads();
   for (uint32_t j = tid; j < cnt_valid; j += OS_THREADS) {
-    const uint64_t key = S.keys[j];
+    const KI key = S.keys[j];
     const uint32_t dd = (uint32_t)((key >> shift) & 255u);
     const uint32_t out = S.gbase[dd] + (j - S.dstart[dd]);
-    kout[out] = key;
+    kout[out] = kmap(key);
     if (VALS) vout[out] = S.vals[j];
   }
 }
