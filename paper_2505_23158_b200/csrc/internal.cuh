@@ -35,16 +35,20 @@ enum Ticket {
 };
 
 // Splat payload for compositing (64 B, one per survivor).  mean2d is kept in
-// fp64 so the tile-local fp32 offset is exact to fp32 rounding; q_eff is the
-// per-splat cut-off on the quadratic form that encodes both q > 9 and
-// alpha < alpha_min, tol its fp32 error bound (guard band).
+// fp64 so the tile-local fp32 offset is exact to fp32 rounding.  The fp32
+// conic is stored in exponent units: qs = KQ * q with KQ = -log2(e)/2, so a
+// pixel's alpha is exp2(qs + log2 o) with no per-pixel scaling.  q_eff, the
+// per-splat cut-off on q that encodes both q > 9 and alpha < alpha_min, and
+// tol, the fp32 error bound of q near it, become the guard band [lo, hi] on
+// qs: qs > hi keeps for certain, lo <= qs <= hi is re-decided in fp64.
+constexpr double KQ = -0.72134752044448170;  // -0.5 / ln 2
 struct __align__(16) Payload {
   double mx, my;
-  float A, B2, C, o;    // conic (A, 2B, C), effective opacity
-  float r, g, b;        // colour
-  uint32_t src;         // concatenated input index
-  float q_eff, tol;
-  float bx, by;         // half-widths of a box containing every pixel that can be non-skipped
+  float As, B2s, Cs, lo2;  // KQ * (A, 2B, C), log2 of the effective opacity
+  float r, g, b;           // colour
+  uint32_t src;            // concatenated input index
+  float hi, lo;            // guard band on qs (hi rounded up, lo rounded down)
+  float bx, by;            // half-widths of a box containing every pixel that can be non-skipped
 };
 static_assert(sizeof(Payload) == 64, "payload must be 64 B");
 

@@ -63,23 +63,25 @@ __device__ __forceinline__ bool ref_decide(double gx, double gy, double mx, doub
 // Can the ellipse {q <= cut} reach a pixel centre in [xlo,xhi] x [ylo,yhi]
 // (tile-local)?  Exact minimum of the convex quadratic form over the
 // rectangle (interior, else the four edges), with a margin for fp32 rounding.
+// In the scaled form qs = KQ * q (KQ < 0) the minimum of q is the maximum of
+// qs; the extremal points do not depend on the scale.
 __device__ __forceinline__ bool ellipse_meets_block(float mx, float my, float A, float B2, float C,
-                                                    float cut, float tol, float xlo, float xhi,
-                                                    float ylo, float yhi) {
-  if (!(cut > -INFINITY)) return false;
+                                                    float lo, float xlo, float xhi, float ylo,
+                                                    float yhi) {
+  if (!(lo < INFINITY)) return false;
   if (mx >= xlo && mx <= xhi && my >= ylo && my <= yhi) return true;
   const float ex0 = xlo - mx, ex1 = xhi - mx, ey0 = ylo - my, ey1 = yhi - my;
-  float qmin = INFINITY;
+  float qmax = -INFINITY;
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
-    const float dx = s ? ex1 : ex0;  // vertical edge: minimise over dy
+    const float dx = s ? ex1 : ex0;  // vertical edge: extremise over dy
     const float dy = fminf(fmaxf(-B2 * dx / (2.f * C), ey0), ey1);
-    qmin = fminf(qmin, A * dx * dx + B2 * dx * dy + C * dy * dy);
-    const float dy2 = s ? ey1 : ey0;  // horizontal edge: minimise over dx
+    qmax = fmaxf(qmax, A * dx * dx + B2 * dx * dy + C * dy * dy);
+    const float dy2 = s ? ey1 : ey0;  // horizontal edge: extremise over dx
     const float dx2 = fminf(fmaxf(-B2 * dy2 / (2.f * A), ex0), ex1);
-    qmin = fminf(qmin, A * dx2 * dx2 + B2 * dx2 * dy2 + C * dy2 * dy2);
+    qmax = fmaxf(qmax, A * dx2 * dx2 + B2 * dx2 * dy2 + C * dy2 * dy2);
   }
-  return !(qmin > cut + tol + 1e-3f * (1.f + fabsf(cut)));  // NaN -> meets
+  return !(qmax < lo - 1e-3f * (1.f + fabsf(lo)));  // NaN -> meets
 }
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
@@ -206,6 +208,19 @@ __global__ void __launch_bounds__(CC<EXACT>::CT) k_composite(
       ir[p] = ig[p] = ib[p] = br[p] = bg[p] = bb[p] = 0.0;
     }
   }
+  // FAST tracks liveness in T itself (T >= t_min); out-of-image pixels never live
+  if (!EXACT) {
+#pragma unroll
+    for (int p = 0; p < PX; ++p)
+      if (!((alive >> p) & 1u)) T[p] = -INFINITY;
+  }
+  auto live_any = [&]() -> bool {
+    if (EXACT) return alive != 0u;
+    float m = T[0];
+#pragma unroll
+    for (int p = 1; p < PX; ++p) m = fmaxf(m, T[p]);
+    return m >= cpar.tmin_f;
+  };
   uint32_t guard = 0;
 #ifdef LODGE_COUNTERS
   unsigned long long c_list = 0, c_iter = 0, c_hit = 0, c_px = 0, c_batch = 0;
@@ -252,7 +267,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT) k_composite(
     // per-warp member list: members whose ellipse can reach a pixel centre
     uint8_t *wl = S.wlist + warp * CB;
     int cnt = 0;
-    if (__any_sync(FULL_MASK, alive != 0u)) {
+    if (__any_sync(FULL_MASK, live_any())) {
       for (int q0 = 0; q0 < n; q0 += 32) {
         const int j = q0 + lane;
         bool hit = false;
@@ -269,8 +284,8 @@ __global__ void __launch_bounds__(CC<EXACT>::CT) k_composite(
           }
           hit = !(mxl + pj.bx < wx_lo || mxl - pj.bx > wx_hi || myl + pj.by < wy_lo ||
                   myl - pj.by > wy_hi) &&
-                ellipse_meets_block(mxl, myl, pj.A, pj.B2, pj.C, pj.q_eff, pj.tol, wx_lo, wx_hi,
-                                    wy_lo, wy_hi);
+                ellipse_meets_block(mxl, myl, pj.As, pj.B2s, pj.Cs, pj.lo, wx_lo, wx_hi, wy_lo,
+                                    wy_hi);
         }
         const uint32_t hm = __ballot_sync(FULL_MASK, hit);
         if (hit) wl[cnt + __popc(hm & lanemask_lt())] = (uint8_t)j;
@@ -283,7 +298,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT) k_composite(
     c_batch += 1;
 #endif
     for (int i = 0; i < cnt; ++i) {
-      if (!__any_sync(FULL_MASK, alive != 0u)) break;
+      if (!__any_sync(FULL_MASK, live_any())) break;
 #ifdef LODGE_COUNTERS
       c_iter += 1;
 #endif
@@ -320,66 +335,75 @@ __global__ void __launch_bounds__(CC<EXACT>::CT) k_composite(
           if (lane == 0 && wb) atomicMax(&S.maxw[j], wb);
         }
       } else {
+        // qs = KQ * q in exponent units: keep iff qs > hi (and the pixel is
+        // alive: T >= t_min, out-of-image pixels hold T = -1), re-decide in
+        // fp64 iff lo <= qs <= hi, alpha = min(exp2(qs + log2 o), clamp)
         const float2 mm = reinterpret_cast<const float2 *>(&pj.mx)[0];
-        const float4 cn = *reinterpret_cast<const float4 *>(&pj.A);    // A, 2B, C, o
-        const float2 qt = *reinterpret_cast<const float2 *>(&pj.q_eff);  // q_eff, tol
+        const float4 cn = *reinterpret_cast<const float4 *>(&pj.As);  // KQ*(A, 2B, C), log2 o
+        const float2 band = *reinterpret_cast<const float2 *>(&pj.hi);
         const float dx = fpx - mm.x;
         const float adx2 = cn.x * dx * dx, bdx = cn.y * dx;
-        float q[PX], a[PX];
-        uint32_t keep = 0, inb = 0;
+        float qs[PX];
+        bool near = false;
 #pragma unroll
         for (int p = 0; p < PX; ++p) {
           const float dy = (fpy0 + 2.f * p) - mm.y;
-          q[p] = fmaf(dy, fmaf(cn.z, dy, bdx), adx2);
-          const float d = q[p] - qt.x;
-          keep |= (d < -qt.y) ? (1u << p) : 0u;
-          inb |= (fabsf(d) <= qt.y) ? (1u << p) : 0u;
-          a[p] = fminf(cn.w * ex2_approx(fmaxf(q[p], 0.f) * -0.72134752044448170f),
-                       cpar.clamp_f);
+          qs[p] = fmaf(dy, fmaf(cn.z, dy, bdx), adx2);
+          near |= T[p] >= cpar.tmin_f && qs[p] >= band.y && !(qs[p] > band.x);
         }
-        keep &= alive;
-        inb &= alive;
-#ifdef LODGE_COUNTERS
-        {
-          const uint32_t h = (keep | inb);
-          c_hit += __any_sync(FULL_MASK, h != 0u) ? 1 : 0;
-          c_px += __popc(h);
-        }
-#endif
-        if (__any_sync(FULL_MASK, inb != 0u)) {
-          // guard band: re-decide in fp64 with the reference's op order (rare)
-          if (inb) {
-            const uint32_t m = S.m[k][j];
-            const Payload pg = payload[m];
-            const Precise pr = precise[m];
-#pragma unroll
-            for (int p = 0; p < PX; ++p) {
-              if ((inb >> p) & 1u) {
-                double ad;
-                if (!ref_decide(gx, gy0 + 2.0 * p, pg.mx, pg.my, pr, rp, ad)) keep |= 1u << p;
-                a[p] = (float)ad;
-                ++guard;
-              }
-            }
-          }
-        }
-        float wmax = 0.f;
         float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
         if (need_image) c = *reinterpret_cast<const float4 *>(&pj.r);
-#pragma unroll
-        for (int p = 0; p < PX; ++p) {
-          const bool kp = (keep >> p) & 1u;
-          const float w = kp ? T[p] * a[p] : 0.f;
+        float wmax = 0.f;
+        // one pixel's blend step; kept: T >= t_min and not skipped
+        auto blend = [&](int p, bool kept, float a) {
+          const float w = kept ? T[p] * a : 0.f;
           if (need_image) {
             cr[p] = fmaf(w, c.x, cr[p]);
             cg[p] = fmaf(w, c.y, cg[p]);
             cb[p] = fmaf(w, c.z, cb[p]);
           }
-          T[p] = kp ? T[p] * (1.f - a[p]) : T[p];
-          vis[p] += kp ? 1 : 0;
-          if (!(T[p] >= cpar.tmin_f)) alive &= ~(1u << p);
+          T[p] -= w;
+          vis[p] += kept ? 1 : 0;
           wmax = fmaxf(wmax, w);
+#ifdef LODGE_COUNTERS
+          c_px += kept ? 1 : 0;
+#endif
+        };
+        if (!__any_sync(FULL_MASK, near)) {
+          // common case: every decision is certain in fp32, predicates only
+#pragma unroll
+          for (int p = 0; p < PX; ++p)
+            blend(p, T[p] >= cpar.tmin_f && qs[p] > band.x,
+                  fminf(ex2_approx(qs[p] + cn.w), cpar.clamp_f));
+        } else {
+          // guard band: re-decide in fp64 with the reference's op order (rare)
+          bool kp[PX];
+          float a[PX];
+#pragma unroll
+          for (int p = 0; p < PX; ++p) {
+            kp[p] = T[p] >= cpar.tmin_f && qs[p] > band.x;
+            a[p] = fminf(ex2_approx(qs[p] + cn.w), cpar.clamp_f);
+          }
+          if (near) {
+            const uint32_t m = S.m[k][j];
+            const Payload pg = payload[m];
+            const Precise pr = precise[m];
+#pragma unroll
+            for (int p = 0; p < PX; ++p) {
+              if (T[p] >= cpar.tmin_f && qs[p] >= band.y && !(qs[p] > band.x)) {
+                double ad;
+                kp[p] = !ref_decide(gx, gy0 + 2.0 * p, pg.mx, pg.my, pr, rp, ad);
+                a[p] = (float)ad;
+                ++guard;
+              }
+            }
+          }
+#pragma unroll
+          for (int p = 0; p < PX; ++p) blend(p, kp[p], a[p]);
         }
+#ifdef LODGE_COUNTERS
+        c_hit += __any_sync(FULL_MASK, wmax > 0.f || near) ? 1 : 0;
+#endif
         if (record_max) {
           const unsigned wb = __reduce_max_sync(FULL_MASK, __float_as_uint(wmax));
           if (lane == 0 && wb) atomicMax(&S.maxw32[j], wb);
@@ -402,7 +426,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT) k_composite(
       }
     }
     // also the WAR barrier: buffer k is re-filled by the next-but-one issue
-    if (__syncthreads_count(alive != 0u) == 0) {
+    if (__syncthreads_count(live_any()) == 0) {
       if (b + CB < e) {  // drain the stage already in flight before exiting
         if (k == 0) mbar_wait(&S.bar[1], phase1);
         else mbar_wait(&S.bar[0], phase0);

@@ -300,7 +300,8 @@ __device__ __forceinline__ void eval_sh_dev_scalar(const ST *__restrict__ k, int
 
 // Compositing payload from fp64 batch values (shared by K2 and the compat
 // import).  q_eff folds both skip tests of src/raster.py:356 into one cut-off
-// on q; tol bounds |q_fp32 - q_fp64| near that cut-off.
+// on q; tol bounds |q_fp32 - q_fp64| near that cut-off; both
+// are stored as the scaled guard band [lo, hi] (internal.cuh Payload).
 __device__ __forceinline__ void make_payload(double mx, double my, double A, double B, double C,
                                              double o, const double rgb[3], uint32_t src,
                                              double ex, double ey,
@@ -308,10 +309,10 @@ __device__ __forceinline__ void make_payload(double mx, double my, double A, dou
                                              Precise &pr) {
   pl.mx = mx;
   pl.my = my;
-  pl.A = (float)A;
-  pl.B2 = (float)(2.0 * B);
-  pl.C = (float)C;
-  pl.o = (float)o;
+  pl.As = (float)(KQ * A);
+  pl.B2s = (float)(KQ * (2.0 * B));
+  pl.Cs = (float)(KQ * C);
+  pl.lo2 = (float)log2(o);
   pl.r = (float)rgb[0];
   pl.g = (float)rgb[1];
   pl.b = (float)rgb[2];
@@ -331,8 +332,10 @@ __device__ __forceinline__ void make_payload(double mx, double my, double A, dou
     const double cond = lmax / lmin;
     tol = 5.96e-8 * (48.0 * cond * qr + 96.0 * sqrt(lmax * cond * qr) + 4.0 * qr) + 1e-9 * qr;
   }
-  pl.q_eff = (float)q_eff;
-  pl.tol = (float)tol;
+  // the scaled coefficients carry one rounding each, like (float)A did, so
+  // |qs_fp32 - KQ * q_fp64| <= |KQ| * tol; KQ < 0 flips the band
+  pl.hi = __double2float_ru(KQ * (q_eff - tol));
+  pl.lo = __double2float_rd(KQ * (q_eff + tol));
   // {q <= Q} lies in |dx| <= sqrt(Q/9) * ex, |dy| <= sqrt(Q/9) * ey (ex = 3 sqrt(cov00));
   // Q = q_eff + tol bounds every pixel the fp64 reference may keep.  Generous
   // relative/absolute margins cover the rounding of cov2d and of the bounds.
