@@ -363,19 +363,22 @@ __global__ void __launch_bounds__(CC<EXACT>::CT) k_composite(
             cb[p] = fmaf(w, c.z, cb[p]);
           }
           T[p] -= w;
-          vis[p] += kept ? 1 : 0;
+          if (kept) ++vis[p];
           wmax = fmaxf(wmax, w);
 #ifdef LODGE_COUNTERS
           c_px += kept ? 1 : 0;
 #endif
         };
-        if (!__any_sync(FULL_MASK, near)) {
-          // common case: every decision is certain in fp32, predicates only
-#pragma unroll
-          for (int p = 0; p < PX; ++p)
-            blend(p, T[p] >= cpar.tmin_f && qs[p] > band.x,
-                  fminf(ex2_approx(qs[p] + cn.w), cpar.clamp_f));
-        } else {
+        auto finish = [&]() {
+#ifdef LODGE_COUNTERS
+          c_hit += __any_sync(FULL_MASK, wmax > 0.f || near) ? 1 : 0;
+#endif
+          if (record_max) {
+            const unsigned wb = __reduce_max_sync(FULL_MASK, __float_as_uint(wmax));
+            if (lane == 0 && wb) atomicMax(&S.maxw32[j], wb);
+          }
+        };
+        if (__any_sync(FULL_MASK, near)) {
           // guard band: re-decide in fp64 with the reference's op order (rare)
           bool kp[PX];
           float a[PX];
@@ -400,14 +403,36 @@ __global__ void __launch_bounds__(CC<EXACT>::CT) k_composite(
           }
 #pragma unroll
           for (int p = 0; p < PX; ++p) blend(p, kp[p], a[p]);
+          finish();
+          continue;
         }
+        // common case: every decision is certain in fp32.  One PTX block per
+        // pixel keeps the keep test a predicate (nvcc otherwise materialises
+        // the count increment as a select and a copy).
+#pragma unroll
+        for (int p = 0; p < PX; ++p) {
+          const float a = fminf(ex2_approx(qs[p] + cn.w), cpar.clamp_f);
+          float w;
+          asm("{\n\t.reg .pred k;\n\t"
+              "setp.ge.f32 k, %2, %4;\n\t"
+              "setp.gt.and.f32 k, %3, %5, k;\n\t"
+              "mul.rn.f32 %0, %2, %6;\n\t"
+              "selp.f32 %0, %0, 0f00000000, k;\n\t"
+              "@k add.s32 %1, %1, 1;\n\t}"
+              : "=f"(w), "+r"(vis[p])
+              : "f"(T[p]), "f"(qs[p]), "f"(cpar.tmin_f), "f"(band.x), "f"(a));
+          if (need_image) {
+            cr[p] = fmaf(w, c.x, cr[p]);
+            cg[p] = fmaf(w, c.y, cg[p]);
+            cb[p] = fmaf(w, c.z, cb[p]);
+          }
+          T[p] -= w;
+          wmax = fmaxf(wmax, w);
 #ifdef LODGE_COUNTERS
-        c_hit += __any_sync(FULL_MASK, wmax > 0.f || near) ? 1 : 0;
+          c_px += (w > 0.f) ? 1 : 0;
 #endif
-        if (record_max) {
-          const unsigned wb = __reduce_max_sync(FULL_MASK, __float_as_uint(wmax));
-          if (lane == 0 && wb) atomicMax(&S.maxw32[j], wb);
         }
+        finish();
       }
     }
     __syncthreads();
