@@ -87,6 +87,11 @@ __device__ __forceinline__ bool ellipse_meets_block(float mx, float my, float A,
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
 }
@@ -133,7 +138,10 @@ struct CompParams {
 };
 
 template <bool EXACT>
-__global__ void __launch_bounds__(CC<EXACT>::CT) k_composite(
+#ifndef LODGE_COMP_MINB
+#define LODGE_COMP_MINB 1
+#endif
+__global__ void __launch_bounds__(CC<EXACT>::CT, LODGE_COMP_MINB) k_composite(
     const uint32_t *__restrict__ list, const uint32_t *__restrict__ tile_start,
     const uint32_t *__restrict__ tile_order, const Payload *__restrict__ payload,
     const Precise *__restrict__ precise, FrameState *fs, const CompParams cpar, void *image,
@@ -255,8 +263,19 @@ __global__ void __launch_bounds__(CC<EXACT>::CT) k_composite(
       if (j < n) {
         Payload &pj = PL[j];
         if (!EXACT) {
+          // (mx, my, mid, half): the guard band [lo, hi] as a centre and a
+          // half-width that covers it after rounding, so the per-pixel near
+          // test is |qs - mid| <= half (half = inf: always near; -1: never)
           const float mxl = (float)(pj.mx - ox), myl = (float)(pj.my - oy);
-          reinterpret_cast<float2 *>(&pj.mx)[0] = make_float2(mxl, myl);
+          const float hi = pj.hi, lo = pj.lo;
+          float mid = 0.f, half = -1.f;
+          if (lo <= hi && fabsf(lo) < INFINITY && fabsf(hi) < INFINITY) {
+            mid = 0.5f * (lo + hi);
+            half = fmaxf(__fsub_ru(hi, mid), __fsub_ru(mid, lo));
+          } else if (lo < INFINITY) {
+            half = INFINITY;
+          }
+          reinterpret_cast<float4 *>(&pj.mx)[0] = make_float4(mxl, myl, mid, half);
           S.maxw32[j] = 0u;
         } else {
           S.maxw[j] = 0ull;
@@ -266,6 +285,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT) k_composite(
     __syncthreads();
     // per-warp member list: members whose ellipse can reach a pixel centre
     uint8_t *wl = S.wlist + warp * CB;
+    const uint32_t wl_sa = smem_addr(wl);  // read back with 32-bit shared addressing
     int cnt = 0;
     if (__any_sync(FULL_MASK, live_any())) {
       for (int q0 = 0; q0 < n; q0 += 32) {
@@ -302,7 +322,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT) k_composite(
 #ifdef LODGE_COUNTERS
       c_iter += 1;
 #endif
-      const int j = wl[i];
+      const int j = lds_u8(wl_sa + (uint32_t)i);
       const Payload &pj = PL[j];
       if (EXACT) {
         const Precise &d = S.pr[k][j];
@@ -338,18 +358,18 @@ __global__ void __launch_bounds__(CC<EXACT>::CT) k_composite(
         // qs = KQ * q in exponent units: keep iff qs > hi (and the pixel is
         // alive: T >= t_min, out-of-image pixels hold T = -1), re-decide in
         // fp64 iff lo <= qs <= hi, alpha = min(exp2(qs + log2 o), clamp)
-        const float2 mm = reinterpret_cast<const float2 *>(&pj.mx)[0];
+        const float4 mm = reinterpret_cast<const float4 *>(&pj.mx)[0];  // mx, my, mid, half
         const float4 cn = *reinterpret_cast<const float4 *>(&pj.As);  // KQ*(A, 2B, C), log2 o
         const float2 band = *reinterpret_cast<const float2 *>(&pj.hi);
         const float dx = fpx - mm.x;
         const float adx2 = cn.x * dx * dx, bdx = cn.y * dx;
         float qs[PX];
-        bool near = false;
+        bool near = false;  // dead pixels may vote too; the fp64 path re-checks
 #pragma unroll
         for (int p = 0; p < PX; ++p) {
           const float dy = (fpy0 + 2.f * p) - mm.y;
           qs[p] = fmaf(dy, fmaf(cn.z, dy, bdx), adx2);
-          near |= T[p] >= cpar.tmin_f && qs[p] >= band.y && !(qs[p] > band.x);
+          near |= fabsf(qs[p] - mm.z) <= mm.w;
         }
         float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
         if (need_image) c = *reinterpret_cast<const float4 *>(&pj.r);
