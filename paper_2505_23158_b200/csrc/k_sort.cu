@@ -24,10 +24,10 @@ constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096 keys per partition
 // Key maps applied at the scatter (see launch_tile_sort).
 enum : int { MAP_ID = 0, MAP_PACK = 1, MAP_LOW = 2 };
 
-template <bool VALS, typename KI, typename KO, int MAP>
+template <bool VALS, typename KI, typename KO, int MAP, int NB = 8>
 __global__ void __launch_bounds__(OS_THREADS, VALS ? 2 : 3) k_onesweep(
     const KI *__restrict__ kin, KO *__restrict__ kout, const uint32_t *__restrict__ vin,
-    uint32_t *__restrict__ vout, const uint32_t *n_ptr, int shift, int nb, int sb,
+    uint32_t *__restrict__ vout, const uint32_t *n_ptr, int shift, int sb,
     const uint32_t *__restrict__ digit_off, uint64_t *status, FrameState *fs, int tk) {
   extern __shared__ __align__(16) uint8_t smem[];
   OSmem<OS_ITEMS, VALS, KI> &S = *reinterpret_cast<OSmem<OS_ITEMS, VALS, KI> *>(smem);
@@ -56,8 +56,8 @@ __global__ void __launch_bounds__(OS_THREADS, VALS ? 2 : 3) k_onesweep(
     else
       return (KO)key;
   };
-  onesweep_partition<OS_ITEMS, VALS>(S, k, vmask, part, min((uint32_t)OS_TILE, n - base), shift,
-                                     nb, digit_off, status, fs->epoch + tk, kout, kmap, vout,
+  onesweep_partition<OS_ITEMS, NB, VALS>(S, k, vmask, part, min((uint32_t)OS_TILE, n - base),
+                                         shift, digit_off, status, fs->epoch + tk, kout, kmap, vout,
                                      [&](uint32_t li) { return vin[base + li]; });
 }
 
@@ -97,16 +97,32 @@ __global__ void k_depth_scan(FrameState *fs) {
   }
 }
 
-template <bool VALS, typename KI, typename KO, int MAP>
-static size_t os_kernel_smem() {
+// One onesweep pass (dynamic shared memory opted in once per instantiation).
+template <bool VALS, typename KI, typename KO, int MAP, int NB>
+static void os_launch(unsigned grid, cudaStream_t s, const KI *kin, KO *kout, const uint32_t *vin,
+                      uint32_t *vout, const uint32_t *n_ptr, int shift, int sb,
+                      const uint32_t *digit_off, uint64_t *status, FrameState *fs, int tk) {
   static bool done = false;
   const size_t sm = sizeof(OSmem<OS_ITEMS, VALS, KI>);
   if (!done) {
-    cudaFuncSetAttribute(k_onesweep<VALS, KI, KO, MAP>,
+    cudaFuncSetAttribute(k_onesweep<VALS, KI, KO, MAP, NB>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     done = true;
   }
-  return sm;
+  k_onesweep<VALS, KI, KO, MAP, NB><<<grid, OS_THREADS, sm, s>>>(
+      kin, kout, vin, vout, n_ptr, shift, sb, digit_off, status, fs, tk);
+}
+
+// Same, with the digit width chosen at run time (nb <= 4 ranks on 4 bits).
+template <bool VALS, typename KI, typename KO, int MAP, typename... A>
+static void os_launch_nb(int nb, A... args) {
+  switch (nb) {
+    case 5: os_launch<VALS, KI, KO, MAP, 5>(args...); break;
+    case 6: os_launch<VALS, KI, KO, MAP, 6>(args...); break;
+    case 7: os_launch<VALS, KI, KO, MAP, 7>(args...); break;
+    case 8: os_launch<VALS, KI, KO, MAP, 8>(args...); break;
+    default: os_launch<VALS, KI, KO, MAP, 4>(args...); break;
+  }
 }
 
 void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
@@ -118,12 +134,12 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
   k_depth_scan<<<1, 256, 0, s>>>(fs);
   *launches += 2;
   const unsigned grid = (unsigned)((M_cap + OS_TILE - 1) / OS_TILE);
-  const size_t sm = os_kernel_smem<true, uint64_t, uint64_t, MAP_ID>();
   for (int p = 0; p < 8; ++p) {
     const int a = p & 1;
-    k_onesweep<true, uint64_t, uint64_t, MAP_ID><<<grid, OS_THREADS, sm, s>>>(
-        w.key_depth[a], w.key_depth[a ^ 1], w.val_depth[a], w.val_depth[a ^ 1], &fs->n_sort,
-        8 * p, 8, 32, fs->off_depth[p], w.status, fs, TK_DEPTH0 + p);
+    os_launch<true, uint64_t, uint64_t, MAP_ID, 8>(
+        grid, s, (const uint64_t *)w.key_depth[a], w.key_depth[a ^ 1],
+        (const uint32_t *)w.val_depth[a], w.val_depth[a ^ 1], &fs->n_sort, 8 * p, 32,
+        fs->off_depth[p], w.status, fs, TK_DEPTH0 + p);
     ++*launches;
   }
 }
@@ -149,11 +165,14 @@ void launch_tile_sort(Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
   const int lo_bits = std::min(8, std::max(1, bit_width(T - 1)));
   uint32_t *u32_1 = reinterpret_cast<uint32_t *>(w.pairs[1]);
   uint32_t *u32_0 = reinterpret_cast<uint32_t *>(w.pairs[0]);
+  const uint32_t *nin = &fs->n_pairs;
+  const uint32_t *no_v = nullptr;
+  uint32_t *no_vo = nullptr;
+  const uint64_t *p0 = w.pairs[0];
   if (T <= 256) {
-    const size_t sm = os_kernel_smem<false, uint64_t, uint32_t, MAP_LOW>();
-    k_onesweep<false, uint64_t, uint32_t, MAP_LOW><<<grid, OS_THREADS, sm, s>>>(
-        w.pairs[0], u32_1, nullptr, nullptr, &fs->n_pairs, 32, lo_bits, 32, fs->off_tile[0],
-        w.status, fs, TK_TILE0);
+    os_launch_nb<false, uint64_t, uint32_t, MAP_LOW>(lo_bits, grid, s, p0, u32_1, no_v, no_vo,
+                                                     nin, 32, 32, (const uint32_t *)fs->off_tile[0],
+                                                     w.status, fs, (int)TK_TILE0);
     ++*launches;
     w.list = u32_1;
     return;
@@ -161,23 +180,17 @@ void launch_tile_sort(Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
   const int hi_bits = bit_width((T - 1) >> 8);
   const int sb = std::max(1, bit_width((uint64_t)std::max<int64_t>(w.M_cap, 1) - 1));
   if (hi_bits + sb <= 32) {
-    const size_t sm1 = os_kernel_smem<false, uint64_t, uint32_t, MAP_PACK>();
-    k_onesweep<false, uint64_t, uint32_t, MAP_PACK><<<grid, OS_THREADS, sm1, s>>>(
-        w.pairs[0], u32_1, nullptr, nullptr, &fs->n_pairs, 32, 8, sb, fs->off_tile[0], w.status,
-        fs, TK_TILE0);
-    const size_t sm2 = os_kernel_smem<false, uint32_t, uint32_t, MAP_LOW>();
-    k_onesweep<false, uint32_t, uint32_t, MAP_LOW><<<grid, OS_THREADS, sm2, s>>>(
-        u32_1, u32_0, nullptr, nullptr, &fs->n_pairs, sb, hi_bits, sb, fs->off_tile[1], w.status,
-        fs, TK_TILE0 + 1);
+    os_launch<false, uint64_t, uint32_t, MAP_PACK, 8>(grid, s, p0, u32_1, no_v, no_vo, nin, 32, sb,
+                                                      fs->off_tile[0], w.status, fs, TK_TILE0);
+    os_launch_nb<false, uint32_t, uint32_t, MAP_LOW>(
+        hi_bits, grid, s, (const uint32_t *)u32_1, u32_0, no_v, no_vo, nin, sb, sb,
+        (const uint32_t *)fs->off_tile[1], w.status, fs, (int)TK_TILE0 + 1);
   } else {
-    const size_t sm1 = os_kernel_smem<false, uint64_t, uint64_t, MAP_ID>();
-    k_onesweep<false, uint64_t, uint64_t, MAP_ID><<<grid, OS_THREADS, sm1, s>>>(
-        w.pairs[0], w.pairs[1], nullptr, nullptr, &fs->n_pairs, 32, 8, 32, fs->off_tile[0],
-        w.status, fs, TK_TILE0);
-    const size_t sm2 = os_kernel_smem<false, uint64_t, uint32_t, MAP_LOW>();
-    k_onesweep<false, uint64_t, uint32_t, MAP_LOW><<<grid, OS_THREADS, sm2, s>>>(
-        w.pairs[1], u32_0, nullptr, nullptr, &fs->n_pairs, 40, hi_bits, 32, fs->off_tile[1],
-        w.status, fs, TK_TILE0 + 1);
+    os_launch<false, uint64_t, uint64_t, MAP_ID, 8>(grid, s, p0, w.pairs[1], no_v, no_vo, nin, 32,
+                                                    32, fs->off_tile[0], w.status, fs, TK_TILE0);
+    os_launch_nb<false, uint64_t, uint32_t, MAP_LOW>(
+        hi_bits, grid, s, (const uint64_t *)w.pairs[1], u32_0, no_v, no_vo, nin, 40, 32,
+        (const uint32_t *)fs->off_tile[1], w.status, fs, (int)TK_TILE0 + 1);
   }
   *launches += 2;
   w.list = u32_0;

@@ -3,6 +3,8 @@
 // can be non-zero (fewer ballots per item); the scatter writes kmap(key),
 // which lets a pass narrow the key it hands to the next one.
 #pragma once
+#include <type_traits>
+
 #include "internal.cuh"
 
 namespace lodge {
@@ -10,21 +12,24 @@ namespace lodge {
 constexpr int OS_THREADS = 256;
 constexpr int OS_WSTRIDE = 257;  // per-warp digit counters (+1 bucket for invalid items)
 
-// Lanes holding the same digit d (d = 256 marks invalid items) from nb + 1
-// ballots: cheaper than MATCH.ANY, whose latency dominated the ranking.
-__device__ __forceinline__ uint32_t digit_peers(uint32_t d, int nb) {
+// Lanes holding the same digit d from NB ballots (+1 on bit 8, which marks
+// invalid items, when the partition is ragged): cheaper than MATCH.ANY, whose
+// latency dominated the ranking.
+template <int NB, bool CHECKV>
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
   uint32_t peers = FULL_MASK;
 #pragma unroll
-  for (int b = 0; b < 8; ++b) {
-    if (b < nb) {
-      const bool bit = (d >> b) & 1u;
-      const uint32_t bal = __ballot_sync(FULL_MASK, bit);
-      peers &= bit ? bal : ~bal;
-    }
+  for (int b = 0; b < NB; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const uint32_t bal = __ballot_sync(FULL_MASK, bit);
+    peers &= bit ? bal : ~bal;
   }
-  const bool inv = d >> 8;
-  const uint32_t bal = __ballot_sync(FULL_MASK, inv);
-  return peers & (inv ? bal : ~bal);
+  if (CHECKV) {
+    const bool inv = d >> 8;
+    const uint32_t bal = __ballot_sync(FULL_MASK, inv);
+    peers &= inv ? bal : ~bal;
+  }
+  return peers;
 }
 
 template <int ITEMS, bool VALS, typename KI = uint64_t>
@@ -45,10 +50,10 @@ struct OSmem {
 // vmask marks valid items; cnt_valid = number of valid elements, which are
 // the partition's first cnt_valid.  Writes keys (and vget(li) values) to
 // their digit-sorted global positions digit_off[d] + prefix + local rank.
-template <int ITEMS, bool VALS, typename KI, typename KO, typename KMap, typename VGet>
+template <int ITEMS, int NB, bool VALS, typename KI, typename KO, typename KMap, typename VGet>
 __device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI> &S, KI (&k)[ITEMS],
                                                    uint32_t vmask, uint32_t part,
-                                                   uint32_t cnt_valid, int shift, int nb,
+                                                   uint32_t cnt_valid, int shift,
                                                    const uint32_t *__restrict__ digit_off,
                                                    uint64_t *status, uint32_t epoch,
                                                    KO *__restrict__ kout, KMap kmap,
@@ -60,21 +65,27 @@ __device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI> &S, KI
     (&S.whist[0][0][0])[i] = 0;
   __syncthreads();
   uint32_t *wh0 = S.whist[0][warp], *wh1 = S.whist[1][warp];
+  auto rank_items = [&](auto ragged) {
+    constexpr bool CV = decltype(ragged)::value;
 #pragma unroll
-  for (int i = 0; i < H; ++i) {
-    const uint32_t d0 = ((vmask >> i) & 1u) ? (uint32_t)((k[i] >> shift) & 255u) : 256u;
-    const uint32_t d1 = ((vmask >> (i + H)) & 1u) ? (uint32_t)((k[i + H] >> shift) & 255u) : 256u;
-    const uint32_t p0 = digit_peers(d0, nb);
-    const uint32_t p1 = digit_peers(d1, nb);
-    const uint32_t c0 = wh0[d0], c1 = wh1[d1];
-    const uint32_t lt = lanemask_lt();
-    __syncwarp();
-    if ((p0 & lt) == 0u) wh0[d0] = c0 + __popc(p0);  // lowest peer lane updates
-    if ((p1 & lt) == 0u) wh1[d1] = c1 + __popc(p1);
-    __syncwarp();
-    S.rank[warp * (ITEMS * 32) + i * 32 + lane] = (uint16_t)(c0 + __popc(p0 & lt));
-    S.rank[warp * (ITEMS * 32) + (i + H) * 32 + lane] = (uint16_t)(c1 + __popc(p1 & lt));
-  }
+    for (int i = 0; i < H; ++i) {
+      const uint32_t d0 = (!CV || ((vmask >> i) & 1u)) ? (uint32_t)((k[i] >> shift) & 255u) : 256u;
+      const uint32_t d1 =
+          (!CV || ((vmask >> (i + H)) & 1u)) ? (uint32_t)((k[i + H] >> shift) & 255u) : 256u;
+      const uint32_t p0 = digit_peers<NB, CV>(d0);
+      const uint32_t p1 = digit_peers<NB, CV>(d1);
+      const uint32_t c0 = wh0[d0], c1 = wh1[d1];
+      const uint32_t lt = lanemask_lt();
+      __syncwarp();
+      if ((p0 & lt) == 0u) wh0[d0] = c0 + __popc(p0);  // lowest peer lane updates
+      if ((p1 & lt) == 0u) wh1[d1] = c1 + __popc(p1);
+      __syncwarp();
+      S.rank[warp * (ITEMS * 32) + i * 32 + lane] = (uint16_t)(c0 + __popc(p0 & lt));
+      S.rank[warp * (ITEMS * 32) + (i + H) * 32 + lane] = (uint16_t)(c1 + __popc(p1 & lt));
+    }
+  };
+  if (cnt_valid == (uint32_t)(OS_THREADS * ITEMS)) rank_items(std::false_type{});
+  else rank_items(std::true_type{});
   __syncthreads();
   // per digit: exclusive offsets over (warp, chain) and the partition total
   const uint32_t dg = tid;  // 256 threads == 256 digits
