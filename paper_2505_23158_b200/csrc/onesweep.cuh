@@ -15,20 +15,33 @@ constexpr int OS_WSTRIDE = 257;  // per-warp digit counters (+1 bucket for inval
 // Lanes holding the same digit d from NB ballots (+1 on bit 8, which marks
 // invalid items, when the partition is ragged): cheaper than MATCH.ANY, whose
 // latency dominated the ranking.
+// peers &= lanes whose bit (d & MASK) equals this lane's (bit test, ballot and
+// two predicated ANDs; nvcc's own lowering spends six instructions here).
+template <uint32_t MASK>
+__device__ __forceinline__ void peer_bit(uint32_t &peers, uint32_t d) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t, bal;\n\t"
+      "and.b32 t, %1, %2;\n\t"
+      "setp.ne.u32 p, t, 0;\n\t"
+      "vote.sync.ballot.b32 bal, p, 0xffffffff;\n\t"
+      "@p and.b32 %0, %0, bal;\n\t"
+      "not.b32 bal, bal;\n\t"
+      "@!p and.b32 %0, %0, bal;\n\t}"
+      : "+r"(peers)
+      : "r"(d), "n"(MASK));
+}
+
 template <int NB, bool CHECKV>
 __device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
   uint32_t peers = FULL_MASK;
-#pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    const bool bit = (d >> b) & 1u;
-    const uint32_t bal = __ballot_sync(FULL_MASK, bit);
-    peers &= bit ? bal : ~bal;
-  }
-  if (CHECKV) {
-    const bool inv = d >> 8;
-    const uint32_t bal = __ballot_sync(FULL_MASK, inv);
-    peers &= inv ? bal : ~bal;
-  }
+  if (NB > 0) peer_bit<1u>(peers, d);
+  if (NB > 1) peer_bit<2u>(peers, d);
+  if (NB > 2) peer_bit<4u>(peers, d);
+  if (NB > 3) peer_bit<8u>(peers, d);
+  if (NB > 4) peer_bit<16u>(peers, d);
+  if (NB > 5) peer_bit<32u>(peers, d);
+  if (NB > 6) peer_bit<64u>(peers, d);
+  if (NB > 7) peer_bit<128u>(peers, d);
+  if (CHECKV) peer_bit<256u>(peers, d);
   return peers;
 }
 
