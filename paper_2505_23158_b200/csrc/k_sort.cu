@@ -25,7 +25,10 @@ constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096 keys per partition
 enum : int { MAP_ID = 0, MAP_PACK = 1, MAP_LOW = 2 };
 
 template <bool VALS, typename KI, typename KO, int MAP, int NB = 8>
-__global__ void __launch_bounds__(OS_THREADS, VALS ? 2 : 3) k_onesweep(
+#ifndef LODGE_OS_MINB
+#define LODGE_OS_MINB 3
+#endif
+__global__ void __launch_bounds__(OS_THREADS, VALS ? 2 : LODGE_OS_MINB) k_onesweep(
     const KI *__restrict__ kin, KO *__restrict__ kout, const uint32_t *__restrict__ vin,
     uint32_t *__restrict__ vout, const uint32_t *n_ptr, int shift, int sb,
     const uint32_t *__restrict__ digit_off, uint64_t *status, FrameState *fs, int tk) {
