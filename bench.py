@@ -137,8 +137,9 @@ def stage_bytes(U, AB, M, P, W, H, sh_terms, geom_bytes=48, sh_elem=4):
         "depth_sort": M * (8.0 + 8 * 24.0),
         "tile_setup": 0.0,
         "duplicate": M * 12.0 + P * 8.0,
-        "tile_sort": 2 * 16.0 * P,
-        "composite": P * 8.0 + M * 64.0 + W * H * 16.0 + U * 4.0,
+        # pass 1 reads u64 pairs, writes packed u32; pass 2 reads and writes u32
+        "tile_sort": (8.0 + 4.0 + 4.0 + 4.0) * P,
+        "composite": P * 4.0 + M * 64.0 + W * H * 16.0 + U * 4.0,
     }
 
 
@@ -320,6 +321,24 @@ def run_lodge(args):
     ms = e0.elapsed_time(e1)
     stage_ms, nprof_frames = r.profile_read()
     r.profile(False)
+    stage_timing = "events around each stage on its stream, inside the timed region"
+    if S > 1:
+        # with frames in flight on several streams a stage's events also span
+        # the other streams' kernels: re-time the stages on one stream over
+        # the same views, serialised, right after the timed region
+        n_stage = min(n_timed, 64)
+        r.profile(True, n_stage)
+        k = 0
+        for s in range(args.warmup, args.warmup + args.steps):
+            for j, v in enumerate(schedule[s]):
+                if k < n_stage:
+                    r.render(cams[pos[v]], frames[j], slot=0)
+                k += 1
+        torch.cuda.synchronize()
+        stage_ms, nprof_frames = r.profile_read()
+        r.profile(False)
+        stage_timing = (f"events around each stage, {nprof_frames} of the timed views re-rendered "
+                        "serially on one stream after the timed region")
     stats = read_stats(stats_all)
     overflow = sum(s.overflow for s in stats)
     ms_max = ms
@@ -473,7 +492,8 @@ def run_lodge(args):
                        "pairs_per_s": P * value, "gaussians_per_s": U * value,
                        "overflow_frames": int(overflow), "setup_s": round(setup_s, 1)},
             "e2e": e2e, "gpu_launches": int(launches_per_frame * total_frames),
-            "roofline": roofline, "stages": stages, "cpu_baseline": cpu, "clocks": clk,
+            "roofline": roofline, "stages": stages, "stage_timing": stage_timing,
+            "cpu_baseline": cpu, "clocks": clk,
             "parity_sample": parity, "gathered": gathered_views,
         }
         print(json.dumps(line), flush=True)

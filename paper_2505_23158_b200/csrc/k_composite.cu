@@ -317,53 +317,53 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, LODGE_COMP_MINB) k_composite(
     c_list += cnt;
     c_batch += 1;
 #endif
-    for (int i = 0; i < cnt; ++i) {
-      if (!__any_sync(FULL_MASK, live_any())) break;
+    if (EXACT) {
+      for (int i = 0; i < cnt; ++i) {
+        if (!__any_sync(FULL_MASK, live_any())) break;
 #ifdef LODGE_COUNTERS
-      c_iter += 1;
+        c_iter += 1;
 #endif
-      const int j = lds_u8(wl_sa + (uint32_t)i);
-      const Payload &pj = PL[j];
-      if (EXACT) {
-        const Precise &d = S.pr[k][j];
-        double wmax = 0.0;
-#pragma unroll
-        for (int p = 0; p < PX; ++p) {
-          if (!((alive >> p) & 1u)) continue;
-          double a;
-          const bool sk = ref_decide(gx, gy0 + 2.0 * p, pj.mx, pj.my, d, rp, a);
-          if (sk) a = 0.0;
-          const double before = __dmul_rn(cp[p], tr[p]);
-          cp[p] = __dmul_rn(cp[p], __dsub_rn(1.0, a));
-          const double w = __dmul_rn(before, a);
-          if (need_image) {
-            br[p] = __dadd_rn(br[p], __dmul_rn(w, d.r));
-            bg[p] = __dadd_rn(bg[p], __dmul_rn(w, d.g));
-            bb[p] = __dadd_rn(bb[p], __dmul_rn(w, d.b));
+        const int j = lds_u8(wl_sa + (uint32_t)i);
+        const Payload &pj = PL[j];
+          const Precise &d = S.pr[k][j];
+          double wmax = 0.0;
+  #pragma unroll
+          for (int p = 0; p < PX; ++p) {
+            if (!((alive >> p) & 1u)) continue;
+            double a;
+            const bool sk = ref_decide(gx, gy0 + 2.0 * p, pj.mx, pj.my, d, rp, a);
+            if (sk) a = 0.0;
+            const double before = __dmul_rn(cp[p], tr[p]);
+            cp[p] = __dmul_rn(cp[p], __dsub_rn(1.0, a));
+            const double w = __dmul_rn(before, a);
+            if (need_image) {
+              br[p] = __dadd_rn(br[p], __dmul_rn(w, d.r));
+              bg[p] = __dadd_rn(bg[p], __dmul_rn(w, d.g));
+              bb[p] = __dadd_rn(bb[p], __dmul_rn(w, d.b));
+            }
+            vis[p] += sk ? 0 : 1;
+            if (!(__dmul_rn(cp[p], tr[p]) >= rp.t_min)) alive &= ~(1u << p);
+            wmax = fmax(wmax, w);
           }
-          vis[p] += sk ? 0 : 1;
-          if (!(__dmul_rn(cp[p], tr[p]) >= rp.t_min)) alive &= ~(1u << p);
-          wmax = fmax(wmax, w);
-        }
-        if (record_max) {
-          unsigned long long wb = (unsigned long long)__double_as_longlong(wmax);
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long ob = __shfl_xor_sync(FULL_MASK, wb, o);
-            wb = ob > wb ? ob : wb;
+          if (record_max) {
+            unsigned long long wb = (unsigned long long)__double_as_longlong(wmax);
+  #pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              const unsigned long long ob = __shfl_xor_sync(FULL_MASK, wb, o);
+              wb = ob > wb ? ob : wb;
+            }
+            if (lane == 0 && wb) atomicMax(&S.maxw[j], wb);
           }
-          if (lane == 0 && wb) atomicMax(&S.maxw[j], wb);
-        }
-      } else {
-        // qs = KQ * q in exponent units: keep iff qs > hi (and the pixel is
-        // alive: T >= t_min, out-of-image pixels hold T = -1), re-decide in
-        // fp64 iff lo <= qs <= hi, alpha = min(exp2(qs + log2 o), clamp)
-        const float4 mm = reinterpret_cast<const float4 *>(&pj.mx)[0];  // mx, my, mid, half
-        const float4 cn = *reinterpret_cast<const float4 *>(&pj.As);  // KQ*(A, 2B, C), log2 o
-        const float2 band = *reinterpret_cast<const float2 *>(&pj.hi);
+      }
+    } else {
+      // qs = KQ * q in exponent units: keep iff qs > hi (and the pixel is
+      // alive: T >= t_min; out-of-image pixels hold T = -inf), re-decide in
+      // fp64 iff lo <= qs <= hi, alpha = min(exp2(qs + log2 o), clamp)
+      auto quad = [&](const Payload &pj, float (&qs)[PX], float4 &mm, float4 &cn) -> bool {
+        mm = reinterpret_cast<const float4 *>(&pj.mx)[0];  // mx, my, mid, half
+        cn = *reinterpret_cast<const float4 *>(&pj.As);   // KQ*(A, 2B, C), log2 o
         const float dx = fpx - mm.x;
         const float adx2 = cn.x * dx * dx, bdx = cn.y * dx;
-        float qs[PX];
         bool near = false;  // dead pixels may vote too; the fp64 path re-checks
 #pragma unroll
         for (int p = 0; p < PX; ++p) {
@@ -371,40 +371,65 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, LODGE_COMP_MINB) k_composite(
           qs[p] = fmaf(dy, fmaf(cn.z, dy, bdx), adx2);
           near |= fabsf(qs[p] - mm.z) <= mm.w;
         }
-        float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (need_image) c = *reinterpret_cast<const float4 *>(&pj.r);
+        return near;
+      };
+      auto colour = [&](const Payload &pj) {
+        return need_image ? *reinterpret_cast<const float4 *>(&pj.r)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      };
+      auto finish = [&](int j, float wmax) {
+#ifdef LODGE_COUNTERS
+        c_hit += __any_sync(FULL_MASK, wmax > 0.f) ? 1 : 0;
+#endif
+        if (record_max) {
+          const unsigned wb = __reduce_max_sync(FULL_MASK, __float_as_uint(wmax));
+          if (lane == 0 && wb) atomicMax(&S.maxw32[j], wb);
+        }
+      };
+      // one pixel's blend step with every decision certain in fp32; one PTX
+      // block keeps the keep test a predicate (nvcc otherwise materialises
+      // the count increment as a select and a copy)
+      auto step = [&](int p, float qs, float hi, float a, const float4 &c, float &wmax) {
+        float w;
+        asm("{\n\t.reg .pred k;\n\t"
+            "setp.ge.f32 k, %2, %4;\n\t"
+            "setp.gt.and.f32 k, %3, %5, k;\n\t"
+            "mul.rn.f32 %0, %2, %6;\n\t"
+            "selp.f32 %0, %0, 0f00000000, k;\n\t"
+            "@k add.s32 %1, %1, 1;\n\t}"
+            : "=f"(w), "+r"(vis[p])
+            : "f"(T[p]), "f"(qs), "f"(cpar.tmin_f), "f"(hi), "f"(a));
+        if (need_image) {
+          cr[p] = fmaf(w, c.x, cr[p]);
+          cg[p] = fmaf(w, c.y, cg[p]);
+          cb[p] = fmaf(w, c.z, cb[p]);
+        }
+        T[p] -= w;
+        wmax = fmaxf(wmax, w);
+#ifdef LODGE_COUNTERS
+        c_px += (w > 0.f) ? 1 : 0;
+#endif
+      };
+      // one member, including the guard band: pixels whose fp32 qs is within
+      // the band re-decide in fp64 with the reference's op order (rare)
+      auto one = [&](int j) {
+#ifdef LODGE_COUNTERS
+        c_iter += 1;
+#endif
+        const Payload &pj = PL[j];
+        float qs[PX];
+        float4 mm, cn;
+        const bool near = quad(pj, qs, mm, cn);
+        const float hi = pj.hi;
+        const float4 c = colour(pj);
         float wmax = 0.f;
-        // one pixel's blend step; kept: T >= t_min and not skipped
-        auto blend = [&](int p, bool kept, float a) {
-          const float w = kept ? T[p] * a : 0.f;
-          if (need_image) {
-            cr[p] = fmaf(w, c.x, cr[p]);
-            cg[p] = fmaf(w, c.y, cg[p]);
-            cb[p] = fmaf(w, c.z, cb[p]);
-          }
-          T[p] -= w;
-          if (kept) ++vis[p];
-          wmax = fmaxf(wmax, w);
-#ifdef LODGE_COUNTERS
-          c_px += kept ? 1 : 0;
-#endif
-        };
-        auto finish = [&]() {
-#ifdef LODGE_COUNTERS
-          c_hit += __any_sync(FULL_MASK, wmax > 0.f || near) ? 1 : 0;
-#endif
-          if (record_max) {
-            const unsigned wb = __reduce_max_sync(FULL_MASK, __float_as_uint(wmax));
-            if (lane == 0 && wb) atomicMax(&S.maxw32[j], wb);
-          }
-        };
         if (__any_sync(FULL_MASK, near)) {
-          // guard band: re-decide in fp64 with the reference's op order (rare)
+          const float lo = pj.lo;
           bool kp[PX];
           float a[PX];
 #pragma unroll
           for (int p = 0; p < PX; ++p) {
-            kp[p] = T[p] >= cpar.tmin_f && qs[p] > band.x;
+            kp[p] = T[p] >= cpar.tmin_f && qs[p] > hi;
             a[p] = fminf(ex2_approx(qs[p] + cn.w), cpar.clamp_f);
           }
           if (near) {
@@ -413,7 +438,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, LODGE_COMP_MINB) k_composite(
             const Precise pr = precise[m];
 #pragma unroll
             for (int p = 0; p < PX; ++p) {
-              if (T[p] >= cpar.tmin_f && qs[p] >= band.y && !(qs[p] > band.x)) {
+              if (T[p] >= cpar.tmin_f && qs[p] >= lo && !(qs[p] > hi)) {
                 double ad;
                 kp[p] = !ref_decide(gx, gy0 + 2.0 * p, pg.mx, pg.my, pr, rp, ad);
                 a[p] = (float)ad;
@@ -422,37 +447,68 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, LODGE_COMP_MINB) k_composite(
             }
           }
 #pragma unroll
-          for (int p = 0; p < PX; ++p) blend(p, kp[p], a[p]);
-          finish();
-          continue;
+          for (int p = 0; p < PX; ++p) {
+            const float w = kp[p] ? T[p] * a[p] : 0.f;
+            if (need_image) {
+              cr[p] = fmaf(w, c.x, cr[p]);
+              cg[p] = fmaf(w, c.y, cg[p]);
+              cb[p] = fmaf(w, c.z, cb[p]);
+            }
+            T[p] -= w;
+            if (kp[p]) ++vis[p];
+            wmax = fmaxf(wmax, w);
+#ifdef LODGE_COUNTERS
+            c_px += kp[p] ? 1 : 0;
+#endif
+          }
+        } else {
+#pragma unroll
+          for (int p = 0; p < PX; ++p)
+            step(p, qs[p], hi, fminf(ex2_approx(qs[p] + cn.w), cpar.clamp_f), c, wmax);
         }
-        // common case: every decision is certain in fp32.  One PTX block per
-        // pixel keeps the keep test a predicate (nvcc otherwise materialises
-        // the count increment as a select and a copy).
+        finish(j, wmax);
+      };
+      // two consecutive members: both quadratic forms and alphas first (they
+      // do not depend on T), then the two blend steps in list order
+      auto two = [&](int ja, int jb) {
+        const Payload &pa = PL[ja], &pb = PL[jb];
+        float qa[PX], qb[PX];
+        float4 ma, ca, mb, cb4;
+        const bool near = quad(pa, qa, ma, ca) | quad(pb, qb, mb, cb4);
+        if (__any_sync(FULL_MASK, near)) {
+          one(ja);
+          one(jb);
+          return;
+        }
+#ifdef LODGE_COUNTERS
+        c_iter += 2;
+#endif
+        float aa[PX], ab[PX];
 #pragma unroll
         for (int p = 0; p < PX; ++p) {
-          const float a = fminf(ex2_approx(qs[p] + cn.w), cpar.clamp_f);
-          float w;
-          asm("{\n\t.reg .pred k;\n\t"
-              "setp.ge.f32 k, %2, %4;\n\t"
-              "setp.gt.and.f32 k, %3, %5, k;\n\t"
-              "mul.rn.f32 %0, %2, %6;\n\t"
-              "selp.f32 %0, %0, 0f00000000, k;\n\t"
-              "@k add.s32 %1, %1, 1;\n\t}"
-              : "=f"(w), "+r"(vis[p])
-              : "f"(T[p]), "f"(qs[p]), "f"(cpar.tmin_f), "f"(band.x), "f"(a));
-          if (need_image) {
-            cr[p] = fmaf(w, c.x, cr[p]);
-            cg[p] = fmaf(w, c.y, cg[p]);
-            cb[p] = fmaf(w, c.z, cb[p]);
-          }
-          T[p] -= w;
-          wmax = fmaxf(wmax, w);
-#ifdef LODGE_COUNTERS
-          c_px += (w > 0.f) ? 1 : 0;
-#endif
+          aa[p] = fminf(ex2_approx(qa[p] + ca.w), cpar.clamp_f);
+          ab[p] = fminf(ex2_approx(qb[p] + cb4.w), cpar.clamp_f);
         }
-        finish();
+        const float ha = pa.hi, hb = pb.hi;
+        const float4 colA = colour(pa), colB = colour(pb);
+        float wa = 0.f, wb = 0.f;
+#pragma unroll
+        for (int p = 0; p < PX; ++p) step(p, qa[p], ha, aa[p], colA, wa);
+#pragma unroll
+        for (int p = 0; p < PX; ++p) step(p, qb[p], hb, ab[p], colB, wb);
+        finish(ja, wa);
+        finish(jb, wb);
+      };
+      for (int i = 0; i < cnt;) {
+        if (!__any_sync(FULL_MASK, live_any())) break;
+        const int ja = lds_u8(wl_sa + (uint32_t)i);
+        if (i + 1 < cnt) {
+          two(ja, lds_u8(wl_sa + (uint32_t)(i + 1)));
+          i += 2;
+        } else {
+          one(ja);
+          i += 1;
+        }
       }
     }
     __syncthreads();
