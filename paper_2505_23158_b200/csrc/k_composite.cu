@@ -141,6 +141,9 @@ template <bool EXACT>
 #ifndef LODGE_COMP_MINB
 #define LODGE_COMP_MINB 1
 #endif
+#ifndef LODGE_COMP_GROUP
+#define LODGE_COMP_GROUP 4  // list members per FAST iteration
+#endif
 __global__ void __launch_bounds__(CC<EXACT>::CT, LODGE_COMP_MINB) k_composite(
     const uint32_t *__restrict__ list, const uint32_t *__restrict__ tile_start,
     const uint32_t *__restrict__ tile_order, const Payload *__restrict__ payload,
@@ -468,46 +471,51 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, LODGE_COMP_MINB) k_composite(
         }
         finish(j, wmax);
       };
-      // two consecutive members: both quadratic forms and alphas first (they
-      // do not depend on T), then the two blend steps in list order
-      auto two = [&](int ja, int jb) {
-        const Payload &pa = PL[ja], &pb = PL[jb];
-        float qa[PX], qb[PX];
-        float4 ma, ca, mb, cb4;
-        const bool near = quad(pa, qa, ma, ca) | quad(pb, qb, mb, cb4);
+      // G consecutive members: all quadratic forms and alphas first (they do
+      // not depend on T), then the blend steps in list order
+      constexpr int G = LODGE_COMP_GROUP;
+      auto group = [&](const int (&js)[G]) {
+        float q[G][PX];
+        float4 mm[G], cn[G];
+        bool near = false;
+#pragma unroll
+        for (int u = 0; u < G; ++u) near |= quad(PL[js[u]], q[u], mm[u], cn[u]);
         if (__any_sync(FULL_MASK, near)) {
-          one(ja);
-          one(jb);
+#pragma unroll
+          for (int u = 0; u < G; ++u) one(js[u]);
           return;
         }
 #ifdef LODGE_COUNTERS
-        c_iter += 2;
+        c_iter += G;
 #endif
-        float aa[PX], ab[PX];
+        float a[G][PX];
 #pragma unroll
-        for (int p = 0; p < PX; ++p) {
-          aa[p] = fminf(ex2_approx(qa[p] + ca.w), cpar.clamp_f);
-          ab[p] = fminf(ex2_approx(qb[p] + cb4.w), cpar.clamp_f);
+        for (int u = 0; u < G; ++u)
+#pragma unroll
+          for (int p = 0; p < PX; ++p) a[u][p] = fminf(ex2_approx(q[u][p] + cn[u].w), cpar.clamp_f);
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          const Payload &pj = PL[js[u]];
+          const float hi = pj.hi;
+          const float4 c = colour(pj);
+          float w = 0.f;
+#pragma unroll
+          for (int p = 0; p < PX; ++p) step(p, q[u][p], hi, a[u][p], c, w);
+          finish(js[u], w);
         }
-        const float ha = pa.hi, hb = pb.hi;
-        const float4 colA = colour(pa), colB = colour(pb);
-        float wa = 0.f, wb = 0.f;
-#pragma unroll
-        for (int p = 0; p < PX; ++p) step(p, qa[p], ha, aa[p], colA, wa);
-#pragma unroll
-        for (int p = 0; p < PX; ++p) step(p, qb[p], hb, ab[p], colB, wb);
-        finish(ja, wa);
-        finish(jb, wb);
       };
-      for (int i = 0; i < cnt;) {
+      int i = 0;
+      for (; i + G <= cnt; i += G) {
         if (!__any_sync(FULL_MASK, live_any())) break;
-        const int ja = lds_u8(wl_sa + (uint32_t)i);
-        if (i + 1 < cnt) {
-          two(ja, lds_u8(wl_sa + (uint32_t)(i + 1)));
-          i += 2;
-        } else {
-          one(ja);
-          i += 1;
+        int js[G];
+#pragma unroll
+        for (int u = 0; u < G; ++u) js[u] = lds_u8(wl_sa + (uint32_t)(i + u));
+        group(js);
+      }
+      if (i + G > cnt) {  // the tail (the loop did not stop on dead pixels)
+        for (; i < cnt; ++i) {
+          if (!__any_sync(FULL_MASK, live_any())) break;
+          one(lds_u8(wl_sa + (uint32_t)i));
         }
       }
     }
