@@ -7,10 +7,8 @@
 //
 // K1 restates compose_active (src/blending.py:119-128): per level, the
 // sorted union of the two chunks' sets with tag 3 (both, mod 1), 1 (primary
-// only, mod t), 2 (other only, mod 1-t).  Each set element finds its union
-// slot by a binary search in the other set: slot(a_i) = i + |{b < a_i}|,
-// slot(b_j) = j + |{a < b_j}| (b_j not in A).  Union sizes follow from the
-// intersection count, accumulated with one atomic per warp.
+// only, mod t), 2 (other only, mod 1-t), as a stable merge-path merge of the
+// two sets that drops the second copy of common values (k_union_merge).
 #include "internal.cuh"
 
 namespace lodge {
@@ -86,20 +84,78 @@ void launch_blend_factor(const double *in, int32_t n, double *out, cudaStream_t 
   k_blend_factor<<<(n + 127) / 128, 128, 0, s>>>(in, n, out);
 }
 
-// Per-frame selection into the frame state; also zeroes intersection counts.
+// (d, j) ordered lexicographically, i.e. lexsort((arange, dist)) order.
+__device__ __forceinline__ bool dist_before(double da, int32_t ja, double db, int32_t jb) {
+  if (jb < 0) return ja >= 0;
+  if (ja < 0) return false;
+  return da < db || (!(db < da) && ja < jb);
+}
+
+// Warp arg-min of (d, j) over the lanes' candidates (j < 0: none).
+__device__ __forceinline__ void warp_argmin(double &d, int32_t &j) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double od = __shfl_xor_sync(FULL_MASK, d, o);
+    const int32_t oj = __shfl_xor_sync(FULL_MASK, j, o);
+    if (dist_before(od, oj, d, j)) {
+      d = od;
+      j = oj;
+    }
+  }
+}
+
+// Per-frame selection into the frame state (one warp): the same fp64
+// distances as select_one, lanes over chunks, then the two smallest (d, j).
 __global__ void k_select_frame(const double *centers, int32_t K, const lodge_camera *cam,
                                int32_t have_pair, int32_t pf, int32_t po, double t_val,
                                FrameState *fs) {
-  if (threadIdx.x == 0) {
-    lodge_frame_stats &st = fs->stats;
-    if (have_pair) {
+  lodge_frame_stats &st = fs->stats;
+  const int lane = threadIdx.x & 31;
+  if (have_pair) {
+    if (lane == 0) {
       st.f = pf;
       st.o = po;
       st.t = (po < 0) ? 1.0 : t_val;
       st.t_bar = st.t;
-    } else {
-      select_one(centers, K, cam->pos[0], cam->pos[1], cam->pos[2], &st.f, &st.o, &st.t_bar,
-                 &st.t);
+    }
+  } else if (threadIdx.x < 32) {
+    const double px = cam->pos[0], py = cam->pos[1], pz = cam->pos[2];
+    // each lane keeps its best two (d, j) over chunks lane, lane + 32, ...
+    double d0 = 0.0, d1 = 0.0;
+    int32_t b0 = -1, b1 = -1;
+    for (int32_t j = lane; j < K; j += 32) {
+      const double x = centers[3 * j] - px, y = centers[3 * j + 1] - py,
+                   z = centers[3 * j + 2] - pz;
+      const double d = sqrt((x * x + y * y) + z * z);
+      if (dist_before(d, j, d0, b0)) {
+        d1 = d0; b1 = b0; d0 = d; b0 = j;
+      } else if (dist_before(d, j, d1, b1)) {
+        d1 = d; b1 = j;
+      }
+    }
+    double bd = d0;
+    int32_t bj = b0;
+    warp_argmin(bd, bj);  // the nearest chunk
+    // runner-up: each lane's best candidate other than the winner
+    double cd = (b0 == bj) ? d1 : d0;
+    int32_t cj = (b0 == bj) ? b1 : b0;
+    warp_argmin(cd, cj);
+    if (lane == 0) {
+      st.f = bj;
+      if (K > 1) {
+        st.o = cj;
+        const double *mf = centers + 3 * bj, *mo = centers + 3 * cj;
+        const double fo0 = mf[0] - mo[0], fo1 = mf[1] - mo[1], fo2 = mf[2] - mo[2];
+        const double co0 = px - mo[0], co1 = py - mo[1], co2 = pz - mo[2];
+        const double d2 = dot3_blas(fo0, fo1, fo2, fo0, fo1, fo2);
+        const double tbar = dot3_blas(co0, co1, co2, fo0, fo1, fo2) / d2;
+        st.t_bar = tbar;
+        st.t = fmin(1.0, fmax(0.0, tbar));
+      } else {
+        st.o = -1;
+        st.t_bar = 1.0;
+        st.t = 1.0;
+      }
     }
   }
   if (threadIdx.x < LODGE_MAX_LEVELS) fs->stats.U_level[threadIdx.x] = 0;
@@ -111,6 +167,9 @@ void launch_select_frame(const double *centers, int32_t K, const lodge_camera *c
   k_select_frame<<<1, 32, 0, s>>>(centers, K, cam, have_pair, pair_f, pair_o, t_val, fs);
 }
 
+constexpr int UN_THREADS = 256, UN_ITEMS = 8;
+constexpr uint32_t UN_TILE = UN_THREADS * UN_ITEMS;  // merged elements per CTA
+
 struct UnionArgs {
   const int64_t *offsets;
   const uint32_t *data;
@@ -120,13 +179,7 @@ struct UnionArgs {
   uint32_t part_base[LODGE_MAX_LEVELS + 1];  // CTA-count table offsets per level
 };
 
-// One CTA = 256 consecutive diagonals of level l's stable merge S =
-// merge(A, B) (A first on ties).  The CTA's window of A and B is found by two
-// merge-path searches and staged in shared memory; each thread then locates
-// its element by a short search there.  The B copy of a value present in
-// both sets is dropped (keep = false).  Compacting the kept elements in S
-// order yields np.union1d(A, B) with its tags (count -> scan -> write, so no
-// look-back chain serialises the CTAs).  Returns false if the CTA is idle.
+// The two sorted sets of level l for the frame's chunk pair.
 struct UnionLevel {
   const uint32_t *A, *B;
   uint32_t na, nb;
@@ -157,8 +210,8 @@ __device__ __forceinline__ int union_level_of(const UnionArgs &a, uint32_t g, ui
 }
 
 // Merge-path splits for every CTA boundary of every level, all in parallel:
-// splits[part_base[l] + l + p] = #A among the first min(256 p, n_l) merged
-// elements, p = 0 .. ceil(n_l / 256).
+// splits[part_base[l] + l + p] = #A among the first min(UN_TILE p, n_l)
+// merged elements, p = 0 .. ceil(n_l / UN_TILE).
 __global__ void k_union_split(UnionArgs a, FrameState *fs, uint32_t *splits) {
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= a.part_base[a.L] + a.L) return;
@@ -167,8 +220,8 @@ __global__ void k_union_split(UnionArgs a, FrameState *fs, uint32_t *splits) {
   const uint32_t p = g - a.part_base[l] - l;
   const UnionLevel u = union_level(a, fs, l);
   const uint32_t n = u.na + u.nb;
-  if (p > (n + 255u) / 256u) return;
-  const uint32_t d = min(p * 256u, n);
+  if (p > (n + UN_TILE - 1) / UN_TILE) return;
+  const uint32_t d = min(p * UN_TILE, n);
   uint32_t lo = d > u.nb ? d - u.nb : 0u, hi = d < u.na ? d : u.na;
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
@@ -178,126 +231,104 @@ __global__ void k_union_split(UnionArgs a, FrameState *fs, uint32_t *splits) {
   splits[g] = lo;
 }
 
-__device__ __forceinline__ bool union_block(const UnionArgs &a, const FrameState *fs, int l,
-                                            uint32_t part, const uint32_t *splits, bool &keep,
-                                            uint32_t &v, uint8_t &tag) {
-  const int32_t f = fs->stats.f, o = fs->stats.o;
-  const int64_t fa = a.offsets[(int64_t)f * a.L + l];
-  const uint32_t na = (uint32_t)(a.offsets[(int64_t)f * a.L + l + 1] - fa);
-  const uint32_t *A = a.data + fa;
-  uint32_t nb = 0;
-  const uint32_t *B = A;
-  if (o >= 0) {
-    const int64_t fb = a.offsets[(int64_t)o * a.L + l];
-    nb = (uint32_t)(a.offsets[(int64_t)o * a.L + l + 1] - fb);
-    B = a.data + fb;
-  }
-  __shared__ uint32_t s_a[258], s_b[258];  // A[i0-1 .. i1], B[j0 .. j1]
-  const uint32_t n = na + nb;
-  if (part * 256u >= n) return false;  // block-uniform
-  const uint32_t d0 = part * 256u, d1 = min(d0 + 256u, n);
+// One CTA = UN_TILE consecutive diagonals of level l's stable merge
+// S = merge(A, B) (A first on ties), CTAs in ticket order.  The CTA's windows
+// of A and B (from the precomputed merge-path splits) are staged in shared
+// memory; each thread finds the start of its UN_ITEMS diagonals by one
+// merge-path search there and merges them sequentially.  The B copy of a
+// value present in both sets is dropped; the kept elements are compacted in
+// S order by a block scan and a per-level decoupled look-back, which yields
+// np.union1d(A, B) with its tags in one pass.
+__global__ void __launch_bounds__(UN_THREADS) k_union_merge(UnionArgs a, FrameState *fs,
+                                                           const uint32_t *splits,
+                                                           uint64_t *lb_status,
+                                                           uint32_t *union_idx,
+                                                           uint8_t *union_tag) {
+  __shared__ uint32_t s_a[UN_TILE + 2], s_b[UN_TILE + 1];  // A[i0-1 .. i1], B[j0 .. j1]
+  __shared__ uint32_t s_w[UN_THREADS / 32 + 1];
+  __shared__ uint32_t s_tk;
+  const uint32_t g = take_ticket(&fs->tickets[TK_UNION0], &s_tk);
+  uint32_t part;
+  const int l = union_level_of(a, g, part);
+  const UnionLevel u = union_level(a, fs, l);
+  const uint32_t n = u.na + u.nb;
+  if (part * UN_TILE >= n) return;  // block-uniform: idle slot of this level
+  const uint32_t d0 = part * UN_TILE, d1 = min(d0 + UN_TILE, n);
   const uint32_t *sp = splits + a.part_base[l] + l + part;
   const uint32_t i0 = sp[0], i1 = sp[1], j0 = d0 - i0, j1 = d1 - i1;
-  // stage A[i0-1 .. i1] (one element back for the duplicate test, one ahead
-  // for the tie test) and B[j0 .. j1]
-  for (uint32_t q = threadIdx.x; q < i1 - i0 + 2; q += 256) {
+  for (uint32_t q = threadIdx.x; q < i1 - i0 + 2; q += UN_THREADS) {
     const int64_t ia = (int64_t)i0 - 1 + q;
-    s_a[q] = (ia >= 0 && ia < na) ? __ldg(A + ia) : 0xffffffffu;
+    s_a[q] = (ia >= 0 && ia < u.na) ? __ldg(u.A + ia) : 0xffffffffu;
   }
-  for (uint32_t q = threadIdx.x; q < j1 - j0 + 1; q += 256)
-    s_b[q] = (j0 + q < nb) ? __ldg(B + j0 + q) : 0xffffffffu;
+  for (uint32_t q = threadIdx.x; q < j1 - j0 + 1; q += UN_THREADS)
+    s_b[q] = (j0 + q < u.nb) ? __ldg(u.B + j0 + q) : 0xffffffffu;
   __syncthreads();
-  const uint32_t t = d0 + threadIdx.x;
-  keep = false;
-  v = 0;
-  tag = 0;
-  if (t < n) {
-    // merge-path search inside the staged window (local diagonal t - d0)
-    const uint32_t dl = t - d0;
-    uint32_t lo = dl > (j1 - j0) ? dl - (j1 - j0) : 0u, hi = min(dl, i1 - i0);
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (s_a[mid + 1] <= s_b[dl - 1 - mid]) lo = mid + 1;
-      else hi = mid;
+  // this thread's diagonals [dl, dl + UN_ITEMS) of the window
+  const uint32_t wa = i1 - i0, wb = j1 - j0, dn = d1 - d0;
+  const uint32_t dl = min((uint32_t)threadIdx.x * UN_ITEMS, dn);
+  uint32_t lo = dl > wb ? dl - wb : 0u, hi = min(dl, wa);
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (s_a[mid + 1] <= s_b[dl - 1 - mid]) lo = mid + 1;
+    else hi = mid;
+  }
+  uint32_t ia = lo, jb = dl - lo;  // window positions
+  uint32_t vals[UN_ITEMS];
+  uint8_t tags[UN_ITEMS];
+  uint32_t kmask = 0, kc = 0;
+#pragma unroll
+  for (int it = 0; it < UN_ITEMS; ++it) {
+    if (dl + it < dn) {
+      const uint32_t av = s_a[ia + 1], bv = s_b[jb];
+      const bool a_ok = i0 + ia < u.na, b_ok = j0 + jb < u.nb;
+      if (a_ok && (!b_ok || av <= bv)) {
+        vals[it] = av;
+        tags[it] = (b_ok && bv == av) ? 3 : 1;
+        kmask |= 1u << it;
+        ++ia;
+      } else {
+        vals[it] = bv;
+        tags[it] = 2;
+        if (!(i0 + ia > 0 && s_a[ia] == bv)) kmask |= 1u << it;
+        ++jb;
+      }
     }
-    const uint32_t i = i0 + lo, j = j0 + (dl - lo);  // global positions
-    const uint32_t av = s_a[lo + 1], bv = s_b[dl - lo];
-    if (i < na && (j >= nb || av <= bv)) {
-      v = av;
-      tag = (j < nb && bv == v) ? 3 : 1;
-      keep = true;
-    } else {
-      v = bv;
-      keep = !(i > 0 && s_a[lo] == v);
-      tag = 2;
-    }
   }
-  return true;
-}
-
-// flattened grid over all levels' CTAs: kept elements per CTA.
-__global__ void __launch_bounds__(256) k_union_count(UnionArgs a, FrameState *fs,
-                                                     const uint32_t *splits, uint32_t *cnt) {
-  uint32_t part;
-  const int l = union_level_of(a, blockIdx.x, part);
-  bool keep;
-  uint32_t v;
-  uint8_t tag;
-  if (!union_block(a, fs, l, part, splits, keep, v, tag)) return;
-  const uint32_t c = __syncthreads_count(keep);
-  if (threadIdx.x == 0) cnt[a.part_base[l] + part] = c;
-}
-
-// grid L x 1024 threads: exclusive scan of the CTA counts of level l, U_l.
-__global__ void __launch_bounds__(1024) k_union_scan(UnionArgs a, FrameState *fs, uint32_t *cnt) {
-  __shared__ uint32_t s_sum[1024];
-  const int l = blockIdx.x;
-  const int32_t f = fs->stats.f, o = fs->stats.o;
-  uint32_t n = (uint32_t)(a.offsets[(int64_t)f * a.L + l + 1] - a.offsets[(int64_t)f * a.L + l]);
-  if (o >= 0) n += (uint32_t)(a.offsets[(int64_t)o * a.L + l + 1] - a.offsets[(int64_t)o * a.L + l]);
-  const uint32_t np = (n + 255u) / 256u;
-  uint32_t *c = cnt + a.part_base[l];
-  const uint32_t per = (np + 1023u) / 1024u, b = threadIdx.x * per, e = min(np, b + per);
-  uint32_t loc = 0;
-  for (uint32_t q = b; q < e; ++q) loc += c[q];
-  s_sum[threadIdx.x] = loc;
-  __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {
-    const uint32_t t = threadIdx.x >= off ? s_sum[threadIdx.x - off] : 0u;
-    __syncthreads();
-    s_sum[threadIdx.x] += t;
-    __syncthreads();
-  }
-  uint32_t run = s_sum[threadIdx.x] - loc;
-  for (uint32_t q = b; q < e; ++q) {
-    const uint32_t x = c[q];
-    c[q] = run;
-    run += x;
-  }
-  if (threadIdx.x == 1023) fs->stats.U_level[l] = s_sum[1023];
-}
-
-// flattened grid: recompute the CTA's merge and write the kept elements in order.
-__global__ void __launch_bounds__(256) k_union_write(UnionArgs a, FrameState *fs,
-                                                     const uint32_t *splits, const uint32_t *cnt,
-                                                     uint32_t *union_idx, uint8_t *union_tag) {
-  __shared__ uint32_t s_w[8];
-  uint32_t part;
-  const int l = union_level_of(a, blockIdx.x, part);
-  bool keep;
-  uint32_t v;
-  uint8_t tag;
-  if (!union_block(a, fs, l, part, splits, keep, v, tag)) return;
+  kc = __popc(kmask);
+  // block exclusive scan of the kept counts
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t bal = __ballot_sync(FULL_MASK, keep);
-  if (lane == 0) s_w[warp] = __popc(bal);
+  uint32_t inc = kc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) s_w[warp] = inc;
   __syncthreads();
-  uint32_t pre = cnt[a.part_base[l] + part];
-  for (int w = 0; w < warp; ++w) pre += s_w[w];
-  if (!keep) return;
-  const uint32_t m = pre + __popc(bal & lanemask_lt());
-  union_idx[a.slot_base[l] + m] = v;
-  union_tag[a.slot_base[l] + m] = tag;
+  if (warp == 0) {
+    uint32_t wv = lane < UN_THREADS / 32 ? s_w[lane] : 0u;
+    uint32_t wi = wv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(FULL_MASK, wi, o);
+      if (lane >= o) wi += t;
+    }
+    const uint32_t total = __shfl_sync(FULL_MASK, wi, UN_THREADS / 32 - 1);
+    const uint32_t pre = lookback_warp(lb_status + a.part_base[l], part, total,
+                                       fs->epoch + TK_UNION0);
+    if (lane < UN_THREADS / 32) s_w[lane] = pre + wi - wv;
+    if (lane == 0 && (part + 1) * UN_TILE >= n) fs->stats.U_level[l] = pre + total;
+  }
+  __syncthreads();
+  uint32_t m = a.slot_base[l] + s_w[warp] + inc - kc;
+#pragma unroll
+  for (int it = 0; it < UN_ITEMS; ++it) {
+    if ((kmask >> it) & 1u) {
+      union_idx[m] = vals[it];
+      union_tag[m] = tags[it];
+      ++m;
+    }
+  }
 }
 
 __global__ void k_union_sizes(int32_t L, FrameState *fs) {
@@ -320,17 +351,17 @@ void launch_union(const lodge_chunks &ch, const LevelSlots &ls, FrameState *fs, 
   a.status_stride = union_status_stride(max_slots);
   a.part_base[0] = 0;
   for (int l = 0; l < ch.L; ++l)
-    a.part_base[l + 1] = a.part_base[l] + (ls.slot_base[l + 1] - ls.slot_base[l] + 255) / 256;
-  // scratch in the look-back buffer: CTA counts, then the merge-path splits
-  // (count words have zero flag bits, so no look-back ever reads them as ready)
-  uint32_t *cnt = reinterpret_cast<uint32_t *>(status);
-  uint32_t *splits = cnt + a.part_base[ch.L];
+    a.part_base[l + 1] =
+        a.part_base[l] + (ls.slot_base[l + 1] - ls.slot_base[l] + UN_TILE - 1) / UN_TILE;
+  // scratch in the look-back buffer: the merge-path splits as u32 (values
+  // < 2^30 leave the flag bits clear, so no look-back reads them as ready),
+  // then the per-level look-back words
   const uint32_t nparts = a.part_base[ch.L];
+  uint32_t *splits = reinterpret_cast<uint32_t *>(status);
+  uint64_t *lb = status + (nparts + ch.L + 2) / 2 + 1;
   if (max_slots > 0 && nparts > 0) {
     k_union_split<<<(nparts + ch.L + 255) / 256, 256, 0, s>>>(a, fs, splits);
-    k_union_count<<<nparts, 256, 0, s>>>(a, fs, splits, cnt);
-    k_union_scan<<<ch.L, 1024, 0, s>>>(a, fs, cnt);
-    k_union_write<<<nparts, 256, 0, s>>>(a, fs, splits, cnt, union_idx, union_tag);
+    k_union_merge<<<nparts, UN_THREADS, 0, s>>>(a, fs, splits, lb, union_idx, union_tag);
   }
   k_union_sizes<<<1, 32, 0, s>>>(ch.L, fs);
 }
