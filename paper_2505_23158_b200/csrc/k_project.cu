@@ -407,59 +407,74 @@ template <typename GT, typename ST>
 __global__ void __launch_bounds__(256, 2) k_project_frame(ProjLevels lv, Work w, FrameState *fs,
                                                        const lodge_camera *__restrict__ cam_p,
                                                        lodge_raster_params rp, int32_t shade) {
+  // persistent CTAs (grid-stride over the slots): the camera and the level
+  // table are staged once per CTA
   __shared__ lodge_camera cam;
-  if (threadIdx.x == 0) cam = *cam_p;
+  __shared__ uint32_t s_used[LODGE_MAX_LEVELS], s_cat[LODGE_MAX_LEVELS];
+  __shared__ double s_t;
+  if (threadIdx.x == 0) {
+    cam = *cam_p;
+    s_t = fs->stats.t;
+    uint32_t c = 0;
+    for (int k = 0; k < lv.L; ++k) {
+      s_cat[k] = c;  // concatenated index offset of level k
+      s_used[k] = fs->stats.U_level[k];
+      c += s_used[k];
+    }
+  }
   __syncthreads();
-  const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
-  // map slot -> level
-  int l = 0;
-  while (l + 1 < lv.L && slot >= lv.slot_base[l + 1]) ++l;
-  const uint32_t pos = slot - lv.slot_base[l];
-  const bool valid = slot < lv.slot_base[lv.L] && pos < fs->stats.U_level[l];
-  uint32_t cat_off = 0;  // concatenated index offset of level l
-  for (int k = 0; k < l; ++k) cat_off += fs->stats.U_level[k];
-  const uint32_t g = cat_off + pos;
-  Proj p;
-  p.ok = false;
-  double v[12];
-  uint32_t gidx = 0;
-  if (valid) {
-    gidx = w.union_idx[slot];
-    const uint8_t tag = w.union_tag[slot];
-    const double t = fs->stats.t;
-    const double mod = (tag == 3) ? 1.0 : (tag == 1 ? t : 1.0 - t);
-    load_geom<GT>(reinterpret_cast<const GT *>(lv.geom[l]) + (size_t)gidx * 12, v);
-    p = project_core(v, cam, rp, mod, true);
-  }
-  const bool keep = valid && p.ok;
-  const uint32_t nkeep = __popc(__ballot_sync(FULL_MASK, keep));
-  if ((threadIdx.x & 31) == 0 && nkeep) atomicAdd(&fs->stats.M, nkeep);
   const int32_t tiles_x = (cam.w + 15) / 16, tiles_y = (cam.h + 15) / 16;
-  const uint64_t rc = keep ? tile_rect(p.mx, p.my, p.ex, p.ey, tiles_x, tiles_y) : 0ull;
-  add_tile_diff(w.tile_diff, rc, tiles_x, keep);
-  if (!valid) return;
-  w.val_depth[0][g] = g;
-  if (!keep) {
-    w.key_depth[0][g] = ~0ull;
-    return;
+  const uint32_t nslots = lv.slot_base[lv.L];
+  uint32_t nkeep_cta = 0;  // survivors seen by this thread's warp (lane 0 counts)
+  for (uint32_t base = blockIdx.x * blockDim.x; base < nslots; base += gridDim.x * blockDim.x) {
+    const uint32_t slot = base + threadIdx.x;
+    // map slot -> level
+    int l = 0;
+    while (l + 1 < lv.L && slot >= lv.slot_base[l + 1]) ++l;
+    const uint32_t pos = slot - lv.slot_base[l];
+    const bool valid = slot < nslots && pos < s_used[l];
+    const uint32_t g = s_cat[l] + pos;
+    Proj p;
+    p.ok = false;
+    double v[12];
+    uint32_t gidx = 0;
+    if (valid) {
+      gidx = w.union_idx[slot];
+      const uint8_t tag = w.union_tag[slot];
+      const double t = s_t;
+      const double mod = (tag == 3) ? 1.0 : (tag == 1 ? t : 1.0 - t);
+      load_geom<GT>(reinterpret_cast<const GT *>(lv.geom[l]) + (size_t)gidx * 12, v);
+      p = project_core(v, cam, rp, mod, true);
+    }
+    const bool keep = valid && p.ok;
+    nkeep_cta += __popc(__ballot_sync(FULL_MASK, keep));
+    const uint64_t rc = keep ? tile_rect(p.mx, p.my, p.ex, p.ey, tiles_x, tiles_y) : 0ull;
+    add_tile_diff(w.tile_diff, rc, tiles_x, keep);
+    if (!valid) continue;
+    w.val_depth[0][g] = g;
+    if (!keep) {
+      w.key_depth[0][g] = ~0ull;
+      continue;
+    }
+    const uint64_t m = g;
+    double rgb[3] = {0.0, 0.0, 0.0};
+    if (shade) {
+      const int deg = lv.degree[l];
+      const int terms = (deg + 1) * (deg + 1);
+      eval_sh_dev<ST>(reinterpret_cast<const ST *>(lv.sh[l]) + (size_t)gidx * 3 * terms, terms,
+                      deg, v, cam, rgb);
+    }
+    const double inv_det = 1.0 / p.det;
+    const double A = p.c11 * inv_det, B = (-p.c01) * inv_det, C = p.c00 * inv_det;
+    Payload pl;
+    Precise pr;
+    make_payload(p.mx, p.my, A, B, C, p.op, rgb, g, p.ex, p.ey, rp, pl, pr);
+    w.payload[m] = pl;
+    w.precise[m] = pr;
+    w.rect[m] = rc;
+    w.key_depth[0][m] = (uint64_t)__double_as_longlong(p.z);
   }
-  const uint64_t m = g;
-  double rgb[3] = {0.0, 0.0, 0.0};
-  if (shade) {
-    const int deg = lv.degree[l];
-    const int terms = (deg + 1) * (deg + 1);
-    eval_sh_dev<ST>(reinterpret_cast<const ST *>(lv.sh[l]) + (size_t)gidx * 3 * terms, terms, deg,
-                    v, cam, rgb);
-  }
-  const double inv_det = 1.0 / p.det;
-  const double A = p.c11 * inv_det, B = (-p.c01) * inv_det, C = p.c00 * inv_det;
-  Payload pl;
-  Precise pr;
-  make_payload(p.mx, p.my, A, B, C, p.op, rgb, g, p.ex, p.ey, rp, pl, pr);
-  w.payload[m] = pl;
-  w.precise[m] = pr;
-  w.rect[m] = rc;
-  w.key_depth[0][m] = (uint64_t)__double_as_longlong(p.z);
+  if ((threadIdx.x & 31) == 0 && nkeep_cta) atomicAdd(&fs->stats.M, nkeep_cta);
 }
 
 // ---------------------------------------------------------------------------
@@ -556,7 +571,15 @@ template <typename GT, typename ST>
 static void launch_pf(const ProjLevels &lv, const Work &w, FrameState *fs,
                       const lodge_camera *cam, const lodge_raster_params &rp, int32_t shade,
                       uint32_t nslots, cudaStream_t s) {
-  k_project_frame<GT, ST><<<(nslots + 255) / 256, 256, 0, s>>>(lv, w, fs, cam, rp, shade);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const uint32_t want = (nslots + 255) / 256, cap = 2u * (uint32_t)sms;  // 2 CTAs per SM
+  k_project_frame<GT, ST><<<want < cap ? want : cap, 256, 0, s>>>(lv, w, fs, cam, rp, shade);
 }
 
 int launch_project_frame(const lodge_level *levels, const LevelSlots &ls, const Work &w,
