@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t tile
 constexpr int DUP_THREADS = 256;
 constexpr int EMIT_ITEMS = 8;
 constexpr int EMIT_CHUNK = DUP_THREADS * EMIT_ITEMS;  // pairs per emission CTA
+constexpr int COUNT_ITEMS = 8;                        // splats per thread in k_dup_count
 
 // Pass 1, one thread per depth-sorted splat: tile count, exclusive scan of
 // the counts in depth order (single-pass look-back), the splat's rectangle
@@ -133,6 +134,7 @@ constexpr int EMIT_CHUNK = DUP_THREADS * EMIT_ITEMS;  // pairs per emission CTA
 __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__restrict__ order,
                                                            const uint64_t *__restrict__ rect,
                                                            Work w, FrameState *fs) {
+  constexpr int IT = COUNT_ITEMS;  // consecutive depth-order splats per thread
   __shared__ uint32_t s_w[DUP_THREADS / 32];
   __shared__ uint32_t s_part, s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -140,16 +142,30 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
   __syncthreads();
   const uint32_t part = s_part;
   const uint32_t M = fs->stats.overflow ? 0u : fs->stats.M;
-  const uint32_t r = part * DUP_THREADS + tid;
-  if (part * DUP_THREADS >= M) return;
+  const uint32_t r0 = part * (DUP_THREADS * IT) + tid * IT;
+  if (part * (DUP_THREADS * IT) >= M) return;
+  uint32_t m[IT], c[IT];
+  uint64_t rc[IT];
+  if (r0 + IT <= M) {  // order is 16-byte aligned and r0 a multiple of IT
+#pragma unroll
+    for (int q = 0; q < IT / 4; ++q) {
+      const uint4 o4 = *reinterpret_cast<const uint4 *>(order + r0 + 4 * q);
+      m[4 * q] = o4.x; m[4 * q + 1] = o4.y; m[4 * q + 2] = o4.z; m[4 * q + 3] = o4.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < IT; ++i) m[i] = (r0 + i < M) ? order[r0 + i] : 0u;
+  }
   uint32_t cnt = 0;
-  if (r < M) {
-    const uint32_t m = order[r];
-    const uint64_t rc = rect[m];
-    const uint32_t x0 = rc & 0xffff, x1 = (rc >> 16) & 0xffff, y0 = (rc >> 32) & 0xffff,
-                   y1 = rc >> 48;
-    cnt = (x1 - x0 + 1) * (y1 - y0 + 1);
-    w.rect_sorted[r] = rc;
+#pragma unroll
+  for (int i = 0; i < IT; ++i) rc[i] = (r0 + i < M) ? rect[m[i]] : 0ull;
+#pragma unroll
+  for (int i = 0; i < IT; ++i) {
+    const uint32_t x0 = rc[i] & 0xffff, x1 = (rc[i] >> 16) & 0xffff, y0 = (rc[i] >> 32) & 0xffff,
+                   y1 = rc[i] >> 48;
+    c[i] = (r0 + i < M) ? (x1 - x0 + 1) * (y1 - y0 + 1) : 0u;
+    cnt += c[i];
+    if (r0 + i < M) w.rect_sorted[r0 + i] = rc[i];
   }
   uint32_t inc = cnt;
 #pragma unroll
@@ -173,12 +189,19 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
     if (lane == 0) s_base = pre;
   }
   __syncthreads();
-  if (r >= M) return;
-  const uint32_t off = s_base + s_w[warp] + inc - cnt;
-  w.splat_off[r] = off;
-  if (r == M - 1) w.splat_off[M] = off + cnt;
-  for (uint32_t c = (off + EMIT_CHUNK - 1) / EMIT_CHUNK; c * EMIT_CHUNK < off + cnt; ++c)
-    w.chunk_first[c] = r;
+  if (r0 >= M) return;
+  uint32_t off = s_base + s_w[warp] + inc - cnt;
+#pragma unroll
+  for (int i = 0; i < IT; ++i) {
+    const uint32_t r = r0 + i;
+    if (r < M) {
+      w.splat_off[r] = off;
+      if (r == M - 1) w.splat_off[M] = off + c[i];
+      for (uint32_t k = (off + EMIT_CHUNK - 1) / EMIT_CHUNK; k * EMIT_CHUNK < off + c[i]; ++k)
+        w.chunk_first[k] = r;
+      off += c[i];
+    }
+  }
 }
 
 // Pass 2, EMIT_CHUNK pairs per CTA regardless of splat sizes: the owners of
@@ -241,7 +264,8 @@ void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32
 void launch_duplicate(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_cap,
                       cudaStream_t s) {
   if (M_cap <= 0) return;
-  const unsigned grid = (unsigned)((M_cap + DUP_THREADS - 1) / DUP_THREADS);
+  const unsigned grid =
+      (unsigned)((M_cap + DUP_THREADS * COUNT_ITEMS - 1) / (DUP_THREADS * COUNT_ITEMS));
   k_dup_count<<<grid, DUP_THREADS, 0, s>>>(w.val_depth[0], w.rect, w, fs);
   const unsigned egrid = (unsigned)((w.P_cap + EMIT_CHUNK - 1) / EMIT_CHUNK);
   k_dup_emit<<<egrid, DUP_THREADS, 0, s>>>(w.val_depth[0], tiles_x, w, fs);
