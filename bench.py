@@ -44,7 +44,7 @@ BLOCK = 16
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--steps", type=int, default=24)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="lodge", choices=["lodge", "reference"])
     ap.add_argument("--config", default="config3")
@@ -82,7 +82,11 @@ def my_views(rank, world, n_steps_total, block):
 # clocks (nvidia-smi sampled during the timed region)
 # ---------------------------------------------------------------------------
 class Clocks:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi sampler (every 100 ms) started before the warm-up, so it is
+    running when the timed region begins; stop() keeps the samples stamped
+    inside [t0, t1] of the timed region, widened to the nearest sample on
+    each side when the region is shorter than the sampling period."""
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -90,14 +94,30 @@ class Clocks:
         self.gpu = gpu_index
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         self.p = None
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+        time.sleep(0.25)  # let the sample after the region land
+
+    @staticmethod
+    def _stamp(s):
+        import datetime
+        try:
+            return datetime.datetime.strptime(s, "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            return None
 
     def stop(self):
         if self.p is None:
@@ -111,18 +131,28 @@ class Clocks:
         rows = []
         for line in open(self.f.name):
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 9:
-                rows.append(parts)
+            if len(parts) >= 10:
+                rows.append((self._stamp(parts[0]), parts[1:]))
         os.unlink(self.f.name)
-        if not rows:
+        if self.t0 is not None and self.t1 is not None:
+            inside = [r for ts, r in rows if ts is not None and self.t0 <= ts <= self.t1]
+            before = [r for ts, r in rows if ts is not None and ts < self.t0][-1:]
+            after = [r for ts, r in rows if ts is not None and ts > self.t1][:1]
+            sel = inside if len(inside) >= 2 else before + inside + after
+        else:
+            sel = [r for _, r in rows]
+        if not sel:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        sm = [float(r[1]) for r in sel if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in sel if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        reasons = sorted({names[i] for r in sel for i in range(4) if r[5 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+                "samples": len(sel),
+                "window": "inside the timed region" if len(sel) == len(
+                    [1 for ts, _ in rows if ts is not None and self.t0 is not None
+                     and self.t0 <= ts <= self.t1]) else "timed region plus one sample either side"}
 
 
 # ---------------------------------------------------------------------------
@@ -282,6 +312,8 @@ def run_lodge(args):
     P_max = max(s.P for s in st_sz)
     r.reserve(int(P_max * 1.05) + 4096)
     launches_per_frame = r.last_launch_count()
+    clocks = Clocks(local)
+    clocks.start()  # sampling before the timed region starts
     for s in range(args.warmup):
         for j, v in enumerate(schedule[s]):
             r.render(cams[pos[v]], frames[j], slot=j % r.n_streams)
@@ -293,12 +325,11 @@ def run_lodge(args):
     # region is bracketed by events on the current stream that every slot
     # stream waits on / is waited for.
     S = r.n_streams
-    clocks = Clocks(local)
     r.profile(True, n_timed)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.mark_start()
     cur = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(cur)
@@ -315,6 +346,7 @@ def run_lodge(args):
         cur.wait_stream(r.stream_of(q))
     e1.record(cur)
     torch.cuda.synchronize()
+    clocks.mark_end()
     clk = clocks.stop()
     if world > 1:
         dist.barrier()

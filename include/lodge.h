@@ -86,6 +86,10 @@ typedef struct {
 /* Render flags */
 #define LODGE_NEED_IMAGE 1
 #define LODGE_RECORD_MAX 2
+/* With LODGE_RECORD_MAX: maxw is not zeroed first, the frame's per-input
+ * max weights are max-ed into it on the device -- the max over views of
+ * score_active_selection (src/lod.py:95-131) without a host round trip. */
+#define LODGE_ACCUMULATE_MAX 4
 
 /* Device outputs of one frame (src/raster.py:119-127).  image is float
  * (FAST) or double (EXACT), (h, w, 3); tile_count (tiles_y*tiles_x) int32;

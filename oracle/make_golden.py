@@ -224,12 +224,62 @@ def make_config1():
     return d
 
 
+def _config1_objects():
+    """Reference objects rebuilt from the committed config1.npz."""
+    d = np.load(os.path.join(OUT, "config1.npz"))
+    levels = []
+    for l in range(int(d["n_levels"])):
+        p = f"L{l}/"
+        sc = Scene(d[p + "means"], d[p + "scales"], d[p + "rotations"], d[p + "opacities"],
+                   d[p + "sh"], d[p + "fv"], int(d[p + "deg"]))
+        levels.append(LodLevel(l, float(d[p + "depth_threshold"]), sc,
+                               np.arange(len(sc), dtype=np.int64)))
+    cams = []
+    for v in range(8):
+        p = f"v{v}/"
+        cams.append(Camera(d[p + "pos"], d[p + "quat"], d[p + "focal"], d[p + "pp"],
+                           tuple(int(x) for x in d[p + "res"]), float(d[p + "near"]), f"v{v}"))
+    K, L = d["centers"].shape[0], int(d["n_levels"])
+    sets = tuple(tuple(d[f"set/{j}/{l}"] for l in range(L)) for j in range(K))
+    plan = ChunkPlan(d["centers"], d["radii"], sets, np.zeros(0, np.int64))
+    return d, levels, cams, plan
+
+
+def make_importance():
+    """Importance scoring on the config-1 data:
+    a  compute_importance(level 0, views 0-3, PerturbSpec(2, 5))
+    b  score_active_selection(both levels, chunk 2's sets, views 4-5, PerturbSpec(1, 9))
+    c  visibility_filter_chunk(chunk 0, views 0-1, perturb_count 2, seed 3)"""
+    from splatlod.lod import PerturbSpec, compute_importance, score_active_selection
+    d, levels, cams, plan = _config1_objects()
+    rc = R.RasterConfig()
+    out = {}
+    t0 = time.time()
+    cfg = LodBuildConfig()
+    imp = compute_importance(levels[0], cams[0:4], cfg, PerturbSpec(2, 5))
+    out["a/scores"] = imp.scores
+    out["a/gamma"] = np.array(imp.threshold_base)
+    sc = score_active_selection(levels, plan.active_sets[2], cams[4:6], rc, PerturbSpec(1, 9))
+    for l, s in enumerate(sc):
+        out[f"b/scores{l}"] = s
+    ccfg = ChunkBuildConfig(d1=float(d["thresholds"][0]), perturb_count=2, perturb_seed=3,
+                            vis_threshold=cfg.gamma)
+    kept = visibility_filter_chunk(plan, 0, levels, cams[0:2], ccfg, rc)
+    for l, s in enumerate(kept):
+        out[f"c/kept{l}"] = np.asarray(s, np.int64)
+    out["c/vis_threshold"] = np.array(ccfg.vis_threshold)
+    print("importance", round(time.time() - t0, 1), "s; a", int((imp.scores > 0).sum()),
+          "b", [int((s > 0).sum()) for s in sc], "c", [len(s) for s in kept])
+    return out
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     t0 = time.time()
     np.savez_compressed(os.path.join(OUT, "cases.npz"), **make_cases())
     print("cases", round(time.time() - t0, 1), "s")
     np.savez_compressed(os.path.join(OUT, "config1.npz"), **make_config1())
+    np.savez_compressed(os.path.join(OUT, "importance.npz"), **make_importance())
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)) // 1024, "KiB")
 

@@ -242,6 +242,20 @@ def rasterize(batch, w, h, cfg: RasterCfg, need_image=True, record_max=True, lis
     return out
 
 
+def importance(levels, sets, cameras, cfg: RasterCfg):
+    """score_active_selection (src/lod.py:95-122) over the given, already
+    perturbed views: per view project every level's set with shade=False,
+    concat, rasterize with need_image=False / record_max_weight=True, and
+    keep the running np.maximum of per_gaussian_max_weight.  Returns one
+    score array per level."""
+    offsets = np.cumsum([0] + [len(s) for s in sets])
+    scores = np.zeros(offsets[-1])
+    for cam in cameras:
+        out = render_selection(levels, sets, None, cam, cfg, need_image=False, record_max=True)
+        np.maximum(scores, out["per_gaussian_max_weight"], out=scores)
+    return [scores[offsets[l]:offsets[l + 1]] for l in range(len(sets))]
+
+
 def render_selection(levels, sets, mods, camera: Camera, cfg: RasterCfg, need_image=True,
                      record_max=True, lists=False):
     """project_selection + rasterize (src/blending.py:132-137, src/lod.py:216-227)."""

@@ -16,6 +16,9 @@ from .blending import (blend_factor, compose_active, nearest_two_chunks, render_
                        render_selection, stream_step)
 from .renderer import Frame, Renderer
 from .device import default_precision, set_default_precision
+from .types import ImportanceScores, PerturbSpec
+from .importance import (compute_importance, random_rotations, score_active_selection,
+                         visibility_filter_chunk)
 
 __version__ = "0.1.0"
 
@@ -26,4 +29,6 @@ __all__ = [
     "tile_cover_counts", "visibility_histogram", "project_selection", "blend_factor",
     "compose_active", "nearest_two_chunks", "render_blend_state", "render_selection",
     "stream_step", "Frame", "Renderer", "default_precision", "set_default_precision",
+    "ImportanceScores", "PerturbSpec", "compute_importance", "random_rotations",
+    "score_active_selection", "visibility_filter_chunk",
 ]

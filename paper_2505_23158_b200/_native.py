@@ -23,6 +23,7 @@ PREC_FAST = 0
 PREC_EXACT = 1
 NEED_IMAGE = 1
 RECORD_MAX = 2
+ACCUMULATE_MAX = 4
 
 ERR = {-1: "BAD_ARG", -2: "CUDA", -3: "OOM", -4: "CAPACITY"}
 

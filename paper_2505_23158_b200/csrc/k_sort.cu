@@ -28,7 +28,10 @@ template <bool VALS, typename KI, typename KO, int MAP, int NB = 8>
 #ifndef LODGE_OS_MINB
 #define LODGE_OS_MINB 3
 #endif
-__global__ void __launch_bounds__(OS_THREADS, VALS ? 2 : LODGE_OS_MINB) k_onesweep(
+#ifndef LODGE_OS_VMINB
+#define LODGE_OS_VMINB 2
+#endif
+__global__ void __launch_bounds__(OS_THREADS, VALS ? LODGE_OS_VMINB : LODGE_OS_MINB) k_onesweep(
     const KI *__restrict__ kin, KO *__restrict__ kout, const uint32_t *__restrict__ vin,
     uint32_t *__restrict__ vout, const uint32_t *n_ptr, int shift, int sb,
     const uint32_t *__restrict__ digit_off, uint64_t *status, FrameState *fs, int tk) {

@@ -311,7 +311,8 @@ int lodge_rasterize(lodge_ctx *c, const lodge_batch *b, int64_t M, int64_t n_inp
   *c->cam_host = *cam;
   CK(cudaMemcpyAsync(c->cam_dev, c->cam_host, sizeof(lodge_camera), cudaMemcpyHostToDevice, s));
   const bool exact = c->precision == LODGE_PREC_EXACT;
-  if ((flags & LODGE_RECORD_MAX) && out->maxw_dev && n_inputs > 0)
+  if ((flags & LODGE_RECORD_MAX) && !(flags & LODGE_ACCUMULATE_MAX) && out->maxw_dev &&
+      n_inputs > 0)
     CK(cudaMemsetAsync(out->maxw_dev, 0, (exact ? 8 : 4) * (size_t)n_inputs, s));
   int32_t nl = 0;
   launch_begin_frame(c->fs, s);
@@ -390,7 +391,7 @@ int lodge_render_frame(lodge_ctx *c, const lodge_level *levels, int32_t n_levels
   c->mark(1);
   launch_union(*ch, ls, c->fs, w.status, w.union_idx, w.union_tag, s); nl += 2;
   c->mark(2);
-  if ((flags & LODGE_RECORD_MAX) && out->maxw_dev)
+  if ((flags & LODGE_RECORD_MAX) && !(flags & LODGE_ACCUMULATE_MAX) && out->maxw_dev)
     CK(cudaMemsetAsync(out->maxw_dev, 0, (exact ? 8 : 4) * (size_t)U_cap, s));
   rc = launch_project_frame(levels, ls, w, c->fs, cam_dev, *rp, (flags & LODGE_NEED_IMAGE) ? 1 : 0,
                             exact, s);

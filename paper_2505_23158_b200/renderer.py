@@ -130,16 +130,21 @@ class Renderer:
         return torch.from_numpy(host).to(self.device)
 
     def render(self, cam_row: torch.Tensor, frame: Frame, pair=None, t: float = None,
-               need_image: bool = True, record_max: bool = True, slot: int = 0) -> Frame:
+               need_image: bool = True, record_max: bool = True, slot: int = 0,
+               accumulate_max: bool = False) -> Frame:
         """Enqueue one frame on slot `slot`'s stream (the current stream for a
         single-slot renderer).  cam_row: one row of upload_cameras().
-        pair=None: nearest two chunks chosen on device."""
+        pair=None: nearest two chunks chosen on device.  accumulate_max: max
+        this frame's per-input weights into frame.maxw instead of resetting it
+        (a device-side max over views, src/lod.py:95-131)."""
         out = N.FrameOut()
         out.image_dev = frame.image.data_ptr() if (need_image and frame.image is not None) else None
         out.tile_count_dev = frame.tile_count.data_ptr()
         out.visible_dev = frame.visible.data_ptr()
         out.maxw_dev = frame.maxw.data_ptr() if (record_max and frame.maxw is not None) else None
         flags = (N.NEED_IMAGE if need_image else 0) | (N.RECORD_MAX if record_max else 0)
+        if accumulate_max:
+            flags |= N.ACCUMULATE_MAX
         pr = None
         tv = None
         if pair is not None:
