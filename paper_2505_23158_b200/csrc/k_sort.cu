@@ -7,10 +7,10 @@
 //   2. duplicated (tile<<32 | splat) pairs by tile id only, stable, which is
 //      np.argsort(tile_ids, kind="stable") over pairs emitted in depth order.
 // One partition per CTA: keys in registers in warp-contiguous order, stable
-// warp-level ranking with __match_any_sync over two independent counter
-// chains per warp (ILP), per-digit decoupled look-back across partitions
-// (virtual partition ids from an atomic ticket for forward progress), then a
-// shared-memory staged, digit-run-coalesced scatter.
+// warp-level ranking by per-bit ballots over two independent counter chains
+// per warp (ILP), per-digit decoupled look-back across partitions (virtual
+// partition ids from an atomic ticket for forward progress), then a
+// shared-memory staged, digit-run-coalesced scatter (onesweep.cuh).
 #include <algorithm>
 
 #include "internal.cuh"
@@ -36,7 +36,8 @@ __global__ void __launch_bounds__(OS_THREADS, VALS ? LODGE_OS_VMINB : LODGE_OS_M
     uint32_t *__restrict__ vout, const uint32_t *n_ptr, int shift, int sb,
     const uint32_t *__restrict__ digit_off, uint64_t *status, FrameState *fs, int tk) {
   extern __shared__ __align__(16) uint8_t smem[];
-  OSmem<OS_ITEMS, VALS, KI> &S = *reinterpret_cast<OSmem<OS_ITEMS, VALS, KI> *>(smem);
+  using Smem = OSmem<OS_ITEMS, VALS, KI, (1 << NB)>;
+  Smem &S = *reinterpret_cast<Smem *>(smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) S.misc[0] = atomicAdd(&fs->tickets[tk], 1u);
   __syncthreads();
@@ -109,7 +110,7 @@ static void os_launch(unsigned grid, cudaStream_t s, const KI *kin, KO *kout, co
                       uint32_t *vout, const uint32_t *n_ptr, int shift, int sb,
                       const uint32_t *digit_off, uint64_t *status, FrameState *fs, int tk) {
   static bool done = false;
-  const size_t sm = sizeof(OSmem<OS_ITEMS, VALS, KI>);
+  const size_t sm = sizeof(OSmem<OS_ITEMS, VALS, KI, (1 << NB)>);
   if (!done) {
     cudaFuncSetAttribute(k_onesweep<VALS, KI, KO, MAP, NB>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -1,7 +1,9 @@
 // One onesweep partition (the radix passes of k_sort.cu).  Input keys KI are
-// ranked on an 8-bit digit (k >> shift) & 255 of which only the low nb bits
-// can be non-zero (fewer ballots per item); the scatter writes kmap(key),
-// which lets a pass narrow the key it hands to the next one.
+// ranked on the digit (k >> shift) & (D - 1), D = 2^NB <= 256 (a pass whose
+// digit has fewer significant bits ranks with fewer ballots and does all of
+// its per-digit work -- counters, scans, look-back -- over D digits only);
+// the scatter writes kmap(key), which lets a pass narrow the key it hands to
+// the next one.
 #pragma once
 #include <type_traits>
 
@@ -10,11 +12,7 @@
 namespace lodge {
 
 constexpr int OS_THREADS = 256;
-constexpr int OS_WSTRIDE = 257;  // per-warp digit counters (+1 bucket for invalid items)
 
-// Lanes holding the same digit d from NB ballots (+1 on bit 8, which marks
-// invalid items, when the partition is ragged): cheaper than MATCH.ANY, whose
-// latency dominated the ranking.
 // peers &= lanes whose bit (d & MASK) equals this lane's (bit test, ballot and
 // two predicated ANDs; nvcc's own lowering spends six instructions here).
 template <uint32_t MASK>
@@ -30,6 +28,9 @@ __device__ __forceinline__ void peer_bit(uint32_t &peers, uint32_t d) {
       : "r"(d), "n"(MASK));
 }
 
+// Lanes holding the same digit d from NB ballots, plus one on bit NB (which
+// marks invalid items, d = D) when the partition is ragged: cheaper than
+// MATCH.ANY, whose latency dominated the ranking.
 template <int NB, bool CHECKV>
 __device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
   uint32_t peers = FULL_MASK;
@@ -41,17 +42,17 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
   if (NB > 5) peer_bit<32u>(peers, d);
   if (NB > 6) peer_bit<64u>(peers, d);
   if (NB > 7) peer_bit<128u>(peers, d);
-  if (CHECKV) peer_bit<256u>(peers, d);
+  if (CHECKV) peer_bit<(1u << NB)>(peers, d);
   return peers;
 }
 
-template <int ITEMS, bool VALS, typename KI = uint64_t>
+template <int ITEMS, bool VALS, typename KI, int D>
 struct OSmem {
   KI keys[OS_THREADS * ITEMS];
   uint32_t vals[VALS ? OS_THREADS * ITEMS : 1];
-  uint32_t whist[2][OS_THREADS / 32][OS_WSTRIDE];  // two ranking chains per warp
-  uint32_t dstart[256];
-  uint32_t gbase[256];
+  uint32_t whist[2][OS_THREADS / 32][D + 1];  // two ranking chains per warp (+ invalid bucket)
+  uint32_t dstart[D];
+  uint32_t gbase[D];
   uint32_t misc[32];
   uint16_t rank[OS_THREADS * ITEMS];
 };
@@ -63,18 +64,21 @@ struct OSmem {
 // vmask marks valid items; cnt_valid = number of valid elements, which are
 // the partition's first cnt_valid.  Writes keys (and vget(li) values) to
 // their digit-sorted global positions digit_off[d] + prefix + local rank.
+// Look-back status words: D per partition.
 template <int ITEMS, int NB, bool VALS, typename KI, typename KO, typename KMap, typename VGet>
-__device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI> &S, KI (&k)[ITEMS],
-                                                   uint32_t vmask, uint32_t part,
-                                                   uint32_t cnt_valid, int shift,
+__device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI, (1 << NB)> &S,
+                                                   KI (&k)[ITEMS], uint32_t vmask,
+                                                   uint32_t part, uint32_t cnt_valid, int shift,
                                                    const uint32_t *__restrict__ digit_off,
                                                    uint64_t *status, uint32_t epoch,
                                                    KO *__restrict__ kout, KMap kmap,
                                                    uint32_t *__restrict__ vout, VGet vget) {
   static_assert(ITEMS % 2 == 0, "two ranking chains");
+  static_assert(NB >= 1 && NB <= 8, "digit of 1..8 bits");
   constexpr int H = ITEMS / 2;
+  constexpr uint32_t D = 1u << NB, DM = D - 1u;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < 2 * (OS_THREADS / 32) * OS_WSTRIDE; i += OS_THREADS)
+  for (int i = tid; i < 2 * (OS_THREADS / 32) * (int)(D + 1); i += OS_THREADS)
     (&S.whist[0][0][0])[i] = 0;
   __syncthreads();
   uint32_t *wh0 = S.whist[0][warp], *wh1 = S.whist[1][warp];
@@ -82,9 +86,9 @@ __device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI> &S, KI
     constexpr bool CV = decltype(ragged)::value;
 #pragma unroll
     for (int i = 0; i < H; ++i) {
-      const uint32_t d0 = (!CV || ((vmask >> i) & 1u)) ? (uint32_t)((k[i] >> shift) & 255u) : 256u;
+      const uint32_t d0 = (!CV || ((vmask >> i) & 1u)) ? (uint32_t)((k[i] >> shift) & DM) : D;
       const uint32_t d1 =
-          (!CV || ((vmask >> (i + H)) & 1u)) ? (uint32_t)((k[i + H] >> shift) & 255u) : 256u;
+          (!CV || ((vmask >> (i + H)) & 1u)) ? (uint32_t)((k[i + H] >> shift) & DM) : D;
       const uint32_t p0 = digit_peers<NB, CV>(d0);
       const uint32_t p1 = digit_peers<NB, CV>(d1);
       const uint32_t c0 = wh0[d0], c1 = wh1[d1];
@@ -100,64 +104,72 @@ __device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI> &S, KI
   if (cnt_valid == (uint32_t)(OS_THREADS * ITEMS)) rank_items(std::false_type{});
   else rank_items(std::true_type{});
   __syncthreads();
-  // per digit: exclusive offsets over (warp, chain) and the partition total
-  const uint32_t dg = tid;  // 256 threads == 256 digits
+  // thread dg < D: digit dg's exclusive offsets over (warp, chain), its
+  // partition total, then its look-back across partitions
+  const uint32_t dg = tid;
   uint32_t tot = 0;
+  if (dg < D) {
 #pragma unroll
-  for (int w = 0; w < OS_THREADS / 32; ++w) {
-    const uint32_t a = S.whist[0][w][dg], b = S.whist[1][w][dg];
-    S.whist[0][w][dg] = tot;
-    S.whist[1][w][dg] = tot + a;
-    tot += a + b;
-  }
-  // publish aggregate, then look back LB partitions per round trip
-  uint64_t *st = status + (size_t)part * 256;
-  uint32_t excl = 0;
-  if (part == 0) {
-    st_store(st + dg, st_pack(epoch, ST_PREFIX, tot));
-  } else {
-    st_store(st + dg, st_pack(epoch, ST_AGG, tot));
-    constexpr int LB = 8;
-    int64_t q = (int64_t)part - 1;
-    bool done = false;
-    while (!done) {
-      uint64_t sv[LB];
-#pragma unroll
-      for (int i = 0; i < LB; ++i)
-        sv[i] = (q - i >= 0) ? st_load(status + (size_t)(q - i) * 256 + dg)
-                             : st_pack(epoch, ST_PREFIX, 0u);
-#pragma unroll
-      for (int i = 0; i < LB; ++i) {
-        if (done) break;
-        const uint32_t flag =
-            ((uint32_t)(sv[i] >> 32) == epoch) ? (uint32_t)((sv[i] >> 30) & 3u) : 0u;
-        if (flag == ST_EMPTY) break;  // retry from partition q
-        excl += (uint32_t)(sv[i] & 0x3fffffffu);
-        --q;
-        if (flag == ST_PREFIX) done = true;
-      }
+    for (int w = 0; w < OS_THREADS / 32; ++w) {
+      const uint32_t a = S.whist[0][w][dg], b = S.whist[1][w][dg];
+      S.whist[0][w][dg] = tot;
+      S.whist[1][w][dg] = tot + a;
+      tot += a + b;
     }
-    st_store(st + dg, st_pack(epoch, ST_PREFIX, excl + tot));
-  }
-  S.gbase[dg] = digit_off[dg] + excl;
-  uint32_t inc = tot;  // partition-local exclusive scan of the digit totals
+    uint64_t *st = status + (size_t)part * D;
+    uint32_t excl = 0;
+    if (part == 0) {
+      st_store(st + dg, st_pack(epoch, ST_PREFIX, tot));
+    } else {
+      st_store(st + dg, st_pack(epoch, ST_AGG, tot));
+      constexpr int LB = 8;  // partitions read per round trip
+      int64_t q = (int64_t)part - 1;
+      bool done = false;
+      while (!done) {
+        uint64_t sv[LB];
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
-    if (lane >= o) inc += t;
-  }
-  if (lane == 31) S.misc[1 + warp] = inc;
-  __syncthreads();
-  uint32_t wpre = 0;
+        for (int i = 0; i < LB; ++i)
+          sv[i] = (q - i >= 0) ? st_load(status + (size_t)(q - i) * D + dg)
+                               : st_pack(epoch, ST_PREFIX, 0u);
 #pragma unroll
-  for (int w = 0; w < OS_THREADS / 32; ++w) wpre += (w < warp) ? S.misc[1 + w] : 0u;
-  S.dstart[dg] = wpre + inc - tot;
+        for (int i = 0; i < LB; ++i) {
+          if (done) break;
+          const uint32_t flag =
+              ((uint32_t)(sv[i] >> 32) == epoch) ? (uint32_t)((sv[i] >> 30) & 3u) : 0u;
+          if (flag == ST_EMPTY) break;  // retry from partition q
+          excl += (uint32_t)(sv[i] & 0x3fffffffu);
+          --q;
+          if (flag == ST_PREFIX) done = true;
+        }
+      }
+      st_store(st + dg, st_pack(epoch, ST_PREFIX, excl + tot));
+    }
+    S.gbase[dg] = digit_off[dg] + excl;
+  }
+  // partition-local exclusive scan of the digit totals (zero beyond D)
+  constexpr int DW = (int)((D + 31) / 32);  // warps holding digits
+  uint32_t inc = tot;
+  if (warp < DW) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (DW > 1 && lane == 31) S.misc[1 + warp] = inc;
+  }
+  if (DW > 1) __syncthreads();
+  if (dg < D) {
+    uint32_t wpre = 0;
+#pragma unroll
+    for (int w = 0; w < DW; ++w) wpre += (w < warp) ? S.misc[1 + w] : 0u;
+    S.dstart[dg] = wpre + inc - tot;
+  }
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     if ((vmask >> i) & 1u) {
       const uint32_t li = warp * (ITEMS * 32) + i * 32 + lane;
-      const uint32_t di = (uint32_t)((k[i] >> shift) & 255u);
+      const uint32_t di = (uint32_t)((k[i] >> shift) & DM);
       const uint32_t lp = S.dstart[di] + S.whist[i < H ? 0 : 1][warp][di] + S.rank[li];
       S.keys[lp] = k[i];
       if (VALS) S.vals[lp] = vget(li);
@@ -166,7 +178,7 @@ __device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI> &S, KI
   __syncthreads();
   for (uint32_t j = tid; j < cnt_valid; j += OS_THREADS) {
     const KI key = S.keys[j];
-    const uint32_t dd = (uint32_t)((key >> shift) & 255u);
+    const uint32_t dd = (uint32_t)((key >> shift) & DM);
     const uint32_t out = S.gbase[dd] + (j - S.dstart[dd]);
     kout[out] = kmap(key);
     if (VALS) vout[out] = S.vals[j];
