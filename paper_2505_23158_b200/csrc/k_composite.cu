@@ -4,27 +4,30 @@
 // One CTA per 16x16 tile (heaviest tiles first).  FAST: 64 threads, 4 pixels
 // per thread, each warp owning a 16x8 pixel block; EXACT: 128 threads, 2
 // pixels per thread, 16x4 blocks.  The tile's sorted member list is consumed
-// in batches of 256 members through a two-stage TMA pipeline: for batch b+1
-// each thread issues cp.async.bulk copies of its members' 64 B payloads
-// (plus the 64 B fp64 records in EXACT mode) into the idle shared-memory
-// stage, completing on that stage's mbarrier, while the warps composite batch
-// b.  After a stage lands each member's mean is converted once to tile-local
-// fp32 in place.  Each warp then compacts (8 ballots) the members whose
-// ellipse can reach one of its pixel centres -- the minimum of the quadratic
-// form over the block's centre rectangle against the member's cut-off -- and
-// walks only those, in list order.  Warp votes stop a warp when all its
-// pixels have T < t_min and the CTA when all pixels have (the reference's
-// per-block break is the same per-pixel rule).  Per-member max weights reduce
-// in-warp with redux.sync, per CTA with shared-memory atomics, then one global
-// atomicMax on the float bits per member and batch.
+// in batches (128 members FAST, 256 EXACT) through a two-stage TMA pipeline:
+// for batch b+1 each thread issues cp.async.bulk copies of its members' 64 B
+// payloads (plus the 64 B fp64 records in EXACT mode) into the idle
+// shared-memory stage, completing on that stage's mbarrier, while the warps
+// composite batch b.  After a stage lands each member's mean is converted
+// once to tile-local fp32 in place.  Each warp then compacts (ballots) the
+// members whose ellipse can reach one of its pixel centres -- the extremum of
+// the quadratic form over the block's centre rectangle against the member's
+// cut-off -- and walks only those, in list order.  Warp votes stop a warp
+// when all its pixels have T < t_min and the CTA when all pixels have (the
+// reference's per-block break is the same per-pixel rule).  Per-member max
+// weights reduce in-warp with redux.sync, per CTA with shared-memory atomics,
+// then one global atomicMax on the float bits per member and batch.
 //
-// FAST: fp32 FMA/MUFU, branch-free.  Both skip tests of src/raster.py:356
-// are folded into one per-splat cut-off q_eff on the quadratic form; pixels
-// whose fp32 q lies within the splat's error bound of q_eff re-decide in fp64
-// with the reference's operation order (rare, warp-voted branch), so skip
-// decisions match the fp64 reference.  EXACT: fp64, reproducing the blocked
-// cumprod transmittance of the reference (blocks of 1024 members), so
-// per_pixel_visible and max weights match it to the ulp of exp.
+// FAST: fp32 FMA/MUFU.  Both skip tests of src/raster.py:356 are folded into
+// one per-splat cut-off on the quadratic form, stored with the conic in
+// exponent units (internal.cuh Payload) as a guard band [lo, hi]; pixels
+// whose fp32 value lies in the band re-decide in fp64 with the reference's
+// operation order (rare, warp-voted branch), so skip decisions match the fp64
+// reference.  The list is walked in groups of LODGE_COMP_GROUP members: their
+// quadratic forms and alphas first (independent of T), then the blends in
+// order.  EXACT: fp64, reproducing the blocked cumprod transmittance of the
+// reference (blocks of 1024 members), so per_pixel_visible and max weights
+// match it to the ulp of exp.
 // Compiled with -fmad=false; the fast path fuses explicitly with fmaf.
 #include "internal.cuh"
 
