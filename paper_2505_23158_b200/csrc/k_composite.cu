@@ -75,13 +75,16 @@ __device__ __forceinline__ bool ellipse_meets_block(float mx, float my, float A,
   if (mx >= xlo && mx <= xhi && my >= ylo && my <= yhi) return true;
   const float ex0 = xlo - mx, ex1 = xhi - mx, ey0 = ylo - my, ey1 = yhi - my;
   float qmax = -INFINITY;
+  // an approximate extremal coordinate only lowers the evaluated maximum at
+  // second order (C * err^2), far inside the margin below
+  const float hc = __fdividef(-0.5f * B2, C), ha = __fdividef(-0.5f * B2, A);
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
     const float dx = s ? ex1 : ex0;  // vertical edge: extremise over dy
-    const float dy = fminf(fmaxf(-B2 * dx / (2.f * C), ey0), ey1);
+    const float dy = fminf(fmaxf(hc * dx, ey0), ey1);
     qmax = fmaxf(qmax, A * dx * dx + B2 * dx * dy + C * dy * dy);
     const float dy2 = s ? ey1 : ey0;  // horizontal edge: extremise over dx
-    const float dx2 = fminf(fmaxf(-B2 * dy2 / (2.f * A), ex0), ex1);
+    const float dx2 = fminf(fmaxf(ha * dy2, ex0), ex1);
     qmax = fmaxf(qmax, A * dx2 * dx2 + B2 * dx2 * dy2 + C * dy2 * dy2);
   }
   return !(qmax < lo - 1e-3f * (1.f + fabsf(lo)));  // NaN -> meets
