@@ -18,8 +18,18 @@
 
 namespace lodge {
 
-constexpr int OS_ITEMS = 16;
-constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096 keys per partition
+#ifndef LODGE_OS_ITEMS_T1
+#define LODGE_OS_ITEMS_T1 16
+#endif
+#ifndef LODGE_OS_ITEMS_T2
+#define LODGE_OS_ITEMS_T2 32
+#endif
+// Keys per thread: 16 for the depth passes (key + value), per-build choices
+// for the tile passes on u64 and u32 keys.
+template <bool VALS, typename KI>
+__host__ __device__ constexpr int os_items() {
+  return VALS ? 16 : (sizeof(KI) == 8 ? LODGE_OS_ITEMS_T1 : LODGE_OS_ITEMS_T2);
+}
 
 // Key maps applied at the scatter (see launch_tile_sort).
 enum : int { MAP_ID = 0, MAP_PACK = 1, MAP_LOW = 2 };
@@ -31,11 +41,19 @@ template <bool VALS, typename KI, typename KO, int MAP, int NB = 8>
 #ifndef LODGE_OS_VMINB
 #define LODGE_OS_VMINB 2
 #endif
-__global__ void __launch_bounds__(OS_THREADS, VALS ? LODGE_OS_VMINB : LODGE_OS_MINB) k_onesweep(
+#ifndef LODGE_OS_MINB_T1
+#define LODGE_OS_MINB_T1 LODGE_OS_MINB
+#endif
+__global__ void __launch_bounds__(OS_THREADS, VALS ? LODGE_OS_VMINB
+                                                   : (sizeof(KI) == 8 ? LODGE_OS_MINB_T1
+                                                                      : LODGE_OS_MINB))
+    k_onesweep(
     const KI *__restrict__ kin, KO *__restrict__ kout, const uint32_t *__restrict__ vin,
     uint32_t *__restrict__ vout, const uint32_t *n_ptr, int shift, int sb,
     const uint32_t *__restrict__ digit_off, uint64_t *status, FrameState *fs, int tk) {
   extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int OS_ITEMS = os_items<VALS, KI>();
+  constexpr uint32_t OS_TILE = OS_THREADS * OS_ITEMS;
   using Smem = OSmem<OS_ITEMS, VALS, KI, (1 << NB)>;
   Smem &S = *reinterpret_cast<Smem *>(smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -106,11 +124,13 @@ __global__ void k_depth_scan(FrameState *fs) {
 
 // One onesweep pass (dynamic shared memory opted in once per instantiation).
 template <bool VALS, typename KI, typename KO, int MAP, int NB>
-static void os_launch(unsigned grid, cudaStream_t s, const KI *kin, KO *kout, const uint32_t *vin,
+static void os_launch(int64_t cap, cudaStream_t s, const KI *kin, KO *kout, const uint32_t *vin,
                       uint32_t *vout, const uint32_t *n_ptr, int shift, int sb,
                       const uint32_t *digit_off, uint64_t *status, FrameState *fs, int tk) {
+  constexpr int64_t TILE = (int64_t)OS_THREADS * os_items<VALS, KI>();
+  const unsigned grid = (unsigned)((cap + TILE - 1) / TILE);
   static bool done = false;
-  const size_t sm = sizeof(OSmem<OS_ITEMS, VALS, KI, (1 << NB)>);
+  const size_t sm = sizeof(OSmem<os_items<VALS, KI>(), VALS, KI, (1 << NB)>);
   if (!done) {
     cudaFuncSetAttribute(k_onesweep<VALS, KI, KO, MAP, NB>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -140,11 +160,10 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
   k_depth_hist<<<hist_blocks, 256, 0, s>>>(w.key_depth[0], fs);
   k_depth_scan<<<1, 256, 0, s>>>(fs);
   *launches += 2;
-  const unsigned grid = (unsigned)((M_cap + OS_TILE - 1) / OS_TILE);
   for (int p = 0; p < 8; ++p) {
     const int a = p & 1;
     os_launch<true, uint64_t, uint64_t, MAP_ID, 8>(
-        grid, s, (const uint64_t *)w.key_depth[a], w.key_depth[a ^ 1],
+        M_cap, s, (const uint64_t *)w.key_depth[a], w.key_depth[a ^ 1],
         (const uint32_t *)w.val_depth[a], w.val_depth[a ^ 1], &fs->n_sort, 8 * p, 32,
         fs->off_depth[p], w.status, fs, TK_DEPTH0 + p);
     ++*launches;
@@ -167,7 +186,7 @@ static int bit_width(uint64_t v) {
 // Tile ranges come from tile_start, so the lists need no tile bits.
 void launch_tile_sort(Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
                       int32_t *launches, cudaStream_t s) {
-  const unsigned grid = (unsigned)((w.P_cap + OS_TILE - 1) / OS_TILE);
+  const int64_t grid = w.P_cap;  // keys: the launchers size their grids
   const uint32_t T = (uint32_t)tiles_x * (uint32_t)tiles_y;
   const int lo_bits = std::min(8, std::max(1, bit_width(T - 1)));
   uint32_t *u32_1 = reinterpret_cast<uint32_t *>(w.pairs[1]);
