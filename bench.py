@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--views-per-step", type=int, default=BLOCK)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--streams", type=int, default=2,
+    ap.add_argument("--streams", type=int, default=4,
                     help="frames in flight per GPU (one liblodge context + stream each)")
     ap.add_argument("--cpu-views", type=int, default=1, help="views in the CPU baseline sample")
     return ap.parse_args()
