@@ -55,9 +55,12 @@ typedef struct {
  *       filter_variance], fp64 (96 B) or fp32 (48 B) per LODGE_GEOM_FP32.
  * sh:   (n, 3, (deg+1)^2) coefficients, fp64 or fp32 per LODGE_SH_FP32.
  * Arithmetic is fp64 either way (fp32 storage is the asset's native
- * precision, src/assets.py:240-254). */
+ * precision, src/assets.py:240-254).  LODGE_GEOM_QNORM: the stored rotations
+ * are the asset's raw values, normalised in fp64 when read, exactly as
+ * read_asset does at load time (src/assets.py:275-278). */
 #define LODGE_GEOM_FP32 1
 #define LODGE_SH_FP32 2
+#define LODGE_GEOM_QNORM 4
 typedef struct {
   int64_t n;
   int32_t sh_degree;
@@ -221,6 +224,29 @@ int32_t lodge_last_launch_count(lodge_ctx *ctx);
  * [1] warp iterations, [2] iterations with a pixel inside the cut-off,
  * [3] pixel evaluations inside the cut-off, [4] warp-batches. */
 int lodge_debug_counters(lodge_ctx *ctx, uint64_t *out8);
+
+/* ---- asset upload -------------------------------
+ * replaces the decode + value checks of _parse_level_blob, src/assets.py:
+ * 257-282, on the device.  blob_dev: one level's data.bin blob already in
+ * device memory, n little-endian fp32 records [mean3, scale3, rot4, opacity,
+ * fv, sh 3*(deg+1)^2] (src/assets.py:240-254).  Splits them into the
+ * level store (geom_dev: n x 12 fp32, raw rotations -- render the level with
+ * LODGE_GEOM_QNORM; sh_dev: n x 3 x (deg+1)^2 fp32) and checks every record.
+ * Synchronous; *violations gets the checks that failed, in the reference's
+ * order of raising: */
+#define LODGE_ASSET_NONFINITE 1 /* "level blob contains non-finite values" */
+#define LODGE_ASSET_SCALE 2     /* "... non-positive scales" */
+#define LODGE_ASSET_OPACITY 4   /* "... out-of-range opacity" */
+#define LODGE_ASSET_FV 8        /* "... negative filter variance" */
+#define LODGE_ASSET_ROTATION 16 /* "... non-unit rotations" (| |q| - 1 | > 1e-3) */
+int lodge_asset_split(lodge_ctx *ctx, const void *blob_dev, int64_t n, int32_t sh_degree,
+                      float *geom_dev, float *sh_dev, int32_t *violations);
+
+/* Index-set checks of read_asset (src/assets.py:448-453) for every set of
+ * a chunk plan: set_flags (K*L, host) gets bit 0 if set (j, l) is not
+ * strictly increasing, bit 1 if an index is >= level_sizes[l] (host, L). */
+int lodge_asset_check_sets(lodge_ctx *ctx, const lodge_chunks *chunks,
+                           const int64_t *level_sizes, int32_t *set_flags);
 
 #ifdef __cplusplus
 }

@@ -273,6 +273,85 @@ def make_importance():
     return out
 
 
+ASSET_CORRUPTIONS = [
+    # (name, kind, args) applied by tests/asset_util.py corrupt(); the
+    # reference's read_asset message for each is recorded below
+    ("nan_mean", "f32", ("L0", 5, 0, "nan")),
+    ("neg_scale", "f32", ("L0", 7, 4, -0.5)),
+    ("opacity_gt1", "f32", ("L1", 3, 10, 1.5)),
+    ("neg_fv", "f32", ("L1", 0, 11, -1.0)),
+    ("bad_rot", "f32", ("L0", 11, 6, 3.0)),
+    ("nan_sh", "f32", ("L1", 9, 13, "inf")),
+    ("unsorted_set", "u32swap", (1, 0, 2)),
+    ("set_oob", "u32set", (2, 1, -1, 4076)),
+    ("bad_version", "manifest", ("format_version", 2)),
+    ("bad_degree", "manifest", ("sh_degree", 5)),
+    ("count_mismatch", "level_field", (1, "gaussian_count", 4075)),
+    ("prov_mismatch", "level_field", (0, "provenance_length", 4)),
+    ("range_overflow", "level_field", (1, "length", 10 ** 9)),
+    ("set_count", "set_field", (3, 1, "count", 1)),
+    ("missing_sets", "drop_set", (2,)),
+    ("bad_magic", "container_magic", ()),
+    ("bad_container_version", "container_version", (9,)),
+    ("short_container", "container_truncate", (10,)),
+    ("bad_json", "manifest_bytes", (b"{not json",)),
+]
+
+
+def make_asset():
+    """config-1 levels + plan written by the reference's write_asset
+    (directory and container), read_asset's error message for each entry of
+    ASSET_CORRUPTIONS, and two views rendered from the reference's
+    read_asset result (the asset stores fp32 and normalises rotations)."""
+    import json
+    import shutil
+    import splatlod.assets as A
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests"))
+    import asset_util as AU
+    d, levels, cams, plan = _config1_objects()
+    plan = ChunkPlan(plan.centers, plan.radii, plan.active_sets,
+                     np.array([0, 0, 1, 1, 2, 2, 3, 3], np.int64))
+    adir = os.path.join(OUT, "asset_c1")
+    shutil.rmtree(adir, ignore_errors=True)
+    A.write_asset(adir, levels, plan, sh_degree=int(levels[0].scene.sh_degree),
+                  reference_focal=104.0, filter_scale=1.0, gamma=LodBuildConfig().gamma,
+                  seeds={"golden": 7}, config_hash="golden")
+    msgs = {}
+    tmp = os.path.join("/tmp", "lodge_asset_corrupt")
+    for name, kind, args in ASSET_CORRUPTIONS:
+        shutil.rmtree(tmp, ignore_errors=True)
+        path = AU.corrupt(adir, tmp, kind, args)
+        try:
+            A.read_asset(path)
+            msgs[name] = ""
+        except A.AssetError as e:
+            msgs[name] = str(e).replace(str(path), "<path>")
+    out = {"messages": np.array(json.dumps(msgs))}
+    asset = A.read_asset(adir)
+    rc = R.RasterConfig()
+    for v in (1, 6):
+        cam = cams[v]
+        p = f"v{v}/"
+        f, o = nearest_two_chunks(asset.plan, cam.position)
+        t_bar, t = blend_factor(cam.position, asset.plan.centers[f], asset.plan.centers[o])
+        out[p + "pair"] = np.array([f, o])
+        out[p + "t"] = np.array([t_bar, t])
+        sel = compose_active(asset.plan, asset.levels, f, o, t)
+        batch = project_selection(asset.levels, sel.sets, cam, rc, modulations=sel.modulations)
+        res = R.rasterize(batch, cam, rc)
+        out[p + "image"] = res.image
+        out[p + "tile_count"] = res.per_tile_count
+        out[p + "visible"] = res.per_pixel_visible
+        out[p + "maxw"] = res.per_gaussian_max_weight
+        out[p + "src"] = batch.source_index
+        out[p + "depth"] = batch.depth
+    for l, lv in enumerate(asset.levels):
+        out[f"L{l}/rotations"] = lv.scene.rotations
+        out[f"L{l}/provenance"] = lv.provenance
+    print("asset", {k: v[:40] for k, v in msgs.items()})
+    return out
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     t0 = time.time()

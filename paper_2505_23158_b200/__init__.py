@@ -19,6 +19,7 @@ from .device import default_precision, set_default_precision
 from .types import ImportanceScores, PerturbSpec
 from .importance import (compute_importance, random_rotations, score_active_selection,
                          visibility_filter_chunk)
+from .asset import AssetError, DeviceAsset, load_asset
 
 __version__ = "0.1.0"
 
@@ -30,5 +31,6 @@ __all__ = [
     "compose_active", "nearest_two_chunks", "render_blend_state", "render_selection",
     "stream_step", "Frame", "Renderer", "default_precision", "set_default_precision",
     "ImportanceScores", "PerturbSpec", "compute_importance", "random_rotations",
-    "score_active_selection", "visibility_filter_chunk",
+    "score_active_selection", "visibility_filter_chunk", "AssetError", "DeviceAsset",
+    "load_asset",
 ]

@@ -19,6 +19,7 @@ CSRC = os.path.join(_HERE, "csrc")
 MAX_LEVELS = 8
 GEOM_FP32 = 1
 SH_FP32 = 2
+GEOM_QNORM = 4
 PREC_FAST = 0
 PREC_EXACT = 1
 NEED_IMAGE = 1
@@ -102,6 +103,10 @@ EXPORTS = {
     "lodge_to_srgb8": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p], C.c_int),
     "lodge_last_launch_count": ([C.c_void_p], C.c_int32),
     "lodge_debug_counters": ([C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
+    "lodge_asset_split": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
+                           C.POINTER(C.c_int32)], C.c_int),
+    "lodge_asset_check_sets": ([C.c_void_p, C.POINTER(Chunks), C.POINTER(C.c_int64),
+                                C.POINTER(C.c_int32)], C.c_int),
 }
 N_STAGES = 8
 STAGES = ("select", "union", "project", "depth_sort", "tile_setup", "duplicate", "tile_sort",

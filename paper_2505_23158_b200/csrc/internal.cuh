@@ -228,4 +228,8 @@ void launch_composite(const Work &w, FrameState *fs, const lodge_camera *cam_dev
                       const lodge_frame_out &out, uint32_t n_inputs_cap, cudaStream_t s);
 void launch_export_lists(const Work &w, FrameState *fs, int32_t T, int64_t *tile_offsets,
                          int64_t *tile_src, int64_t cap, cudaStream_t s);
+void launch_asset_split(const float *blob, int64_t n, int32_t width, float *geom, float *sh,
+                        int32_t *flags_dev, cudaStream_t s);
+void launch_asset_sets(const lodge_chunks &ch, const int64_t *level_size_dev, int32_t *flags_dev,
+                       cudaStream_t s);
 }  // namespace lodge

@@ -58,6 +58,17 @@ __device__ __forceinline__ void load_geom<float>(const float *__restrict__ g, do
   }
 }
 
+// read_asset's load-time normalisation of the raw asset rotations
+// (src/assets.py:275-278): q / np.linalg.norm(q), the norm summed in
+// add.reduce's order over the length-4 row.
+__device__ __forceinline__ void normalize_rot(double v[12]) {
+  const double nn = sqrt(((v[6] * v[6] + v[7] * v[7]) + v[8] * v[8]) + v[9] * v[9]);
+  v[6] = v[6] / nn;
+  v[7] = v[7] / nn;
+  v[8] = v[8] / nn;
+  v[9] = v[9] / nn;
+}
+
 // v: [mean3, scale3, rot4 wxyz, opacity, fv]
 __device__ __forceinline__ Proj project_core(const double v[12], const lodge_camera &cam,
                                              const lodge_raster_params &rp, double mod,
@@ -394,6 +405,7 @@ struct ProjLevels {
   const void *geom[LODGE_MAX_LEVELS];
   const void *sh[LODGE_MAX_LEVELS];
   int32_t degree[LODGE_MAX_LEVELS];
+  int32_t qnorm[LODGE_MAX_LEVELS];  // LODGE_GEOM_QNORM per level
   uint32_t slot_base[LODGE_MAX_LEVELS + 1];
   int32_t L;
 };
@@ -444,6 +456,7 @@ __global__ void __launch_bounds__(256, 2) k_project_frame(ProjLevels lv, Work w,
       const double t = s_t;
       const double mod = (tag == 3) ? 1.0 : (tag == 1 ? t : 1.0 - t);
       load_geom<GT>(reinterpret_cast<const GT *>(lv.geom[l]) + (size_t)gidx * 12, v);
+      if (lv.qnorm[l]) normalize_rot(v);
       p = project_core(v, cam, rp, mod, true);
     }
     const bool keep = valid && p.ok;
@@ -486,7 +499,7 @@ __global__ void __launch_bounds__(256) k_project_compat(const GT *geom, const ST
                                                         const double *mod, Work w, FrameState *fs,
                                                         const lodge_camera *__restrict__ cam_p,
                                                         lodge_raster_params rp, int32_t shade,
-                                                        lodge_batch out) {
+                                                        lodge_batch out, int32_t qnorm) {
   __shared__ uint32_t s_warp[32];
   __shared__ uint32_t s_base;
   __shared__ lodge_camera cam;
@@ -500,6 +513,7 @@ __global__ void __launch_bounds__(256) k_project_compat(const GT *geom, const ST
   if (e < n) {
     g = idx ? idx[e] : e;
     load_geom<GT>(geom + (size_t)g * 12, v);
+    if (qnorm) normalize_rot(v);
     p = project_core(v, cam, rp, mod ? mod[e] : 1.0, mod != nullptr);
   }
   const int64_t m = compact_slot(e < n && p.ok, w.status, fs->epoch + TK_COMPACT, part, s_warp,
@@ -587,12 +601,14 @@ int launch_project_frame(const lodge_level *levels, const LevelSlots &ls, const 
                          const lodge_raster_params &rp, int32_t shade, int32_t, cudaStream_t s) {
   ProjLevels lv;
   lv.L = ls.n_levels;
-  const int32_t fl = levels[0].flags;
+  const int32_t prec_bits = LODGE_GEOM_FP32 | LODGE_SH_FP32;
+  const int32_t fl = levels[0].flags & prec_bits;
   for (int l = 0; l < lv.L; ++l) {
-    if (levels[l].flags != fl) return -1;  // one storage precision per store
+    if ((levels[l].flags & prec_bits) != fl) return -1;  // one storage precision per store
     lv.geom[l] = levels[l].geom_dev;
     lv.sh[l] = levels[l].sh_dev;
     lv.degree[l] = levels[l].sh_degree;
+    lv.qnorm[l] = (levels[l].flags & LODGE_GEOM_QNORM) ? 1 : 0;
   }
   for (int l = 0; l <= LODGE_MAX_LEVELS; ++l) lv.slot_base[l] = l <= lv.L ? ls.slot_base[l] : 0;
   const uint32_t nslots = ls.slot_base[lv.L];
@@ -615,7 +631,8 @@ int launch_project_compat(const lodge_level &level, const int64_t *idx, int64_t 
 #define LP(GT, ST)                                                                         \
   k_project_compat<GT, ST><<<grid, 256, 0, s>>>((const GT *)level.geom_dev,                \
                                                 (const ST *)level.sh_dev, level.sh_degree, \
-                                                idx, n, mod, w, fs, cam_dev, rp, shade, *out)
+                                                idx, n, mod, w, fs, cam_dev, rp, shade, *out, \
+                                                (level.flags & LODGE_GEOM_QNORM) ? 1 : 0)
   if (g32 && s32) LP(float, float);
   else if (g32) LP(float, double);
   else if (s32) LP(double, float);

@@ -494,4 +494,51 @@ int lodge_debug_counters(lodge_ctx *c, uint64_t *out8) {
   return 0;
 }
 
+int lodge_asset_split(lodge_ctx *c, const void *blob_dev, int64_t n, int32_t sh_degree,
+                      float *geom_dev, float *sh_dev, int32_t *violations) {
+  if (!c || !violations || (n > 0 && (!blob_dev || !geom_dev || !sh_dev)))
+    return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  if (n < 0) return set_err(LODGE_ERR_BAD_ARG, "negative record count");
+  if (sh_degree < 0 || sh_degree > 3) return set_err(LODGE_ERR_BAD_ARG, "sh degree must be in 0..3");
+  *violations = 0;
+  if (n == 0) return 0;
+  CK(cudaSetDevice(c->device));
+  const int32_t width = 12 + 3 * (sh_degree + 1) * (sh_degree + 1);
+  int32_t *flags = nullptr;
+  CK(cudaMallocAsync(&flags, sizeof(int32_t), c->stream));
+  CK(cudaMemsetAsync(flags, 0, sizeof(int32_t), c->stream));
+  launch_asset_split(reinterpret_cast<const float *>(blob_dev), n, width, geom_dev, sh_dev,
+                     flags, c->stream);
+  const int rc = check_launch("lodge_asset_split");
+  CK(cudaMemcpyAsync(violations, flags, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaFreeAsync(flags, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return rc;
+}
+
+int lodge_asset_check_sets(lodge_ctx *c, const lodge_chunks *ch, const int64_t *level_sizes,
+                           int32_t *set_flags) {
+  if (!c || !ch || !level_sizes || !set_flags) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  if (ch->K < 0 || ch->L < 1 || ch->L > LODGE_MAX_LEVELS)
+    return set_err(LODGE_ERR_BAD_ARG, "bad chunk plan shape");
+  const int32_t nsets = ch->K * ch->L;
+  if (nsets == 0) return 0;
+  CK(cudaSetDevice(c->device));
+  int64_t *lsz = nullptr;
+  int32_t *flags = nullptr;
+  CK(cudaMallocAsync(&lsz, sizeof(int64_t) * ch->L, c->stream));
+  CK(cudaMallocAsync(&flags, sizeof(int32_t) * nsets, c->stream));
+  CK(cudaMemcpyAsync(lsz, level_sizes, sizeof(int64_t) * ch->L, cudaMemcpyHostToDevice,
+                     c->stream));
+  CK(cudaMemsetAsync(flags, 0, sizeof(int32_t) * nsets, c->stream));
+  launch_asset_sets(*ch, lsz, flags, c->stream);
+  const int rc = check_launch("lodge_asset_check_sets");
+  CK(cudaMemcpyAsync(set_flags, flags, sizeof(int32_t) * nsets, cudaMemcpyDeviceToHost,
+                     c->stream));
+  CK(cudaFreeAsync(lsz, c->stream));
+  CK(cudaFreeAsync(flags, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return rc;
+}
+
 }  // extern "C"

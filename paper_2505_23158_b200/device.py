@@ -220,6 +220,27 @@ class DevicePlan:
             self.struct.max_set[l] = int(self.max_set[l])
         return self
 
+    @classmethod
+    def from_tensor(cls, centers, offsets, data: torch.Tensor, L: int, device: torch.device):
+        """Like from_arrays, with the concatenated sets already a device
+        int32 tensor (the uint32 bit patterns), e.g. gathered by load_asset."""
+        self = cls.__new__(cls)
+        centers = np.ascontiguousarray(centers, np.float64)
+        offsets = np.ascontiguousarray(offsets, np.int64)
+        self.K, self.L = centers.shape[0], int(L)
+        self.centers = torch.from_numpy(centers).to(device)
+        self.offsets = torch.from_numpy(offsets).to(device)
+        self.data = data
+        self.max_set = np.diff(offsets).reshape(self.K, self.L).max(axis=0)
+        self.struct = N.Chunks()
+        self.struct.K, self.struct.L = self.K, self.L
+        self.struct.centers_dev = self.centers.data_ptr()
+        self.struct.offsets_dev = self.offsets.data_ptr()
+        self.struct.data_dev = self.data.data_ptr()
+        for l in range(self.L):
+            self.struct.max_set[l] = int(self.max_set[l])
+        return self
+
     @property
     def union_capacity(self) -> int:
         return int(2 * self.max_set.sum())
