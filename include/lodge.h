@@ -225,6 +225,18 @@ int32_t lodge_last_launch_count(lodge_ctx *ctx);
  * [3] pixel evaluations inside the cut-off, [4] warp-batches. */
 int lodge_debug_counters(lodge_ctx *ctx, uint64_t *out8);
 
+/* ---- threshold-search cost table ----------------
+ * replaces ThresholdSearcher._table, src/thresholds.py:80-90: project the
+ * level's inputs (idx_dev, or all n when NULL) with shade=False; for the M
+ * survivors, in input order, the tile cover count (tile_cover_counts,
+ * src/raster.py:316-324) and the fp64 camera distance ||mean - position||;
+ * stable sort by distance.  Writes dist_dev[0..M) (sorted distances) and
+ * prefix_dev[0..M] (0 then the running sum of the covers in that order,
+ * int64).  Capacities n and n+1.  Synchronous; *out_m = M. */
+int lodge_cover_table(lodge_ctx *ctx, const lodge_level *level, const int64_t *idx_dev,
+                      int64_t n, const lodge_camera *cam, const lodge_raster_params *rp,
+                      double *dist_dev, int64_t *prefix_dev, int64_t *out_m);
+
 /* ---- asset upload -------------------------------
  * replaces the decode + value checks of _parse_level_blob, src/assets.py:
  * 257-282, on the device.  blob_dev: one level's data.bin blob already in

@@ -352,6 +352,43 @@ def make_asset():
     return out
 
 
+def make_thresholds():
+    """Threshold-search cost tables on config-1 data:
+    the reference ThresholdSearcher over views 0-3 with the config-1 build
+    config; _table for the base level and for provisional levels at d1 and
+    2.5 d1 (built by the reference, stored so the tests need no LOD build),
+    and evaluate() of [d1] and [d1, 2.5 d1]."""
+    from splatlod.thresholds import ThresholdSearcher
+    d, levels, cams, plan = _config1_objects()
+    base = LodLevel.base(levels[0].scene)
+    cfg = LodBuildConfig(importance_views=tuple(cams), reference_focal=mean_focal(cams))
+    views = cams[0:4]
+    s = ThresholdSearcher(base, views, cfg)
+    d1 = float(d["thresholds"][0])
+    depths = [0.0, d1, 2.5 * d1]
+    out = {"depths": np.array(depths)}
+    t0 = time.time()
+    for k, dep in enumerate(depths):
+        lv = s.provisional_level(dep)
+        if k:
+            scene_arrays(lv.scene, f"P{k}/", out)
+            out[f"P{k}/provenance"] = lv.provenance
+        for vi in range(len(views)):
+            dist, prefix = s._table(dep, vi)
+            out[f"T{k}/{vi}/dist"] = dist
+            out[f"T{k}/{vi}/prefix"] = prefix
+    for name, ths in (("e1", [d1]), ("e2", [d1, 2.5 * d1])):
+        ev = s.evaluate(ths)
+        out[name + "/thresholds"] = np.array(ev.thresholds)
+        out[name + "/mean"] = np.array(ev.mean_gaussians_per_tile)
+        out[name + "/per_view"] = np.array(ev.per_view_cost)
+        out[name + "/build"] = np.array(ev.build_cost_proxy)
+    print("thresholds", round(time.time() - t0, 1), "s; levels",
+          [len(s.provisional_level(x)) for x in depths],
+          "mean cost", float(out["e1/mean"]), float(out["e2/mean"]))
+    return out
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     t0 = time.time()

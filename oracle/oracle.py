@@ -242,6 +242,26 @@ def rasterize(batch, w, h, cfg: RasterCfg, need_image=True, record_max=True, lis
     return out
 
 
+def cover_table(scene, camera: Camera, cfg: RasterCfg, position):
+    """ThresholdSearcher._table (src/thresholds.py:80-90): project with
+    shade=False, tile_cover_counts (src/raster.py:303-324) of the survivors,
+    their distances np.linalg.norm(means[src] - position, axis=1), stable
+    argsort by distance, prefix = [0, cumsum(cover[order])]."""
+    b = project(scene, None, camera, cfg, None, shade=False)
+    tiles_x, tiles_y = -(-camera.w // 16), -(-camera.h // 16)
+    mean2d = np.asarray(b["mean2d"]).reshape(-1, 2)
+    ext = np.asarray(b["extent"]).reshape(-1, 2)
+    x0 = np.clip(np.floor((mean2d[:, 0] - ext[:, 0]) / 16), 0, tiles_x - 1).astype(np.int64)
+    x1 = np.clip(np.floor((mean2d[:, 0] + ext[:, 0]) / 16), 0, tiles_x - 1).astype(np.int64)
+    y0 = np.clip(np.floor((mean2d[:, 1] - ext[:, 1]) / 16), 0, tiles_y - 1).astype(np.int64)
+    y1 = np.clip(np.floor((mean2d[:, 1] + ext[:, 1]) / 16), 0, tiles_y - 1).astype(np.int64)
+    cover = (x1 - x0 + 1) * (y1 - y0 + 1)
+    src = np.asarray(b["src"], np.int64)
+    dist = np.linalg.norm(np.asarray(scene.means)[src] - np.asarray(position), axis=1)
+    order = np.argsort(dist, kind="stable")
+    return dist[order], np.concatenate([[0], np.cumsum(cover[order])])
+
+
 def importance(levels, sets, cameras, cfg: RasterCfg):
     """score_active_selection (src/lod.py:95-122) over the given, already
     perturbed views: per view project every level's set with shade=False,

@@ -20,6 +20,7 @@ from .types import ImportanceScores, PerturbSpec
 from .importance import (compute_importance, random_rotations, score_active_selection,
                          visibility_filter_chunk)
 from .asset import AssetError, DeviceAsset, load_asset
+from .thresholds import CostEvaluation, ThresholdSearcher, cover_table, evaluate_cost
 
 __version__ = "0.1.0"
 
@@ -32,5 +33,5 @@ __all__ = [
     "stream_step", "Frame", "Renderer", "default_precision", "set_default_precision",
     "ImportanceScores", "PerturbSpec", "compute_importance", "random_rotations",
     "score_active_selection", "visibility_filter_chunk", "AssetError", "DeviceAsset",
-    "load_asset",
+    "load_asset", "CostEvaluation", "ThresholdSearcher", "cover_table", "evaluate_cost",
 ]

@@ -232,4 +232,9 @@ void launch_asset_split(const float *blob, int64_t n, int32_t width, float *geom
                         int32_t *flags_dev, cudaStream_t s);
 void launch_asset_sets(const lodge_chunks &ch, const int64_t *level_size_dev, int32_t *flags_dev,
                        cudaStream_t s);
+int launch_cover_keys(const lodge_level &level, const int64_t *idx, int64_t n, const Work &w,
+                      FrameState *fs, const lodge_camera *cam_dev, const lodge_raster_params &rp,
+                      cudaStream_t s);
+void launch_cover_table(const Work &w, FrameState *fs, int64_t n_cap, double *dist,
+                        int64_t *prefix, int32_t *launches, cudaStream_t s);
 }  // namespace lodge

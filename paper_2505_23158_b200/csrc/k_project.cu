@@ -545,6 +545,62 @@ __global__ void __launch_bounds__(256) k_project_compat(const GT *geom, const ST
   atomicMax(&fs->stats.M, (uint32_t)(m + 1));
 }
 
+// Threshold-search cost table, first half (ThresholdSearcher._table,
+// src/thresholds.py:80-90): project_scene(shade=False) of every input, and
+// for each survivor, compacted in input order (the batch order), its tile
+// cover count (tile_cover_counts, src/raster.py:316-324) and its camera
+// distance np.linalg.norm(means[src] - position) = sqrt((dx*dx + dy*dy) +
+// dz*dz) as a depth-sort key (IEEE bits of a non-negative double) with the
+// count as its value; the stable depth sort then yields argsort(dist, stable).
+template <typename GT>
+__global__ void __launch_bounds__(256) k_cover_keys(const GT *geom, const int64_t *idx, int64_t n,
+                                                    int32_t qnorm, Work w, FrameState *fs,
+                                                    const lodge_camera *__restrict__ cam_p,
+                                                    lodge_raster_params rp) {
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_base;
+  __shared__ lodge_camera cam;
+  if (threadIdx.x == 0) cam = *cam_p;
+  const uint32_t part = take_ticket(&fs->tickets[TK_COMPACT], &s_base);
+  const int64_t e = (int64_t)part * blockDim.x + threadIdx.x;
+  Proj p;
+  p.ok = false;
+  double v[12];
+  if (e < n) {
+    const int64_t g = idx ? idx[e] : e;
+    load_geom<GT>(geom + (size_t)g * 12, v);
+    if (qnorm) normalize_rot(v);
+    p = project_core(v, cam, rp, 1.0, false);
+  }
+  const int64_t m = compact_slot(e < n && p.ok, w.status, fs->epoch + TK_COMPACT, part, s_warp,
+                                 &s_base);
+  if (m < 0) return;
+  const int32_t tiles_x = (cam.w + 15) / 16, tiles_y = (cam.h + 15) / 16;
+  const uint64_t rc = tile_rect(p.mx, p.my, p.ex, p.ey, tiles_x, tiles_y);
+  const uint32_t x0 = rc & 0xffff, x1 = (rc >> 16) & 0xffff, y0 = (rc >> 32) & 0xffff,
+                 y1 = rc >> 48;
+  const double dx = v[0] - cam.pos[0], dy = v[1] - cam.pos[1], dz = v[2] - cam.pos[2];
+  const double dist = sqrt((dx * dx + dy * dy) + dz * dz);
+  w.key_depth[0][m] = (uint64_t)__double_as_longlong(dist);
+  w.val_depth[0][m] = (x1 - x0 + 1) * (y1 - y0 + 1);
+  atomicMax(&fs->stats.M, (uint32_t)(m + 1));
+}
+
+int launch_cover_keys(const lodge_level &level, const int64_t *idx, int64_t n, const Work &w,
+                      FrameState *fs, const lodge_camera *cam_dev, const lodge_raster_params &rp,
+                      cudaStream_t s) {
+  if (n <= 0) return 0;
+  const unsigned grid = (unsigned)((n + 255) / 256);
+  const int32_t qn = (level.flags & LODGE_GEOM_QNORM) ? 1 : 0;
+  if (level.flags & LODGE_GEOM_FP32)
+    k_cover_keys<float><<<grid, 256, 0, s>>>((const float *)level.geom_dev, idx, n, qn, w, fs,
+                                             cam_dev, rp);
+  else
+    k_cover_keys<double><<<grid, 256, 0, s>>>((const double *)level.geom_dev, idx, n, qn, w, fs,
+                                              cam_dev, rp);
+  return 0;
+}
+
 // Compat rasterize: import a host-made Splat2DBatch into the internal form.
 __global__ void __launch_bounds__(256) k_import_batch(lodge_batch b, int64_t M, Work w,
                                                       FrameState *fs,

@@ -516,6 +516,40 @@ int lodge_asset_split(lodge_ctx *c, const void *blob_dev, int64_t n, int32_t sh_
   return rc;
 }
 
+int lodge_cover_table(lodge_ctx *c, const lodge_level *level, const int64_t *idx_dev, int64_t n,
+                      const lodge_camera *cam, const lodge_raster_params *rp, double *dist_dev,
+                      int64_t *prefix_dev, int64_t *out_m) {
+  if (!c || !level || !rp || !out_m || (n > 0 && (!dist_dev || !prefix_dev)))
+    return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  int rc = check_cam(cam);
+  if (rc) return rc;
+  if (n < 0 || n > 0x3fffffff) return set_err(LODGE_ERR_BAD_ARG, "bad input count");
+  *out_m = 0;
+  CK(cudaSetDevice(c->device));
+  if (n == 0) {
+    const int64_t zero = 0;
+    if (prefix_dev) CK(cudaMemcpy(prefix_dev, &zero, sizeof(zero), cudaMemcpyHostToDevice));
+    return 0;
+  }
+  if ((rc = ensure_M(c, n)) ||
+      (rc = ensure_status(c, (n + 4095) / 4096 * 256 + (n + 255) / 256 + 256)))
+    return rc;
+  cudaStream_t s = c->stream;
+  *c->cam_host = *cam;
+  CK(cudaMemcpyAsync(c->cam_dev, c->cam_host, sizeof(lodge_camera), cudaMemcpyHostToDevice, s));
+  int32_t nl = 0;
+  launch_begin_frame(c->fs, s);
+  launch_cover_keys(*level, idx_dev, n, c->w, c->fs, c->cam_dev, *rp, s);
+  launch_cover_table(c->w, c->fs, n, dist_dev, prefix_dev, &nl, s);
+  rc = check_launch("lodge_cover_table");
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(c->stats_host, &c->fs->stats, sizeof(lodge_frame_stats),
+                     cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *out_m = c->stats_host->M;
+  return 0;
+}
+
 int lodge_asset_check_sets(lodge_ctx *c, const lodge_chunks *ch, const int64_t *level_sizes,
                            int32_t *set_flags) {
   if (!c || !ch || !level_sizes || !set_flags) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
