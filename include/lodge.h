@@ -225,6 +225,20 @@ int32_t lodge_last_launch_count(lodge_ctx *ctx);
  * [3] pixel evaluations inside the cut-off, [4] warp-batches. */
 int lodge_debug_counters(lodge_ctx *ctx, uint64_t *out8);
 
+/* ---- LOD-mode and full-mode frames --------------
+ * replaces render_lod (src/lod.py:230-237) and the "full" / "lod" branches
+ * of _mode_selection + _render_mode (src/cli.py:219-243): the active sets
+ * are chosen on the device -- lod: level l keeps the Gaussians with
+ * bounds[l] <= ||mean - camera position|| < bounds[l+1] (select_active,
+ * src/lod.py:192-211; bounds host, n_levels+1 values, the caller folds the
+ * depth offsets in); full: every Gaussian of level 0, the other levels
+ * empty -- then the fused path of lodge_render_frame.  maxw has one entry
+ * per selected input, level-major.  Async on the context stream. */
+int lodge_render_lod(lodge_ctx *ctx, const lodge_level *levels, int32_t n_levels,
+                     const double *bounds, int32_t full, const lodge_camera *cam_dev, int32_t w,
+                     int32_t h, const lodge_raster_params *rp, int32_t flags,
+                     const lodge_frame_out *out, lodge_frame_stats *stats_dev);
+
 /* ---- threshold-search cost table ----------------
  * replaces ThresholdSearcher._table, src/thresholds.py:80-90: project the
  * level's inputs (idx_dev, or all n when NULL) with shade=False; for the M

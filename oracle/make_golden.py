@@ -389,6 +389,40 @@ def make_thresholds():
     return out
 
 
+def make_modes():
+    """LOD-mode and full-mode frames on config-1 data:
+    render_lod (src/lod.py:230-237) for views 1 and 5, with and without depth
+    offsets, and the CLI's full mode (src/cli.py:221-226 + :236-243)."""
+    from splatlod.lod import render_lod, select_active
+    d, levels, cams, plan = _config1_objects()
+    rc = R.RasterConfig()
+    out = {}
+    t0 = time.time()
+    for v in (1, 5):
+        cam = cams[v]
+        for tag, offs in (("lod", None), ("lodoff", [0.0, 1.5])):
+            res = render_lod(levels, cam, rc, depth_offsets=offs)
+            p = f"v{v}/{tag}/"
+            out[p + "image"] = res.image
+            out[p + "tile_count"] = res.per_tile_count
+            out[p + "visible"] = res.per_pixel_visible
+            out[p + "maxw"] = res.per_gaussian_max_weight
+            for l, s in enumerate(select_active(levels, cam.position, offs)):
+                out[p + f"set{l}"] = s
+        sets = [np.arange(len(levels[0]), dtype=np.int64)]
+        sets += [np.zeros(0, dtype=np.int64) for _ in levels[1:]]
+        mods = [np.ones(len(s)) for s in sets]
+        batch = project_selection(levels, sets, cam, rc, modulations=mods)
+        res = R.rasterize(batch, cam, rc)
+        p = f"v{v}/full/"
+        out[p + "image"] = res.image
+        out[p + "tile_count"] = res.per_tile_count
+        out[p + "visible"] = res.per_pixel_visible
+        out[p + "maxw"] = res.per_gaussian_max_weight
+    print("modes", round(time.time() - t0, 1), "s")
+    return out
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     t0 = time.time()

@@ -242,6 +242,18 @@ def rasterize(batch, w, h, cfg: RasterCfg, need_image=True, record_max=True, lis
     return out
 
 
+def select_active(levels, position, bounds):
+    """select_active (src/lod.py:192-211) for precomputed band bounds: level l
+    keeps flatnonzero(bounds[l] <= ||means - position|| < bounds[l+1])."""
+    q = np.asarray(position, float)
+    sets = []
+    for l, lv in enumerate(levels):
+        means = np.asarray(getattr(lv, "scene", lv).means)
+        dist = np.linalg.norm(means - q, axis=1)
+        sets.append(np.flatnonzero((dist >= bounds[l]) & (dist < bounds[l + 1])))
+    return sets
+
+
 def cover_table(scene, camera: Camera, cfg: RasterCfg, position):
     """ThresholdSearcher._table (src/thresholds.py:80-90): project with
     shade=False, tile_cover_counts (src/raster.py:303-324) of the survivors,

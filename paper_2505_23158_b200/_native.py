@@ -103,6 +103,9 @@ EXPORTS = {
     "lodge_to_srgb8": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p], C.c_int),
     "lodge_last_launch_count": ([C.c_void_p], C.c_int32),
     "lodge_debug_counters": ([C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
+    "lodge_render_lod": ([C.c_void_p, C.POINTER(Level), C.c_int32, C.POINTER(C.c_double),
+                          C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.POINTER(RasterParams),
+                          C.c_int32, C.POINTER(FrameOut), C.c_void_p], C.c_int),
     "lodge_cover_table": ([C.c_void_p, C.POINTER(Level), C.c_void_p, C.c_int64,
                            C.POINTER(Camera), C.POINTER(RasterParams), C.c_void_p, C.c_void_p,
                            C.POINTER(C.c_int64)], C.c_int),

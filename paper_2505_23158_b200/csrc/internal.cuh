@@ -232,6 +232,10 @@ void launch_asset_split(const float *blob, int64_t n, int32_t width, float *geom
                         int32_t *flags_dev, cudaStream_t s);
 void launch_asset_sets(const lodge_chunks &ch, const int64_t *level_size_dev, int32_t *flags_dev,
                        cudaStream_t s);
+void launch_band_select(const lodge_level *levels, int32_t L, const double *bounds, int32_t full,
+                        const LevelSlots &ls, FrameState *fs, const lodge_camera *cam,
+                        uint64_t *status, uint32_t *union_idx, uint8_t *union_tag,
+                        cudaStream_t s);
 int launch_cover_keys(const lodge_level &level, const int64_t *idx, int64_t n, const Work &w,
                       FrameState *fs, const lodge_camera *cam_dev, const lodge_raster_params &rp,
                       cudaStream_t s);

@@ -339,6 +339,114 @@ __global__ void k_union_sizes(int32_t L, FrameState *fs) {
   fs->n_sort = U;  // fused path: every input is a depth-sort key (culled -> ~0)
 }
 
+// LOD-mode selection (select_active, reference src/lod.py:192-211): level l
+// keeps the Gaussians whose camera distance ||mean - position|| (NumPy's
+// sqrt((dx*dx + dy*dy) + dz*dz)) lies in [lo_l, hi_l); full mode is level 0
+// with [0, inf) and empty bands elsewhere.  Kept indices are compacted in
+// index order into the level's slots (tag 3: modulation 1), UN_TILE inputs
+// per CTA in ticket order, block scan + per-level decoupled look-back.
+struct BandArgs {
+  const void *geom[LODGE_MAX_LEVELS];
+  int64_t n[LODGE_MAX_LEVELS];
+  double lo[LODGE_MAX_LEVELS], hi[LODGE_MAX_LEVELS];
+  uint32_t slot_base[LODGE_MAX_LEVELS + 1];
+  uint32_t part_base[LODGE_MAX_LEVELS + 1];
+  int32_t L, geom32;
+};
+
+__global__ void __launch_bounds__(UN_THREADS) k_band_select(BandArgs a, FrameState *fs,
+                                                           const lodge_camera *__restrict__ cam,
+                                                           uint64_t *lb_status,
+                                                           uint32_t *union_idx,
+                                                           uint8_t *union_tag) {
+  __shared__ uint32_t s_w[UN_THREADS / 32];
+  __shared__ uint32_t s_tk;
+  const uint32_t g = take_ticket(&fs->tickets[TK_UNION0], &s_tk);
+  int l = 0;
+  while (l + 1 < a.L && g >= a.part_base[l + 1]) ++l;
+  const uint32_t part = g - a.part_base[l];
+  const int64_t n = a.n[l];
+  const int64_t i0 = (int64_t)part * UN_TILE + (int64_t)threadIdx.x * UN_ITEMS;
+  const double px = cam->pos[0], py = cam->pos[1], pz = cam->pos[2];
+  uint32_t kmask = 0;
+#pragma unroll
+  for (int it = 0; it < UN_ITEMS; ++it) {
+    const int64_t i = i0 + it;
+    if (i < n) {
+      double mx, my, mz;
+      if (a.geom32) {
+        const float *r = reinterpret_cast<const float *>(a.geom[l]) + i * 12;
+        mx = r[0]; my = r[1]; mz = r[2];
+      } else {
+        const double *r = reinterpret_cast<const double *>(a.geom[l]) + i * 12;
+        mx = r[0]; my = r[1]; mz = r[2];
+      }
+      const double dx = mx - px, dy = my - py, dz = mz - pz;
+      const double d = sqrt((dx * dx + dy * dy) + dz * dz);
+      if (d >= a.lo[l] && d < a.hi[l]) kmask |= 1u << it;
+    }
+  }
+  const uint32_t kc = __popc(kmask);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = kc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t wv = lane < UN_THREADS / 32 ? s_w[lane] : 0u;
+    uint32_t wi = wv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(FULL_MASK, wi, o);
+      if (lane >= o) wi += t;
+    }
+    const uint32_t total = __shfl_sync(FULL_MASK, wi, UN_THREADS / 32 - 1);
+    const uint32_t pre = lookback_warp(lb_status + a.part_base[l], part, total,
+                                       fs->epoch + TK_UNION0);
+    if (lane < UN_THREADS / 32) s_w[lane] = pre + wi - wv;
+    if (lane == 0 && (int64_t)(part + 1) * UN_TILE >= n) fs->stats.U_level[l] = pre + total;
+  }
+  __syncthreads();
+  uint32_t m = a.slot_base[l] + s_w[warp] + inc - kc;
+#pragma unroll
+  for (int it = 0; it < UN_ITEMS; ++it) {
+    if ((kmask >> it) & 1u) {
+      union_idx[m] = (uint32_t)(i0 + it);
+      union_tag[m] = 3;
+      ++m;
+    }
+  }
+}
+
+void launch_band_select(const lodge_level *levels, int32_t L, const double *bounds, int32_t full,
+                        const LevelSlots &ls, FrameState *fs, const lodge_camera *cam,
+                        uint64_t *status, uint32_t *union_idx, uint8_t *union_tag,
+                        cudaStream_t s) {
+  BandArgs a;
+  a.L = L;
+  a.geom32 = (levels[0].flags & LODGE_GEOM_FP32) ? 1 : 0;
+  a.part_base[0] = 0;
+  for (int l = 0; l < LODGE_MAX_LEVELS; ++l) {
+    const bool on = l < L && (!full || l == 0);
+    a.geom[l] = l < L ? levels[l].geom_dev : nullptr;
+    a.n[l] = on ? levels[l].n : 0;
+    a.lo[l] = full ? 0.0 : (l < L ? bounds[l] : 0.0);
+    a.hi[l] = full ? INFINITY : (l < L ? bounds[l + 1] : 0.0);
+  }
+  for (int l = 0; l <= LODGE_MAX_LEVELS; ++l) a.slot_base[l] = l <= L ? ls.slot_base[l] : 0;
+  for (int l = 0; l < L; ++l)
+    a.part_base[l + 1] = a.part_base[l] + (uint32_t)((a.n[l] + UN_TILE - 1) / UN_TILE);
+  for (int l = L + 1; l <= LODGE_MAX_LEVELS; ++l) a.part_base[l] = a.part_base[L];
+  const uint32_t nparts = a.part_base[L];
+  if (nparts > 0)
+    k_band_select<<<nparts, UN_THREADS, 0, s>>>(a, fs, cam, status, union_idx, union_tag);
+  k_union_sizes<<<1, 32, 0, s>>>(L, fs);
+}
+
 void launch_union(const lodge_chunks &ch, const LevelSlots &ls, FrameState *fs, uint64_t *status,
                   uint32_t *union_idx, uint8_t *union_tag, cudaStream_t s) {
   UnionArgs a;
@@ -374,7 +482,12 @@ __global__ void k_begin_frame(FrameState *fs) {
     fs->stats.P = 0;
     fs->stats.overflow = 0;
     fs->stats.guard_hits = 0;
+    fs->stats.f = -1;  // set by k_select_frame on the chunk paths
+    fs->stats.o = -1;
+    fs->stats.t = 1.0;
+    fs->stats.t_bar = 1.0;
   }
+  if (i < LODGE_MAX_LEVELS) fs->stats.U_level[i] = 0;
   if (i < 32) fs->tickets[i] = 0;
   if (i < 8) fs->counters[i] = 0;
   for (int k = i; k < 8 * 256; k += blockDim.x) (&fs->hist_depth[0][0])[k] = 0;

@@ -344,6 +344,11 @@ int lodge_rasterize(lodge_ctx *c, const lodge_batch *b, int64_t M, int64_t n_inp
   return 0;
 }
 
+static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots &ls,
+                       const lodge_camera *cam_dev, int32_t W, int32_t H,
+                       const lodge_raster_params &rp, int32_t flags, const lodge_frame_out *out,
+                       lodge_frame_stats *stats_dev, int32_t nl, const char *name);
+
 int lodge_render_frame(lodge_ctx *c, const lodge_level *levels, int32_t n_levels,
                        const lodge_chunks *ch, const lodge_camera *cam_dev, int32_t W, int32_t H,
                        const lodge_raster_params *rp, const int32_t *pair,
@@ -390,11 +395,27 @@ int lodge_render_frame(lodge_ctx *c, const lodge_level *levels, int32_t n_levels
                       tv, c->fs, s); ++nl;
   c->mark(1);
   launch_union(*ch, ls, c->fs, w.status, w.union_idx, w.union_tag, s); nl += 2;
+  return render_tail(c, levels, ls, cam_dev, W, H, *rp, flags, out, stats_dev, nl,
+                     "lodge_render_frame");
+}
+
+// Everything after the active-set stage, shared by the chunk and LOD paths:
+// projection -> depth sort -> tile setup -> duplication -> tile sort ->
+// compositing, on the context stream, stage marks 2..8.
+static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots &ls,
+                       const lodge_camera *cam_dev, int32_t W, int32_t H,
+                       const lodge_raster_params &rp, int32_t flags, const lodge_frame_out *out,
+                       lodge_frame_stats *stats_dev, int32_t nl, const char *name) {
+  cudaStream_t s = c->stream;
+  Work &w = c->w;
+  const bool exact = c->precision == LODGE_PREC_EXACT;
+  const int64_t U_cap = ls.slot_base[ls.n_levels];
+  const int32_t tiles_x = (W + 15) / 16, tiles_y = (H + 15) / 16;
   c->mark(2);
   if ((flags & LODGE_RECORD_MAX) && !(flags & LODGE_ACCUMULATE_MAX) && out->maxw_dev)
     CK(cudaMemsetAsync(out->maxw_dev, 0, (exact ? 8 : 4) * (size_t)U_cap, s));
-  rc = launch_project_frame(levels, ls, w, c->fs, cam_dev, *rp, (flags & LODGE_NEED_IMAGE) ? 1 : 0,
-                            exact, s);
+  int rc = launch_project_frame(levels, ls, w, c->fs, cam_dev, rp,
+                                (flags & LODGE_NEED_IMAGE) ? 1 : 0, exact, s);
   if (rc) return set_err(LODGE_ERR_BAD_ARG, "all levels must share one storage precision");
   ++nl;
   c->mark(3);
@@ -406,13 +427,53 @@ int lodge_render_frame(lodge_ctx *c, const lodge_level *levels, int32_t n_levels
   c->mark(6);
   launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s);
   c->mark(7);
-  launch_composite(w, c->fs, cam_dev, W, H, *rp, flags, exact, *out, 0, s); ++nl;
+  launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, 0, s); ++nl;
   c->mark(8);
   if (c->prof && c->prof_frames < c->prof_cap) ++c->prof_frames;
   if (stats_dev)
     CK(cudaMemcpyAsync(stats_dev, &c->fs->stats, sizeof(lodge_frame_stats), cudaMemcpyDeviceToDevice, s));
   c->launches = nl;
-  return check_launch("lodge_render_frame");
+  return check_launch(name);
+}
+
+int lodge_render_lod(lodge_ctx *c, const lodge_level *levels, int32_t n_levels,
+                     const double *bounds, int32_t full, const lodge_camera *cam_dev, int32_t W,
+                     int32_t H, const lodge_raster_params *rp, int32_t flags,
+                     const lodge_frame_out *out, lodge_frame_stats *stats_dev) {
+  if (!c || !levels || !cam_dev || !rp || !out || (!full && !bounds))
+    return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  if (n_levels < 1 || n_levels > LODGE_MAX_LEVELS)
+    return set_err(LODGE_ERR_BAD_ARG, "level count must be in 1.." + std::to_string(LODGE_MAX_LEVELS));
+  if (W <= 0 || H <= 0) return set_err(LODGE_ERR_BAD_ARG, "camera resolution must be positive");
+  int rc = check_tile_smem(W, H);
+  if (rc) return rc;
+  for (int l = 0; l < n_levels; ++l) {
+    if (levels[l].sh_degree < 0 || levels[l].sh_degree > 3)
+      return set_err(LODGE_ERR_BAD_ARG, "sh degree must be in 0..3");
+    if (levels[l].n > 0x3fffffff) return set_err(LODGE_ERR_BAD_ARG, "level too large");
+  }
+  CK(cudaSetDevice(c->device));
+  LevelSlots ls;
+  ls.n_levels = n_levels;
+  ls.slot_base[0] = 0;
+  for (int l = 0; l < n_levels; ++l)
+    ls.slot_base[l + 1] = ls.slot_base[l] + ((full && l > 0) ? 0u : (uint32_t)levels[l].n);
+  const int64_t U_cap = ls.slot_base[n_levels];
+  if (U_cap > 0x3fffffff) return set_err(LODGE_ERR_BAD_ARG, "too many inputs");
+  if ((rc = ensure_slots(c, U_cap)) || (rc = ensure_M(c, std::max<int64_t>(U_cap, 1))) ||
+      (rc = ensure_tiles(c, W, H)) || (rc = ensure_P(c, 1)) ||
+      (rc = ensure_status(c, (c->w.M_cap + 4095) / 4096 * 256 + (U_cap + 255) / 256 + 256)))
+    return rc;
+  c->last_slots = ls;
+  int32_t nl = 0;
+  c->mark(0);
+  launch_begin_frame(c->fs, c->stream); ++nl;
+  c->mark(1);
+  launch_band_select(levels, n_levels, bounds, full, ls, c->fs, cam_dev, c->w.status,
+                     c->w.union_idx, c->w.union_tag, c->stream);
+  nl += 2;
+  return render_tail(c, levels, ls, cam_dev, W, H, *rp, flags, out, stats_dev, nl,
+                     "lodge_render_lod");
 }
 
 int lodge_frame_lists(lodge_ctx *c, int32_t T, int64_t *tile_offsets, int64_t *tile_src,

@@ -1,14 +1,16 @@
-"""Drop-in project_selection (reference src/lod.py:216-227)."""
+"""Drop-in project_selection (reference src/lod.py:216-227) and the LOD-mode /
+full-mode renders (src/lod.py:230-237, src/cli.py:221-243) on the fused path."""
 
 from __future__ import annotations
 
 from typing import Optional, Sequence
 
 import numpy as np
+import torch
 
-from .device import context
+from .device import _device, context, default_precision, level_for
 from .raster import DeviceBatch, project_scene_device
-from .types import RasterConfig
+from .types import RasterConfig, TileRenderOutput
 
 
 def project_selection_device(levels: Sequence, sets: Sequence, camera, raster_cfg,
@@ -31,3 +33,54 @@ def project_selection(levels: Sequence, sets: Sequence, camera, raster_cfg: Rast
     """Project per-level index sets into one splat batch (level-major order)."""
     return project_selection_device(levels, sets, camera, raster_cfg, modulations,
                                     shade).to_host()
+
+
+def lod_bounds(levels: Sequence, depth_offsets: Optional[Sequence[float]] = None) -> list:
+    """The distance bands of select_active (src/lod.py:186-205): level l
+    covers [d_l + off_l, d_{l+1} + off_{l+1}), level 0 from 0, the last band
+    to infinity.  Validates as the reference does."""
+    ds = [lv.depth_threshold for lv in levels]
+    if any(b <= a for a, b in zip(ds, ds[1:])):
+        raise ValueError(f"levels must have strictly increasing depth thresholds, got {ds}")
+    n = len(levels)
+    offs = np.zeros(n) if depth_offsets is None else np.asarray(depth_offsets, float)
+    if offs.shape[0] != n:
+        raise ValueError("need one depth offset per level")
+    return [0.0] + [levels[l].depth_threshold + offs[l] for l in range(1, n)] + [np.inf]
+
+
+def _frame_to_host(fr, st, raster_cfg) -> TileRenderOutput:
+    U = int(st.U)
+    return TileRenderOutput(
+        None if fr.image is None else fr.image.to(torch.float64).cpu().numpy(),
+        fr.tile_count.to(torch.int64).cpu().numpy(),
+        fr.visible.to(torch.int64).cpu().numpy(),
+        None if fr.maxw is None else fr.maxw[:U].to(torch.float64).cpu().numpy(),
+        raster_cfg.metadata() if hasattr(raster_cfg, "metadata") else {})
+
+
+def _lod_renderer(levels, raster_cfg, device=None):
+    from .renderer import Renderer
+    dev = _device(device)
+    dl = [level_for(getattr(lv, "scene", lv), dev, "fp64") for lv in levels]
+    return Renderer(dl, None, dev, raster_cfg=raster_cfg, precision=default_precision())
+
+
+def render_lod(levels: Sequence, camera, raster_cfg: RasterConfig = RasterConfig(),
+               depth_offsets: Optional[Sequence[float]] = None, need_image: bool = True):
+    """Select active Gaussians at the camera position and rasterize them
+    (src/lod.py:230-237): the Eq. 2 band predicate runs on the device inside
+    the fused frame (lodge_render_lod)."""
+    bounds = lod_bounds(levels, depth_offsets)
+    r = _lod_renderer(levels, raster_cfg)
+    fr, st = r.render_lod_camera(camera, bounds, False, need_image, True)
+    return _frame_to_host(fr, st, raster_cfg)
+
+
+def render_full(levels: Sequence, camera, raster_cfg: RasterConfig = RasterConfig(),
+                need_image: bool = True):
+    """The CLI's "full" mode (src/cli.py:221-226, rendered by _render_mode
+    :236-243): every Gaussian of level 0, the other levels empty."""
+    r = _lod_renderer(levels, raster_cfg)
+    fr, st = r.render_lod_camera(camera, None, True, need_image, True)
+    return _frame_to_host(fr, st, raster_cfg)

@@ -66,14 +66,17 @@ class Renderer:
                 self.levels.append(lv)
             else:
                 self.levels.append(DeviceLevel(getattr(lv, "scene", lv), self.device, storage))
-        self.plan = plan if isinstance(plan, DevicePlan) else DevicePlan(plan, self.device)
-        if self.plan.L != len(self.levels):
+        # plan=None: LOD / full modes only (render_lod)
+        self.plan = (plan if (plan is None or isinstance(plan, DevicePlan))
+                     else DevicePlan(plan, self.device))
+        if self.plan is not None and self.plan.L != len(self.levels):
             raise ValueError("chunk plan and level list disagree on the level count")
         self._level_arr = (N.Level * len(self.levels))(*[l.struct for l in self.levels])
         self.precision = precision
         self.cfg = raster_cfg
         self._rp = params_struct(raster_cfg)
-        self.U_cap = self.plan.union_capacity
+        lod_cap = sum(l.n for l in self.levels)
+        self.U_cap = max(self.plan.union_capacity, lod_cap) if self.plan is not None else lod_cap
 
     # ------------------------------------------------------------------
     @property
@@ -121,7 +124,9 @@ class Renderer:
                      torch.empty((height, width, 3), dtype=fdt, device=d) if need_image else None,
                      torch.empty((ty, tx), dtype=torch.int32, device=d),
                      torch.empty((height, width), dtype=torch.int32, device=d),
-                     torch.empty(max(self.U_cap, 1), dtype=fdt, device=d) if record_max else None,
+                     # zeroed: a frame clears only the entries its own slot
+                     # layout can write, which may be fewer than U_cap
+                     torch.zeros(max(self.U_cap, 1), dtype=fdt, device=d) if record_max else None,
                      torch.zeros(STATS_BYTES, dtype=torch.uint8, device=d))
 
     def upload_cameras(self, cameras) -> torch.Tensor:
@@ -157,6 +162,50 @@ class Renderer:
             None if tv is None else C.byref(tv), flags, C.byref(out), ptr(frame.stats)),
             "lodge_render_frame")
         return frame
+
+    def render_lod(self, cam_row: torch.Tensor, frame: Frame, bounds=None, full: bool = False,
+                   need_image: bool = True, record_max: bool = True, slot: int = 0,
+                   accumulate_max: bool = False) -> Frame:
+        """Enqueue one LOD-mode frame (level l keeps the Gaussians with
+        bounds[l] <= camera distance < bounds[l+1], src/lod.py:192-237) or,
+        with full=True, a full-mode frame (all of level 0, src/cli.py:221-226)
+        on slot `slot`'s stream."""
+        if not full:
+            if bounds is None or len(bounds) != len(self.levels) + 1:
+                raise ValueError("need one distance bound per level plus one")
+            b = (C.c_double * len(bounds))(*[float(x) for x in bounds])
+        else:
+            b = None
+        need = self.levels[0].n if full else sum(l.n for l in self.levels)
+        if record_max and frame.maxw is not None and frame.maxw.numel() < need:
+            raise ValueError("frame.maxw holds fewer entries than the inputs this mode selects")
+        out = N.FrameOut()
+        out.image_dev = frame.image.data_ptr() if (need_image and frame.image is not None) else None
+        out.tile_count_dev = frame.tile_count.data_ptr()
+        out.visible_dev = frame.visible.data_ptr()
+        out.maxw_dev = frame.maxw.data_ptr() if (record_max and frame.maxw is not None) else None
+        flags = ((N.NEED_IMAGE if need_image else 0) | (N.RECORD_MAX if record_max else 0) |
+                 (N.ACCUMULATE_MAX if accumulate_max else 0))
+        N.check(N.lib().lodge_render_lod(
+            self._bind(slot), self._level_arr, len(self.levels), b, int(bool(full)),
+            ptr(cam_row), frame.width, frame.height, C.byref(self._rp), flags, C.byref(out),
+            ptr(frame.stats)), "lodge_render_lod")
+        return frame
+
+    def render_lod_camera(self, camera, bounds=None, full=False, need_image=True,
+                          record_max=True):
+        """Convenience: one host camera -> device frame + stats (grows the
+        pair buffers and renders again on overflow)."""
+        w, h = (int(v) for v in camera.resolution)
+        fr = self.alloc_frame(w, h, need_image, record_max)
+        cams = self.upload_cameras([camera])
+        self.render_lod(cams[0], fr, bounds, full, need_image, record_max)
+        st = fr.read_stats()
+        if st.overflow:
+            self.reserve(int(st.P))
+            self.render_lod(cams[0], fr, bounds, full, need_image, record_max)
+            st = fr.read_stats()
+        return fr, st
 
     def to_srgb8(self, frame: Frame, out: torch.Tensor, slot: int = 0) -> torch.Tensor:
         """8-bit sRGB of the frame's image on the device (src/images.py:10-17)."""
