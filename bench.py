@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--streams", type=int, default=4,
                     help="frames in flight per GPU (one liblodge context + stream each)")
     ap.add_argument("--cpu-views", type=int, default=1, help="views in the CPU baseline sample")
+    ap.add_argument("--mode", default="blend", choices=["blend", "chunks", "lod", "full"],
+                    help="render mode of the reference CLI (src/cli.py:219-243); the "
+                         "metric is quoted on blend")
     return ap.parse_args()
 
 
@@ -193,16 +196,44 @@ def load_traffic(kernel_stage):
 # ---------------------------------------------------------------------------
 # CPU reference (oracle restatement of the reference algorithm)
 # ---------------------------------------------------------------------------
-def cpu_render_view(cfg, cam, O):
-    f, o, tb, t = O.select(cfg.centers, cam.position)
+def lod_bounds_of(cfg):
+    """select_active's bands for the fixture levels (src/lod.py:203)."""
+    return [0.0] + [float(cfg.levels[l][2]) for l in range(1, cfg.L)] + [float("inf")]
+
+
+def nearest_chunk(centers, position):
+    """nearest_two_chunks' first id (src/blending.py:77-84): lexsort by (dist, id)."""
+    d = np.linalg.norm(np.asarray(centers) - np.asarray(position), axis=1)
+    return int(np.lexsort((np.arange(d.shape[0]), d))[0])
+
+
+def cpu_render_view(cfg, cam, O, mode="blend"):
+    """One view of the given mode on the host cores (oracle restatement):
+    blend / chunks (src/blending.py:77-137), lod (src/lod.py:192-237), full
+    (src/cli.py:221-226)."""
     oc = O.camera_from(cam)
     rc = O.cfg_struct(_raster_cfg())
     parts = []
-    for l in range(cfg.L):
-        b = cfg.set(o, l).astype(np.int64) if o is not None else np.zeros(0, np.int64)
-        idx, mod, _ = O.union(cfg.set(f, l).astype(np.int64), b, t)
-        g, s, _ = cfg.levels[l]
-        parts.append(O.project_f32(g, s, cfg.degree, idx, oc, rc, mod))
+    if mode in ("blend", "chunks"):
+        f, o, tb, t = O.select(cfg.centers, cam.position)
+        if mode == "chunks":
+            o, t = None, 1.0
+        for l in range(cfg.L):
+            b = cfg.set(o, l).astype(np.int64) if o is not None else np.zeros(0, np.int64)
+            idx, mod, _ = O.union(cfg.set(f, l).astype(np.int64), b, t)
+            g, s, _ = cfg.levels[l]
+            parts.append(O.project_f32(g, s, cfg.degree, idx, oc, rc, mod))
+    else:
+        bounds = lod_bounds_of(cfg)
+        q = np.asarray(cam.position, float)
+        for l in range(cfg.L):
+            g, s, _ = cfg.levels[l]
+            if mode == "full":
+                idx = np.arange(g.shape[0]) if l == 0 else np.zeros(0, np.int64)
+            else:
+                dist = np.linalg.norm(g[:, 0:3].astype(np.float64) - q, axis=1)
+                idx = np.flatnonzero((dist >= bounds[l]) & (dist < bounds[l + 1]))
+            parts.append(O.project_f32(g, s, cfg.degree, idx.astype(np.int64), oc, rc, None))
     batch = O.concat(parts)
     w, h = cam.resolution
     return O.rasterize(batch, w, h, rc, lists=False), batch
@@ -234,11 +265,11 @@ def run_reference(args):
     sweep = cfg.sweep(SWEEP_VIEWS)
     views = [v for blk in my_views(0, 1, args.warmup + args.steps, BLOCK) for v in blk[:1]]
     for v in views[:args.warmup]:
-        cpu_render_view(cfg, sweep[v], O)
+        cpu_render_view(cfg, sweep[v], O, args.mode)
     times = []
     for v in views[args.warmup:]:
         t0 = time.perf_counter()
-        cpu_render_view(cfg, sweep[v], O)
+        cpu_render_view(cfg, sweep[v], O, args.mode)
         times.append(time.perf_counter() - t0)
     total = sum(times)
     fps = len(times) / total
@@ -247,7 +278,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_name(args.config), "views_per_step": 1},
+            "config": {"workload": workload_name(args.config), "views_per_step": 1,
+                       "mode": args.mode},
             "cpu_baseline": {"value": fps, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": f"1 sweep view per step ({len(times)} views), oracle/ C "
                                        f"restatement with OpenMP on {cores} threads, "
@@ -292,6 +324,17 @@ def run_lodge(args):
     cams = r.upload_cameras([sweep[v] for v in flat])
     frames = [r.alloc_frame(W, H) for _ in range(B)]
     n_timed = args.steps * B
+    bounds = lod_bounds_of(cfg)
+    near = {v: nearest_chunk(cfg.centers, sweep[v].position) for v in flat}
+
+    def do_render(cam_row, frame, slot, v):
+        """One frame of args.mode (the CLI's render modes, src/cli.py:219-243)."""
+        if args.mode == "blend":
+            r.render(cam_row, frame, slot=slot)
+        elif args.mode == "chunks":
+            r.render(cam_row, frame, pair=(near[v], None), slot=slot)
+        else:
+            r.render_lod(cam_row, frame, bounds, full=args.mode == "full", slot=slot)
     stats_all = torch.zeros((n_timed, STATS_BYTES), dtype=torch.uint8, device=dev)
 
     def read_stats(t):
@@ -304,7 +347,7 @@ def run_lodge(args):
     torch.cuda.synchronize()
     for i, v in enumerate(flat):
         fr = frames[0]
-        r.render(cams[pos[v]], fr, slot=0)
+        do_render(cams[pos[v]], fr, 0, v)
         with torch.cuda.stream(r.stream_of(0)):
             sizing[i].copy_(fr.stats)
     torch.cuda.synchronize()
@@ -316,7 +359,7 @@ def run_lodge(args):
     clocks.start()  # sampling before the timed region starts
     for s in range(args.warmup):
         for j, v in enumerate(schedule[s]):
-            r.render(cams[pos[v]], frames[j], slot=j % r.n_streams)
+            do_render(cams[pos[v]], frames[j], j % r.n_streams, v)
     torch.cuda.synchronize()
     setup_s = time.time() - t_setup
 
@@ -338,7 +381,7 @@ def run_lodge(args):
     k = 0
     for s in range(args.warmup, args.warmup + args.steps):
         for j, v in enumerate(schedule[s]):
-            r.render(cams[pos[v]], frames[j], slot=j % S)
+            do_render(cams[pos[v]], frames[j], j % S, v)
             with torch.cuda.stream(r.stream_of(j % S)):
                 stats_all[k].copy_(frames[j].stats, non_blocking=True)
             k += 1
@@ -364,7 +407,7 @@ def run_lodge(args):
         for s in range(args.warmup, args.warmup + args.steps):
             for j, v in enumerate(schedule[s]):
                 if k < n_stage:
-                    r.render(cams[pos[v]], frames[j], slot=0)
+                    do_render(cams[pos[v]], frames[j], 0, v)
                 k += 1
         torch.cuda.synchronize()
         stage_ms, nprof_frames = r.profile_read()
@@ -442,8 +485,8 @@ def run_lodge(args):
             copied[par].record(cur)
             for q in range(S):
                 r.stream_of(q).wait_stream(cur)
-            for j in range(B):
-                r.render(cam_dev[par][j], frames[j], slot=j % S)
+            for j, v in enumerate(schedule[s]):
+                do_render(cam_dev[par][j], frames[j], j % S, v)
                 r.to_srgb8(frames[j], img8[j], slot=j % S)
                 with torch.cuda.stream(r.stream_of(j % S)):
                     st_dev[j].copy_(frames[j].stats, non_blocking=True)
@@ -488,14 +531,14 @@ def run_lodge(args):
         cam = sweep[v]
         t0 = time.perf_counter()
         for _ in range(args.cpu_views):
-            ref, batch = cpu_render_view(cfg, cam, O)
+            ref, batch = cpu_render_view(cfg, cam, O, args.mode)
         dt = (time.perf_counter() - t0) / args.cpu_views
         cpu = {"value": 1.0 / dt, "unit": UNIT, "cores": O.num_threads(), "kind": "port",
                "sample": f"{args.cpu_views} view(s) of the same sweep (z={cam.position[2]:.2f}), "
                          f"oracle/ C restatement, OpenMP {O.num_threads()} threads, "
                          f"{cpu_model()}, {dt:.1f} s/view"}
         fr = frames[0]
-        r.render(cams[pos[v]], fr, slot=0)
+        do_render(cams[pos[v]], fr, 0, v)
         torch.cuda.synchronize()
         st = fr.read_stats()
         img = fr.image.double().cpu().numpy()
@@ -512,7 +555,8 @@ def run_lodge(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64 projection / f32 compositing (fp64 guard band)", "data": "synthetic",
-            "config": {"workload": workload_name(args.config), "resolution": [W, H],
+            "config": {"workload": workload_name(args.config), "mode": args.mode,
+                       "resolution": [W, H],
                        "views_per_step_per_gpu": B, "frames_timed": total_frames,
                        "precision": args.precision, "store": "fp32 records, replicated",
                        "store_gb": round(store_gb, 2),
