@@ -34,7 +34,7 @@ __host__ __device__ constexpr int os_items() {
 // Key maps applied at the scatter (see launch_tile_sort).
 enum : int { MAP_ID = 0, MAP_PACK = 1, MAP_LOW = 2 };
 
-template <bool VALS, typename KI, typename KO, int MAP, int NB = 8>
+template <bool VALS, typename KI, typename KO, int MAP, int NB = 8, bool DROP = false>
 #ifndef LODGE_OS_MINB
 #define LODGE_OS_MINB 3
 #endif
@@ -68,9 +68,20 @@ __global__ void __launch_bounds__(OS_THREADS, VALS ? LODGE_OS_VMINB
 #pragma unroll
   for (int i = 0; i < OS_ITEMS; ++i) {
     const uint32_t idx = base + warp * (OS_ITEMS * 32) + i * 32 + lane;
-    const bool valid = idx < n;
+    k[i] = idx < n ? kin[idx] : (KI)~(KI)0;
+    // drop: culled inputs (key ~0) leave the sort here, the output holds
+    // only the survivors (their count, fs->stats.M, is the later passes' n)
+    const bool valid = idx < n && !(DROP && k[i] == (KI)~(KI)0);
     vmask |= valid ? (1u << i) : 0u;
-    k[i] = valid ? kin[idx] : (KI)~(KI)0;
+  }
+  uint32_t cnt = min((uint32_t)OS_TILE, n - base);
+  if (DROP) {  // the partition's valid items, not its positional size
+    const uint32_t c = __reduce_add_sync(FULL_MASK, (uint32_t)__popc(vmask));
+    if (lane == 0) S.misc[2 + warp] = c;
+    __syncthreads();
+    cnt = 0;
+#pragma unroll
+    for (int w = 0; w < OS_THREADS / 32; ++w) cnt += S.misc[2 + w];
   }
   const uint32_t lowmask = sb >= 32 ? 0xffffffffu : ((1u << sb) - 1u);
   auto kmap = [&](KI key) -> KO {
@@ -81,9 +92,9 @@ __global__ void __launch_bounds__(OS_THREADS, VALS ? LODGE_OS_VMINB
     else
       return (KO)key;
   };
-  onesweep_partition<OS_ITEMS, NB, VALS>(S, k, vmask, part, min((uint32_t)OS_TILE, n - base),
-                                         shift, digit_off, status, fs->epoch + tk, kout, kmap, vout,
-                                     [&](uint32_t li) { return vin[base + li]; });
+  onesweep_partition<OS_ITEMS, NB, VALS>(S, k, vmask, part, cnt, shift, digit_off, status,
+                                         fs->epoch + tk, kout, kmap, vout,
+                                         [&](uint32_t li) { return vin[base + li]; });
 }
 
 // Upfront histogram of all eight 8-bit digits of the depth keys.
@@ -95,6 +106,7 @@ __global__ void __launch_bounds__(256) k_depth_hist(const uint64_t *__restrict__
   const uint32_t n = fs->n_sort;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint64_t k = keys[i];
+    if (k == ~0ull) continue;  // culled: dropped by the first pass
 #pragma unroll
     for (int p = 0; p < 8; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255u], 1u);
   }
@@ -123,7 +135,7 @@ __global__ void k_depth_scan(FrameState *fs) {
 }
 
 // One onesweep pass (dynamic shared memory opted in once per instantiation).
-template <bool VALS, typename KI, typename KO, int MAP, int NB>
+template <bool VALS, typename KI, typename KO, int MAP, int NB, bool DROP = false>
 static void os_launch(int64_t cap, cudaStream_t s, const KI *kin, KO *kout, const uint32_t *vin,
                       uint32_t *vout, const uint32_t *n_ptr, int shift, int sb,
                       const uint32_t *digit_off, uint64_t *status, FrameState *fs, int tk) {
@@ -132,11 +144,11 @@ static void os_launch(int64_t cap, cudaStream_t s, const KI *kin, KO *kout, cons
   static bool done = false;
   const size_t sm = sizeof(OSmem<os_items<VALS, KI>(), VALS, KI, (1 << NB)>);
   if (!done) {
-    cudaFuncSetAttribute(k_onesweep<VALS, KI, KO, MAP, NB>,
+    cudaFuncSetAttribute(k_onesweep<VALS, KI, KO, MAP, NB, DROP>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     done = true;
   }
-  k_onesweep<VALS, KI, KO, MAP, NB><<<grid, OS_THREADS, sm, s>>>(
+  k_onesweep<VALS, KI, KO, MAP, NB, DROP><<<grid, OS_THREADS, sm, s>>>(
       kin, kout, vin, vout, n_ptr, shift, sb, digit_off, status, fs, tk);
 }
 
@@ -162,10 +174,14 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
   *launches += 2;
   for (int p = 0; p < 8; ++p) {
     const int a = p & 1;
-    os_launch<true, uint64_t, uint64_t, MAP_ID, 8>(
-        M_cap, s, (const uint64_t *)w.key_depth[a], w.key_depth[a ^ 1],
-        (const uint32_t *)w.val_depth[a], w.val_depth[a ^ 1], &fs->n_sort, 8 * p, 32,
-        fs->off_depth[p], w.status, fs, TK_DEPTH0 + p);
+    // pass 0 reads all n_sort keys and drops the culled ones; passes 1..7
+    // sort the M survivors
+    auto launch = p == 0 ? os_launch<true, uint64_t, uint64_t, MAP_ID, 8, true>
+                         : os_launch<true, uint64_t, uint64_t, MAP_ID, 8, false>;
+    launch(M_cap, s, (const uint64_t *)w.key_depth[a], w.key_depth[a ^ 1],
+           (const uint32_t *)w.val_depth[a], w.val_depth[a ^ 1],
+           p == 0 ? &fs->n_sort : &fs->stats.M, 8 * p, 32, fs->off_depth[p], w.status, fs,
+           TK_DEPTH0 + p);
     ++*launches;
   }
 }
