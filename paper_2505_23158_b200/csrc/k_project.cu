@@ -1,9 +1,12 @@
 // K2: EWA projection with the Eq. 3 smoothing-filter opacity factor, 2-D
-// dilation, culling and SH colour; one thread per active Gaussian, fp64
-// arithmetic in the reference's operation order (compiled with
-// -fmad=false; every fma() below is one OpenBLAS places).  Survivors are
-// compacted in input order by a single-pass decoupled look-back scan, so the
-// concatenated source index order is preserved (tie order).
+// dilation, culling and SH colour; one active Gaussian per thread and step
+// (persistent CTAs), fp64 arithmetic in the reference's operation order
+// (compiled with -fmad=false; every fma() below is one OpenBLAS places).
+// The fused frame writes every output at the dense concatenated input index
+// (culled inputs get depth key ~0 and leave in the depth sort's first pass),
+// so the source index order -- the depth sort's tie order -- needs no
+// compaction; the compat entry points (lodge_project, the cost
+// table) compact survivors in input order with a decoupled look-back scan.
 //
 // Restates reference src/raster.py:188-291 (project_scene),
 // src/raster.py:176-185 (filter_opacity_factor), src/raster.py:136-173
@@ -416,7 +419,10 @@ struct ProjLevels {
 // all U inputs orders the M survivors by (depth, g) -- exactly
 // np.lexsort((source_index, depth)) -- and leaves the culled ones after them.
 template <typename GT, typename ST>
-__global__ void __launch_bounds__(256, 2) k_project_frame(ProjLevels lv, Work w, FrameState *fs,
+#ifndef LODGE_PROJ_MINB
+#define LODGE_PROJ_MINB 2  // resident CTAs per SM (the persistent grid's size)
+#endif
+__global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLevels lv, Work w, FrameState *fs,
                                                        const lodge_camera *__restrict__ cam_p,
                                                        lodge_raster_params rp, int32_t shade) {
   // persistent CTAs (grid-stride over the slots): the camera and the level
@@ -648,7 +654,7 @@ static void launch_pf(const ProjLevels &lv, const Work &w, FrameState *fs,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  const uint32_t want = (nslots + 255) / 256, cap = 2u * (uint32_t)sms;  // 2 CTAs per SM
+  const uint32_t want = (nslots + 255) / 256, cap = LODGE_PROJ_MINB * (uint32_t)sms;
   k_project_frame<GT, ST><<<want < cap ? want : cap, 256, 0, s>>>(lv, w, fs, cam, rp, shade);
 }
 
