@@ -55,6 +55,10 @@ def parse():
     ap.add_argument("--streams", type=int, default=4,
                     help="frames in flight per GPU (one liblodge context + stream each)")
     ap.add_argument("--cpu-views", type=int, default=1, help="views in the CPU baseline sample")
+    ap.add_argument("--residency", default="full", choices=["full", "stream"],
+                    help="full: the whole store resident; stream: chunk slabs loaded "
+                         "asynchronously into --slots device slots (SURVEY.md 8f rank 4)")
+    ap.add_argument("--slots", type=int, default=3)
     ap.add_argument("--mode", default="blend", choices=["blend", "chunks", "lod", "full"],
                     help="render mode of the reference CLI (src/cli.py:219-243); the "
                          "metric is quoted on blend")
@@ -309,12 +313,26 @@ def run_lodge(args):
         dist.init_process_group("nccl", device_id=dev)
     t_setup = time.time()
     cfg = scenes.build(args.config)
-    levels = [DeviceLevel.from_tensors(torch.from_numpy(g).to(dev), torch.from_numpy(s).to(dev),
-                                       cfg.degree) for g, s, _ in cfg.levels]
-    plan = DevicePlan.from_arrays(cfg.centers, cfg.offsets, cfg.data, cfg.L, dev)
+    store = None
+    if args.residency == "stream":
+        # residency-bounded store: chunk slabs streamed into args.slots slots
+        if args.mode not in ("blend", "chunks"):
+            raise SystemExit("--residency stream renders the chunk modes (blend, chunks)")
+        from paper_2505_23158_b200.streaming import StreamingStore, host_pair
+        store = StreamingStore([(g, s) for g, s, _ in cfg.levels], cfg.centers, cfg.offsets,
+                               cfg.data, dev, n_slots=args.slots)
+        levels = store.device_levels()
+        plan = store.attach(DevicePlan.from_arrays(cfg.centers, cfg.offsets, cfg.data, cfg.L,
+                                                   dev))
+        store_gb = store.resident_bytes() / 1e9
+    else:
+        levels = [DeviceLevel.from_tensors(torch.from_numpy(g).to(dev),
+                                           torch.from_numpy(s).to(dev), cfg.degree)
+                  for g, s, _ in cfg.levels]
+        plan = DevicePlan.from_arrays(cfg.centers, cfg.offsets, cfg.data, cfg.L, dev)
+        store_gb = sum(l.nbytes() for l in levels) / 1e9
     r = LG.Renderer(levels, plan, device=dev, storage="fp32", precision=args.precision,
                     n_streams=args.streams)
-    store_gb = sum(l.nbytes() for l in levels) / 1e9
     B = args.views_per_step
     schedule = my_views(rank, world, args.warmup + args.steps, B)
     sweep = cfg.sweep(SWEEP_VIEWS)
@@ -326,10 +344,20 @@ def run_lodge(args):
     n_timed = args.steps * B
     bounds = lod_bounds_of(cfg)
     near = {v: nearest_chunk(cfg.centers, sweep[v].position) for v in flat}
+    pairs = ({v: host_pair(cfg.centers, sweep[v].position) for v in flat}
+             if store is not None else None)
 
     def do_render(cam_row, frame, slot, v):
         """One frame of args.mode (the CLI's render modes, src/cli.py:219-243)."""
-        if args.mode == "blend":
+        if store is not None:  # chunk pair decided on the host, slabs made resident
+            f, o, t = pairs[v]
+            if args.mode == "chunks":
+                o, t = None, 1.0
+            st = r.stream_of(slot)
+            store.require([f, o], st)
+            r.render(cam_row, frame, pair=(f, o), t=t, slot=slot)
+            store.release([f, o], st)
+        elif args.mode == "blend":
             r.render(cam_row, frame, slot=slot)
         elif args.mode == "chunks":
             r.render(cam_row, frame, pair=(near[v], None), slot=slot)
@@ -558,7 +586,10 @@ def run_lodge(args):
             "config": {"workload": workload_name(args.config), "mode": args.mode,
                        "resolution": [W, H],
                        "views_per_step_per_gpu": B, "frames_timed": total_frames,
-                       "precision": args.precision, "store": "fp32 records, replicated",
+                       "precision": args.precision,
+                       "store": ("fp32 records, replicated" if store is None else
+                                 f"fp32 chunk slabs, {args.slots} resident slots, "
+                                 f"{store.loads} loads ({store.bytes_loaded / 1e9:.1f} GB)"),
                        "store_gb": round(store_gb, 2),
                        "l2": "inputs larger than L2: per-frame working set "
                              f"~{(sb['project'] + sb['tile_sort'] + sb['composite']) / 1e9:.1f} GB"

@@ -77,6 +77,15 @@ typedef struct {
   const int64_t *offsets_dev;
   const uint32_t *data_dev;
   int64_t max_set[LODGE_MAX_LEVELS]; /* host-side: max_j |set(j,l)| */
+  /* Residency-bounded store (the background chunk
+   * reload of src/blending.py:140-194): when non-NULL, device tables of K*L
+   * pointers, entry j*L+l = the records of set (j, l) in set order (geometry
+   * n x 12 and SH n x 3T in the levels' storage precision), resident at
+   * least for the frame's chunk pair; lodge_render_frame then reads
+   * Gaussians from the pair's chunk slabs instead of the level stores
+   * (whose geom_dev / sh_dev may be NULL). */
+  const void *const *slab_geom_dev;
+  const void *const *slab_sh_dev;
 } lodge_chunks;
 
 /* Compositing precision.  FAST: fp32 FMA/MUFU compositing with an fp64

@@ -21,6 +21,7 @@ from .importance import (compute_importance, random_rotations, score_active_sele
                          visibility_filter_chunk)
 from .asset import AssetError, DeviceAsset, load_asset
 from .thresholds import CostEvaluation, ThresholdSearcher, cover_table, evaluate_cost
+from .streaming import StreamingStore, host_pair
 
 __version__ = "0.1.0"
 
@@ -34,5 +35,5 @@ __all__ = [
     "ImportanceScores", "PerturbSpec", "compute_importance", "random_rotations",
     "score_active_selection", "visibility_filter_chunk", "AssetError", "DeviceAsset",
     "load_asset", "CostEvaluation", "ThresholdSearcher", "cover_table", "evaluate_cost",
-    "lod_bounds", "render_full", "render_lod",
+    "lod_bounds", "render_full", "render_lod", "StreamingStore", "host_pair",
 ]

@@ -207,7 +207,9 @@ void launch_union(const lodge_chunks &ch, const LevelSlots &ls, FrameState *fs, 
 int launch_project_frame(const lodge_level *levels, const LevelSlots &ls, const Work &w,
                          FrameState *fs, const lodge_camera *cam_dev,
                          const lodge_raster_params &rp, int32_t shade, int32_t exact,
-                         cudaStream_t s);
+                         cudaStream_t s,
+                         const void *const *slab_geom = nullptr,
+                         const void *const *slab_sh = nullptr);
 int launch_project_compat(const lodge_level &level, const int64_t *idx, int64_t n,
                           const double *mod, const Work &w, FrameState *fs,
                           const lodge_camera *cam_dev, const lodge_raster_params &rp,

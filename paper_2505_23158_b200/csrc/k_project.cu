@@ -411,6 +411,10 @@ struct ProjLevels {
   int32_t qnorm[LODGE_MAX_LEVELS];  // LODGE_GEOM_QNORM per level
   uint32_t slot_base[LODGE_MAX_LEVELS + 1];
   int32_t L;
+  // chunk slabs (lodge_chunks.slab_*_dev), or NULL: the union then holds
+  // positions in the owning chunk's set and these tables locate the records
+  const void *const *slab_geom;
+  const void *const *slab_sh;
 };
 
 // Outputs are written at the dense concatenated input index g (level-major
@@ -430,9 +434,12 @@ __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLeve
   __shared__ lodge_camera cam;
   __shared__ uint32_t s_used[LODGE_MAX_LEVELS], s_cat[LODGE_MAX_LEVELS];
   __shared__ double s_t;
+  __shared__ int32_t s_f, s_o;
   if (threadIdx.x == 0) {
     cam = *cam_p;
     s_t = fs->stats.t;
+    s_f = fs->stats.f;
+    s_o = fs->stats.o < 0 ? fs->stats.f : fs->stats.o;
     uint32_t c = 0;
     for (int k = 0; k < lv.L; ++k) {
       s_cat[k] = c;  // concatenated index offset of level k
@@ -456,12 +463,19 @@ __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLeve
     p.ok = false;
     double v[12];
     uint32_t gidx = 0;
+    const GT *gp = reinterpret_cast<const GT *>(lv.geom[l]);
+    const ST *sp = reinterpret_cast<const ST *>(lv.sh[l]);
     if (valid) {
       gidx = w.union_idx[slot];
       const uint8_t tag = w.union_tag[slot];
       const double t = s_t;
       const double mod = (tag == 3) ? 1.0 : (tag == 1 ? t : 1.0 - t);
-      load_geom<GT>(reinterpret_cast<const GT *>(lv.geom[l]) + (size_t)gidx * 12, v);
+      if (lv.slab_geom) {  // tag 3 / 1: the primary chunk's slab, 2: the other's
+        const int32_t e = ((tag == 2) ? s_o : s_f) * lv.L + l;
+        gp = reinterpret_cast<const GT *>(lv.slab_geom[e]);
+        sp = reinterpret_cast<const ST *>(lv.slab_sh[e]);
+      }
+      load_geom<GT>(gp + (size_t)gidx * 12, v);
       if (lv.qnorm[l]) normalize_rot(v);
       p = project_core(v, cam, rp, mod, true);
     }
@@ -480,8 +494,7 @@ __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLeve
     if (shade) {
       const int deg = lv.degree[l];
       const int terms = (deg + 1) * (deg + 1);
-      eval_sh_dev<ST>(reinterpret_cast<const ST *>(lv.sh[l]) + (size_t)gidx * 3 * terms, terms,
-                      deg, v, cam, rgb);
+      eval_sh_dev<ST>(sp + (size_t)gidx * 3 * terms, terms, deg, v, cam, rgb);
     }
     const double inv_det = 1.0 / p.det;
     const double A = p.c11 * inv_det, B = (-p.c01) * inv_det, C = p.c00 * inv_det;
@@ -660,9 +673,12 @@ static void launch_pf(const ProjLevels &lv, const Work &w, FrameState *fs,
 
 int launch_project_frame(const lodge_level *levels, const LevelSlots &ls, const Work &w,
                          FrameState *fs, const lodge_camera *cam_dev,
-                         const lodge_raster_params &rp, int32_t shade, int32_t, cudaStream_t s) {
+                         const lodge_raster_params &rp, int32_t shade, int32_t, cudaStream_t s,
+                         const void *const *slab_geom, const void *const *slab_sh) {
   ProjLevels lv;
   lv.L = ls.n_levels;
+  lv.slab_geom = slab_geom;
+  lv.slab_sh = slab_sh;
   const int32_t prec_bits = LODGE_GEOM_FP32 | LODGE_SH_FP32;
   const int32_t fl = levels[0].flags & prec_bits;
   for (int l = 0; l < lv.L; ++l) {

@@ -177,6 +177,7 @@ struct UnionArgs {
   uint32_t status_stride;  // look-back words per level
   uint32_t slot_base[LODGE_MAX_LEVELS + 1];
   uint32_t part_base[LODGE_MAX_LEVELS + 1];  // CTA-count table offsets per level
+  int32_t slab;                              // write set positions (chunk slabs)
 };
 
 // The two sorted sets of level l for the frame's chunk pair.
@@ -281,13 +282,15 @@ __global__ void __launch_bounds__(UN_THREADS) k_union_merge(UnionArgs a, FrameSt
     if (dl + it < dn) {
       const uint32_t av = s_a[ia + 1], bv = s_b[jb];
       const bool a_ok = i0 + ia < u.na, b_ok = j0 + jb < u.nb;
+      // slab mode: the position in the owning chunk's set (tag 3/1: the
+      // primary, 2: the other) instead of the Gaussian's index
       if (a_ok && (!b_ok || av <= bv)) {
-        vals[it] = av;
+        vals[it] = a.slab ? i0 + ia : av;
         tags[it] = (b_ok && bv == av) ? 3 : 1;
         kmask |= 1u << it;
         ++ia;
       } else {
-        vals[it] = bv;
+        vals[it] = a.slab ? j0 + jb : bv;
         tags[it] = 2;
         if (!(i0 + ia > 0 && s_a[ia] == bv)) kmask |= 1u << it;
         ++jb;
@@ -457,6 +460,7 @@ void launch_union(const lodge_chunks &ch, const LevelSlots &ls, FrameState *fs, 
   for (int l = 0; l <= LODGE_MAX_LEVELS; ++l) a.slot_base[l] = (l <= ch.L) ? ls.slot_base[l] : 0;
   for (int l = 0; l < ch.L; ++l) max_slots = max(max_slots, ls.slot_base[l + 1] - ls.slot_base[l]);
   a.status_stride = union_status_stride(max_slots);
+  a.slab = ch.slab_geom_dev != nullptr ? 1 : 0;
   a.part_base[0] = 0;
   for (int l = 0; l < ch.L; ++l)
     a.part_base[l + 1] =

@@ -347,7 +347,8 @@ int lodge_rasterize(lodge_ctx *c, const lodge_batch *b, int64_t M, int64_t n_inp
 static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots &ls,
                        const lodge_camera *cam_dev, int32_t W, int32_t H,
                        const lodge_raster_params &rp, int32_t flags, const lodge_frame_out *out,
-                       lodge_frame_stats *stats_dev, int32_t nl, const char *name);
+                       lodge_frame_stats *stats_dev, int32_t nl, const char *name,
+                       const lodge_chunks *ch);
 
 int lodge_render_frame(lodge_ctx *c, const lodge_level *levels, int32_t n_levels,
                        const lodge_chunks *ch, const lodge_camera *cam_dev, int32_t W, int32_t H,
@@ -396,7 +397,7 @@ int lodge_render_frame(lodge_ctx *c, const lodge_level *levels, int32_t n_levels
   c->mark(1);
   launch_union(*ch, ls, c->fs, w.status, w.union_idx, w.union_tag, s); nl += 2;
   return render_tail(c, levels, ls, cam_dev, W, H, *rp, flags, out, stats_dev, nl,
-                     "lodge_render_frame");
+                     "lodge_render_frame", ch);
 }
 
 // Everything after the active-set stage, shared by the chunk and LOD paths:
@@ -405,7 +406,8 @@ int lodge_render_frame(lodge_ctx *c, const lodge_level *levels, int32_t n_levels
 static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots &ls,
                        const lodge_camera *cam_dev, int32_t W, int32_t H,
                        const lodge_raster_params &rp, int32_t flags, const lodge_frame_out *out,
-                       lodge_frame_stats *stats_dev, int32_t nl, const char *name) {
+                       lodge_frame_stats *stats_dev, int32_t nl, const char *name,
+                       const lodge_chunks *ch) {
   cudaStream_t s = c->stream;
   Work &w = c->w;
   const bool exact = c->precision == LODGE_PREC_EXACT;
@@ -415,7 +417,8 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
   if ((flags & LODGE_RECORD_MAX) && !(flags & LODGE_ACCUMULATE_MAX) && out->maxw_dev)
     CK(cudaMemsetAsync(out->maxw_dev, 0, (exact ? 8 : 4) * (size_t)U_cap, s));
   int rc = launch_project_frame(levels, ls, w, c->fs, cam_dev, rp,
-                                (flags & LODGE_NEED_IMAGE) ? 1 : 0, exact, s);
+                                (flags & LODGE_NEED_IMAGE) ? 1 : 0, exact, s,
+                                ch ? ch->slab_geom_dev : nullptr, ch ? ch->slab_sh_dev : nullptr);
   if (rc) return set_err(LODGE_ERR_BAD_ARG, "all levels must share one storage precision");
   ++nl;
   c->mark(3);
@@ -473,7 +476,7 @@ int lodge_render_lod(lodge_ctx *c, const lodge_level *levels, int32_t n_levels,
                      c->w.union_idx, c->w.union_tag, c->stream);
   nl += 2;
   return render_tail(c, levels, ls, cam_dev, W, H, *rp, flags, out, stats_dev, nl,
-                     "lodge_render_lod");
+                     "lodge_render_lod", nullptr);
 }
 
 int lodge_frame_lists(lodge_ctx *c, int32_t T, int64_t *tile_offsets, int64_t *tile_src,
