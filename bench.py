@@ -485,8 +485,8 @@ def run_lodge(args):
     e2e = None
     if not args.no_e2e:
         # double-buffered pinned camera upload (the host refills a buffer only
-        # after its previous copy completed), renders on the slot streams, then
-        # the 8-bit images + stats read back on the current stream each step
+        # after its previous copy completed), renders on the slot streams, each
+        # frame's 8-bit image + stats read back on its slot stream
         cam_host = [torch.empty((B, cams.shape[1]), dtype=torch.uint8).pin_memory()
                     for _ in range(2)]
         cam_dev = [torch.empty((B, cams.shape[1]), dtype=torch.uint8, device=dev)
@@ -495,7 +495,6 @@ def run_lodge(args):
         img8 = torch.empty((B, H, W, 3), dtype=torch.uint8, device=dev)
         img8_host = torch.empty((B, H, W, 3), dtype=torch.uint8).pin_memory()
         st_host = torch.empty((B, STATS_BYTES), dtype=torch.uint8).pin_memory()
-        st_dev = torch.empty((B, STATS_BYTES), dtype=torch.uint8, device=dev)
         cams_host = cams.cpu()
         if world > 1:
             dist.barrier()
@@ -516,12 +515,13 @@ def run_lodge(args):
             for j, v in enumerate(schedule[s]):
                 do_render(cam_dev[par][j], frames[j], j % S, v)
                 r.to_srgb8(frames[j], img8[j], slot=j % S)
+                # each frame's read-back on its own stream, so it overlaps the
+                # frames still rendering instead of gating the next step
                 with torch.cuda.stream(r.stream_of(j % S)):
-                    st_dev[j].copy_(frames[j].stats, non_blocking=True)
-            for q in range(S):
-                cur.wait_stream(r.stream_of(q))
-            img8_host.copy_(img8, non_blocking=True)
-            st_host.copy_(st_dev, non_blocking=True)
+                    img8_host[j].copy_(img8[j], non_blocking=True)
+                    st_host[j].copy_(frames[j].stats, non_blocking=True)
+        for q in range(S):
+            cur.wait_stream(r.stream_of(q))
         f1.record(cur)
         torch.cuda.synchronize()
         ems = f0.elapsed_time(f1)
