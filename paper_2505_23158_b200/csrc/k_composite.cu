@@ -145,12 +145,12 @@ struct CompParams {
 
 template <bool EXACT>
 #ifndef LODGE_COMP_MINB
-#define LODGE_COMP_MINB 1
+#define LODGE_COMP_MINB 9  // FAST: resident CTAs per SM (register cap; 9 x 64 threads)
 #endif
 #ifndef LODGE_COMP_GROUP
 #define LODGE_COMP_GROUP 4  // list members per FAST iteration
 #endif
-__global__ void __launch_bounds__(CC<EXACT>::CT, LODGE_COMP_MINB) k_composite(
+__global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_composite(
     const uint32_t *__restrict__ list, const uint32_t *__restrict__ tile_start,
     const uint32_t *__restrict__ tile_order, const Payload *__restrict__ payload,
     const Precise *__restrict__ precise, FrameState *fs, const CompParams cpar, void *image,
