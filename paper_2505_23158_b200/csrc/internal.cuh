@@ -202,7 +202,7 @@ void launch_select_frame(const double *centers, int32_t K, const lodge_camera *c
                          const int32_t *pair, const double *t_override, int32_t have_pair,
                          int32_t pair_f, int32_t pair_o, double t_val, FrameState *fs,
                          cudaStream_t s);
-void launch_union(const lodge_chunks &ch, const LevelSlots &ls, FrameState *fs, uint64_t *status,
+int launch_union(const lodge_chunks &ch, const LevelSlots &ls, FrameState *fs, uint64_t *status,
                   uint32_t *union_idx, uint8_t *union_tag, cudaStream_t s);
 int launch_project_frame(const lodge_level *levels, const LevelSlots &ls, const Work &w,
                          FrameState *fs, const lodge_camera *cam_dev,

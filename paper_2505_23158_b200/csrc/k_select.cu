@@ -450,7 +450,7 @@ void launch_band_select(const lodge_level *levels, int32_t L, const double *boun
   k_union_sizes<<<1, 32, 0, s>>>(L, fs);
 }
 
-void launch_union(const lodge_chunks &ch, const LevelSlots &ls, FrameState *fs, uint64_t *status,
+int launch_union(const lodge_chunks &ch, const LevelSlots &ls, FrameState *fs, uint64_t *status,
                   uint32_t *union_idx, uint8_t *union_tag, cudaStream_t s) {
   UnionArgs a;
   a.offsets = ch.offsets_dev;
@@ -471,11 +471,14 @@ void launch_union(const lodge_chunks &ch, const LevelSlots &ls, FrameState *fs, 
   const uint32_t nparts = a.part_base[ch.L];
   uint32_t *splits = reinterpret_cast<uint32_t *>(status);
   uint64_t *lb = status + (nparts + ch.L + 2) / 2 + 1;
+  int launches = 1;
   if (max_slots > 0 && nparts > 0) {
     k_union_split<<<(nparts + ch.L + 255) / 256, 256, 0, s>>>(a, fs, splits);
     k_union_merge<<<nparts, UN_THREADS, 0, s>>>(a, fs, splits, lb, union_idx, union_tag);
+    launches += 2;
   }
   k_union_sizes<<<1, 32, 0, s>>>(ch.L, fs);
+  return launches;  // kernels enqueued
 }
 
 __global__ void k_begin_frame(FrameState *fs) {

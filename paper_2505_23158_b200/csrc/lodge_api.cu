@@ -395,7 +395,7 @@ int lodge_render_frame(lodge_ctx *c, const lodge_level *levels, int32_t n_levels
   launch_select_frame(ch->centers_dev, ch->K, cam_dev, nullptr, nullptr, pair != nullptr, pf, po,
                       tv, c->fs, s); ++nl;
   c->mark(1);
-  launch_union(*ch, ls, c->fs, w.status, w.union_idx, w.union_tag, s); nl += 2;
+  nl += launch_union(*ch, ls, c->fs, w.status, w.union_idx, w.union_tag, s);
   return render_tail(c, levels, ls, cam_dev, W, H, *rp, flags, out, stats_dev, nl,
                      "lodge_render_frame", ch);
 }
@@ -426,7 +426,7 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
   c->mark(4);
   launch_tile_setup(w, c->fs, out->tile_count_dev, tiles_x, tiles_y, s); ++nl;
   c->mark(5);
-  launch_duplicate(w, c->fs, tiles_x, U_cap, s); ++nl;
+  launch_duplicate(w, c->fs, tiles_x, U_cap, s); nl += 2;  // count, emit
   c->mark(6);
   launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s);
   c->mark(7);
