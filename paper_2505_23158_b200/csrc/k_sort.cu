@@ -18,6 +18,9 @@
 
 namespace lodge {
 
+#ifndef LODGE_OS_ITEMS_D
+#define LODGE_OS_ITEMS_D 20  // depth passes (u64 key + u32 value); one wave at config 3
+#endif
 #ifndef LODGE_OS_ITEMS_T1
 #define LODGE_OS_ITEMS_T1 16
 #endif
@@ -28,7 +31,7 @@ namespace lodge {
 // for the tile passes on u64 and u32 keys.
 template <bool VALS, typename KI>
 __host__ __device__ constexpr int os_items() {
-  return VALS ? 16 : (sizeof(KI) == 8 ? LODGE_OS_ITEMS_T1 : LODGE_OS_ITEMS_T2);
+  return VALS ? LODGE_OS_ITEMS_D : (sizeof(KI) == 8 ? LODGE_OS_ITEMS_T1 : LODGE_OS_ITEMS_T2);
 }
 
 // Key maps applied at the scatter (see launch_tile_sort).
