@@ -107,3 +107,29 @@ def test_overflow_recovers(street):
     cam = scenes.camera(12.0)
     fr, st = r.render_camera(cam)
     assert st.overflow == 0 and st.P > 0
+
+
+@pytest.mark.parametrize("res", [(3840, 2160), (1277, 719), (17, 1)])
+@pytest.mark.parametrize("precision", ["fast", "exact"])
+def test_street_other_resolutions_vs_oracle(street, res, precision):
+    """4K (8160 -> 32640 tiles: the tile sort's high digit grows to 8 bits),
+    an odd size with partial edge tiles, and a one-row strip (single tile
+    pass), through the fused path in both precisions."""
+    cfg, _ = street
+    w, h = res
+    r = L.Renderer(street[1].levels, street[1].plan, precision=precision)
+    cam = scenes.camera(47.0, width=w, height=h, focal=scenes.FOCAL * max(w, 64) / 1920)
+    fr, st = r.render_camera(cam)
+    (f, o, t), sel, ref = oracle_frame(cfg, cam)
+    assert st.M == len(ref["batch"]["src"]) and st.P == ref["P"]
+    assert np.array_equal(fr.tile_count.cpu().numpy(), ref["per_tile_count"])
+    offs, src = frame_lists(r, fr, st)
+    assert np.array_equal(offs, ref["tile_offsets"]) and np.array_equal(src, ref["tile_src"])
+    img = fr.image.double().cpu().numpy()
+    if precision == "exact":
+        assert np.abs(img - ref["image"]).max() <= 1e-12
+        assert np.array_equal(fr.visible.cpu().numpy(), ref["per_pixel_visible"])
+        mw = fr.maxw[:st.U].double().cpu().numpy()
+        np.testing.assert_allclose(mw, ref["per_gaussian_max_weight"], rtol=1e-12)
+    else:
+        assert np.abs(img - ref["image"]).max() <= 1e-3
