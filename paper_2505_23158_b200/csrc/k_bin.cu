@@ -224,22 +224,55 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_emit(const uint32_t *__rest
   const uint32_t r0 = w.chunk_first[c];
   const uint32_t r1 = (j1 < P) ? w.chunk_first[c + 1] : M - 1;
   const uint32_t nr = r1 - r0 + 1;
+  const uint32_t npair = j1 - j0;
+  __shared__ uint16_t s_own[EMIT_CHUNK];   // owner (local index) of each pair
+  __shared__ uint32_t s_wmax[DUP_THREADS / 32];
+  for (uint32_t k = threadIdx.x; k < EMIT_CHUNK; k += DUP_THREADS) s_own[k] = 0;
   for (uint32_t q = threadIdx.x; q < nr; q += DUP_THREADS) {
     s_off[q] = w.splat_off[r0 + q];
     s_rect[q] = w.rect_sorted[r0 + q];
     s_m[q] = order[r0 + q];
   }
   __syncthreads();
+  // each owner marks its first pair in the chunk; an inclusive max-scan then
+  // gives every pair its owner (owners have >= 1 pair, so starts differ)
+  for (uint32_t q = threadIdx.x; q < nr; q += DUP_THREADS) {
+    const uint32_t st = s_off[q] > j0 ? s_off[q] - j0 : 0u;
+    if (st < npair) s_own[st] = (uint16_t)q;
+  }
+  __syncthreads();
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t v[EMIT_ITEMS], run = 0;
+#pragma unroll
+    for (int i = 0; i < EMIT_ITEMS; ++i) {
+      v[i] = s_own[threadIdx.x * EMIT_ITEMS + i];
+      run = max(run, v[i]);
+      v[i] = run;
+    }
+    uint32_t inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
+      if (lane >= o) inc = max(inc, t);
+    }
+    if (lane == 31) s_wmax[warp] = inc;
+    __syncthreads();
+    uint32_t pre = __shfl_up_sync(FULL_MASK, inc, 1);
+    if (lane == 0) pre = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < DUP_THREADS / 32; ++w2)
+      if (w2 < warp) pre = max(pre, s_wmax[w2]);
+#pragma unroll
+    for (int i = 0; i < EMIT_ITEMS; ++i)
+      s_own[threadIdx.x * EMIT_ITEMS + i] = (uint16_t)max(pre, v[i]);
+  }
+  __syncthreads();
 #pragma unroll
   for (int it = 0; it < EMIT_ITEMS; ++it) {
     const uint32_t j = j0 + it * DUP_THREADS + threadIdx.x;
     if (j >= j1) break;
-    uint32_t lo = 0, hi = nr - 1;
-    while (lo < hi) {  // last q with s_off[q] <= j
-      const uint32_t mid = (lo + hi + 1) >> 1;
-      if (s_off[mid] <= j) lo = mid;
-      else hi = mid - 1;
-    }
+    const uint32_t lo = s_own[j - j0];
     const uint64_t rc = s_rect[lo];
     const uint32_t x0 = rc & 0xffff, x1 = (rc >> 16) & 0xffff, y0 = (rc >> 32) & 0xffff;
     const uint32_t wdt = x1 - x0 + 1;
