@@ -104,8 +104,8 @@ __device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI, (1 << 
   if (cnt_valid == (uint32_t)(OS_THREADS * ITEMS)) rank_items(std::false_type{});
   else rank_items(std::true_type{});
   __syncthreads();
-  // thread dg < D: digit dg's exclusive offsets over (warp, chain), its
-  // partition total, then its look-back across partitions
+  // thread dg < D: digit dg's exclusive offsets over (warp, chain) and its
+  // partition total
   const uint32_t dg = tid;
   uint32_t tot = 0;
   if (dg < D) {
@@ -116,6 +116,30 @@ __device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI, (1 << 
       S.whist[1][w][dg] = tot + a;
       tot += a + b;
     }
+  }
+  // partition-local exclusive scan of the digit totals (zero beyond D)
+  constexpr int DW = (int)((D + 31) / 32);  // warps holding digits
+  uint32_t inc = tot;
+  if (warp < DW) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (DW > 1 && lane == 31) S.misc[1 + warp] = inc;
+  }
+  if (DW > 1) __syncthreads();
+  if (dg < D) {
+    uint32_t wpre = 0;
+#pragma unroll
+    for (int w = 0; w < DW; ++w) wpre += (w < warp) ? S.misc[1 + w] : 0u;
+    S.dstart[dg] = wpre + inc - tot;
+  }
+  __syncthreads();
+  // look-back across partitions for digit dg (threads < D), overlapped with
+  // the staging of this partition's keys by every warp: the staging needs only
+  // the partition-local offsets, the global scatter below needs the look-back
+  if (dg < D) {
     uint64_t *st = status + (size_t)part * D;
     uint32_t excl = 0;
     if (part == 0) {
@@ -146,25 +170,6 @@ __device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI, (1 << 
     }
     S.gbase[dg] = digit_off[dg] + excl;
   }
-  // partition-local exclusive scan of the digit totals (zero beyond D)
-  constexpr int DW = (int)((D + 31) / 32);  // warps holding digits
-  uint32_t inc = tot;
-  if (warp < DW) {
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
-      if (lane >= o) inc += t;
-    }
-    if (DW > 1 && lane == 31) S.misc[1 + warp] = inc;
-  }
-  if (DW > 1) __syncthreads();
-  if (dg < D) {
-    uint32_t wpre = 0;
-#pragma unroll
-    for (int w = 0; w < DW; ++w) wpre += (w < warp) ? S.misc[1 + w] : 0u;
-    S.dstart[dg] = wpre + inc - tot;
-  }
-  __syncthreads();
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     if ((vmask >> i) & 1u) {
