@@ -14,6 +14,9 @@ Files:
                modulation, alpha_min=0, dilation 0, odd resolutions).
   config1.npz  BASELINE config 1 (SURVEY.md 8d recipe): deep_street 10k,
                2 LOD levels, 4 chunks, 8 views at 128x128, stateless blend.
+  importance / asset / thresholds / modes / street .npz: see each make_*.
+
+    python oracle/make_golden.py street      # regenerate one file
 """
 
 from __future__ import annotations
@@ -423,16 +426,94 @@ def make_modes():
     return out
 
 
-def main():
-    os.makedirs(OUT, exist_ok=True)
+def make_street():
+    """Residency streaming and blend renders (src/blending.py:140-203) on the
+    reference's own street_runtime fixture (tests/test_blending.py:21-33):
+    deep_street(6, 1500 fine, 8 views, 80x64, f 70, length 70), one built
+    level at 9.0 (single round), three chunk centres on the corridor axis.
+    Records the stream_step walk z = 8..44 (400 steps, every state and
+    event), a teleport, and render_blend_state frames at six walk positions,
+    plus the swap-instant and t = 1 renders of TestSwapConsistency."""
+    from splatlod.blending import render_blend_state, render_selection, stream_step
     t0 = time.time()
-    np.savez_compressed(os.path.join(OUT, "cases.npz"), **make_cases())
-    print("cases", round(time.time() - t0, 1), "s")
-    np.savez_compressed(os.path.join(OUT, "config1.npz"), **make_config1())
-    np.savez_compressed(os.path.join(OUT, "importance.npz"), **make_importance())
+    scene, cams = deep_street(seed=6, n_fine=1500, n_views=8, resolution=(80, 64),
+                              focal=70.0, length=70.0)
+    cfg = LodBuildConfig(importance_views=tuple(cams), reference_focal=70.0)
+    levels, _ = build_levels(scene, [9.0], cfg, single_round=True)
+    positions = np.stack([c.position for c in cams])
+    centers = np.array([[0.0, 0.5, 12.0], [0.0, 0.5, 28.0], [0.0, 0.5, 44.0]])
+    radii = chunk_radii(centers, positions)
+    plan = build_chunk_active_sets(levels, centers, radii)
+    d = {"n_levels": np.array(len(levels)), "centers": plan.centers, "radii": plan.radii}
+    for l, lv in enumerate(levels):
+        scene_arrays(lv.scene, f"L{l}/", d)
+        d[f"L{l}/depth_threshold"] = np.array(lv.depth_threshold)
+    for j in range(plan.n_chunks):
+        for l in range(plan.n_levels):
+            d[f"set/{j}/{l}"] = plan.active_sets[j][l]
+    for v, cam in enumerate(cams):
+        cam_arrays(cam, f"v{v}/", d)
+    rc = R.RasterConfig()
+    kinds = {"load": 0, "unload": 1, "swap_primary": 2}
+
+    def walk(tag, zs, render_at=()):
+        state, ev, st = None, [], []
+        for i, z in enumerate(zs):
+            pos = np.array([0.0, 0.5, z])
+            state, events = stream_step(state, plan, pos)
+            ev += [(i, kinds[e.kind], e.chunk_id) + tuple(e.camera_position) for e in events]
+            lc = state.loaded_chunks + (-1,) * (2 - len(state.loaded_chunks))
+            st.append(lc + (state.primary_id, state.t_bar, state.t))
+            if i in render_at:
+                cam = cams[0]
+                view = Camera(pos, cam.orientation, cam.focal, cam.principal_point,
+                              cam.resolution, cam.near_plane)
+                out = render_blend_state(state, plan, levels, view, rc)
+                p = f"{tag}/r{i}/"
+                d[p + "image"] = out.image
+                d[p + "tile_count"] = out.per_tile_count
+                d[p + "visible"] = out.per_pixel_visible
+                d[p + "maxw"] = out.per_gaussian_max_weight
+        d[tag + "/zs"] = np.asarray(zs, np.float64)
+        d[tag + "/events"] = np.array(ev, np.float64).reshape(-1, 6)
+        d[tag + "/states"] = np.array(st, np.float64)
+
+    walk("walk", np.linspace(8.0, 44.0, 400), render_at=(0, 90, 170, 200, 260, 399))
+    walk("teleport", np.array([10.0, 60.0]))
+    # swap instant (tests/test_blending.py:201-215) and t = 1 (:108-115)
+    cam = cams[0]
+    swap_pos = plan.centers[1]
+    view = Camera(swap_pos, cam.orientation, cam.focal, cam.principal_point, cam.resolution,
+                  cam.near_plane)
+    for tag, o in (("swap_old", 0), ("swap_new", 2)):
+        t = blend_factor(swap_pos, plan.centers[1], plan.centers[o])[1]
+        d[tag + "/t"] = np.array(t)
+        d[tag + "/image"] = render_selection(levels, compose_active(plan, levels, 1, o, t),
+                                             view, rc).image
+    d["t_one/image"] = render_selection(levels, compose_active(plan, levels, 0, 1, 1.0),
+                                        cams[2], rc).image
+    print("street", round(time.time() - t0, 1), "s; levels", [len(l) for l in levels],
+          "sets", [[len(s) for s in ch] for ch in plan.active_sets],
+          "events", d["walk/events"].shape[0])
+    return d
+
+
+GENERATORS = {"cases": make_cases, "config1": make_config1, "importance": make_importance,
+              "asset": make_asset, "thresholds": make_thresholds, "modes": make_modes,
+              "street": make_street}
+
+
+def main(names=None):
+    """Regenerate the named golden files (default: all); config1 must exist
+    (or be generated first) for the generators that reuse its objects."""
+    os.makedirs(OUT, exist_ok=True)
+    for name in names or list(GENERATORS):
+        t0 = time.time()
+        np.savez_compressed(os.path.join(OUT, name + ".npz"), **GENERATORS[name]())
+        print(name, round(time.time() - t0, 1), "s")
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)) // 1024, "KiB")
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:])
