@@ -248,6 +248,18 @@ int lodge_render_lod(lodge_ctx *ctx, const lodge_level *levels, int32_t n_levels
                      int32_t h, const lodge_raster_params *rp, int32_t flags,
                      const lodge_frame_out *out, lodge_frame_stats *stats_dev);
 
+/* The band selection alone: replaces select_active (src/lod.py:192-211) and,
+ * called once per chunk centre with the radius folded into bounds,
+ * build_chunk_active_sets (src/chunks.py:122-135).  Level l keeps the
+ * Gaussians with bounds[l] <= ||mean - pos|| < bounds[l+1] (bounds host,
+ * n_levels+1 values), in ascending index order.  pos_dev: device double[3].
+ * idx_dev: uint32, capacity sum of levels[].n; level l's members start at
+ * sum_{k<l} levels[k].n.  sizes_dev: uint32 per level.  Async on the context
+ * stream. */
+int lodge_select_active(lodge_ctx *ctx, const lodge_level *levels, int32_t n_levels,
+                        const double *bounds, const double *pos_dev, uint32_t *idx_dev,
+                        uint32_t *sizes_dev);
+
 /* ---- threshold-search cost table ----------------
  * replaces ThresholdSearcher._table, src/thresholds.py:80-90: project the
  * level's inputs (idx_dev, or all n when NULL) with shade=False; for the M

@@ -11,7 +11,8 @@ from .types import (ActiveSelection, BlendState, Camera, ChunkPlan, Gaussian, Lo
                     quat_to_matrix)
 from .raster import (project_gaussian, project_scene, rasterize, render_scene,
                      tile_cover_counts, visibility_histogram)
-from .lod import lod_bounds, project_selection, render_full, render_lod
+from .lod import (build_chunk_active_sets, lod_bounds, project_selection, render_full,
+                  render_lod, select_active)
 from .blending import (blend_factor, compose_active, nearest_two_chunks, render_blend_state,
                        render_selection, stream_step)
 from .renderer import Frame, Renderer
@@ -35,5 +36,6 @@ __all__ = [
     "ImportanceScores", "PerturbSpec", "compute_importance", "random_rotations",
     "score_active_selection", "visibility_filter_chunk", "AssetError", "DeviceAsset",
     "load_asset", "CostEvaluation", "ThresholdSearcher", "cover_table", "evaluate_cost",
-    "lod_bounds", "render_full", "render_lod", "StreamingStore", "host_pair",
+    "lod_bounds", "render_full", "render_lod", "select_active", "build_chunk_active_sets",
+    "StreamingStore", "host_pair",
 ]

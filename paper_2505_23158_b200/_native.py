@@ -107,6 +107,8 @@ EXPORTS = {
     "lodge_render_lod": ([C.c_void_p, C.POINTER(Level), C.c_int32, C.POINTER(C.c_double),
                           C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.POINTER(RasterParams),
                           C.c_int32, C.POINTER(FrameOut), C.c_void_p], C.c_int),
+    "lodge_select_active": ([C.c_void_p, C.POINTER(Level), C.c_int32, C.POINTER(C.c_double),
+                             C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "lodge_cover_table": ([C.c_void_p, C.POINTER(Level), C.c_void_p, C.c_int64,
                            C.POINTER(Camera), C.POINTER(RasterParams), C.c_void_p, C.c_void_p,
                            C.POINTER(C.c_int64)], C.c_int),

@@ -235,7 +235,7 @@ void launch_asset_split(const float *blob, int64_t n, int32_t width, float *geom
 void launch_asset_sets(const lodge_chunks &ch, const int64_t *level_size_dev, int32_t *flags_dev,
                        cudaStream_t s);
 void launch_band_select(const lodge_level *levels, int32_t L, const double *bounds, int32_t full,
-                        const LevelSlots &ls, FrameState *fs, const lodge_camera *cam,
+                        const LevelSlots &ls, FrameState *fs, const double *pos_dev,
                         uint64_t *status, uint32_t *union_idx, uint8_t *union_tag,
                         cudaStream_t s);
 int launch_cover_keys(const lodge_level &level, const int64_t *idx, int64_t n, const Work &w,

@@ -358,7 +358,7 @@ struct BandArgs {
 };
 
 __global__ void __launch_bounds__(UN_THREADS) k_band_select(BandArgs a, FrameState *fs,
-                                                           const lodge_camera *__restrict__ cam,
+                                                           const double *__restrict__ pos,
                                                            uint64_t *lb_status,
                                                            uint32_t *union_idx,
                                                            uint8_t *union_tag) {
@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(UN_THREADS) k_band_select(BandArgs a, FrameSta
   const uint32_t part = g - a.part_base[l];
   const int64_t n = a.n[l];
   const int64_t i0 = (int64_t)part * UN_TILE + (int64_t)threadIdx.x * UN_ITEMS;
-  const double px = cam->pos[0], py = cam->pos[1], pz = cam->pos[2];
+  const double px = pos[0], py = pos[1], pz = pos[2];
   uint32_t kmask = 0;
 #pragma unroll
   for (int it = 0; it < UN_ITEMS; ++it) {
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(UN_THREADS) k_band_select(BandArgs a, FrameSta
 }
 
 void launch_band_select(const lodge_level *levels, int32_t L, const double *bounds, int32_t full,
-                        const LevelSlots &ls, FrameState *fs, const lodge_camera *cam,
+                        const LevelSlots &ls, FrameState *fs, const double *pos,
                         uint64_t *status, uint32_t *union_idx, uint8_t *union_tag,
                         cudaStream_t s) {
   BandArgs a;
@@ -446,7 +446,7 @@ void launch_band_select(const lodge_level *levels, int32_t L, const double *boun
   for (int l = L + 1; l <= LODGE_MAX_LEVELS; ++l) a.part_base[l] = a.part_base[L];
   const uint32_t nparts = a.part_base[L];
   if (nparts > 0)
-    k_band_select<<<nparts, UN_THREADS, 0, s>>>(a, fs, cam, status, union_idx, union_tag);
+    k_band_select<<<nparts, UN_THREADS, 0, s>>>(a, fs, pos, status, union_idx, union_tag);
   k_union_sizes<<<1, 32, 0, s>>>(L, fs);
 }
 

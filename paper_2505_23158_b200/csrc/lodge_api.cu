@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <cstddef>
 #include <string>
 
 #include "internal.cuh"
@@ -439,6 +440,12 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
   return check_launch(name);
 }
 
+// device address of a device camera's position (address arithmetic only)
+static const double *cam_pos(const lodge_camera *cam_dev) {
+  return reinterpret_cast<const double *>(reinterpret_cast<const char *>(cam_dev) +
+                                          offsetof(lodge_camera, pos));
+}
+
 int lodge_render_lod(lodge_ctx *c, const lodge_level *levels, int32_t n_levels,
                      const double *bounds, int32_t full, const lodge_camera *cam_dev, int32_t W,
                      int32_t H, const lodge_raster_params *rp, int32_t flags,
@@ -472,11 +479,45 @@ int lodge_render_lod(lodge_ctx *c, const lodge_level *levels, int32_t n_levels,
   c->mark(0);
   launch_begin_frame(c->fs, c->stream); ++nl;
   c->mark(1);
-  launch_band_select(levels, n_levels, bounds, full, ls, c->fs, cam_dev, c->w.status,
+  launch_band_select(levels, n_levels, bounds, full, ls, c->fs, cam_pos(cam_dev), c->w.status,
                      c->w.union_idx, c->w.union_tag, c->stream);
   nl += 2;
   return render_tail(c, levels, ls, cam_dev, W, H, *rp, flags, out, stats_dev, nl,
                      "lodge_render_lod", nullptr);
+}
+
+int lodge_select_active(lodge_ctx *c, const lodge_level *levels, int32_t n_levels,
+                        const double *bounds, const double *pos_dev, uint32_t *idx_dev,
+                        uint32_t *sizes_dev) {
+  if (!c || !levels || !bounds || !pos_dev || !idx_dev || !sizes_dev)
+    return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  if (n_levels < 1 || n_levels > LODGE_MAX_LEVELS)
+    return set_err(LODGE_ERR_BAD_ARG, "level count must be in 1.." + std::to_string(LODGE_MAX_LEVELS));
+  for (int l = 0; l < n_levels; ++l) {
+    if (levels[l].n > 0x3fffffff) return set_err(LODGE_ERR_BAD_ARG, "level too large");
+    if (levels[l].n > 0 && !levels[l].geom_dev) return set_err(LODGE_ERR_BAD_ARG, "NULL level geometry");
+  }
+  CK(cudaSetDevice(c->device));
+  LevelSlots ls;
+  ls.n_levels = n_levels;
+  ls.slot_base[0] = 0;
+  for (int l = 0; l < n_levels; ++l) ls.slot_base[l + 1] = ls.slot_base[l] + (uint32_t)levels[l].n;
+  const int64_t U_cap = ls.slot_base[n_levels];
+  if (U_cap > 0x3fffffff) return set_err(LODGE_ERR_BAD_ARG, "too many inputs");
+  int rc;
+  if ((rc = ensure_slots(c, std::max<int64_t>(U_cap, 1))) ||
+      (rc = ensure_status(c, (U_cap + 255) / 256 + 256)))
+    return rc;
+  // the band kernel compacts straight into the caller's buffer (level l at
+  // slot_base[l]); its tags go to the context's scratch
+  launch_begin_frame(c->fs, c->stream);
+  launch_band_select(levels, n_levels, bounds, 0, ls, c->fs, pos_dev, c->w.status, idx_dev,
+                     c->w.union_tag, c->stream);
+  CK(cudaMemcpyAsync(sizes_dev,
+                     reinterpret_cast<const char *>(c->fs) + offsetof(FrameState, stats) +
+                         offsetof(lodge_frame_stats, U_level),
+                     4 * (size_t)n_levels, cudaMemcpyDeviceToDevice, c->stream));
+  return check_launch("lodge_select_active");
 }
 
 int lodge_frame_lists(lodge_ctx *c, int32_t T, int64_t *tile_offsets, int64_t *tile_src,

@@ -3,14 +3,16 @@ full-mode renders (src/lod.py:230-237, src/cli.py:221-243) on the fused path."""
 
 from __future__ import annotations
 
+import ctypes as C
 from typing import Optional, Sequence
 
 import numpy as np
 import torch
 
-from .device import _device, context, default_precision, level_for
+from . import _native as N
+from .device import _device, context, default_precision, level_for, ptr
 from .raster import DeviceBatch, project_scene_device
-from .types import RasterConfig, TileRenderOutput
+from .types import ChunkPlan, RasterConfig, TileRenderOutput
 
 
 def project_selection_device(levels: Sequence, sets: Sequence, camera, raster_cfg,
@@ -47,6 +49,55 @@ def lod_bounds(levels: Sequence, depth_offsets: Optional[Sequence[float]] = None
     if offs.shape[0] != n:
         raise ValueError("need one depth offset per level")
     return [0.0] + [levels[l].depth_threshold + offs[l] for l in range(1, n)] + [np.inf]
+
+
+def _band_sets(levels, queries, device=None) -> list:
+    """[(position, bounds)] -> per-query per-level ascending int64 index sets
+    from the device band kernel (lodge_select_active)."""
+    ctx = context(device)
+    dev = ctx.device
+    dl = [level_for(getattr(lv, "scene", lv), dev, "fp64") for lv in levels]
+    arr = (N.Level * len(dl))(*[d.struct for d in dl])
+    sizes_n = [int(d.struct.n) for d in dl]
+    base = np.concatenate([[0], np.cumsum(sizes_n)]).astype(np.int64)
+    pos = torch.tensor(np.asarray([q for q, _ in queries], np.float64).reshape(-1, 3),
+                       dtype=torch.float64, device=dev)
+    idx = torch.empty(max(int(base[-1]), 1), dtype=torch.int32, device=dev)
+    sizes = torch.empty((len(queries), len(dl)), dtype=torch.int32, device=dev)
+    lib = N.lib()
+    out = []
+    for k, (_, bounds) in enumerate(queries):
+        b = (C.c_double * (len(dl) + 1))(*[float(v) for v in bounds])
+        N.check(lib.lodge_select_active(ctx.bind(), arr, len(dl), b, ptr(pos[k]), ptr(idx),
+                                        ptr(sizes[k])), "lodge_select_active")
+        sz = sizes[k].cpu().numpy()  # syncs the context stream; idx is reused
+        flat = idx.cpu().numpy().view(np.uint32)
+        out.append([flat[base[l]:base[l] + sz[l]].astype(np.int64) for l in range(len(dl))])
+    return out
+
+
+def select_active(levels: Sequence, query_point, depth_offsets: Optional[Sequence[float]] = None,
+                  device=None) -> list:
+    """Drop-in select_active (src/lod.py:192-211): per level, the ascending
+    indices whose distance to query_point lies in the level's band, chosen
+    by the device band kernel (the one lodge_render_lod runs per frame)."""
+    bounds = lod_bounds(levels, depth_offsets)
+    return _band_sets(levels, [(np.asarray(query_point, np.float64), bounds)], device)[0]
+
+
+def build_chunk_active_sets(levels: Sequence, centers, radii, camera_assignment=None,
+                            device=None) -> ChunkPlan:
+    """Drop-in build_chunk_active_sets (src/chunks.py:122-135): each chunk's
+    active sets are the band selection at its centre with every boundary
+    above level 0 moved out by its radius."""
+    centers = np.asarray(centers, dtype=np.float64)
+    radii = np.asarray(radii, dtype=np.float64)
+    queries = [(centers[j], lod_bounds(levels, [0.0] + [float(radii[j])] * (len(levels) - 1)))
+               for j in range(centers.shape[0])]
+    sets = tuple(tuple(s) for s in _band_sets(levels, queries, device))
+    assignment = (np.zeros(0, dtype=np.int64) if camera_assignment is None
+                  else np.asarray(camera_assignment, dtype=np.int64))
+    return ChunkPlan(centers, radii, sets, assignment)
 
 
 def _frame_to_host(fr, st, raster_cfg) -> TileRenderOutput:
