@@ -143,7 +143,10 @@ struct CompParams {
   int32_t flags, tiles_x, W, H;
 };
 
-template <bool EXACT>
+// MODE < 0: need_image / record_max from cpar.flags at run time (EXACT);
+// otherwise bit 0 = image, bit 1 = max weights, fixed at compile time (FAST:
+// no per-member branches on either)
+template <bool EXACT, int MODE>
 #ifndef LODGE_COMP_MINB
 #define LODGE_COMP_MINB 9  // FAST: resident CTAs per SM (register cap; 9 x 64 threads)
 #endif
@@ -168,8 +171,9 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
   const float wx_lo = 0.5f, wx_hi = 15.5f;
   const float wy_lo = (float)(warp * ROWS) + 0.5f, wy_hi = wy_lo + (float)(ROWS - 1);
   const int px = tx * 16 + lx, py0 = ty * 16 + ly0;
-  const bool need_image = cpar.flags & LODGE_NEED_IMAGE;
-  const bool record_max = (cpar.flags & LODGE_RECORD_MAX) && maxw != nullptr;
+  const bool need_image = MODE < 0 ? (cpar.flags & LODGE_NEED_IMAGE) != 0 : (MODE & 1) != 0;
+  const bool record_max =
+      MODE < 0 ? (cpar.flags & LODGE_RECORD_MAX) && maxw != nullptr : (MODE & 2) != 0;
   const uint32_t s = tile_start[t];
   uint32_t e = tile_start[t + 1];
   if (fs->stats.overflow) e = s;
@@ -386,14 +390,21 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
         return need_image ? *reinterpret_cast<const float4 *>(&pj.r)
                           : make_float4(0.f, 0.f, 0.f, 0.f);
       };
+      // lane 0 maxes a member's warp-wide weight into its staged slot: one
+      // predicated shared reduction, no branch around it
+      const uint32_t maxw_sa = smem_addr(&S.maxw32[0]);
+      auto record = [&](int j, unsigned wb) {
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "setp.ne.u32 p, %1, 0;\n\t"
+                     "setp.eq.and.u32 p, %2, 0, p;\n\t"
+                     "@p red.shared.max.u32 [%0], %1;\n\t}"
+                     :: "r"(maxw_sa + 4u * (uint32_t)j), "r"(wb), "r"(lane));
+      };
       auto finish = [&](int j, float wmax) {
 #ifdef LODGE_COUNTERS
         c_hit += __any_sync(FULL_MASK, wmax > 0.f) ? 1 : 0;
 #endif
-        if (record_max) {
-          const unsigned wb = __reduce_max_sync(FULL_MASK, __float_as_uint(wmax));
-          if (lane == 0 && wb) atomicMax(&S.maxw32[j], wb);
-        }
+        if (record_max) record(j, __reduce_max_sync(FULL_MASK, __float_as_uint(wmax)));
       };
       // one pixel's blend step with every decision certain in fp32; one PTX
       // block keeps the keep test a predicate (nvcc otherwise materialises
@@ -499,16 +510,27 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
         for (int u = 0; u < G; ++u)
 #pragma unroll
           for (int p = 0; p < PX; ++p) a[u][p] = fminf(ex2_approx(q[u][p] + cn[u].w), cpar.clamp_f);
+        float wm[G];
 #pragma unroll
         for (int u = 0; u < G; ++u) {
           const Payload &pj = PL[js[u]];
           const float hi = pj.hi;
           const float4 c = colour(pj);
-          float w = 0.f;
+          wm[u] = 0.f;
 #pragma unroll
-          for (int p = 0; p < PX; ++p) step(p, q[u][p], hi, a[u][p], c, w);
-          finish(js[u], w);
+          for (int p = 0; p < PX; ++p) step(p, q[u][p], hi, a[u][p], c, wm[u]);
         }
+        if (record_max) {  // the group's warp reductions back to back
+          unsigned wb[G];
+#pragma unroll
+          for (int u = 0; u < G; ++u) wb[u] = __reduce_max_sync(FULL_MASK, __float_as_uint(wm[u]));
+#pragma unroll
+          for (int u = 0; u < G; ++u) record(js[u], wb[u]);
+        }
+#ifdef LODGE_COUNTERS
+#pragma unroll
+        for (int u = 0; u < G; ++u) c_hit += __any_sync(FULL_MASK, wm[u] > 0.f) ? 1 : 0;
+#endif
       };
       int i = 0;
       for (; i + G <= cnt; i += G) {
@@ -587,7 +609,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
   }
 }
 
-template <bool EXACT>
+template <bool EXACT, int MODE>
 static void launch_comp(const Work &w, FrameState *fs, int32_t W, int32_t H,
                         const lodge_raster_params &rp, int32_t flags, const lodge_frame_out &out,
                         cudaStream_t s) {
@@ -596,7 +618,8 @@ static void launch_comp(const Work &w, FrameState *fs, int32_t W, int32_t H,
   const size_t sm = sizeof(CompSmem<EXACT>);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_composite<EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_composite<EXACT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
     attr = true;
   }
   CompParams cp;
@@ -607,16 +630,27 @@ static void launch_comp(const Work &w, FrameState *fs, int32_t W, int32_t H,
   cp.tiles_x = tiles_x;
   cp.W = W;
   cp.H = H;
-  k_composite<EXACT><<<T, CC<EXACT>::CT, sm, s>>>(w.list, w.tile_start, w.tile_order,
-                                                   w.payload, w.precise, fs, cp, out.image_dev,
-                                                   out.visible_dev, out.maxw_dev);
+  k_composite<EXACT, MODE><<<T, CC<EXACT>::CT, sm, s>>>(w.list, w.tile_start, w.tile_order,
+                                                         w.payload, w.precise, fs, cp,
+                                                         out.image_dev, out.visible_dev,
+                                                         out.maxw_dev);
 }
 
 void launch_composite(const Work &w, FrameState *fs, const lodge_camera *, int32_t W, int32_t H,
                       const lodge_raster_params &rp, int32_t flags, int32_t exact,
                       const lodge_frame_out &out, uint32_t, cudaStream_t s) {
-  if (exact) launch_comp<true>(w, fs, W, H, rp, flags, out, s);
-  else launch_comp<false>(w, fs, W, H, rp, flags, out, s);
+  if (exact) {
+    launch_comp<true, -1>(w, fs, W, H, rp, flags, out, s);
+    return;
+  }
+  const int mode = ((flags & LODGE_NEED_IMAGE) ? 1 : 0) |
+                   (((flags & LODGE_RECORD_MAX) && out.maxw_dev) ? 2 : 0);
+  switch (mode) {
+    case 3: launch_comp<false, 3>(w, fs, W, H, rp, flags, out, s); break;
+    case 2: launch_comp<false, 2>(w, fs, W, H, rp, flags, out, s); break;
+    case 1: launch_comp<false, 1>(w, fs, W, H, rp, flags, out, s); break;
+    default: launch_comp<false, 0>(w, fs, W, H, rp, flags, out, s); break;
+  }
 }
 
 // Compat / inspection: export the sorted per-tile lists as source indices.
