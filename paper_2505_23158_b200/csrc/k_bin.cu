@@ -7,6 +7,7 @@
 // splat instead of one per pair), integrated here; the duplication kernel
 // uses a single-pass look-back scan and block-cooperative emission so one
 // huge splat (all 8160 tiles at 1080p) does not serialise a thread.
+#include "emit.cuh"
 #include "internal.cuh"
 
 namespace lodge {
@@ -122,9 +123,7 @@ __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t tile
   }
 }
 
-constexpr int DUP_THREADS = 256;
-constexpr int EMIT_ITEMS = 8;
-constexpr int EMIT_CHUNK = DUP_THREADS * EMIT_ITEMS;  // pairs per emission CTA
+constexpr int EMIT_ITEMS = EMIT_CHUNK / DUP_THREADS;
 constexpr int COUNT_ITEMS = 8;                        // splats per thread in k_dup_count
 
 // Pass 1, one thread per depth-sorted splat: tile count, exclusive scan of
@@ -204,81 +203,25 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
   }
 }
 
-// Pass 2, EMIT_CHUNK pairs per CTA regardless of splat sizes: the owners of
-// the chunk's pairs are a contiguous depth-order range [chunk_first[c],
-// chunk_first[c+1]] staged in shared memory; each pair finds its owner by a
-// binary search there and writes (tile << 32 | splat) coalesced, in depth
-// order (the tile passes in k_sort.cu then sort them stably by tile).
+// Pass 2, EMIT_CHUNK pairs per CTA regardless of splat sizes (emit.cuh),
+// written (tile << 32 | splat) coalesced, in depth order (the tile passes in
+// k_sort.cu then sort them stably by tile).
 __global__ void __launch_bounds__(DUP_THREADS) k_dup_emit(const uint32_t *__restrict__ order,
                                                           int32_t tiles_x, Work w,
                                                           FrameState *fs) {
-  __shared__ uint32_t s_off[EMIT_CHUNK + 2];
-  __shared__ uint64_t s_rect[EMIT_CHUNK + 1];
-  __shared__ uint32_t s_m[EMIT_CHUNK + 1];
+  __shared__ EmitSmem<EMIT_CHUNK> E;
   const uint32_t P = fs->n_pairs;
-  const uint32_t M = fs->stats.M;
-  const uint32_t c = blockIdx.x;
-  const uint32_t j0 = c * EMIT_CHUNK;
+  const uint32_t j0 = blockIdx.x * EMIT_CHUNK;
   if (j0 >= P) return;
   const uint32_t j1 = min(j0 + (uint32_t)EMIT_CHUNK, P);
-  const uint32_t r0 = w.chunk_first[c];
-  const uint32_t r1 = (j1 < P) ? w.chunk_first[c + 1] : M - 1;
-  const uint32_t nr = r1 - r0 + 1;
-  const uint32_t npair = j1 - j0;
-  __shared__ uint16_t s_own[EMIT_CHUNK];   // owner (local index) of each pair
-  __shared__ uint32_t s_wmax[DUP_THREADS / 32];
-  for (uint32_t k = threadIdx.x; k < EMIT_CHUNK; k += DUP_THREADS) s_own[k] = 0;
-  for (uint32_t q = threadIdx.x; q < nr; q += DUP_THREADS) {
-    s_off[q] = w.splat_off[r0 + q];
-    s_rect[q] = w.rect_sorted[r0 + q];
-    s_m[q] = order[r0 + q];
-  }
-  __syncthreads();
-  // each owner marks its first pair in the chunk; an inclusive max-scan then
-  // gives every pair its owner (owners have >= 1 pair, so starts differ)
-  for (uint32_t q = threadIdx.x; q < nr; q += DUP_THREADS) {
-    const uint32_t st = s_off[q] > j0 ? s_off[q] - j0 : 0u;
-    if (st < npair) s_own[st] = (uint16_t)q;
-  }
-  __syncthreads();
-  {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t v[EMIT_ITEMS], run = 0;
-#pragma unroll
-    for (int i = 0; i < EMIT_ITEMS; ++i) {
-      v[i] = s_own[threadIdx.x * EMIT_ITEMS + i];
-      run = max(run, v[i]);
-      v[i] = run;
-    }
-    uint32_t inc = run;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
-      if (lane >= o) inc = max(inc, t);
-    }
-    if (lane == 31) s_wmax[warp] = inc;
-    __syncthreads();
-    uint32_t pre = __shfl_up_sync(FULL_MASK, inc, 1);
-    if (lane == 0) pre = 0;
-#pragma unroll
-    for (int w2 = 0; w2 < DUP_THREADS / 32; ++w2)
-      if (w2 < warp) pre = max(pre, s_wmax[w2]);
-#pragma unroll
-    for (int i = 0; i < EMIT_ITEMS; ++i)
-      s_own[threadIdx.x * EMIT_ITEMS + i] = (uint16_t)max(pre, v[i]);
-  }
-  __syncthreads();
+  uint32_t r0, r1;
+  emit_owners(w, j0, j1, P, fs->stats.M, r0, r1);
+  emit_stage(E, order, w, j0, j1, r0, r1);
 #pragma unroll
   for (int it = 0; it < EMIT_ITEMS; ++it) {
     const uint32_t j = j0 + it * DUP_THREADS + threadIdx.x;
     if (j >= j1) break;
-    const uint32_t lo = s_own[j - j0];
-    const uint64_t rc = s_rect[lo];
-    const uint32_t x0 = rc & 0xffff, x1 = (rc >> 16) & 0xffff, y0 = (rc >> 32) & 0xffff;
-    const uint32_t wdt = x1 - x0 + 1;
-    const uint32_t local = j - s_off[lo];
-    const uint32_t ty = y0 + local / wdt, tx = x0 + local % wdt;
-    w.pairs[0][j] = ((uint64_t)(ty * (uint32_t)tiles_x + tx) << 32) | s_m[lo];
+    w.pairs[0][j] = emit_pair(E, j, j0, tiles_x);
   }
 }
 
