@@ -265,7 +265,9 @@ def run_reference(args):
     from fixtures import scenes
     from oracle import oracle as O
     O.lib()
-    cfg = scenes.build(args.config)
+    # all host cores, whatever OMP_NUM_THREADS the launcher exported
+    O.set_threads(os.cpu_count() or 1)
+    cfg = scenes.build(args.config, threads=os.cpu_count() or 1)
     sweep = cfg.sweep(SWEEP_VIEWS)
     views = [v for blk in my_views(0, 1, args.warmup + args.steps, BLOCK) for v in blk[:1]]
     for v in views[:args.warmup]:
@@ -307,12 +309,23 @@ def run_lodge(args):
     from paper_2505_23158_b200.renderer import STATS_BYTES
 
     rank, world, local = env_rank()
+    # LODGE_BENCH_PLUMBING=1: every rank on cuda:0 over gloo -- a check that
+    # the torchrun path runs end to end on a one-GPU box (the ranks never
+    # wait on each other's kernels); its numbers are not scaling numbers
+    plumbing = os.environ.get("LODGE_BENCH_PLUMBING") == "1"
+    if plumbing:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if plumbing:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     t_setup = time.time()
-    cfg = scenes.build(args.config)
+    # the host cores shared by the ranks of this node (torchrun exports
+    # OMP_NUM_THREADS=1)
+    cfg = scenes.build(args.config, threads=max(1, (os.cpu_count() or 1) // world))
     store = None
     if args.residency == "stream":
         # residency-bounded store: chunk slabs streamed into args.slots slots
@@ -555,6 +568,7 @@ def run_lodge(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
         O.lib()
+        O.set_threads(os.cpu_count() or 1)
         v = schedule[args.warmup][0]
         cam = sweep[v]
         t0 = time.perf_counter()

@@ -54,6 +54,7 @@ def lib():
         L.synth_gather_level.argtypes = [P, P, C.c_int32, P, C.c_int64, C.c_float, P, P]
         L.synth_bands.argtypes = [P, C.c_int64, P, C.c_int32, P, P, P, P, P]
         L.synth_threads.restype = C.c_int32
+        L.synth_set_threads.argtypes = [C.c_int32]
         _lib = L
     return _lib
 
@@ -134,9 +135,12 @@ class Config:
         return sum(g.nbytes + s.nbytes for g, s, _ in self.levels)
 
 
-def build(name: str, seed: int = 7, verbose: bool = False) -> Config:
+def build(name: str, seed: int = 7, verbose: bool = False, threads: int = 0) -> Config:
+    """threads > 0: OpenMP threads of the generator (else the runtime's default)."""
     spec = CONFIGS[name]
     L = lib()
+    if threads > 0:
+        L.synth_set_threads(int(threads))
     t0 = time.time()
     deg = spec["degree"]
     terms = (deg + 1) ** 2

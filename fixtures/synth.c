@@ -220,6 +220,14 @@ void synth_bands(const float *geom, int64_t n, const double *centers, int32_t K,
   }
 }
 
+void synth_set_threads(int32_t n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 int32_t synth_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

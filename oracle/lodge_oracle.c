@@ -444,6 +444,16 @@ int64_t orc_rasterize(int64_t n_inputs, int64_t M, const int64_t *src, const dou
   return P;
 }
 
+/* Host threads of the OpenMP loops (the bench's CPU arm uses every core even
+   when a launcher such as torchrun exported OMP_NUM_THREADS=1). */
+void orc_set_threads(int32_t n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 int32_t orc_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

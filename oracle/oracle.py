@@ -64,6 +64,7 @@ def lib():
                                     C.c_int32, _D, _I64, _I64, _D, _I64, _I64, C.c_int64]
         L.orc_rasterize.restype = C.c_int64
         L.orc_num_threads.restype = C.c_int32
+        L.orc_set_threads.argtypes = [C.c_int32]
         L.orc_project_f32.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, _I64, C.c_int64, _D,
                                       C.POINTER(Camera), C.POINTER(RasterCfg), C.c_int32,
                                       _I64, _D, _D, _D, _D, _D, _D, _D, _I32]
@@ -78,6 +79,11 @@ def _p(a, t):
 
 def num_threads() -> int:
     return int(lib().orc_num_threads())
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of the oracle's parallel loops."""
+    lib().orc_set_threads(int(n))
 
 
 def camera_struct(R, pos, focal, pp, resolution, near) -> Camera:
