@@ -171,7 +171,9 @@ def stage_bytes(U, AB, M, P, W, H, sh_terms, geom_bytes=48, sh_elem=4):
         "select": 0.0,
         "union": 4.0 * AB + 5.0 * U,
         "project": U * (5.0 + geom_bytes) + M * (sh_b + 8 + 4 + 8 + 64 + 64),
-        "depth_sort": M * (8.0 + 8 * 24.0),
+        # 32-bit keys: histogram (8 B/input), first pass (u64 key + index in,
+        # u32 key + index out), three u32 key + index passes, tie scan
+        "depth_sort": U * (8.0 + 12.0) + M * 8.0 + 3 * M * 16.0 + M * 4.0,
         "tile_setup": 0.0,
         "duplicate": M * 12.0 + P * 8.0,
         # pass 1 reads u64 pairs, writes packed u32; pass 2 reads and writes u32

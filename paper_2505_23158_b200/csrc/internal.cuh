@@ -219,6 +219,8 @@ void launch_import_batch(const lodge_batch &b, int64_t M, const Work &w, FrameSt
                          int32_t exact, cudaStream_t s);
 void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
                        cudaStream_t s);
+void launch_depth_sort64(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
+                         cudaStream_t s);
 void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32_t tiles_x,
                        int32_t tiles_y, cudaStream_t s);
 void launch_duplicate(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_cap,

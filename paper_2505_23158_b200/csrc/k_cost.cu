@@ -115,7 +115,7 @@ void launch_cover_table(const Work &w, FrameState *fs, int64_t n_cap, double *di
                         int64_t *prefix, int32_t *launches, cudaStream_t s) {
   k_cover_nsort<<<1, 1, 0, s>>>(fs);
   ++*launches;
-  launch_depth_sort(w, fs, n_cap, launches, s);
+  launch_depth_sort64(w, fs, n_cap, launches, s);
   const unsigned nb = (unsigned)((n_cap + SC_TILE - 1) / SC_TILE);
   uint64_t *sums = w.rect;  // scratch: the rectangles are not used on this path
   k_cover_sums<<<nb, SC_THREADS, 0, s>>>(w.val_depth[0], fs, sums);

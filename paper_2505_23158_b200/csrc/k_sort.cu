@@ -1,9 +1,13 @@
 // K4: onesweep LSD radix sort (Adinets & Merrill 2022) for the two global
 // orderings of rasterize (reference src/raster.py:401 and :421-423):
 //   1. inputs by fp64 depth, stable over the concatenated input order, which
-//      is exactly np.lexsort((source_index, depth)) (the key is the IEEE bit
-//      pattern; z > near > 0 so it is monotone as an unsigned integer; culled
-//      inputs carry ~0 and sort last);
+//      is exactly np.lexsort((source_index, depth)).  Frames sort a 32-bit
+//      key -- the fp32 round-toward-zero bit pattern of the depth, monotone
+//      in it (z > near > 0) -- in four passes, then k_depth_ties re-orders
+//      each run of equal 32-bit keys by the full fp64 depth (and index):
+//      the result is the order of the fp64 keys.  Culled inputs carry ~0
+//      and leave the sort in its first pass.  The cost tables sort the full
+//      64-bit pattern in eight passes.
 //   2. duplicated (tile<<32 | splat) pairs by tile id only, stable, which is
 //      np.argsort(tile_ids, kind="stable") over pairs emitted in depth order.
 // One partition per CTA: keys in registers in warp-contiguous order, stable
@@ -100,6 +104,158 @@ __global__ void __launch_bounds__(OS_THREADS, VALS ? LODGE_OS_VMINB
                                          [&](uint32_t li) { return vin[base + li]; });
 }
 
+// ---- frame depth sort: 32-bit keys + tie repair ----------------------------
+// fp32 (round toward zero) bit pattern of a positive fp64 depth key: a
+// non-decreasing map, so sorting it leaves only ties of equal 32-bit keys
+// to resolve by the full key.  ~0 (culled) stays ~0 (a NaN pattern, never
+// produced by a positive depth).
+__device__ __forceinline__ uint32_t depth_key32(uint64_t k) {
+  return k == ~0ull ? ~0u
+                    : __float_as_uint(__double2float_rz(__longlong_as_double((long long)k)));
+}
+
+// One pass over 32-bit depth keys; FIRST reads the u64 keys the projection
+// wrote (at the concatenated input index), maps them and drops the culled.
+template <bool FIRST>
+__global__ void __launch_bounds__(OS_THREADS, LODGE_OS_VMINB)
+    k_depth_pass(const uint64_t *__restrict__ kin64, const uint32_t *__restrict__ kin32,
+                 uint32_t *__restrict__ kout, const uint32_t *__restrict__ vin,
+                 uint32_t *__restrict__ vout, const uint32_t *n_ptr, int shift,
+                 const uint32_t *__restrict__ digit_off, uint64_t *status, FrameState *fs,
+                 int tk) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int IT = LODGE_OS_ITEMS_D;
+  constexpr uint32_t TILE = OS_THREADS * IT;
+  using Smem = OSmem<IT, true, uint32_t, 256>;
+  Smem &S = *reinterpret_cast<Smem *>(smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) S.misc[0] = atomicAdd(&fs->tickets[tk], 1u);
+  __syncthreads();
+  const uint32_t part = S.misc[0];
+  const uint32_t n = *n_ptr;
+  const uint32_t base = part * TILE;
+  if (base >= n) return;
+  uint32_t k[IT];
+  uint32_t vmask = 0;
+#pragma unroll
+  for (int i = 0; i < IT; ++i) {
+    const uint32_t idx = base + warp * (IT * 32) + i * 32 + lane;
+    k[i] = idx < n ? (FIRST ? depth_key32(kin64[idx]) : kin32[idx]) : ~0u;
+    const bool valid = idx < n && !(FIRST && k[i] == ~0u);
+    vmask |= valid ? (1u << i) : 0u;
+  }
+  uint32_t cnt = min(TILE, n - base);
+  if (FIRST) {  // the partition's valid items, not its positional size
+    const uint32_t c = __reduce_add_sync(FULL_MASK, (uint32_t)__popc(vmask));
+    if (lane == 0) S.misc[2 + warp] = c;
+    __syncthreads();
+    cnt = 0;
+#pragma unroll
+    for (int w = 0; w < OS_THREADS / 32; ++w) cnt += S.misc[2 + w];
+  }
+  onesweep_partition<IT, 8, true>(S, k, vmask, part, cnt, shift, digit_off, status,
+                                  fs->epoch + tk, kout, [](uint32_t key) { return key; }, vout,
+                                  [&](uint32_t li) { return vin[base + li]; });
+}
+
+// Histograms of the four 8-bit digits of the 32-bit depth keys.
+__global__ void __launch_bounds__(256) k_depth_hist32(const uint64_t *__restrict__ keys,
+                                                     FrameState *fs) {
+  __shared__ uint32_t h[4][256];
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t n = fs->n_sort;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    if (k == ~0ull) continue;  // culled: dropped by the first pass
+    const uint32_t k32 = depth_key32(k);
+#pragma unroll
+    for (int p = 0; p < 4; ++p) atomicAdd(&h[p][(k32 >> (8 * p)) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) {
+    const uint32_t c = (&h[0][0])[i];
+    if (c) atomicAdd(&fs->hist_depth[0][0] + i, c);
+  }
+}
+
+// Tie repair after the 32-bit passes: every run of equal 32-bit keys is in
+// input order (the passes are stable); re-order it by (fp64 key, index).
+// Runs of up to TIE_SHORT members are sorted by the thread that owns the run
+// start; longer ones (only adversarial inputs: > 32 depths within one fp32
+// ulp) by the whole CTA through `scratch`, by rank counting.
+constexpr int TIE_SHORT = 32;
+constexpr int TIE_SEG = 4096;  // run starts examined per CTA step
+__global__ void __launch_bounds__(256) k_depth_ties(const uint32_t *__restrict__ k32,
+                                                    uint32_t *val,
+                                                    const uint64_t *__restrict__ full,
+                                                    uint32_t *scratch, FrameState *fs) {
+  __shared__ uint32_t s_long[TIE_SEG / (TIE_SHORT + 1) + 1];
+  __shared__ uint32_t s_nlong, s_end;
+  const uint32_t M = fs->stats.M;
+  const int tid = threadIdx.x;
+  for (uint32_t seg = blockIdx.x * TIE_SEG; seg < M; seg += gridDim.x * TIE_SEG) {
+    if (tid == 0) s_nlong = 0;
+    __syncthreads();
+    const uint32_t segend = min(seg + (uint32_t)TIE_SEG, M);
+    for (uint32_t i = seg + tid; i < segend; i += blockDim.x) {
+      const uint32_t k = k32[i];
+      if (i + 1 >= M || k32[i + 1] != k) continue;  // no tie follows
+      if (i > 0 && k32[i - 1] == k) continue;       // not a run start
+      uint32_t e = i + 2;
+      while (e < M && e - i <= (uint32_t)TIE_SHORT && k32[e] == k) ++e;
+      if (e - i > (uint32_t)TIE_SHORT) {
+        s_long[atomicAdd(&s_nlong, 1u)] = i;
+        continue;
+      }
+      const uint32_t n = e - i;
+      uint32_t g[TIE_SHORT];
+      uint64_t f[TIE_SHORT];
+      for (uint32_t j = 0; j < n; ++j) {  // insertion sort by (full key, index)
+        const uint32_t gj = val[i + j];
+        const uint64_t fj = full[gj];
+        uint32_t q = j;
+        while (q > 0 && (f[q - 1] > fj || (f[q - 1] == fj && g[q - 1] > gj))) {
+          f[q] = f[q - 1];
+          g[q] = g[q - 1];
+          --q;
+        }
+        f[q] = fj;
+        g[q] = gj;
+      }
+      for (uint32_t j = 0; j < n; ++j) val[i + j] = g[j];
+    }
+    __syncthreads();
+    const uint32_t nlong = s_nlong;
+    for (uint32_t r = 0; r < nlong; ++r) {
+      const uint32_t i0 = s_long[r];
+      const uint32_t k = k32[i0];
+      if (tid == 0) s_end = M;
+      __syncthreads();
+      for (uint32_t b = i0 + TIE_SHORT; b < M; b += blockDim.x) {  // run end
+        const uint32_t idx = b + tid;
+        if (idx < M && k32[idx] != k) atomicMin(&s_end, idx);
+        if (__syncthreads_or(s_end < M)) break;
+      }
+      const uint32_t n = s_end - i0;
+      for (uint32_t j = tid; j < n; j += blockDim.x) {
+        const uint32_t gj = val[i0 + j];
+        const uint64_t fj = full[gj];
+        uint32_t rank = 0;
+        for (uint32_t q = 0; q < n; ++q) {
+          const uint32_t gq = val[i0 + q];
+          const uint64_t fq = full[gq];
+          rank += (fq < fj || (fq == fj && gq < gj)) ? 1u : 0u;
+        }
+        scratch[i0 + rank] = gj;
+      }
+      __syncthreads();
+      for (uint32_t j = tid; j < n; j += blockDim.x) val[i0 + j] = scratch[i0 + j];
+      __syncthreads();
+    }
+  }
+}
+
 // Upfront histogram of all eight 8-bit digits of the depth keys.
 __global__ void __launch_bounds__(256) k_depth_hist(const uint64_t *__restrict__ keys,
                                                     FrameState *fs) {
@@ -167,8 +323,47 @@ static void os_launch_nb(int nb, A... args) {
   }
 }
 
+// Frames: four passes over 32-bit keys (u32 ping-pong in the two halves of
+// key_depth[1]; key_depth[0] keeps the full keys by input index for the tie
+// repair), sorted input indices in val_depth[0].
 void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
                        cudaStream_t s) {
+  if (M_cap <= 0) return;
+  int hist_blocks = (int)((M_cap + 1023) / 1024);
+  if (hist_blocks > 148 * 4) hist_blocks = 148 * 4;
+  k_depth_hist32<<<hist_blocks, 256, 0, s>>>(w.key_depth[0], fs);
+  k_depth_scan<<<1, 256, 0, s>>>(fs);
+  *launches += 2;
+  constexpr int64_t TILE = (int64_t)OS_THREADS * LODGE_OS_ITEMS_D;
+  const unsigned grid = (unsigned)((M_cap + TILE - 1) / TILE);
+  const size_t sm = sizeof(OSmem<LODGE_OS_ITEMS_D, true, uint32_t, 256>);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_depth_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_depth_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    attr = true;
+  }
+  uint32_t *k32[2] = {reinterpret_cast<uint32_t *>(w.key_depth[1]),
+                      reinterpret_cast<uint32_t *>(w.key_depth[1]) + M_cap};
+  // keys 0: u64 -> k32[0], 1: k32[0] -> k32[1], 2: k32[1] -> k32[0], 3: k32[0] -> k32[1]
+  k_depth_pass<true><<<grid, OS_THREADS, sm, s>>>(w.key_depth[0], nullptr, k32[0], w.val_depth[0],
+                                                  w.val_depth[1], &fs->n_sort, 0,
+                                                  fs->off_depth[0], w.status, fs, TK_DEPTH0);
+  for (int p = 1; p < 4; ++p) {
+    const int a = p & 1;  // values: [1] -> [0] -> [1] -> [0]
+    k_depth_pass<false><<<grid, OS_THREADS, sm, s>>>(
+        nullptr, k32[a ^ 1], k32[a], w.val_depth[a], w.val_depth[a ^ 1], &fs->stats.M, 8 * p,
+        fs->off_depth[p], w.status, fs, TK_DEPTH0 + p);
+  }
+  k_depth_ties<<<148 * 4, 256, 0, s>>>(k32[1], w.val_depth[0], w.key_depth[0], w.val_depth[1], fs);
+  *launches += 5;
+}
+
+// Cost tables: eight passes over the full 64-bit keys (the sorted keys are
+// read back in key_depth[0]).
+void launch_depth_sort64(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
+                         cudaStream_t s) {
   if (M_cap <= 0) return;
   int hist_blocks = (int)((M_cap + 1023) / 1024);
   if (hist_blocks > 148 * 4) hist_blocks = 148 * 4;
