@@ -59,6 +59,9 @@ def parse():
                     help="full: the whole store resident; stream: chunk slabs loaded "
                          "asynchronously into --slots device slots (SURVEY.md 8f rank 4)")
     ap.add_argument("--slots", type=int, default=3)
+    ap.add_argument("--phase-budget", type=int, default=1280,
+                    help="FAST frames: first-phase pairs per tile of the two depth phases "
+                         "(lodge_set_phase_budget); 0 = one pass over the full lists")
     ap.add_argument("--mode", default="blend", choices=["blend", "chunks", "lod", "full"],
                     help="render mode of the reference CLI (src/cli.py:219-243); the "
                          "metric is quoted on blend")
@@ -165,8 +168,16 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # algorithmic bytes per stage
 # ---------------------------------------------------------------------------
-def stage_bytes(U, AB, M, P, W, H, sh_terms, geom_bytes=48, sh_elem=4):
+def stage_bytes(U, AB, M, P, W, H, sh_terms, geom_bytes=48, sh_elem=4, P1=None, P2=0.0):
+    """Algorithmic bytes per frame of each stage.
+    Two-phase frames (P1 = pairs of the first depth phase < P): tile_setup is
+    the counting pass, duplicate / tile_sort / composite the first phase,
+    second_phase the enumeration, compaction, sort and compositing of the
+    P2 pairs the unfinished tiles still need."""
     sh_b = 3 * sh_terms * sh_elem
+    two = P1 is not None and (P1 < P or P2 > 0)
+    P1 = P if P1 is None else P1
+    count = M * (4.0 + 8.0 + 8.0 + 4.0)  # order + rect in, rect + offset out
     return {
         "select": 0.0,
         "union": 4.0 * AB + 5.0 * U,
@@ -174,11 +185,12 @@ def stage_bytes(U, AB, M, P, W, H, sh_terms, geom_bytes=48, sh_elem=4):
         # 32-bit keys: histogram (8 B/input), first pass (u64 key + index in,
         # u32 key + index out), three u32 key + index passes, tie scan
         "depth_sort": U * (8.0 + 12.0) + M * 8.0 + 3 * M * 16.0 + M * 4.0,
-        "tile_setup": 0.0,
-        "duplicate": M * 12.0 + P * 8.0,
+        "tile_setup": count if two else 0.0,
+        "duplicate": P1 * 8.0 if two else M * 12.0 + P * 8.0,
         # pass 1 reads u64 pairs, writes packed u32; pass 2 reads and writes u32
-        "tile_sort": (8.0 + 4.0 + 4.0 + 4.0) * P,
-        "composite": P * 4.0 + M * 64.0 + W * H * 16.0 + U * 4.0,
+        "tile_sort": (8.0 + 4.0 + 4.0 + 4.0) * P1,
+        "composite": P1 * 4.0 + M * 64.0 + W * H * 16.0 + U * 4.0,
+        "second_phase": (M * 8.0 + P2 * (8.0 + 20.0 + 4.0)) if two else 0.0,
     }
 
 
@@ -347,7 +359,7 @@ def run_lodge(args):
         plan = DevicePlan.from_arrays(cfg.centers, cfg.offsets, cfg.data, cfg.L, dev)
         store_gb = sum(l.nbytes() for l in levels) / 1e9
     r = LG.Renderer(levels, plan, device=dev, storage="fp32", precision=args.precision,
-                    n_streams=args.streams)
+                    n_streams=args.streams, phase_budget=args.phase_budget)
     B = args.views_per_step
     schedule = my_views(rank, world, args.warmup + args.steps, B)
     sweep = cfg.sweep(SWEEP_VIEWS)
@@ -459,6 +471,9 @@ def run_lodge(args):
                         "serially on one stream after the timed region")
     stats = read_stats(stats_all)
     overflow = sum(s.overflow for s in stats)
+    faults = sum(1 for s in stats if s.fault)
+    if faults:
+        print(f"[bench] {faults} frame(s) reported device bounds faults", file=sys.stderr)
     ms_max = ms
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -475,7 +490,9 @@ def run_lodge(args):
         return int(cfg.offsets[(j + 1) * cfg.L] - cfg.offsets[j * cfg.L]) if j >= 0 else 0
 
     AB = np.mean([set_total(s.f) + set_total(s.o) for s in stats])
-    sb = stage_bytes(U, AB, M, P, W, H, (cfg.degree + 1) ** 2)
+    P1 = np.mean([s.P_first for s in stats])
+    P2 = np.mean([s.P_second for s in stats])
+    sb = stage_bytes(U, AB, M, P, W, H, (cfg.degree + 1) ** 2, P1=P1, P2=P2)
     peak, peak_kind = load_peaks()
     stages = {}
     for i, name in enumerate(N.STAGES):
@@ -483,7 +500,7 @@ def run_lodge(args):
         gbs = sb[name] / (per / 1000.0) / 1e9 if per > 0 else 0.0
         stages[name] = {"ms_per_frame": round(per, 5), "bytes_per_frame": round(sb[name]),
                         "GB_s": round(gbs, 1), "frac": round(gbs / peak, 4)}
-    hbm_stages = ["union", "project", "depth_sort", "duplicate", "tile_sort"]
+    hbm_stages = ["union", "project", "depth_sort", "duplicate", "tile_sort", "second_phase"]
     dom = max(N.STAGES, key=lambda k: stages[k]["ms_per_frame"])
     dom_hbm = max(hbm_stages, key=lambda k: stages[k]["ms_per_frame"])
     rf_stage = dom if dom in hbm_stages else dom_hbm
@@ -603,6 +620,7 @@ def run_lodge(args):
                        "resolution": [W, H],
                        "views_per_step_per_gpu": B, "frames_timed": total_frames,
                        "precision": args.precision,
+                       "phase_budget": args.phase_budget if args.precision == "fast" else 0,
                        "store": ("fp32 records, replicated" if store is None else
                                  f"fp32 chunk slabs, {args.slots} resident slots, "
                                  f"{store.loads} loads ({store.bytes_loaded / 1e9:.1f} GB)"),
@@ -611,9 +629,11 @@ def run_lodge(args):
                              f"~{(sb['project'] + sb['tile_sort'] + sb['composite']) / 1e9:.1f} GB"
                              " >> 126 MB L2; no explicit flush",
                        "mean_U": round(U), "mean_M": round(M), "mean_P": round(P),
+                       "mean_P_sorted": [round(P1), round(P2)],
                        "levels": cfg.n_gaussians(), "chunks": cfg.K,
                        "pairs_per_s": P * value, "gaussians_per_s": U * value,
-                       "overflow_frames": int(overflow), "setup_s": round(setup_s, 1)},
+                       "overflow_frames": int(overflow), "fault_frames": int(faults),
+                       "setup_s": round(setup_s, 1)},
             "e2e": e2e, "gpu_launches": int(launches_per_frame * total_frames),
             "roofline": roofline, "stages": stages, "stage_timing": stage_timing,
             "cpu_baseline": cpu, "clocks": clk,

@@ -102,6 +102,11 @@ typedef struct {
  * max weights are max-ed into it on the device -- the max over views of
  * score_active_selection (src/lod.py:95-131) without a host round trip. */
 #define LODGE_ACCUMULATE_MAX 4
+/* Composite every tile's full sorted list in one pass, so the lists stay
+ * inspectable with lodge_frame_lists.  Without it FAST frames composite in
+ * two depth phases (lodge_set_phase_budget): identical outputs, but the
+ * lists left after the frame are only the second phase's. */
+#define LODGE_FULL_LISTS 8
 
 /* Device outputs of one frame (src/raster.py:119-127).  image is float
  * (FAST) or double (EXACT), (h, w, 3); tile_count (tiles_y*tiles_x) int32;
@@ -125,6 +130,10 @@ typedef struct {
   uint32_t P;            /* tile-splat pairs */
   uint32_t overflow;     /* 1 if P exceeded the pair capacity */
   uint32_t guard_hits;   /* FAST: pixel-splat decisions re-checked in fp64 */
+  uint32_t P_first;      /* pairs sorted in the first (or only) depth phase */
+  uint32_t P_second;     /* pairs sorted in the second phase (two-phase frames) */
+  uint32_t fault;        /* nonzero: a device-side bounds check fired (one bit per
+                            site, internal.cuh FAULT_*); the frame's outputs are invalid */
 } lodge_frame_stats;
 
 /* ---- context ---------------------------------------------------------- */
@@ -135,6 +144,12 @@ int lodge_set_stream(lodge_ctx *ctx, void *cuda_stream);
 /* Reserve workspace: survivors M and pairs P.  Grown automatically by the
  * synchronous entry points; the async frame path reports overflow. */
 int lodge_reserve(lodge_ctx *ctx, int64_t max_splats, int64_t max_pairs);
+/* Two-phase FAST frames: the depth-ordered splats whose pairs
+ * start within pairs_per_tile * T of the pair sequence are binned, sorted and
+ * composited first; only the tiles left with live pixels receive, sort and
+ * composite the rest of their pairs.  Outputs are bitwise those of one pass.
+ * 0 disables (every frame one pass); default 1280. */
+int lodge_set_phase_budget(lodge_ctx *ctx, int32_t pairs_per_tile);
 int lodge_set_precision(lodge_ctx *ctx, int32_t precision);
 
 /* ---- chunk selection: nearest_two_chunks + blend_factor ---------------
@@ -213,11 +228,13 @@ int lodge_frame_union(lodge_ctx *ctx, int32_t level, uint32_t *idx_dev, uint8_t 
 
 /* Stage profiling: when enabled, lodge_render_frame records CUDA events on
  * the context stream at the boundaries of its LODGE_N_STAGES stages (select,
- * union, project, depth sort, tile setup, duplicate, tile sort, composite)
+ * union, project, depth sort, tile setup, duplicate, tile sort, composite,
+ * second phase; two-phase frames count the counting pass under tile setup
+ * and the first phase's emission / sort / compositing under the next three)
  * for up to `max_frames` frames.  lodge_profile_read synchronises those
  * events and returns the summed milliseconds per stage and the frame count,
  * then clears the record. */
-#define LODGE_N_STAGES 8
+#define LODGE_N_STAGES 9
 int lodge_profile(lodge_ctx *ctx, int32_t enable, int32_t max_frames);
 int lodge_profile_read(lodge_ctx *ctx, double *stage_ms, int32_t *frames);
 

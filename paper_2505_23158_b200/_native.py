@@ -25,6 +25,7 @@ PREC_EXACT = 1
 NEED_IMAGE = 1
 RECORD_MAX = 2
 ACCUMULATE_MAX = 4
+FULL_LISTS = 8
 
 ERR = {-1: "BAD_ARG", -2: "CUDA", -3: "OOM", -4: "CAPACITY"}
 
@@ -64,7 +65,8 @@ class FrameOut(C.Structure):
 class FrameStats(C.Structure):
     _fields_ = [("f", C.c_int32), ("o", C.c_int32), ("t_bar", C.c_double), ("t", C.c_double),
                 ("U", C.c_uint32), ("U_level", C.c_uint32 * MAX_LEVELS), ("M", C.c_uint32),
-                ("P", C.c_uint32), ("overflow", C.c_uint32), ("guard_hits", C.c_uint32)]
+                ("P", C.c_uint32), ("overflow", C.c_uint32), ("guard_hits", C.c_uint32),
+                ("P_first", C.c_uint32), ("P_second", C.c_uint32), ("fault", C.c_uint32)]
 
 
 class Batch(C.Structure):
@@ -76,6 +78,7 @@ class Batch(C.Structure):
 
 EXPORTS = {
     "lodge_create": ([C.c_int32, C.POINTER(C.c_void_p)], C.c_int),
+    "lodge_set_phase_budget": ([C.c_void_p, C.c_int32], C.c_int),
     "lodge_destroy": ([C.c_void_p], None),
     "lodge_last_error": ([], C.c_char_p),
     "lodge_set_stream": ([C.c_void_p, C.c_void_p], C.c_int),
@@ -117,9 +120,9 @@ EXPORTS = {
     "lodge_asset_check_sets": ([C.c_void_p, C.POINTER(Chunks), C.POINTER(C.c_int64),
                                 C.POINTER(C.c_int32)], C.c_int),
 }
-N_STAGES = 8
+N_STAGES = 9
 STAGES = ("select", "union", "project", "depth_sort", "tile_setup", "duplicate", "tile_sort",
-          "composite")
+          "composite", "second_phase")
 
 _lib = None
 _lock = threading.Lock()

@@ -28,10 +28,14 @@ struct EmitSmem {
 template <int NP>
 __device__ __forceinline__ void emit_stage(EmitSmem<NP> &E, const uint32_t *__restrict__ order,
                                            const Work &w, uint32_t j0, uint32_t j1,
-                                           uint32_t r0, uint32_t r1) {
+                                           uint32_t r0, uint32_t r1, uint32_t *fault) {
   constexpr int IT = NP / DUP_THREADS;
   static_assert(NP % DUP_THREADS == 0, "whole pairs per thread");
-  const uint32_t nr = r1 - r0 + 1;
+  uint32_t nr = r1 - r0 + 1;
+  if (r1 < r0 || nr > (uint32_t)NP + 1u) {  // owners have >= 1 pair: nr <= pairs + 1
+    if (threadIdx.x == 0) raise_fault(fault, FAULT_OWNERS);
+    nr = 1;
+  }
   const uint32_t npair = j1 - j0;
   for (uint32_t k = threadIdx.x; k < NP; k += DUP_THREADS) E.own[k] = 0;
   for (uint32_t q = threadIdx.x; q < nr; q += DUP_THREADS) {
@@ -40,10 +44,13 @@ __device__ __forceinline__ void emit_stage(EmitSmem<NP> &E, const uint32_t *__re
     E.m[q] = order[r0 + q];
   }
   __syncthreads();
-  // owners have >= 1 pair, so their first pairs differ
+  // owners with >= 1 pair mark their first pairs, which differ (an owner
+  // without pairs -- a second-phase splat that meets no alive tile -- marks
+  // nothing)
   for (uint32_t q = threadIdx.x; q < nr; q += DUP_THREADS) {
+    const uint32_t next = (q + 1 < nr) ? E.off[q + 1] : w.splat_off[r0 + q + 1];
     const uint32_t st = E.off[q] > j0 ? E.off[q] - j0 : 0u;
-    if (st < npair) E.own[st] = (uint16_t)q;
+    if (st < npair && next > E.off[q]) E.own[st] = (uint16_t)q;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -23,6 +23,12 @@ struct FrameState {
   uint32_t hist_depth[8][256];        // onesweep digit histograms (depth keys)
   uint32_t off_depth[8][256];         // their exclusive scans
   uint32_t off_tile[2][256];          // digit offsets for the two tile passes
+  // two-phase frames: the depth-order splat split, and the
+  // second phase's tile count and pair total
+  uint32_t split_S;                   // splats [0, S) form the first phase
+  uint32_t P_A;                       // their pairs (a prefix of the pair sequence)
+  uint32_t n_alive;                   // tiles the second phase composites
+  uint32_t n_owners_b;                // second-phase splats that meet an alive tile
   unsigned long long counters[8];     // LODGE_COUNTERS builds: compositing work counters
 };
 
@@ -32,6 +38,9 @@ enum Ticket {
   TK_DEPTH0 = 2,   // .. TK_DEPTH0 + 7
   TK_TILE0 = 10,   // .. TK_TILE0 + 1
   TK_UNION0 = 12,  // .. TK_UNION0 + LODGE_MAX_LEVELS - 1
+  TK_DUPB = 20,    // second phase: enumeration scan
+  TK_EMITB = 21,   //               ordered pair compaction
+  TK_TILEB0 = 22,  //               tile passes (.. TK_TILEB0 + 1)
 };
 
 // Splat payload for compositing (64 B, one per survivor).  mean2d is kept in
@@ -74,11 +83,31 @@ struct Work {
   uint32_t *tile_order;     // T: tiles, heaviest first (composite schedule)
   int32_t *tile_diff;       // (tiles_x+1)*(tiles_y+1) 2-D difference array
   uint32_t *tile_start;     // T+1
+  // two-phase frames
+  int32_t *tile_diff_a;     // (tiles_x+1)*(tiles_y+1): first-phase splats only
+  uint32_t *count_all;      // T: pairs per tile over all splats
+  uint32_t *tile_start_b;   // T+1: second-phase list ranges
+  uint32_t *tile_order_b;   // T: second-phase tiles, heaviest first
+  uint32_t *alive;          // ceil(T/32) bitmap: tiles the second phase composites
+  uint32_t *sat;            // (tiles_y+1)*(tiles_x+1) summed-area table of alive tiles
+  float4 *state;            // W*H: (T, r, g, b) of pixels of alive tiles after phase one
   uint64_t *status;         // look-back status words (epoch | flags | value)
   uint32_t *union_idx;      // slots
   uint8_t *union_tag;       // slots
   int64_t M_cap, P_cap, status_cap, slot_cap;
 };
+
+// Device-side bounds checks: a violated invariant sets its bit in
+// stats.fault and the offending access is skipped (the frame is reported
+// invalid instead of faulting the context).
+enum : uint32_t {
+  FAULT_OWNERS = 1,   // an emission CTA's owner range exceeds its staging
+  FAULT_COMPACT = 2,  // second-phase compaction beyond the pair count
+  FAULT_SCATTER = 4,  // a onesweep scatter beyond the key count
+};
+__device__ __forceinline__ void raise_fault(uint32_t *fault, uint32_t bit) {
+  atomicOr(fault, bit);
+}
 
 // Status word: [63:32] epoch, [31:30] flag, [29:0] value.
 enum : uint32_t { ST_EMPTY = 0, ST_AGG = 1, ST_PREFIX = 2 };
@@ -173,6 +202,27 @@ __device__ __forceinline__ int64_t compact_slot(bool keep, uint64_t *status, uin
   return (int64_t)(*s_base) + s_warp[warp] + __popc(bal & lanemask_lt());
 }
 
+// Warp-aggregated atomic: lanes hitting the same counter combine first (the
+// corners of border-clipped splats are shared by many splats).  Called by
+// the whole warp; inactive lanes pass idx = -1.
+__device__ __forceinline__ void warp_add(int32_t *base, int32_t idx, int32_t v) {
+  const uint32_t peers = __match_any_sync(FULL_MASK, idx);
+  if (idx >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1)
+    atomicAdd(base + idx, v * __popc(peers));
+}
+
+// 2-D difference-array update for a tile rectangle (whole warp; valid flag).
+__device__ __forceinline__ void add_tile_diff(int32_t *diff, uint64_t rc, int32_t tiles_x,
+                                              bool valid) {
+  const int32_t x0 = (int32_t)(rc & 0xffff), x1 = (int32_t)((rc >> 16) & 0xffff);
+  const int32_t y0 = (int32_t)((rc >> 32) & 0xffff), y1 = (int32_t)(rc >> 48);
+  const int32_t stride = tiles_x + 1;
+  warp_add(diff, valid ? y0 * stride + x0 : -1, 1);
+  warp_add(diff, valid ? y0 * stride + x1 + 1 : -1, -1);
+  warp_add(diff, valid ? (y1 + 1) * stride + x0 : -1, -1);
+  warp_add(diff, valid ? (y1 + 1) * stride + x1 + 1 : -1, 1);
+}
+
 __host__ __device__ __forceinline__ uint32_t union_status_stride(uint32_t max_slots) {
   return (max_slots + 255u) / 256u + 1u;
 }
@@ -222,14 +272,26 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
 void launch_depth_sort64(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
                          cudaStream_t s);
 void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32_t tiles_x,
-                       int32_t tiles_y, cudaStream_t s);
+                       int32_t tiles_y, cudaStream_t s, bool two_phase = false);
+// two-phase frames: first-phase pair budget of the counting pass
+void launch_dup_count(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_cap,
+                      uint32_t budget, cudaStream_t s);
+void launch_dup_emit(const Work &w, FrameState *fs, int32_t tiles_x, cudaStream_t s,
+                     bool first_phase);
+void launch_setup_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
+                    cudaStream_t s);
+void launch_enum_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
+                   int64_t M_cap, cudaStream_t s);
 void launch_duplicate(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_cap,
                       cudaStream_t s);
 void launch_tile_sort(Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
-                      int32_t *launches, cudaStream_t s);
+                      int32_t *launches, cudaStream_t s, int tk0 = 10 /* TK_TILE0 */);
+// phase 0: one pass over the full lists; 1 / 2: the two depth phases of a
+// FAST frame (1 saves the state of unfinished tiles, 2 resumes them)
 void launch_composite(const Work &w, FrameState *fs, const lodge_camera *cam_dev, int32_t W,
                       int32_t H, const lodge_raster_params &rp, int32_t flags, int32_t exact,
-                      const lodge_frame_out &out, uint32_t n_inputs_cap, cudaStream_t s);
+                      const lodge_frame_out &out, uint32_t n_inputs_cap, cudaStream_t s,
+                      int phase = 0);
 void launch_export_lists(const Work &w, FrameState *fs, int32_t T, int64_t *tile_offsets,
                          int64_t *tile_src, int64_t cap, cudaStream_t s);
 void launch_asset_split(const float *blob, int64_t n, int32_t width, float *geom, float *sh,

@@ -12,52 +12,29 @@
 
 namespace lodge {
 
-// Single block.  diff: (ty+1) x (tx+1).  Produces tile_count (int32, may be
-// NULL), tile_start (T+1), the two tile-digit offset tables, P, n_pairs, and
-// re-zeroes diff for the next frame.
-__global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t tiles_x,
-                                                     int32_t tiles_y, int32_t *tile_count,
-                                                     uint32_t *tile_start, uint32_t *tile_order,
-                                                     FrameState *fs, int64_t P_cap) {
-  extern __shared__ int32_t sd[];  // (tx+1)*(ty+1)
-  __shared__ uint32_t h0[256], h1[256];
-  __shared__ uint32_t s_sum[1024];
-  __shared__ uint32_t s_bk[33];
+// Per-tile list layout from per-tile list counts (one block of 1024
+// threads): tile_start (T+1), the two onesweep tile-digit offset tables, the
+// heavy-first tile order (tiles with an empty list last; *s_nz = the
+// others).  Returns the list total in *s_tot.
+template <typename CountFn>
+__device__ __forceinline__ void lists_from_counts(CountFn count, int T, uint32_t *tile_start,
+                                                  uint32_t *tile_order, FrameState *fs,
+                                                  uint32_t *s_sum, uint32_t *h0, uint32_t *h1,
+                                                  uint32_t *s_bk, uint32_t *s_tot,
+                                                  uint32_t *s_nz) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int stride = tiles_x + 1;
-  const int nd = stride * (tiles_y + 1);
-  for (int i = tid; i < nd; i += nt) {
-    sd[i] = diff[i];
-    diff[i] = 0;
-  }
   for (int i = tid; i < 256; i += nt) h0[i] = h1[i] = 0;
+  if (tid < 33) s_bk[tid] = 0;
   __syncthreads();
-  for (int y = tid; y < tiles_y; y += nt) {  // prefix along x
-    int32_t run = 0;
-    for (int x = 0; x < tiles_x; ++x) {
-      run += sd[y * stride + x];
-      sd[y * stride + x] = run;
-    }
-  }
-  __syncthreads();
-  for (int x = tid; x < tiles_x; x += nt) {  // prefix along y
-    int32_t run = 0;
-    for (int y = 0; y < tiles_y; ++y) {
-      run += sd[y * stride + x];
-      sd[y * stride + x] = run;
-    }
-  }
-  __syncthreads();
-  const int T = tiles_x * tiles_y;
   const int per = (T + nt - 1) / nt;
   const int b = tid * per, e = min(T, b + per);
   uint32_t loc = 0;
   for (int t = b; t < e; ++t) {
-    const uint32_t c = (uint32_t)sd[(t / tiles_x) * stride + (t % tiles_x)];
+    const uint32_t c = count(t);
     loc += c;
-    if (tile_count) tile_count[t] = (int32_t)c;
     atomicAdd(&h0[t & 255], c);
     atomicAdd(&h1[(t >> 8) & 255], c);
+    atomicAdd(&s_bk[c ? 32 - __clz(c) : 0], 1u);
   }
   s_sum[tid] = loc;
   __syncthreads();
@@ -71,40 +48,28 @@ __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t tile
   uint32_t run = s_sum[tid] - loc;
   for (int t = b; t < e; ++t) {
     tile_start[t] = run;
-    run += (uint32_t)sd[(t / tiles_x) * stride + (t % tiles_x)];
+    run += count(t);
   }
   // composite schedule: tiles by descending log2(count) so the longest lists
   // start first (order affects scheduling only, never results)
-  if (tid < 33) s_bk[tid] = 0;
-  __syncthreads();
-  for (int t = b; t < e; ++t) {
-    const uint32_t c = (uint32_t)sd[(t / tiles_x) * stride + (t % tiles_x)];
-    atomicAdd(&s_bk[c ? 32 - __clz(c) : 0], 1u);
-  }
-  __syncthreads();
   if (tid == 0) {
     uint32_t acc = 0;
     for (int k = 32; k >= 0; --k) {
       const uint32_t v = s_bk[k];
       s_bk[k] = acc;
+      if (k == 0) *s_nz = acc;  // tiles with a non-empty list
       acc += v;
     }
   }
   __syncthreads();
+  if (tid == nt - 1) {
+    *s_tot = s_sum[nt - 1];
+    tile_start[T] = s_sum[nt - 1];
+  }
   for (int t = b; t < e; ++t) {
-    const uint32_t c = (uint32_t)sd[(t / tiles_x) * stride + (t % tiles_x)];
+    const uint32_t c = count(t);
     tile_order[atomicAdd(&s_bk[c ? 32 - __clz(c) : 0], 1u)] = (uint32_t)t;
   }
-  if (tid == nt - 1) {
-    const uint32_t P = s_sum[nt - 1];
-    tile_start[T] = P;
-    fs->stats.P = P;
-    fs->stats.overflow = (int64_t)P > P_cap ? 1u : 0u;
-    // on overflow nothing is duplicated or sorted (the digit offsets assume
-    // all P pairs); the host grows the buffers and renders the frame again
-    fs->n_pairs = (int64_t)P <= P_cap ? P : 0u;
-  }
-  __syncthreads();
   if (tid < 32) {  // digit offsets for the two onesweep passes over tile ids
     for (int p = 0; p < 2; ++p) {
       uint32_t *h = p ? h1 : h0;
@@ -121,58 +86,238 @@ __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t tile
       }
     }
   }
+  __syncthreads();
+}
+
+// 2-D prefix (in place) of an (ty+1) x (tx+1) difference array in shared
+// memory: entry (y, x) becomes the count of tile (y, x).
+__device__ __forceinline__ void integrate_diff(int32_t *sd, int32_t tiles_x, int32_t tiles_y) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int stride = tiles_x + 1;
+  for (int y = tid; y < tiles_y; y += nt) {  // prefix along x
+    int32_t run = 0;
+    for (int x = 0; x < tiles_x; ++x) {
+      run += sd[y * stride + x];
+      sd[y * stride + x] = run;
+    }
+  }
+  __syncthreads();
+  for (int x = tid; x < tiles_x; x += nt) {  // prefix along y
+    int32_t run = 0;
+    for (int y = 0; y < tiles_y; ++y) {
+      run += sd[y * stride + x];
+      sd[y * stride + x] = run;
+    }
+  }
+  __syncthreads();
+}
+
+// Single block.  diff: (ty+1) x (tx+1) over all survivors -> tile_count
+// (int32, may be NULL) = per_tile_count, P.  One-phase frames lay the lists
+// out from the same counts; two-phase frames (diff_a != NULL) from diff_a,
+// the first-phase splats, keeping the full counts in count_all.  Both
+// difference arrays are re-zeroed for the next frame; the alive bitmap is
+// cleared for the first phase's compositor.
+__global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t *diff_a,
+                                                     int32_t tiles_x, int32_t tiles_y,
+                                                     int32_t *tile_count, uint32_t *count_all,
+                                                     uint32_t *alive, uint32_t *tile_start,
+                                                     uint32_t *tile_order, FrameState *fs,
+                                                     int64_t P_cap) {
+  extern __shared__ int32_t sd[];  // (tx+1)*(ty+1), twice with diff_a
+  __shared__ uint32_t h0[256], h1[256];
+  __shared__ uint32_t s_sum[1024];
+  __shared__ uint32_t s_bk[33];
+  __shared__ uint32_t s_tot, s_all, s_nz;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int stride = tiles_x + 1;
+  const int nd = stride * (tiles_y + 1);
+  int32_t *sa = sd + nd;
+  for (int i = tid; i < nd; i += nt) {
+    sd[i] = diff[i];
+    diff[i] = 0;
+    if (diff_a) {
+      sa[i] = diff_a[i];
+      diff_a[i] = 0;
+    }
+  }
+  const int T = tiles_x * tiles_y;
+  if (alive)
+    for (int i = tid; i < (T + 31) / 32; i += nt) alive[i] = 0u;
+  if (tid == 0) s_all = 0;
+  __syncthreads();
+  integrate_diff(sd, tiles_x, tiles_y);
+  if (diff_a) integrate_diff(sa, tiles_x, tiles_y);
+  auto at = [&](const int32_t *a, int t) {
+    return (uint32_t)a[(t / tiles_x) * stride + (t % tiles_x)];
+  };
+  uint32_t all = 0;
+  for (int t = tid; t < T; t += nt) {
+    const uint32_t c = at(sd, t);
+    all += c;
+    if (tile_count) tile_count[t] = (int32_t)c;
+    if (count_all) count_all[t] = c;
+  }
+  atomicAdd(&s_all, all);
+  const int32_t *lc = diff_a ? sa : sd;
+  lists_from_counts([&](int t) { return at(lc, t); }, T, tile_start, tile_order, fs, s_sum, h0,
+                    h1, s_bk, &s_tot, &s_nz);
+  if (tid == 0) {
+    const uint32_t P = s_all;
+    fs->stats.P = P;
+    fs->stats.overflow = (int64_t)P > P_cap ? 1u : 0u;
+    // on overflow nothing is duplicated or sorted (the digit offsets assume
+    // all listed pairs); the host grows the buffers and renders the frame again
+    fs->n_pairs = (int64_t)P <= P_cap ? s_tot : 0u;
+    fs->stats.P_first = s_tot;
+  }
+}
+
+// Second phase of a two-phase frame (one block of 1024 threads): list
+// counts of the tiles the first phase left unfinished (alive bitmap, written
+// by k_composite<phase 1>) = their pairs not in the first phase; their list
+// layout and order (tiles without a second-phase list last, n_alive = the
+// others), and the summed-area table of the alive tiles the enumeration
+// pass queries per splat rectangle.
+__global__ void __launch_bounds__(1024) k_setup_b(const uint32_t *__restrict__ alive,
+                                                  const uint32_t *__restrict__ count_all,
+                                                  const uint32_t *__restrict__ start_a,
+                                                  int32_t tiles_x, int32_t tiles_y,
+                                                  uint32_t *tile_start, uint32_t *tile_order,
+                                                  uint32_t *sat, FrameState *fs) {
+  extern __shared__ int32_t ss[];  // (tx+1)*(ty+1) summed-area table
+  __shared__ uint32_t h0[256], h1[256];
+  __shared__ uint32_t s_sum[1024];
+  __shared__ uint32_t s_bk[33];
+  __shared__ uint32_t s_tot, s_nz;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int stride = tiles_x + 1;
+  const int nd = stride * (tiles_y + 1);
+  const int T = tiles_x * tiles_y;
+  auto live = [&](int t) { return (alive[t >> 5] >> (t & 31)) & 1u; };
+  auto cnt = [&](int t) {
+    return live(t) ? count_all[t] - (start_a[t + 1] - start_a[t]) : 0u;
+  };
+  // sat[(y+1)*stride + (x+1)] = alive(y, x), row 0 / column 0 zero, then a
+  // 2-D prefix over the whole table
+  for (int i = tid; i < nd; i += nt) {
+    const int y = i / stride, x = i % stride;
+    ss[i] = (y > 0 && x > 0) ? (int32_t)live((y - 1) * tiles_x + (x - 1)) : 0;
+  }
+  __syncthreads();
+  for (int y = tid; y <= tiles_y; y += nt) {
+    int32_t run = 0;
+    for (int x = 0; x <= tiles_x; ++x) {
+      run += ss[y * stride + x];
+      ss[y * stride + x] = run;
+    }
+  }
+  __syncthreads();
+  for (int x = tid; x <= tiles_x; x += nt) {
+    int32_t run = 0;
+    for (int y = 0; y <= tiles_y; ++y) {
+      run += ss[y * stride + x];
+      ss[y * stride + x] = run;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < nd; i += nt) sat[i] = (uint32_t)ss[i];
+  lists_from_counts(cnt, T, tile_start, tile_order, fs, s_sum, h0, h1, s_bk, &s_tot, &s_nz);
+  if (tid == 0) {
+    fs->n_alive = s_nz;
+    fs->n_pairs = fs->stats.overflow ? 0u : s_tot;
+    fs->stats.P_second = s_tot;
+  }
 }
 
 constexpr int EMIT_ITEMS = EMIT_CHUNK / DUP_THREADS;
 constexpr int COUNT_ITEMS = 8;                        // splats per thread in k_dup_count
 
+// Any alive tile in the rectangle (summed-area table of k_setup_b)?
+__device__ __forceinline__ bool rect_alive(const uint32_t *__restrict__ sat, uint64_t rc,
+                                           int32_t tiles_x) {
+  const uint32_t x0 = rc & 0xffff, x1 = (rc >> 16) & 0xffff, y0 = (rc >> 32) & 0xffff,
+                 y1 = rc >> 48;
+  const uint32_t st = tiles_x + 1;
+  return sat[(y1 + 1) * st + x1 + 1] - sat[y0 * st + x1 + 1] - sat[(y1 + 1) * st + x0] +
+             sat[y0 * st + x0] != 0u;
+}
+
 // Pass 1, one thread per depth-sorted splat: tile count, exclusive scan of
 // the counts in depth order (single-pass look-back), the splat's rectangle
 // and id in depth order, and for every EMIT_CHUNK boundary inside the
 // splat's pair range the splat that owns it (the emission CTAs' splitters).
+// Two-phase frames: budget > 0 makes the splats whose pairs start before it
+// the first phase (their rectangles go to the tile_diff_a difference array;
+// split_S and P_A record the split).  SECOND: the enumeration of the second
+// phase over splats [split_S, M) -- only the splats that meet an alive tile,
+// compacted in depth order (a second look-back) into the owner list the
+// emission reads: rectangles in w.rect, ids in w.val_depth[1] (both dead by
+// then), pair offsets and splitters over that list.
+template <bool SECOND>
 __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__restrict__ order,
                                                            const uint64_t *__restrict__ rect,
-                                                           Work w, FrameState *fs) {
+                                                           Work w, FrameState *fs,
+                                                           uint32_t budget, int32_t tiles_x,
+                                                           uint32_t chunk_cap) {
   constexpr int IT = COUNT_ITEMS;  // consecutive depth-order splats per thread
-  __shared__ uint32_t s_w[DUP_THREADS / 32];
-  __shared__ uint32_t s_part, s_base;
+  constexpr int TK = SECOND ? TK_DUPB : TK_DUP;
+  __shared__ uint32_t s_w[DUP_THREADS / 32], s_z[DUP_THREADS / 32];
+  __shared__ uint32_t s_part, s_base, s_zbase;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_part = atomicAdd(&fs->tickets[TK_DUP], 1u);
+  if (tid == 0) s_part = atomicAdd(&fs->tickets[TK], 1u);
   __syncthreads();
   const uint32_t part = s_part;
-  const uint32_t M = fs->stats.overflow ? 0u : fs->stats.M;
+  const uint32_t S = SECOND ? fs->split_S : 0u;
+  const uint32_t M = fs->stats.overflow ? S : fs->stats.M;
+  const uint32_t n = M - S;
   const uint32_t r0 = part * (DUP_THREADS * IT) + tid * IT;
-  if (part * (DUP_THREADS * IT) >= M) return;
-  uint32_t m[IT], c[IT];
+  if (part * (DUP_THREADS * IT) >= n) return;
+  uint32_t c[IT];
   uint64_t rc[IT];
-  if (r0 + IT <= M) {  // order is 16-byte aligned and r0 a multiple of IT
+  if (SECOND) {
 #pragma unroll
-    for (int q = 0; q < IT / 4; ++q) {
-      const uint4 o4 = *reinterpret_cast<const uint4 *>(order + r0 + 4 * q);
-      m[4 * q] = o4.x; m[4 * q + 1] = o4.y; m[4 * q + 2] = o4.z; m[4 * q + 3] = o4.w;
-    }
+    for (int i = 0; i < IT; ++i) rc[i] = (r0 + i < n) ? w.rect_sorted[S + r0 + i] : 0ull;
   } else {
+    uint32_t m[IT];
+    if (r0 + IT <= n) {  // order is 16-byte aligned and r0 a multiple of IT
 #pragma unroll
-    for (int i = 0; i < IT; ++i) m[i] = (r0 + i < M) ? order[r0 + i] : 0u;
+      for (int q = 0; q < IT / 4; ++q) {
+        const uint4 o4 = *reinterpret_cast<const uint4 *>(order + r0 + 4 * q);
+        m[4 * q] = o4.x; m[4 * q + 1] = o4.y; m[4 * q + 2] = o4.z; m[4 * q + 3] = o4.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < IT; ++i) m[i] = (r0 + i < n) ? order[r0 + i] : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < IT; ++i) rc[i] = (r0 + i < n) ? rect[m[i]] : 0ull;
   }
-  uint32_t cnt = 0;
-#pragma unroll
-  for (int i = 0; i < IT; ++i) rc[i] = (r0 + i < M) ? rect[m[i]] : 0ull;
+  uint32_t cnt = 0, nz = 0;
 #pragma unroll
   for (int i = 0; i < IT; ++i) {
     const uint32_t x0 = rc[i] & 0xffff, x1 = (rc[i] >> 16) & 0xffff, y0 = (rc[i] >> 32) & 0xffff,
                    y1 = rc[i] >> 48;
-    c[i] = (r0 + i < M) ? (x1 - x0 + 1) * (y1 - y0 + 1) : 0u;
+    c[i] = (r0 + i < n) ? (x1 - x0 + 1) * (y1 - y0 + 1) : 0u;
+    if (SECOND && c[i] && !rect_alive(w.sat, rc[i], tiles_x)) c[i] = 0u;
     cnt += c[i];
-    if (r0 + i < M) w.rect_sorted[r0 + i] = rc[i];
+    nz += c[i] ? 1u : 0u;
+    if (!SECOND && r0 + i < n) w.rect_sorted[r0 + i] = rc[i];
   }
-  uint32_t inc = cnt;
+  uint32_t inc = cnt, zinc = nz;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
     if (lane >= o) inc += t;
+    if (SECOND) {
+      const uint32_t tz = __shfl_up_sync(FULL_MASK, zinc, o);
+      if (lane >= o) zinc += tz;
+    }
   }
-  if (lane == 31) s_w[warp] = inc;
+  if (lane == 31) {
+    s_w[warp] = inc;
+    s_z[warp] = zinc;
+  }
   __syncthreads();
   if (warp == 0) {
     const uint32_t wv = lane < DUP_THREADS / 32 ? s_w[lane] : 0u;
@@ -184,21 +329,58 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
     }
     const uint32_t total = __shfl_sync(FULL_MASK, winc, 31);
     if (lane < DUP_THREADS / 32) s_w[lane] = winc - wv;
-    const uint32_t pre = lookback_warp(w.status, part, total, fs->epoch + TK_DUP);
+    const uint32_t pre = lookback_warp(w.status, part, total, fs->epoch + TK);
     if (lane == 0) s_base = pre;
+  } else if (SECOND && warp == 1) {  // the owner compaction's look-back
+    const uint32_t zv = lane < DUP_THREADS / 32 ? s_z[lane] : 0u;
+    uint32_t zi = zv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(FULL_MASK, zi, o);
+      if (lane >= o) zi += t;
+    }
+    const uint32_t total = __shfl_sync(FULL_MASK, zi, 31);
+    if (lane < DUP_THREADS / 32) s_z[lane] = zi - zv;
+    const uint32_t pre =
+        lookback_warp(w.status + (w.status_cap >> 1), part, total, fs->epoch + TK);
+    if (lane == 0) s_zbase = pre;
   }
   __syncthreads();
-  if (r0 >= M) return;
   uint32_t off = s_base + s_w[warp] + inc - cnt;
+  uint32_t k = SECOND ? s_zbase + s_z[warp] + zinc - nz : 0u;  // owner index
 #pragma unroll
   for (int i = 0; i < IT; ++i) {
     const uint32_t r = r0 + i;
-    if (r < M) {
-      w.splat_off[r] = off;
-      if (r == M - 1) w.splat_off[M] = off + c[i];
-      for (uint32_t k = (off + EMIT_CHUNK - 1) / EMIT_CHUNK; k * EMIT_CHUNK < off + c[i]; ++k)
-        w.chunk_first[k] = r;
+    const bool valid = r < n;
+    // first phase: every splat owns its pairs; second: the splats with pairs
+    const bool own = valid && (!SECOND || c[i] > 0);
+    const uint32_t q = SECOND ? k : r;
+    if (own) {
+      w.splat_off[q] = off;
+      if (SECOND) {
+        w.rect[q] = rc[i];
+        w.val_depth[1][q] = order[S + r];
+      }
+      for (uint32_t kk = (off + EMIT_CHUNK - 1) / EMIT_CHUNK;
+           kk * EMIT_CHUNK < off + c[i] && kk < chunk_cap; ++kk)
+        w.chunk_first[kk] = q;
+    }
+    if (valid && r == n - 1) {  // totals: owners and pairs
+      const uint32_t nq = SECOND ? k + (c[i] ? 1u : 0u) : n;
+      w.splat_off[nq] = off + c[i];
+      if (SECOND) fs->n_owners_b = nq;
+    }
+    if (!SECOND && budget) {  // whole warp: the difference-array update is collective
+      const bool first = valid && off < budget;
+      add_tile_diff(w.tile_diff_a, rc[i], tiles_x, first);
+      if (first && (off + c[i] >= budget || r == n - 1)) {
+        fs->split_S = r + 1;
+        fs->P_A = off + c[i];
+      }
+    }
+    if (valid) {
       off += c[i];
+      if (SECOND && c[i]) ++k;
     }
   }
 }
@@ -206,17 +388,19 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
 // Pass 2, EMIT_CHUNK pairs per CTA regardless of splat sizes (emit.cuh),
 // written (tile << 32 | splat) coalesced, in depth order (the tile passes in
 // k_sort.cu then sort them stably by tile).
+// first_phase: the pairs [0, P_A) of a two-phase frame, owned by the
+// splats [0, split_S).
 __global__ void __launch_bounds__(DUP_THREADS) k_dup_emit(const uint32_t *__restrict__ order,
                                                           int32_t tiles_x, Work w,
-                                                          FrameState *fs) {
+                                                          FrameState *fs, int32_t first_phase) {
   __shared__ EmitSmem<EMIT_CHUNK> E;
   const uint32_t P = fs->n_pairs;
   const uint32_t j0 = blockIdx.x * EMIT_CHUNK;
   if (j0 >= P) return;
   const uint32_t j1 = min(j0 + (uint32_t)EMIT_CHUNK, P);
   uint32_t r0, r1;
-  emit_owners(w, j0, j1, P, fs->stats.M, r0, r1);
-  emit_stage(E, order, w, j0, j1, r0, r1);
+  emit_owners(w, j0, j1, P, first_phase ? fs->split_S : fs->stats.M, r0, r1);
+  emit_stage(E, order, w, j0, j1, r0, r1, &fs->stats.fault);
 #pragma unroll
   for (int it = 0; it < EMIT_ITEMS; ++it) {
     const uint32_t j = j0 + it * DUP_THREADS + threadIdx.x;
@@ -225,26 +409,137 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_emit(const uint32_t *__rest
   }
 }
 
+// Second phase of a two-phase frame: the enumerated pairs of the owner list
+// of k_dup_count<true> (EMIT_CHUNK per CTA, as k_dup_emit), keeping those whose tile
+// is alive, compacted in order (block scan + decoupled look-back over CTAs
+// taken in ticket order), so each alive tile receives, in depth order, its
+// pairs beyond the first phase.
+__global__ void __launch_bounds__(DUP_THREADS) k_emit_b(const uint32_t *__restrict__ order,
+                                                        int32_t tiles_x, int32_t n_tiles,
+                                                        Work w, FrameState *fs) {
+  __shared__ EmitSmem<EMIT_CHUNK> E;
+  __shared__ uint32_t s_alive[2048];  // T <= 65536 (check_tile_smem)
+  __shared__ uint32_t s_cnt[EMIT_ITEMS][DUP_THREADS / 32];
+  __shared__ uint32_t s_part, s_base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_part = atomicAdd(&fs->tickets[TK_EMITB], 1u);
+  __syncthreads();
+  const uint32_t part = s_part;
+  const uint32_t n = fs->stats.overflow ? 0u : fs->n_owners_b;
+  const uint32_t Pe = n ? w.splat_off[n] : 0u;  // enumerated pairs
+  const uint32_t j0 = part * EMIT_CHUNK;
+  if (j0 >= Pe) return;
+  const uint32_t j1 = min(j0 + (uint32_t)EMIT_CHUNK, Pe);
+  for (int i = tid; i < (n_tiles + 31) / 32; i += DUP_THREADS) s_alive[i] = w.alive[i];
+  uint32_t r0, r1;
+  emit_owners(w, j0, j1, Pe, n, r0, r1);
+  Work wb = w;  // the compacted owner list of k_dup_count<true>
+  wb.rect_sorted = w.rect;
+  emit_stage(E, w.val_depth[1], wb, j0, j1, r0, r1, &fs->stats.fault);  // ends with a barrier
+  uint64_t key[EMIT_ITEMS];
+  uint32_t keep = 0;
+#pragma unroll
+  for (int it = 0; it < EMIT_ITEMS; ++it) {
+    const uint32_t j = j0 + it * DUP_THREADS + tid;
+    key[it] = j < j1 ? emit_pair(E, j, j0, tiles_x) : 0ull;
+    const uint32_t t = (uint32_t)(key[it] >> 32);
+    const bool k = j < j1 && ((s_alive[t >> 5] >> (t & 31)) & 1u);
+    keep |= k ? (1u << it) : 0u;
+    const uint32_t bal = __ballot_sync(FULL_MASK, k);
+    if (lane == 0) s_cnt[it][warp] = __popc(bal);
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive offsets over (round, warp), then the look-back
+    uint32_t v[EMIT_ITEMS], tot = 0;
+#pragma unroll
+    for (int it = 0; it < EMIT_ITEMS; ++it) {
+      v[it] = lane < DUP_THREADS / 32 ? s_cnt[it][lane] : 0u;
+      uint32_t inc = v[it];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
+        if (lane >= o) inc += t;
+      }
+      if (lane < DUP_THREADS / 32) s_cnt[it][lane] = tot + inc - v[it];
+      tot += __shfl_sync(FULL_MASK, inc, 31);
+    }
+    const uint32_t pre = lookback_warp(w.status, part, tot, fs->epoch + TK_EMITB);
+    if (lane == 0) s_base = pre;
+  }
+  __syncthreads();
+  const uint32_t base = s_base;
+  const uint32_t limit = fs->n_pairs;  // the second phase's pair total (k_setup_b)
+#pragma unroll
+  for (int it = 0; it < EMIT_ITEMS; ++it) {
+    const uint32_t bal = __ballot_sync(FULL_MASK, (keep >> it) & 1u);
+    if ((keep >> it) & 1u) {
+      const uint32_t o = base + s_cnt[it][warp] + __popc(bal & lanemask_lt());
+      if (o < limit) w.pairs[0][o] = key[it];
+      else raise_fault(&fs->stats.fault, FAULT_COMPACT);
+    }
+  }
+}
+
 void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32_t tiles_x,
-                       int32_t tiles_y, cudaStream_t s) {
-  const size_t sm = (size_t)(tiles_x + 1) * (tiles_y + 1) * 4;
+                       int32_t tiles_y, cudaStream_t s, bool two_phase) {
+  const size_t nd = (size_t)(tiles_x + 1) * (tiles_y + 1) * 4;
+  const size_t sm = two_phase ? 2 * nd : nd;
   static size_t attr = 0;
   if (sm > 48 * 1024 && sm > attr) {
     cudaFuncSetAttribute(k_tile_setup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = sm;
   }
-  k_tile_setup<<<1, 1024, sm, s>>>(w.tile_diff, tiles_x, tiles_y, tile_count, w.tile_start,
-                                   w.tile_order, fs, w.P_cap);
+  k_tile_setup<<<1, 1024, sm, s>>>(w.tile_diff, two_phase ? w.tile_diff_a : nullptr, tiles_x,
+                                   tiles_y, tile_count, two_phase ? w.count_all : nullptr,
+                                   two_phase ? w.alive : nullptr, w.tile_start, w.tile_order, fs,
+                                   w.P_cap);
+}
+
+static uint32_t chunk_cap(const Work &w) { return (uint32_t)(w.P_cap / EMIT_CHUNK + 4); }
+
+void launch_dup_count(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_cap,
+                      uint32_t budget, cudaStream_t s) {
+  if (M_cap <= 0) return;
+  const unsigned grid =
+      (unsigned)((M_cap + DUP_THREADS * COUNT_ITEMS - 1) / (DUP_THREADS * COUNT_ITEMS));
+  k_dup_count<false><<<grid, DUP_THREADS, 0, s>>>(w.val_depth[0], w.rect, w, fs, budget, tiles_x,
+                                                  chunk_cap(w));
+}
+
+void launch_dup_emit(const Work &w, FrameState *fs, int32_t tiles_x, cudaStream_t s,
+                     bool first_phase) {
+  const unsigned egrid = (unsigned)((w.P_cap + EMIT_CHUNK - 1) / EMIT_CHUNK);
+  k_dup_emit<<<egrid, DUP_THREADS, 0, s>>>(w.val_depth[0], tiles_x, w, fs, first_phase ? 1 : 0);
 }
 
 void launch_duplicate(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_cap,
                       cudaStream_t s) {
   if (M_cap <= 0) return;
+  launch_dup_count(w, fs, tiles_x, M_cap, 0u, s);
+  launch_dup_emit(w, fs, tiles_x, s, false);
+}
+
+void launch_setup_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
+                    cudaStream_t s) {
+  const size_t sm = (size_t)(tiles_x + 1) * (tiles_y + 1) * 4;
+  static size_t attr = 0;
+  if (sm > 48 * 1024 && sm > attr) {
+    cudaFuncSetAttribute(k_setup_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = sm;
+  }
+  k_setup_b<<<1, 1024, sm, s>>>(w.alive, w.count_all, w.tile_start, tiles_x, tiles_y,
+                                w.tile_start_b, w.tile_order_b, w.sat, fs);
+}
+
+void launch_enum_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
+                   int64_t M_cap, cudaStream_t s) {
+  if (M_cap <= 0) return;
   const unsigned grid =
       (unsigned)((M_cap + DUP_THREADS * COUNT_ITEMS - 1) / (DUP_THREADS * COUNT_ITEMS));
-  k_dup_count<<<grid, DUP_THREADS, 0, s>>>(w.val_depth[0], w.rect, w, fs);
+  k_dup_count<true><<<grid, DUP_THREADS, 0, s>>>(w.val_depth[0], w.rect, w, fs, 0u, tiles_x,
+                                                 chunk_cap(w));
   const unsigned egrid = (unsigned)((w.P_cap + EMIT_CHUNK - 1) / EMIT_CHUNK);
-  k_dup_emit<<<egrid, DUP_THREADS, 0, s>>>(w.val_depth[0], tiles_x, w, fs);
+  k_emit_b<<<egrid, DUP_THREADS, 0, s>>>(w.val_depth[0], tiles_x, tiles_x * tiles_y, w, fs);
 }
 
 }  // namespace lodge

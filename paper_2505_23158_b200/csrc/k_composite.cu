@@ -141,12 +141,23 @@ struct CompParams {
   lodge_raster_params rp;
   float tmin_f, clamp_f;
   int32_t flags, tiles_x, W, H;
+  // two-phase frames
+  const uint32_t *count_all;  // pairs per tile over all splats
+  uint32_t *alive;            // bitmap of tiles the second phase resumes
+  float4 *state;              // (T, r, g, b) per pixel of those tiles
 };
 
 // MODE < 0: need_image / record_max from cpar.flags at run time (EXACT);
 // otherwise bit 0 = image, bit 1 = max weights, fixed at compile time (FAST:
 // no per-member branches on either)
-template <bool EXACT, int MODE>
+// PH (FAST only): 0 one pass over the full lists; 1 the first depth phase of
+// a two-phase frame -- a tile that still has live pixels and pairs beyond
+// the phase saves (T, colour) per pixel and its visible counts and sets its
+// alive bit instead of writing its image; 2 the second phase -- alive tiles
+// only (tile_order lists them first, fs->n_alive of them), resumed from the
+// saved state.  The per-pixel blend sequence is the one-pass sequence split
+// at a member boundary, so the outputs are bitwise those of one pass.
+template <bool EXACT, int MODE, int PH = 0>
 #ifndef LODGE_COMP_MINB
 #define LODGE_COMP_MINB 9  // FAST: resident CTAs per SM (register cap; 9 x 64 threads)
 #endif
@@ -165,6 +176,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
   const lodge_raster_params &rp = cpar.rp;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (PH == 2 && blockIdx.x >= fs->n_alive) return;
   const uint32_t t = tile_order ? tile_order[blockIdx.x] : blockIdx.x;
   const int tx = t % cpar.tiles_x, ty = t / cpar.tiles_x;
   const int lx = lane & 15, ly0 = warp * ROWS + (lane >> 4);  // pixel p at row ly0 + 2p
@@ -232,8 +244,19 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
   // FAST tracks liveness in T itself (T >= t_min); out-of-image pixels never live
   if (!EXACT) {
 #pragma unroll
-    for (int p = 0; p < PX; ++p)
-      if (!((alive >> p) & 1u)) T[p] = -INFINITY;
+    for (int p = 0; p < PX; ++p) {
+      if (!((alive >> p) & 1u)) {
+        T[p] = -INFINITY;
+      } else if (PH == 2) {  // resume the first phase's state
+        const size_t pix = (size_t)(py0 + 2 * p) * cpar.W + px;
+        const float4 st = cpar.state[pix];
+        T[p] = st.x;
+        cr[p] = st.y;
+        cg[p] = st.z;
+        cb[p] = st.w;
+        vis[p] = visible[pix];
+      }
+    }
   }
   auto live_any = [&]() -> bool {
     if (EXACT) return alive != 0u;
@@ -585,12 +608,21 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
     if (c_batch > 16) atomicAdd(&fs->counters[6], 1ull);
   }
 #endif
+  bool resume = false;  // PH 1: the second phase continues this tile
+  if (PH == 1) {
+    resume = __syncthreads_count(live_any()) > 0 && cpar.count_all[t] > e - s;
+    if (resume && tid == 0) atomicOr(&cpar.alive[t >> 5], 1u << (t & 31));
+  }
 #pragma unroll
   for (int p = 0; p < PX; ++p) {
     const int py = py0 + 2 * p;
     if (!(px < cpar.W && py < cpar.H)) continue;
     const size_t pix = (size_t)py * cpar.W + px;
     if (visible) visible[pix] = vis[p];
+    if (PH == 1 && resume) {
+      cpar.state[pix] = make_float4(T[p], cr[p], cg[p], cb[p]);
+      continue;
+    }
     if (!(need_image && image)) continue;
     if (EXACT) {
       const int pe = EXACT ? p : 0;
@@ -609,7 +641,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
   }
 }
 
-template <bool EXACT, int MODE>
+template <bool EXACT, int MODE, int PH = 0>
 static void launch_comp(const Work &w, FrameState *fs, int32_t W, int32_t H,
                         const lodge_raster_params &rp, int32_t flags, const lodge_frame_out &out,
                         cudaStream_t s) {
@@ -618,8 +650,8 @@ static void launch_comp(const Work &w, FrameState *fs, int32_t W, int32_t H,
   const size_t sm = sizeof(CompSmem<EXACT>);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_composite<EXACT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
+    cudaFuncSetAttribute(k_composite<EXACT, MODE, PH>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
   CompParams cp;
@@ -630,15 +662,28 @@ static void launch_comp(const Work &w, FrameState *fs, int32_t W, int32_t H,
   cp.tiles_x = tiles_x;
   cp.W = W;
   cp.H = H;
-  k_composite<EXACT, MODE><<<T, CC<EXACT>::CT, sm, s>>>(w.list, w.tile_start, w.tile_order,
-                                                         w.payload, w.precise, fs, cp,
-                                                         out.image_dev, out.visible_dev,
-                                                         out.maxw_dev);
+  cp.count_all = w.count_all;
+  cp.alive = w.alive;
+  cp.state = w.state;
+  k_composite<EXACT, MODE, PH><<<T, CC<EXACT>::CT, sm, s>>>(
+      w.list, PH == 2 ? w.tile_start_b : w.tile_start, PH == 2 ? w.tile_order_b : w.tile_order,
+      w.payload, w.precise, fs, cp, out.image_dev, out.visible_dev, out.maxw_dev);
+}
+
+template <int MODE>
+static void launch_fast(const Work &w, FrameState *fs, int32_t W, int32_t H,
+                        const lodge_raster_params &rp, int32_t flags, const lodge_frame_out &out,
+                        cudaStream_t s, int phase) {
+  switch (phase) {
+    case 1: launch_comp<false, MODE, 1>(w, fs, W, H, rp, flags, out, s); break;
+    case 2: launch_comp<false, MODE, 2>(w, fs, W, H, rp, flags, out, s); break;
+    default: launch_comp<false, MODE, 0>(w, fs, W, H, rp, flags, out, s); break;
+  }
 }
 
 void launch_composite(const Work &w, FrameState *fs, const lodge_camera *, int32_t W, int32_t H,
                       const lodge_raster_params &rp, int32_t flags, int32_t exact,
-                      const lodge_frame_out &out, uint32_t, cudaStream_t s) {
+                      const lodge_frame_out &out, uint32_t, cudaStream_t s, int phase) {
   if (exact) {
     launch_comp<true, -1>(w, fs, W, H, rp, flags, out, s);
     return;
@@ -646,10 +691,10 @@ void launch_composite(const Work &w, FrameState *fs, const lodge_camera *, int32
   const int mode = ((flags & LODGE_NEED_IMAGE) ? 1 : 0) |
                    (((flags & LODGE_RECORD_MAX) && out.maxw_dev) ? 2 : 0);
   switch (mode) {
-    case 3: launch_comp<false, 3>(w, fs, W, H, rp, flags, out, s); break;
-    case 2: launch_comp<false, 2>(w, fs, W, H, rp, flags, out, s); break;
-    case 1: launch_comp<false, 1>(w, fs, W, H, rp, flags, out, s); break;
-    default: launch_comp<false, 0>(w, fs, W, H, rp, flags, out, s); break;
+    case 3: launch_fast<3>(w, fs, W, H, rp, flags, out, s, phase); break;
+    case 2: launch_fast<2>(w, fs, W, H, rp, flags, out, s, phase); break;
+    case 1: launch_fast<1>(w, fs, W, H, rp, flags, out, s, phase); break;
+    default: launch_fast<0>(w, fs, W, H, rp, flags, out, s, phase); break;
   }
 }
 

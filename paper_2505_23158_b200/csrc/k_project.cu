@@ -379,27 +379,6 @@ __device__ __forceinline__ uint64_t tile_rect(double mx, double my, double ex, d
   return (uint64_t)x0 | ((uint64_t)x1 << 16) | ((uint64_t)y0 << 32) | ((uint64_t)y1 << 48);
 }
 
-// Warp-aggregated atomic: lanes hitting the same counter combine first (the
-// corners of border-clipped splats are shared by many splats).  Called by
-// the whole warp; inactive lanes pass idx = -1.
-__device__ __forceinline__ void warp_add(int32_t *base, int32_t idx, int32_t v) {
-  const uint32_t peers = __match_any_sync(FULL_MASK, idx);
-  if (idx >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1)
-    atomicAdd(base + idx, v * __popc(peers));
-}
-
-// 2-D difference-array update for a tile rectangle (whole warp; valid flag).
-__device__ __forceinline__ void add_tile_diff(int32_t *diff, uint64_t rc, int32_t tiles_x,
-                                              bool valid) {
-  const int32_t x0 = (int32_t)(rc & 0xffff), x1 = (int32_t)((rc >> 16) & 0xffff);
-  const int32_t y0 = (int32_t)((rc >> 32) & 0xffff), y1 = (int32_t)(rc >> 48);
-  const int32_t stride = tiles_x + 1;
-  warp_add(diff, valid ? y0 * stride + x0 : -1, 1);
-  warp_add(diff, valid ? y0 * stride + x1 + 1 : -1, -1);
-  warp_add(diff, valid ? (y1 + 1) * stride + x0 : -1, -1);
-  warp_add(diff, valid ? (y1 + 1) * stride + x1 + 1 : -1, 1);
-}
-
 // ---------------------------------------------------------------------------
 // Frame mode: inputs come from the K1 union (tags), outputs are the internal
 // compositing representation.

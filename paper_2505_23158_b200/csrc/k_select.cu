@@ -489,6 +489,13 @@ __global__ void k_begin_frame(FrameState *fs) {
     fs->stats.P = 0;
     fs->stats.overflow = 0;
     fs->stats.guard_hits = 0;
+    fs->stats.P_first = 0;
+    fs->stats.P_second = 0;
+    fs->stats.fault = 0;
+    fs->split_S = 0;
+    fs->P_A = 0;
+    fs->n_alive = 0;
+    fs->n_owners_b = 0;
     fs->stats.f = -1;  // set by k_select_frame on the chunk paths
     fs->stats.o = -1;
     fs->stats.t = 1.0;

@@ -99,9 +99,11 @@ __global__ void __launch_bounds__(OS_THREADS, VALS ? LODGE_OS_VMINB
     else
       return (KO)key;
   };
+  // the output holds n keys (DROP: the survivors, counted into stats.M)
   onesweep_partition<OS_ITEMS, NB, VALS>(S, k, vmask, part, cnt, shift, digit_off, status,
                                          fs->epoch + tk, kout, kmap, vout,
-                                         [&](uint32_t li) { return vin[base + li]; });
+                                         [&](uint32_t li) { return vin[base + li]; },
+                                         DROP ? fs->stats.M : n, &fs->stats.fault);
 }
 
 // ---- frame depth sort: 32-bit keys + tie repair ----------------------------
@@ -155,7 +157,8 @@ __global__ void __launch_bounds__(OS_THREADS, LODGE_OS_VMINB)
   }
   onesweep_partition<IT, 8, true>(S, k, vmask, part, cnt, shift, digit_off, status,
                                   fs->epoch + tk, kout, [](uint32_t key) { return key; }, vout,
-                                  [&](uint32_t li) { return vin[base + li]; });
+                                  [&](uint32_t li) { return vin[base + li]; },
+                                  FIRST ? fs->stats.M : n, &fs->stats.fault);
 }
 
 // Histograms of the four 8-bit digits of the 32-bit depth keys.
@@ -399,7 +402,7 @@ static int bit_width(uint64_t v) {
 //             pass 2 on tile >> 8 -> list (u32 in pairs[0]).
 // Tile ranges come from tile_start, so the lists need no tile bits.
 void launch_tile_sort(Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
-                      int32_t *launches, cudaStream_t s) {
+                      int32_t *launches, cudaStream_t s, int tk0) {
   const int64_t grid = w.P_cap;  // keys: the launchers size their grids
   const uint32_t T = (uint32_t)tiles_x * (uint32_t)tiles_y;
   const int lo_bits = std::min(8, std::max(1, bit_width(T - 1)));
@@ -412,7 +415,7 @@ void launch_tile_sort(Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
   if (T <= 256) {
     os_launch_nb<false, uint64_t, uint32_t, MAP_LOW>(lo_bits, grid, s, p0, u32_1, no_v, no_vo,
                                                      nin, 32, 32, (const uint32_t *)fs->off_tile[0],
-                                                     w.status, fs, (int)TK_TILE0);
+                                                     w.status, fs, tk0);
     ++*launches;
     w.list = u32_1;
     return;
@@ -421,16 +424,16 @@ void launch_tile_sort(Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
   const int sb = std::max(1, bit_width((uint64_t)std::max<int64_t>(w.M_cap, 1) - 1));
   if (hi_bits + sb <= 32) {
     os_launch<false, uint64_t, uint32_t, MAP_PACK, 8>(grid, s, p0, u32_1, no_v, no_vo, nin, 32, sb,
-                                                      fs->off_tile[0], w.status, fs, TK_TILE0);
+                                                      fs->off_tile[0], w.status, fs, tk0);
     os_launch_nb<false, uint32_t, uint32_t, MAP_LOW>(
         hi_bits, grid, s, (const uint32_t *)u32_1, u32_0, no_v, no_vo, nin, sb, sb,
-        (const uint32_t *)fs->off_tile[1], w.status, fs, (int)TK_TILE0 + 1);
+        (const uint32_t *)fs->off_tile[1], w.status, fs, tk0 + 1);
   } else {
     os_launch<false, uint64_t, uint64_t, MAP_ID, 8>(grid, s, p0, w.pairs[1], no_v, no_vo, nin, 32,
-                                                    32, fs->off_tile[0], w.status, fs, TK_TILE0);
+                                                    32, fs->off_tile[0], w.status, fs, tk0);
     os_launch_nb<false, uint64_t, uint32_t, MAP_LOW>(
         hi_bits, grid, s, (const uint64_t *)w.pairs[1], u32_0, no_v, no_vo, nin, 40, 32,
-        (const uint32_t *)fs->off_tile[1], w.status, fs, (int)TK_TILE0 + 1);
+        (const uint32_t *)fs->off_tile[1], w.status, fs, tk0 + 1);
   }
   *launches += 2;
   w.list = u32_0;

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cstddef>
 #include <string>
@@ -36,6 +37,9 @@ struct lodge_ctx {
   lodge_frame_stats *stats_host = nullptr;  // pinned
   Work w{};
   int64_t tiles_cap = 0;  // capacity of tile_start (T+1) and diff
+  int64_t pixels_cap = 0;  // capacity of the two-phase pixel state
+  int32_t phase_budget = 1280;  // first-phase pairs per tile of two-phase frames (0: one pass)
+  bool debug_sync = false;  // LODGE_DEBUG_SYNC=1: synchronise and check after every stage
   int32_t launches = 0;
   LevelSlots last_slots{};  // slot layout of the last union
   // stage profiling
@@ -102,14 +106,32 @@ static int ensure_P(lodge_ctx *c, int64_t need) {
 static int ensure_tiles(lodge_ctx *c, int32_t W, int32_t H) {
   const int64_t tx = (W + 15) / 16, ty = (H + 15) / 16;
   const int64_t need = (tx + 1) * (ty + 1) + 1;
-  if (need <= c->tiles_cap && c->w.tile_diff) return 0;
-  cudaFree(c->w.tile_diff); cudaFree(c->w.tile_start); cudaFree(c->w.tile_order);
-  c->tiles_cap = 0;
-  CK(cudaMalloc(&c->w.tile_diff, 4 * need));
-  CK(cudaMemset(c->w.tile_diff, 0, 4 * need));
-  CK(cudaMalloc(&c->w.tile_start, 4 * need));
-  CK(cudaMalloc(&c->w.tile_order, 4 * need));
-  c->tiles_cap = need;
+  Work &w = c->w;
+  if (need > c->tiles_cap || !w.tile_diff) {
+    void *old[] = {w.tile_diff, w.tile_start, w.tile_order, w.tile_diff_a, w.count_all,
+                   w.tile_start_b, w.tile_order_b, w.alive, w.sat};
+    for (void *p : old) cudaFree(p);
+    c->tiles_cap = 0;
+    CK(cudaMalloc(&w.tile_diff, 4 * need));
+    CK(cudaMemset(w.tile_diff, 0, 4 * need));
+    CK(cudaMalloc(&w.tile_diff_a, 4 * need));
+    CK(cudaMemset(w.tile_diff_a, 0, 4 * need));
+    CK(cudaMalloc(&w.tile_start, 4 * need));
+    CK(cudaMalloc(&w.tile_order, 4 * need));
+    CK(cudaMalloc(&w.count_all, 4 * need));
+    CK(cudaMalloc(&w.tile_start_b, 4 * need));
+    CK(cudaMalloc(&w.tile_order_b, 4 * need));
+    CK(cudaMalloc(&w.alive, 4 * (need / 32 + 1)));
+    CK(cudaMalloc(&w.sat, 4 * need));
+    c->tiles_cap = need;
+  }
+  const int64_t px = (int64_t)W * H;
+  if (px > c->pixels_cap || !w.state) {
+    cudaFree(w.state);
+    c->pixels_cap = 0;
+    CK(cudaMalloc(&w.state, sizeof(float4) * px));
+    c->pixels_cap = px;
+  }
   return 0;
 }
 
@@ -131,6 +153,19 @@ static int check_launch(const char *what) {
     return set_err(LODGE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
   return 0;
 }
+
+// LODGE_DEBUG_SYNC builds of a frame: a device fault is reported with the
+// stage that raised it
+#define DSYNC(what)                                                                   \
+  do {                                                                                \
+    if (c->debug_sync) {                                                              \
+      cudaError_t _e = cudaStreamSynchronize(s);                                      \
+      if (_e == cudaSuccess) _e = cudaGetLastError();                                 \
+      if (_e != cudaSuccess)                                                          \
+        return set_err(LODGE_ERR_CUDA, std::string("after ") + (what) + ": " +        \
+                                           cudaGetErrorString(_e));                   \
+    }                                                                                 \
+  } while (0)
 
 static int check_cam(const lodge_camera *cam) {
   if (!cam) return set_err(LODGE_ERR_BAD_ARG, "camera is NULL");
@@ -159,6 +194,10 @@ int lodge_create(int32_t device, lodge_ctx **out) {
   CK(cudaSetDevice(device));
   lodge_ctx *c = new lodge_ctx();
   c->device = device;
+  {
+    const char *d = getenv("LODGE_DEBUG_SYNC");
+    c->debug_sync = d && d[0] == '1';
+  }
   CK(cudaMalloc(&c->fs, sizeof(FrameState)));
   CK(cudaMemset(c->fs, 0, sizeof(FrameState)));
   CK(cudaMalloc(&c->cam_dev, sizeof(lodge_camera)));
@@ -178,7 +217,8 @@ void lodge_destroy(lodge_ctx *c) {
   void *ptrs[] = {w.key_depth[0], w.key_depth[1], w.val_depth[0], w.val_depth[1], w.rect,
                   w.payload, w.precise, w.pairs[0], w.pairs[1], w.tile_diff, w.tile_start,
                   w.status, w.union_idx, w.union_tag, c->fs, c->cam_dev, w.rect_sorted,
-                  w.splat_off, w.chunk_first, w.tile_order};
+                  w.splat_off, w.chunk_first, w.tile_order, w.tile_diff_a, w.count_all,
+                  w.tile_start_b, w.tile_order_b, w.alive, w.sat, w.state};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c->cam_host) cudaFreeHost(c->cam_host);
@@ -189,6 +229,13 @@ void lodge_destroy(lodge_ctx *c) {
 int lodge_set_stream(lodge_ctx *c, void *stream) {
   if (!c) return set_err(LODGE_ERR_BAD_ARG, "ctx is NULL");
   c->stream = (cudaStream_t)stream;
+  return 0;
+}
+
+int lodge_set_phase_budget(lodge_ctx *c, int32_t pairs_per_tile) {
+  if (!c) return set_err(LODGE_ERR_BAD_ARG, "ctx is NULL");
+  if (pairs_per_tile < 0) return set_err(LODGE_ERR_BAD_ARG, "phase budget must be >= 0");
+  c->phase_budget = pairs_per_tile;
   return 0;
 }
 
@@ -401,6 +448,14 @@ int lodge_render_frame(lodge_ctx *c, const lodge_level *levels, int32_t n_levels
                      "lodge_render_frame", ch);
 }
 
+// Two depth phases: FAST compositing, lists not needed for inspection, and
+// both tile difference arrays fit the setup kernel's shared memory.
+static bool two_phase(const lodge_ctx *c, int32_t W, int32_t H, int32_t flags) {
+  const int64_t tx = (W + 15) / 16, ty = (H + 15) / 16;
+  return c->precision == LODGE_PREC_FAST && c->phase_budget > 0 &&
+         !(flags & LODGE_FULL_LISTS) && 2 * (tx + 1) * (ty + 1) * 4 <= 200 * 1024;
+}
+
 // Everything after the active-set stage, shared by the chunk and LOD paths:
 // projection -> depth sort -> tile setup -> duplication -> tile sort ->
 // compositing, on the context stream, stage marks 2..8.
@@ -422,17 +477,57 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
                                 ch ? ch->slab_geom_dev : nullptr, ch ? ch->slab_sh_dev : nullptr);
   if (rc) return set_err(LODGE_ERR_BAD_ARG, "all levels must share one storage precision");
   ++nl;
+  DSYNC("launch_project_frame");
   c->mark(3);
   launch_depth_sort(w, c->fs, U_cap, &nl, s);
+  DSYNC("launch_depth_sort");
   c->mark(4);
-  launch_tile_setup(w, c->fs, out->tile_count_dev, tiles_x, tiles_y, s); ++nl;
-  c->mark(5);
-  launch_duplicate(w, c->fs, tiles_x, U_cap, s); nl += 2;  // count, emit
-  c->mark(6);
-  launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s);
-  c->mark(7);
-  launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, 0, s); ++nl;
-  c->mark(8);
+  if (two_phase(c, W, H, flags)) {
+    // FAST frames in two depth phases: the splats whose pairs
+    // start within the budget are binned, sorted and composited first; the
+    // tiles that still have live pixels then receive the rest of their pairs
+    const uint32_t budget = (uint32_t)std::min<int64_t>(
+        (int64_t)c->phase_budget * tiles_x * tiles_y, 0x7fffffff);
+    launch_dup_count(w, c->fs, tiles_x, U_cap, budget, s);
+    DSYNC("launch_dup_count");
+    launch_tile_setup(w, c->fs, out->tile_count_dev, tiles_x, tiles_y, s, true);
+    DSYNC("launch_tile_setup");
+    nl += 2;
+    c->mark(5);
+    launch_dup_emit(w, c->fs, tiles_x, s, true); ++nl;
+    DSYNC("launch_dup_emit");
+    c->mark(6);
+    launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s);
+    DSYNC("launch_tile_sort");
+    c->mark(7);
+    launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, 0, s, 1); ++nl;
+    DSYNC("launch_composite");
+    c->mark(8);
+    launch_setup_b(w, c->fs, tiles_x, tiles_y, s);
+    DSYNC("launch_setup_b");
+    launch_enum_b(w, c->fs, tiles_x, tiles_y, U_cap, s);
+    DSYNC("launch_enum_b");
+    nl += 3;
+    launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s, TK_TILEB0);
+    DSYNC("launch_tile_sort (second phase)");
+    launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, 0, s, 2); ++nl;
+    DSYNC("launch_composite (second phase)");
+    c->mark(9);
+  } else {
+    launch_tile_setup(w, c->fs, out->tile_count_dev, tiles_x, tiles_y, s); ++nl;
+    DSYNC("launch_tile_setup");
+    c->mark(5);
+    launch_duplicate(w, c->fs, tiles_x, U_cap, s); nl += 2;  // count, emit
+    DSYNC("launch_duplicate");
+    c->mark(6);
+    launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s);
+    DSYNC("launch_tile_sort");
+    c->mark(7);
+    launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, 0, s); ++nl;
+    DSYNC("launch_composite");
+    c->mark(8);
+    c->mark(9);
+  }
   if (c->prof && c->prof_frames < c->prof_cap) ++c->prof_frames;
   if (stats_dev)
     CK(cudaMemcpyAsync(stats_dev, &c->fs->stats, sizeof(lodge_frame_stats), cudaMemcpyDeviceToDevice, s));

@@ -46,11 +46,16 @@ class Renderer:
     """n_streams > 1 keeps that many frames in flight: each slot owns a
     liblodge context (workspace + frame state) and a CUDA stream, so the
     latency-bound stages of one frame overlap the bandwidth-bound stages of
-    another.  render(..., slot=k) enqueues on slot k's stream."""
+    another.  render(..., slot=k) enqueues on slot k's stream.
+
+    FAST frames composite in two depth phases (lodge_set_phase_budget:
+    phase_budget first-phase pairs per tile, 0 = one pass); full_lists=True
+    keeps one pass so the sorted per-tile lists stay inspectable
+    (lodge_frame_lists).  The outputs are the same either way."""
 
     def __init__(self, levels: Sequence, plan, device=None, storage: str = "fp32",
                  precision: str = "fast", raster_cfg: RasterConfig = RasterConfig(),
-                 n_streams: int = 1):
+                 n_streams: int = 1, full_lists: bool = False, phase_budget: int = 1280):
         self.ctx = context(device)
         self.device = self.ctx.device
         if n_streams < 1:
@@ -73,6 +78,10 @@ class Renderer:
             raise ValueError("chunk plan and level list disagree on the level count")
         self._level_arr = (N.Level * len(self.levels))(*[l.struct for l in self.levels])
         self.precision = precision
+        self.full_lists = bool(full_lists)
+        if phase_budget < 0:
+            raise ValueError("phase_budget must be >= 0")
+        self.phase_budget = int(phase_budget)
         self.cfg = raster_cfg
         self._rp = params_struct(raster_cfg)
         lod_cap = sum(l.n for l in self.levels)
@@ -91,9 +100,12 @@ class Renderer:
     def _bind(self, slot: int):
         ctx, s = self._slots[slot]
         if s is None:
-            return ctx.bind(self.precision)
-        with torch.cuda.stream(s):
-            return ctx.bind(self.precision)
+            p = ctx.bind(self.precision)
+        else:
+            with torch.cuda.stream(s):
+                p = ctx.bind(self.precision)
+        N.check(N.lib().lodge_set_phase_budget(p, self.phase_budget), "lodge_set_phase_budget")
+        return p
 
     def reserve(self, max_pairs: int):
         for k in range(self.n_streams):
@@ -147,7 +159,8 @@ class Renderer:
         out.tile_count_dev = frame.tile_count.data_ptr()
         out.visible_dev = frame.visible.data_ptr()
         out.maxw_dev = frame.maxw.data_ptr() if (record_max and frame.maxw is not None) else None
-        flags = (N.NEED_IMAGE if need_image else 0) | (N.RECORD_MAX if record_max else 0)
+        flags = ((N.NEED_IMAGE if need_image else 0) | (N.RECORD_MAX if record_max else 0) |
+                 (N.FULL_LISTS if self.full_lists else 0))
         if accumulate_max:
             flags |= N.ACCUMULATE_MAX
         pr = None
@@ -185,7 +198,8 @@ class Renderer:
         out.visible_dev = frame.visible.data_ptr()
         out.maxw_dev = frame.maxw.data_ptr() if (record_max and frame.maxw is not None) else None
         flags = ((N.NEED_IMAGE if need_image else 0) | (N.RECORD_MAX if record_max else 0) |
-                 (N.ACCUMULATE_MAX if accumulate_max else 0))
+                 (N.ACCUMULATE_MAX if accumulate_max else 0) |
+                 (N.FULL_LISTS if self.full_lists else 0))
         N.check(N.lib().lodge_render_lod(
             self._bind(slot), self._level_arr, len(self.levels), b, int(bool(full)),
             ptr(cam_row), frame.width, frame.height, C.byref(self._rp), flags, C.byref(out),
@@ -205,6 +219,8 @@ class Renderer:
             self.reserve(int(st.P))
             self.render_lod(cams[0], fr, bounds, full, need_image, record_max)
             st = fr.read_stats()
+        if st.fault:
+            raise RuntimeError(f"liblodge: device bounds check fired (fault bits {st.fault:#x})")
         return fr, st
 
     def to_srgb8(self, frame: Frame, out: torch.Tensor, slot: int = 0) -> torch.Tensor:
@@ -229,4 +245,6 @@ class Renderer:
             self.reserve(int(st.P))
             self.render(cams[0], fr, pair=pair, t=t, need_image=need_image, record_max=record_max)
             st = fr.read_stats()
+        if st.fault:
+            raise RuntimeError(f"liblodge: device bounds check fired (fault bits {st.fault:#x})")
         return fr, st

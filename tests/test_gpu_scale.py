@@ -32,7 +32,7 @@ def street():
     levels = [DeviceLevel.from_tensors(torch.from_numpy(g).to(dev), torch.from_numpy(s).to(dev),
                                        cfg.degree) for g, s, _ in cfg.levels]
     plan = DevicePlan.from_arrays(cfg.centers, cfg.offsets, cfg.data, cfg.L, dev)
-    r = L.Renderer(levels, plan, storage="fp32", precision="fast")
+    r = L.Renderer(levels, plan, storage="fp32", precision="fast", full_lists=True)
     return cfg, r
 
 
@@ -117,7 +117,7 @@ def test_street_other_resolutions_vs_oracle(street, res, precision):
     pass), through the fused path in both precisions."""
     cfg, _ = street
     w, h = res
-    r = L.Renderer(street[1].levels, street[1].plan, precision=precision)
+    r = L.Renderer(street[1].levels, street[1].plan, precision=precision, full_lists=True)
     cam = scenes.camera(47.0, width=w, height=h, focal=scenes.FOCAL * max(w, 64) / 1920)
     fr, st = r.render_camera(cam)
     (f, o, t), sel, ref = oracle_frame(cfg, cam)
