@@ -29,6 +29,7 @@ struct FrameState {
   uint32_t P_A;                       // their pairs (a prefix of the pair sequence)
   uint32_t n_alive;                   // tiles the second phase composites
   uint32_t n_owners_b;                // second-phase splats that meet an alive tile
+  uint32_t alive_box[4];              // x0, x1, y0, y1: bounding box of the alive tiles
   unsigned long long counters[8];     // LODGE_COUNTERS builds: compositing work counters
 };
 

@@ -7,6 +7,8 @@
 // splat instead of one per pair), integrated here; the duplication kernel
 // uses a single-pass look-back scan and block-cooperative emission so one
 // huge splat (all 8160 tiles at 1080p) does not serialise a thread.
+#include <algorithm>
+
 #include "emit.cuh"
 #include "internal.cuh"
 
@@ -189,22 +191,35 @@ __global__ void __launch_bounds__(1024) k_setup_b(const uint32_t *__restrict__ a
   __shared__ uint32_t h0[256], h1[256];
   __shared__ uint32_t s_sum[1024];
   __shared__ uint32_t s_bk[33];
-  __shared__ uint32_t s_tot, s_nz;
+  __shared__ uint32_t s_tot, s_nz, s_box[4];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int stride = tiles_x + 1;
   const int nd = stride * (tiles_y + 1);
   const int T = tiles_x * tiles_y;
+  if (tid == 0) {
+    s_box[0] = s_box[2] = 0xffffffffu;
+    s_box[1] = s_box[3] = 0u;
+  }
   auto live = [&](int t) { return (alive[t >> 5] >> (t & 31)) & 1u; };
   auto cnt = [&](int t) {
     return live(t) ? count_all[t] - (start_a[t + 1] - start_a[t]) : 0u;
   };
   // sat[(y+1)*stride + (x+1)] = alive(y, x), row 0 / column 0 zero, then a
   // 2-D prefix over the whole table
+  __syncthreads();
   for (int i = tid; i < nd; i += nt) {
     const int y = i / stride, x = i % stride;
-    ss[i] = (y > 0 && x > 0) ? (int32_t)live((y - 1) * tiles_x + (x - 1)) : 0;
+    const bool a = y > 0 && x > 0 && live((y - 1) * tiles_x + (x - 1));
+    ss[i] = a ? 1 : 0;
+    if (a) {  // bounding box of the alive tiles
+      atomicMin(&s_box[0], (uint32_t)(x - 1));
+      atomicMax(&s_box[1], (uint32_t)(x - 1));
+      atomicMin(&s_box[2], (uint32_t)(y - 1));
+      atomicMax(&s_box[3], (uint32_t)(y - 1));
+    }
   }
   __syncthreads();
+  if (tid < 4) fs->alive_box[tid] = s_box[tid];
   for (int y = tid; y <= tiles_y; y += nt) {
     int32_t run = 0;
     for (int x = 0; x <= tiles_x; ++x) {
@@ -251,9 +266,10 @@ __device__ __forceinline__ bool rect_alive(const uint32_t *__restrict__ sat, uin
 // the first phase (their rectangles go to the tile_diff_a difference array;
 // split_S and P_A record the split).  SECOND: the enumeration of the second
 // phase over splats [split_S, M) -- only the splats that meet an alive tile,
-// compacted in depth order (a second look-back) into the owner list the
-// emission reads: rectangles in w.rect, ids in w.val_depth[1] (both dead by
-// then), pair offsets and splitters over that list.
+// their rectangles clipped to the alive tiles' bounding box, compacted in
+// depth order (a second look-back) into the owner list the emission reads:
+// rectangles in w.rect, ids in w.val_depth[1] (both dead by then), pair
+// offsets and splitters over that list.
 template <bool SECOND>
 __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__restrict__ order,
                                                            const uint64_t *__restrict__ rect,
@@ -299,7 +315,15 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
     const uint32_t x0 = rc[i] & 0xffff, x1 = (rc[i] >> 16) & 0xffff, y0 = (rc[i] >> 32) & 0xffff,
                    y1 = rc[i] >> 48;
     c[i] = (r0 + i < n) ? (x1 - x0 + 1) * (y1 - y0 + 1) : 0u;
-    if (SECOND && c[i] && !rect_alive(w.sat, rc[i], tiles_x)) c[i] = 0u;
+    if (SECOND && c[i]) {  // clip to the alive tiles' bounding box (all else is dead)
+      const uint32_t cx0 = max(x0, fs->alive_box[0]), cx1 = min(x1, fs->alive_box[1]);
+      const uint32_t cy0 = max(y0, fs->alive_box[2]), cy1 = min(y1, fs->alive_box[3]);
+      rc[i] = (uint64_t)cx0 | ((uint64_t)cx1 << 16) | ((uint64_t)cy0 << 32) |
+              ((uint64_t)cy1 << 48);
+      c[i] = (cx0 <= cx1 && cy0 <= cy1 && rect_alive(w.sat, rc[i], tiles_x))
+                 ? (cx1 - cx0 + 1) * (cy1 - cy0 + 1)
+                 : 0u;
+    }
     cnt += c[i];
     nz += c[i] ? 1u : 0u;
     if (!SECOND && r0 + i < n) w.rect_sorted[r0 + i] = rc[i];
@@ -395,17 +419,21 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_emit(const uint32_t *__rest
                                                           FrameState *fs, int32_t first_phase) {
   __shared__ EmitSmem<EMIT_CHUNK> E;
   const uint32_t P = fs->n_pairs;
-  const uint32_t j0 = blockIdx.x * EMIT_CHUNK;
-  if (j0 >= P) return;
-  const uint32_t j1 = min(j0 + (uint32_t)EMIT_CHUNK, P);
-  uint32_t r0, r1;
-  emit_owners(w, j0, j1, P, first_phase ? fs->split_S : fs->stats.M, r0, r1);
-  emit_stage(E, order, w, j0, j1, r0, r1, &fs->stats.fault);
+  const uint32_t n_own = first_phase ? fs->split_S : fs->stats.M;
+  // persistent CTAs, grid-stride over the chunks
+  for (uint32_t c = blockIdx.x; c * EMIT_CHUNK < P; c += gridDim.x) {
+    const uint32_t j0 = c * EMIT_CHUNK;
+    const uint32_t j1 = min(j0 + (uint32_t)EMIT_CHUNK, P);
+    uint32_t r0, r1;
+    emit_owners(w, j0, j1, P, n_own, r0, r1);
+    emit_stage(E, order, w, j0, j1, r0, r1, &fs->stats.fault);
 #pragma unroll
-  for (int it = 0; it < EMIT_ITEMS; ++it) {
-    const uint32_t j = j0 + it * DUP_THREADS + threadIdx.x;
-    if (j >= j1) break;
-    w.pairs[0][j] = emit_pair(E, j, j0, tiles_x);
+    for (int it = 0; it < EMIT_ITEMS; ++it) {
+      const uint32_t j = j0 + it * DUP_THREADS + threadIdx.x;
+      if (j >= j1) break;
+      w.pairs[0][j] = emit_pair(E, j, j0, tiles_x);
+    }
+    __syncthreads();  // the next chunk restages E
   }
 }
 
@@ -422,15 +450,18 @@ __global__ void __launch_bounds__(DUP_THREADS) k_emit_b(const uint32_t *__restri
   __shared__ uint32_t s_cnt[EMIT_ITEMS][DUP_THREADS / 32];
   __shared__ uint32_t s_part, s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t n = fs->stats.overflow ? 0u : fs->n_owners_b;
+  const uint32_t Pe = n ? w.splat_off[n] : 0u;  // enumerated pairs
+  if (Pe == 0) return;
+  for (int i = tid; i < (n_tiles + 31) / 32; i += DUP_THREADS) s_alive[i] = w.alive[i];
+  // persistent CTAs: chunks in ticket order (the compaction's look-back)
+  for (;;) {
   if (tid == 0) s_part = atomicAdd(&fs->tickets[TK_EMITB], 1u);
   __syncthreads();
   const uint32_t part = s_part;
-  const uint32_t n = fs->stats.overflow ? 0u : fs->n_owners_b;
-  const uint32_t Pe = n ? w.splat_off[n] : 0u;  // enumerated pairs
   const uint32_t j0 = part * EMIT_CHUNK;
-  if (j0 >= Pe) return;
+  if (j0 >= Pe) break;
   const uint32_t j1 = min(j0 + (uint32_t)EMIT_CHUNK, Pe);
-  for (int i = tid; i < (n_tiles + 31) / 32; i += DUP_THREADS) s_alive[i] = w.alive[i];
   uint32_t r0, r1;
   emit_owners(w, j0, j1, Pe, n, r0, r1);
   Work wb = w;  // the compacted owner list of k_dup_count<true>
@@ -478,6 +509,8 @@ __global__ void __launch_bounds__(DUP_THREADS) k_emit_b(const uint32_t *__restri
       else raise_fault(&fs->stats.fault, FAULT_COMPACT);
     }
   }
+  __syncthreads();  // the next chunk restages E and the counters
+  }
 }
 
 void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32_t tiles_x,
@@ -506,9 +539,22 @@ void launch_dup_count(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_
                                                   chunk_cap(w));
 }
 
+// Resident CTAs of a kernel on this device (persistent grids).
+template <typename K>
+static int64_t resident_ctas(K kernel, int threads) {
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, 0);
+  return (int64_t)std::max(per, 1) * std::max(sms, 1);
+}
+
 void launch_dup_emit(const Work &w, FrameState *fs, int32_t tiles_x, cudaStream_t s,
                      bool first_phase) {
-  const unsigned egrid = (unsigned)((w.P_cap + EMIT_CHUNK - 1) / EMIT_CHUNK);
+  static int64_t resident = 0;
+  if (!resident) resident = resident_ctas(k_dup_emit, DUP_THREADS);
+  const unsigned egrid =
+      (unsigned)std::min<int64_t>((w.P_cap + EMIT_CHUNK - 1) / EMIT_CHUNK, resident);
   k_dup_emit<<<egrid, DUP_THREADS, 0, s>>>(w.val_depth[0], tiles_x, w, fs, first_phase ? 1 : 0);
 }
 
@@ -538,7 +584,10 @@ void launch_enum_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles
       (unsigned)((M_cap + DUP_THREADS * COUNT_ITEMS - 1) / (DUP_THREADS * COUNT_ITEMS));
   k_dup_count<true><<<grid, DUP_THREADS, 0, s>>>(w.val_depth[0], w.rect, w, fs, 0u, tiles_x,
                                                  chunk_cap(w));
-  const unsigned egrid = (unsigned)((w.P_cap + EMIT_CHUNK - 1) / EMIT_CHUNK);
+  static int64_t resident = 0;
+  if (!resident) resident = resident_ctas(k_emit_b, DUP_THREADS);
+  const unsigned egrid =
+      (unsigned)std::min<int64_t>((w.P_cap + EMIT_CHUNK - 1) / EMIT_CHUNK, resident);
   k_emit_b<<<egrid, DUP_THREADS, 0, s>>>(w.val_depth[0], tiles_x, tiles_x * tiles_y, w, fs);
 }
 

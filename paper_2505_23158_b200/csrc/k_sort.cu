@@ -64,12 +64,14 @@ __global__ void __launch_bounds__(OS_THREADS, VALS ? LODGE_OS_VMINB
   using Smem = OSmem<OS_ITEMS, VALS, KI, (1 << NB)>;
   Smem &S = *reinterpret_cast<Smem *>(smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t n = *n_ptr;
+  // persistent CTAs: partitions in ticket order until the keys run out
+  for (;;) {
   if (tid == 0) S.misc[0] = atomicAdd(&fs->tickets[tk], 1u);
   __syncthreads();
   const uint32_t part = S.misc[0];
-  const uint32_t n = *n_ptr;
   const uint32_t base = part * OS_TILE;
-  if (base >= n) return;
+  if (base >= n) break;
   KI k[OS_ITEMS];
   uint32_t vmask = 0;
 #pragma unroll
@@ -104,6 +106,8 @@ __global__ void __launch_bounds__(OS_THREADS, VALS ? LODGE_OS_VMINB
                                          fs->epoch + tk, kout, kmap, vout,
                                          [&](uint32_t li) { return vin[base + li]; },
                                          DROP ? fs->stats.M : n, &fs->stats.fault);
+  __syncthreads();  // the next partition reuses the shared memory
+  }
 }
 
 // ---- frame depth sort: 32-bit keys + tie repair ----------------------------
@@ -131,12 +135,13 @@ __global__ void __launch_bounds__(OS_THREADS, LODGE_OS_VMINB)
   using Smem = OSmem<IT, true, uint32_t, 256>;
   Smem &S = *reinterpret_cast<Smem *>(smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t n = *n_ptr;
+  for (;;) {  // persistent CTAs, partitions in ticket order
   if (tid == 0) S.misc[0] = atomicAdd(&fs->tickets[tk], 1u);
   __syncthreads();
   const uint32_t part = S.misc[0];
-  const uint32_t n = *n_ptr;
   const uint32_t base = part * TILE;
-  if (base >= n) return;
+  if (base >= n) break;
   uint32_t k[IT];
   uint32_t vmask = 0;
 #pragma unroll
@@ -159,6 +164,8 @@ __global__ void __launch_bounds__(OS_THREADS, LODGE_OS_VMINB)
                                   fs->epoch + tk, kout, [](uint32_t key) { return key; }, vout,
                                   [&](uint32_t li) { return vin[base + li]; },
                                   FIRST ? fs->stats.M : n, &fs->stats.fault);
+  __syncthreads();
+  }
 }
 
 // Histograms of the four 8-bit digits of the 32-bit depth keys.
@@ -188,7 +195,7 @@ __global__ void __launch_bounds__(256) k_depth_hist32(const uint64_t *__restrict
 // start; longer ones (only adversarial inputs: > 32 depths within one fp32
 // ulp) by the whole CTA through `scratch`, by rank counting.
 constexpr int TIE_SHORT = 32;
-constexpr int TIE_SEG = 4096;  // run starts examined per CTA step
+constexpr int TIE_SEG = 1024;  // run starts examined per CTA step
 __global__ void __launch_bounds__(256) k_depth_ties(const uint32_t *__restrict__ k32,
                                                     uint32_t *val,
                                                     const uint64_t *__restrict__ full,
@@ -296,20 +303,32 @@ __global__ void k_depth_scan(FrameState *fs) {
   }
 }
 
+// Grid of a persistent kernel: its resident CTAs on this device (at most
+// `need`).  Queried once per kernel (static per instantiation at the call).
+template <typename K>
+static unsigned resident_grid(K kernel, int threads, size_t smem, int64_t need) {
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+  const int64_t r = (int64_t)std::max(per, 1) * std::max(sms, 1);
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, r));
+}
+
 // One onesweep pass (dynamic shared memory opted in once per instantiation).
 template <bool VALS, typename KI, typename KO, int MAP, int NB, bool DROP = false>
 static void os_launch(int64_t cap, cudaStream_t s, const KI *kin, KO *kout, const uint32_t *vin,
                       uint32_t *vout, const uint32_t *n_ptr, int shift, int sb,
                       const uint32_t *digit_off, uint64_t *status, FrameState *fs, int tk) {
   constexpr int64_t TILE = (int64_t)OS_THREADS * os_items<VALS, KI>();
-  const unsigned grid = (unsigned)((cap + TILE - 1) / TILE);
-  static bool done = false;
+  static unsigned resident = 0;
   const size_t sm = sizeof(OSmem<os_items<VALS, KI>(), VALS, KI, (1 << NB)>);
-  if (!done) {
+  if (!resident) {
     cudaFuncSetAttribute(k_onesweep<VALS, KI, KO, MAP, NB, DROP>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    done = true;
+    resident = resident_grid(k_onesweep<VALS, KI, KO, MAP, NB, DROP>, OS_THREADS, sm, 1 << 30);
   }
+  const unsigned grid = (unsigned)std::min<int64_t>((cap + TILE - 1) / TILE, resident);
   k_onesweep<VALS, KI, KO, MAP, NB, DROP><<<grid, OS_THREADS, sm, s>>>(
       kin, kout, vin, vout, n_ptr, shift, sb, digit_off, status, fs, tk);
 }
@@ -338,15 +357,15 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
   k_depth_scan<<<1, 256, 0, s>>>(fs);
   *launches += 2;
   constexpr int64_t TILE = (int64_t)OS_THREADS * LODGE_OS_ITEMS_D;
-  const unsigned grid = (unsigned)((M_cap + TILE - 1) / TILE);
   const size_t sm = sizeof(OSmem<LODGE_OS_ITEMS_D, true, uint32_t, 256>);
-  static bool attr = false;
-  if (!attr) {
+  static unsigned resident = 0;
+  if (!resident) {
     cudaFuncSetAttribute(k_depth_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaFuncSetAttribute(k_depth_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
-    attr = true;
+    resident = resident_grid(k_depth_pass<true>, OS_THREADS, sm, 1 << 30);
   }
+  const unsigned grid = (unsigned)std::min<int64_t>((M_cap + TILE - 1) / TILE, resident);
   uint32_t *k32[2] = {reinterpret_cast<uint32_t *>(w.key_depth[1]),
                       reinterpret_cast<uint32_t *>(w.key_depth[1]) + M_cap};
   // keys 0: u64 -> k32[0], 1: k32[0] -> k32[1], 2: k32[1] -> k32[0], 3: k32[0] -> k32[1]
@@ -359,7 +378,8 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
         nullptr, k32[a ^ 1], k32[a], w.val_depth[a], w.val_depth[a ^ 1], &fs->stats.M, 8 * p,
         fs->off_depth[p], w.status, fs, TK_DEPTH0 + p);
   }
-  k_depth_ties<<<148 * 4, 256, 0, s>>>(k32[1], w.val_depth[0], w.key_depth[0], w.val_depth[1], fs);
+  const unsigned tgrid = (unsigned)std::min<int64_t>((M_cap + TIE_SEG - 1) / TIE_SEG, 148 * 16);
+  k_depth_ties<<<tgrid, 256, 0, s>>>(k32[1], w.val_depth[0], w.key_depth[0], w.val_depth[1], fs);
   *launches += 5;
 }
 
