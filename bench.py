@@ -472,8 +472,6 @@ def run_lodge(args):
     stats = read_stats(stats_all)
     overflow = sum(s.overflow for s in stats)
     faults = sum(1 for s in stats if s.fault)
-    if faults:
-        print(f"[bench] {faults} frame(s) reported device bounds faults", file=sys.stderr)
     ms_max = ms
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -610,6 +608,10 @@ def run_lodge(args):
             "P_oracle": int(ref["P"]), "M": int(st.M), "M_oracle": int(len(batch["src"])),
             "image_max_abs": err, "psnr_db": (math.inf if mse == 0 else -10 * math.log10(mse))}
 
+    sticky = r.fault_flags()  # every frame of the run, timed or not
+    if faults or sticky:
+        print(f"[bench] device bounds checks fired: {faults} timed frame(s), "
+              f"flags {sticky:#x}", file=sys.stderr)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -633,6 +635,7 @@ def run_lodge(args):
                        "levels": cfg.n_gaussians(), "chunks": cfg.K,
                        "pairs_per_s": P * value, "gaussians_per_s": U * value,
                        "overflow_frames": int(overflow), "fault_frames": int(faults),
+                       "fault_flags": int(sticky),
                        "setup_s": round(setup_s, 1)},
             "e2e": e2e, "gpu_launches": int(launches_per_frame * total_frames),
             "roofline": roofline, "stages": stages, "stage_timing": stage_timing,

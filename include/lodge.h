@@ -245,6 +245,10 @@ int lodge_to_srgb8(lodge_ctx *ctx, const float *image_dev, int64_t n_pixels, uin
 /* Number of kernels the last lodge_render_frame enqueued. */
 int32_t lodge_last_launch_count(lodge_ctx *ctx);
 
+/* OR of the stats.fault bits of every frame this context rendered
+ * (synchronous): 0 unless a device-side bounds check ever fired. */
+int lodge_fault_flags(lodge_ctx *ctx, uint32_t *flags);
+
 /* Compositing work counters of the last frame (synchronous; all zero unless
  * liblodge was built with -DLODGE_COUNTERS): [0] per-warp list entries,
  * [1] warp iterations, [2] iterations with a pixel inside the cut-off,

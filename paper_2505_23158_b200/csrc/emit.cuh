@@ -28,13 +28,15 @@ struct EmitSmem {
 template <int NP>
 __device__ __forceinline__ void emit_stage(EmitSmem<NP> &E, const uint32_t *__restrict__ order,
                                            const Work &w, uint32_t j0, uint32_t j1,
-                                           uint32_t r0, uint32_t r1, uint32_t *fault) {
+                                           uint32_t r0, uint32_t r1, FrameState *fs) {
   constexpr int IT = NP / DUP_THREADS;
   static_assert(NP % DUP_THREADS == 0, "whole pairs per thread");
   uint32_t nr = r1 - r0 + 1;
-  if (r1 < r0 || nr > (uint32_t)NP + 1u) {  // owners have >= 1 pair: nr <= pairs + 1
-    if (threadIdx.x == 0) raise_fault(fault, FAULT_OWNERS);
+  if (r1 < r0 || nr > (uint32_t)NP + 1u || r1 >= (uint32_t)w.M_cap) {
+    // owners have >= 1 pair: nr <= pairs + 1
+    if (threadIdx.x == 0) raise_fault(fs, FAULT_OWNERS);
     nr = 1;
+    r0 = 0;
   }
   const uint32_t npair = j1 - j0;
   for (uint32_t k = threadIdx.x; k < NP; k += DUP_THREADS) E.own[k] = 0;

@@ -30,6 +30,7 @@ struct FrameState {
   uint32_t n_alive;                   // tiles the second phase composites
   uint32_t n_owners_b;                // second-phase splats that meet an alive tile
   uint32_t alive_box[4];              // x0, x1, y0, y1: bounding box of the alive tiles
+  uint32_t fault_sticky;              // OR of every frame's stats.fault (lodge_fault_flags)
   unsigned long long counters[8];     // LODGE_COUNTERS builds: compositing work counters
 };
 
@@ -105,9 +106,12 @@ enum : uint32_t {
   FAULT_OWNERS = 1,   // an emission CTA's owner range exceeds its staging
   FAULT_COMPACT = 2,  // second-phase compaction beyond the pair count
   FAULT_SCATTER = 4,  // a onesweep scatter beyond the key count
+  FAULT_LIST = 8,     // a compositor list range or member beyond its buffer
+  FAULT_TILE = 16,    // an emitted pair's tile beyond the frame
 };
-__device__ __forceinline__ void raise_fault(uint32_t *fault, uint32_t bit) {
-  atomicOr(fault, bit);
+__device__ __forceinline__ void raise_fault(FrameState *fs, uint32_t bit) {
+  atomicOr(&fs->stats.fault, bit);
+  atomicOr(&fs->fault_sticky, bit);
 }
 
 // Status word: [63:32] epoch, [31:30] flag, [29:0] value.

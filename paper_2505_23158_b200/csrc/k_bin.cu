@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_emit(const uint32_t *__rest
     const uint32_t j1 = min(j0 + (uint32_t)EMIT_CHUNK, P);
     uint32_t r0, r1;
     emit_owners(w, j0, j1, P, n_own, r0, r1);
-    emit_stage(E, order, w, j0, j1, r0, r1, &fs->stats.fault);
+    emit_stage(E, order, w, j0, j1, r0, r1, fs);
 #pragma unroll
     for (int it = 0; it < EMIT_ITEMS; ++it) {
       const uint32_t j = j0 + it * DUP_THREADS + threadIdx.x;
@@ -466,14 +466,18 @@ __global__ void __launch_bounds__(DUP_THREADS) k_emit_b(const uint32_t *__restri
   emit_owners(w, j0, j1, Pe, n, r0, r1);
   Work wb = w;  // the compacted owner list of k_dup_count<true>
   wb.rect_sorted = w.rect;
-  emit_stage(E, w.val_depth[1], wb, j0, j1, r0, r1, &fs->stats.fault);  // ends with a barrier
+  emit_stage(E, w.val_depth[1], wb, j0, j1, r0, r1, fs);  // ends with a barrier
   uint64_t key[EMIT_ITEMS];
   uint32_t keep = 0;
 #pragma unroll
   for (int it = 0; it < EMIT_ITEMS; ++it) {
     const uint32_t j = j0 + it * DUP_THREADS + tid;
     key[it] = j < j1 ? emit_pair(E, j, j0, tiles_x) : 0ull;
-    const uint32_t t = (uint32_t)(key[it] >> 32);
+    uint32_t t = (uint32_t)(key[it] >> 32);
+    if (t >= (uint32_t)n_tiles) {
+      raise_fault(fs, FAULT_TILE);
+      t = 0;
+    }
     const bool k = j < j1 && ((s_alive[t >> 5] >> (t & 31)) & 1u);
     keep |= k ? (1u << it) : 0u;
     const uint32_t bal = __ballot_sync(FULL_MASK, k);
@@ -506,7 +510,7 @@ __global__ void __launch_bounds__(DUP_THREADS) k_emit_b(const uint32_t *__restri
     if ((keep >> it) & 1u) {
       const uint32_t o = base + s_cnt[it][warp] + __popc(bal & lanemask_lt());
       if (o < limit) w.pairs[0][o] = key[it];
-      else raise_fault(&fs->stats.fault, FAULT_COMPACT);
+      else raise_fault(fs, FAULT_COMPACT);
     }
   }
   __syncthreads();  // the next chunk restages E and the counters

@@ -29,6 +29,8 @@
 // reference (blocks of 1024 members), so per_pixel_visible and max weights
 // match it to the ulp of exp.
 // Compiled with -fmad=false; the fast path fuses explicitly with fmaf.
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace lodge {
@@ -145,6 +147,7 @@ struct CompParams {
   const uint32_t *count_all;  // pairs per tile over all splats
   uint32_t *alive;            // bitmap of tiles the second phase resumes
   float4 *state;              // (T, r, g, b) per pixel of those tiles
+  uint32_t n_list, n_payload;  // capacities of the list and payload buffers (bounds checks)
 };
 
 // MODE < 0: need_image / record_max from cpar.flags at run time (EXACT);
@@ -189,6 +192,10 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
   const uint32_t s = tile_start[t];
   uint32_t e = tile_start[t + 1];
   if (fs->stats.overflow) e = s;
+  if (e < s || e > cpar.n_list) {
+    if (tid == 0) raise_fault(fs, FAULT_LIST);
+    e = s;
+  }
 
   const float fpx = (float)lx + 0.5f, fpy0 = (float)ly0 + 0.5f;
   const double gx = (double)px + 0.5, gy0 = (double)py0 + 0.5;
@@ -215,7 +222,11 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
     for (int h = 0; h < CB / CT; ++h) {
       const int j = tid + h * CT;
       if (j < n) {
-        const uint32_t m = list[bb + j];
+        uint32_t m = list[bb + j];
+        if (m >= cpar.n_payload) {
+          raise_fault(fs, FAULT_LIST);
+          m = 0;
+        }
         S.m[k][j] = m;
         bulk_g2s(&S.pl[k][j], payload + m, 64, &S.bar[k]);
         if (EXACT) bulk_g2s(&S.pr[k][j], precise + m, 64, &S.bar[k]);
@@ -665,6 +676,8 @@ static void launch_comp(const Work &w, FrameState *fs, int32_t W, int32_t H,
   cp.count_all = w.count_all;
   cp.alive = w.alive;
   cp.state = w.state;
+  cp.n_list = (uint32_t)std::min<int64_t>(2 * w.P_cap, 0xffffffffll);
+  cp.n_payload = (uint32_t)w.M_cap;
   k_composite<EXACT, MODE, PH><<<T, CC<EXACT>::CT, sm, s>>>(
       w.list, PH == 2 ? w.tile_start_b : w.tile_start, PH == 2 ? w.tile_order_b : w.tile_order,
       w.payload, w.precise, fs, cp, out.image_dev, out.visible_dev, out.maxw_dev);

@@ -402,6 +402,9 @@ struct ProjLevels {
 // all U inputs orders the M survivors by (depth, g) -- exactly
 // np.lexsort((source_index, depth)) -- and leaves the culled ones after them.
 template <typename GT, typename ST>
+#ifndef LODGE_PROJ_SHPF
+#define LODGE_PROJ_SHPF 0  // L2 prefetch of the SH record before the projection math
+#endif
 #ifndef LODGE_PROJ_MINB
 #define LODGE_PROJ_MINB 2  // resident CTAs per SM (the persistent grid's size)
 #endif
@@ -454,6 +457,15 @@ __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLeve
         gp = reinterpret_cast<const GT *>(lv.slab_geom[e]);
         sp = reinterpret_cast<const ST *>(lv.slab_sh[e]);
       }
+#if LODGE_PROJ_SHPF
+      if (shade) {  // the SH record travels to L2 while the projection computes
+        const int deg = lv.degree[l];
+        const char *sb = reinterpret_cast<const char *>(sp + (size_t)gidx * 3 * (deg + 1) * (deg + 1));
+        const int bytes = 3 * (deg + 1) * (deg + 1) * (int)sizeof(ST);
+        for (int o = 0; o < bytes; o += 64)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(sb + o));
+      }
+#endif
       load_geom<GT>(gp + (size_t)gidx * 12, v);
       if (lv.qnorm[l]) normalize_rot(v);
       p = project_core(v, cam, rp, mod, true);

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(OS_THREADS, VALS ? LODGE_OS_VMINB
   onesweep_partition<OS_ITEMS, NB, VALS>(S, k, vmask, part, cnt, shift, digit_off, status,
                                          fs->epoch + tk, kout, kmap, vout,
                                          [&](uint32_t li) { return vin[base + li]; },
-                                         DROP ? fs->stats.M : n, &fs->stats.fault);
+                                         DROP ? fs->stats.M : n, fs);
   __syncthreads();  // the next partition reuses the shared memory
   }
 }
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(OS_THREADS, LODGE_OS_VMINB)
   onesweep_partition<IT, 8, true>(S, k, vmask, part, cnt, shift, digit_off, status,
                                   fs->epoch + tk, kout, [](uint32_t key) { return key; }, vout,
                                   [&](uint32_t li) { return vin[base + li]; },
-                                  FIRST ? fs->stats.M : n, &fs->stats.fault);
+                                  FIRST ? fs->stats.M : n, fs);
   __syncthreads();
   }
 }

@@ -687,6 +687,15 @@ int lodge_to_srgb8(lodge_ctx *c, const float *img, int64_t n, uint8_t *out) {
 
 int32_t lodge_last_launch_count(lodge_ctx *c) { return c ? c->launches : 0; }
 
+int lodge_fault_flags(lodge_ctx *c, uint32_t *flags) {
+  if (!c || !flags) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(flags, reinterpret_cast<const char *>(c->fs) + offsetof(FrameState, fault_sticky),
+                sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
 int lodge_debug_counters(lodge_ctx *c, uint64_t *out8) {
   if (!c || !out8) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
   CK(cudaStreamSynchronize(c->stream));

@@ -73,7 +73,7 @@ __device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI, (1 << 
                                                    uint64_t *status, uint32_t epoch,
                                                    KO *__restrict__ kout, KMap kmap,
                                                    uint32_t *__restrict__ vout, VGet vget,
-                                                   uint32_t n_out, uint32_t *fault) {
+                                                   uint32_t n_out, FrameState *fs) {
   static_assert(ITEMS % 2 == 0, "two ranking chains");
   static_assert(NB >= 1 && NB <= 8, "digit of 1..8 bits");
   constexpr int H = ITEMS / 2;
@@ -187,7 +187,7 @@ __device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI, (1 << 
     const uint32_t dd = (uint32_t)((key >> shift) & DM);
     const uint32_t out = S.gbase[dd] + (j - S.dstart[dd]);
     if (out >= n_out) {  // digit offsets inconsistent with the keys
-      raise_fault(fault, FAULT_SCATTER);
+      raise_fault(fs, FAULT_SCATTER);
       continue;
     }
     kout[out] = kmap(key);

@@ -231,6 +231,16 @@ class Renderer:
                                        frame.width * frame.height, ptr(out)), "lodge_to_srgb8")
         return out
 
+    def fault_flags(self) -> int:
+        """OR over every frame of every slot of the device bounds-check bits
+        (0 = no check ever fired); synchronises the slots."""
+        f = 0
+        for ctx, _ in self._slots:
+            v = C.c_uint32()
+            N.check(N.lib().lodge_fault_flags(ctx.ptr, C.byref(v)), "lodge_fault_flags")
+            f |= v.value
+        return f
+
     def last_launch_count(self) -> int:
         return int(N.lib().lodge_last_launch_count(self.ctx.ptr))
 
