@@ -498,7 +498,8 @@ def run_lodge(args):
         gbs = sb[name] / (per / 1000.0) / 1e9 if per > 0 else 0.0
         stages[name] = {"ms_per_frame": round(per, 5), "bytes_per_frame": round(sb[name]),
                         "GB_s": round(gbs, 1), "frac": round(gbs / peak, 4)}
-    hbm_stages = ["union", "project", "depth_sort", "duplicate", "tile_sort", "second_phase"]
+    # second_phase mixes a sort with compositing: reported under stages only
+    hbm_stages = ["union", "project", "depth_sort", "duplicate", "tile_sort"]
     dom = max(N.STAGES, key=lambda k: stages[k]["ms_per_frame"])
     dom_hbm = max(hbm_stages, key=lambda k: stages[k]["ms_per_frame"])
     rf_stage = dom if dom in hbm_stages else dom_hbm

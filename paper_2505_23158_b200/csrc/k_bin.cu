@@ -438,16 +438,24 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_emit(const uint32_t *__rest
 }
 
 // Second phase of a two-phase frame: the enumerated pairs of the owner list
-// of k_dup_count<true> (EMIT_CHUNK per CTA, as k_dup_emit), keeping those whose tile
+// of k_dup_count<true> (EB_CHUNK per CTA step, as k_dup_emit), keeping those whose tile
 // is alive, compacted in order (block scan + decoupled look-back over CTAs
 // taken in ticket order), so each alive tile receives, in depth order, its
 // pairs beyond the first phase.
+#ifndef LODGE_EMITB_CHUNK
+#define LODGE_EMITB_CHUNK 4096  // enumerated pairs per CTA step (a multiple of EMIT_CHUNK)
+#endif
+constexpr int EB_CHUNK = LODGE_EMITB_CHUNK;
+constexpr int EB_ITEMS = EB_CHUNK / DUP_THREADS;
+static_assert(EB_CHUNK % EMIT_CHUNK == 0 && EB_ITEMS <= 32, "whole splitter chunks, <= 32 rounds");
+
 __global__ void __launch_bounds__(DUP_THREADS) k_emit_b(const uint32_t *__restrict__ order,
                                                         int32_t tiles_x, int32_t n_tiles,
                                                         Work w, FrameState *fs) {
-  __shared__ EmitSmem<EMIT_CHUNK> E;
+  extern __shared__ __align__(16) uint8_t eb_smem[];
+  EmitSmem<EB_CHUNK> &E = *reinterpret_cast<EmitSmem<EB_CHUNK> *>(eb_smem);
   __shared__ uint32_t s_alive[2048];  // T <= 65536 (check_tile_smem)
-  __shared__ uint32_t s_cnt[EMIT_ITEMS][DUP_THREADS / 32];
+  __shared__ uint32_t s_cnt[EB_ITEMS][DUP_THREADS / 32];
   __shared__ uint32_t s_part, s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t n = fs->stats.overflow ? 0u : fs->n_owners_b;
@@ -459,18 +467,18 @@ __global__ void __launch_bounds__(DUP_THREADS) k_emit_b(const uint32_t *__restri
   if (tid == 0) s_part = atomicAdd(&fs->tickets[TK_EMITB], 1u);
   __syncthreads();
   const uint32_t part = s_part;
-  const uint32_t j0 = part * EMIT_CHUNK;
+  const uint32_t j0 = part * EB_CHUNK;
   if (j0 >= Pe) break;
-  const uint32_t j1 = min(j0 + (uint32_t)EMIT_CHUNK, Pe);
+  const uint32_t j1 = min(j0 + (uint32_t)EB_CHUNK, Pe);
   uint32_t r0, r1;
   emit_owners(w, j0, j1, Pe, n, r0, r1);
   Work wb = w;  // the compacted owner list of k_dup_count<true>
   wb.rect_sorted = w.rect;
   emit_stage(E, w.val_depth[1], wb, j0, j1, r0, r1, fs);  // ends with a barrier
-  uint64_t key[EMIT_ITEMS];
+  uint64_t key[EB_ITEMS];
   uint32_t keep = 0;
 #pragma unroll
-  for (int it = 0; it < EMIT_ITEMS; ++it) {
+  for (int it = 0; it < EB_ITEMS; ++it) {
     const uint32_t j = j0 + it * DUP_THREADS + tid;
     key[it] = j < j1 ? emit_pair(E, j, j0, tiles_x) : 0ull;
     uint32_t t = (uint32_t)(key[it] >> 32);
@@ -485,9 +493,9 @@ __global__ void __launch_bounds__(DUP_THREADS) k_emit_b(const uint32_t *__restri
   }
   __syncthreads();
   if (warp == 0) {  // exclusive offsets over (round, warp), then the look-back
-    uint32_t v[EMIT_ITEMS], tot = 0;
+    uint32_t v[EB_ITEMS], tot = 0;
 #pragma unroll
-    for (int it = 0; it < EMIT_ITEMS; ++it) {
+    for (int it = 0; it < EB_ITEMS; ++it) {
       v[it] = lane < DUP_THREADS / 32 ? s_cnt[it][lane] : 0u;
       uint32_t inc = v[it];
 #pragma unroll
@@ -505,7 +513,7 @@ __global__ void __launch_bounds__(DUP_THREADS) k_emit_b(const uint32_t *__restri
   const uint32_t base = s_base;
   const uint32_t limit = fs->n_pairs;  // the second phase's pair total (k_setup_b)
 #pragma unroll
-  for (int it = 0; it < EMIT_ITEMS; ++it) {
+  for (int it = 0; it < EB_ITEMS; ++it) {
     const uint32_t bal = __ballot_sync(FULL_MASK, (keep >> it) & 1u);
     if ((keep >> it) & 1u) {
       const uint32_t o = base + s_cnt[it][warp] + __popc(bal & lanemask_lt());
@@ -589,10 +597,18 @@ void launch_enum_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles
   k_dup_count<true><<<grid, DUP_THREADS, 0, s>>>(w.val_depth[0], w.rect, w, fs, 0u, tiles_x,
                                                  chunk_cap(w));
   static int64_t resident = 0;
-  if (!resident) resident = resident_ctas(k_emit_b, DUP_THREADS);
+  constexpr size_t sm = sizeof(EmitSmem<EB_CHUNK>);
+  if (!resident) {
+    cudaFuncSetAttribute(k_emit_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_emit_b, DUP_THREADS, sm);
+    resident = (int64_t)std::max(per, 1) * std::max(sms, 1);
+  }
   const unsigned egrid =
-      (unsigned)std::min<int64_t>((w.P_cap + EMIT_CHUNK - 1) / EMIT_CHUNK, resident);
-  k_emit_b<<<egrid, DUP_THREADS, 0, s>>>(w.val_depth[0], tiles_x, tiles_x * tiles_y, w, fs);
+      (unsigned)std::min<int64_t>((w.P_cap + EB_CHUNK - 1) / EB_CHUNK, resident);
+  k_emit_b<<<egrid, DUP_THREADS, sm, s>>>(w.val_depth[0], tiles_x, tiles_x * tiles_y, w, fs);
 }
 
 }  // namespace lodge
