@@ -22,7 +22,7 @@ def main(path, title="launch list"):
             v * 1000.0 if unit in ("ms", "msecond") else v)
         n, t = agg.get(name, (0, 0.0))
         agg[name] = (n + 1, t + us)
-    frames = max(1, agg.get("k_begin_frame", (1, 0))[0])
+    frames = max(1, sum(n for k, (n, _) in agg.items() if k.endswith("k_begin_frame")))
     total = sum(t for _, t in agg.values())
     out = [f"# {title}", "",
            "Per-launch times are cold-cache and serialised under ncu: compare shares, not",
