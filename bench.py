@@ -168,7 +168,8 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # algorithmic bytes per stage
 # ---------------------------------------------------------------------------
-def stage_bytes(U, AB, M, P, W, H, sh_terms, geom_bytes=48, sh_elem=4, P1=None, P2=0.0):
+def stage_bytes(U, AB, M, P, W, H, sh_terms, geom_bytes=48, sh_elem=4, P1=None, P2=0.0,
+                M1=None, M2=0.0):
     """Algorithmic bytes per frame of each stage.
     Two-phase frames (P1 = pairs of the first depth phase < P): tile_setup is
     the counting pass, duplicate / tile_sort / composite the first phase,
@@ -177,20 +178,25 @@ def stage_bytes(U, AB, M, P, W, H, sh_terms, geom_bytes=48, sh_elem=4, P1=None, 
     sh_b = 3 * sh_terms * sh_elem
     two = P1 is not None and (P1 < P or P2 > 0)
     P1 = P if P1 is None else P1
+    M1 = M if (M1 is None or not two) else M1
     count = M * (4.0 + 8.0 + 8.0 + 4.0)  # order + rect in, rect + offset out
+    # k_payload: id, geometry and SH in, payload + fp64 record out, per
+    # composited splat
+    payload = 4.0 + 8.0 + geom_bytes + sh_b + 128.0
     return {
         "select": 0.0,
         "union": 4.0 * AB + 5.0 * U,
-        "project": U * (5.0 + geom_bytes) + M * (sh_b + 8 + 4 + 8 + 64 + 64),
+        # geometry only: union slot + record in, key + index + rectangle out
+        "project": U * (5.0 + geom_bytes + 12.0) + M * 8.0,
         # 32-bit keys: histogram (8 B/input), first pass (u64 key + index in,
         # u32 key + index out), three u32 key + index passes, tie scan
         "depth_sort": U * (8.0 + 12.0) + M * 8.0 + 3 * M * 16.0 + M * 4.0,
-        "tile_setup": count if two else 0.0,
+        "tile_setup": (count if two else 0.0) + M1 * payload,
         "duplicate": P1 * 8.0 if two else M * 12.0 + P * 8.0,
         # pass 1 reads u64 pairs, writes packed u32; pass 2 reads and writes u32
         "tile_sort": (8.0 + 4.0 + 4.0 + 4.0) * P1,
         "composite": P1 * 4.0 + M * 64.0 + W * H * 16.0 + U * 4.0,
-        "second_phase": (M * 8.0 + P2 * (8.0 + 20.0 + 4.0)) if two else 0.0,
+        "second_phase": (M * 8.0 + M2 * payload + P2 * (8.0 + 20.0 + 4.0)) if two else 0.0,
     }
 
 
@@ -490,7 +496,9 @@ def run_lodge(args):
     AB = np.mean([set_total(s.f) + set_total(s.o) for s in stats])
     P1 = np.mean([s.P_first for s in stats])
     P2 = np.mean([s.P_second for s in stats])
-    sb = stage_bytes(U, AB, M, P, W, H, (cfg.degree + 1) ** 2, P1=P1, P2=P2)
+    M1 = np.mean([s.M_first for s in stats])
+    M2 = np.mean([s.M_second for s in stats])
+    sb = stage_bytes(U, AB, M, P, W, H, (cfg.degree + 1) ** 2, P1=P1, P2=P2, M1=M1, M2=M2)
     peak, peak_kind = load_peaks()
     stages = {}
     for i, name in enumerate(N.STAGES):
@@ -633,6 +641,7 @@ def run_lodge(args):
                              " >> 126 MB L2; no explicit flush",
                        "mean_U": round(U), "mean_M": round(M), "mean_P": round(P),
                        "mean_P_sorted": [round(P1), round(P2)],
+                       "mean_M_composited": [round(M1), round(M2)],
                        "levels": cfg.n_gaussians(), "chunks": cfg.K,
                        "pairs_per_s": P * value, "gaussians_per_s": U * value,
                        "overflow_frames": int(overflow), "fault_frames": int(faults),

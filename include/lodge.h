@@ -134,6 +134,8 @@ typedef struct {
   uint32_t P_second;     /* pairs sorted in the second phase (two-phase frames) */
   uint32_t fault;        /* nonzero: a device-side bounds check fired (one bit per
                             site, internal.cuh FAULT_*); the frame's outputs are invalid */
+  uint32_t M_first;      /* two-phase frames: splats of the first phase */
+  uint32_t M_second;     /* two-phase frames: later splats that meet an unfinished tile */
 } lodge_frame_stats;
 
 /* ---- context ---------------------------------------------------------- */

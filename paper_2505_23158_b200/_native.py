@@ -66,7 +66,8 @@ class FrameStats(C.Structure):
     _fields_ = [("f", C.c_int32), ("o", C.c_int32), ("t_bar", C.c_double), ("t", C.c_double),
                 ("U", C.c_uint32), ("U_level", C.c_uint32 * MAX_LEVELS), ("M", C.c_uint32),
                 ("P", C.c_uint32), ("overflow", C.c_uint32), ("guard_hits", C.c_uint32),
-                ("P_first", C.c_uint32), ("P_second", C.c_uint32), ("fault", C.c_uint32)]
+                ("P_first", C.c_uint32), ("P_second", C.c_uint32), ("fault", C.c_uint32),
+                ("M_first", C.c_uint32), ("M_second", C.c_uint32)]
 
 
 class Batch(C.Structure):

@@ -265,6 +265,13 @@ int launch_project_frame(const lodge_level *levels, const LevelSlots &ls, const 
                          cudaStream_t s,
                          const void *const *slab_geom = nullptr,
                          const void *const *slab_sh = nullptr);
+// Compositing records of the splats ids[0 .. *n_ptr) (concatenated indices
+// g), n_cap an upper bound of *n_ptr for the grid.
+int launch_payload(const lodge_level *levels, const LevelSlots &ls, const Work &w,
+                   FrameState *fs, const lodge_camera *cam_dev, const lodge_raster_params &rp,
+                   int32_t shade, const uint32_t *ids, const uint32_t *n_ptr, int64_t n_cap,
+                   cudaStream_t s, const void *const *slab_geom = nullptr,
+                   const void *const *slab_sh = nullptr);
 int launch_project_compat(const lodge_level &level, const int64_t *idx, int64_t n,
                           const double *mod, const Work &w, FrameState *fs,
                           const lodge_camera *cam_dev, const lodge_raster_params &rp,

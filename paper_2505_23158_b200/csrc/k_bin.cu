@@ -392,13 +392,17 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
     if (valid && r == n - 1) {  // totals: owners and pairs
       const uint32_t nq = SECOND ? k + (c[i] ? 1u : 0u) : n;
       w.splat_off[nq] = off + c[i];
-      if (SECOND) fs->n_owners_b = nq;
+      if (SECOND) {
+        fs->n_owners_b = nq;
+        fs->stats.M_second = nq;
+      }
     }
     if (!SECOND && budget) {  // whole warp: the difference-array update is collective
       const bool first = valid && off < budget;
       add_tile_diff(w.tile_diff_a, rc[i], tiles_x, first);
       if (first && (off + c[i] >= budget || r == n - 1)) {
         fs->split_S = r + 1;
+        fs->stats.M_first = r + 1;
         fs->P_A = off + c[i];
       }
     }

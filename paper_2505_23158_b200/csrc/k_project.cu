@@ -14,6 +14,8 @@
 // (_tile_ranges) and src/lod.py:216-227 (project_selection, level-major).
 #include <type_traits>
 
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace lodge {
@@ -396,41 +398,77 @@ struct ProjLevels {
   const void *const *slab_sh;
 };
 
-// Outputs are written at the dense concatenated input index g (level-major
-// union position, the reference's Splat2DBatch.concat source index), with no
-// compaction: culled inputs get depth key ~0, so the stable depth sort over
-// all U inputs orders the M survivors by (depth, g) -- exactly
-// np.lexsort((source_index, depth)) -- and leaves the culled ones after them.
+// Shared per-CTA frame context of the frame kernels (camera, blend factor,
+// chunk pair, per-level concatenated offsets and sizes).
+struct FrameCtx {
+  lodge_camera cam;
+  double t;
+  int32_t f, o;
+  uint32_t used[LODGE_MAX_LEVELS], cat[LODGE_MAX_LEVELS];
+};
+
+__device__ __forceinline__ void stage_frame_ctx(FrameCtx &F, const ProjLevels &lv,
+                                                const FrameState *fs,
+                                                const lodge_camera *__restrict__ cam_p) {
+  if (threadIdx.x == 0) {
+    F.cam = *cam_p;
+    F.t = fs->stats.t;
+    F.f = fs->stats.f;
+    F.o = fs->stats.o < 0 ? fs->stats.f : fs->stats.o;
+    uint32_t c = 0;
+    for (int k = 0; k < lv.L; ++k) {
+      F.cat[k] = c;  // concatenated index offset of level k
+      F.used[k] = fs->stats.U_level[k];
+      c += F.used[k];
+    }
+  }
+  __syncthreads();
+}
+
+// The record of union slot `slot` of level l: geometry loaded (rotation
+// normalised if the level asks), modulation from the blend tag, SH pointer
+// and record index for the colour.  Shared by the projection and the
+// payload kernel, so both evaluate the identical fp64 projection.
 template <typename GT, typename ST>
-#ifndef LODGE_PROJ_SHPF
-#define LODGE_PROJ_SHPF 0  // L2 prefetch of the SH record before the projection math
-#endif
+__device__ __forceinline__ Proj slot_project(const ProjLevels &lv, const Work &w,
+                                             const FrameCtx &F, const lodge_raster_params &rp,
+                                             int l, uint32_t slot, double v[12],
+                                             const ST *&sp, uint32_t &gidx) {
+  const GT *gp = reinterpret_cast<const GT *>(lv.geom[l]);
+  sp = reinterpret_cast<const ST *>(lv.sh[l]);
+  gidx = w.union_idx[slot];
+  const uint8_t tag = w.union_tag[slot];
+  const double mod = (tag == 3) ? 1.0 : (tag == 1 ? F.t : 1.0 - F.t);
+  if (lv.slab_geom) {  // tag 3 / 1: the primary chunk's slab, 2: the other's
+    const int32_t e = ((tag == 2) ? F.o : F.f) * lv.L + l;
+    gp = reinterpret_cast<const GT *>(lv.slab_geom[e]);
+    sp = reinterpret_cast<const ST *>(lv.slab_sh[e]);
+  }
+  load_geom<GT>(gp + (size_t)gidx * 12, v);
+  if (lv.qnorm[l]) normalize_rot(v);
+  return project_core(v, F.cam, rp, mod, true);
+}
+
+// K2, geometry only.  Outputs are written at the dense concatenated input
+// index g (level-major union position, the reference's Splat2DBatch.concat
+// source index), with no compaction: culled inputs get depth key ~0, so the
+// stable depth sort over all U inputs orders the M survivors by (depth, g)
+// -- exactly np.lexsort((source_index, depth)) -- and leaves the culled ones
+// after them.  Colour and the compositing records are left to k_payload,
+// which runs only for the splats a frame composites (a few percent of M on
+// the bench sweep: the tiles finish early).
+template <typename GT, typename ST>
 #ifndef LODGE_PROJ_MINB
 #define LODGE_PROJ_MINB 2  // resident CTAs per SM (the persistent grid's size)
 #endif
 __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLevels lv, Work w, FrameState *fs,
                                                        const lodge_camera *__restrict__ cam_p,
-                                                       lodge_raster_params rp, int32_t shade) {
+                                                       lodge_raster_params rp) {
   // persistent CTAs (grid-stride over the slots): the camera and the level
   // table are staged once per CTA
-  __shared__ lodge_camera cam;
-  __shared__ uint32_t s_used[LODGE_MAX_LEVELS], s_cat[LODGE_MAX_LEVELS];
-  __shared__ double s_t;
-  __shared__ int32_t s_f, s_o;
-  if (threadIdx.x == 0) {
-    cam = *cam_p;
-    s_t = fs->stats.t;
-    s_f = fs->stats.f;
-    s_o = fs->stats.o < 0 ? fs->stats.f : fs->stats.o;
-    uint32_t c = 0;
-    for (int k = 0; k < lv.L; ++k) {
-      s_cat[k] = c;  // concatenated index offset of level k
-      s_used[k] = fs->stats.U_level[k];
-      c += s_used[k];
-    }
-  }
-  __syncthreads();
-  const int32_t tiles_x = (cam.w + 15) / 16, tiles_y = (cam.h + 15) / 16;
+  __shared__ FrameCtx F;
+  stage_frame_ctx(F, lv, fs, cam_p);
+  const int32_t tiles_x = (F.cam.w + 15) / 16, tiles_y = (F.cam.h + 15) / 16;
   const uint32_t nslots = lv.slot_base[lv.L];
   uint32_t nkeep_cta = 0;  // survivors seen by this thread's warp (lane 0 counts)
   for (uint32_t base = blockIdx.x * blockDim.x; base < nslots; base += gridDim.x * blockDim.x) {
@@ -439,36 +477,15 @@ __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLeve
     int l = 0;
     while (l + 1 < lv.L && slot >= lv.slot_base[l + 1]) ++l;
     const uint32_t pos = slot - lv.slot_base[l];
-    const bool valid = slot < nslots && pos < s_used[l];
-    const uint32_t g = s_cat[l] + pos;
+    const bool valid = slot < nslots && pos < F.used[l];
+    const uint32_t g = F.cat[l] + pos;
     Proj p;
     p.ok = false;
-    double v[12];
-    uint32_t gidx = 0;
-    const GT *gp = reinterpret_cast<const GT *>(lv.geom[l]);
-    const ST *sp = reinterpret_cast<const ST *>(lv.sh[l]);
     if (valid) {
-      gidx = w.union_idx[slot];
-      const uint8_t tag = w.union_tag[slot];
-      const double t = s_t;
-      const double mod = (tag == 3) ? 1.0 : (tag == 1 ? t : 1.0 - t);
-      if (lv.slab_geom) {  // tag 3 / 1: the primary chunk's slab, 2: the other's
-        const int32_t e = ((tag == 2) ? s_o : s_f) * lv.L + l;
-        gp = reinterpret_cast<const GT *>(lv.slab_geom[e]);
-        sp = reinterpret_cast<const ST *>(lv.slab_sh[e]);
-      }
-#if LODGE_PROJ_SHPF
-      if (shade) {  // the SH record travels to L2 while the projection computes
-        const int deg = lv.degree[l];
-        const char *sb = reinterpret_cast<const char *>(sp + (size_t)gidx * 3 * (deg + 1) * (deg + 1));
-        const int bytes = 3 * (deg + 1) * (deg + 1) * (int)sizeof(ST);
-        for (int o = 0; o < bytes; o += 64)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(sb + o));
-      }
-#endif
-      load_geom<GT>(gp + (size_t)gidx * 12, v);
-      if (lv.qnorm[l]) normalize_rot(v);
-      p = project_core(v, cam, rp, mod, true);
+      double v[12];
+      const ST *sp;
+      uint32_t gidx;
+      p = slot_project<GT, ST>(lv, w, F, rp, l, slot, v, sp, gidx);
     }
     const bool keep = valid && p.ok;
     nkeep_cta += __popc(__ballot_sync(FULL_MASK, keep));
@@ -476,28 +493,51 @@ __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLeve
     add_tile_diff(w.tile_diff, rc, tiles_x, keep);
     if (!valid) continue;
     w.val_depth[0][g] = g;
-    if (!keep) {
-      w.key_depth[0][g] = ~0ull;
-      continue;
-    }
-    const uint64_t m = g;
+    w.key_depth[0][g] = keep ? (uint64_t)__double_as_longlong(p.z) : ~0ull;
+    if (keep) w.rect[g] = rc;
+  }
+  if ((threadIdx.x & 31) == 0 && nkeep_cta) atomicAdd(&fs->stats.M, nkeep_cta);
+}
+
+// Compositing records (payload + fp64 record, colour from the SH) of the
+// splats ids[0 .. *n): concatenated indices g of survivors.  The projection
+// is re-evaluated from the same record with the same code as K2, so every
+// field is bit-identical to an eager evaluation.
+#ifndef LODGE_PAYLOAD_MINB
+#define LODGE_PAYLOAD_MINB 3  // resident CTAs per SM (register cap)
+#endif
+template <typename GT, typename ST>
+__global__ void __launch_bounds__(256, LODGE_PAYLOAD_MINB) k_payload(ProjLevels lv, Work w, FrameState *fs,
+                                                 const lodge_camera *__restrict__ cam_p,
+                                                 lodge_raster_params rp, int32_t shade,
+                                                 const uint32_t *__restrict__ ids,
+                                                 const uint32_t *n_ptr) {
+  __shared__ FrameCtx F;
+  stage_frame_ctx(F, lv, fs, cam_p);
+  const uint32_t n = fs->stats.overflow ? 0u : *n_ptr;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t g = ids[i];
+    int l = 0;
+    while (l + 1 < lv.L && g >= F.cat[l + 1]) ++l;
+    const uint32_t slot = lv.slot_base[l] + (g - F.cat[l]);
+    double v[12];
+    const ST *sp;
+    uint32_t gidx;
+    const Proj p = slot_project<GT, ST>(lv, w, F, rp, l, slot, v, sp, gidx);
     double rgb[3] = {0.0, 0.0, 0.0};
     if (shade) {
       const int deg = lv.degree[l];
       const int terms = (deg + 1) * (deg + 1);
-      eval_sh_dev<ST>(sp + (size_t)gidx * 3 * terms, terms, deg, v, cam, rgb);
+      eval_sh_dev<ST>(sp + (size_t)gidx * 3 * terms, terms, deg, v, F.cam, rgb);
     }
     const double inv_det = 1.0 / p.det;
     const double A = p.c11 * inv_det, B = (-p.c01) * inv_det, C = p.c00 * inv_det;
     Payload pl;
     Precise pr;
     make_payload(p.mx, p.my, A, B, C, p.op, rgb, g, p.ex, p.ey, rp, pl, pr);
-    w.payload[m] = pl;
-    w.precise[m] = pr;
-    w.rect[m] = rc;
-    w.key_depth[0][m] = (uint64_t)__double_as_longlong(p.z);
+    w.payload[g] = pl;
+    w.precise[g] = pr;
   }
-  if ((threadIdx.x & 31) == 0 && nkeep_cta) atomicAdd(&fs->stats.M, nkeep_cta);
 }
 
 // ---------------------------------------------------------------------------
@@ -647,26 +687,37 @@ __global__ void __launch_bounds__(256) k_import_batch(lodge_batch b, int64_t M, 
   }
 }
 
-template <typename GT, typename ST>
-static void launch_pf(const ProjLevels &lv, const Work &w, FrameState *fs,
-                      const lodge_camera *cam, const lodge_raster_params &rp, int32_t shade,
-                      uint32_t nslots, cudaStream_t s) {
-  static int sms = 0;
-  if (!sms) {
+static int g_sms = 0;
+static int sm_count() {
+  if (!g_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
   }
-  const uint32_t want = (nslots + 255) / 256, cap = LODGE_PROJ_MINB * (uint32_t)sms;
-  k_project_frame<GT, ST><<<want < cap ? want : cap, 256, 0, s>>>(lv, w, fs, cam, rp, shade);
+  return g_sms;
 }
 
-int launch_project_frame(const lodge_level *levels, const LevelSlots &ls, const Work &w,
-                         FrameState *fs, const lodge_camera *cam_dev,
-                         const lodge_raster_params &rp, int32_t shade, int32_t, cudaStream_t s,
-                         const void *const *slab_geom, const void *const *slab_sh) {
-  ProjLevels lv;
+template <typename GT, typename ST>
+static void launch_pf(const ProjLevels &lv, const Work &w, FrameState *fs,
+                      const lodge_camera *cam, const lodge_raster_params &rp, uint32_t nslots,
+                      cudaStream_t s) {
+  const uint32_t want = (nslots + 255) / 256, cap = LODGE_PROJ_MINB * (uint32_t)sm_count();
+  k_project_frame<GT, ST><<<want < cap ? want : cap, 256, 0, s>>>(lv, w, fs, cam, rp);
+}
+
+template <typename GT, typename ST>
+static void launch_pl(const ProjLevels &lv, const Work &w, FrameState *fs,
+                      const lodge_camera *cam, const lodge_raster_params &rp, int32_t shade,
+                      const uint32_t *ids, const uint32_t *n_ptr, int64_t n_cap, cudaStream_t s) {
+  const int64_t want = (n_cap + 255) / 256, cap = 4 * (int64_t)sm_count();
+  k_payload<GT, ST><<<(unsigned)std::max<int64_t>(1, std::min(want, cap)), 256, 0, s>>>(
+      lv, w, fs, cam, rp, shade, ids, n_ptr);
+}
+
+static int proj_levels(const lodge_level *levels, const LevelSlots &ls,
+                       const void *const *slab_geom, const void *const *slab_sh, ProjLevels &lv,
+                       bool &g32, bool &s32) {
   lv.L = ls.n_levels;
   lv.slab_geom = slab_geom;
   lv.slab_sh = slab_sh;
@@ -680,13 +731,39 @@ int launch_project_frame(const lodge_level *levels, const LevelSlots &ls, const 
     lv.qnorm[l] = (levels[l].flags & LODGE_GEOM_QNORM) ? 1 : 0;
   }
   for (int l = 0; l <= LODGE_MAX_LEVELS; ++l) lv.slot_base[l] = l <= lv.L ? ls.slot_base[l] : 0;
+  g32 = fl & LODGE_GEOM_FP32;
+  s32 = fl & LODGE_SH_FP32;
+  return 0;
+}
+
+int launch_project_frame(const lodge_level *levels, const LevelSlots &ls, const Work &w,
+                         FrameState *fs, const lodge_camera *cam_dev,
+                         const lodge_raster_params &rp, int32_t, int32_t, cudaStream_t s,
+                         const void *const *slab_geom, const void *const *slab_sh) {
+  ProjLevels lv;
+  bool g32, s32;
+  if (proj_levels(levels, ls, slab_geom, slab_sh, lv, g32, s32)) return -1;
   const uint32_t nslots = ls.slot_base[lv.L];
   if (nslots == 0) return 0;
-  const bool g32 = fl & LODGE_GEOM_FP32, s32 = fl & LODGE_SH_FP32;
-  if (g32 && s32) launch_pf<float, float>(lv, w, fs, cam_dev, rp, shade, nslots, s);
-  else if (g32) launch_pf<float, double>(lv, w, fs, cam_dev, rp, shade, nslots, s);
-  else if (s32) launch_pf<double, float>(lv, w, fs, cam_dev, rp, shade, nslots, s);
-  else launch_pf<double, double>(lv, w, fs, cam_dev, rp, shade, nslots, s);
+  if (g32 && s32) launch_pf<float, float>(lv, w, fs, cam_dev, rp, nslots, s);
+  else if (g32) launch_pf<float, double>(lv, w, fs, cam_dev, rp, nslots, s);
+  else if (s32) launch_pf<double, float>(lv, w, fs, cam_dev, rp, nslots, s);
+  else launch_pf<double, double>(lv, w, fs, cam_dev, rp, nslots, s);
+  return 0;
+}
+
+int launch_payload(const lodge_level *levels, const LevelSlots &ls, const Work &w,
+                   FrameState *fs, const lodge_camera *cam_dev, const lodge_raster_params &rp,
+                   int32_t shade, const uint32_t *ids, const uint32_t *n_ptr, int64_t n_cap,
+                   cudaStream_t s, const void *const *slab_geom, const void *const *slab_sh) {
+  ProjLevels lv;
+  bool g32, s32;
+  if (proj_levels(levels, ls, slab_geom, slab_sh, lv, g32, s32)) return -1;
+  if (n_cap <= 0) return 0;
+  if (g32 && s32) launch_pl<float, float>(lv, w, fs, cam_dev, rp, shade, ids, n_ptr, n_cap, s);
+  else if (g32) launch_pl<float, double>(lv, w, fs, cam_dev, rp, shade, ids, n_ptr, n_cap, s);
+  else if (s32) launch_pl<double, float>(lv, w, fs, cam_dev, rp, shade, ids, n_ptr, n_cap, s);
+  else launch_pl<double, double>(lv, w, fs, cam_dev, rp, shade, ids, n_ptr, n_cap, s);
   return 0;
 }
 

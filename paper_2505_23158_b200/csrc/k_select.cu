@@ -492,6 +492,8 @@ __global__ void k_begin_frame(FrameState *fs) {
     fs->stats.P_first = 0;
     fs->stats.P_second = 0;
     fs->stats.fault = 0;
+    fs->stats.M_first = 0;
+    fs->stats.M_second = 0;
     fs->split_S = 0;
     fs->P_A = 0;
     fs->n_alive = 0;

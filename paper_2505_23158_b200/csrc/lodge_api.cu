@@ -472,9 +472,11 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
   c->mark(2);
   if ((flags & LODGE_RECORD_MAX) && !(flags & LODGE_ACCUMULATE_MAX) && out->maxw_dev)
     CK(cudaMemsetAsync(out->maxw_dev, 0, (exact ? 8 : 4) * (size_t)U_cap, s));
-  int rc = launch_project_frame(levels, ls, w, c->fs, cam_dev, rp,
-                                (flags & LODGE_NEED_IMAGE) ? 1 : 0, exact, s,
-                                ch ? ch->slab_geom_dev : nullptr, ch ? ch->slab_sh_dev : nullptr);
+  const int32_t shade = (flags & LODGE_NEED_IMAGE) ? 1 : 0;
+  const void *const *slab_geom = ch ? ch->slab_geom_dev : nullptr;
+  const void *const *slab_sh = ch ? ch->slab_sh_dev : nullptr;
+  int rc = launch_project_frame(levels, ls, w, c->fs, cam_dev, rp, shade, exact, s, slab_geom,
+                                slab_sh);
   if (rc) return set_err(LODGE_ERR_BAD_ARG, "all levels must share one storage precision");
   ++nl;
   DSYNC("launch_project_frame");
@@ -490,6 +492,10 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
         (int64_t)c->phase_budget * tiles_x * tiles_y, 0x7fffffff);
     launch_dup_count(w, c->fs, tiles_x, U_cap, budget, s);
     DSYNC("launch_dup_count");
+    // compositing records of the first phase's splats only
+    launch_payload(levels, ls, w, c->fs, cam_dev, rp, shade, w.val_depth[0], &c->fs->split_S,
+                   U_cap, s, slab_geom, slab_sh); ++nl;
+    DSYNC("launch_payload");
     launch_tile_setup(w, c->fs, out->tile_count_dev, tiles_x, tiles_y, s, true);
     DSYNC("launch_tile_setup");
     nl += 2;
@@ -507,13 +513,20 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
     DSYNC("launch_setup_b");
     launch_enum_b(w, c->fs, tiles_x, tiles_y, U_cap, s);
     DSYNC("launch_enum_b");
-    nl += 3;
+    // ... and of the later splats that meet an unfinished tile
+    launch_payload(levels, ls, w, c->fs, cam_dev, rp, shade, w.val_depth[1], &c->fs->n_owners_b,
+                   U_cap, s, slab_geom, slab_sh);
+    DSYNC("launch_payload (second phase)");
+    nl += 4;
     launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s, TK_TILEB0);
     DSYNC("launch_tile_sort (second phase)");
     launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, 0, s, 2); ++nl;
     DSYNC("launch_composite (second phase)");
     c->mark(9);
   } else {
+    launch_payload(levels, ls, w, c->fs, cam_dev, rp, shade, w.val_depth[0], &c->fs->stats.M,
+                   U_cap, s, slab_geom, slab_sh); ++nl;
+    DSYNC("launch_payload");
     launch_tile_setup(w, c->fs, out->tile_count_dev, tiles_x, tiles_y, s); ++nl;
     DSYNC("launch_tile_setup");
     c->mark(5);
