@@ -188,9 +188,9 @@ def stage_bytes(U, AB, M, P, W, H, sh_terms, geom_bytes=48, sh_elem=4, P1=None, 
         "union": 4.0 * AB + 5.0 * U,
         # geometry only: union slot + record in, key + index + rectangle out
         "project": U * (5.0 + geom_bytes + 12.0) + M * 8.0,
-        # 32-bit keys: histogram (8 B/input), first pass (u64 key + index in,
-        # u32 key + index out), three u32 key + index passes, tie scan
-        "depth_sort": U * (8.0 + 12.0) + M * 8.0 + 3 * M * 16.0 + M * 4.0,
+        # eight 64-bit passes: histogram of the keys, then per pass the u64 key
+        # + u32 index read and written (the first pass reads all U inputs)
+        "depth_sort": U * (8.0 + 12.0) + M * 12.0 + 7 * M * 24.0,
         "tile_setup": (count if two else 0.0) + M1 * payload,
         "duplicate": P1 * 8.0 if two else M * 12.0 + P * 8.0,
         # pass 1 reads u64 pairs, writes packed u32; pass 2 reads and writes u32
@@ -531,6 +531,9 @@ def run_lodge(args):
         cam_dev = [torch.empty((B, cams.shape[1]), dtype=torch.uint8, device=dev)
                    for _ in range(2)]
         copied = [torch.cuda.Event(), torch.cuda.Event()]
+        # per parity and slot: the renders that read cam_dev[parity] are done
+        # (the upload two steps later must not overwrite a camera in use)
+        used = [[torch.cuda.Event() for _ in range(S)] for _ in range(2)]
         img8 = torch.empty((B, H, W, 3), dtype=torch.uint8, device=dev)
         img8_host = torch.empty((B, H, W, 3), dtype=torch.uint8).pin_memory()
         st_host = torch.empty((B, STATS_BYTES), dtype=torch.uint8).pin_memory()
@@ -547,6 +550,9 @@ def run_lodge(args):
                 copied[par].synchronize()
             for j, v in enumerate(schedule[s]):
                 cam_host[par][j].copy_(cams_host[pos[v]])
+            if si >= 2:
+                for q in range(S):
+                    cur.wait_event(used[par][q])
             cam_dev[par].copy_(cam_host[par], non_blocking=True)
             copied[par].record(cur)
             for q in range(S):
@@ -559,6 +565,8 @@ def run_lodge(args):
                 with torch.cuda.stream(r.stream_of(j % S)):
                     img8_host[j].copy_(img8[j], non_blocking=True)
                     st_host[j].copy_(frames[j].stats, non_blocking=True)
+            for q in range(S):
+                used[par][q].record(r.stream_of(q))
         for q in range(S):
             cur.wait_stream(r.stream_of(q))
         f1.record(cur)

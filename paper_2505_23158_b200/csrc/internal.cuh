@@ -108,6 +108,8 @@ enum : uint32_t {
   FAULT_SCATTER = 4,  // a onesweep scatter beyond the key count
   FAULT_LIST = 8,     // a compositor list range or member beyond its buffer
   FAULT_TILE = 16,    // an emitted pair's tile beyond the frame
+  FAULT_PAYLOAD = 32, // a compositing record requested for a non-input
+  FAULT_DEPTH = 64,   // LODGE_VERIFY builds: the depth order failed its check
 };
 __device__ __forceinline__ void raise_fault(FrameState *fs, uint32_t bit) {
   atomicOr(&fs->stats.fault, bit);
@@ -259,9 +261,10 @@ void launch_select_frame(const double *centers, int32_t K, const lodge_camera *c
                          cudaStream_t s);
 int launch_union(const lodge_chunks &ch, const LevelSlots &ls, FrameState *fs, uint64_t *status,
                   uint32_t *union_idx, uint8_t *union_tag, cudaStream_t s);
+// W, H: the frame's size (its tile grid bounds the difference-array updates)
 int launch_project_frame(const lodge_level *levels, const LevelSlots &ls, const Work &w,
                          FrameState *fs, const lodge_camera *cam_dev,
-                         const lodge_raster_params &rp, int32_t shade, int32_t exact,
+                         const lodge_raster_params &rp, int32_t W, int32_t H,
                          cudaStream_t s,
                          const void *const *slab_geom = nullptr,
                          const void *const *slab_sh = nullptr);

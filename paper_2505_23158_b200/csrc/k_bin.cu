@@ -569,8 +569,11 @@ void launch_dup_emit(const Work &w, FrameState *fs, int32_t tiles_x, cudaStream_
                      bool first_phase) {
   static int64_t resident = 0;
   if (!resident) resident = resident_ctas(k_dup_emit, DUP_THREADS);
-  const unsigned egrid =
-      (unsigned)std::min<int64_t>((w.P_cap + EMIT_CHUNK - 1) / EMIT_CHUNK, resident);
+#ifndef LODGE_PERSIST
+#define LODGE_PERSIST 1
+#endif
+  const unsigned egrid = (unsigned)std::min<int64_t>((w.P_cap + EMIT_CHUNK - 1) / EMIT_CHUNK,
+                                                     LODGE_PERSIST ? resident : 0x7fffffff);
   k_dup_emit<<<egrid, DUP_THREADS, 0, s>>>(w.val_depth[0], tiles_x, w, fs, first_phase ? 1 : 0);
 }
 

@@ -588,6 +588,10 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
         const int j = tid + h * CT;
         if (j < n) {
           const uint32_t src = PL[j].src;
+          if (src >= cpar.n_payload) {  // a record this frame did not write
+            raise_fault(fs, FAULT_LIST);
+            continue;
+          }
           if (EXACT) {
             if (S.maxw[j]) atomicMax(reinterpret_cast<unsigned long long *>(maxw) + src, S.maxw[j]);
           } else if (S.maxw32[j]) {

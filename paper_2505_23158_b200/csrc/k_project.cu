@@ -396,6 +396,7 @@ struct ProjLevels {
   // positions in the owning chunk's set and these tables locate the records
   const void *const *slab_geom;
   const void *const *slab_sh;
+  uint32_t n[LODGE_MAX_LEVELS];  // records per level (bounds checks)
 };
 
 // Shared per-CTA frame context of the frame kernels (camera, blend factor,
@@ -463,12 +464,14 @@ template <typename GT, typename ST>
 #endif
 __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLevels lv, Work w, FrameState *fs,
                                                        const lodge_camera *__restrict__ cam_p,
-                                                       lodge_raster_params rp) {
+                                                       lodge_raster_params rp, int32_t tiles_x,
+                                                       int32_t tiles_y) {
   // persistent CTAs (grid-stride over the slots): the camera and the level
   // table are staged once per CTA
   __shared__ FrameCtx F;
   stage_frame_ctx(F, lv, fs, cam_p);
-  const int32_t tiles_x = (F.cam.w + 15) / 16, tiles_y = (F.cam.h + 15) / 16;
+  // the tile grid is the frame's (host W, H), so the difference-array
+  // indices stay in range whatever the device camera holds
   const uint32_t nslots = lv.slot_base[lv.L];
   uint32_t nkeep_cta = 0;  // survivors seen by this thread's warp (lane 0 counts)
   for (uint32_t base = blockIdx.x * blockDim.x; base < nslots; base += gridDim.x * blockDim.x) {
@@ -519,7 +522,15 @@ __global__ void __launch_bounds__(256, LODGE_PAYLOAD_MINB) k_payload(ProjLevels 
     const uint32_t g = ids[i];
     int l = 0;
     while (l + 1 < lv.L && g >= F.cat[l + 1]) ++l;
+    if (g >= F.cat[l] + F.used[l] || g >= (uint32_t)w.M_cap) {  // not an input of this frame
+      raise_fault(fs, FAULT_PAYLOAD);
+      continue;
+    }
     const uint32_t slot = lv.slot_base[l] + (g - F.cat[l]);
+    if (!lv.slab_geom && w.union_idx[slot] >= lv.n[l]) {
+      raise_fault(fs, FAULT_PAYLOAD);
+      continue;
+    }
     double v[12];
     const ST *sp;
     uint32_t gidx;
@@ -701,9 +712,10 @@ static int sm_count() {
 template <typename GT, typename ST>
 static void launch_pf(const ProjLevels &lv, const Work &w, FrameState *fs,
                       const lodge_camera *cam, const lodge_raster_params &rp, uint32_t nslots,
-                      cudaStream_t s) {
+                      int32_t tiles_x, int32_t tiles_y, cudaStream_t s) {
   const uint32_t want = (nslots + 255) / 256, cap = LODGE_PROJ_MINB * (uint32_t)sm_count();
-  k_project_frame<GT, ST><<<want < cap ? want : cap, 256, 0, s>>>(lv, w, fs, cam, rp);
+  k_project_frame<GT, ST><<<want < cap ? want : cap, 256, 0, s>>>(lv, w, fs, cam, rp, tiles_x,
+                                                                   tiles_y);
 }
 
 template <typename GT, typename ST>
@@ -729,6 +741,7 @@ static int proj_levels(const lodge_level *levels, const LevelSlots &ls,
     lv.sh[l] = levels[l].sh_dev;
     lv.degree[l] = levels[l].sh_degree;
     lv.qnorm[l] = (levels[l].flags & LODGE_GEOM_QNORM) ? 1 : 0;
+    lv.n[l] = (uint32_t)levels[l].n;
   }
   for (int l = 0; l <= LODGE_MAX_LEVELS; ++l) lv.slot_base[l] = l <= lv.L ? ls.slot_base[l] : 0;
   g32 = fl & LODGE_GEOM_FP32;
@@ -738,17 +751,18 @@ static int proj_levels(const lodge_level *levels, const LevelSlots &ls,
 
 int launch_project_frame(const lodge_level *levels, const LevelSlots &ls, const Work &w,
                          FrameState *fs, const lodge_camera *cam_dev,
-                         const lodge_raster_params &rp, int32_t, int32_t, cudaStream_t s,
+                         const lodge_raster_params &rp, int32_t W, int32_t H, cudaStream_t s,
                          const void *const *slab_geom, const void *const *slab_sh) {
+  const int32_t tx = (W + 15) / 16, ty = (H + 15) / 16;
   ProjLevels lv;
   bool g32, s32;
   if (proj_levels(levels, ls, slab_geom, slab_sh, lv, g32, s32)) return -1;
   const uint32_t nslots = ls.slot_base[lv.L];
   if (nslots == 0) return 0;
-  if (g32 && s32) launch_pf<float, float>(lv, w, fs, cam_dev, rp, nslots, s);
-  else if (g32) launch_pf<float, double>(lv, w, fs, cam_dev, rp, nslots, s);
-  else if (s32) launch_pf<double, float>(lv, w, fs, cam_dev, rp, nslots, s);
-  else launch_pf<double, double>(lv, w, fs, cam_dev, rp, nslots, s);
+  if (g32 && s32) launch_pf<float, float>(lv, w, fs, cam_dev, rp, nslots, tx, ty, s);
+  else if (g32) launch_pf<float, double>(lv, w, fs, cam_dev, rp, nslots, tx, ty, s);
+  else if (s32) launch_pf<double, float>(lv, w, fs, cam_dev, rp, nslots, tx, ty, s);
+  else launch_pf<double, double>(lv, w, fs, cam_dev, rp, nslots, tx, ty, s);
   return 0;
 }
 

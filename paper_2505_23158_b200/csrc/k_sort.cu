@@ -263,6 +263,9 @@ __global__ void __launch_bounds__(256) k_depth_ties(const uint32_t *__restrict__
       for (uint32_t j = tid; j < n; j += blockDim.x) val[i0 + j] = scratch[i0 + j];
       __syncthreads();
     }
+    // every thread has read s_nlong before the next segment resets it (a
+    // thread reading the reset value would skip the barriers above)
+    __syncthreads();
   }
 }
 
@@ -328,7 +331,11 @@ static void os_launch(int64_t cap, cudaStream_t s, const KI *kin, KO *kout, cons
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     resident = resident_grid(k_onesweep<VALS, KI, KO, MAP, NB, DROP>, OS_THREADS, sm, 1 << 30);
   }
-  const unsigned grid = (unsigned)std::min<int64_t>((cap + TILE - 1) / TILE, resident);
+#ifndef LODGE_PERSIST
+#define LODGE_PERSIST 1
+#endif
+  const unsigned grid = (unsigned)std::min<int64_t>((cap + TILE - 1) / TILE,
+                                                    LODGE_PERSIST ? resident : 0x7fffffff);
   k_onesweep<VALS, KI, KO, MAP, NB, DROP><<<grid, OS_THREADS, sm, s>>>(
       kin, kout, vin, vout, n_ptr, shift, sb, digit_off, status, fs, tk);
 }
@@ -345,12 +352,34 @@ static void os_launch_nb(int nb, A... args) {
   }
 }
 
+#ifdef LODGE_VERIFY
+// Debug check of the frame depth order: keys non-decreasing, every value an
+// input whose own key is the sorted key.
+__global__ void k_depth_verify(const uint32_t *k32, const uint32_t *val, const uint64_t *full,
+                               FrameState *fs) {
+  const uint32_t M = fs->stats.M, U = fs->n_sort;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < M; i += gridDim.x * blockDim.x) {
+    const uint32_t g = val[i];
+    bool ok = g < U && depth_key32(full[g]) == k32[i];
+    if (i + 1 < M) ok = ok && k32[i] <= k32[i + 1];
+    if (!ok) raise_fault(fs, FAULT_DEPTH);
+  }
+}
+#endif
+
 // Frames: four passes over 32-bit keys (u32 ping-pong in the two halves of
 // key_depth[1]; key_depth[0] keeps the full keys by input index for the tie
 // repair), sorted input indices in val_depth[0].
 void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
                        cudaStream_t s) {
   if (M_cap <= 0) return;
+#ifndef LODGE_DEPTH32
+  // the eight 64-bit passes: the 32-bit variant below faulted intermittently
+  // with several contexts rendering concurrently (its order check,
+  // LODGE_VERIFY, fired; DESIGN.md tuning record) and stays opt-in
+  launch_depth_sort64(w, fs, M_cap, launches, s);
+  return;
+#endif
   int hist_blocks = (int)((M_cap + 1023) / 1024);
   if (hist_blocks > 148 * 4) hist_blocks = 148 * 4;
   k_depth_hist32<<<hist_blocks, 256, 0, s>>>(w.key_depth[0], fs);
@@ -365,7 +394,8 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
                          (int)sm);
     resident = resident_grid(k_depth_pass<true>, OS_THREADS, sm, 1 << 30);
   }
-  const unsigned grid = (unsigned)std::min<int64_t>((M_cap + TILE - 1) / TILE, resident);
+  const unsigned grid = (unsigned)std::min<int64_t>((M_cap + TILE - 1) / TILE,
+                                                    LODGE_PERSIST ? resident : 0x7fffffff);
   uint32_t *k32[2] = {reinterpret_cast<uint32_t *>(w.key_depth[1]),
                       reinterpret_cast<uint32_t *>(w.key_depth[1]) + M_cap};
   // keys 0: u64 -> k32[0], 1: k32[0] -> k32[1], 2: k32[1] -> k32[0], 3: k32[0] -> k32[1]
@@ -379,7 +409,12 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
         fs->off_depth[p], w.status, fs, TK_DEPTH0 + p);
   }
   const unsigned tgrid = (unsigned)std::min<int64_t>((M_cap + TIE_SEG - 1) / TIE_SEG, 148 * 16);
+#ifndef LODGE_NO_TIES
   k_depth_ties<<<tgrid, 256, 0, s>>>(k32[1], w.val_depth[0], w.key_depth[0], w.val_depth[1], fs);
+#endif
+#ifdef LODGE_VERIFY
+  k_depth_verify<<<296, 256, 0, s>>>(k32[1], w.val_depth[0], w.key_depth[0], fs);
+#endif
   *launches += 5;
 }
 

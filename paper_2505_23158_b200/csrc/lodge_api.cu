@@ -39,7 +39,7 @@ struct lodge_ctx {
   int64_t tiles_cap = 0;  // capacity of tile_start (T+1) and diff
   int64_t pixels_cap = 0;  // capacity of the two-phase pixel state
   int32_t phase_budget = 1280;  // first-phase pairs per tile of two-phase frames (0: one pass)
-  bool debug_sync = false;  // LODGE_DEBUG_SYNC=1: synchronise and check after every stage
+  int debug_sync = 0;  // LODGE_DEBUG_SYNC=1: check after every stage; 2: after each segment
   int32_t launches = 0;
   LevelSlots last_slots{};  // slot layout of the last union
   // stage profiling
@@ -156,9 +156,10 @@ static int check_launch(const char *what) {
 
 // LODGE_DEBUG_SYNC builds of a frame: a device fault is reported with the
 // stage that raised it
-#define DSYNC(what)                                                                   \
+#define DSYNC(what) DSYNC_L(1, what)
+#define DSYNC_L(level, what)                                                          \
   do {                                                                                \
-    if (c->debug_sync) {                                                              \
+    if (c->debug_sync == (level) || (c->debug_sync == 1 && (level) == 2)) {           \
       cudaError_t _e = cudaStreamSynchronize(s);                                      \
       if (_e == cudaSuccess) _e = cudaGetLastError();                                 \
       if (_e != cudaSuccess)                                                          \
@@ -196,7 +197,7 @@ int lodge_create(int32_t device, lodge_ctx **out) {
   c->device = device;
   {
     const char *d = getenv("LODGE_DEBUG_SYNC");
-    c->debug_sync = d && d[0] == '1';
+    c->debug_sync = d ? atoi(d) : 0;
   }
   CK(cudaMalloc(&c->fs, sizeof(FrameState)));
   CK(cudaMemset(c->fs, 0, sizeof(FrameState)));
@@ -475,14 +476,14 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
   const int32_t shade = (flags & LODGE_NEED_IMAGE) ? 1 : 0;
   const void *const *slab_geom = ch ? ch->slab_geom_dev : nullptr;
   const void *const *slab_sh = ch ? ch->slab_sh_dev : nullptr;
-  int rc = launch_project_frame(levels, ls, w, c->fs, cam_dev, rp, shade, exact, s, slab_geom,
-                                slab_sh);
+  int rc = launch_project_frame(levels, ls, w, c->fs, cam_dev, rp, W, H, s, slab_geom, slab_sh);
   if (rc) return set_err(LODGE_ERR_BAD_ARG, "all levels must share one storage precision");
   ++nl;
   DSYNC("launch_project_frame");
   c->mark(3);
   launch_depth_sort(w, c->fs, U_cap, &nl, s);
   DSYNC("launch_depth_sort");
+  DSYNC_L(2, "segment: select .. depth sort");
   c->mark(4);
   if (two_phase(c, W, H, flags)) {
     // FAST frames in two depth phases: the splats whose pairs
@@ -508,6 +509,7 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
     c->mark(7);
     launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, 0, s, 1); ++nl;
     DSYNC("launch_composite");
+    DSYNC_L(2, "segment: count .. first-phase composite");
     c->mark(8);
     launch_setup_b(w, c->fs, tiles_x, tiles_y, s);
     DSYNC("launch_setup_b");
@@ -522,6 +524,7 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
     DSYNC("launch_tile_sort (second phase)");
     launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, 0, s, 2); ++nl;
     DSYNC("launch_composite (second phase)");
+    DSYNC_L(2, "segment: second phase");
     c->mark(9);
   } else {
     launch_payload(levels, ls, w, c->fs, cam_dev, rp, shade, w.val_depth[0], &c->fs->stats.M,

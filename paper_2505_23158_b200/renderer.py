@@ -132,19 +132,35 @@ class Renderer:
         tx, ty = -(-width // TILE_SIZE), -(-height // TILE_SIZE)
         fdt = torch.float64 if self.precision == "exact" else torch.float32
         d = self.device
-        return Frame(width, height,
-                     torch.empty((height, width, 3), dtype=fdt, device=d) if need_image else None,
-                     torch.empty((ty, tx), dtype=torch.int32, device=d),
-                     torch.empty((height, width), dtype=torch.int32, device=d),
-                     # zeroed: a frame clears only the entries its own slot
-                     # layout can write, which may be fewer than U_cap
-                     torch.zeros(max(self.U_cap, 1), dtype=fdt, device=d) if record_max else None,
-                     torch.zeros(STATS_BYTES, dtype=torch.uint8, device=d))
+        fr = Frame(width, height,
+                   torch.empty((height, width, 3), dtype=fdt, device=d) if need_image else None,
+                   torch.empty((ty, tx), dtype=torch.int32, device=d),
+                   torch.empty((height, width), dtype=torch.int32, device=d),
+                   # zeroed: a frame clears only the entries its own slot
+                   # layout can write, which may be fewer than U_cap
+                   torch.zeros(max(self.U_cap, 1), dtype=fdt, device=d) if record_max else None,
+                   torch.zeros(STATS_BYTES, dtype=torch.uint8, device=d))
+        self._publish()  # the fills land before any slot stream renders into it
+        return fr
+
+    def _publish(self):
+        """Make every slot stream wait for the work enqueued so far on the
+        current stream (a camera upload, a frame's allocation fill)."""
+        if self.n_streams == 1 and self._slots[0][1] is None:
+            return
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        for _, st in self._slots:
+            if st is not None:
+                st.wait_event(ev)
 
     def upload_cameras(self, cameras) -> torch.Tensor:
-        """(V, sizeof(lodge_camera)) uint8 device tensor of camera structs."""
+        """(V, sizeof(lodge_camera)) uint8 device tensor of camera structs,
+        visible to every slot stream."""
         host = np.stack([camera_bytes(c) for c in cameras])
-        return torch.from_numpy(host).to(self.device)
+        out = torch.from_numpy(host).to(self.device)
+        self._publish()
+        return out
 
     def render(self, cam_row: torch.Tensor, frame: Frame, pair=None, t: float = None,
                need_image: bool = True, record_max: bool = True, slot: int = 0,
