@@ -449,11 +449,14 @@ int lodge_render_frame(lodge_ctx *c, const lodge_level *levels, int32_t n_levels
                      "lodge_render_frame", ch);
 }
 
-// Two depth phases: FAST compositing, lists not needed for inspection, and
-// both tile difference arrays fit the setup kernel's shared memory.
-static bool two_phase(const lodge_ctx *c, int32_t W, int32_t H, int32_t flags) {
+// Two depth phases: FAST compositing, lists not needed for inspection, a
+// visible buffer, and both tile difference arrays fit the setup kernel's
+// shared memory.
+static bool two_phase(const lodge_ctx *c, int32_t W, int32_t H, int32_t flags,
+                      const lodge_frame_out *out) {
   const int64_t tx = (W + 15) / 16, ty = (H + 15) / 16;
-  return c->precision == LODGE_PREC_FAST && c->phase_budget > 0 &&
+  // the visible counts of unfinished tiles carry over in the visible buffer
+  return c->precision == LODGE_PREC_FAST && c->phase_budget > 0 && out->visible_dev &&
          !(flags & LODGE_FULL_LISTS) && 2 * (tx + 1) * (ty + 1) * 4 <= 200 * 1024;
 }
 
@@ -485,7 +488,7 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
   DSYNC("launch_depth_sort");
   DSYNC_L(2, "segment: select .. depth sort");
   c->mark(4);
-  if (two_phase(c, W, H, flags)) {
+  if (two_phase(c, W, H, flags, out)) {
     // FAST frames in two depth phases: the splats whose pairs
     // start within the budget are binned, sorted and composited first; the
     // tiles that still have live pixels then receive the rest of their pairs
