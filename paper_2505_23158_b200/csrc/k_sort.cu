@@ -353,6 +353,21 @@ static void os_launch_nb(int nb, A... args) {
 }
 
 #ifdef LODGE_VERIFY
+// Debug check of one pass: its output is ordered by the pass digit, and the
+// value's own key has the output key (bit 8 + pass of stats.fault).
+__global__ void k_pass_verify(const uint32_t *kout, const uint32_t *vout, const uint64_t *full,
+                              const uint32_t *n_ptr, int shift, int pass, FrameState *fs) {
+  const uint32_t n = *n_ptr, U = fs->n_sort;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t g = vout[i];
+    bool ok = g < U && depth_key32(full[g]) == kout[i];
+    if (i + 1 < n) ok = ok && ((kout[i] >> shift) & 255u) <= ((kout[i + 1] >> shift) & 255u);
+    if (!ok) raise_fault(fs, 256u << pass);
+  }
+}
+#endif
+
+#ifdef LODGE_VERIFY
 // Debug check of the frame depth order: keys non-decreasing, every value an
 // input whose own key is the sorted key.
 __global__ void k_depth_verify(const uint32_t *k32, const uint32_t *val, const uint64_t *full,
@@ -402,11 +417,19 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
   k_depth_pass<true><<<grid, OS_THREADS, sm, s>>>(w.key_depth[0], nullptr, k32[0], w.val_depth[0],
                                                   w.val_depth[1], &fs->n_sort, 0,
                                                   fs->off_depth[0], w.status, fs, TK_DEPTH0);
+#ifdef LODGE_VERIFY
+  k_pass_verify<<<296, 256, 0, s>>>(k32[0], w.val_depth[1], w.key_depth[0], &fs->stats.M, 0, 0,
+                                    fs);
+#endif
   for (int p = 1; p < 4; ++p) {
     const int a = p & 1;  // values: [1] -> [0] -> [1] -> [0]
     k_depth_pass<false><<<grid, OS_THREADS, sm, s>>>(
         nullptr, k32[a ^ 1], k32[a], w.val_depth[a], w.val_depth[a ^ 1], &fs->stats.M, 8 * p,
         fs->off_depth[p], w.status, fs, TK_DEPTH0 + p);
+#ifdef LODGE_VERIFY
+    k_pass_verify<<<296, 256, 0, s>>>(k32[a], w.val_depth[a ^ 1], w.key_depth[0], &fs->stats.M,
+                                      8 * p, p, fs);
+#endif
   }
   const unsigned tgrid = (unsigned)std::min<int64_t>((M_cap + TIE_SEG - 1) / TIE_SEG, 148 * 16);
 #ifndef LODGE_NO_TIES
