@@ -56,6 +56,7 @@ def test_two_phase_equals_one_pass(street, budget, z):
     fr2, st2 = two.render_camera(cam)
     got = outputs(fr2, st2)
     assert_same(got, ref)
+    assert st2.fault == 0 and st1.fault == 0
     assert st2.P_first <= st2.P and st2.P_first + st2.P_second <= st2.P
     if budget >= (1 << 20):
         assert st2.P_first == st2.P and st2.P_second == 0
@@ -95,3 +96,4 @@ def test_two_phase_frames_in_flight(street):
     torch.cuda.synchronize()
     for j, fr in enumerate(frames):
         assert_same(outputs(fr, fr.read_stats()), refs[j])
+    assert two.fault_flags() == 0 and one.fault_flags() == 0
