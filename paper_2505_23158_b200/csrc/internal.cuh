@@ -106,10 +106,12 @@ enum : uint32_t {
   FAULT_OWNERS = 1,   // an emission CTA's owner range exceeds its staging
   FAULT_COMPACT = 2,  // second-phase compaction beyond the pair count
   FAULT_SCATTER = 4,  // a onesweep scatter beyond the key count
-  FAULT_LIST = 8,     // a compositor list range or member beyond its buffer
+  FAULT_LIST = 8,     // a compositor tile list range beyond the list buffer
   FAULT_TILE = 16,    // an emitted pair's tile beyond the frame
   FAULT_PAYLOAD = 32, // a compositing record requested for a non-input
   FAULT_DEPTH = 64,   // LODGE_VERIFY builds: the depth order failed its check
+  FAULT_MEMBER = 128, // a compositor list member beyond the payload buffer
+  FAULT_SRC = 256,    // a staged record whose input index is beyond the max-weight buffer
 };
 __device__ __forceinline__ void raise_fault(FrameState *fs, uint32_t bit) {
   atomicOr(&fs->stats.fault, bit);

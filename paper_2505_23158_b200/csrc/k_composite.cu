@@ -191,8 +191,10 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
       MODE < 0 ? (cpar.flags & LODGE_RECORD_MAX) && maxw != nullptr : (MODE & 2) != 0;
   const uint32_t s = tile_start[t];
   uint32_t e = tile_start[t + 1];
-  if (fs->stats.overflow) e = s;
-  if (e < s || e > cpar.n_list) {
+  if (fs->stats.overflow) {
+    e = s;  // the pair buffers overflowed: this attempt is discarded and re-rendered
+            // after they grow, and its tile ranges are stale, so they are not checked
+  } else if (e < s || e > cpar.n_list) {
     if (tid == 0) raise_fault(fs, FAULT_LIST);
     e = s;
   }
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
       if (j < n) {
         uint32_t m = list[bb + j];
         if (m >= cpar.n_payload) {
-          raise_fault(fs, FAULT_LIST);
+          raise_fault(fs, FAULT_MEMBER);
           m = 0;
         }
         S.m[k][j] = m;
@@ -589,7 +591,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
         if (j < n) {
           const uint32_t src = PL[j].src;
           if (src >= cpar.n_payload) {  // a record this frame did not write
-            raise_fault(fs, FAULT_LIST);
+            raise_fault(fs, FAULT_SRC);
             continue;
           }
           if (EXACT) {
