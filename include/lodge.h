@@ -257,6 +257,16 @@ int lodge_fault_flags(lodge_ctx *ctx, uint32_t *flags);
  * [3] pixel evaluations inside the cut-off, [4] warp-batches. */
 int lodge_debug_counters(lodge_ctx *ctx, uint64_t *out8);
 
+/* Diagnostic: the frame depth sort alone (the onesweep passes of
+ * np.lexsort((index, depth)), src/raster.py:401) over n caller keys; keys
+ * equal to ~0 are dropped as culled inputs are.  Writes the surviving keys
+ * sorted and their input indices; out_m_dev (device, 2 x uint32) receives
+ * the survivor count and the frame's fault bits.  Async on the context
+ * stream. */
+int lodge_debug_depth_sort(lodge_ctx *ctx, const uint64_t *keys_dev, int64_t n,
+                           uint64_t *sorted_keys_dev, uint32_t *sorted_idx_dev,
+                           uint32_t *out_m_dev);
+
 /* ---- LOD-mode and full-mode frames --------------
  * replaces render_lod (src/lod.py:230-237) and the "full" / "lod" branches
  * of _mode_selection + _render_mode (src/cli.py:219-243): the active sets

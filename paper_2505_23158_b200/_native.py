@@ -13,7 +13,10 @@ import subprocess
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblodge.so")
+# LODGE_LIB=name loads a diagnostic build liblodge_<name>.so (csrc/Makefile
+# VARIANT=name, e.g. the LODGE_VERIFY order checks of the stress test)
+_VARIANT = os.environ.get("LODGE_LIB", "")
+LIB_PATH = os.path.join(_HERE, f"liblodge_{_VARIANT}.so" if _VARIANT else "liblodge.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 MAX_LEVELS = 8
@@ -109,6 +112,8 @@ EXPORTS = {
     "lodge_to_srgb8": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p], C.c_int),
     "lodge_last_launch_count": ([C.c_void_p], C.c_int32),
     "lodge_debug_counters": ([C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
+    "lodge_debug_depth_sort": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                C.c_void_p], C.c_int),
     "lodge_render_lod": ([C.c_void_p, C.POINTER(Level), C.c_int32, C.POINTER(C.c_double),
                           C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.POINTER(RasterParams),
                           C.c_int32, C.POINTER(FrameOut), C.c_void_p], C.c_int),
@@ -130,13 +135,24 @@ _lib = None
 _lock = threading.Lock()
 
 
-def build(verbose: bool = False) -> str:
-    """Compile liblodge.so for sm_100a in place (make -C csrc)."""
-    out = subprocess.run(["make", "-C", CSRC], capture_output=True, text=True)
-    if out.returncode != 0:
-        raise LodgeError("liblodge build failed:\n" + out.stdout[-4000:] + out.stderr[-4000:])
-    if verbose:
-        print(out.stdout[-2000:])
+# diagnostic variants built next to the product library: name -> nvcc defines
+VARIANTS = {
+    "verify": "-DLODGE_VERIFY",
+}
+
+
+def build(verbose: bool = False, variants: bool = True) -> str:
+    """Compile liblodge.so (and the diagnostic variants) for sm_100a in place
+    (make -C csrc)."""
+    jobs = [[]]
+    if variants:
+        jobs += [[f"VARIANT={k}", f"EXTRA={v}"] for k, v in VARIANTS.items()]
+    for extra in jobs:
+        out = subprocess.run(["make", "-j4", "-C", CSRC] + extra, capture_output=True, text=True)
+        if out.returncode != 0:
+            raise LodgeError("liblodge build failed:\n" + out.stdout[-4000:] + out.stderr[-4000:])
+        if verbose:
+            print(out.stdout[-2000:])
     return LIB_PATH
 
 

@@ -96,6 +96,7 @@ struct Work {
   uint64_t *status;         // look-back status words (epoch | flags | value)
   uint32_t *union_idx;      // slots
   uint8_t *union_tag;       // slots
+  uint32_t *vrank;          // LODGE_VERIFY builds: depth rank of each input (M_cap)
   int64_t M_cap, P_cap, status_cap, slot_cap;
 };
 
@@ -111,7 +112,9 @@ enum : uint32_t {
   FAULT_PAYLOAD = 32, // a compositing record requested for a non-input
   FAULT_DEPTH = 64,   // LODGE_VERIFY builds: the depth order failed its check
   FAULT_MEMBER = 128, // a compositor list member beyond the payload buffer
-  FAULT_SRC = 256,    // a staged record whose input index is beyond the max-weight buffer
+  FAULT_SRC = 256,    // a staged record whose input index is beyond the caller's max-weight buffer
+  FAULT_LISTORD = 512, // LODGE_VERIFY builds: a per-tile list failed its order check
+  FAULT_STAGE = 1024,  // LODGE_VERIFY builds: a onesweep partition staged a key outside its digit run
 };
 __device__ __forceinline__ void raise_fault(FrameState *fs, uint32_t bit) {
   atomicOr(&fs->stats.fault, bit);
@@ -123,6 +126,12 @@ enum : uint32_t { ST_EMPTY = 0, ST_AGG = 1, ST_PREFIX = 2 };
 __device__ __forceinline__ uint64_t st_pack(uint32_t epoch, uint32_t flag, uint32_t v) {
   return ((uint64_t)epoch << 32) | ((uint64_t)flag << 30) | (uint64_t)(v & 0x3fffffffu);
 }
+// Look-back status cells: one 64-bit word per (partition, digit) holding
+// epoch, flag and value together, so a reader needs no ordering beyond the
+// single-copy atomicity of the word: relaxed loads and stores at gpu scope.
+// (The intermittent wrong orders of round 1 were a warp left diverged by the
+// per-lane spin below reaching an aligned CTA barrier, not a memory-order
+// issue: see onesweep.cuh and DESIGN.md "Diverged warps at aligned barriers".)
 __device__ __forceinline__ void st_store(uint64_t *p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -139,6 +148,7 @@ __device__ __forceinline__ uint32_t lookback_warp(uint64_t *status, uint32_t par
   const int lane = threadIdx.x & 31;
   if (part == 0) {
     if (lane == 0) st_store(status, st_pack(epoch, ST_PREFIX, agg));
+    __syncwarp();
     return 0;
   }
   if (lane == 0) st_store(status + part, st_pack(epoch, ST_AGG, agg));
@@ -155,6 +165,7 @@ __device__ __forceinline__ uint32_t lookback_warp(uint64_t *status, uint32_t par
       } while (flag == ST_EMPTY);
       val = (uint32_t)(s & 0x3fffffffu);
     }
+    __syncwarp();  // the lanes' spins end at different times: reconverge
     // lanes beyond q<0 act as an implicit zero prefix
     uint32_t pmask = __ballot_sync(FULL_MASK, flag == ST_PREFIX);
     int first = __ffs(pmask) - 1;  // nearest partition holding a prefix
@@ -166,6 +177,7 @@ __device__ __forceinline__ uint32_t lookback_warp(uint64_t *status, uint32_t par
     window_end -= 32;
   }
   if (lane == 0) st_store(status + part, st_pack(epoch, ST_PREFIX, prefix + agg));
+  __syncwarp();  // callers continue into aligned barriers with the warp converged
   return prefix;
 }
 
@@ -236,6 +248,19 @@ __host__ __device__ __forceinline__ uint32_t union_status_stride(uint32_t max_sl
   return (max_slots + 255u) / 256u + 1u;
 }
 
+// Per-device launch-configuration cache (opt-in shared-memory sizes, resident
+// CTA counts): both are properties of a (kernel, device), and one process can
+// hold contexts on several devices.
+constexpr int LODGE_MAX_DEVICES = 64;
+struct PerDevice {
+  int64_t v[LODGE_MAX_DEVICES] = {};
+  int64_t &operator()() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return v[(d >= 0 && d < LODGE_MAX_DEVICES) ? d : 0];
+  }
+};
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -288,6 +313,8 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
                        cudaStream_t s);
 void launch_depth_sort64(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
                          cudaStream_t s);
+void launch_debug_depth_sort(const Work &w, FrameState *fs, const uint64_t *keys, uint32_t n,
+                             uint64_t *ko, uint32_t *vo, uint32_t *m_out, cudaStream_t s);
 void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32_t tiles_x,
                        int32_t tiles_y, cudaStream_t s, bool two_phase = false);
 // two-phase frames: first-phase pair budget of the counting pass
@@ -303,11 +330,16 @@ void launch_duplicate(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_
                       cudaStream_t s);
 void launch_tile_sort(Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
                       int32_t *launches, cudaStream_t s, int tk0 = 10 /* TK_TILE0 */);
+#ifdef LODGE_VERIFY
+// debug builds: order check of the per-tile lists of the last tile sort
+void launch_list_verify(const Work &w, FrameState *fs, uint32_t T, bool second, cudaStream_t s);
+#endif
 // phase 0: one pass over the full lists; 1 / 2: the two depth phases of a
-// FAST frame (1 saves the state of unfinished tiles, 2 resumes them)
+// FAST frame (1 saves the state of unfinished tiles, 2 resumes them).
+// n_maxw: entries of out.maxw_dev (inputs of the batch / slots of the frame)
 void launch_composite(const Work &w, FrameState *fs, const lodge_camera *cam_dev, int32_t W,
                       int32_t H, const lodge_raster_params &rp, int32_t flags, int32_t exact,
-                      const lodge_frame_out &out, uint32_t n_inputs_cap, cudaStream_t s,
+                      const lodge_frame_out &out, uint32_t n_maxw, cudaStream_t s,
                       int phase = 0);
 void launch_export_lists(const Work &w, FrameState *fs, int32_t T, int64_t *tile_offsets,
                          int64_t *tile_src, int64_t cap, cudaStream_t s);

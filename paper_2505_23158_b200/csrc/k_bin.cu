@@ -533,10 +533,10 @@ void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32
                        int32_t tiles_y, cudaStream_t s, bool two_phase) {
   const size_t nd = (size_t)(tiles_x + 1) * (tiles_y + 1) * 4;
   const size_t sm = two_phase ? 2 * nd : nd;
-  static size_t attr = 0;
-  if (sm > 48 * 1024 && sm > attr) {
+  static PerDevice attr;
+  if (sm > 48 * 1024 && (int64_t)sm > attr()) {
     cudaFuncSetAttribute(k_tile_setup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = sm;
+    attr() = (int64_t)sm;
   }
   k_tile_setup<<<1, 1024, sm, s>>>(w.tile_diff, two_phase ? w.tile_diff_a : nullptr, tiles_x,
                                    tiles_y, tile_count, two_phase ? w.count_all : nullptr,
@@ -567,8 +567,9 @@ static int64_t resident_ctas(K kernel, int threads) {
 
 void launch_dup_emit(const Work &w, FrameState *fs, int32_t tiles_x, cudaStream_t s,
                      bool first_phase) {
-  static int64_t resident = 0;
-  if (!resident) resident = resident_ctas(k_dup_emit, DUP_THREADS);
+  static PerDevice res;
+  if (!res()) res() = resident_ctas(k_dup_emit, DUP_THREADS);
+  const int64_t resident = res();
 #ifndef LODGE_PERSIST
 #define LODGE_PERSIST 1
 #endif
@@ -587,10 +588,10 @@ void launch_duplicate(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_
 void launch_setup_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
                     cudaStream_t s) {
   const size_t sm = (size_t)(tiles_x + 1) * (tiles_y + 1) * 4;
-  static size_t attr = 0;
-  if (sm > 48 * 1024 && sm > attr) {
+  static PerDevice attr;
+  if (sm > 48 * 1024 && (int64_t)sm > attr()) {
     cudaFuncSetAttribute(k_setup_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = sm;
+    attr() = (int64_t)sm;
   }
   k_setup_b<<<1, 1024, sm, s>>>(w.alive, w.count_all, w.tile_start, tiles_x, tiles_y,
                                 w.tile_start_b, w.tile_order_b, w.sat, fs);
@@ -603,16 +604,17 @@ void launch_enum_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles
       (unsigned)((M_cap + DUP_THREADS * COUNT_ITEMS - 1) / (DUP_THREADS * COUNT_ITEMS));
   k_dup_count<true><<<grid, DUP_THREADS, 0, s>>>(w.val_depth[0], w.rect, w, fs, 0u, tiles_x,
                                                  chunk_cap(w));
-  static int64_t resident = 0;
+  static PerDevice res;
   constexpr size_t sm = sizeof(EmitSmem<EB_CHUNK>);
-  if (!resident) {
+  if (!res()) {
     cudaFuncSetAttribute(k_emit_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_emit_b, DUP_THREADS, sm);
-    resident = (int64_t)std::max(per, 1) * std::max(sms, 1);
+    res() = (int64_t)std::max(per, 1) * std::max(sms, 1);
   }
+  const int64_t resident = res();
   const unsigned egrid =
       (unsigned)std::min<int64_t>((w.P_cap + EB_CHUNK - 1) / EB_CHUNK, resident);
   k_emit_b<<<egrid, DUP_THREADS, sm, s>>>(w.val_depth[0], tiles_x, tiles_x * tiles_y, w, fs);

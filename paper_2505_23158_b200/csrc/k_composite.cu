@@ -148,6 +148,7 @@ struct CompParams {
   uint32_t *alive;            // bitmap of tiles the second phase resumes
   float4 *state;              // (T, r, g, b) per pixel of those tiles
   uint32_t n_list, n_payload;  // capacities of the list and payload buffers (bounds checks)
+  uint32_t n_maxw;             // entries of the caller's max-weight buffer (bounds check)
 };
 
 // MODE < 0: need_image / record_max from cpar.flags at run time (EXACT);
@@ -590,7 +591,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
         const int j = tid + h * CT;
         if (j < n) {
           const uint32_t src = PL[j].src;
-          if (src >= cpar.n_payload) {  // a record this frame did not write
+          if (src >= cpar.n_maxw) {  // an input beyond the max-weight buffer
             raise_fault(fs, FAULT_SRC);
             continue;
           }
@@ -661,15 +662,15 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
 template <bool EXACT, int MODE, int PH = 0>
 static void launch_comp(const Work &w, FrameState *fs, int32_t W, int32_t H,
                         const lodge_raster_params &rp, int32_t flags, const lodge_frame_out &out,
-                        cudaStream_t s) {
+                        uint32_t n_maxw, cudaStream_t s) {
   const int32_t tiles_x = (W + 15) / 16, tiles_y = (H + 15) / 16;
   const unsigned T = (unsigned)(tiles_x * tiles_y);
   const size_t sm = sizeof(CompSmem<EXACT>);
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (!attr()) {
     cudaFuncSetAttribute(k_composite<EXACT, MODE, PH>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = true;
+    attr() = 1;
   }
   CompParams cp;
   cp.rp = rp;
@@ -684,6 +685,7 @@ static void launch_comp(const Work &w, FrameState *fs, int32_t W, int32_t H,
   cp.state = w.state;
   cp.n_list = (uint32_t)std::min<int64_t>(2 * w.P_cap, 0xffffffffll);
   cp.n_payload = (uint32_t)w.M_cap;
+  cp.n_maxw = n_maxw;
   k_composite<EXACT, MODE, PH><<<T, CC<EXACT>::CT, sm, s>>>(
       w.list, PH == 2 ? w.tile_start_b : w.tile_start, PH == 2 ? w.tile_order_b : w.tile_order,
       w.payload, w.precise, fs, cp, out.image_dev, out.visible_dev, out.maxw_dev);
@@ -692,28 +694,28 @@ static void launch_comp(const Work &w, FrameState *fs, int32_t W, int32_t H,
 template <int MODE>
 static void launch_fast(const Work &w, FrameState *fs, int32_t W, int32_t H,
                         const lodge_raster_params &rp, int32_t flags, const lodge_frame_out &out,
-                        cudaStream_t s, int phase) {
+                        uint32_t n_maxw, cudaStream_t s, int phase) {
   switch (phase) {
-    case 1: launch_comp<false, MODE, 1>(w, fs, W, H, rp, flags, out, s); break;
-    case 2: launch_comp<false, MODE, 2>(w, fs, W, H, rp, flags, out, s); break;
-    default: launch_comp<false, MODE, 0>(w, fs, W, H, rp, flags, out, s); break;
+    case 1: launch_comp<false, MODE, 1>(w, fs, W, H, rp, flags, out, n_maxw, s); break;
+    case 2: launch_comp<false, MODE, 2>(w, fs, W, H, rp, flags, out, n_maxw, s); break;
+    default: launch_comp<false, MODE, 0>(w, fs, W, H, rp, flags, out, n_maxw, s); break;
   }
 }
 
 void launch_composite(const Work &w, FrameState *fs, const lodge_camera *, int32_t W, int32_t H,
                       const lodge_raster_params &rp, int32_t flags, int32_t exact,
-                      const lodge_frame_out &out, uint32_t, cudaStream_t s, int phase) {
+                      const lodge_frame_out &out, uint32_t n_maxw, cudaStream_t s, int phase) {
   if (exact) {
-    launch_comp<true, -1>(w, fs, W, H, rp, flags, out, s);
+    launch_comp<true, -1>(w, fs, W, H, rp, flags, out, n_maxw, s);
     return;
   }
   const int mode = ((flags & LODGE_NEED_IMAGE) ? 1 : 0) |
                    (((flags & LODGE_RECORD_MAX) && out.maxw_dev) ? 2 : 0);
   switch (mode) {
-    case 3: launch_fast<3>(w, fs, W, H, rp, flags, out, s, phase); break;
-    case 2: launch_fast<2>(w, fs, W, H, rp, flags, out, s, phase); break;
-    case 1: launch_fast<1>(w, fs, W, H, rp, flags, out, s, phase); break;
-    default: launch_fast<0>(w, fs, W, H, rp, flags, out, s, phase); break;
+    case 3: launch_fast<3>(w, fs, W, H, rp, flags, out, n_maxw, s, phase); break;
+    case 2: launch_fast<2>(w, fs, W, H, rp, flags, out, n_maxw, s, phase); break;
+    case 1: launch_fast<1>(w, fs, W, H, rp, flags, out, n_maxw, s, phase); break;
+    default: launch_fast<0>(w, fs, W, H, rp, flags, out, n_maxw, s, phase); break;
   }
 }
 

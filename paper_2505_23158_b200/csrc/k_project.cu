@@ -698,15 +698,15 @@ __global__ void __launch_bounds__(256) k_import_batch(lodge_batch b, int64_t M, 
   }
 }
 
-static int g_sms = 0;
 static int sm_count() {
-  if (!g_sms) {
-    int dev = 0;
+  static PerDevice sms;
+  if (!sms()) {
+    int dev = 0, n = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_sms <= 0) g_sms = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    sms() = n > 0 ? n : 148;
   }
-  return g_sms;
+  return (int)sms();
 }
 
 template <typename GT, typename ST>

@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(OS_THREADS, VALS ? LODGE_OS_VMINB
 #pragma unroll
   for (int i = 0; i < OS_ITEMS; ++i) {
     const uint32_t idx = base + warp * (OS_ITEMS * 32) + i * 32 + lane;
-    k[i] = idx < n ? kin[idx] : (KI)~(KI)0;
+    k[i] = idx < n ? os_ld(kin + idx) : (KI)~(KI)0;
     // drop: culled inputs (key ~0) leave the sort here, the output holds
     // only the survivors (their count, fs->stats.M, is the later passes' n)
     const bool valid = idx < n && !(DROP && k[i] == (KI)~(KI)0);
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(OS_THREADS, VALS ? LODGE_OS_VMINB
   // the output holds n keys (DROP: the survivors, counted into stats.M)
   onesweep_partition<OS_ITEMS, NB, VALS>(S, k, vmask, part, cnt, shift, digit_off, status,
                                          fs->epoch + tk, kout, kmap, vout,
-                                         [&](uint32_t li) { return vin[base + li]; },
+                                         [&](uint32_t li) { return os_ld(vin + base + li); },
                                          DROP ? fs->stats.M : n, fs);
   __syncthreads();  // the next partition reuses the shared memory
   }
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(OS_THREADS, LODGE_OS_VMINB)
 #pragma unroll
   for (int i = 0; i < IT; ++i) {
     const uint32_t idx = base + warp * (IT * 32) + i * 32 + lane;
-    k[i] = idx < n ? (FIRST ? depth_key32(kin64[idx]) : kin32[idx]) : ~0u;
+    k[i] = idx < n ? (FIRST ? depth_key32(os_ld(kin64 + idx)) : os_ld(kin32 + idx)) : ~0u;
     const bool valid = idx < n && !(FIRST && k[i] == ~0u);
     vmask |= valid ? (1u << i) : 0u;
   }
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(OS_THREADS, LODGE_OS_VMINB)
   }
   onesweep_partition<IT, 8, true>(S, k, vmask, part, cnt, shift, digit_off, status,
                                   fs->epoch + tk, kout, [](uint32_t key) { return key; }, vout,
-                                  [&](uint32_t li) { return vin[base + li]; },
+                                  [&](uint32_t li) { return os_ld(vin + base + li); },
                                   FIRST ? fs->stats.M : n, fs);
   __syncthreads();
   }
@@ -324,13 +324,14 @@ static void os_launch(int64_t cap, cudaStream_t s, const KI *kin, KO *kout, cons
                       uint32_t *vout, const uint32_t *n_ptr, int shift, int sb,
                       const uint32_t *digit_off, uint64_t *status, FrameState *fs, int tk) {
   constexpr int64_t TILE = (int64_t)OS_THREADS * os_items<VALS, KI>();
-  static unsigned resident = 0;
+  static PerDevice res;
   const size_t sm = sizeof(OSmem<os_items<VALS, KI>(), VALS, KI, (1 << NB)>);
-  if (!resident) {
+  if (!res()) {
     cudaFuncSetAttribute(k_onesweep<VALS, KI, KO, MAP, NB, DROP>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    resident = resident_grid(k_onesweep<VALS, KI, KO, MAP, NB, DROP>, OS_THREADS, sm, 1 << 30);
+    res() = resident_grid(k_onesweep<VALS, KI, KO, MAP, NB, DROP>, OS_THREADS, sm, 1 << 30);
   }
+  const int64_t resident = res();
 #ifndef LODGE_PERSIST
 #define LODGE_PERSIST 1
 #endif
@@ -382,16 +383,68 @@ __global__ void k_depth_verify(const uint32_t *k32, const uint32_t *val, const u
 }
 #endif
 
+#ifdef LODGE_VERIFY
+// Debug check of the 64-bit frame depth order: (key, index) strictly
+// increasing -- np.lexsort((index, depth)) -- and every index an input.
+__global__ void k_depth_verify64(const uint64_t *k, const uint32_t *val, FrameState *fs) {
+  const uint32_t M = fs->stats.M, U = fs->n_sort;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < M; i += gridDim.x * blockDim.x) {
+    bool ok = val[i] < U && k[i] != ~0ull;
+    if (i + 1 < M) ok = ok && (k[i] < k[i + 1] || (k[i] == k[i + 1] && val[i] < val[i + 1]));
+    if (!ok) raise_fault(fs, FAULT_DEPTH);
+  }
+}
+
+// Debug check of the per-tile lists of a tile sort.  List members are input
+// indices; vrank holds each survivor's position in the depth order, so a
+// tile's members must have strictly increasing ranks (np.lexsort((src,
+// depth)) restricted to the tile, src/raster.py:401-423), and the list
+// ranges must lie inside the sorted pairs.
+__global__ void k_depth_rank(const uint32_t *val, uint32_t *vrank, uint32_t cap,
+                             FrameState *fs) {
+  const uint32_t M = fs->stats.M;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < M; i += gridDim.x * blockDim.x) {
+    const uint32_t g = val[i];
+    if (g < cap) vrank[g] = i;
+    else raise_fault(fs, FAULT_LISTORD);
+  }
+}
+
+__global__ void k_list_verify(const uint32_t *list, const uint32_t *tile_start, uint32_t T,
+                              const uint32_t *vrank, uint32_t cap, FrameState *fs) {
+  if (fs->stats.overflow) return;  // a discarded attempt: no lists
+  const uint32_t n = fs->n_pairs;
+  for (uint32_t t = blockIdx.x; t < T; t += gridDim.x) {
+    const uint32_t s = tile_start[t], e = tile_start[t + 1];
+    if (e < s || e > n) {
+      if (threadIdx.x == 0) raise_fault(fs, FAULT_LISTORD);
+      continue;
+    }
+    for (uint32_t i = s + threadIdx.x; i + 1 < e; i += blockDim.x) {
+      const uint32_t a = list[i], b = list[i + 1];
+      if (a >= cap || b >= cap || vrank[a] >= vrank[b]) raise_fault(fs, FAULT_LISTORD);
+    }
+  }
+}
+
+void launch_list_verify(const Work &w, FrameState *fs, uint32_t T, bool second,
+                        cudaStream_t s) {
+  if (!w.vrank) return;
+  if (!second)
+    k_depth_rank<<<296, 256, 0, s>>>(w.val_depth[0], w.vrank, (uint32_t)w.M_cap, fs);
+  k_list_verify<<<std::min<uint32_t>(T, 148 * 8), 128, 0, s>>>(
+      w.list, second ? w.tile_start_b : w.tile_start, T, w.vrank, (uint32_t)w.M_cap, fs);
+}
+#endif
+
 // Frames: four passes over 32-bit keys (u32 ping-pong in the two halves of
 // key_depth[1]; key_depth[0] keeps the full keys by input index for the tie
 // repair), sorted input indices in val_depth[0].
 void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
                        cudaStream_t s) {
   if (M_cap <= 0) return;
-#ifndef LODGE_DEPTH32
-  // the eight 64-bit passes: the 32-bit variant below faulted intermittently
-  // with several contexts rendering concurrently (its order check,
-  // LODGE_VERIFY, fired; DESIGN.md tuning record) and stays opt-in
+#ifdef LODGE_DEPTH64
+  // opt-in: the eight 64-bit passes (0.17 vs 0.12 ms per config-3 frame)
   launch_depth_sort64(w, fs, M_cap, launches, s);
   return;
 #endif
@@ -402,13 +455,14 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
   *launches += 2;
   constexpr int64_t TILE = (int64_t)OS_THREADS * LODGE_OS_ITEMS_D;
   const size_t sm = sizeof(OSmem<LODGE_OS_ITEMS_D, true, uint32_t, 256>);
-  static unsigned resident = 0;
-  if (!resident) {
+  static PerDevice res;
+  if (!res()) {
     cudaFuncSetAttribute(k_depth_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaFuncSetAttribute(k_depth_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
-    resident = resident_grid(k_depth_pass<true>, OS_THREADS, sm, 1 << 30);
+    res() = resident_grid(k_depth_pass<true>, OS_THREADS, sm, 1 << 30);
   }
+  const int64_t resident = res();
   const unsigned grid = (unsigned)std::min<int64_t>((M_cap + TILE - 1) / TILE,
                                                     LODGE_PERSIST ? resident : 0x7fffffff);
   uint32_t *k32[2] = {reinterpret_cast<uint32_t *>(w.key_depth[1]),
@@ -441,6 +495,65 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
   *launches += 5;
 }
 
+// Diagnostic entry (lodge_debug_depth_sort): caller keys -> key_depth[0],
+// identity values, n_sort = n, M = the keys that are not ~0.
+__global__ void k_debug_sort_in(const uint64_t *keys, uint32_t n, uint64_t *k0, uint32_t *v0,
+                                FrameState *fs) {
+  __shared__ uint32_t s_m;
+  if (threadIdx.x == 0) s_m = 0;
+  __syncthreads();
+  uint32_t m = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    k0[i] = k;
+    v0[i] = i;
+    m += k != ~0ull ? 1u : 0u;
+  }
+  atomicAdd(&s_m, m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(&fs->stats.M, s_m);
+    if (blockIdx.x == 0) fs->n_sort = n;
+  }
+}
+
+__global__ void k_debug_sort_out(const uint64_t *k0, const uint32_t *v0, FrameState *fs,
+                                 uint64_t *ko, uint32_t *vo, uint32_t *m_out) {
+  const uint32_t M = fs->stats.M;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < M; i += gridDim.x * blockDim.x) {
+    ko[i] = k0[i];
+    vo[i] = v0[i];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    m_out[0] = M;
+    m_out[1] = fs->stats.fault;
+  }
+}
+
+void launch_debug_depth_sort(const Work &w, FrameState *fs, const uint64_t *keys, uint32_t n,
+                             uint64_t *ko, uint32_t *vo, uint32_t *m_out, cudaStream_t s) {
+  k_debug_sort_in<<<296, 256, 0, s>>>(keys, n, w.key_depth[0], w.val_depth[0], fs);
+  int32_t nl = 0;
+  launch_depth_sort(w, fs, n, &nl, s);
+  k_debug_sort_out<<<296, 256, 0, s>>>(w.key_depth[0], w.val_depth[0], fs, ko, vo, m_out);
+}
+
+#ifdef LODGE_VERIFY_PASS
+// Debug check after 64-bit pass p: the output is ordered by the digits
+// 0..p (the LSD invariant), stable (equal digit prefixes keep the index
+// order of pass 0's input), fault bit 1 << (16 + p).
+__global__ void k_pass_verify64(const uint64_t *k, const uint32_t *v, int shift, int p,
+                                FrameState *fs) {
+  const uint32_t M = fs->stats.M;
+  const uint64_t mask = shift >= 56 ? ~0ull : ((1ull << (shift + 8)) - 1ull);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i + 1 < M;
+       i += gridDim.x * blockDim.x) {
+    const uint64_t a = k[i] & mask, b = k[i + 1] & mask;
+    if (a > b || (a == b && v[i] >= v[i + 1])) raise_fault(fs, 1u << (16 + p));
+  }
+}
+#endif
+
 // Cost tables: eight passes over the full 64-bit keys (the sorted keys are
 // read back in key_depth[0]).
 void launch_depth_sort64(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
@@ -462,7 +575,13 @@ void launch_depth_sort64(const Work &w, FrameState *fs, int64_t M_cap, int32_t *
            p == 0 ? &fs->n_sort : &fs->stats.M, 8 * p, 32, fs->off_depth[p], w.status, fs,
            TK_DEPTH0 + p);
     ++*launches;
+#ifdef LODGE_VERIFY_PASS
+    k_pass_verify64<<<296, 256, 0, s>>>(w.key_depth[a ^ 1], w.val_depth[a ^ 1], 8 * p, p, fs);
+#endif
   }
+#ifdef LODGE_VERIFY
+  k_depth_verify64<<<296, 256, 0, s>>>(w.key_depth[0], w.val_depth[0], fs);
+#endif
 }
 
 static int bit_width(uint64_t v) {

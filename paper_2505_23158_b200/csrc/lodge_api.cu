@@ -52,6 +52,13 @@ struct lodge_ctx {
   }
 };
 
+// LODGE_DEBUG_ALLOC=1: log every workspace allocation (pointer, bytes) to stderr
+static void log_alloc(const lodge_ctx *c, const char *what, const void *p, int64_t bytes) {
+  static const bool on = getenv("LODGE_DEBUG_ALLOC") != nullptr;
+  if (on) fprintf(stderr, "[lodge alloc] ctx %p %s %p %lld\n", (const void *)c, what, p,
+                  (long long)bytes);
+}
+
 static int ensure_M(lodge_ctx *c, int64_t need) {
   Work &w = c->w;
   if (need <= w.M_cap && w.payload) return 0;
@@ -59,7 +66,8 @@ static int ensure_M(lodge_ctx *c, int64_t need) {
   cudaFree(w.key_depth[0]); cudaFree(w.key_depth[1]);
   cudaFree(w.val_depth[0]); cudaFree(w.val_depth[1]);
   cudaFree(w.rect); cudaFree(w.payload); cudaFree(w.precise);
-  cudaFree(w.rect_sorted); cudaFree(w.splat_off);
+  cudaFree(w.rect_sorted); cudaFree(w.splat_off); cudaFree(w.vrank);
+  w.vrank = nullptr;
   w.M_cap = 0;
   CK(cudaMalloc(&w.rect_sorted, 8 * ncap));
   CK(cudaMalloc(&w.splat_off, 4 * (ncap + 1)));
@@ -70,7 +78,14 @@ static int ensure_M(lodge_ctx *c, int64_t need) {
   CK(cudaMalloc(&w.rect, 8 * ncap));
   CK(cudaMalloc(&w.payload, sizeof(Payload) * ncap));
   CK(cudaMalloc(&w.precise, sizeof(Precise) * ncap));
+#ifdef LODGE_VERIFY
+  CK(cudaMalloc(&w.vrank, 4 * ncap));
+#endif
   w.M_cap = ncap;
+  log_alloc(c, "key_depth0", w.key_depth[0], 8 * ncap);
+  log_alloc(c, "key_depth1", w.key_depth[1], 8 * ncap);
+  log_alloc(c, "val_depth0", w.val_depth[0], 4 * ncap);
+  log_alloc(c, "val_depth1", w.val_depth[1], 4 * ncap);
   return 0;
 }
 
@@ -85,6 +100,7 @@ static int ensure_status(lodge_ctx *c, int64_t words) {
   CK(cudaMalloc(&w.status, 8 * ncap));
   CK(cudaMemset(w.status, 0, 8 * ncap));  // epoch 0 is never used
   w.status_cap = ncap;
+  log_alloc(c, "status", w.status, 8 * ncap);
   return 0;
 }
 
@@ -201,6 +217,7 @@ int lodge_create(int32_t device, lodge_ctx **out) {
   }
   CK(cudaMalloc(&c->fs, sizeof(FrameState)));
   CK(cudaMemset(c->fs, 0, sizeof(FrameState)));
+  log_alloc(c, "fs", c->fs, sizeof(FrameState));
   CK(cudaMalloc(&c->cam_dev, sizeof(lodge_camera)));
   CK(cudaMallocHost(&c->cam_host, sizeof(lodge_camera)));
   CK(cudaMallocHost(&c->stats_host, sizeof(lodge_frame_stats)));
@@ -219,7 +236,7 @@ void lodge_destroy(lodge_ctx *c) {
                   w.payload, w.precise, w.pairs[0], w.pairs[1], w.tile_diff, w.tile_start,
                   w.status, w.union_idx, w.union_tag, c->fs, c->cam_dev, w.rect_sorted,
                   w.splat_off, w.chunk_first, w.tile_order, w.tile_diff_a, w.count_all,
-                  w.tile_start_b, w.tile_order_b, w.alive, w.sat, w.state};
+                  w.tile_start_b, w.tile_order_b, w.alive, w.sat, w.state, w.vrank};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c->cam_host) cudaFreeHost(c->cam_host);
@@ -383,7 +400,8 @@ int lodge_rasterize(lodge_ctx *c, const lodge_batch *b, int64_t M, int64_t n_inp
   Work &w = c->w;
   launch_duplicate(w, c->fs, tiles_x, M, s);
   launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s);
-  launch_composite(w, c->fs, c->cam_dev, cam->w, cam->h, *rp, flags, exact, *out, 0, s);
+  launch_composite(w, c->fs, c->cam_dev, cam->w, cam->h, *rp, flags, exact, *out,
+                   (uint32_t)n_inputs, s);
   if (tile_offsets && tile_src) launch_export_lists(w, c->fs, T, tile_offsets, tile_src, list_cap, s);
   rc = check_launch("lodge_rasterize");
   if (rc) return rc;
@@ -508,9 +526,13 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
     DSYNC("launch_dup_emit");
     c->mark(6);
     launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s);
+#ifdef LODGE_VERIFY
+    launch_list_verify(w, c->fs, (uint32_t)(tiles_x * tiles_y), false, s);
+#endif
     DSYNC("launch_tile_sort");
     c->mark(7);
-    launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, 0, s, 1); ++nl;
+    launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, (uint32_t)U_cap, s, 1);
+    ++nl;
     DSYNC("launch_composite");
     DSYNC_L(2, "segment: count .. first-phase composite");
     c->mark(8);
@@ -524,8 +546,12 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
     DSYNC("launch_payload (second phase)");
     nl += 4;
     launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s, TK_TILEB0);
+#ifdef LODGE_VERIFY
+    launch_list_verify(w, c->fs, (uint32_t)(tiles_x * tiles_y), true, s);
+#endif
     DSYNC("launch_tile_sort (second phase)");
-    launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, 0, s, 2); ++nl;
+    launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, (uint32_t)U_cap, s, 2);
+    ++nl;
     DSYNC("launch_composite (second phase)");
     DSYNC_L(2, "segment: second phase");
     c->mark(9);
@@ -540,9 +566,13 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
     DSYNC("launch_duplicate");
     c->mark(6);
     launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s);
+#ifdef LODGE_VERIFY
+    launch_list_verify(w, c->fs, (uint32_t)(tiles_x * tiles_y), false, s);
+#endif
     DSYNC("launch_tile_sort");
     c->mark(7);
-    launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, 0, s); ++nl;
+    launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, (uint32_t)U_cap, s);
+    ++nl;
     DSYNC("launch_composite");
     c->mark(8);
     c->mark(9);
@@ -720,6 +750,23 @@ int lodge_debug_counters(lodge_ctx *c, uint64_t *out8) {
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaMemcpy(out8, c->fs->counters, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return 0;
+}
+
+int lodge_debug_depth_sort(lodge_ctx *c, const uint64_t *keys_dev, int64_t n,
+                           uint64_t *sorted_keys_dev, uint32_t *sorted_idx_dev,
+                           uint32_t *out_m_dev) {
+  if (!c || (n > 0 && (!keys_dev || !sorted_keys_dev || !sorted_idx_dev)) || !out_m_dev)
+    return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  if (n < 0 || n > 0x3fffffff) return set_err(LODGE_ERR_BAD_ARG, "bad key count");
+  CK(cudaSetDevice(c->device));
+  int rc;
+  if ((rc = ensure_M(c, std::max<int64_t>(n, 1))) ||
+      (rc = ensure_status(c, (c->w.M_cap + 4095) / 4096 * 256 + 256)))
+    return rc;
+  launch_begin_frame(c->fs, c->stream);
+  launch_debug_depth_sort(c->w, c->fs, keys_dev, (uint32_t)n, sorted_keys_dev, sorted_idx_dev,
+                          out_m_dev, c->stream);
+  return check_launch("lodge_debug_depth_sort");
 }
 
 int lodge_asset_split(lodge_ctx *c, const void *blob_dev, int64_t n, int32_t sh_degree,

@@ -13,6 +13,11 @@ namespace lodge {
 
 constexpr int OS_THREADS = 256;
 
+template <typename T>
+__device__ __forceinline__ T os_ld(const T *p) {
+  return *p;
+}
+
 // peers &= lanes whose bit (d & MASK) equals this lane's (bit test, ballot and
 // two predicated ANDs; nvcc's own lowering spends six instructions here).
 template <uint32_t MASK>
@@ -137,6 +142,12 @@ __device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI, (1 << 
     S.dstart[dg] = wpre + inc - tot;
   }
   __syncthreads();
+#ifdef LODGE_VERIFY
+  if (dg < D) {  // debug builds: digit runs tile [0, cnt_valid)
+    const uint32_t nxt = dg + 1 < D ? S.dstart[dg + 1] : cnt_valid;
+    if (S.dstart[dg] + tot != nxt) raise_fault(fs, FAULT_STAGE);
+  }
+#endif
   // look-back across partitions for digit dg (threads < D), overlapped with
   // the staging of this partition's keys by every warp: the staging needs only
   // the partition-local offsets, the global scatter below needs the look-back
@@ -169,8 +180,21 @@ __device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI, (1 << 
       }
       st_store(st + dg, st_pack(epoch, ST_PREFIX, excl + tot));
     }
-    S.gbase[dg] = digit_off[dg] + excl;
+    S.gbase[dg] = os_ld(digit_off + dg) + excl;
   }
+  // Reconverge the warp.  Each lane spun on its own digit's predecessor cell
+  // above, so the lanes leave the look-back at different times, and the
+  // compiler cannot force reconvergence after a spin loop (forward progress
+  // under independent thread scheduling).  A warp still diverged here would
+  // reach the staging and then __syncthreads() -- bar.sync, an *aligned*
+  // barrier that every lane of a warp must execute together -- part by part:
+  // the barrier could release the CTA before the late lanes staged their
+  // keys, and the scatter then read stale slots (round 1's intermittent
+  // wrong orders under concurrent contexts).  LODGE_OS_NO_RECONVERGE
+  // rebuilds that defect, for the stress tests' positive control.
+#ifndef LODGE_OS_NO_RECONVERGE
+  __syncwarp();
+#endif
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     if ((vmask >> i) & 1u) {
@@ -185,6 +209,12 @@ __device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI, (1 << 
   for (uint32_t j = tid; j < cnt_valid; j += OS_THREADS) {
     const KI key = S.keys[j];
     const uint32_t dd = (uint32_t)((key >> shift) & DM);
+#ifdef LODGE_VERIFY
+    {  // debug builds: the staged key lies in its digit's run
+      const uint32_t e = dd + 1 < D ? S.dstart[dd + 1] : cnt_valid;
+      if (j < S.dstart[dd] || j >= e) raise_fault(fs, FAULT_STAGE);
+    }
+#endif
     const uint32_t out = S.gbase[dd] + (j - S.dstart[dd]);
     if (out >= n_out) {  // digit offsets inconsistent with the keys
       raise_fault(fs, FAULT_SCATTER);

@@ -138,6 +138,10 @@ def score_active_selection(levels: Sequence, sets: Sequence, views: Sequence,
         while batch:
             render(batch)
             st = read(batch)
+            bad = [i for i in batch if st[i].fault]
+            if bad:  # a skipped write would leave the scores too low
+                raise RuntimeError("liblodge: device bounds check fired while scoring "
+                                   f"(views {bad[:8]}, fault bits {st[bad[0]].fault:#x})")
             redo = [i for i in batch if st[i].overflow]
             if redo:
                 r.reserve(int(max(st[i].P for i in redo) * 1.25) + 4096)

@@ -144,9 +144,11 @@ def project_gaussian(g, camera, cfg: RasterConfig = RasterConfig()):
 
 
 def rasterize_device(db: DeviceBatch, camera, cfg=RasterConfig(), need_image=True,
-                     record_max_weight=True, precision=None, lists=False, device=None):
-    """Bin, sort and composite a device batch; returns device tensors."""
-    ctx = context(device)
+                     record_max_weight=True, precision=None, lists=False, device=None,
+                     ctx=None):
+    """Bin, sort and composite a device batch; returns device tensors.
+    ctx: a device.Context to run on (default: the device's shared one)."""
+    ctx = ctx or context(device)
     dev = ctx.device
     w, h = (int(v) for v in camera.resolution)
     tx, ty = _tiles(camera)
@@ -194,6 +196,9 @@ def rasterize_device(db: DeviceBatch, camera, cfg=RasterConfig(), need_image=Tru
         N.check(lib.lodge_rasterize(ctx.bind(prec), C.byref(bs), M, db.n_inputs, C.byref(cam),
                                     C.byref(rp), flags, C.byref(out), None, None, 0,
                                     C.byref(res["stats"])), "lodge_rasterize")
+    if res["stats"].fault:
+        raise N.LodgeError("lodge_rasterize: device bounds check fired "
+                           f"(fault bits {res['stats'].fault:#x})")
     return res
 
 

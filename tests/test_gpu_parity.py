@@ -152,6 +152,33 @@ def test_config1_render_selection(c1, c1_objects, v, prec):
     (check_exact if prec == "exact" else check_fast)(res, c1, p + "o_")
 
 
+@pytest.mark.parametrize("v", [5, 7])
+@pytest.mark.parametrize("prec", ["exact", "fast"])
+def test_config1_rasterize_fresh_context(c1, c1_objects, v, prec):
+    """lodge_rasterize on a context whose workspace has never grown: the
+    views' n_inputs (5991) exceed max(M, 4096), and max weights of inputs at
+    index >= 4096 must land (the bound is the caller's max-weight buffer,
+    not the payload capacity)."""
+    levels, _ = c1_objects
+    p = f"v{v}/"
+    cam = camera(c1, p)
+    sets = [c1[p + f"sel{l}"] for l in range(len(levels))]
+    mods = [c1[p + f"mod{l}"] for l in range(len(levels))]
+    db = L.lod.project_selection_device(levels, sets, cam, L.RasterConfig(), mods)
+    assert db.n_inputs > max(len(db), 4096)
+    ref = c1[p + "o_maxw"]
+    assert np.count_nonzero(ref[4096:]) > 0
+    fresh = D.Context(D.context().device)
+    res = rasterize_device(db, cam, L.RasterConfig(), True, True, precision=prec, ctx=fresh)
+    assert res["stats"].fault == 0
+    mw = res["maxw"].double().cpu().numpy()
+    if prec == "exact":
+        np.testing.assert_allclose(mw, ref, rtol=1e-12, atol=1e-300)
+    else:
+        np.testing.assert_allclose(mw, ref, atol=2e-3)
+        assert ref[4096:].max() > 0.01  # so a dropped write would fail the bar
+
+
 @pytest.mark.parametrize("prec", ["exact", "fast"])
 def test_config1_fused_frame(c1, c1_objects, prec):
     """lodge_render_frame (device-side select -> ... -> composite) vs golden."""
