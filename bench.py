@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--phase-budget", type=int, default=1280,
                     help="FAST frames: first-phase pairs per tile of the two depth phases "
                          "(lodge_set_phase_budget); 0 = one pass over the full lists")
+    ap.add_argument("--exact-steps", type=int, default=2,
+                    help="steps of the secondary EXACT-precision (fp64 compositing) sample")
     ap.add_argument("--mode", default="blend", choices=["blend", "chunks", "lod", "full"],
                     help="render mode of the reference CLI (src/cli.py:219-243); the "
                          "metric is quoted on blend")
@@ -80,12 +82,23 @@ def workload_name(cfg_name):
             "street1080": "46k-Gaussian street, 2 LODs, 4 chunks, SH1, 1920x1080"}[cfg_name]
 
 
-def my_views(rank, world, n_steps_total, block):
+def schedules(rank, world, steps, warmup, block):
     """Block-cyclic view assignment (paper_2505_23158_b200/shard.py): block b
-    of `block` consecutive sweep views goes to rank b % world; step s of this
-    rank uses its s-th block (cyclic)."""
-    from paper_2505_23158_b200.shard import step_schedule
-    return step_schedule(SWEEP_VIEWS, world, rank, n_steps_total, block)
+    of `block` consecutive sweep views goes to rank b % world.  The timed
+    steps take this rank's blocks spread evenly over the whole 4096-view
+    sweep (step s -> block floor((s + 1/2) * n_mine / steps)); the warm-up
+    steps take blocks in between."""
+    from paper_2505_23158_b200.shard import spread_schedule
+    return (spread_schedule(SWEEP_VIEWS, world, rank, steps, block, 0.5),
+            spread_schedule(SWEEP_VIEWS, world, rank, warmup, block, 0.0))
+
+
+def config_of(args, W=1920, H=1080):
+    """The workload definition, identical in both arms (run statistics go
+    under "run")."""
+    return {"workload": workload_name(args.config), "mode": args.mode, "resolution": [W, H],
+            "sweep_views": SWEEP_VIEWS, "views_per_block": BLOCK,
+            "schedule": "block-cyclic over ranks, timed blocks spread over the sweep"}
 
 
 # ---------------------------------------------------------------------------
@@ -173,8 +186,8 @@ def stage_bytes(U, AB, M, P, W, H, sh_terms, geom_bytes=48, sh_elem=4, P1=None, 
     """Algorithmic bytes per frame of each stage.
     Two-phase frames (P1 = pairs of the first depth phase < P): tile_setup is
     the counting pass, duplicate / tile_sort / composite the first phase,
-    second_phase the enumeration, compaction, sort and compositing of the
-    P2 pairs the unfinished tiles still need."""
+    second_phase the enumeration, compaction and sort of the P2 pairs the
+    unfinished tiles still need, composite_b their compositing."""
     sh_b = 3 * sh_terms * sh_elem
     two = P1 is not None and (P1 < P or P2 > 0)
     P1 = P if P1 is None else P1
@@ -188,15 +201,19 @@ def stage_bytes(U, AB, M, P, W, H, sh_terms, geom_bytes=48, sh_elem=4, P1=None, 
         "union": 4.0 * AB + 5.0 * U,
         # geometry only: union slot + record in, key + index + rectangle out
         "project": U * (5.0 + geom_bytes + 12.0) + M * 8.0,
-        # eight 64-bit passes: histogram of the keys, then per pass the u64 key
-        # + u32 index read and written (the first pass reads all U inputs)
-        "depth_sort": U * (8.0 + 12.0) + M * 12.0 + 7 * M * 24.0,
+        # 32-bit keys: histogram read of the U u64 keys; pass 1 reads the U
+        # u64 keys + u32 indices and writes M u32 keys + indices; three passes
+        # read and write M x 8 B; the tie repair reads the M sorted keys
+        "depth_sort": U * 8.0 + U * 12.0 + M * 8.0 + 3 * M * 16.0 + M * 4.0,
         "tile_setup": (count if two else 0.0) + M1 * payload,
         "duplicate": P1 * 8.0 if two else M * 12.0 + P * 8.0,
         # pass 1 reads u64 pairs, writes packed u32; pass 2 reads and writes u32
         "tile_sort": (8.0 + 4.0 + 4.0 + 4.0) * P1,
-        "composite": P1 * 4.0 + M * 64.0 + W * H * 16.0 + U * 4.0,
-        "second_phase": (M * 8.0 + M2 * payload + P2 * (8.0 + 20.0 + 4.0)) if two else 0.0,
+        "composite": P1 * 4.0 + M1 * 64.0 + W * H * 16.0 + U * 4.0,
+        # owner scan over the later splats' rectangles, their compositing
+        # records, the emitted pairs (8 B) and their two tile passes (20 B)
+        "second_phase": (M * 8.0 + M2 * payload + P2 * (8.0 + 20.0)) if two else 0.0,
+        "composite_b": (P2 * 4.0 + M2 * 64.0) if two else 0.0,
     }
 
 
@@ -289,27 +306,30 @@ def run_reference(args):
     O.set_threads(os.cpu_count() or 1)
     cfg = scenes.build(args.config, threads=os.cpu_count() or 1)
     sweep = cfg.sweep(SWEEP_VIEWS)
-    views = [v for blk in my_views(0, 1, args.warmup + args.steps, BLOCK) for v in blk[:1]]
-    for v in views[:args.warmup]:
-        cpu_render_view(cfg, sweep[v], O, args.mode)
+    timed, warm = schedules(0, 1, args.steps, args.warmup, BLOCK)
+    # one view per step: the first view of the block the GPU arm's rank 0
+    # times at that step (the same spread over the sweep)
+    for blk in warm:
+        cpu_render_view(cfg, sweep[blk[0]], O, args.mode)
     times = []
-    for v in views[args.warmup:]:
+    for blk in timed:
         t0 = time.perf_counter()
-        cpu_render_view(cfg, sweep[v], O, args.mode)
+        cpu_render_view(cfg, sweep[blk[0]], O, args.mode)
         times.append(time.perf_counter() - t0)
     total = sum(times)
     fps = len(times) / total
     cores = O.num_threads()
+    zs = [float(sweep[blk[0]].position[2]) for blk in timed]
     line = {"metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_name(args.config), "views_per_step": 1,
-                       "mode": args.mode},
+            "config": config_of(args),
             "cpu_baseline": {"value": fps, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"1 sweep view per step ({len(times)} views), oracle/ C "
-                                       f"restatement with OpenMP on {cores} threads, "
-                                       f"{cpu_model()}"},
+                             "sample": f"1 view per step ({len(times)} views, z {min(zs):.0f}.."
+                                       f"{max(zs):.0f} of the sweep, the first view of each "
+                                       f"block the GPU arm times), oracle/ C restatement with "
+                                       f"OpenMP on {cores} threads, {cpu_model()}"},
             "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -318,6 +338,11 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+FP32_LANES_PER_SM = 128   # FP32 FMA lanes per SM (sm_100)
+MUFU_PER_SM = 16          # ex2 per SM per clock (sm_100; B200_PROFILING.md)
+FLOPS_PER_PAIR = 20       # fp32 ops per (pixel, member) evaluation
+
+
 def run_lodge(args):
     import torch
     import torch.distributed as dist
@@ -325,10 +350,12 @@ def run_lodge(args):
     from fixtures import scenes
     import paper_2505_23158_b200 as LG
     from paper_2505_23158_b200 import _native as N
+    from paper_2505_23158_b200 import shard
     from paper_2505_23158_b200.device import DeviceLevel, DevicePlan
     from paper_2505_23158_b200.renderer import STATS_BYTES
 
     rank, world, local = env_rank()
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
     # LODGE_BENCH_PLUMBING=1: every rank on cuda:0 over gloo -- a check that
     # the torchrun path runs end to end on a one-GPU box (the ranks never
     # wait on each other's kernels); its numbers are not scaling numbers
@@ -341,11 +368,17 @@ def run_lodge(args):
         if plumbing:
             dist.init_process_group("gloo")
         else:
+            # NCCL's init log names every rank and its device (the driver's
+            # rank check); the data path itself exchanges nothing
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
+    barrier = dist.barrier if world > 1 else (lambda: None)
     t_setup = time.time()
-    # the host cores shared by the ranks of this node (torchrun exports
-    # OMP_NUM_THREADS=1)
-    cfg = scenes.build(args.config, threads=max(1, (os.cpu_count() or 1) // world))
+    # the fixture is generated once per node (local rank 0, every host core)
+    # and memory-mapped by the node's other ranks
+    cfg = scenes.build_shared(args.config, local, local_world, barrier,
+                              key=os.environ.get("MASTER_PORT", ""))
     store = None
     if args.residency == "stream":
         # residency-bounded store: chunk slabs streamed into args.slots slots
@@ -359,18 +392,22 @@ def run_lodge(args):
                                                    dev))
         store_gb = store.resident_bytes() / 1e9
     else:
-        levels = [DeviceLevel.from_tensors(torch.from_numpy(g).to(dev),
-                                           torch.from_numpy(s).to(dev), cfg.degree)
-                  for g, s, _ in cfg.levels]
-        plan = DevicePlan.from_arrays(cfg.centers, cfg.offsets, cfg.data, cfg.L, dev)
+        import warnings
+        with warnings.catch_warnings():  # memory-mapped (read-only) fixture arrays
+            warnings.simplefilter("ignore", UserWarning)
+            levels = [DeviceLevel.from_tensors(torch.from_numpy(g).to(dev),
+                                               torch.from_numpy(s).to(dev), cfg.degree)
+                      for g, s, _ in cfg.levels]
+        plan = DevicePlan.from_arrays(cfg.centers, cfg.offsets, np.asarray(cfg.data), cfg.L,
+                                      dev)
         store_gb = sum(l.nbytes() for l in levels) / 1e9
     r = LG.Renderer(levels, plan, device=dev, storage="fp32", precision=args.precision,
                     n_streams=args.streams, phase_budget=args.phase_budget)
     B = args.views_per_step
-    schedule = my_views(rank, world, args.warmup + args.steps, B)
+    timed, warm = schedules(rank, world, args.steps, args.warmup, B)
     sweep = cfg.sweep(SWEEP_VIEWS)
     W, H = sweep[0].resolution
-    flat = sorted({v for blk in schedule for v in blk})
+    flat = sorted({v for blk in timed + warm for v in blk})
     pos = {v: i for i, v in enumerate(flat)}
     cams = r.upload_cameras([sweep[v] for v in flat])
     frames = [r.alloc_frame(W, H) for _ in range(B)]
@@ -380,23 +417,22 @@ def run_lodge(args):
     pairs = ({v: host_pair(cfg.centers, sweep[v].position) for v in flat}
              if store is not None else None)
 
-    def do_render(cam_row, frame, slot, v):
+    def do_render(rr, cam_row, frame, slot, v):
         """One frame of args.mode (the CLI's render modes, src/cli.py:219-243)."""
         if store is not None:  # chunk pair decided on the host, slabs made resident
             f, o, t = pairs[v]
             if args.mode == "chunks":
                 o, t = None, 1.0
-            st = r.stream_of(slot)
+            st = rr.stream_of(slot)
             store.require([f, o], st)
-            r.render(cam_row, frame, pair=(f, o), t=t, slot=slot)
+            rr.render(cam_row, frame, pair=(f, o), t=t, slot=slot)
             store.release([f, o], st)
         elif args.mode == "blend":
-            r.render(cam_row, frame, slot=slot)
+            rr.render(cam_row, frame, slot=slot)
         elif args.mode == "chunks":
-            r.render(cam_row, frame, pair=(near[v], None), slot=slot)
+            rr.render(cam_row, frame, pair=(near[v], None), slot=slot)
         else:
-            r.render_lod(cam_row, frame, bounds, full=args.mode == "full", slot=slot)
-    stats_all = torch.zeros((n_timed, STATS_BYTES), dtype=torch.uint8, device=dev)
+            rr.render_lod(cam_row, frame, bounds, full=args.mode == "full", slot=slot)
 
     def read_stats(t):
         raw = t.cpu().numpy()
@@ -407,20 +443,18 @@ def run_lodge(args):
     r.reserve(64 << 20)
     torch.cuda.synchronize()
     for i, v in enumerate(flat):
-        fr = frames[0]
-        do_render(cams[pos[v]], fr, 0, v)
+        do_render(r, cams[pos[v]], frames[0], 0, v)
         with torch.cuda.stream(r.stream_of(0)):
-            sizing[i].copy_(fr.stats)
+            sizing[i].copy_(frames[0].stats)
     torch.cuda.synchronize()
-    st_sz = read_stats(sizing)
-    P_max = max(s.P for s in st_sz)
+    P_max = max(s.P for s in read_stats(sizing))
     r.reserve(int(P_max * 1.05) + 4096)
     launches_per_frame = r.last_launch_count()
     clocks = Clocks(local)
     clocks.start()  # sampling before the timed region starts
-    for s in range(args.warmup):
-        for j, v in enumerate(schedule[s]):
-            do_render(cams[pos[v]], frames[j], j % r.n_streams, v)
+    for blk in warm:
+        for j, v in enumerate(blk):
+            do_render(r, cams[pos[v]], frames[j], j % r.n_streams, v)
     torch.cuda.synchronize()
     setup_s = time.time() - t_setup
 
@@ -429,7 +463,7 @@ def run_lodge(args):
     # region is bracketed by events on the current stream that every slot
     # stream waits on / is waited for.
     S = r.n_streams
-    r.profile(True, n_timed)
+    stats_all = torch.zeros((n_timed, STATS_BYTES), dtype=torch.uint8, device=dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -440,9 +474,9 @@ def run_lodge(args):
     for q in range(S):
         r.stream_of(q).wait_event(e0)
     k = 0
-    for s in range(args.warmup, args.warmup + args.steps):
-        for j, v in enumerate(schedule[s]):
-            do_render(cams[pos[v]], frames[j], j % S, v)
+    for blk in timed:
+        for j, v in enumerate(blk):
+            do_render(r, cams[pos[v]], frames[j], j % S, v)
             with torch.cuda.stream(r.stream_of(j % S)):
                 stats_all[k].copy_(frames[j].stats, non_blocking=True)
             k += 1
@@ -455,49 +489,40 @@ def run_lodge(args):
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    stage_ms, nprof_frames = r.profile_read()
-    r.profile(False)
-    stage_timing = "events around each stage on its stream, inside the timed region"
-    if S > 1:
-        # with frames in flight on several streams a stage's events also span
-        # the other streams' kernels: re-time the stages on one stream over
-        # the same views, serialised, right after the timed region
-        n_stage = min(n_timed, 64)
-        r.profile(True, n_stage)
-        k = 0
-        for s in range(args.warmup, args.warmup + args.steps):
-            for j, v in enumerate(schedule[s]):
-                if k < n_stage:
-                    do_render(cams[pos[v]], frames[j], 0, v)
-                k += 1
-        torch.cuda.synchronize()
-        stage_ms, nprof_frames = r.profile_read()
-        r.profile(False)
-        stage_timing = (f"events around each stage, {nprof_frames} of the timed views re-rendered "
-                        "serially on one stream after the timed region")
-    stats = read_stats(stats_all)
-    overflow = sum(s.overflow for s in stats)
-    faults = sum(1 for s in stats if s.fault)
-    ms_max = ms
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
+    ms_max = shard.max_over_ranks(ms, dev)
     total_frames = n_timed * world
     value = total_frames / (ms_max / 1000.0)
+    stats = read_stats(stats_all)
+    overflow = sum(1 for s in stats if s.overflow)
+    faults = sum(1 for s in stats if s.fault)
+
+    # ---- per-stage times: the timed views re-rendered serially on one
+    # stream (with frames in flight a stage's events would also span the
+    # other streams' kernels)
+    n_stage = min(n_timed, 64)
+    r.profile(True, n_stage)
+    k = 0
+    for blk in timed:
+        for j, v in enumerate(blk):
+            if k < n_stage:
+                do_render(r, cams[pos[v]], frames[j], 0, v)
+            k += 1
+    torch.cuda.synchronize()
+    stage_ms, nprof_frames = r.profile_read()
+    r.profile(False)
+    stage_timing = (f"events around each stage, {nprof_frames} of the timed views re-rendered "
+                    "serially on one stream after the timed region")
 
     # ---- per-stage roofline ----------------------------------------------
-    U = np.mean([s.U for s in stats])
-    M = np.mean([s.M for s in stats])
-    P = np.mean([s.P for s in stats])
+    mean = lambda f: float(np.mean([f(s) for s in stats]))  # noqa: E731
+    U, M, P = mean(lambda s: s.U), mean(lambda s: s.M), mean(lambda s: s.P)
+
     def set_total(j):  # sum over levels of |set(j, l)|
         return int(cfg.offsets[(j + 1) * cfg.L] - cfg.offsets[j * cfg.L]) if j >= 0 else 0
 
-    AB = np.mean([set_total(s.f) + set_total(s.o) for s in stats])
-    P1 = np.mean([s.P_first for s in stats])
-    P2 = np.mean([s.P_second for s in stats])
-    M1 = np.mean([s.M_first for s in stats])
-    M2 = np.mean([s.M_second for s in stats])
+    AB = mean(lambda s: set_total(s.f) + set_total(s.o))
+    P1, P2 = mean(lambda s: s.P_first), mean(lambda s: s.P_second)
+    M1, M2 = mean(lambda s: s.M_first), mean(lambda s: s.M_second)
     sb = stage_bytes(U, AB, M, P, W, H, (cfg.degree + 1) ** 2, P1=P1, P2=P2, M1=M1, M2=M2)
     peak, peak_kind = load_peaks()
     stages = {}
@@ -506,19 +531,67 @@ def run_lodge(args):
         gbs = sb[name] / (per / 1000.0) / 1e9 if per > 0 else 0.0
         stages[name] = {"ms_per_frame": round(per, 5), "bytes_per_frame": round(sb[name]),
                         "GB_s": round(gbs, 1), "frac": round(gbs / peak, 4)}
-    # second_phase mixes a sort with compositing: reported under stages only
+    # compositing (K6) against the FP32 and MUFU pipes:
+    # E = 256 * sum over tiles of m_t pixel-member evaluations per frame
+    m_t = mean(lambda s: s.comp_members)
+    E = 256.0 * m_t
+    t_comp = (stages["composite"]["ms_per_frame"] + stages["composite_b"]["ms_per_frame"]) / 1e3
+    props = torch.cuda.get_device_properties(dev)
+    sm_hz = (clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965.0) * 1e6
+    fp32_peak = props.multi_processor_count * FP32_LANES_PER_SM * 2 * sm_hz
+    mufu_peak = props.multi_processor_count * MUFU_PER_SM * sm_hz
+    compositor = {"members_iterated_per_frame": round(m_t), "E_per_frame": E,
+                  "seconds_per_frame": round(t_comp, 7),
+                  "fp32_frac": round(FLOPS_PER_PAIR * E / t_comp / fp32_peak, 4) if t_comp else None,
+                  "mufu_frac": round(E / t_comp / mufu_peak, 4) if t_comp else None,
+                  "fp32_peak_tflops": round(fp32_peak / 1e12, 1),
+                  "mufu_peak_tex2": round(mufu_peak / 1e12, 2),
+                  "clock_mhz": round(sm_hz / 1e6), "sms": props.multi_processor_count,
+                  "note": "E = 256 x members a tile iterates before all its pixels have "
+                          "T < t_min (stats.comp_members, both phases); 20 fp32 ops and one "
+                          "ex2 per evaluation; time = composite + composite_b stages"}
     hbm_stages = ["union", "project", "depth_sort", "duplicate", "tile_sort"]
     dom = max(N.STAGES, key=lambda k: stages[k]["ms_per_frame"])
-    dom_hbm = max(hbm_stages, key=lambda k: stages[k]["ms_per_frame"])
-    rf_stage = dom if dom in hbm_stages else dom_hbm
+    rf_stage = max(hbm_stages, key=lambda k: stages[k]["ms_per_frame"])
     rs = stages[rf_stage]
     roofline = {"bound": "hbm", "kernel": rf_stage, "achieved": rs["GB_s"], "peak": peak,
                 "unit": "GB/s", "frac": rs["frac"], "peak_kind": peak_kind,
                 "traffic": load_traffic(rf_stage),
                 "bytes_per_launch": rs["bytes_per_frame"], "ms_per_launch": rs["ms_per_frame"],
                 "dominant_stage": dom,
-                "note": "composite is FP32/MUFU-bound, not HBM; see stages" if dom == "composite"
-                else ""}
+                "note": ("the longest HBM-bound stage; composite is FP32/MUFU-bound, see "
+                         "compositor" if dom.startswith("composite") else "")}
+
+    # ---- EXACT precision (fp64 compositing) on a short sample --------------
+    exact = None
+    if args.precision == "fast" and args.exact_steps > 0 and args.mode == "blend" \
+            and store is None:
+        rx = LG.Renderer(levels, plan, device=dev, storage="fp32", precision="exact",
+                         n_streams=S)
+        rx.reserve(int(P_max * 1.05) + 4096)
+        fx = [rx.alloc_frame(W, H) for _ in range(B)]
+        sx = timed[:args.exact_steps]
+        for j, v in enumerate(sx[0]):  # warm-up
+            rx.render(cams[pos[v]], fx[j], slot=j % S)
+        torch.cuda.synchronize()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record(cur)
+        for q in range(S):
+            rx.stream_of(q).wait_event(x0)
+        for blk in sx:
+            for j, v in enumerate(blk):
+                rx.render(cams[pos[v]], fx[j], slot=j % S)
+        for q in range(S):
+            cur.wait_stream(rx.stream_of(q))
+        x1.record(cur)
+        torch.cuda.synchronize()
+        xms = shard.max_over_ranks(x0.elapsed_time(x1), dev)
+        nx = sum(len(b) for b in sx)
+        exact = {"value": nx * world / (xms / 1000.0), "unit": UNIT, "frames": nx * world,
+                 "note": "fp64 compositing reproducing the reference's blocked transmittance "
+                         "(image <= 1e-12 of the oracle), same views, frames in flight"}
+        del rx, fx
+        torch.cuda.empty_cache()
 
     # ---- end to end through the public API --------------------------------
     e2e = None
@@ -541,14 +614,13 @@ def run_lodge(args):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        cur = torch.cuda.current_stream(dev)
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(cur)
-        for si, s in enumerate(range(args.warmup, args.warmup + args.steps)):
+        for si, blk in enumerate(timed):
             par = si & 1
             if si >= 2:
                 copied[par].synchronize()
-            for j, v in enumerate(schedule[s]):
+            for j, v in enumerate(blk):
                 cam_host[par][j].copy_(cams_host[pos[v]])
             if si >= 2:
                 for q in range(S):
@@ -557,8 +629,8 @@ def run_lodge(args):
             copied[par].record(cur)
             for q in range(S):
                 r.stream_of(q).wait_stream(cur)
-            for j, v in enumerate(schedule[s]):
-                do_render(cam_dev[par][j], frames[j], j % S, v)
+            for j, v in enumerate(blk):
+                do_render(r, cam_dev[par][j], frames[j], j % S, v)
                 r.to_srgb8(frames[j], img8[j], slot=j % S)
                 # each frame's read-back on its own stream, so it overlaps the
                 # frames still rendering instead of gating the next step
@@ -571,39 +643,44 @@ def run_lodge(args):
             cur.wait_stream(r.stream_of(q))
         f1.record(cur)
         torch.cuda.synchronize()
-        ems = f0.elapsed_time(f1)
-        if world > 1:
-            t = torch.tensor([ems], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = shard.max_over_ranks(f0.elapsed_time(f1), dev)
         e2e = {"value": total_frames / (ems / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": int(B * cams.shape[1]),
                "d2h_bytes_per_step": int(B * (H * W * 3 + STATS_BYTES)),
                "path": "Renderer.render + to_srgb8 (8-bit sRGB like splatlod render), pinned "
                        "host camera upload and image/stats read-back every step"}
 
-    # ---- gather per-rank metrics and per-view results over NCCL ------------
-    from paper_2505_23158_b200 import shard
-    per_rank = torch.tensor([ms, float(n_timed), P, float(overflow)], dtype=torch.float64,
-                            device=dev)
+    # ---- gather per-rank metrics and the timed view ids over NCCL ----------
+    per_rank = torch.tensor([ms, float(n_timed), P, float(overflow), float(faults)],
+                            dtype=torch.float64, device=dev)
     gathered = shard.gather_rows(per_rank)
-    overflow = int(gathered[:, 3].sum().item())
-    last = schedule[args.warmup + args.steps - 1]
-    view_ids = torch.tensor(last, dtype=torch.int64, device=dev)
-    sums = torch.stack([frames[j].image.double().sum().reshape(1) for j in range(len(last))])
-    g_ids, g_sums = shard.gather_views(view_ids, sums, max_per_rank=B)
-    gathered_views = {"views": int(g_ids.numel()), "image_checksum": float(g_sums.sum().item()),
-                      "how": "per-view image sums of each rank's last step, all_gather "
-                             + ("NCCL" if world > 1 else "(single rank)")}
+    overflow_all = int(gathered[:, 3].sum().item())
+    faults_all = int(gathered[:, 4].sum().item())
+    my_ids = torch.tensor([v for blk in timed for v in blk], dtype=torch.int64, device=dev)
+    last = timed[-1]
+    sums = torch.stack([frames[j].image.double().sum() for j in range(len(last))]).reshape(-1, 1)
+    g_ids, _ = shard.gather_views(my_ids, torch.zeros((my_ids.numel(), 1), device=dev),
+                                  max_per_rank=n_timed)
+    _, g_sums = shard.gather_views(torch.tensor(last, dtype=torch.int64, device=dev), sums,
+                                   max_per_rank=B)
+    ids = g_ids.cpu().numpy()
+    coverage = {"views": int(ids.size), "distinct": int(np.unique(ids).size),
+                "expected": total_frames, "first": int(ids.min()), "last": int(ids.max()),
+                "z_range": [round(float(sweep[int(ids.min())].position[2]), 1),
+                            round(float(sweep[int(ids.max())].position[2]), 1)],
+                "image_checksum_last_step": float(g_sums.sum().item()),
+                "how": "all_gather over " + ("NCCL" if world > 1 and not plumbing else
+                                            "gloo" if world > 1 else "(single rank)")}
+    coverage["all_distinct"] = coverage["distinct"] == coverage["views"] == total_frames
 
-    # ---- CPU baseline (rank 0, N=1): oracle on a bounded sample ------------
+    # ---- CPU baseline and parity sample (rank 0, after the timed region) ---
     cpu = None
     parity = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         from oracle import oracle as O
         O.lib()
         O.set_threads(os.cpu_count() or 1)
-        v = schedule[args.warmup][0]
+        v = timed[0][0]
         cam = sweep[v]
         t0 = time.perf_counter()
         for _ in range(args.cpu_views):
@@ -614,7 +691,7 @@ def run_lodge(args):
                          f"oracle/ C restatement, OpenMP {O.num_threads()} threads, "
                          f"{cpu_model()}, {dt:.1f} s/view"}
         fr = frames[0]
-        do_render(cams[pos[v]], fr, 0, v)
+        do_render(r, cams[pos[v]], fr, 0, v)
         torch.cuda.synchronize()
         st = fr.read_stats()
         img = fr.image.double().cpu().numpy()
@@ -623,47 +700,55 @@ def run_lodge(args):
         parity = {"view": int(v), "tile_count_exact": bool(np.array_equal(
             fr.tile_count.cpu().numpy(), ref["per_tile_count"])), "P": int(st.P),
             "P_oracle": int(ref["P"]), "M": int(st.M), "M_oracle": int(len(batch["src"])),
-            "image_max_abs": err, "psnr_db": (math.inf if mse == 0 else -10 * math.log10(mse))}
+            "image_max_abs": err, "psnr_db": (math.inf if mse == 0 else -10 * math.log10(mse)),
+            "lists": "bit-exact per-tile lists at this scale: tests/test_gpu_bench_parity.py"}
 
     sticky = r.fault_flags()  # every frame of the run, timed or not
-    if faults or sticky:
-        print(f"[bench] device bounds checks fired: {faults} timed frame(s), "
-              f"flags {sticky:#x}", file=sys.stderr)
+    invalid = []
+    if overflow_all:
+        invalid.append(f"{overflow_all} timed frame(s) overflowed their pair buffers")
+    if faults_all or sticky:
+        invalid.append(f"device bounds checks fired ({faults_all} timed frame(s), "
+                       f"flags {sticky:#x})")
+    if invalid:
+        print("[bench] INVALID: " + "; ".join(invalid), file=sys.stderr)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64 projection / f32 compositing (fp64 guard band)", "data": "synthetic",
-            "config": {"workload": workload_name(args.config), "mode": args.mode,
-                       "resolution": [W, H],
-                       "views_per_step_per_gpu": B, "frames_timed": total_frames,
-                       "precision": args.precision,
-                       "phase_budget": args.phase_budget if args.precision == "fast" else 0,
-                       "store": ("fp32 records, replicated" if store is None else
-                                 f"fp32 chunk slabs, {args.slots} resident slots, "
-                                 f"{store.loads} loads ({store.bytes_loaded / 1e9:.1f} GB)"),
-                       "store_gb": round(store_gb, 2),
-                       "l2": "inputs larger than L2: per-frame working set "
-                             f"~{(sb['project'] + sb['tile_sort'] + sb['composite']) / 1e9:.1f} GB"
-                             " >> 126 MB L2; no explicit flush",
-                       "mean_U": round(U), "mean_M": round(M), "mean_P": round(P),
-                       "mean_P_sorted": [round(P1), round(P2)],
-                       "mean_M_composited": [round(M1), round(M2)],
-                       "levels": cfg.n_gaussians(), "chunks": cfg.K,
-                       "pairs_per_s": P * value, "gaussians_per_s": U * value,
-                       "overflow_frames": int(overflow), "fault_frames": int(faults),
-                       "fault_flags": int(sticky),
-                       "setup_s": round(setup_s, 1)},
+            "config": config_of(args, W, H),
+            "run": {"precision": args.precision,
+                    "phase_budget": args.phase_budget if args.precision == "fast" else 0,
+                    "frames_in_flight_per_gpu": S, "views_per_step_per_gpu": B,
+                    "frames_timed": total_frames,
+                    "store": ("fp32 records, replicated" if store is None else
+                              f"fp32 chunk slabs, {args.slots} resident slots, "
+                              f"{store.loads} loads ({store.bytes_loaded / 1e9:.1f} GB)"),
+                    "store_gb": round(store_gb, 2),
+                    "l2": "inputs larger than L2: per-frame working set "
+                          f"~{(sb['project'] + sb['tile_sort'] + sb['composite']) / 1e9:.2f} GB"
+                          " and a 7.5 GB store >> 126 MB L2; no explicit flush",
+                    "mean_U": round(U), "mean_M": round(M), "mean_P": round(P),
+                    "mean_P_sorted": [round(P1), round(P2)],
+                    "mean_M_composited": [round(M1), round(M2)],
+                    "levels": cfg.n_gaussians(), "chunks": cfg.K,
+                    "pairs_per_s": P * value, "gaussians_per_s": U * value,
+                    "overflow_frames": overflow_all, "fault_frames": faults_all,
+                    "fault_flags": int(sticky), "setup_s": round(setup_s, 1)},
             "e2e": e2e, "gpu_launches": int(launches_per_frame * total_frames),
-            "roofline": roofline, "stages": stages, "stage_timing": stage_timing,
+            "roofline": roofline, "compositor": compositor, "stages": stages,
+            "stage_timing": stage_timing, "exact": exact,
             "cpu_baseline": cpu, "clocks": clk,
-            "parity_sample": parity, "gathered": gathered_views,
+            "parity_sample": parity, "gathered": coverage,
         }
+        if invalid:
+            line["invalid"] = "; ".join(invalid)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
-    return 0
+    return 1 if invalid else 0
 
 
 def main():

@@ -199,6 +199,60 @@ def build(name: str, seed: int = 7, verbose: bool = False, threads: int = 0) -> 
     return cfg
 
 
+def _scratch_dir(nbytes: int, key: str) -> str:
+    """/dev/shm when it has room for the arrays (page cache shared by the
+    ranks), else /tmp."""
+    import shutil
+    for root in ("/dev/shm", "/tmp"):
+        try:
+            if shutil.disk_usage(root).free > 1.2 * nbytes:
+                return os.path.join(root, key)
+        except OSError:
+            continue
+    return os.path.join("/tmp", key)
+
+
+def build_shared(name: str, local_rank: int, local_world: int, barrier, seed: int = 7,
+                 key: str = "") -> Config:
+    """One generation per node for multi-rank runs: local rank 0 builds the
+    config with every host core and writes its arrays (.npy) to a scratch
+    directory; the other local ranks memory-map them (no per-rank copy of the
+    ~8 GB host arrays).  barrier() must synchronise the node's ranks."""
+    import json
+    import shutil
+    if local_world <= 1:
+        return build(name, seed, threads=os.cpu_count() or 1)
+    spec = CONFIGS[name]
+    n0 = int(lib().synth_count(spec["n_fine"]))
+    est = n0 * (48 + 12 * (spec["degree"] + 1) ** 2) * 2
+    d = _scratch_dir(est, f"lodge_fixture_{name}_{seed}_{key or os.getppid()}")
+    if local_rank == 0:
+        cfg = build(name, seed, threads=os.cpu_count() or 1)
+        os.makedirs(d, exist_ok=True)
+        meta = {"name": cfg.name, "degree": cfg.degree, "length": cfg.length,
+                "L": cfg.L, "d": [float(x[2]) for x in cfg.levels], "timings": cfg.timings}
+        for l, (g, s, _) in enumerate(cfg.levels):
+            np.save(os.path.join(d, f"g{l}.npy"), g)
+            np.save(os.path.join(d, f"s{l}.npy"), s)
+        for k in ("centers", "radii", "offsets", "data", "rig_z"):
+            np.save(os.path.join(d, f"{k}.npy"), getattr(cfg, k))
+        with open(os.path.join(d, "meta.json"), "w") as f:
+            json.dump(meta, f)
+    barrier()
+    if local_rank != 0:
+        meta = json.load(open(os.path.join(d, "meta.json")))
+        ld = lambda k: np.load(os.path.join(d, f"{k}.npy"), mmap_mode="r")  # noqa: E731
+        levels = [(ld(f"g{l}"), ld(f"s{l}"), meta["d"][l]) for l in range(meta["L"])]
+        cfg = Config(meta["name"], levels, meta["degree"], np.array(ld("centers")),
+                     np.array(ld("radii")), np.array(ld("offsets")), ld("data"),
+                     np.array(ld("rig_z")), meta["length"],
+                     dict(meta["timings"], shared_from=d))
+    barrier()  # every rank has mapped the files: rank 0 may unlink them
+    if local_rank == 0:
+        shutil.rmtree(d, ignore_errors=True)
+    return cfg
+
+
 def scene_objects(cfg: Config, l: int):
     """fp64 Scene-like view of level l (for the oracle / drop-in API)."""
     g, s, _ = cfg.levels[l]

@@ -136,6 +136,9 @@ typedef struct {
                             site, internal.cuh FAULT_*); the frame's outputs are invalid */
   uint32_t M_first;      /* two-phase frames: splats of the first phase */
   uint32_t M_second;     /* two-phase frames: later splats that meet an unfinished tile */
+  uint32_t comp_members; /* compositing work: sum over tiles (and phases) of the list
+                            members a tile iterates before all its pixels have
+                            T < t_min, or its whole list (SURVEY.md 8d m_t) */
 } lodge_frame_stats;
 
 /* ---- context ---------------------------------------------------------- */
@@ -231,18 +234,39 @@ int lodge_frame_union(lodge_ctx *ctx, int32_t level, uint32_t *idx_dev, uint8_t 
 /* Stage profiling: when enabled, lodge_render_frame records CUDA events on
  * the context stream at the boundaries of its LODGE_N_STAGES stages (select,
  * union, project, depth sort, tile setup, duplicate, tile sort, composite,
- * second phase; two-phase frames count the counting pass under tile setup
- * and the first phase's emission / sort / compositing under the next three)
+ * second phase, second-phase composite; two-phase frames count the counting
+ * pass under tile setup, the first phase's emission / sort / compositing
+ * under the next three, and the second phase's enumeration, emission and
+ * sort under "second phase")
  * for up to `max_frames` frames.  lodge_profile_read synchronises those
  * events and returns the summed milliseconds per stage and the frame count,
  * then clears the record. */
-#define LODGE_N_STAGES 9
+#define LODGE_N_STAGES 10
 int lodge_profile(lodge_ctx *ctx, int32_t enable, int32_t max_frames);
 int lodge_profile_read(lodge_ctx *ctx, double *stage_ms, int32_t *frames);
 
 /* Linear [0,1] RGB (fp32, n pixels) -> 8-bit sRGB, round(srgb(x) * 255)
  * (reference src/images.py:10-17).  Async. */
 int lodge_to_srgb8(lodge_ctx *ctx, const float *image_dev, int64_t n_pixels, uint8_t *out_dev);
+
+/* ---- frame report (the reference bench's per-frame fields) -------------
+ * replaces visibility_histogram (src/raster.py:464-479) and the per-mode
+ * metrics of cmd_bench (src/cli.py:283-320) on the device.  out_dev
+ * (n_edges + 1 uint64) receives the histogram of visible (n_pixels int32)
+ * over the n_edges - 1 bins [e_i, e_{i+1}) -- the last absorbs values
+ * >= e_{n-1}, values below e_0 go to the first (np.searchsorted side=right,
+ * clipped) --, then the sum of tile_count (n_tiles int32; mean_per_tile =
+ * sum / n_tiles) and the number of nonzero max weights among n_inputs
+ * (visible_gaussians; maxw may be NULL).  edges_host: 2 <= n_edges <= 257,
+ * strictly increasing, else BAD_ARG with the reference's messages.  Async. */
+int lodge_frame_report(lodge_ctx *ctx, const int32_t *visible_dev, int64_t n_pixels,
+                       const double *edges_host, int32_t n_edges,
+                       const int32_t *tile_count_dev, int64_t n_tiles, const void *maxw_dev,
+                       int32_t maxw_fp64, int64_t n_inputs, uint64_t *out_dev);
+/* Sum of squared differences of two fp32 images of n values into *out_dev
+ * (fp64): psnr_vs_full = -10 log10(sum / n) (src/cli.py:293-294).  Async. */
+int lodge_sq_err(lodge_ctx *ctx, const float *a_dev, const float *b_dev, int64_t n,
+                 double *out_dev);
 
 /* Number of kernels the last lodge_render_frame enqueued. */
 int32_t lodge_last_launch_count(lodge_ctx *ctx);

@@ -70,7 +70,8 @@ class FrameStats(C.Structure):
                 ("U", C.c_uint32), ("U_level", C.c_uint32 * MAX_LEVELS), ("M", C.c_uint32),
                 ("P", C.c_uint32), ("overflow", C.c_uint32), ("guard_hits", C.c_uint32),
                 ("P_first", C.c_uint32), ("P_second", C.c_uint32), ("fault", C.c_uint32),
-                ("M_first", C.c_uint32), ("M_second", C.c_uint32)]
+                ("M_first", C.c_uint32), ("M_second", C.c_uint32),
+                ("comp_members", C.c_uint32)]
 
 
 class Batch(C.Structure):
@@ -112,6 +113,10 @@ EXPORTS = {
     "lodge_to_srgb8": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p], C.c_int),
     "lodge_last_launch_count": ([C.c_void_p], C.c_int32),
     "lodge_debug_counters": ([C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
+    "lodge_frame_report": ([C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_double), C.c_int32,
+                            C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int64, C.c_void_p],
+                           C.c_int),
+    "lodge_sq_err": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p], C.c_int),
     "lodge_debug_depth_sort": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                 C.c_void_p], C.c_int),
     "lodge_render_lod": ([C.c_void_p, C.POINTER(Level), C.c_int32, C.POINTER(C.c_double),
@@ -127,9 +132,9 @@ EXPORTS = {
     "lodge_asset_check_sets": ([C.c_void_p, C.POINTER(Chunks), C.POINTER(C.c_int64),
                                 C.POINTER(C.c_int32)], C.c_int),
 }
-N_STAGES = 9
+N_STAGES = 10
 STAGES = ("select", "union", "project", "depth_sort", "tile_setup", "duplicate", "tile_sort",
-          "composite", "second_phase")
+          "composite", "second_phase", "composite_b")
 
 _lib = None
 _lock = threading.Lock()

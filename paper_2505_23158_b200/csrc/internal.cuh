@@ -343,6 +343,11 @@ void launch_composite(const Work &w, FrameState *fs, const lodge_camera *cam_dev
                       int phase = 0);
 void launch_export_lists(const Work &w, FrameState *fs, int32_t T, int64_t *tile_offsets,
                          int64_t *tile_src, int64_t cap, cudaStream_t s);
+void launch_frame_report(const int32_t *visible, int64_t n_px, const double *edges_dev,
+                         int32_t n_edges, const int32_t *tile_count, int64_t n_tiles,
+                         const void *maxw, int32_t maxw_fp64, int64_t n_inputs,
+                         unsigned long long *out, cudaStream_t s);
+void launch_sq_err(const float *a, const float *b, int64_t n, double *out, cudaStream_t s);
 void launch_asset_split(const float *blob, int64_t n, int32_t width, float *geom, float *sh,
                         int32_t *flags_dev, cudaStream_t s);
 void launch_asset_sets(const lodge_chunks &ch, const int64_t *level_size_dev, int32_t *flags_dev,

@@ -137,6 +137,7 @@ struct CompSmem {
   uint32_t maxw32[CB];
   uint8_t wlist[CC<EXACT>::NW * CB];
   uint64_t bar[2];
+  uint32_t mt;  // end of the members the tile iterated (max over warps)
 };
 
 struct CompParams {
@@ -214,8 +215,12 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
     mbar_init(&S.bar[0], 1);
     mbar_init(&S.bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    S.mt = s;
   }
   __syncthreads();
+  // list position just past the last member this warp blended before all its
+  // pixels were done (compositing work, stats.comp_members)
+  uint32_t wend = s;
 
   auto issue = [&](uint32_t bb, int k) {  // stage members [bb, bb+256) into buffer k
     const int n = (int)min((uint32_t)CB, e - bb);
@@ -337,7 +342,9 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
     uint8_t *wl = S.wlist + warp * CB;
     const uint32_t wl_sa = smem_addr(wl);  // read back with 32-bit shared addressing
     int cnt = 0;
-    if (__any_sync(FULL_MASK, live_any())) {
+    const bool alive0 = __any_sync(FULL_MASK, live_any());
+    int done_i = 0;  // list entries this warp went through in this batch
+    if (alive0) {
       for (int q0 = 0; q0 < n; q0 += 32) {
         const int j = q0 + lane;
         bool hit = false;
@@ -368,7 +375,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
     c_batch += 1;
 #endif
     if (EXACT) {
-      for (int i = 0; i < cnt; ++i) {
+      for (int i = 0; i < cnt; ++i, done_i = i) {
         if (!__any_sync(FULL_MASK, live_any())) break;
 #ifdef LODGE_COUNTERS
         c_iter += 1;
@@ -583,7 +590,10 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
           one(lds_u8(wl_sa + (uint32_t)i));
         }
       }
+      done_i = i;
     }
+    if (alive0 && done_i > 0 && !__any_sync(FULL_MASK, live_any()))
+      wend = b + lds_u8(wl_sa + (uint32_t)(done_i - 1)) + 1u;
     __syncthreads();
     if (record_max) {
 #pragma unroll
@@ -626,6 +636,13 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
     if (c_batch > 16) atomicAdd(&fs->counters[6], 1ull);
   }
 #endif
+  {  // members iterated (SURVEY.md 8d m_t): the whole list while a pixel is
+     // still alive, else the furthest member a warp blended before its pixels
+     // were done
+    if (lane == 0) atomicMax(&S.mt, wend);
+    const int live = __syncthreads_or(live_any());
+    if (tid == 0) atomicAdd(&fs->stats.comp_members, live ? e - s : S.mt - s);
+  }
   bool resume = false;  // PH 1: the second phase continues this tile
   if (PH == 1) {
     resume = __syncthreads_count(live_any()) > 0 && cpar.count_all[t] > e - s;

@@ -42,6 +42,7 @@ struct lodge_ctx {
   int debug_sync = 0;  // LODGE_DEBUG_SYNC=1: check after every stage; 2: after each segment
   int32_t launches = 0;
   LevelSlots last_slots{};  // slot layout of the last union
+  double *edges_dev = nullptr;  // lodge_frame_report's bin edges (257)
   // stage profiling
   bool prof = false;
   int32_t prof_cap = 0, prof_frames = 0;
@@ -236,7 +237,8 @@ void lodge_destroy(lodge_ctx *c) {
                   w.payload, w.precise, w.pairs[0], w.pairs[1], w.tile_diff, w.tile_start,
                   w.status, w.union_idx, w.union_tag, c->fs, c->cam_dev, w.rect_sorted,
                   w.splat_off, w.chunk_first, w.tile_order, w.tile_diff_a, w.count_all,
-                  w.tile_start_b, w.tile_order_b, w.alive, w.sat, w.state, w.vrank};
+                  w.tile_start_b, w.tile_order_b, w.alive, w.sat, w.state, w.vrank,
+                  c->edges_dev};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c->cam_host) cudaFreeHost(c->cam_host);
@@ -550,11 +552,12 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
     launch_list_verify(w, c->fs, (uint32_t)(tiles_x * tiles_y), true, s);
 #endif
     DSYNC("launch_tile_sort (second phase)");
+    c->mark(9);
     launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, (uint32_t)U_cap, s, 2);
     ++nl;
     DSYNC("launch_composite (second phase)");
     DSYNC_L(2, "segment: second phase");
-    c->mark(9);
+    c->mark(10);
   } else {
     launch_payload(levels, ls, w, c->fs, cam_dev, rp, shade, w.val_depth[0], &c->fs->stats.M,
                    U_cap, s, slab_geom, slab_sh); ++nl;
@@ -576,6 +579,7 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
     DSYNC("launch_composite");
     c->mark(8);
     c->mark(9);
+    c->mark(10);
   }
   if (c->prof && c->prof_frames < c->prof_cap) ++c->prof_frames;
   if (stats_dev)
@@ -750,6 +754,41 @@ int lodge_debug_counters(lodge_ctx *c, uint64_t *out8) {
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaMemcpy(out8, c->fs->counters, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return 0;
+}
+
+int lodge_frame_report(lodge_ctx *c, const int32_t *visible_dev, int64_t n_pixels,
+                       const double *edges_host, int32_t n_edges,
+                       const int32_t *tile_count_dev, int64_t n_tiles, const void *maxw_dev,
+                       int32_t maxw_fp64, int64_t n_inputs, uint64_t *out_dev) {
+  if (!c || !edges_host || !out_dev || (n_pixels > 0 && !visible_dev) ||
+      (n_tiles > 0 && !tile_count_dev))
+    return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  if (n_edges < 2) return set_err(LODGE_ERR_BAD_ARG, "need at least two bin edges");
+  if (n_edges > 257) return set_err(LODGE_ERR_BAD_ARG, "at most 256 histogram bins");
+  for (int i = 0; i + 1 < n_edges; ++i)
+    if (!(edges_host[i + 1] > edges_host[i]))
+      return set_err(LODGE_ERR_BAD_ARG, "bin edges must be strictly increasing");
+  if (n_pixels < 0 || n_tiles < 0 || n_inputs < 0) return set_err(LODGE_ERR_BAD_ARG, "negative size");
+  CK(cudaSetDevice(c->device));
+  if (!c->edges_dev) CK(cudaMalloc(&c->edges_dev, 257 * sizeof(double)));
+  CK(cudaMemcpyAsync(c->edges_dev, edges_host, sizeof(double) * n_edges, cudaMemcpyHostToDevice,
+                     c->stream));
+  launch_frame_report(visible_dev, n_pixels, c->edges_dev, n_edges, tile_count_dev, n_tiles,
+                      maxw_dev, maxw_fp64, maxw_dev ? n_inputs : 0,
+                      reinterpret_cast<unsigned long long *>(out_dev), c->stream);
+  // (a pageable-memory copy is staged before cudaMemcpyAsync returns, so the
+  // caller may reuse edges_host at once)
+  return check_launch("lodge_frame_report");
+}
+
+int lodge_sq_err(lodge_ctx *c, const float *a_dev, const float *b_dev, int64_t n,
+                 double *out_dev) {
+  if (!c || !out_dev || (n > 0 && (!a_dev || !b_dev)))
+    return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
+  if (n < 0) return set_err(LODGE_ERR_BAD_ARG, "negative size");
+  CK(cudaSetDevice(c->device));
+  launch_sq_err(a_dev, b_dev, n, out_dev, c->stream);
+  return check_launch("lodge_sq_err");
 }
 
 int lodge_debug_depth_sort(lodge_ctx *c, const uint64_t *keys_dev, int64_t n,

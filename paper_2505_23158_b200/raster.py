@@ -241,14 +241,59 @@ def tile_cover_counts(batch, camera) -> np.ndarray:
     return (x1 - x0 + 1) * (y1 - y0 + 1)
 
 
-def visibility_histogram(out, bin_edges) -> np.ndarray:
-    """Histogram of per-pixel visible counts (src/raster.py:464-479), a host
-    metric over the returned per_pixel_visible array."""
+def check_bin_edges(bin_edges) -> np.ndarray:
+    """visibility_histogram's edge validation with the reference's messages
+    (src/raster.py:471-475)."""
     edges = np.asarray(bin_edges, dtype=np.float64)
     if edges.ndim != 1 or edges.shape[0] < 2:
         raise ValueError("need at least two bin edges")
     if not np.all(np.diff(edges) > 0):
         raise ValueError(f"bin edges must be strictly increasing, got {edges}")
+    return edges
+
+
+def frame_report_device(visible, tile_count, maxw, n_inputs: int, bin_edges, device=None,
+                        ctx=None):
+    """Device report of one frame (K7, csrc/k_report.cu): the visibility
+    histogram of per_pixel_visible (src/raster.py:464-479), the per-tile
+    count sum and the number of inputs with a nonzero max weight (the
+    reference bench's mean_per_tile / visible_gaussians, src/cli.py:283-320).
+    Returns (hist int64 ndarray, tile_count_sum, visible_gaussians)."""
+    edges = check_bin_edges(bin_edges)
+    if edges.shape[0] > 257:
+        raise ValueError("at most 256 histogram bins")
+    ctx = ctx or context(device)
+    out = torch.zeros(edges.shape[0] + 1, dtype=torch.int64, device=ctx.device)
+    e = np.ascontiguousarray(edges)
+    vis = visible.contiguous()
+    tc = tile_count.contiguous()
+    fp64 = 1 if (maxw is not None and maxw.dtype == torch.float64) else 0
+    N.check(N.lib().lodge_frame_report(
+        ctx.bind(), ptr(vis), vis.numel(), e.ctypes.data_as(C.POINTER(C.c_double)), e.shape[0],
+        ptr(tc), tc.numel(), ptr(maxw), fp64, int(n_inputs) if maxw is not None else 0,
+        ptr(out)), "lodge_frame_report")
+    o = out.cpu().numpy()
+    n_bins = edges.shape[0] - 1
+    return o[:n_bins].copy(), int(o[n_bins]), int(o[n_bins + 1])
+
+
+def squared_error_device(a, b, device=None, ctx=None) -> float:
+    """Sum of squared differences of two fp32 device images (psnr_vs_full)."""
+    if a.dtype != torch.float32 or b.dtype != torch.float32 or a.numel() != b.numel():
+        raise ValueError("squared_error_device needs two fp32 images of one size")
+    ctx = ctx or context(device)
+    out = torch.zeros(1, dtype=torch.float64, device=ctx.device)
+    N.check(N.lib().lodge_sq_err(ctx.bind(), ptr(a.contiguous()), ptr(b.contiguous()),
+                                 a.numel(), ptr(out)), "lodge_sq_err")
+    return float(out.item())
+
+
+def visibility_histogram(out, bin_edges) -> np.ndarray:
+    """Histogram of per-pixel visible counts (src/raster.py:464-479) over a
+    host TileRenderOutput, as the reference computes it (the drop-in accepts
+    the reference's own output objects); device frames use
+    frame_report_device / Renderer.report, the same binning in one kernel."""
+    edges = check_bin_edges(bin_edges)
     vals = np.asarray(out.per_pixel_visible).reshape(-1)
     which = np.searchsorted(edges, vals, side="right") - 1
     np.clip(which, 0, edges.shape[0] - 2, out=which)

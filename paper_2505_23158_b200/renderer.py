@@ -23,6 +23,8 @@ from .device import (CAMERA_BYTES, Context, DeviceLevel, DevicePlan, camera_byte
 from .types import TILE_SIZE, RasterConfig
 
 STATS_BYTES = C.sizeof(N.FrameStats)
+# the reference CLI's default --histogram-bins (src/cli.py)
+DEFAULT_HISTOGRAM_EDGES = (0, 1, 2, 4, 8, 16, 32, 64, 128, 256)
 
 
 @dataclass
@@ -246,6 +248,32 @@ class Renderer:
         N.check(N.lib().lodge_to_srgb8(self._bind(slot), ptr(frame.image),
                                        frame.width * frame.height, ptr(out)), "lodge_to_srgb8")
         return out
+
+    def report(self, frame: Frame, stats=None, bin_edges=None, full_frame: Frame = None):
+        """The reference bench's per-frame report fields (src/cli.py:283-320),
+        computed on the device (csrc/k_report.cu): visibility_histogram,
+        mean_per_tile, visible_gaussians (nonzero max weights),
+        resident_gaussians (the chunk pair's union size: ChunkPlan.
+        resident_count, src/scene.py:266-272, is sum over levels of
+        |union1d(A_l, B_l)| = U), chunk_pair, and psnr_vs_full when the
+        full-mode frame of the same view is given."""
+        from .raster import frame_report_device, squared_error_device
+        torch.cuda.synchronize(self.device)  # the frame may come from any slot stream
+        st = stats if stats is not None else frame.read_stats()
+        edges = DEFAULT_HISTOGRAM_EDGES if bin_edges is None else bin_edges
+        hist, tsum, vis = frame_report_device(frame.visible, frame.tile_count, frame.maxw,
+                                              st.U, edges, ctx=self.ctx)
+        rep = {"mean_per_tile": tsum / frame.tile_count.numel(), "visible_gaussians": vis,
+               "resident_gaussians": int(st.U), "visibility_histogram": hist.tolist(),
+               "chunk_pair": ([int(st.f), None if st.o < 0 else int(st.o)]
+                              if st.f >= 0 else None)}
+        if full_frame is not None:
+            if frame.image is None or full_frame.image is None:
+                raise ValueError("psnr_vs_full needs both images")
+            sq = squared_error_device(frame.image, full_frame.image, ctx=self.ctx)
+            mse = sq / frame.image.numel()
+            rep["psnr_vs_full"] = float("inf") if mse == 0 else -10.0 * float(np.log10(mse))
+        return rep
 
     def fault_flags(self) -> int:
         """OR over every frame of every slot of the device bounds-check bits

@@ -38,6 +38,21 @@ def step_schedule(n_views: int, world: int, rank: int, n_steps: int,
     return [mine[s % len(mine)] for s in range(n_steps)]
 
 
+def spread_schedule(n_views: int, world: int, rank: int, n_steps: int, block: int = 16,
+                    offset: float = 0.5) -> List[List[int]]:
+    """Views per step for this rank, spread over the whole sweep: step s takes
+    this rank's block floor((s + offset) * n_mine / n_steps), so a short run
+    samples the path evenly instead of its first blocks.  Distinct blocks
+    whenever n_steps <= the rank's block count (cycling otherwise)."""
+    mine = block_cyclic(n_views, world, rank, block)
+    if not mine:
+        return [[] for _ in range(n_steps)]
+    if n_steps > len(mine):
+        return [mine[s % len(mine)] for s in range(n_steps)]
+    return [mine[min(len(mine) - 1, int((s + offset) * len(mine) / n_steps))]
+            for s in range(n_steps)]
+
+
 def max_over_ranks(value: float, device: Optional[torch.device] = None) -> float:
     """Max of a per-rank scalar (e.g. device-timed ms); identity without a group."""
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:

@@ -33,6 +33,21 @@ def test_block_cyclic_ragged_and_errors():
         shard.block_cyclic(10, 1, 0, 0)
 
 
+def test_spread_schedule_covers_the_sweep():
+    for world in (1, 2, 4, 8):
+        steps = 20
+        seen = []
+        for r in range(world):
+            sched = shard.spread_schedule(4096, world, r, steps, 16)
+            assert len(sched) == steps
+            firsts = [blk[0] for blk in sched]
+            assert firsts == sorted(firsts) and len(set(firsts)) == steps
+            seen.extend(v for blk in sched for v in blk)
+        assert len(seen) == len(set(seen)) == steps * 16 * world
+        # evenly spread: the sampled blocks reach both ends of the path
+        assert min(seen) < 4096 // steps and max(seen) > 4096 - 4096 // steps - 16 * world
+
+
 def test_step_schedule_cycles():
     s = shard.step_schedule(64, 4, 1, 5, 16)
     assert s[0] == list(range(16, 32)) and s[1] == s[0]
