@@ -37,7 +37,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = "frames/sec at 1080p (1/2/4/8 B200, views sharded) vs CPU ref; % of HBM roofline"
 UNIT = "frames/s"
-SWEEP_VIEWS = 4096
+SWEEP_VIEWS = 4096   # config 5: the sweep over config 3
+
+
+def sweep_views(cfg_name):
+    """Views of the timed path: the config-5 sweep (4096), or config 4's
+    1024-view Lissajous path through the room."""
+    return 1024 if cfg_name == "config4" else SWEEP_VIEWS
 BLOCK = 16
 
 
@@ -79,25 +85,28 @@ def workload_name(cfg_name):
     return {"config3": "config5 sweep over config3: 4096 views, 1920x1080, 20M Gaussians, "
                        "5 LODs, 64 chunks, SH3, chunk opacity blending",
             "config2": "config2 scene (1M Gaussians, 3 LODs, 16 chunks, SH3) swept at 1920x1080",
+            "config4": "config4 indoor room: 6M Gaussians, 4 LODs, 32 chunks on a 2-D Voronoi "
+                       "tiling, SH3, 1024-view Lissajous path at 1920x1080 with chunk opacity "
+                       "blending",
             "street1080": "46k-Gaussian street, 2 LODs, 4 chunks, SH1, 1920x1080"}[cfg_name]
 
 
-def schedules(rank, world, steps, warmup, block):
+def schedules(rank, world, steps, warmup, block, n_views=SWEEP_VIEWS):
     """Block-cyclic view assignment (paper_2505_23158_b200/shard.py): block b
     of `block` consecutive sweep views goes to rank b % world.  The timed
     steps take this rank's blocks spread evenly over the whole 4096-view
     sweep (step s -> block floor((s + 1/2) * n_mine / steps)); the warm-up
     steps take blocks in between."""
     from paper_2505_23158_b200.shard import spread_schedule
-    return (spread_schedule(SWEEP_VIEWS, world, rank, steps, block, 0.5),
-            spread_schedule(SWEEP_VIEWS, world, rank, warmup, block, 0.0))
+    return (spread_schedule(n_views, world, rank, steps, block, 0.5),
+            spread_schedule(n_views, world, rank, warmup, block, 0.0))
 
 
 def config_of(args, W=1920, H=1080):
     """The workload definition, identical in both arms (run statistics go
     under "run")."""
     return {"workload": workload_name(args.config), "mode": args.mode, "resolution": [W, H],
-            "sweep_views": SWEEP_VIEWS, "views_per_block": BLOCK,
+            "sweep_views": sweep_views(args.config), "views_per_block": BLOCK,
             "schedule": "block-cyclic over ranks, timed blocks spread over the sweep"}
 
 
@@ -305,8 +314,9 @@ def run_reference(args):
     # all host cores, whatever OMP_NUM_THREADS the launcher exported
     O.set_threads(os.cpu_count() or 1)
     cfg = scenes.build(args.config, threads=os.cpu_count() or 1)
-    sweep = cfg.sweep(SWEEP_VIEWS)
-    timed, warm = schedules(0, 1, args.steps, args.warmup, BLOCK)
+    nv = sweep_views(args.config)
+    sweep = cfg.sweep(nv)
+    timed, warm = schedules(0, 1, args.steps, args.warmup, BLOCK, nv)
     # one view per step: the first view of the block the GPU arm's rank 0
     # times at that step (the same spread over the sweep)
     for blk in warm:
@@ -404,8 +414,9 @@ def run_lodge(args):
     r = LG.Renderer(levels, plan, device=dev, storage="fp32", precision=args.precision,
                     n_streams=args.streams, phase_budget=args.phase_budget)
     B = args.views_per_step
-    timed, warm = schedules(rank, world, args.steps, args.warmup, B)
-    sweep = cfg.sweep(SWEEP_VIEWS)
+    nv = sweep_views(args.config)
+    timed, warm = schedules(rank, world, args.steps, args.warmup, B, nv)
+    sweep = cfg.sweep(nv)
     W, H = sweep[0].resolution
     flat = sorted({v for blk in timed + warm for v in blk})
     pos = {v: i for i, v in enumerate(flat)}

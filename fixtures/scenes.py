@@ -1,6 +1,7 @@
 """Bench/test fixture configs (SURVEY.md 8d recipes) built with fixtures/synth.c.
 
     cfg = build("config3")     # 20M Gaussians, 5 LODs, 64 chunks, SH3
+    cfg = build("config4")     # indoor room, 6M Gaussians, 4 LODs, 32 chunks (2-D Voronoi)
     cfg.levels  -> [(geom fp32 (n,12), sh fp32 (n,3,16), depth_threshold)]
     cfg.plan    -> centers (K,3), radii (K,), offsets (K*L+1), data uint32
     cfg.sweep(n)-> n trajectory cameras along the corridor (config 5)
@@ -36,7 +37,13 @@ CONFIGS = {
                     K=16, views=64),
     "config3": dict(n_fine=19_994_380, length=2000.0, degree=3, d=(10.0, 28.0, 47.0, 63.0),
                     keep=(0.31, 0.13, 0.076, 0.049), K=64, views=256),
+    # Zip-NeRF-style room (synth_room), d = 0.2 * (10, 28, 47),
+    # a 16 x 12 camera grid at height 1.6, k-means k = 32 over it, a
+    # 1024-view Lissajous path crossing the chunk junctions
+    "config4": dict(n_fine=5_986_062, length=0.0, degree=3, d=(2.0, 5.6, 9.4),
+                    keep=(0.31, 0.13, 0.076), K=32, views=(16, 12), scene="room"),
 }
+ROOM_X, ROOM_Z, ROOM_EYE = 20.0, 15.0, 1.6
 WIDTH, HEIGHT, FOCAL = 1920, 1080, 1560.0
 
 
@@ -49,6 +56,9 @@ def lib():
         P = C.c_void_p
         L.synth_count.argtypes = [C.c_int64]
         L.synth_count.restype = C.c_int64
+        L.synth_room_count.argtypes = [C.c_int64]
+        L.synth_room_count.restype = C.c_int64
+        L.synth_room.argtypes = [C.c_uint64, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]
         L.synth_street.argtypes = [C.c_uint64, C.c_int64, C.c_double, C.c_int32, P, P]
         L.synth_prune_key.argtypes = [P, C.c_int64, P]
         L.synth_gather_level.argtypes = [P, P, C.c_int32, P, C.c_int64, C.c_float, P, P]
@@ -63,17 +73,37 @@ def _p(a):
     return None if a is None else C.c_void_p(a.ctypes.data)
 
 
-def camera(z: float, width=WIDTH, height=HEIGHT, focal=FOCAL, x=0.0, y=0.5):
-    """Identity-orientation trajectory camera (pkg/scripts/make_deep_street.py:34-36)."""
-    return SimpleNamespace(position=np.array([x, y, z], np.float64),
-                           orientation=np.array([1.0, 0.0, 0.0, 0.0]),
-                           rotation_matrix=np.eye(3), focal=np.array([focal, focal]),
+def camera(z: float, width=WIDTH, height=HEIGHT, focal=FOCAL, x=0.0, y=0.5, yaw=0.0):
+    """Trajectory camera at (x, y, z) looking along (sin yaw, 0, cos yaw);
+    yaw 0 is the identity orientation of pkg/scripts/make_deep_street.py:34-36.
+    rotation_matrix maps world offsets to camera coordinates (src/scene.py:
+    116-117); orientation is its wxyz quaternion (a rotation about y by -yaw)."""
+    c, s = float(np.cos(yaw)), float(np.sin(yaw))
+    R = np.eye(3) if yaw == 0.0 else np.array([[c, 0.0, -s], [0.0, 1.0, 0.0], [s, 0.0, c]])
+    quat = np.array([np.cos(-yaw / 2), 0.0, np.sin(-yaw / 2), 0.0])
+    return SimpleNamespace(position=np.array([x, y, z], np.float64), orientation=quat,
+                           rotation_matrix=R, focal=np.array([focal, focal]),
                            principal_point=np.array([width / 2, height / 2]),
                            resolution=(width, height), near_plane=0.05)
 
 
+def lissajous(n: int):
+    """Config 4 path: n views on x = 0.85 X sin(3s + pi/2), z = 0.8 Z sin(2s),
+    s in [0, 2 pi), at eye height, each looking along the path tangent -- a
+    dense diagonal sweep through the room that crosses the chunk junctions."""
+    s = np.linspace(0.0, 2 * np.pi, n, endpoint=False)
+    x = 0.85 * ROOM_X * np.sin(3 * s + np.pi / 2)
+    z = 0.8 * ROOM_Z * np.sin(2 * s)
+    dx = 0.85 * ROOM_X * 3 * np.cos(3 * s + np.pi / 2)
+    dz = 0.8 * ROOM_Z * 2 * np.cos(2 * s)
+    yaw = np.arctan2(dx, dz)
+    return [camera(float(z[i]), x=float(x[i]), y=ROOM_EYE, yaw=float(yaw[i])) for i in range(n)]
+
+
 def kmeans_1d(positions: np.ndarray, k: int, iters: int = 50):
-    """Lloyd iterations from quantile seeds (deterministic)."""
+    """Lloyd iterations from quantile seeds (deterministic): seeds are the
+    positions at evenly spaced list indices (a path for the corridor, the
+    row-major grid for the room); any dimension."""
     pts = np.asarray(positions, np.float64)
     seeds = np.round(np.linspace(0, len(pts) - 1, k)).astype(np.int64)
     centers = pts[seeds].copy()
@@ -109,6 +139,7 @@ class Config:
     rig_z: np.ndarray
     length: float
     timings: dict = field(default_factory=dict)
+    rig: np.ndarray = None  # (V, 3) rig positions (config 4: the 2-D grid)
 
     @property
     def K(self):
@@ -122,10 +153,16 @@ class Config:
         return self.data[self.offsets[j * self.L + l]:self.offsets[j * self.L + l + 1]]
 
     def sweep(self, n: int):
-        """Config 5 path: z from 4 to 0.65*length, identity orientation."""
+        """Config 5 path: z from 4 to 0.65*length, identity orientation; the
+        room (config 4): the Lissajous path."""
+        if self.name == "config4":
+            return lissajous(n)
         return [camera(float(z)) for z in np.linspace(4.0, 0.65 * self.length, n)]
 
     def rig_camera(self, i: int):
+        if self.rig is not None:
+            p = self.rig[i]
+            return camera(float(p[2]), x=float(p[0]), y=float(p[1]))
         return camera(float(self.rig_z[i]))
 
     def n_gaussians(self):
@@ -144,10 +181,14 @@ def build(name: str, seed: int = 7, verbose: bool = False, threads: int = 0) -> 
     t0 = time.time()
     deg = spec["degree"]
     terms = (deg + 1) ** 2
-    n = int(L.synth_count(spec["n_fine"]))
+    room = spec.get("scene") == "room"
+    n = int((L.synth_room_count if room else L.synth_count)(spec["n_fine"]))
     geom = np.empty((n, 12), np.float32)
     sh = np.empty((n, 3, terms), np.float32)
-    L.synth_street(seed, spec["n_fine"], spec["length"], deg, _p(geom), _p(sh))
+    if room:
+        L.synth_room(seed, spec["n_fine"], deg, _p(geom), _p(sh))
+    else:
+        L.synth_street(seed, spec["n_fine"], spec["length"], deg, _p(geom), _p(sh))
     t1 = time.time()
     levels = [(geom, sh, 0.0)]
     if spec["d"]:
@@ -162,8 +203,15 @@ def build(name: str, seed: int = 7, verbose: bool = False, threads: int = 0) -> 
                                  _p(g), _p(s))
             levels.append((g, s, float(d)))
     t2 = time.time()
-    rig_z = np.linspace(2.0, 0.7 * spec["length"], spec["views"])
-    positions = np.stack([np.zeros_like(rig_z), np.full_like(rig_z, 0.5), rig_z], axis=1)
+    if room:  # a 2-D camera grid at eye height; k-means over it tiles the floor plan
+        nx, nz = spec["views"]
+        gx, gz = np.meshgrid(np.linspace(-0.9 * ROOM_X, 0.9 * ROOM_X, nx),
+                             np.linspace(-0.9 * ROOM_Z, 0.9 * ROOM_Z, nz), indexing="ij")
+        positions = np.stack([gx.reshape(-1), np.full(nx * nz, ROOM_EYE), gz.reshape(-1)], axis=1)
+        rig_z = positions[:, 2].copy()
+    else:
+        rig_z = np.linspace(2.0, 0.7 * spec["length"], spec["views"])
+        positions = np.stack([np.zeros_like(rig_z), np.full_like(rig_z, 0.5), rig_z], axis=1)
     centers, _ = kmeans_1d(positions, spec["K"])
     radii = chunk_radii(centers) if spec["K"] > 1 else np.array([1.0])
     K, nl = spec["K"], len(levels)
@@ -192,7 +240,7 @@ def build(name: str, seed: int = 7, verbose: bool = False, threads: int = 0) -> 
     t3 = time.time()
     cfg = Config(name, levels, deg, centers, radii, offsets, data, rig_z, spec["length"],
                  {"scene_s": t1 - t0, "levels_s": t2 - t1, "chunks_s": t3 - t2,
-                  "threads": int(L.synth_threads())})
+                  "threads": int(L.synth_threads())}, positions if room else None)
     if verbose:
         print(f"[fixtures] {name}: levels {cfg.n_gaussians()} sets {len(data)} "
               f"({cfg.timings})", flush=True)
@@ -223,7 +271,8 @@ def build_shared(name: str, local_rank: int, local_world: int, barrier, seed: in
     if local_world <= 1:
         return build(name, seed, threads=os.cpu_count() or 1)
     spec = CONFIGS[name]
-    n0 = int(lib().synth_count(spec["n_fine"]))
+    cnt = lib().synth_room_count if spec.get("scene") == "room" else lib().synth_count
+    n0 = int(cnt(spec["n_fine"]))
     est = n0 * (48 + 12 * (spec["degree"] + 1) ** 2) * 2
     d = _scratch_dir(est, f"lodge_fixture_{name}_{seed}_{key or os.getppid()}")
     if local_rank == 0:
@@ -236,6 +285,8 @@ def build_shared(name: str, local_rank: int, local_world: int, barrier, seed: in
             np.save(os.path.join(d, f"s{l}.npy"), s)
         for k in ("centers", "radii", "offsets", "data", "rig_z"):
             np.save(os.path.join(d, f"{k}.npy"), getattr(cfg, k))
+        if cfg.rig is not None:
+            np.save(os.path.join(d, "rig.npy"), cfg.rig)
         with open(os.path.join(d, "meta.json"), "w") as f:
             json.dump(meta, f)
     barrier()
@@ -246,7 +297,8 @@ def build_shared(name: str, local_rank: int, local_world: int, barrier, seed: in
         cfg = Config(meta["name"], levels, meta["degree"], np.array(ld("centers")),
                      np.array(ld("radii")), np.array(ld("offsets")), ld("data"),
                      np.array(ld("rig_z")), meta["length"],
-                     dict(meta["timings"], shared_from=d))
+                     dict(meta["timings"], shared_from=d),
+                     np.array(ld("rig")) if os.path.exists(os.path.join(d, "rig.npy")) else None)
     barrier()  # every rank has mapped the files: rank 0 may unlink them
     if local_rank == 0:
         shutil.rmtree(d, ignore_errors=True)

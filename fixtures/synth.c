@@ -173,6 +173,122 @@ void synth_street(uint64_t seed, int64_t n_fine, double length, int32_t degree, 
   }
 }
 
+/* ------------------------------------------------------------------------
+ * Config 4: a Zip-NeRF-style indoor room, 40 x 30 x 4 m
+ * (x in [-20, 20], z in [-15, 15], floor y = 0, ceiling y = 4), with
+ * deep_street's value laws (src/synthetic.py:81-171): a structure layer of
+ * oriented surface splats on jittered grids (floor, ceiling, four walls),
+ * three bands of multi-scale fine clutter (floor, along the walls, ceiling
+ * fixtures) whose colours track the local structure colour, and furniture
+ * blobs on the floor.  Not in the reference: a new seeded generator.
+ * ------------------------------------------------------------------------ */
+#define RX 20.0
+#define RZ 15.0
+#define RH 4.0
+#define R_FLOOR_NX 81
+#define R_FLOOR_NZ 61
+#define R_WALL_NH 9
+#define R_N_FLOOR (R_FLOOR_NX * R_FLOOR_NZ)
+#define R_N_WALLX (R_FLOOR_NX * R_WALL_NH) /* walls z = -+RZ, along x */
+#define R_N_WALLZ (R_FLOOR_NZ * R_WALL_NH) /* walls x = -+RX, along z */
+#define R_N_STRUCT (2 * R_N_FLOOR + 2 * R_N_WALLX + 2 * R_N_WALLZ)
+#define R_N_BLOBS 60
+
+int64_t synth_room_count(int64_t n_fine) {
+  return R_N_STRUCT + 3 * (n_fine / 3) + R_N_BLOBS * BLOB_M;
+}
+
+static void room_color(double x, double z, double c[3]) {
+  const double u = (x + RX) / (2 * RX), v = (z + RZ) / (2 * RZ);
+  c[0] = clampd(0.45 + 0.25 * sin(5.0 * u + 0.3), 0.05, 0.95);
+  c[1] = clampd(0.40 + 0.20 * cos(7.0 * v), 0.05, 0.95);
+  c[2] = clampd(0.38 + 0.22 * sin(3.0 * (u + v) + 1.0), 0.05, 0.95);
+}
+
+void synth_room(uint64_t seed, int64_t n_fine, int32_t degree, float *geom, float *sh) {
+  const int terms = (degree + 1) * (degree + 1);
+  const int64_t n_each = n_fine / 3;
+  const int64_t o_fine = R_N_STRUCT, o_blob = o_fine + 3 * n_each;
+  const double s2 = 0.7071067811865476;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < R_N_STRUCT; ++i) {
+    rng_t r = rng_at(seed, 11, (uint64_t)i);
+    double p[3], s[3], q[4], col[3];
+    int64_t k = i;
+    int part;  /* 0 floor, 1 ceiling, 2/3 walls z = -+RZ, 4/5 walls x = -+RX */
+    if (k < R_N_FLOOR) part = 0;
+    else if ((k -= R_N_FLOOR) < R_N_FLOOR) part = 1;
+    else if ((k -= R_N_FLOOR) < 2 * R_N_WALLX) { part = 2 + (int)(k / R_N_WALLX); k %= R_N_WALLX; }
+    else { k -= 2 * R_N_WALLX; part = 4 + (int)(k / R_N_WALLZ); k %= R_N_WALLZ; }
+    if (part <= 1) {
+      const double x = -RX + 2 * RX * (double)(k / R_FLOOR_NZ) / (R_FLOOR_NX - 1);
+      const double z = -RZ + 2 * RZ * (double)(k % R_FLOOR_NZ) / (R_FLOOR_NZ - 1);
+      p[0] = x; p[1] = part == 0 ? 0.0 : RH; p[2] = z;
+      q[0] = s2; q[1] = part == 0 ? -s2 : s2; q[2] = 0; q[3] = 0;  /* normal -+y */
+    } else if (part <= 3) {
+      const double x = -RX + 2 * RX * (double)(k / R_WALL_NH) / (R_FLOOR_NX - 1);
+      const double y = RH * (double)(k % R_WALL_NH) / (R_WALL_NH - 1);
+      p[0] = x; p[1] = y; p[2] = part == 2 ? -RZ : RZ;
+      q[0] = 1; q[1] = 0; q[2] = 0; q[3] = 0;  /* thin along z: normal -+z */
+    } else {
+      const double z = -RZ + 2 * RZ * (double)(k / R_WALL_NH) / (R_FLOOR_NZ - 1);
+      const double y = RH * (double)(k % R_WALL_NH) / (R_WALL_NH - 1);
+      p[0] = part == 4 ? -RX : RX; p[1] = y; p[2] = z;
+      q[0] = s2; q[1] = 0; q[2] = s2; q[3] = 0;  /* thin along x */
+    }
+    for (int d = 0; d < 3; ++d) p[d] += normal(&r, 0.0, 0.18);
+    const double t = exp(unif_ab(&r, log(0.35), log(0.55)));
+    s[0] = t * unif_ab(&r, 0.7, 1.3); s[1] = t * unif_ab(&r, 0.7, 1.3); s[2] = t * 0.25;
+    const double op = unif_ab(&r, 0.85, 0.98);
+    room_color(p[0], p[2], col);
+    for (int c = 0; c < 3; ++c) col[c] = clampd(col[c] + normal(&r, 0.0, 0.06), 0.02, 1.5);
+    put(geom, sh, terms, i, p, s, q, op, col, &r);
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < 3 * n_each; ++i) {
+    const int band = (int)(i / n_each);
+    rng_t r = rng_at(seed, 12, (uint64_t)i);
+    double p[3], s[3], q[4], col[3];
+    if (band == 0) {  /* floor clutter */
+      p[0] = unif_ab(&r, -RX + 0.3, RX - 0.3); p[1] = unif_ab(&r, 0.05, 0.9);
+      p[2] = unif_ab(&r, -RZ + 0.3, RZ - 0.3);
+    } else if (band == 1) {  /* along the walls, 0.2 .. 2.8 m in */
+      const double u = unif(&r) * 2.0 * (2 * RX + 2 * RZ), in = unif_ab(&r, 0.2, 2.8);
+      if (u < 2 * RX) { p[0] = -RX + u; p[2] = -RZ + in; }
+      else if (u < 4 * RX) { p[0] = -RX + (u - 2 * RX); p[2] = RZ - in; }
+      else if (u < 4 * RX + 2 * RZ) { p[0] = -RX + in; p[2] = -RZ + (u - 4 * RX); }
+      else { p[0] = RX - in; p[2] = -RZ + (u - 4 * RX - 2 * RZ); }
+      p[1] = unif_ab(&r, 0.1, RH - 0.3);
+    } else {  /* ceiling fixtures */
+      p[0] = unif_ab(&r, -RX + 0.3, RX - 0.3); p[1] = unif_ab(&r, RH - 0.8, RH - 0.05);
+      p[2] = unif_ab(&r, -RZ + 0.3, RZ - 0.3);
+    }
+    const double size = exp(unif_ab(&r, log(0.02), log(0.4)));
+    for (int d = 0; d < 3; ++d) s[d] = size * unif_ab(&r, 0.6, 1.4);
+    random_quat(&r, q);
+    const double op = unif_ab(&r, 0.5, 0.95);
+    room_color(p[0], p[2], col);
+    for (int c = 0; c < 3; ++c) col[c] = clampd(col[c] + normal(&r, 0.0, 0.07), 0.02, 1.2);
+    put(geom, sh, terms, o_fine + i, p, s, q, op, col, &r);
+  }
+  for (int b = 0; b < R_N_BLOBS; ++b) {
+    rng_t rb = rng_at(seed, 13, (uint64_t)b);
+    const double c[3] = {unif_ab(&rb, -RX + 2, RX - 2), unif_ab(&rb, 0.3, 1.1),
+                         unif_ab(&rb, -RZ + 2, RZ - 2)};
+    const double bc[3] = {unif_ab(&rb, 0.1, 0.9), unif_ab(&rb, 0.1, 0.9), unif_ab(&rb, 0.1, 0.9)};
+    for (int m = 0; m < BLOB_M; ++m) {
+      rng_t r = rng_at(seed, 14, (uint64_t)(b * BLOB_M + m));
+      double p[3], s[3], q[4], col[3];
+      for (int d = 0; d < 3; ++d) p[d] = c[d] + normal(&r, 0.0, 0.35);
+      for (int d = 0; d < 3; ++d) s[d] = exp(unif_ab(&r, log(0.05), log(0.2)));
+      random_quat(&r, q);
+      const double op = unif_ab(&r, 0.5, 0.95);
+      for (int d = 0; d < 3; ++d) col[d] = clampd(bc[d] + normal(&r, 0.0, 0.08), 0.02, 1.2);
+      put(geom, sh, terms, o_blob + b * BLOB_M + m, p, s, q, op, col, &r);
+    }
+  }
+}
+
 /* LOD pruning proxy key: opacity * max(scale)^2. */
 void synth_prune_key(const float *geom, int64_t n, float *key) {
 #pragma omp parallel for schedule(static)

@@ -498,9 +498,43 @@ def make_street():
     return d
 
 
+REPORT_EDGES = {"default": [0, 1, 2, 4, 8, 16, 32, 64, 128, 256], "coarse": [1, 3, 5],
+                "fractional": [2.5, 7.5, 100.0], "wide": [-5.0, 0.0, 1e6],
+                "fine": list(range(0, 64, 3))}
+
+
+def make_report():
+    """The reference bench's per-frame report fields (src/cli.py:283-320) on
+    the config-1 frames the reference rendered (config1.npz o_* outputs):
+    visibility_histogram for several edge sets (src/raster.py:464-479),
+    mean_per_tile and visible_gaussians, plus the edge-validation messages."""
+    from types import SimpleNamespace
+    c1 = np.load(os.path.join(OUT, "config1.npz"))
+    d = {}
+    for v in range(8):
+        p = f"v{v}/"
+        out = SimpleNamespace(per_pixel_visible=c1[p + "o_visible"])
+        for name, edges in REPORT_EDGES.items():
+            d[p + "hist/" + name] = R.visibility_histogram(out, np.asarray(edges))
+        d[p + "mean_per_tile"] = np.float64(c1[p + "o_tile_count"].mean())
+        d[p + "visible_gaussians"] = np.int64(np.count_nonzero(c1[p + "o_maxw"]))
+    for name, edges in REPORT_EDGES.items():
+        d["edges/" + name] = np.asarray(edges, np.float64)
+    msgs = []
+    for bad in ([1.0], [3.0, 2.0], [0.0, 1.0, 1.0]):
+        try:
+            R.visibility_histogram(SimpleNamespace(per_pixel_visible=np.zeros(4, np.int64)),
+                                   np.asarray(bad))
+            msgs.append("")
+        except ValueError as e:
+            msgs.append(str(e))
+    d["bad_edges_messages"] = np.asarray(msgs)
+    return d
+
+
 GENERATORS = {"cases": make_cases, "config1": make_config1, "importance": make_importance,
               "asset": make_asset, "thresholds": make_thresholds, "modes": make_modes,
-              "street": make_street}
+              "street": make_street, "report": make_report}
 
 
 def main(names=None):

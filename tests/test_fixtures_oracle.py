@@ -37,3 +37,28 @@ def test_project_f32_equals_fp64_restatement():
         b = O.project_f32(g, s, c.degree, idx, oc, rc, mod)
         for k in ("src", "mean2d", "conic", "depth", "opacity", "color", "rect"):
             assert np.array_equal(a[k], b[k]), k
+
+
+def test_config4_room_fixture():
+    """Config 4: 6M Gaussians, 4 LODs at d = 0.2 (10, 28, 47),
+    32 chunks from k-means over a 2-D camera grid at eye height (a Voronoi
+    tiling of the floor plan), and a 1024-view Lissajous path that changes
+    chunk pair often and passes near junctions of three or more chunks."""
+    c = scenes.build("config4")
+    assert c.n_gaussians() == [6_000_000, 1_860_000, 780_000, 456_000]
+    assert c.K == 32 and c.L == 4 and c.degree == 3
+    assert [lv[2] for lv in c.levels[1:]] == [2.0, 5.6, 9.4]
+    assert np.allclose(c.centers[:, 1], scenes.ROOM_EYE)  # 2-D tiling at eye height
+    path = c.sweep(1024)
+    assert len(path) == 1024
+    pairs = [O.select(c.centers, cam.position)[:2] for cam in path]
+    changes = sum(1 for i in range(1, len(pairs)) if pairs[i] != pairs[i - 1])
+    assert changes >= 50 and len(set(pairs)) >= 40
+    near3 = 0
+    for cam in path:
+        d = np.sort(np.linalg.norm(c.centers - cam.position, axis=1))
+        near3 += int(d[2] < 1.3 * d[0])
+    assert near3 >= 20
+    for cam in path[:8]:  # the camera looks along the path tangent: R is a rotation
+        R = cam.rotation_matrix
+        assert np.allclose(R @ R.T, np.eye(3)) and np.isclose(np.linalg.det(R), 1.0)

@@ -1,4 +1,4 @@
-"""GPU parity at the sizes the bench runs (BASELINE configs 2 and 3, 1080p),
+"""GPU parity at the sizes the bench runs (BASELINE configs 2, 3 and 4, 1080p),
 through the fused device path (lodge_render_frame), against the pinned CPU
 oracle (oracle/, fp64 restatement of the reference; the checker only).
 
@@ -11,7 +11,8 @@ The default two-phase frame equals the one-pass frame bitwise (image,
 per_pixel_visible, per_tile_count, max weights, U, M, P).
 
 Config 2 is the survey's named view (cams[12] of the 64-view
-rig, z = 28.3); config 3 views are taken along the config-5 sweep.  Slow:
+rig, z = 28.3); config 3 views are taken along the config-5 sweep, config 4
+views along the room's Lissajous path.  Slow:
 the config-3 store is 7.5 GB and the oracle renders a 1080p config-3 view
 in a few seconds on the box's host cores.
 """
@@ -138,6 +139,15 @@ def test_config2_view12_vs_oracle():
     cfg, _, _ = setup("config2")
     st = check_view("config2", cfg.rig_camera(12))
     assert st.P > 20_000_000  # the survey's measured scale (P = 34.0M with SH1 colours)
+
+
+@pytest.mark.parametrize("view", [300, 700])
+def test_config4_path_view_vs_oracle(view):
+    """Config 4 (indoor room: 6M Gaussians, 4 LODs, 32 chunks on a 2-D
+    Voronoi tiling, SH3) on its Lissajous path (fixtures/scenes.py)."""
+    cfg, _, _ = setup("config4")
+    st = check_view("config4", cfg.sweep(1024)[view])
+    assert st.P > 10_000_000 and st.o >= 0
 
 
 @pytest.mark.parametrize("view", [300, 2048, 3900])
