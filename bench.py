@@ -65,6 +65,10 @@ def parse():
                     help="full: the whole store resident; stream: chunk slabs loaded "
                          "asynchronously into --slots device slots (SURVEY.md 8f rank 4)")
     ap.add_argument("--slots", type=int, default=3)
+    ap.add_argument("--store", default="flat", choices=["flat", "slab"],
+                    help="full residency layout: flat level arrays, or chunk slabs (every "
+                         "chunk's records contiguous in set order; paper_2505_23158_b200."
+                         "device.SlabStore)")
     ap.add_argument("--phase-budget", type=int, default=1280,
                     help="FAST frames: first-phase pairs per tile of the two depth phases "
                          "(lodge_set_phase_budget); 0 = one pass over the full lists")
@@ -411,6 +415,11 @@ def run_lodge(args):
         plan = DevicePlan.from_arrays(cfg.centers, cfg.offsets, np.asarray(cfg.data), cfg.L,
                                       dev)
         store_gb = sum(l.nbytes() for l in levels) / 1e9
+        if args.store == "slab":
+            from paper_2505_23158_b200.device import SlabStore
+            slabs = SlabStore(levels, plan)
+            plan = slabs.attach(plan)
+            store_gb += slabs.nbytes() / 1e9
     r = LG.Renderer(levels, plan, device=dev, storage="fp32", precision=args.precision,
                     n_streams=args.streams, phase_budget=args.phase_budget)
     B = args.views_per_step
@@ -734,13 +743,13 @@ def run_lodge(args):
                     "phase_budget": args.phase_budget if args.precision == "fast" else 0,
                     "frames_in_flight_per_gpu": S, "views_per_step_per_gpu": B,
                     "frames_timed": total_frames,
-                    "store": ("fp32 records, replicated" if store is None else
+                    "store": (f"fp32 records, replicated ({args.store} layout)" if store is None else
                               f"fp32 chunk slabs, {args.slots} resident slots, "
                               f"{store.loads} loads ({store.bytes_loaded / 1e9:.1f} GB)"),
                     "store_gb": round(store_gb, 2),
                     "l2": "inputs larger than L2: per-frame working set "
                           f"~{(sb['project'] + sb['tile_sort'] + sb['composite']) / 1e9:.2f} GB"
-                          " and a 7.5 GB store >> 126 MB L2; no explicit flush",
+                          f" and a {store_gb:.1f} GB store >> 126 MB L2; no explicit flush",
                     "mean_U": round(U), "mean_M": round(M), "mean_P": round(P),
                     "mean_P_sorted": [round(P1), round(P2)],
                     "mean_M_composited": [round(M1), round(M2)],

@@ -232,6 +232,25 @@ __device__ __forceinline__ void warp_add(int32_t *base, int32_t idx, int32_t v) 
     atomicAdd(base + idx, v * __popc(peers));
 }
 
+// Warp-aggregated add into a shared-memory counter array (the CTA-private
+// difference array of the projection).
+__device__ __forceinline__ void warp_add_shared(int32_t *base, int32_t idx, int32_t v) {
+  const uint32_t peers = __match_any_sync(FULL_MASK, idx);
+  if (idx >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(base + idx, v * __popc(peers));
+}
+
+// The same update into a CTA-private difference array in shared memory.
+__device__ __forceinline__ void add_tile_diff_shared(int32_t *diff, uint64_t rc, int32_t tiles_x,
+                                                     bool valid) {
+  const int32_t x0 = (int32_t)(rc & 0xffff), x1 = (int32_t)((rc >> 16) & 0xffff);
+  const int32_t y0 = (int32_t)((rc >> 32) & 0xffff), y1 = (int32_t)(rc >> 48);
+  const int32_t stride = tiles_x + 1;
+  warp_add_shared(diff, valid ? y0 * stride + x0 : -1, 1);
+  warp_add_shared(diff, valid ? y0 * stride + x1 + 1 : -1, -1);
+  warp_add_shared(diff, valid ? (y1 + 1) * stride + x0 : -1, -1);
+  warp_add_shared(diff, valid ? (y1 + 1) * stride + x1 + 1 : -1, 1);
+}
+
 // 2-D difference-array update for a tile rectangle (whole warp; valid flag).
 __device__ __forceinline__ void add_tile_diff(int32_t *diff, uint64_t rc, int32_t tiles_x,
                                               bool valid) {

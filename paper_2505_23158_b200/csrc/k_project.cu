@@ -397,6 +397,7 @@ struct ProjLevels {
   const void *const *slab_geom;
   const void *const *slab_sh;
   uint32_t n[LODGE_MAX_LEVELS];  // records per level (bounds checks)
+  int32_t diff_in_smem;          // k_project_frame: CTA-private difference array
 };
 
 // Shared per-CTA frame context of the frame kernels (camera, blend factor,
@@ -469,6 +470,16 @@ __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLeve
   // persistent CTAs (grid-stride over the slots): the camera and the level
   // table are staged once per CTA
   __shared__ FrameCtx F;
+  // per_tile_count's 2-D difference array, CTA-private in shared memory when
+  // it fits (the host passes its size as the dynamic shared memory), flushed
+  // once at the end: the corners of border-clipped splats are shared by most
+  // of a frame's splats, and global atomics on them serialised the kernel
+  // (0.15 of its 0.27 ms at config 3, profiles/r02_stress.md)
+  extern __shared__ int32_t s_diff[];
+  const int32_t n_diff = (tiles_x + 1) * (tiles_y + 1);
+  const bool priv = lv.diff_in_smem != 0;
+  if (priv)
+    for (int32_t i = threadIdx.x; i < n_diff; i += blockDim.x) s_diff[i] = 0;
   stage_frame_ctx(F, lv, fs, cam_p);
   // the tile grid is the frame's (host W, H), so the difference-array
   // indices stay in range whatever the device camera holds
@@ -493,13 +504,21 @@ __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLeve
     const bool keep = valid && p.ok;
     nkeep_cta += __popc(__ballot_sync(FULL_MASK, keep));
     const uint64_t rc = keep ? tile_rect(p.mx, p.my, p.ex, p.ey, tiles_x, tiles_y) : 0ull;
-    add_tile_diff(w.tile_diff, rc, tiles_x, keep);
+    if (priv) add_tile_diff_shared(s_diff, rc, tiles_x, keep);
+    else add_tile_diff(w.tile_diff, rc, tiles_x, keep);
     if (!valid) continue;
     w.val_depth[0][g] = g;
     w.key_depth[0][g] = keep ? (uint64_t)__double_as_longlong(p.z) : ~0ull;
     if (keep) w.rect[g] = rc;
   }
   if ((threadIdx.x & 31) == 0 && nkeep_cta) atomicAdd(&fs->stats.M, nkeep_cta);
+  if (priv) {
+    __syncthreads();
+    for (int32_t i = threadIdx.x; i < n_diff; i += blockDim.x) {
+      const int32_t v = s_diff[i];
+      if (v) atomicAdd(w.tile_diff + i, v);
+    }
+  }
 }
 
 // Compositing records (payload + fp64 record, colour from the SH) of the
@@ -709,13 +728,26 @@ static int sm_count() {
   return (int)sms();
 }
 
+// Largest CTA-private difference array of the projection (int32 entries):
+// 96 KB, two CTAs per SM -- up to ~2560 x 1440 (4K frames use global atomics).
+constexpr int32_t PROJ_DIFF_SMEM_MAX = 96 * 1024;
+
 template <typename GT, typename ST>
-static void launch_pf(const ProjLevels &lv, const Work &w, FrameState *fs,
+static void launch_pf(ProjLevels lv, const Work &w, FrameState *fs,
                       const lodge_camera *cam, const lodge_raster_params &rp, uint32_t nslots,
                       int32_t tiles_x, int32_t tiles_y, cudaStream_t s) {
   const uint32_t want = (nslots + 255) / 256, cap = LODGE_PROJ_MINB * (uint32_t)sm_count();
-  k_project_frame<GT, ST><<<want < cap ? want : cap, 256, 0, s>>>(lv, w, fs, cam, rp, tiles_x,
-                                                                   tiles_y);
+  const int64_t bytes = 4ll * (tiles_x + 1) * (tiles_y + 1);
+  lv.diff_in_smem = bytes <= PROJ_DIFF_SMEM_MAX ? 1 : 0;
+  const size_t sm = lv.diff_in_smem ? (size_t)bytes : 0;
+  static PerDevice attr;
+  if (sm > 48 * 1024 && !attr()) {
+    cudaFuncSetAttribute(k_project_frame<GT, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         PROJ_DIFF_SMEM_MAX);
+    attr() = 1;
+  }
+  k_project_frame<GT, ST><<<want < cap ? want : cap, 256, sm, s>>>(lv, w, fs, cam, rp, tiles_x,
+                                                                    tiles_y);
 }
 
 template <typename GT, typename ST>
@@ -731,6 +763,7 @@ static int proj_levels(const lodge_level *levels, const LevelSlots &ls,
                        const void *const *slab_geom, const void *const *slab_sh, ProjLevels &lv,
                        bool &g32, bool &s32) {
   lv.L = ls.n_levels;
+  lv.diff_in_smem = 0;
   lv.slab_geom = slab_geom;
   lv.slab_sh = slab_sh;
   const int32_t prec_bits = LODGE_GEOM_FP32 | LODGE_SH_FP32;

@@ -282,3 +282,53 @@ def level_for(scene, device=None, storage="fp64") -> DeviceLevel:
 def plan_for(plan, device=None) -> DevicePlan:
     d = _device(device)
     return _plans.get(plan, d.index, lambda: DevicePlan(plan, d))
+
+
+class SlabStore:
+    """Chunk-slab layout of a resident store (B200 capacity for bandwidth):
+    for every chunk j and level l, the records of the set (j, l) copied
+    contiguously in set order, so a frame's gather (the union of two sets,
+    in index order) reads two streams instead of isolated 48-B records
+    scattered over the level -- each Gaussian is stored once per chunk whose
+    set holds it (config 3: 3.3x the level store, 25 GB of 180 GB).
+
+    The plan's slab tables (lodge_chunks.slab_geom_dev / slab_sh_dev) point
+    lodge_render_frame at the slabs: the union then emits each element's
+    position in its owning chunk's set (tags 3/1 primary, 2 other) and the
+    projection and payload kernels read that slab -- the values are the
+    level store's, so frames are bit-identical to the flat store
+    (tests/test_gpu_streaming.py).  Built on the device by an index gather
+    from the resident levels (a one-time layout transform at load)."""
+
+    def __init__(self, levels, plan: "DevicePlan"):
+        dev = plan.centers.device
+        K, L = plan.K, plan.L
+        offs = plan.offsets.cpu().numpy()
+        data = plan.data.view(torch.int32)
+        self.geom, self.sh = [], []
+        geom_rows, sh_rows = np.zeros(K * L, np.int64), np.zeros(K * L, np.int64)
+        for l, lv in enumerate(levels):
+            # positions of level l's sets inside the plan's data, chunk-major
+            spans = [(int(offs[j * L + l]), int(offs[j * L + l + 1])) for j in range(K)]
+            idx = torch.cat([data[a:b] for a, b in spans]).to(torch.int64) & 0xffffffff
+            g = lv.geom.index_select(0, idx).contiguous()
+            s = lv.sh.index_select(0, idx).contiguous()
+            self.geom.append(g)
+            self.sh.append(s)
+            start = 0
+            for j, (a, b) in enumerate(spans):
+                geom_rows[j * L + l] = g.data_ptr() + start * g.shape[1] * g.element_size()
+                sh_rows[j * L + l] = s.data_ptr() + start * s[0].numel() * s.element_size()
+                start += b - a
+        self.geom_tab = torch.from_numpy(geom_rows).to(dev)
+        self.sh_tab = torch.from_numpy(sh_rows).to(dev)
+        self.levels = levels
+
+    def attach(self, plan: "DevicePlan") -> "DevicePlan":
+        plan.struct.slab_geom_dev = self.geom_tab.data_ptr()
+        plan.struct.slab_sh_dev = self.sh_tab.data_ptr()
+        plan._slabs = self  # keep the slabs alive with the plan
+        return plan
+
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in self.geom + self.sh)
