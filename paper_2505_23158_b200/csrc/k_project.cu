@@ -74,7 +74,33 @@ __device__ __forceinline__ void normalize_rot(double v[12]) {
   v[9] = v[9] / nn;
 }
 
+// Camera rotation patterns (bit 3i+j set: W_ij may be nonzero).  A term
+// (W_ij * cw_jk) * W_lk of cov_cam = W cov_world W^T with W_ij = 0 or W_lk = 0
+// is an exact zero for finite cov_world, and adding it to the running sum
+// leaves the sum unchanged (up to the sign of an all-zero total, which
+// compares equal), so the kernels drop those terms at compile time for
+// cameras whose rotation has that zero pattern: the identity-orientation
+// sweep (config 5) keeps 9 of the 81 terms, yaw-only cameras (config 4) 25.
+enum : int { W_FULL = 0x1FF, W_IDENT = 0x111, W_YAW = 0x155 };
+
+__device__ __forceinline__ int camera_wpattern(const lodge_camera &cam) {
+  int m = 0;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) m |= (cam.R[i] != 0.0) ? (1 << i) : 0;
+  if ((m & ~W_IDENT) == 0) return W_IDENT;
+  if ((m & ~W_YAW) == 0) return W_YAW;
+  return W_FULL;
+}
+
+__device__ __forceinline__ bool all_finite9(const double c[9]) {
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) ok = ok && isfinite(c[i]);
+  return ok;
+}
+
 // v: [mean3, scale3, rot4 wxyz, opacity, fv]
+template <int WM = W_FULL>
 __device__ __forceinline__ Proj project_core(const double v[12], const lodge_camera &cam,
                                              const lodge_raster_params &rp, double mod,
                                              bool has_mod) {
@@ -117,17 +143,36 @@ __device__ __forceinline__ Proj project_core(const double v[12], const lodge_cam
   cw[4] = cw[4] + fv;
   cw[8] = cw[8] + fv;
   double cc[9];
+  if (WM == W_FULL || !all_finite9(cw)) {  // 0 * inf would be a NaN term: keep them all
 #pragma unroll
-  for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < 3; ++i)
 #pragma unroll
-    for (int l = 0; l < 3; ++l) {
-      double acc = 0.0;
+      for (int l = 0; l < 3; ++l) {
+        double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j < 3; ++j)
+        for (int j = 0; j < 3; ++j)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) acc = acc + (W[3 * i + j] * cw[3 * j + k]) * W[3 * l + k];
-      cc[3 * i + l] = acc;
-    }
+          for (int k = 0; k < 3; ++k) acc = acc + (W[3 * i + j] * cw[3 * j + k]) * W[3 * l + k];
+        cc[3 * i + l] = acc;
+      }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          if (!((WM >> (3 * i + j)) & 1)) continue;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            if (!((WM >> (3 * l + k)) & 1)) continue;
+            acc = acc + (W[3 * i + j] * cw[3 * j + k]) * W[3 * l + k];
+          }
+        }
+        cc[3 * i + l] = acc;
+      }
+  }
   const double lim_x = 1.3 * 0.5 * (double)cam.w / fx;
   const double lim_y = 1.3 * 0.5 * (double)cam.h / fy;
   double tx = x / z, ty = y / z;
@@ -181,6 +226,15 @@ __device__ __forceinline__ Proj project_core(const double v[12], const lodge_cam
   p.det = det;
   p.ok = ok;
   return p;
+}
+
+// project_core for the camera's rotation zero pattern (uniform per camera).
+__device__ __forceinline__ Proj project_any(const double v[12], const lodge_camera &cam,
+                                            const lodge_raster_params &rp, double mod,
+                                            bool has_mod, int wpat) {
+  if (wpat == W_IDENT) return project_core<W_IDENT>(v, cam, rp, mod, has_mod);
+  if (wpat == W_YAW) return project_core<W_YAW>(v, cam, rp, mod, has_mod);
+  return project_core<W_FULL>(v, cam, rp, mod, has_mod);
 }
 
 // Coefficients of one record, (3, (DEG+1)^2), loaded with 16-byte vector
@@ -406,6 +460,7 @@ struct FrameCtx {
   lodge_camera cam;
   double t;
   int32_t f, o;
+  int32_t wpat;  // camera rotation zero pattern (project_any)
   uint32_t used[LODGE_MAX_LEVELS], cat[LODGE_MAX_LEVELS];
 };
 
@@ -414,6 +469,7 @@ __device__ __forceinline__ void stage_frame_ctx(FrameCtx &F, const ProjLevels &l
                                                 const lodge_camera *__restrict__ cam_p) {
   if (threadIdx.x == 0) {
     F.cam = *cam_p;
+    F.wpat = camera_wpattern(F.cam);
     F.t = fs->stats.t;
     F.f = fs->stats.f;
     F.o = fs->stats.o < 0 ? fs->stats.f : fs->stats.o;
@@ -430,8 +486,9 @@ __device__ __forceinline__ void stage_frame_ctx(FrameCtx &F, const ProjLevels &l
 // The record of union slot `slot` of level l: geometry loaded (rotation
 // normalised if the level asks), modulation from the blend tag, SH pointer
 // and record index for the colour.  Shared by the projection and the
-// payload kernel, so both evaluate the identical fp64 projection.
-template <typename GT, typename ST>
+// payload kernel, so both evaluate the identical fp64 projection (DISPATCH:
+// drop the exact-zero camera terms, project_any; the fields are the same).
+template <typename GT, typename ST, bool DISPATCH = true>
 __device__ __forceinline__ Proj slot_project(const ProjLevels &lv, const Work &w,
                                              const FrameCtx &F, const lodge_raster_params &rp,
                                              int l, uint32_t slot, double v[12],
@@ -448,7 +505,8 @@ __device__ __forceinline__ Proj slot_project(const ProjLevels &lv, const Work &w
   }
   load_geom<GT>(gp + (size_t)gidx * 12, v);
   if (lv.qnorm[l]) normalize_rot(v);
-  return project_core(v, F.cam, rp, mod, true);
+  return DISPATCH ? project_any(v, F.cam, rp, mod, true, F.wpat)
+                  : project_core<W_FULL>(v, F.cam, rp, mod, true);
 }
 
 // K2, geometry only.  Outputs are written at the dense concatenated input
@@ -553,7 +611,7 @@ __global__ void __launch_bounds__(256, LODGE_PAYLOAD_MINB) k_payload(ProjLevels 
     double v[12];
     const ST *sp;
     uint32_t gidx;
-    const Proj p = slot_project<GT, ST>(lv, w, F, rp, l, slot, v, sp, gidx);
+    const Proj p = slot_project<GT, ST, false>(lv, w, F, rp, l, slot, v, sp, gidx);
     double rgb[3] = {0.0, 0.0, 0.0};
     if (shade) {
       const int deg = lv.degree[l];
@@ -594,7 +652,7 @@ __global__ void __launch_bounds__(256) k_project_compat(const GT *geom, const ST
     g = idx ? idx[e] : e;
     load_geom<GT>(geom + (size_t)g * 12, v);
     if (qnorm) normalize_rot(v);
-    p = project_core(v, cam, rp, mod ? mod[e] : 1.0, mod != nullptr);
+    p = project_any(v, cam, rp, mod ? mod[e] : 1.0, mod != nullptr, camera_wpattern(cam));
   }
   const int64_t m = compact_slot(e < n && p.ok, w.status, fs->epoch + TK_COMPACT, part, s_warp,
                                  &s_base);
@@ -650,7 +708,7 @@ __global__ void __launch_bounds__(256) k_cover_keys(const GT *geom, const int64_
     const int64_t g = idx ? idx[e] : e;
     load_geom<GT>(geom + (size_t)g * 12, v);
     if (qnorm) normalize_rot(v);
-    p = project_core(v, cam, rp, 1.0, false);
+    p = project_any(v, cam, rp, 1.0, false, camera_wpattern(cam));
   }
   const int64_t m = compact_slot(e < n && p.ok, w.status, fs->epoch + TK_COMPACT, part, s_warp,
                                  &s_base);
