@@ -92,6 +92,27 @@ __device__ __forceinline__ bool ellipse_meets_block(float mx, float my, float A,
   return !(qmax < lo - 1e-3f * (1.f + fabsf(lo)));  // NaN -> meets
 }
 
+// Does every pixel centre of the block [xlo,xhi] x [ylo,yhi] keep the member
+// for certain (fp32 qs > hi at every pixel, so no pixel lies in the guard
+// band)?  qs = A dx^2 + B2 dx dy + C dy^2 is concave (KQ < 0), so its minimum
+// over the block is at a corner; the per-pixel values the blend loop
+// computes differ from exact values by a few fp32 roundings of the terms,
+// and the corner values here likewise, so the test keeps a relative margin
+// of 4e-6 (about 60 ulps) over the terms' magnitude.
+__device__ __forceinline__ bool keeps_whole_block(float mx, float my, float A, float B2, float C,
+                                                  float hi, float xlo, float xhi, float ylo,
+                                                  float yhi) {
+  float qmin = INFINITY, mag = 0.f;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float dx = ((c & 1) ? xhi : xlo) - mx, dy = ((c & 2) ? yhi : ylo) - my;
+    const float a = A * dx * dx, b = B2 * dx * dy, cc = C * dy * dy;
+    qmin = fminf(qmin, (a + b) + cc);
+    mag = fmaxf(mag, (fabsf(a) + fabsf(b)) + fabsf(cc));
+  }
+  return qmin > hi + 4e-6f * (mag + fabsf(hi)) + 1e-30f;  // NaN -> false
+}
+
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -364,8 +385,18 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
                 ellipse_meets_block(mxl, myl, pj.As, pj.B2s, pj.Cs, pj.lo, wx_lo, wx_hi, wy_lo,
                                     wy_hi);
         }
+        // FAST (128-member batches): bit 7 of the entry marks a member every
+        // pixel of the block keeps for certain (the blend loop then skips the
+        // guard band)
+        bool ak = false;
+        if (!EXACT && hit) {
+          const Payload &pj = PL[j];
+          const float2 mm = reinterpret_cast<const float2 *>(&pj.mx)[0];
+          ak = keeps_whole_block(mm.x, mm.y, pj.As, pj.B2s, pj.Cs, pj.hi, wx_lo, wx_hi, wy_lo,
+                                 wy_hi);
+        }
         const uint32_t hm = __ballot_sync(FULL_MASK, hit);
-        if (hit) wl[cnt + __popc(hm & lanemask_lt())] = (uint8_t)j;
+        if (hit) wl[cnt + __popc(hm & lanemask_lt())] = (uint8_t)(j | (ak ? 0x80 : 0));
         cnt += __popc(hm);
       }
     }
@@ -380,7 +411,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
 #ifdef LODGE_COUNTERS
         c_iter += 1;
 #endif
-        const int j = lds_u8(wl_sa + (uint32_t)i);
+        const int j = lds_u8(wl_sa + (uint32_t)i);  // EXACT: 256-member batches, no flag
         const Payload &pj = PL[j];
           const Precise &d = S.pr[k][j];
           double wmax = 0.0;
@@ -416,7 +447,9 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
       // qs = KQ * q in exponent units: keep iff qs > hi (and the pixel is
       // alive: T >= t_min; out-of-image pixels hold T = -inf), re-decide in
       // fp64 iff lo <= qs <= hi, alpha = min(exp2(qs + log2 o), clamp)
-      auto quad = [&](const Payload &pj, float (&qs)[PX], float4 &mm, float4 &cn) -> bool {
+      // band: test the guard band (members not flagged all-keep)
+      auto quad = [&](const Payload &pj, float (&qs)[PX], float4 &mm, float4 &cn,
+                      const bool band) -> bool {
         mm = reinterpret_cast<const float4 *>(&pj.mx)[0];  // mx, my, mid, half
         cn = *reinterpret_cast<const float4 *>(&pj.As);   // KQ*(A, 2B, C), log2 o
         const float dx = fpx - mm.x;
@@ -426,7 +459,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
         for (int p = 0; p < PX; ++p) {
           const float dy = (fpy0 + 2.f * p) - mm.y;
           qs[p] = fmaf(dy, fmaf(cn.z, dy, bdx), adx2);
-          near |= fabsf(qs[p] - mm.z) <= mm.w;
+          if (band) near |= fabsf(qs[p] - mm.z) <= mm.w;
         }
         return near;
       };
@@ -453,16 +486,27 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
       // one pixel's blend step with every decision certain in fp32; one PTX
       // block keeps the keep test a predicate (nvcc otherwise materialises
       // the count increment as a select and a copy)
-      auto step = [&](int p, float qs, float hi, float a, const float4 &c, float &wmax) {
+      auto step = [&](int p, float qs, float hi, float a, const float4 &c, float &wmax,
+                      const bool all_keep) {
         float w;
-        asm("{\n\t.reg .pred k;\n\t"
-            "setp.ge.f32 k, %2, %4;\n\t"
-            "setp.gt.and.f32 k, %3, %5, k;\n\t"
-            "mul.rn.f32 %0, %2, %6;\n\t"
-            "selp.f32 %0, %0, 0f00000000, k;\n\t"
-            "@k add.s32 %1, %1, 1;\n\t}"
-            : "=f"(w), "+r"(vis[p])
-            : "f"(T[p]), "f"(qs), "f"(cpar.tmin_f), "f"(hi), "f"(a));
+        if (all_keep) {  // qs > hi at every pixel of the block
+          asm("{\n\t.reg .pred k;\n\t"
+              "setp.ge.f32 k, %2, %3;\n\t"
+              "mul.rn.f32 %0, %2, %4;\n\t"
+              "selp.f32 %0, %0, 0f00000000, k;\n\t"
+              "@k add.s32 %1, %1, 1;\n\t}"
+              : "=f"(w), "+r"(vis[p])
+              : "f"(T[p]), "f"(cpar.tmin_f), "f"(a));
+        } else {
+          asm("{\n\t.reg .pred k;\n\t"
+              "setp.ge.f32 k, %2, %4;\n\t"
+              "setp.gt.and.f32 k, %3, %5, k;\n\t"
+              "mul.rn.f32 %0, %2, %6;\n\t"
+              "selp.f32 %0, %0, 0f00000000, k;\n\t"
+              "@k add.s32 %1, %1, 1;\n\t}"
+              : "=f"(w), "+r"(vis[p])
+              : "f"(T[p]), "f"(qs), "f"(cpar.tmin_f), "f"(hi), "f"(a));
+        }
         if (need_image) {
           cr[p] = fmaf(w, c.x, cr[p]);
           cg[p] = fmaf(w, c.y, cg[p]);
@@ -483,7 +527,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
         const Payload &pj = PL[j];
         float qs[PX];
         float4 mm, cn;
-        const bool near = quad(pj, qs, mm, cn);
+        const bool near = quad(pj, qs, mm, cn, true);
         const float hi = pj.hi;
         const float4 c = colour(pj);
         float wmax = 0.f;
@@ -528,20 +572,23 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
         } else {
 #pragma unroll
           for (int p = 0; p < PX; ++p)
-            step(p, qs[p], hi, fminf(ex2_approx(qs[p] + cn.w), cpar.clamp_f), c, wmax);
+            step(p, qs[p], hi, fminf(ex2_approx(qs[p] + cn.w), cpar.clamp_f), c, wmax, false);
         }
         finish(j, wmax);
       };
       // G consecutive members: all quadratic forms and alphas first (they do
       // not depend on T), then the blend steps in list order
+      // ak: every member of the group is flagged all-keep for this warp's
+      // block: no guard band, no keep test beyond T >= t_min
       constexpr int G = LODGE_COMP_GROUP;
-      auto group = [&](const int (&js)[G]) {
+      auto group = [&](const int (&js)[G], const bool AK) {
         float q[G][PX];
         float4 mm[G], cn[G];
         bool near = false;
 #pragma unroll
-        for (int u = 0; u < G; ++u) near |= quad(PL[js[u]], q[u], mm[u], cn[u]);
-        if (__any_sync(FULL_MASK, near)) {
+        for (int u = 0; u < G; ++u)
+          near |= quad(PL[js[u]], q[u], mm[u], cn[u], !AK);
+        if (!AK && __any_sync(FULL_MASK, near)) {
 #pragma unroll
           for (int u = 0; u < G; ++u) one(js[u]);
           return;
@@ -562,7 +609,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
           const float4 c = colour(pj);
           wm[u] = 0.f;
 #pragma unroll
-          for (int p = 0; p < PX; ++p) step(p, q[u][p], hi, a[u][p], c, wm[u]);
+          for (int p = 0; p < PX; ++p) step(p, q[u][p], hi, a[u][p], c, wm[u], AK);
         }
         if (record_max) {  // the group's warp reductions back to back
           unsigned wb[G];
@@ -580,20 +627,26 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
       for (; i + G <= cnt; i += G) {
         if (!__any_sync(FULL_MASK, live_any())) break;
         int js[G];
+        uint32_t allk = 0x80;
 #pragma unroll
-        for (int u = 0; u < G; ++u) js[u] = lds_u8(wl_sa + (uint32_t)(i + u));
-        group(js);
+        for (int u = 0; u < G; ++u) {
+          const uint32_t ent = lds_u8(wl_sa + (uint32_t)(i + u));
+          js[u] = (int)(ent & 0x7f);
+          allk &= ent;
+        }
+        if (allk) group(js, true);
+        else group(js, false);
       }
       if (i + G > cnt) {  // the tail (the loop did not stop on dead pixels)
         for (; i < cnt; ++i) {
           if (!__any_sync(FULL_MASK, live_any())) break;
-          one(lds_u8(wl_sa + (uint32_t)i));
+          one(lds_u8(wl_sa + (uint32_t)i) & 0x7f);
         }
       }
       done_i = i;
     }
     if (alive0 && done_i > 0 && !__any_sync(FULL_MASK, live_any()))
-      wend = b + lds_u8(wl_sa + (uint32_t)(done_i - 1)) + 1u;
+      wend = b + (lds_u8(wl_sa + (uint32_t)(done_i - 1)) & (EXACT ? 0xffu : 0x7fu)) + 1u;
     __syncthreads();
     if (record_max) {
 #pragma unroll

@@ -519,7 +519,7 @@ __device__ __forceinline__ Proj slot_project(const ProjLevels &lv, const Work &w
 // the bench sweep: the tiles finish early).
 template <typename GT, typename ST>
 #ifndef LODGE_PROJ_MINB
-#define LODGE_PROJ_MINB 2  // resident CTAs per SM (the persistent grid's size)
+#define LODGE_PROJ_MINB 3  // resident CTAs per SM (the persistent grid's size; 80 registers)
 #endif
 __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLevels lv, Work w, FrameState *fs,
                                                        const lodge_camera *__restrict__ cam_p,

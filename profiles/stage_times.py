@@ -54,8 +54,12 @@ def main():
     torch.cuda.synchronize()
     ms, n = r.profile_read()
     st = fr.read_stats()
+    import ctypes as C
+    cnt = (C.c_uint64 * 8)()
+    N.check(N.lib().lodge_debug_counters(r.ctx.ptr, cnt), "counters")
     out = {"lib": os.environ.get("LODGE_LIB", "") or "liblodge", "config": a.config,
            "frames": n, "store": a.store,
+           "counters_last_frame": list(cnt), "comp_members": int(st.comp_members),
            "stage_ms": {k: round(float(v) / max(n, 1), 5) for k, v in zip(N.STAGES, ms)},
            "frame_ms": round(float(sum(ms)) / max(n, 1), 4), "last_fault": int(st.fault)}
     print(json.dumps(out), flush=True)

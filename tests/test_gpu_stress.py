@@ -56,10 +56,8 @@ def test_frames_in_flight_bitwise():
 
 def _verify_lib():
     from paper_2505_23158_b200 import _native
-    path = os.path.join(os.path.dirname(_native.LIB_PATH), "liblodge_verify.so")
-    if not os.path.exists(path):
-        _native.build()
-    return path
+    _native.build()  # make: brings the diagnostic variants up to date with the sources
+    return os.path.join(os.path.dirname(_native.LIB_PATH), "liblodge_verify.so")
 
 
 def test_frames_in_flight_verify_build():
