@@ -86,6 +86,12 @@ typedef struct {
    * (whose geom_dev / sh_dev may be NULL). */
   const void *const *slab_geom_dev;
   const void *const *slab_sh_dev;
+  /* Identity of the plan's contents (any value unique to this plan for its
+   * lifetime; 0: none).  A context whose previous frame used the same plan
+   * uid and chunk pair reuses that frame's union (the sets, their tags and
+   * sizes depend only on the pair; t enters at the projection), skipping
+   * compose_active's merge -- consecutive views of a path share the pair. */
+  uint64_t uid;
 } lodge_chunks;
 
 /* Compositing precision.  FAST: fp32 FMA/MUFU compositing with an fp64

@@ -57,7 +57,7 @@ class Chunks(C.Structure):
     _fields_ = [("K", C.c_int32), ("L", C.c_int32), ("centers_dev", C.c_void_p),
                 ("offsets_dev", C.c_void_p), ("data_dev", C.c_void_p),
                 ("max_set", C.c_int64 * MAX_LEVELS), ("slab_geom_dev", C.c_void_p),
-                ("slab_sh_dev", C.c_void_p)]
+                ("slab_sh_dev", C.c_void_p), ("uid", C.c_uint64)]
 
 
 class FrameOut(C.Structure):

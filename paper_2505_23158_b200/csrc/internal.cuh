@@ -31,6 +31,12 @@ struct FrameState {
   uint32_t n_owners_b;                // second-phase splats that meet an alive tile
   uint32_t alive_box[4];              // x0, x1, y0, y1: bounding box of the alive tiles
   uint32_t fault_sticky;              // OR of every frame's stats.fault (lodge_fault_flags)
+  // union reuse (lodge_chunks.uid): the pair and sizes of the union held in
+  // the context's union buffers
+  uint64_t uc_uid;                    // 0: nothing cached
+  int32_t uc_f, uc_o;
+  uint32_t uc_U[LODGE_MAX_LEVELS];
+  uint32_t uc_hit;                    // this frame reuses the cached union
   unsigned long long counters[8];     // LODGE_COUNTERS builds: compositing work counters
 };
 

@@ -178,7 +178,16 @@ struct UnionArgs {
   uint32_t slot_base[LODGE_MAX_LEVELS + 1];
   uint32_t part_base[LODGE_MAX_LEVELS + 1];  // CTA-count table offsets per level
   int32_t slab;                              // write set positions (chunk slabs)
+  uint64_t uid;                              // lodge_chunks.uid (0: no reuse)
 };
+
+// Reuse of the previous frame's union (same plan contents and chunk pair):
+// decided once per frame by k_union_check, read by the union kernels.
+__global__ void k_union_check(uint64_t uid, FrameState *fs) {
+  if (threadIdx.x != 0) return;
+  fs->uc_hit = (uid != 0 && fs->uc_uid == uid && fs->uc_f == fs->stats.f &&
+                fs->uc_o == fs->stats.o) ? 1u : 0u;
+}
 
 // The two sorted sets of level l for the frame's chunk pair.
 struct UnionLevel {
@@ -214,6 +223,7 @@ __device__ __forceinline__ int union_level_of(const UnionArgs &a, uint32_t g, ui
 // splits[part_base[l] + l + p] = #A among the first min(UN_TILE p, n_l)
 // merged elements, p = 0 .. ceil(n_l / UN_TILE).
 __global__ void k_union_split(UnionArgs a, FrameState *fs, uint32_t *splits) {
+  if (fs->uc_hit) return;
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= a.part_base[a.L] + a.L) return;
   int l = 0;
@@ -248,6 +258,7 @@ __global__ void __launch_bounds__(UN_THREADS) k_union_merge(UnionArgs a, FrameSt
   __shared__ uint32_t s_a[UN_TILE + 2], s_b[UN_TILE + 1];  // A[i0-1 .. i1], B[j0 .. j1]
   __shared__ uint32_t s_w[UN_THREADS / 32 + 1];
   __shared__ uint32_t s_tk;
+  if (fs->uc_hit) return;  // block-uniform: the previous frame's union is this one
   const uint32_t g = take_ticket(&fs->tickets[TK_UNION0], &s_tk);
   uint32_t part;
   const int l = union_level_of(a, g, part);
@@ -334,8 +345,20 @@ __global__ void __launch_bounds__(UN_THREADS) k_union_merge(UnionArgs a, FrameSt
   }
 }
 
-__global__ void k_union_sizes(int32_t L, FrameState *fs) {
+// mode 1: chunk union (record or reuse the cache); 0: band selection (the
+// union buffers now hold something else: drop the cache)
+__global__ void k_union_sizes(int32_t L, FrameState *fs, int32_t mode, uint64_t uid) {
   if (threadIdx.x != 0) return;
+  if (mode == 0) {
+    fs->uc_uid = 0;
+  } else if (fs->uc_hit) {
+    for (int l = 0; l < L; ++l) fs->stats.U_level[l] = fs->uc_U[l];
+  } else {
+    for (int l = 0; l < L; ++l) fs->uc_U[l] = fs->stats.U_level[l];
+    fs->uc_uid = uid;
+    fs->uc_f = fs->stats.f;
+    fs->uc_o = fs->stats.o;
+  }
   uint32_t U = 0;
   for (int l = 0; l < L; ++l) U += fs->stats.U_level[l];
   fs->stats.U = U;
@@ -447,7 +470,7 @@ void launch_band_select(const lodge_level *levels, int32_t L, const double *boun
   const uint32_t nparts = a.part_base[L];
   if (nparts > 0)
     k_band_select<<<nparts, UN_THREADS, 0, s>>>(a, fs, pos, status, union_idx, union_tag);
-  k_union_sizes<<<1, 32, 0, s>>>(L, fs);
+  k_union_sizes<<<1, 32, 0, s>>>(L, fs, 0, 0ull);
 }
 
 int launch_union(const lodge_chunks &ch, const LevelSlots &ls, FrameState *fs, uint64_t *status,
@@ -461,6 +484,7 @@ int launch_union(const lodge_chunks &ch, const LevelSlots &ls, FrameState *fs, u
   for (int l = 0; l < ch.L; ++l) max_slots = max(max_slots, ls.slot_base[l + 1] - ls.slot_base[l]);
   a.status_stride = union_status_stride(max_slots);
   a.slab = ch.slab_geom_dev != nullptr ? 1 : 0;
+  a.uid = ch.uid;
   a.part_base[0] = 0;
   for (int l = 0; l < ch.L; ++l)
     a.part_base[l + 1] =
@@ -471,13 +495,14 @@ int launch_union(const lodge_chunks &ch, const LevelSlots &ls, FrameState *fs, u
   const uint32_t nparts = a.part_base[ch.L];
   uint32_t *splits = reinterpret_cast<uint32_t *>(status);
   uint64_t *lb = status + (nparts + ch.L + 2) / 2 + 1;
-  int launches = 1;
+  int launches = 2;
+  k_union_check<<<1, 32, 0, s>>>(a.uid, fs);
   if (max_slots > 0 && nparts > 0) {
     k_union_split<<<(nparts + ch.L + 255) / 256, 256, 0, s>>>(a, fs, splits);
     k_union_merge<<<nparts, UN_THREADS, 0, s>>>(a, fs, splits, lb, union_idx, union_tag);
     launches += 2;
   }
-  k_union_sizes<<<1, 32, 0, s>>>(ch.L, fs);
+  k_union_sizes<<<1, 32, 0, s>>>(ch.L, fs, 1, a.uid);
   return launches;  // kernels enqueued
 }
 

@@ -158,6 +158,9 @@ static int ensure_slots(lodge_ctx *c, int64_t need) {
   int64_t ncap = std::max<int64_t>(need, 4096);
   cudaFree(w.union_idx); cudaFree(w.union_tag);
   w.slot_cap = 0;
+  // the cached union lived in the freed buffers
+  CK(cudaMemset(reinterpret_cast<char *>(c->fs) + offsetof(FrameState, uc_uid), 0,
+                sizeof(uint64_t)));
   CK(cudaMalloc(&w.union_idx, 4 * ncap));
   CK(cudaMalloc(&w.union_tag, ncap));
   w.slot_cap = ncap;

@@ -167,6 +167,19 @@ class DeviceLevel:
         return self.geom.numel() * self.geom.element_size() + self.sh.numel() * self.sh.element_size()
 
 
+_uid_lock = threading.Lock()
+_uid = [0]
+
+
+def _next_uid() -> int:
+    """Process-unique plan identity (lodge_chunks.uid): never reused, so a
+    context's union reuse can never mistake a new plan at a recycled address
+    for the one it cached."""
+    with _uid_lock:
+        _uid[0] += 1
+        return (os.getpid() << 32) | _uid[0]
+
+
 class DevicePlan:
     """Chunk centres and all K*L sorted uint32 index sets, resident."""
 
@@ -192,6 +205,7 @@ class DevicePlan:
         self.data = torch.from_numpy(data.view(np.int32)).to(device)
         self.max_set = sizes.max(axis=0)
         self.struct = N.Chunks()
+        self.struct.uid = _next_uid()
         self.struct.K, self.struct.L = K, L
         self.struct.centers_dev = self.centers.data_ptr()
         self.struct.offsets_dev = self.offsets.data_ptr()
@@ -212,6 +226,7 @@ class DevicePlan:
         self.data = torch.from_numpy(data.view(np.int32)).to(device)
         self.max_set = np.diff(np.asarray(offsets)).reshape(self.K, self.L).max(axis=0)
         self.struct = N.Chunks()
+        self.struct.uid = _next_uid()
         self.struct.K, self.struct.L = self.K, self.L
         self.struct.centers_dev = self.centers.data_ptr()
         self.struct.offsets_dev = self.offsets.data_ptr()
@@ -233,6 +248,7 @@ class DevicePlan:
         self.data = data
         self.max_set = np.diff(offsets).reshape(self.K, self.L).max(axis=0)
         self.struct = N.Chunks()
+        self.struct.uid = _next_uid()
         self.struct.K, self.struct.L = self.K, self.L
         self.struct.centers_dev = self.centers.data_ptr()
         self.struct.offsets_dev = self.offsets.data_ptr()
@@ -327,6 +343,7 @@ class SlabStore:
     def attach(self, plan: "DevicePlan") -> "DevicePlan":
         plan.struct.slab_geom_dev = self.geom_tab.data_ptr()
         plan.struct.slab_sh_dev = self.sh_tab.data_ptr()
+        plan.struct.uid = _next_uid()  # slab unions hold set positions, not indices
         plan._slabs = self  # keep the slabs alive with the plan
         return plan
 

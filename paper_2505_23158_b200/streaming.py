@@ -126,6 +126,8 @@ class StreamingStore:
 
     def attach(self, plan: DevicePlan) -> DevicePlan:
         """Point a DevicePlan at the slab tables (slab mode)."""
+        from .device import _next_uid
+        plan.struct.uid = _next_uid()  # slab unions hold set positions, not indices
         plan.struct.slab_geom_dev = self.geom_tab.data_ptr()
         plan.struct.slab_sh_dev = self.sh_tab.data_ptr()
         return plan

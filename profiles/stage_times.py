@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--config", default="config3")
     ap.add_argument("--frames", type=int, default=64)
     ap.add_argument("--store", default="flat", choices=["flat", "slab"])
+    ap.add_argument("--phase-budget", type=int, default=1280)
     a = ap.parse_args()
     import torch
 
@@ -37,7 +38,8 @@ def main():
     plan = DevicePlan.from_arrays(cfg.centers, cfg.offsets, cfg.data, cfg.L, dev)
     if a.store == "slab":
         plan = SlabStore(levels, plan).attach(plan)
-    r = L.Renderer(levels, plan, device=dev, storage="fp32", precision="fast")
+    r = L.Renderer(levels, plan, device=dev, storage="fp32", precision="fast",
+                   phase_budget=a.phase_budget)
     nv = bench.sweep_views(a.config)
     sweep = cfg.sweep(nv)
     timed, _ = bench.schedules(0, 1, a.frames, 0, 16, nv)
@@ -58,7 +60,7 @@ def main():
     cnt = (C.c_uint64 * 8)()
     N.check(N.lib().lodge_debug_counters(r.ctx.ptr, cnt), "counters")
     out = {"lib": os.environ.get("LODGE_LIB", "") or "liblodge", "config": a.config,
-           "frames": n, "store": a.store,
+           "frames": n, "store": a.store, "phase_budget": a.phase_budget,
            "counters_last_frame": list(cnt), "comp_members": int(st.comp_members),
            "stage_ms": {k: round(float(v) / max(n, 1), 5) for k, v in zip(N.STAGES, ms)},
            "frame_ms": round(float(sum(ms)) / max(n, 1), 4), "last_fault": int(st.fault)}
