@@ -12,6 +12,10 @@ for order and range on the device (lodge_asset_check_sets).  Rotations are
 stored raw and normalised in fp64 at projection time (LODGE_GEOM_QNORM),
 which reproduces read_asset's load-time normalisation bit for bit.
 
+Restated host code: the manifest, range and count checks below follow
+read_asset (reference src/assets.py:358-472) in order and message text --
+the AssetError messages are part of the drop-in contract.
+
 The manifest, range and count checks are host logic in read_asset's order
 and raise AssetError with its messages (src/assets.py:358-472); the
 value and index-set checks raise the same messages from the device results.

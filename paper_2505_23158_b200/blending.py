@@ -5,6 +5,12 @@ nearest_two_chunks / blend_factor / compose_active run as liblodge kernels
 (K0 select, K1 union with blend tags, fp64 in the reference's operation
 order); stream_step is the reference's O(1) host state machine restated on
 top of them.
+
+Restated host code: `_state_for` and `stream_step` follow reference
+src/blending.py:140-194 line for line (the state machine's events, order and
+messages are part of the drop-in contract, SURVEY.md 2 row 4 keeps it on the
+host); only the two distance / blend-factor evaluations inside are routed to
+the device.  The validation messages of compose_active follow :110-118.
 """
 
 from __future__ import annotations

@@ -49,9 +49,13 @@ def host_pair(centers, position):
 
 
 class StreamingStore:
-    def __init__(self, levels, centers, offsets, data, device, n_slots: int = 3):
+    def __init__(self, levels, centers, offsets, data, device, n_slots: int = 3,
+                 level_flags: int = 0):
         """levels: [(geom (n,12) fp32, sh (n,3,T) fp32)] host arrays; the plan
-        as centers (K,3), offsets (K*L+1), data (uint32 sets)."""
+        as centers (K,3), offsets (K*L+1), data (uint32 sets).  level_flags:
+        extra lodge_level flags of every level (LODGE_GEOM_QNORM for an
+        asset's raw rotations, normalised at projection as read_asset does)."""
+        self.level_flags = int(level_flags)
         if n_slots < 2:
             raise ValueError("a blended frame needs two resident chunks")
         self.device = torch.device(device)
@@ -115,7 +119,7 @@ class StreamingStore:
             lv = DeviceLevel.__new__(DeviceLevel)
             lv.geom = lv.sh = None
             lv.n, lv.degree = n, self.degree
-            lv.flags = N.GEOM_FP32 | N.SH_FP32
+            lv.flags = N.GEOM_FP32 | N.SH_FP32 | self.level_flags
             s = N.Level()
             s.n, s.sh_degree, s.flags = n, self.degree, lv.flags
             s.geom_dev = None

@@ -9,7 +9,11 @@ the GPU in one call (a fused projection + cover + distance kernel compacted
 in batch order, the onesweep sort stable over that order, a scan); the band
 sums stay two binary searches per band on the host, as in the reference.
 
-ThresholdSearcher mirrors the reference class with device tables.  The
+ThresholdSearcher mirrors the reference class with device tables.
+Restated host code: apart from `_table` (the device tables) and
+`evaluate_cost`, the class follows reference src/thresholds.py:51-120 near
+verbatim -- the band sums, caching and CostEvaluation fields must come out
+identical for the reference's greedy_search to accept it.  The
 provisional levels come from a level builder (the reference's own
 `splatlod.lod.build_level`; the LOD build is outside this package's scope),
 and the reference's greedy_search accepts the searcher as is:

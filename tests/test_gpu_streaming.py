@@ -2,7 +2,8 @@
 slabs loaded asynchronously into a few device slots are bit-identical to
 frames rendered from the fully resident store (same fp32 records, same
 kernels), including across evictions and with frames in flight on several
-streams."""
+streams; and slab-mode frames built from the reference's own asset equal the
+reference's renders of it (golden vectors)."""
 
 import numpy as np
 import pytest
@@ -91,3 +92,55 @@ def test_host_pair_matches_device_selection(setup):
                                                     np.zeros(0, np.int64)), cam.position)
         assert (f, o) == (ff, oo)
         assert t == float(C1[f"v{v}/t"][1])
+
+
+def test_slab_frames_match_reference_asset():
+    """Slab mode against the reference itself: the chunk slabs are built from
+    the asset the reference wrote (tests/golden/asset_c1, fp32 records with
+    raw rotations, LODGE_GEOM_QNORM), rendered in EXACT precision with the
+    chunk pair decided on the host, and compared with the reference rendering
+    its own read_asset result (tests/golden/asset.npz; reference
+    src/blending.py:132-137, src/raster.py:380-449)."""
+    import torch
+    import paper_2505_23158_b200 as Lg
+    from paper_2505_23158_b200 import _native as N
+    from paper_2505_23158_b200 import asset as A
+    from paper_2505_23158_b200.device import DevicePlan
+    from paper_2505_23158_b200.streaming import StreamingStore, host_pair
+    from .golden_util import GOLDEN
+    import os
+    gold = load("asset.npz")
+    ast = A.load_asset(os.path.join(GOLDEN, "asset_c1"))
+    dev = torch.device("cuda", 0)
+    levels = [(lv.geom.cpu().numpy(), lv.sh.cpu().numpy()) for lv in ast.levels]
+    centers = ast.plan.centers.cpu().numpy()
+    offsets = ast.plan.offsets.cpu().numpy()
+    data = ast.plan.data.cpu().numpy().view(np.uint32)
+    store = StreamingStore(levels, centers, offsets, data, dev, n_slots=2,
+                           level_flags=N.GEOM_QNORM)
+    plan = store.attach(DevicePlan.from_arrays(centers, offsets, data, len(levels), dev))
+    r = Lg.Renderer(store.device_levels(), plan, dev, precision="exact")
+    r.reserve(1 << 20)
+    for v in (1, 6):
+        cam = golden_cameras([v])[0]
+        f, o, t = host_pair(centers, cam.position)
+        p = f"v{v}/"
+        assert (f, o) == tuple(int(x) for x in gold[p + "pair"])
+        assert t == float(gold[p + "t"][1])
+        row = r.upload_cameras([cam])
+        fr = r.alloc_frame(128, 128)
+        s = r.stream_of(0)
+        store.require([f, o], s)
+        r.render(row[0], fr, pair=(f, o), t=t)
+        store.release([f, o], s)
+        torch.cuda.synchronize()
+        st = fr.read_stats()
+        assert st.fault == 0 and st.overflow == 0
+        assert np.array_equal(fr.tile_count.cpu().numpy(), gold[p + "tile_count"])
+        assert np.array_equal(fr.visible.cpu().numpy(), gold[p + "visible"])
+        np.testing.assert_allclose(fr.image.cpu().numpy(), gold[p + "image"], rtol=0,
+                                   atol=1e-12)
+        U = int(st.U)
+        assert U == gold[p + "maxw"].shape[0]
+        np.testing.assert_allclose(fr.maxw[:U].cpu().numpy(), gold[p + "maxw"], rtol=1e-12,
+                                   atol=0)
