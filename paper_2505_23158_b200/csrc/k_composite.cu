@@ -35,13 +35,18 @@
 
 namespace lodge {
 
-template <bool EXACT>
+// PH 2 (the second depth phase: few, long tiles) may use fewer pixels per
+// thread, i.e. more warps per tile, than the first (LODGE_COMP_PX2).
+template <bool EXACT, int PH = 0>
 struct CC {
   static constexpr int CB = EXACT ? 256 : 128;  // members per batch (divides 1024)
 #ifndef LODGE_COMP_PX
 #define LODGE_COMP_PX 4
 #endif
-  static constexpr int PX = EXACT ? 2 : LODGE_COMP_PX;  // pixels per thread
+#ifndef LODGE_COMP_PX2
+#define LODGE_COMP_PX2 2  // phase 2: 16 x 4 blocks, four warps per tile (few, long tiles)
+#endif
+  static constexpr int PX = EXACT ? 2 : (PH == 2 ? LODGE_COMP_PX2 : LODGE_COMP_PX);  // pixels per thread
   static constexpr int CT = 256 / PX;       // threads per CTA
   static constexpr int NW = CT / 32;        // warps; warp w owns rows [w*ROWS, (w+1)*ROWS)
   static constexpr int ROWS = 2 * PX;
@@ -148,15 +153,15 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
-template <bool EXACT>
+template <bool EXACT, int PH = 0>
 struct CompSmem {
-  static constexpr int CB = CC<EXACT>::CB;
+  static constexpr int CB = CC<EXACT, PH>::CB;
   Payload pl[2][CB];                         // TMA destinations (64 B each)
   Precise pr[EXACT ? 2 : 1][EXACT ? CB : 1];  // EXACT: fp64 records
   uint32_t m[2][CB];                           // member splat ids (guard re-check)
   unsigned long long maxw[EXACT ? CB : 1];
   uint32_t maxw32[CB];
-  uint8_t wlist[CC<EXACT>::NW * CB];
+  uint8_t wlist[CC<EXACT, PH>::NW * CB];
   uint64_t bar[2];
   uint32_t mt;  // end of the members the tile iterated (max over warps)
 };
@@ -190,15 +195,22 @@ template <bool EXACT, int MODE, int PH = 0>
 #ifndef LODGE_COMP_GROUP
 #define LODGE_COMP_GROUP 4  // list members per FAST iteration
 #endif
-__global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_composite(
+#ifndef LODGE_COMP_MINB2
+#define LODGE_COMP_MINB2 7  // phase 2 with LODGE_COMP_PX2 = 2 (128 threads): 72 registers
+#endif
+__global__ void __launch_bounds__(CC<EXACT, PH>::CT,
+                                  EXACT ? 1
+                                        : (CC<EXACT, PH>::PX < LODGE_COMP_PX ? LODGE_COMP_MINB2
+                                                                             : LODGE_COMP_MINB))
+    k_composite(
     const uint32_t *__restrict__ list, const uint32_t *__restrict__ tile_start,
     const uint32_t *__restrict__ tile_order, const Payload *__restrict__ payload,
     const Precise *__restrict__ precise, FrameState *fs, const CompParams cpar, void *image,
     int32_t *visible, void *maxw) {
-  constexpr int PX = CC<EXACT>::PX, CT = CC<EXACT>::CT, ROWS = CC<EXACT>::ROWS;
-  constexpr int CB = CC<EXACT>::CB;
+  constexpr int PX = CC<EXACT, PH>::PX, CT = CC<EXACT, PH>::CT, ROWS = CC<EXACT, PH>::ROWS;
+  constexpr int CB = CC<EXACT, PH>::CB;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  CompSmem<EXACT> &S = *reinterpret_cast<CompSmem<EXACT> *>(smem_raw);
+  CompSmem<EXACT, PH> &S = *reinterpret_cast<CompSmem<EXACT, PH> *>(smem_raw);
   const lodge_raster_params &rp = cpar.rp;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -223,6 +235,7 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
   }
 
   const float fpx = (float)lx + 0.5f, fpy0 = (float)ly0 + 0.5f;
+  const float clamp_l2 = log2f(cpar.clamp_f) - 1e-3f;  // all-keep members stay below the clamp
   const double gx = (double)px + 0.5, gy0 = (double)py0 + 0.5;
   const double ox = (double)(tx * 16), oy = (double)(ty * 16);
   constexpr uint32_t REC = EXACT ? 128u : 64u;  // bytes staged per member
@@ -392,7 +405,10 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
         if (!EXACT && hit) {
           const Payload &pj = PL[j];
           const float2 mm = reinterpret_cast<const float2 *>(&pj.mx)[0];
-          ak = keeps_whole_block(mm.x, mm.y, pj.As, pj.B2s, pj.Cs, pj.hi, wx_lo, wx_hi, wy_lo,
+          // ... and whose alpha never reaches the clamp (log2 o a margin below
+          // log2 clamp; qs <= 0 up to rounding), so the clamp is a no-op too
+          ak = pj.lo2 < clamp_l2 &&
+               keeps_whole_block(mm.x, mm.y, pj.As, pj.B2s, pj.Cs, pj.hi, wx_lo, wx_hi, wy_lo,
                                  wy_hi);
         }
         const uint32_t hm = __ballot_sync(FULL_MASK, hit);
@@ -600,7 +616,9 @@ __global__ void __launch_bounds__(CC<EXACT>::CT, EXACT ? 1 : LODGE_COMP_MINB) k_
 #pragma unroll
         for (int u = 0; u < G; ++u)
 #pragma unroll
-          for (int p = 0; p < PX; ++p) a[u][p] = fminf(ex2_approx(q[u][p] + cn[u].w), cpar.clamp_f);
+          for (int p = 0; p < PX; ++p)
+            a[u][p] = AK ? ex2_approx(q[u][p] + cn[u].w)
+                         : fminf(ex2_approx(q[u][p] + cn[u].w), cpar.clamp_f);
         float wm[G];
 #pragma unroll
         for (int u = 0; u < G; ++u) {
@@ -735,7 +753,7 @@ static void launch_comp(const Work &w, FrameState *fs, int32_t W, int32_t H,
                         uint32_t n_maxw, cudaStream_t s) {
   const int32_t tiles_x = (W + 15) / 16, tiles_y = (H + 15) / 16;
   const unsigned T = (unsigned)(tiles_x * tiles_y);
-  const size_t sm = sizeof(CompSmem<EXACT>);
+  const size_t sm = sizeof(CompSmem<EXACT, PH>);
   static PerDevice attr;
   if (!attr()) {
     cudaFuncSetAttribute(k_composite<EXACT, MODE, PH>,
@@ -756,7 +774,7 @@ static void launch_comp(const Work &w, FrameState *fs, int32_t W, int32_t H,
   cp.n_list = (uint32_t)std::min<int64_t>(2 * w.P_cap, 0xffffffffll);
   cp.n_payload = (uint32_t)w.M_cap;
   cp.n_maxw = n_maxw;
-  k_composite<EXACT, MODE, PH><<<T, CC<EXACT>::CT, sm, s>>>(
+  k_composite<EXACT, MODE, PH><<<T, CC<EXACT, PH>::CT, sm, s>>>(
       w.list, PH == 2 ? w.tile_start_b : w.tile_start, PH == 2 ? w.tile_order_b : w.tile_order,
       w.payload, w.precise, fs, cp, out.image_dev, out.visible_dev, out.maxw_dev);
 }
