@@ -118,6 +118,45 @@ __device__ __forceinline__ bool keeps_whole_block(float mx, float my, float A, f
   return qmin > hi + 4e-6f * (mag + fabsf(hi)) + 1e-30f;  // NaN -> false
 }
 
+// Packed fp32 pairs (sm_100 FADD2 / FMUL2 / FFMA2): two independent IEEE
+// round-to-nearest fp32 operations per instruction, lane by lane the same
+// result as the scalar add.rn / mul.rn / fma.rn, so the FAST blend keeps its
+// exact arithmetic while two pixels share each instruction.
+struct __align__(8) F2 {
+  float x, y;
+};
+__device__ __forceinline__ uint64_t f2u(F2 a) { return *reinterpret_cast<uint64_t *>(&a); }
+__device__ __forceinline__ F2 u2f(uint64_t v) { return *reinterpret_cast<F2 *>(&v); }
+__device__ __forceinline__ F2 f2_fma(F2 a, F2 b, F2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+  return u2f(d);
+}
+__device__ __forceinline__ F2 f2_add(F2 a, F2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(d);
+}
+__device__ __forceinline__ F2 f2_sub(F2 a, F2 b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(d);
+}
+__device__ __forceinline__ F2 f2_mul(F2 a, F2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(d);
+}
+__device__ __forceinline__ F2 f2b(float v) { return F2{v, v}; }
+
+// Per-thread pixel values, addressable as scalars (s[p]) or pixel pairs
+// (v[h] = pixels 2h, 2h + 1).
+template <int PX>
+union PxF {
+  F2 v[(PX + 1) / 2];
+  float s[PX];
+};
+
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -276,15 +315,15 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
     }
   };
 
-  float T[PX], cr[PX], cg[PX], cb[PX];                 // FAST
+  PxF<PX> Tu, cru, cgu, cbu;                           // FAST (pixel pairs for FFMA2)
   double tr[EXACT ? PX : 1], cp[EXACT ? PX : 1];      // EXACT transmittance
   double ir[EXACT ? PX : 1], ig[EXACT ? PX : 1], ib[EXACT ? PX : 1];
   double br[EXACT ? PX : 1], bg[EXACT ? PX : 1], bb[EXACT ? PX : 1];
   int32_t vis[PX];
 #pragma unroll
   for (int p = 0; p < PX; ++p) {
-    T[p] = 1.f;
-    cr[p] = cg[p] = cb[p] = 0.f;
+    Tu.s[p] = 1.f;
+    cru.s[p] = cgu.s[p] = cbu.s[p] = 0.f;
     vis[p] = 0;
   }
   if (EXACT) {
@@ -299,23 +338,23 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
 #pragma unroll
     for (int p = 0; p < PX; ++p) {
       if (!((alive >> p) & 1u)) {
-        T[p] = -INFINITY;
+        Tu.s[p] = -INFINITY;
       } else if (PH == 2) {  // resume the first phase's state
         const size_t pix = (size_t)(py0 + 2 * p) * cpar.W + px;
         const float4 st = cpar.state[pix];
-        T[p] = st.x;
-        cr[p] = st.y;
-        cg[p] = st.z;
-        cb[p] = st.w;
+        Tu.s[p] = st.x;
+        cru.s[p] = st.y;
+        cgu.s[p] = st.z;
+        cbu.s[p] = st.w;
         vis[p] = visible[pix];
       }
     }
   }
   auto live_any = [&]() -> bool {
     if (EXACT) return alive != 0u;
-    float m = T[0];
+    float m = Tu.s[0];
 #pragma unroll
-    for (int p = 1; p < PX; ++p) m = fmaxf(m, T[p]);
+    for (int p = 1; p < PX; ++p) m = fmaxf(m, Tu.s[p]);
     return m >= cpar.tmin_f;
   };
   uint32_t guard = 0;
@@ -479,6 +518,26 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
         }
         return near;
       };
+      // the same quadratic forms two pixels at a time (FFMA2; lane for lane
+      // the scalar fmaf chain above)
+      auto quad2 = [&](const Payload &pj, PxF<PX> &qs, float4 &mm, float4 &cn,
+                       const bool band) -> bool {
+        mm = reinterpret_cast<const float4 *>(&pj.mx)[0];  // mx, my, mid, half
+        cn = *reinterpret_cast<const float4 *>(&pj.As);   // KQ*(A, 2B, C), log2 o
+        const float dx = fpx - mm.x;
+        const float adx2 = cn.x * dx * dx, bdx = cn.y * dx;
+        bool near = false;
+#pragma unroll
+        for (int h = 0; h < PX / 2; ++h) {
+          const F2 dy = f2_sub(F2{fpy0 + 4.f * h, fpy0 + 4.f * h + 2.f}, f2b(mm.y));
+          qs.v[h] = f2_fma(dy, f2_fma(f2b(cn.z), dy, f2b(bdx)), f2b(adx2));
+          if (band) {
+            near |= fabsf(qs.v[h].x - mm.z) <= mm.w;
+            near |= fabsf(qs.v[h].y - mm.z) <= mm.w;
+          }
+        }
+        return near;
+      };
       auto colour = [&](const Payload &pj) {
         return need_image ? *reinterpret_cast<const float4 *>(&pj.r)
                           : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -512,7 +571,7 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
               "selp.f32 %0, %0, 0f00000000, k;\n\t"
               "@k add.s32 %1, %1, 1;\n\t}"
               : "=f"(w), "+r"(vis[p])
-              : "f"(T[p]), "f"(cpar.tmin_f), "f"(a));
+              : "f"(Tu.s[p]), "f"(cpar.tmin_f), "f"(a));
         } else {
           asm("{\n\t.reg .pred k;\n\t"
               "setp.ge.f32 k, %2, %4;\n\t"
@@ -521,17 +580,40 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
               "selp.f32 %0, %0, 0f00000000, k;\n\t"
               "@k add.s32 %1, %1, 1;\n\t}"
               : "=f"(w), "+r"(vis[p])
-              : "f"(T[p]), "f"(qs), "f"(cpar.tmin_f), "f"(hi), "f"(a));
+              : "f"(Tu.s[p]), "f"(qs), "f"(cpar.tmin_f), "f"(hi), "f"(a));
         }
         if (need_image) {
-          cr[p] = fmaf(w, c.x, cr[p]);
-          cg[p] = fmaf(w, c.y, cg[p]);
-          cb[p] = fmaf(w, c.z, cb[p]);
+          cru.s[p] = fmaf(w, c.x, cru.s[p]);
+          cgu.s[p] = fmaf(w, c.y, cgu.s[p]);
+          cbu.s[p] = fmaf(w, c.z, cbu.s[p]);
         }
-        T[p] -= w;
+        Tu.s[p] -= w;
         wmax = fmaxf(wmax, w);
 #ifdef LODGE_COUNTERS
         c_px += (w > 0.f) ? 1 : 0;
+#endif
+      };
+      // the blend step for pixels 2h and 2h + 1 (the same operations as
+      // step, paired: FMUL2 / FFMA2 / FADD2 with the keep selection per lane)
+      auto step2 = [&](int h, F2 qs, float hi, F2 a, const float4 &c, float &wmax,
+                       const bool all_keep) {
+        const int p0 = 2 * h, p1 = 2 * h + 1;
+        const bool k0 = Tu.s[p0] >= cpar.tmin_f && (all_keep || qs.x > hi);
+        const bool k1 = Tu.s[p1] >= cpar.tmin_f && (all_keep || qs.y > hi);
+        F2 w = f2_mul(Tu.v[h], a);
+        w.x = k0 ? w.x : 0.f;
+        w.y = k1 ? w.y : 0.f;
+        vis[p0] += k0 ? 1 : 0;
+        vis[p1] += k1 ? 1 : 0;
+        if (need_image) {
+          cru.v[h] = f2_fma(w, f2b(c.x), cru.v[h]);
+          cgu.v[h] = f2_fma(w, f2b(c.y), cgu.v[h]);
+          cbu.v[h] = f2_fma(w, f2b(c.z), cbu.v[h]);
+        }
+        Tu.v[h] = f2_sub(Tu.v[h], w);
+        wmax = fmaxf(wmax, fmaxf(w.x, w.y));
+#ifdef LODGE_COUNTERS
+        c_px += (w.x > 0.f ? 1 : 0) + (w.y > 0.f ? 1 : 0);
 #endif
       };
       // one member, including the guard band: pixels whose fp32 qs is within
@@ -553,7 +635,7 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
           float a[PX];
 #pragma unroll
           for (int p = 0; p < PX; ++p) {
-            kp[p] = T[p] >= cpar.tmin_f && qs[p] > hi;
+            kp[p] = Tu.s[p] >= cpar.tmin_f && qs[p] > hi;
             a[p] = fminf(ex2_approx(qs[p] + cn.w), cpar.clamp_f);
           }
           if (near) {
@@ -562,7 +644,7 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
             const Precise pr = precise[m];
 #pragma unroll
             for (int p = 0; p < PX; ++p) {
-              if (T[p] >= cpar.tmin_f && qs[p] >= lo && !(qs[p] > hi)) {
+              if (Tu.s[p] >= cpar.tmin_f && qs[p] >= lo && !(qs[p] > hi)) {
                 double ad;
                 kp[p] = !ref_decide(gx, gy0 + 2.0 * p, pg.mx, pg.my, pr, rp, ad);
                 a[p] = (float)ad;
@@ -572,13 +654,13 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
           }
 #pragma unroll
           for (int p = 0; p < PX; ++p) {
-            const float w = kp[p] ? T[p] * a[p] : 0.f;
+            const float w = kp[p] ? Tu.s[p] * a[p] : 0.f;
             if (need_image) {
-              cr[p] = fmaf(w, c.x, cr[p]);
-              cg[p] = fmaf(w, c.y, cg[p]);
-              cb[p] = fmaf(w, c.z, cb[p]);
+              cru.s[p] = fmaf(w, c.x, cru.s[p]);
+              cgu.s[p] = fmaf(w, c.y, cgu.s[p]);
+              cbu.s[p] = fmaf(w, c.z, cbu.s[p]);
             }
-            T[p] -= w;
+            Tu.s[p] -= w;
             if (kp[p]) ++vis[p];
             wmax = fmaxf(wmax, w);
 #ifdef LODGE_COUNTERS
@@ -598,12 +680,13 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
       // block: no guard band, no keep test beyond T >= t_min
       constexpr int G = LODGE_COMP_GROUP;
       auto group = [&](const int (&js)[G], const bool AK) {
-        float q[G][PX];
+        static_assert(PX % 2 == 0, "pixel pairs");
+        PxF<PX> q[G];
         float4 mm[G], cn[G];
         bool near = false;
 #pragma unroll
         for (int u = 0; u < G; ++u)
-          near |= quad(PL[js[u]], q[u], mm[u], cn[u], !AK);
+          near |= quad2(PL[js[u]], q[u], mm[u], cn[u], !AK);
         if (!AK && __any_sync(FULL_MASK, near)) {
 #pragma unroll
           for (int u = 0; u < G; ++u) one(js[u]);
@@ -612,13 +695,16 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
 #ifdef LODGE_COUNTERS
         c_iter += G;
 #endif
-        float a[G][PX];
+        PxF<PX> a[G];
 #pragma unroll
         for (int u = 0; u < G; ++u)
 #pragma unroll
-          for (int p = 0; p < PX; ++p)
-            a[u][p] = AK ? ex2_approx(q[u][p] + cn[u].w)
-                         : fminf(ex2_approx(q[u][p] + cn[u].w), cpar.clamp_f);
+          for (int h = 0; h < PX / 2; ++h) {
+            const F2 e = f2_add(q[u].v[h], f2b(cn[u].w));
+            const float a0 = ex2_approx(e.x), a1 = ex2_approx(e.y);
+            a[u].v[h] = AK ? F2{a0, a1}
+                           : F2{fminf(a0, cpar.clamp_f), fminf(a1, cpar.clamp_f)};
+          }
         float wm[G];
 #pragma unroll
         for (int u = 0; u < G; ++u) {
@@ -627,7 +713,7 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
           const float4 c = colour(pj);
           wm[u] = 0.f;
 #pragma unroll
-          for (int p = 0; p < PX; ++p) step(p, q[u][p], hi, a[u][p], c, wm[u], AK);
+          for (int h = 0; h < PX / 2; ++h) step2(h, q[u].v[h], hi, a[u].v[h], c, wm[u], AK);
         }
         if (record_max) {  // the group's warp reductions back to back
           unsigned wb[G];
@@ -726,7 +812,7 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
     const size_t pix = (size_t)py * cpar.W + px;
     if (visible) visible[pix] = vis[p];
     if (PH == 1 && resume) {
-      cpar.state[pix] = make_float4(T[p], cr[p], cg[p], cb[p]);
+      cpar.state[pix] = make_float4(Tu.s[p], cru.s[p], cgu.s[p], cbu.s[p]);
       continue;
     }
     if (!(need_image && image)) continue;
@@ -740,9 +826,9 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
       im[2] = fmin(fmax(b2, 0.0), 1.0);
     } else {
       float *im = reinterpret_cast<float *>(image) + 3 * pix;
-      im[0] = fminf(fmaxf(cr[p], 0.f), 1.f);
-      im[1] = fminf(fmaxf(cg[p], 0.f), 1.f);
-      im[2] = fminf(fmaxf(cb[p], 0.f), 1.f);
+      im[0] = fminf(fmaxf(cru.s[p], 0.f), 1.f);
+      im[1] = fminf(fmaxf(cgu.s[p], 0.f), 1.f);
+      im[2] = fminf(fmaxf(cbu.s[p], 0.f), 1.f);
     }
   }
 }
