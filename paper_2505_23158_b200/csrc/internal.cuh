@@ -106,6 +106,16 @@ struct Work {
   int64_t M_cap, P_cap, status_cap, slot_cap;
 };
 
+// The 32-bit depth keys ping-pong in the two halves of key_depth[1]; the
+// projection's compacted survivor keys start in the second half (the first
+// pass reads them and writes the first half).
+__host__ __device__ inline uint32_t *depth_keys32(const Work &w, int half) {
+  return reinterpret_cast<uint32_t *>(w.key_depth[1]) + (half ? w.M_cap : 0);
+}
+__host__ __device__ inline uint32_t *depth_keys_compact(const Work &w) {
+  return depth_keys32(w, 1);
+}
+
 // Device-side bounds checks: a violated invariant sets its bit in
 // stats.fault and the offending access is skipped (the frame is reported
 // invalid instead of faulting the context).
@@ -334,8 +344,12 @@ int launch_project_compat(const lodge_level &level, const int64_t *idx, int64_t 
 void launch_import_batch(const lodge_batch &b, int64_t M, const Work &w, FrameState *fs,
                          const lodge_camera *cam_dev, const lodge_raster_params &rp,
                          int32_t exact, cudaStream_t s);
+// Depth sort of the frame's inputs.  compacted: the projection left the M
+// survivors as (32-bit key, input index) in depth_keys_compact(w) and
+// val_depth[0] (any order); otherwise key_depth[0] holds fs->n_sort u64 keys
+// by position (~0: culled, dropped by the first pass), values the positions.
 void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
-                       cudaStream_t s);
+                       cudaStream_t s, bool compacted = false);
 void launch_depth_sort64(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
                          cudaStream_t s);
 void launch_debug_depth_sort(const Work &w, FrameState *fs, const uint64_t *keys, uint32_t n,

@@ -517,6 +517,9 @@ __device__ __forceinline__ Proj slot_project(const ProjLevels &lv, const Work &w
 // after them.  Colour and the compositing records are left to k_payload,
 // which runs only for the splats a frame composites (a few percent of M on
 // the bench sweep: the tiles finish early).
+#ifndef PROJ_RUN
+#define PROJ_RUN 128  // survivors staged per warp before a flush
+#endif
 template <typename GT, typename ST>
 #ifndef LODGE_PROJ_MINB
 #define LODGE_PROJ_MINB 3  // resident CTAs per SM (the persistent grid's size; 80 registers)
@@ -542,7 +545,30 @@ __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLeve
   // the tile grid is the frame's (host W, H), so the difference-array
   // indices stay in range whatever the device camera holds
   const uint32_t nslots = lv.slot_base[lv.L];
-  uint32_t nkeep_cta = 0;  // survivors seen by this thread's warp (lane 0 counts)
+  // survivors leave compacted (32-bit depth key, input index) for the depth
+  // sort, staged per warp and flushed in runs (one atomic per run on
+  // stats.M, which ends as the survivor count); the order of the runs does
+  // not matter: the sort orders by (key, fp64 key, index)
+  __shared__ uint32_t s_ck[8][PROJ_RUN], s_cg[8][PROJ_RUN];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t *const ckey = depth_keys_compact(w);
+  uint32_t wc = 0;  // staged survivors of this warp
+  auto flush = [&]() {
+    __syncwarp();
+    uint32_t b0 = 0;
+    if (lane == 0) b0 = atomicAdd(&fs->stats.M, wc);
+    b0 = __shfl_sync(FULL_MASK, b0, 0);
+    for (uint32_t i = lane; i < wc; i += 32) {
+      if (b0 + i < (uint32_t)w.M_cap) {
+        ckey[b0 + i] = s_ck[wid][i];
+        w.val_depth[0][b0 + i] = s_cg[wid][i];
+      } else {
+        raise_fault(fs, FAULT_SCATTER);
+      }
+    }
+    __syncwarp();
+    wc = 0;
+  };
   for (uint32_t base = blockIdx.x * blockDim.x; base < nslots; base += gridDim.x * blockDim.x) {
     const uint32_t slot = base + threadIdx.x;
     // map slot -> level
@@ -560,16 +586,32 @@ __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLeve
       p = slot_project<GT, ST>(lv, w, F, rp, l, slot, v, sp, gidx);
     }
     const bool keep = valid && p.ok;
-    nkeep_cta += __popc(__ballot_sync(FULL_MASK, keep));
+#ifdef LODGE_DEPTH64  // the 64-bit sort reads every input's key by position
+    if (valid) {
+      w.val_depth[0][g] = g;
+      if (!keep) w.key_depth[0][g] = ~0ull;
+    }
+    if (keep) atomicAdd(&fs->stats.M, 1u);
+    const uint32_t kb = 0u;
+#else
+    const uint32_t kb = __ballot_sync(FULL_MASK, keep);
+#endif
+    if (wc + __popc(kb) > PROJ_RUN) flush();
+    if (keep) {
+      const uint32_t at = wc + __popc(kb & ((1u << lane) - 1u));
+      s_ck[wid][at] = __float_as_uint(__double2float_rz(p.z));  // depth_key32
+      s_cg[wid][at] = g;
+    }
+    wc += __popc(kb);
     const uint64_t rc = keep ? tile_rect(p.mx, p.my, p.ex, p.ey, tiles_x, tiles_y) : 0ull;
     if (priv) add_tile_diff_shared(s_diff, rc, tiles_x, keep);
     else add_tile_diff(w.tile_diff, rc, tiles_x, keep);
-    if (!valid) continue;
-    w.val_depth[0][g] = g;
-    w.key_depth[0][g] = keep ? (uint64_t)__double_as_longlong(p.z) : ~0ull;
-    if (keep) w.rect[g] = rc;
+    if (keep) {  // the full key (tie repair) and the rectangle, by input index
+      w.key_depth[0][g] = (uint64_t)__double_as_longlong(p.z);
+      w.rect[g] = rc;
+    }
   }
-  if ((threadIdx.x & 31) == 0 && nkeep_cta) atomicAdd(&fs->stats.M, nkeep_cta);
+  if (wc) flush();
   if (priv) {
     __syncthreads();
     for (int32_t i = threadIdx.x; i < n_diff; i += blockDim.x) {

@@ -168,17 +168,26 @@ __global__ void __launch_bounds__(OS_THREADS, LODGE_OS_VMINB)
   }
 }
 
-// Histograms of the four 8-bit digits of the 32-bit depth keys.
+// Histograms of the four 8-bit digits of the 32-bit depth keys: of the u64
+// keys by position (n_sort of them, culled ~0 skipped) or, COMPACT, of the
+// projection's M compacted 32-bit survivor keys.
+template <bool COMPACT>
 __global__ void __launch_bounds__(256) k_depth_hist32(const uint64_t *__restrict__ keys,
+                                                     const uint32_t *__restrict__ keys32,
                                                      FrameState *fs) {
   __shared__ uint32_t h[4][256];
   for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
   __syncthreads();
-  const uint32_t n = fs->n_sort;
+  const uint32_t n = COMPACT ? fs->stats.M : fs->n_sort;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint64_t k = keys[i];
-    if (k == ~0ull) continue;  // culled: dropped by the first pass
-    const uint32_t k32 = depth_key32(k);
+    uint32_t k32;
+    if (COMPACT) {
+      k32 = keys32[i];
+    } else {
+      const uint64_t k = keys[i];
+      if (k == ~0ull) continue;  // culled: dropped by the first pass
+      k32 = depth_key32(k);
+    }
 #pragma unroll
     for (int p = 0; p < 4; ++p) atomicAdd(&h[p][(k32 >> (8 * p)) & 255u], 1u);
   }
@@ -441,7 +450,7 @@ void launch_list_verify(const Work &w, FrameState *fs, uint32_t T, bool second,
 // key_depth[1]; key_depth[0] keeps the full keys by input index for the tie
 // repair), sorted input indices in val_depth[0].
 void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
-                       cudaStream_t s) {
+                       cudaStream_t s, bool compacted) {
   if (M_cap <= 0) return;
 #ifdef LODGE_DEPTH64
   // opt-in: the eight 64-bit passes (0.17 vs 0.12 ms per config-3 frame)
@@ -450,7 +459,13 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
 #endif
   int hist_blocks = (int)((M_cap + 1023) / 1024);
   if (hist_blocks > 148 * 4) hist_blocks = 148 * 4;
-  k_depth_hist32<<<hist_blocks, 256, 0, s>>>(w.key_depth[0], fs);
+  uint32_t *k32[2] = {depth_keys32(w, 0), depth_keys32(w, 1)};
+  if (compacted) {
+    hist_blocks = std::max(1, hist_blocks / 2);  // 4 B per key instead of 8
+    k_depth_hist32<true><<<hist_blocks, 256, 0, s>>>(nullptr, k32[1], fs);
+  } else {
+    k_depth_hist32<false><<<hist_blocks, 256, 0, s>>>(w.key_depth[0], nullptr, fs);
+  }
   k_depth_scan<<<1, 256, 0, s>>>(fs);
   *launches += 2;
   constexpr int64_t TILE = (int64_t)OS_THREADS * LODGE_OS_ITEMS_D;
@@ -465,12 +480,16 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
   const int64_t resident = res();
   const unsigned grid = (unsigned)std::min<int64_t>((M_cap + TILE - 1) / TILE,
                                                     LODGE_PERSIST ? resident : 0x7fffffff);
-  uint32_t *k32[2] = {reinterpret_cast<uint32_t *>(w.key_depth[1]),
-                      reinterpret_cast<uint32_t *>(w.key_depth[1]) + M_cap};
-  // keys 0: u64 -> k32[0], 1: k32[0] -> k32[1], 2: k32[1] -> k32[0], 3: k32[0] -> k32[1]
-  k_depth_pass<true><<<grid, OS_THREADS, sm, s>>>(w.key_depth[0], nullptr, k32[0], w.val_depth[0],
-                                                  w.val_depth[1], &fs->n_sort, 0,
-                                                  fs->off_depth[0], w.status, fs, TK_DEPTH0);
+  // keys 0: u64 (or the compacted k32[1]) -> k32[0], 1: k32[0] -> k32[1],
+  // 2: k32[1] -> k32[0], 3: k32[0] -> k32[1]
+  if (compacted)
+    k_depth_pass<false><<<grid, OS_THREADS, sm, s>>>(nullptr, k32[1], k32[0], w.val_depth[0],
+                                                     w.val_depth[1], &fs->stats.M, 0,
+                                                     fs->off_depth[0], w.status, fs, TK_DEPTH0);
+  else
+    k_depth_pass<true><<<grid, OS_THREADS, sm, s>>>(w.key_depth[0], nullptr, k32[0],
+                                                    w.val_depth[0], w.val_depth[1], &fs->n_sort,
+                                                    0, fs->off_depth[0], w.status, fs, TK_DEPTH0);
 #ifdef LODGE_VERIFY
   k_pass_verify<<<296, 256, 0, s>>>(k32[0], w.val_depth[1], w.key_depth[0], &fs->stats.M, 0, 0,
                                     fs);

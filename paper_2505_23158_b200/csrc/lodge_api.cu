@@ -507,7 +507,7 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
   ++nl;
   DSYNC("launch_project_frame");
   c->mark(3);
-  launch_depth_sort(w, c->fs, U_cap, &nl, s);
+  launch_depth_sort(w, c->fs, U_cap, &nl, s, true);
   DSYNC("launch_depth_sort");
   DSYNC_L(2, "segment: select .. depth sort");
   c->mark(4);
