@@ -30,6 +30,8 @@ struct FrameState {
   uint32_t n_alive;                   // tiles the second phase composites
   uint32_t n_owners_b;                // second-phase splats that meet an alive tile
   uint32_t alive_box[4];              // x0, x1, y0, y1: bounding box of the alive tiles
+  uint32_t scan_a;                    // first-phase lists built by k_list_scan, not sorted
+  uint32_t n_sort_a;                  // first-phase pairs emitted and sorted (0 when scan_a)
   uint32_t fault_sticky;              // OR of every frame's stats.fault (lodge_fault_flags)
   // union reuse (lodge_chunks.uid): the pair and sizes of the union held in
   // the context's union buffers
@@ -368,7 +370,13 @@ void launch_enum_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles
 void launch_duplicate(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_cap,
                       cudaStream_t s);
 void launch_tile_sort(Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
-                      int32_t *launches, cudaStream_t s, int tk0 = 10 /* TK_TILE0 */);
+                      int32_t *launches, cudaStream_t s, int tk0 = 10 /* TK_TILE0 */,
+                      const uint32_t *n_keys = nullptr /* &fs->n_pairs */);
+// two-phase frames whose first phase is a few large splats (fs->scan_a, set
+// by k_tile_setup): the first-phase per-tile lists straight from the
+// depth-ordered rectangles, into w.list at tile_start (no pairs, no sort)
+void launch_list_scan(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
+                      cudaStream_t s);
 #ifdef LODGE_VERIFY
 // debug builds: order check of the per-tile lists of the last tile sort
 void launch_list_verify(const Work &w, FrameState *fs, uint32_t T, bool second, cudaStream_t s);

@@ -14,6 +14,13 @@
 
 namespace lodge {
 
+#ifndef LODGE_SCAN_MAX
+#define LODGE_SCAN_MAX 65536  // first-phase splats k_list_scan streams per block of tiles
+#endif
+#ifndef LODGE_SCAN_MIN_TILES
+#define LODGE_SCAN_MIN_TILES 64  // ... when they average at least this many tiles each
+#endif
+
 // Per-tile list layout from per-tile list counts (one block of 1024
 // threads): tile_start (T+1), the two onesweep tile-digit offset tables, the
 // heavy-first tile order (tiles with an empty list last; *s_nz = the
@@ -172,7 +179,133 @@ __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t *dif
     // all listed pairs); the host grows the buffers and renders the frame again
     fs->n_pairs = (int64_t)P <= P_cap ? s_tot : 0u;
     fs->stats.P_first = s_tot;
+    // a first phase of few splats with many tiles each (near, large splats)
+    // builds its lists by scanning their rectangles per block of tiles
+    // (k_list_scan) instead of emitting and sorting P_A pairs
+    const uint32_t S = fs->split_S;
+    const bool scan = diff_a && fs->n_pairs > 0 && S <= LODGE_SCAN_MAX &&
+                      (uint64_t)s_tot >= (uint64_t)LODGE_SCAN_MIN_TILES * S;
+    fs->scan_a = scan ? 1u : 0u;
+    fs->n_sort_a = scan ? 0u : fs->n_pairs;
   }
+}
+
+// First-phase per-tile lists by scanning (fs->scan_a): one CTA per block of
+// LS_W x LS_H tiles.  The CTA streams the depth-ordered rectangles of the
+// first-phase splats [0, split_S), keeps those that meet its block in order
+// (ballots + a CTA scan), and each warp -- one tile row of the block --
+// appends the members of its tiles to their lists, so every list is the
+// tile's first-phase splats in depth order: the list the emission + stable
+// tile sort would leave (reference src/raster.py:401-425), at the same
+// tile_start offsets.  Each tile's final count is checked against
+// tile_start (FAULT_LIST).
+constexpr int LS_W = 8, LS_H = 4;          // tiles per block: a warp per row
+constexpr int LS_THREADS = 32 * LS_H;
+constexpr int LS_R = 8;                    // rectangles per thread per scan round
+constexpr int LS_CAP = 2048;               // staged block members
+static_assert(LS_R * LS_H == 32, "one warp scans the round's (item, warp) counts");
+
+__global__ void __launch_bounds__(LS_THREADS) k_list_scan(const uint32_t *__restrict__ order,
+                                                          const uint64_t *__restrict__ rect,
+                                                          const uint32_t *__restrict__ tile_start,
+                                                          uint32_t *__restrict__ list,
+                                                          uint32_t n_list, FrameState *fs,
+                                                          int32_t tiles_x, int32_t tiles_y) {
+  __shared__ uint64_t s_rc[LS_CAP];
+  __shared__ uint32_t s_id[LS_CAP];
+  __shared__ uint32_t s_cnt[LS_R * LS_H];
+  if (!fs->scan_a) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bxn = (tiles_x + LS_W - 1) / LS_W;
+  const uint32_t bx0 = (blockIdx.x % bxn) * LS_W, by0 = (blockIdx.x / bxn) * LS_H;
+  const uint32_t bx1 = min(bx0 + LS_W, (uint32_t)tiles_x) - 1,
+                 by1 = min(by0 + LS_H, (uint32_t)tiles_y) - 1;
+  if (by0 >= (uint32_t)tiles_y) return;
+  const uint32_t ty = by0 + warp;
+  const bool row = ty <= by1;
+  uint32_t cur[LS_W];
+#pragma unroll
+  for (int i = 0; i < LS_W; ++i)
+    cur[i] = (row && bx0 + i <= bx1) ? tile_start[ty * tiles_x + bx0 + i] : 0u;
+  // the staged members [0, n) -> this warp's tile lists
+  auto drain = [&](uint32_t n) {
+    for (uint32_t q0 = 0; q0 < n; q0 += 32) {
+      const uint32_t q = q0 + lane;
+      const uint64_t rc = q < n ? s_rc[q] : 0ull;
+      const uint32_t x0 = rc & 0xffff, x1 = (rc >> 16) & 0xffff, y0 = (rc >> 32) & 0xffff,
+                     y1 = rc >> 48;
+      const bool inrow = row && q < n && y0 <= ty && ty <= y1;
+      if (!__any_sync(FULL_MASK, inrow)) continue;
+      const uint32_t id = q < n ? s_id[q] : 0u;
+#pragma unroll
+      for (int i = 0; i < LS_W; ++i) {
+        const uint32_t tx = bx0 + i;
+        const bool h = inrow && x0 <= tx && tx <= x1 && tx <= bx1;
+        const uint32_t b = __ballot_sync(FULL_MASK, h);
+        if (h) {
+          const uint32_t pos = cur[i] + __popc(b & ((1u << lane) - 1u));
+          if (pos < n_list) list[pos] = id;
+          else raise_fault(fs, FAULT_LIST);
+        }
+        cur[i] += __popc(b);
+      }
+    }
+  };
+  const uint32_t S = fs->split_S;
+  uint32_t n = 0;  // staged members (CTA-uniform)
+  for (uint32_t base = 0; base < S; base += LS_THREADS * LS_R) {
+    uint64_t rc[LS_R];
+    uint32_t hit = 0;
+#pragma unroll
+    for (int i = 0; i < LS_R; ++i) {
+      const uint32_t r = base + i * LS_THREADS + tid;
+      rc[i] = r < S ? rect[r] : 0ull;
+    }
+#pragma unroll
+    for (int i = 0; i < LS_R; ++i) {
+      const uint32_t r = base + i * LS_THREADS + tid;
+      const uint32_t x0 = rc[i] & 0xffff, x1 = (rc[i] >> 16) & 0xffff,
+                     y0 = (rc[i] >> 32) & 0xffff, y1 = rc[i] >> 48;
+      const bool h = r < S && x0 <= bx1 && x1 >= bx0 && y0 <= by1 && y1 >= by0;
+      const uint32_t b = __ballot_sync(FULL_MASK, h);
+      if (lane == 0) s_cnt[i * LS_H + warp] = __popc(b);
+      hit |= h ? (1u << i) : 0u;
+    }
+    __syncthreads();
+    // exclusive offsets over (item, warp) -- the depth order within the round
+    const uint32_t v = s_cnt[lane];
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const uint32_t total = __shfl_sync(FULL_MASK, inc, 31);
+    const uint32_t ex = inc - v;
+    if (n + total > (uint32_t)LS_CAP) {  // make room: drain what is staged
+      drain(n);
+      n = 0;
+    }
+    __syncthreads();  // s_cnt read by all (and the staging drained) before reuse
+#pragma unroll
+    for (int i = 0; i < LS_R; ++i) {
+      const bool h = (hit >> i) & 1u;
+      const uint32_t b = __ballot_sync(FULL_MASK, h);
+      const uint32_t off = __shfl_sync(FULL_MASK, ex, i * LS_H + warp);
+      if (h) {
+        const uint32_t at = n + off + __popc(b & ((1u << lane) - 1u));
+        s_rc[at] = rc[i];
+        s_id[at] = order[base + i * LS_THREADS + tid];
+      }
+    }
+    n += total;
+    __syncthreads();
+  }
+  drain(n);
+#pragma unroll
+  for (int i = 0; i < LS_W; ++i)
+    if (lane == 0 && row && bx0 + i <= bx1 && cur[i] != tile_start[ty * tiles_x + bx0 + i + 1])
+      raise_fault(fs, FAULT_LIST);
 }
 
 // Second phase of a two-phase frame (one block of 1024 threads): list
@@ -422,7 +555,7 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_emit(const uint32_t *__rest
                                                           int32_t tiles_x, Work w,
                                                           FrameState *fs, int32_t first_phase) {
   __shared__ EmitSmem<EMIT_CHUNK> E;
-  const uint32_t P = fs->n_pairs;
+  const uint32_t P = first_phase ? fs->n_sort_a : fs->n_pairs;
   const uint32_t n_own = first_phase ? fs->split_S : fs->stats.M;
   // persistent CTAs, grid-stride over the chunks
   for (uint32_t c = blockIdx.x; c * EMIT_CHUNK < P; c += gridDim.x) {
@@ -583,6 +716,15 @@ void launch_duplicate(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_
   if (M_cap <= 0) return;
   launch_dup_count(w, fs, tiles_x, M_cap, 0u, s);
   launch_dup_emit(w, fs, tiles_x, s, false);
+}
+
+void launch_list_scan(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
+                      cudaStream_t s) {
+  const unsigned grid = (unsigned)(((tiles_x + LS_W - 1) / LS_W) * ((tiles_y + LS_H - 1) / LS_H));
+  const uint32_t n_list = (uint32_t)std::min<int64_t>(w.P_cap, 0xffffffffll);
+  k_list_scan<<<grid, LS_THREADS, 0, s>>>(w.val_depth[0], w.rect_sorted, w.tile_start,
+                                          const_cast<uint32_t *>(w.list), n_list, fs, tiles_x,
+                                          tiles_y);
 }
 
 void launch_setup_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,

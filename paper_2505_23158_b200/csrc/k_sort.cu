@@ -618,13 +618,13 @@ static int bit_width(uint64_t v) {
 //             pass 2 on tile >> 8 -> list (u32 in pairs[0]).
 // Tile ranges come from tile_start, so the lists need no tile bits.
 void launch_tile_sort(Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
-                      int32_t *launches, cudaStream_t s, int tk0) {
+                      int32_t *launches, cudaStream_t s, int tk0, const uint32_t *n_keys) {
   const int64_t grid = w.P_cap;  // keys: the launchers size their grids
   const uint32_t T = (uint32_t)tiles_x * (uint32_t)tiles_y;
   const int lo_bits = std::min(8, std::max(1, bit_width(T - 1)));
   uint32_t *u32_1 = reinterpret_cast<uint32_t *>(w.pairs[1]);
   uint32_t *u32_0 = reinterpret_cast<uint32_t *>(w.pairs[0]);
-  const uint32_t *nin = &fs->n_pairs;
+  const uint32_t *nin = n_keys ? n_keys : &fs->n_pairs;
   const uint32_t *no_v = nullptr;
   uint32_t *no_vo = nullptr;
   const uint64_t *p0 = w.pairs[0];

@@ -530,7 +530,10 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
     launch_dup_emit(w, c->fs, tiles_x, s, true); ++nl;
     DSYNC("launch_dup_emit");
     c->mark(6);
-    launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s);
+    // sorted pairs (n_sort_a of them), or -- a first phase of few large
+    // splats -- the lists scanned from their rectangles; both leave w.list
+    launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s, TK_TILE0, &c->fs->n_sort_a);
+    launch_list_scan(w, c->fs, tiles_x, tiles_y, s); ++nl;
 #ifdef LODGE_VERIFY
     launch_list_verify(w, c->fs, (uint32_t)(tiles_x * tiles_y), false, s);
 #endif
