@@ -30,8 +30,12 @@ struct FrameState {
   uint32_t n_alive;                   // tiles the second phase composites
   uint32_t n_owners_b;                // second-phase splats that meet an alive tile
   uint32_t alive_box[4];              // x0, x1, y0, y1: bounding box of the alive tiles
-  uint32_t scan_a;                    // first-phase lists built by k_list_scan, not sorted
-  uint32_t n_sort_a;                  // first-phase pairs emitted and sorted (0 when scan_a)
+  // block lists: a phase whose splats are few and large keeps,
+  // per block of BLK_W x BLK_H tiles, its splats that meet the block in depth
+  // order with their tile masks; the compositor walks them instead of sorted
+  // per-tile lists
+  uint32_t scan_a, scan_b;            // phase 1 / phase 2 uses block lists
+  uint32_t n_sort_a, n_sort_b;        // pairs emitted and sorted per phase (0 with block lists)
   uint32_t fault_sticky;              // OR of every frame's stats.fault (lodge_fault_flags)
   // union reuse (lodge_chunks.uid): the pair and sizes of the union held in
   // the context's union buffers
@@ -51,7 +55,19 @@ enum Ticket {
   TK_DUPB = 20,    // second phase: enumeration scan
   TK_EMITB = 21,   //               ordered pair compaction
   TK_TILEB0 = 22,  //               tile passes (.. TK_TILEB0 + 1)
+  TK_BLA = 24,     // block lists, phase 1
+  TK_BLB = 25,     // block lists, phase 2
 };
+
+// Block lists: blocks of BLK_W x BLK_H tiles (tile bit (y % BLK_H) * BLK_W +
+// x % BLK_W of an entry's mask), scanned in chunks of BL_CHUNK splats, at
+// most BL_CHMAX chunks (a phase uses block lists only below that many splats).
+constexpr int BLK_W = 8, BLK_H = 4;
+constexpr int BL_CHUNK = 1024;
+constexpr int BL_CHMAX = 64;
+__host__ __device__ inline int32_t block_count(int32_t tiles_x, int32_t tiles_y) {
+  return ((tiles_x + BLK_W - 1) / BLK_W) * ((tiles_y + BLK_H - 1) / BLK_H);
+}
 
 // Splat payload for compositing (64 B, one per survivor).  mean2d is kept in
 // fp64 so the tile-local fp32 offset is exact to fp32 rounding.  The fp32
@@ -105,6 +121,8 @@ struct Work {
   uint32_t *union_idx;      // slots
   uint8_t *union_tag;       // slots
   uint32_t *vrank;          // LODGE_VERIFY builds: depth rank of each input (M_cap)
+  uint32_t *bl_start;       // 2 x (blocks + 1): per phase, block-list capacity offsets
+  uint32_t *bl_len;         // 2 x blocks: per phase, block-list lengths
   int64_t M_cap, P_cap, status_cap, slot_cap;
 };
 
@@ -372,11 +390,10 @@ void launch_duplicate(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_
 void launch_tile_sort(Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
                       int32_t *launches, cudaStream_t s, int tk0 = 10 /* TK_TILE0 */,
                       const uint32_t *n_keys = nullptr /* &fs->n_pairs */);
-// two-phase frames whose first phase is a few large splats (fs->scan_a, set
-// by k_tile_setup): the first-phase per-tile lists straight from the
-// depth-ordered rectangles, into w.list at tile_start (no pairs, no sort)
-void launch_list_scan(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
-                      cudaStream_t s);
+// two-phase frames whose phase `phase` (1, 2) has few large splats
+// (fs->scan_a / scan_b): its block lists, into pairs[phase - 1]
+void launch_block_lists(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
+                        int phase, cudaStream_t s);
 #ifdef LODGE_VERIFY
 // debug builds: order check of the per-tile lists of the last tile sort
 void launch_list_verify(const Work &w, FrameState *fs, uint32_t T, bool second, cudaStream_t s);

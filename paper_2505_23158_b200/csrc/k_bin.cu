@@ -14,11 +14,8 @@
 
 namespace lodge {
 
-#ifndef LODGE_SCAN_MAX
-#define LODGE_SCAN_MAX 65536  // first-phase splats k_list_scan streams per block of tiles
-#endif
 #ifndef LODGE_SCAN_MIN_TILES
-#define LODGE_SCAN_MIN_TILES 64  // ... when they average at least this many tiles each
+#define LODGE_SCAN_MIN_TILES 64  // block lists for a first phase whose splats average this many tiles
 #endif
 
 // Per-tile list layout from per-tile list counts (one block of 1024
@@ -121,6 +118,41 @@ __device__ __forceinline__ void integrate_diff(int32_t *sd, int32_t tiles_x, int
   __syncthreads();
 }
 
+// Block-list capacities (single CTA, after lists_from_counts, which leaves
+// s_sum free): out[b] = the exclusive prefix over blocks of the summed
+// per-tile counts cnt(t) of block b's tiles, out[nb] = the total.  A block's
+// list holds the splats that meet it, each covering >= 1 of its tiles, so its
+// length is at most its tiles' count sum.
+template <typename CountFn>
+__device__ void block_offsets(CountFn cnt, int32_t tiles_x, int32_t tiles_y, uint32_t *out,
+                              uint32_t *s_sum) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int nbx = (tiles_x + BLK_W - 1) / BLK_W, nb = block_count(tiles_x, tiles_y);
+  const int per = (nb + nt - 1) / nt, b0 = tid * per, b1 = min(nb, b0 + per);
+  uint32_t loc = 0;
+  for (int b = b0; b < b1; ++b) {
+    const int x0 = (b % nbx) * BLK_W, y0 = (b / nbx) * BLK_H;
+    uint32_t sum = 0;
+    for (int y = y0; y < min(y0 + BLK_H, tiles_y); ++y)
+      for (int x = x0; x < min(x0 + BLK_W, tiles_x); ++x) sum += cnt(y * tiles_x + x);
+    out[b] = loc;
+    loc += sum;
+  }
+  __syncthreads();
+  s_sum[tid] = loc;
+  __syncthreads();
+  for (int o = 1; o < nt; o <<= 1) {
+    const uint32_t v = tid >= o ? s_sum[tid - o] : 0u;
+    __syncthreads();
+    s_sum[tid] += v;
+    __syncthreads();
+  }
+  const uint32_t base = tid ? s_sum[tid - 1] : 0u;
+  for (int b = b0; b < b1; ++b) out[b] += base;
+  if (tid == nt - 1) out[nb] = s_sum[nt - 1];
+  __syncthreads();
+}
+
 // Single block.  diff: (ty+1) x (tx+1) over all survivors -> tile_count
 // (int32, may be NULL) = per_tile_count, P.  One-phase frames lay the lists
 // out from the same counts; two-phase frames (diff_a != NULL) from diff_a,
@@ -132,7 +164,7 @@ __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t *dif
                                                      int32_t *tile_count, uint32_t *count_all,
                                                      uint32_t *alive, uint32_t *tile_start,
                                                      uint32_t *tile_order, FrameState *fs,
-                                                     int64_t P_cap) {
+                                                     int64_t P_cap, uint32_t *bl_start) {
   extern __shared__ int32_t sd[];  // (tx+1)*(ty+1), twice with diff_a
   __shared__ uint32_t h0[256], h1[256];
   __shared__ uint32_t s_sum[1024];
@@ -171,108 +203,108 @@ __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t *dif
   const int32_t *lc = diff_a ? sa : sd;
   lists_from_counts([&](int t) { return at(lc, t); }, T, tile_start, tile_order, fs, s_sum, h0,
                     h1, s_bk, &s_tot, &s_nz);
+  __syncthreads();
+  const uint32_t P = s_all;
+  const uint32_t n_pairs = (int64_t)P <= P_cap ? s_tot : 0u;
+  // a first phase of few splats with many tiles each (near, large splats)
+  // keeps block lists (k_block_lists) instead of emitting and sorting P_A pairs
+  const uint32_t S = fs->split_S;
+  const bool scan = diff_a && n_pairs > 0 && S <= (uint32_t)(BL_CHUNK * BL_CHMAX) &&
+                    (uint64_t)s_tot >= (uint64_t)LODGE_SCAN_MIN_TILES * S;
+  if (scan) block_offsets([&](int t) { return at(lc, t); }, tiles_x, tiles_y, bl_start, s_sum);
   if (tid == 0) {
-    const uint32_t P = s_all;
     fs->stats.P = P;
     fs->stats.overflow = (int64_t)P > P_cap ? 1u : 0u;
     // on overflow nothing is duplicated or sorted (the digit offsets assume
     // all listed pairs); the host grows the buffers and renders the frame again
-    fs->n_pairs = (int64_t)P <= P_cap ? s_tot : 0u;
+    fs->n_pairs = n_pairs;
     fs->stats.P_first = s_tot;
-    // a first phase of few splats with many tiles each (near, large splats)
-    // builds its lists by scanning their rectangles per block of tiles
-    // (k_list_scan) instead of emitting and sorting P_A pairs
-    const uint32_t S = fs->split_S;
-    const bool scan = diff_a && fs->n_pairs > 0 && S <= LODGE_SCAN_MAX &&
-                      (uint64_t)s_tot >= (uint64_t)LODGE_SCAN_MIN_TILES * S;
     fs->scan_a = scan ? 1u : 0u;
-    fs->n_sort_a = scan ? 0u : fs->n_pairs;
+    fs->n_sort_a = scan ? 0u : n_pairs;
   }
 }
 
-// First-phase per-tile lists by scanning (fs->scan_a): one CTA per block of
-// LS_W x LS_H tiles.  The CTA streams the depth-ordered rectangles of the
-// first-phase splats [0, split_S), keeps those that meet its block in order
-// (ballots + a CTA scan), and each warp -- one tile row of the block --
-// appends the members of its tiles to their lists, so every list is the
-// tile's first-phase splats in depth order: the list the emission + stable
-// tile sort would leave (reference src/raster.py:401-425), at the same
-// tile_start offsets.  Each tile's final count is checked against
-// tile_start (FAULT_LIST).
-constexpr int LS_W = 8, LS_H = 4;          // tiles per block: a warp per row
-constexpr int LS_THREADS = 32 * LS_H;
-constexpr int LS_R = 8;                    // rectangles per thread per scan round
-constexpr int LS_CAP = 2048;               // staged block members
-static_assert(LS_R * LS_H == 32, "one warp scans the round's (item, warp) counts");
+// Block lists of a phase with few large splats (fs->scan_a / scan_b): for
+// each block of BLK_W x BLK_H tiles, the phase's splats that meet it, in
+// depth order, as (tile mask << 32 | splat id) -- bit (y % BLK_H) * BLK_W +
+// x % BLK_W set for every tile of the block the splat's rectangle covers.
+// A tile's members are exactly the entries with its bit set, in list order:
+// the tile's list of the emission + stable tile sort (reference
+// src/raster.py:401-425), which the compositor extracts as it goes.
+// Phase 1: the depth-ordered splats [0, split_S) (rect_sorted, val_depth[0]);
+// phase 2: the owners of k_dup_count<true> (rect, val_depth[1]), their
+// rectangles clipped to the alive tiles (the phase-2 members of an alive
+// tile are unchanged by the clip).  Work items are (chunk of BL_CHUNK
+// splats, block) in ticket order, chunk-major; a chunk's offset in its
+// block's list comes from a decoupled look-back over the block's chunks.
+// Blocks without pairs in the phase (zero capacity) are skipped.
+constexpr int BL_THREADS = 256;
+constexpr int BL_WARPS = BL_THREADS / 32;
+constexpr int BL_R = BL_CHUNK / BL_THREADS;
+static_assert(BL_R * BL_WARPS == 32, "one warp scans the chunk's (item, warp) counts");
+static_assert(BLK_W * BLK_H == 32, "32-bit tile masks");
 
-__global__ void __launch_bounds__(LS_THREADS) k_list_scan(const uint32_t *__restrict__ order,
-                                                          const uint64_t *__restrict__ rect,
-                                                          const uint32_t *__restrict__ tile_start,
-                                                          uint32_t *__restrict__ list,
-                                                          uint32_t n_list, FrameState *fs,
-                                                          int32_t tiles_x, int32_t tiles_y) {
-  __shared__ uint64_t s_rc[LS_CAP];
-  __shared__ uint32_t s_id[LS_CAP];
-  __shared__ uint32_t s_cnt[LS_R * LS_H];
-  if (!fs->scan_a) return;
+template <int PH>
+__global__ void __launch_bounds__(BL_THREADS) k_block_lists(const Work w, FrameState *fs,
+                                                            int32_t tiles_x, int32_t tiles_y) {
+  __shared__ uint32_t s_cnt[32];
+  __shared__ uint32_t s_tk, s_base;
+  if (!(PH == 1 ? fs->scan_a : fs->scan_b) || fs->stats.overflow) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int bxn = (tiles_x + LS_W - 1) / LS_W;
-  const uint32_t bx0 = (blockIdx.x % bxn) * LS_W, by0 = (blockIdx.x / bxn) * LS_H;
-  const uint32_t bx1 = min(bx0 + LS_W, (uint32_t)tiles_x) - 1,
-                 by1 = min(by0 + LS_H, (uint32_t)tiles_y) - 1;
-  if (by0 >= (uint32_t)tiles_y) return;
-  const uint32_t ty = by0 + warp;
-  const bool row = ty <= by1;
-  uint32_t cur[LS_W];
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t nbx = (tiles_x + BLK_W - 1) / BLK_W, nb = block_count(tiles_x, tiles_y);
+  const uint32_t n = PH == 1 ? fs->split_S : fs->n_owners_b;
+  const uint32_t nch = (n + BL_CHUNK - 1) / BL_CHUNK;
+  const uint64_t *__restrict__ rect = PH == 1 ? w.rect_sorted : w.rect;
+  const uint32_t *__restrict__ ids = PH == 1 ? w.val_depth[0] : w.val_depth[1];
+  const uint32_t *bl_start = w.bl_start + (PH == 1 ? 0 : nb + 1);
+  uint32_t *bl_len = w.bl_len + (PH == 1 ? 0 : nb);
+  uint64_t *blist = w.pairs[PH - 1];
+  const int tk = PH == 1 ? TK_BLA : TK_BLB;
+  for (;;) {
+    if (tid == 0) s_tk = atomicAdd(&fs->tickets[tk], 1u);
+    __syncthreads();
+    const uint32_t item = s_tk;
+    __syncthreads();  // every thread has the ticket before the next is drawn
+    const uint32_t c = item / nb, b = item % nb;
+    if (c >= nch || c >= (uint32_t)BL_CHMAX) break;
+    const uint32_t cap0 = bl_start[b], cap1 = bl_start[b + 1];
+    if (cap1 == cap0) continue;  // no pairs of this phase in the block: no members
+    const uint32_t bx0 = (b % nbx) * BLK_W, by0 = (b / nbx) * BLK_H;
+    const uint32_t bx1 = min(bx0 + BLK_W, (uint32_t)tiles_x) - 1,
+                   by1 = min(by0 + BLK_H, (uint32_t)tiles_y) - 1;
+    // phase 2 counts only the alive tiles: an owner joins a block's list when
+    // it covers one of the block's alive tiles (so a list never outgrows its
+    // capacity) and carries only those bits
+    uint32_t keep = 0xffffffffu;
+    if (PH == 2) {
+      const uint32_t bx = bx0 + (lane % BLK_W), by = by0 + (lane / BLK_W);
+      const uint32_t t = by * tiles_x + bx;
+      const bool a = bx <= bx1 && by <= by1 && ((w.alive[t >> 5] >> (t & 31)) & 1u);
+      keep = __ballot_sync(FULL_MASK, a);
+    }
+    uint32_t mask[BL_R];
 #pragma unroll
-  for (int i = 0; i < LS_W; ++i)
-    cur[i] = (row && bx0 + i <= bx1) ? tile_start[ty * tiles_x + bx0 + i] : 0u;
-  // the staged members [0, n) -> this warp's tile lists
-  auto drain = [&](uint32_t n) {
-    for (uint32_t q0 = 0; q0 < n; q0 += 32) {
-      const uint32_t q = q0 + lane;
-      const uint64_t rc = q < n ? s_rc[q] : 0ull;
+    for (int i = 0; i < BL_R; ++i) {
+      const uint32_t r = c * BL_CHUNK + i * BL_THREADS + tid;
+      const uint64_t rc = r < n ? rect[r] : 0xffffull;  // x0 = 0xffff: meets nothing
       const uint32_t x0 = rc & 0xffff, x1 = (rc >> 16) & 0xffff, y0 = (rc >> 32) & 0xffff,
                      y1 = rc >> 48;
-      const bool inrow = row && q < n && y0 <= ty && ty <= y1;
-      if (!__any_sync(FULL_MASK, inrow)) continue;
-      const uint32_t id = q < n ? s_id[q] : 0u;
-#pragma unroll
-      for (int i = 0; i < LS_W; ++i) {
-        const uint32_t tx = bx0 + i;
-        const bool h = inrow && x0 <= tx && tx <= x1 && tx <= bx1;
-        const uint32_t b = __ballot_sync(FULL_MASK, h);
-        if (h) {
-          const uint32_t pos = cur[i] + __popc(b & ((1u << lane) - 1u));
-          if (pos < n_list) list[pos] = id;
-          else raise_fault(fs, FAULT_LIST);
-        }
-        cur[i] += __popc(b);
+      uint32_t m = 0;
+      if (x0 <= bx1 && x1 >= bx0 && y0 <= by1 && y1 >= by0) {
+        const uint32_t cx0 = max(x0, bx0) - bx0, cx1 = min(x1, bx1) - bx0;
+        const uint32_t cy0 = max(y0, by0) - by0, cy1 = min(y1, by1) - by0;
+        const uint32_t row = (2u << cx1) - (1u << cx0);  // columns cx0..cx1 (cx1 <= 7)
+        const uint32_t rows = (uint32_t)((2ull << (BLK_W * cy1 + BLK_W - 1)) -
+                                         (1ull << (BLK_W * cy0)));  // bytes cy0..cy1
+        m = (row * 0x01010101u) & rows & keep;
       }
-    }
-  };
-  const uint32_t S = fs->split_S;
-  uint32_t n = 0;  // staged members (CTA-uniform)
-  for (uint32_t base = 0; base < S; base += LS_THREADS * LS_R) {
-    uint64_t rc[LS_R];
-    uint32_t hit = 0;
-#pragma unroll
-    for (int i = 0; i < LS_R; ++i) {
-      const uint32_t r = base + i * LS_THREADS + tid;
-      rc[i] = r < S ? rect[r] : 0ull;
-    }
-#pragma unroll
-    for (int i = 0; i < LS_R; ++i) {
-      const uint32_t r = base + i * LS_THREADS + tid;
-      const uint32_t x0 = rc[i] & 0xffff, x1 = (rc[i] >> 16) & 0xffff,
-                     y0 = (rc[i] >> 32) & 0xffff, y1 = rc[i] >> 48;
-      const bool h = r < S && x0 <= bx1 && x1 >= bx0 && y0 <= by1 && y1 >= by0;
-      const uint32_t b = __ballot_sync(FULL_MASK, h);
-      if (lane == 0) s_cnt[i * LS_H + warp] = __popc(b);
-      hit |= h ? (1u << i) : 0u;
+      mask[i] = m;
+      const uint32_t bal = __ballot_sync(FULL_MASK, m != 0u);
+      if (lane == 0) s_cnt[i * BL_WARPS + warp] = __popc(bal);
     }
     __syncthreads();
-    // exclusive offsets over (item, warp) -- the depth order within the round
+    // exclusive offsets over (item, warp): the depth order within the chunk
     const uint32_t v = s_cnt[lane];
     uint32_t inc = v;
 #pragma unroll
@@ -282,30 +314,29 @@ __global__ void __launch_bounds__(LS_THREADS) k_list_scan(const uint32_t *__rest
     }
     const uint32_t total = __shfl_sync(FULL_MASK, inc, 31);
     const uint32_t ex = inc - v;
-    if (n + total > (uint32_t)LS_CAP) {  // make room: drain what is staged
-      drain(n);
-      n = 0;
+    if (warp == 0) {
+      const uint32_t pre = lookback_warp(w.status + (size_t)b * BL_CHMAX, c, total,
+                                         fs->epoch + tk);
+      if (lane == 0) s_base = pre;
     }
-    __syncthreads();  // s_cnt read by all (and the staging drained) before reuse
+    __syncthreads();
+    const uint32_t base = cap0 + s_base;
 #pragma unroll
-    for (int i = 0; i < LS_R; ++i) {
-      const bool h = (hit >> i) & 1u;
-      const uint32_t b = __ballot_sync(FULL_MASK, h);
-      const uint32_t off = __shfl_sync(FULL_MASK, ex, i * LS_H + warp);
+    for (int i = 0; i < BL_R; ++i) {
+      const bool h = mask[i] != 0u;
+      const uint32_t bal = __ballot_sync(FULL_MASK, h);
+      const uint32_t off = __shfl_sync(FULL_MASK, ex, i * BL_WARPS + warp);
       if (h) {
-        const uint32_t at = n + off + __popc(b & ((1u << lane) - 1u));
-        s_rc[at] = rc[i];
-        s_id[at] = order[base + i * LS_THREADS + tid];
+        const uint32_t pos = base + off + __popc(bal & lt);
+        if (pos < cap1)
+          blist[pos] = ((uint64_t)mask[i] << 32) | ids[c * BL_CHUNK + i * BL_THREADS + tid];
+        else
+          raise_fault(fs, FAULT_LIST);
       }
     }
-    n += total;
-    __syncthreads();
+    if (tid == 0 && c == nch - 1) bl_len[b] = s_base + total;
+    __syncthreads();  // s_cnt / s_base reused by the next item
   }
-  drain(n);
-#pragma unroll
-  for (int i = 0; i < LS_W; ++i)
-    if (lane == 0 && row && bx0 + i <= bx1 && cur[i] != tile_start[ty * tiles_x + bx0 + i + 1])
-      raise_fault(fs, FAULT_LIST);
 }
 
 // Second phase of a two-phase frame (one block of 1024 threads): list
@@ -319,7 +350,8 @@ __global__ void __launch_bounds__(1024) k_setup_b(const uint32_t *__restrict__ a
                                                   const uint32_t *__restrict__ start_a,
                                                   int32_t tiles_x, int32_t tiles_y,
                                                   uint32_t *tile_start, uint32_t *tile_order,
-                                                  uint32_t *sat, FrameState *fs) {
+                                                  uint32_t *sat, FrameState *fs,
+                                                  uint32_t *bl_start) {
   extern __shared__ int32_t ss[];  // (tx+1)*(ty+1) summed-area table
   __shared__ uint32_t h0[256], h1[256];
   __shared__ uint32_t s_sum[1024];
@@ -370,11 +402,29 @@ __global__ void __launch_bounds__(1024) k_setup_b(const uint32_t *__restrict__ a
   }
   __syncthreads();
   for (int i = tid; i < nd; i += nt) sat[i] = (uint32_t)ss[i];
+#ifdef LODGE_COUNTERS
+  {  // counters[7]: alive tiles | blocks of 8 x 4 tiles holding one << 32
+    const int bxn = (tiles_x + 7) / 8, byn = (tiles_y + 3) / 4;
+    for (int b = tid; b < bxn * byn; b += nt) {
+      const int x0 = (b % bxn) * 8, y0 = (b / bxn) * 4;
+      const int x1 = min(x0 + 8, tiles_x), y1 = min(y0 + 4, tiles_y);
+      const int v = ss[y1 * stride + x1] - ss[y0 * stride + x1] - ss[y1 * stride + x0] +
+                    ss[y0 * stride + x0];
+      if (v) atomicAdd(&fs->counters[7], (1ull << 32) + (unsigned long long)v);
+    }
+  }
+#endif
   lists_from_counts(cnt, T, tile_start, tile_order, fs, s_sum, h0, h1, s_bk, &s_tot, &s_nz);
+  __syncthreads();
+  // phase-2 block lists follow the first phase's choice (k_dup_count<true>
+  // confirms it once the owners are counted)
+  if (fs->scan_a) block_offsets(cnt, tiles_x, tiles_y, bl_start, s_sum);
   if (tid == 0) {
     fs->n_alive = s_nz;
     fs->n_pairs = fs->stats.overflow ? 0u : s_tot;
     fs->stats.P_second = s_tot;
+    fs->scan_b = 0u;
+    fs->n_sort_b = fs->n_pairs;
   }
 }
 
@@ -528,6 +578,11 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
       if (SECOND) {
         fs->n_owners_b = nq;
         fs->stats.M_second = nq;
+        // block lists for the second phase too when its owners fit the chunk
+        // table (else its pairs are emitted and sorted)
+        const bool sb = fs->scan_a && nq <= (uint32_t)(BL_CHUNK * BL_CHMAX);
+        fs->scan_b = sb ? 1u : 0u;
+        fs->n_sort_b = sb ? 0u : fs->n_pairs;
       }
     }
     if (!SECOND && budget) {  // whole warp: the difference-array update is collective
@@ -595,9 +650,9 @@ __global__ void __launch_bounds__(DUP_THREADS) k_emit_b(const uint32_t *__restri
   __shared__ uint32_t s_cnt[EB_ITEMS][DUP_THREADS / 32];
   __shared__ uint32_t s_part, s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t n = fs->stats.overflow ? 0u : fs->n_owners_b;
+  const uint32_t n = (fs->stats.overflow || fs->scan_b) ? 0u : fs->n_owners_b;
   const uint32_t Pe = n ? w.splat_off[n] : 0u;  // enumerated pairs
-  if (Pe == 0) return;
+  if (Pe == 0) return;  // (block lists: no pairs)
   for (int i = tid; i < (n_tiles + 31) / 32; i += DUP_THREADS) s_alive[i] = w.alive[i];
   // persistent CTAs: chunks in ticket order (the compaction's look-back)
   for (;;) {
@@ -674,7 +729,7 @@ void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32
   k_tile_setup<<<1, 1024, sm, s>>>(w.tile_diff, two_phase ? w.tile_diff_a : nullptr, tiles_x,
                                    tiles_y, tile_count, two_phase ? w.count_all : nullptr,
                                    two_phase ? w.alive : nullptr, w.tile_start, w.tile_order, fs,
-                                   w.P_cap);
+                                   w.P_cap, w.bl_start);
 }
 
 static uint32_t chunk_cap(const Work &w) { return (uint32_t)(w.P_cap / EMIT_CHUNK + 4); }
@@ -718,13 +773,14 @@ void launch_duplicate(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_
   launch_dup_emit(w, fs, tiles_x, s, false);
 }
 
-void launch_list_scan(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
-                      cudaStream_t s) {
-  const unsigned grid = (unsigned)(((tiles_x + LS_W - 1) / LS_W) * ((tiles_y + LS_H - 1) / LS_H));
-  const uint32_t n_list = (uint32_t)std::min<int64_t>(w.P_cap, 0xffffffffll);
-  k_list_scan<<<grid, LS_THREADS, 0, s>>>(w.val_depth[0], w.rect_sorted, w.tile_start,
-                                          const_cast<uint32_t *>(w.list), n_list, fs, tiles_x,
-                                          tiles_y);
+void launch_block_lists(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
+                        int phase, cudaStream_t s) {
+  static PerDevice res;
+  if (!res()) res() = resident_ctas(k_block_lists<1>, BL_THREADS);
+  const int64_t items = (int64_t)block_count(tiles_x, tiles_y) * BL_CHMAX;
+  const unsigned grid = (unsigned)std::min<int64_t>(items, res());
+  if (phase == 1) k_block_lists<1><<<grid, BL_THREADS, 0, s>>>(w, fs, tiles_x, tiles_y);
+  else k_block_lists<2><<<grid, BL_THREADS, 0, s>>>(w, fs, tiles_x, tiles_y);
 }
 
 void launch_setup_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
@@ -736,7 +792,8 @@ void launch_setup_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tile
     attr() = (int64_t)sm;
   }
   k_setup_b<<<1, 1024, sm, s>>>(w.alive, w.count_all, w.tile_start, tiles_x, tiles_y,
-                                w.tile_start_b, w.tile_order_b, w.sat, fs);
+                                w.tile_start_b, w.tile_order_b, w.sat, fs,
+                                w.bl_start + block_count(tiles_x, tiles_y) + 1);
 }
 
 void launch_enum_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,

@@ -203,6 +203,9 @@ struct CompSmem {
   uint8_t wlist[CC<EXACT, PH>::NW * CB];
   uint64_t bar[2];
   uint32_t mt;  // end of the members the tile iterated (max over warps)
+  uint32_t bl_cnt[32];  // block-list refill: members per (round item, warp)
+  uint32_t bl_next;     // block-list entry after the batch's last member
+  uint32_t bl_on, bl_cur, bl_end, bl_bit;  // block-list walk (CTA-uniform, kept out of registers)
 };
 
 struct CompParams {
@@ -215,6 +218,10 @@ struct CompParams {
   float4 *state;              // (T, r, g, b) per pixel of those tiles
   uint32_t n_list, n_payload;  // capacities of the list and payload buffers (bounds checks)
   uint32_t n_maxw;             // entries of the caller's max-weight buffer (bounds check)
+  // block lists (phases 1 and 2 when fs->scan_a / scan_b): this phase's
+  // lists, their capacity offsets and lengths (k_block_lists)
+  const uint64_t *blist;
+  const uint32_t *bl_start, *bl_len;
 };
 
 // MODE < 0: need_image / record_max from cpar.flags at run time (EXACT);
@@ -295,10 +302,106 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
   // pixels were done (compositing work, stats.comp_members)
   uint32_t wend = s;
 
+  // Block lists (fs->scan_a / scan_b): the tile's members are the entries of
+  // its block's list with the tile's mask bit, in order; the CTA walks the
+  // list from bl_cur (CTA-uniform) as it stages batches.
+  if (tid == 0) {
+    S.bl_on = PH == 1 ? fs->scan_a : (PH == 2 ? fs->scan_b : 0u);
+    if (S.bl_on) {
+      const uint32_t nbx = (cpar.tiles_x + BLK_W - 1) / BLK_W;
+      const uint32_t bi = (ty / BLK_H) * nbx + tx / BLK_W;
+      const uint32_t c0 = cpar.bl_start[bi];
+      S.bl_cur = c0;
+      S.bl_end = c0 + min(cpar.bl_len[bi], cpar.bl_start[bi + 1] - c0);
+      S.bl_bit = 32u + (ty % BLK_H) * BLK_W + tx % BLK_W;
+    }
+  }
+  __syncthreads();
+  // stage the tile's next n members from the block list into buffer k:
+  // rounds of BR entries per thread, members ranked in list order by
+  // ballots and a scan of the (item, warp) counts
+  auto issue_block = [&](int n, int k) {
+    constexpr int BR = 4;
+    constexpr int NW = CC<EXACT, PH>::NW;
+    static_assert(BR * NW <= 32, "one warp scans the round's counts");
+    uint32_t bl_cur = S.bl_cur;
+    const uint32_t bl_end = S.bl_end, bl_bit = S.bl_bit;
+    int got = 0;
+    while (got < n) {
+      uint64_t v[BR];
+#pragma unroll
+      for (int i = 0; i < BR; ++i) {
+        const uint32_t at = bl_cur + (uint32_t)(i * CT + tid);
+        v[i] = at < bl_end ? cpar.blist[at] : 0ull;
+      }
+      uint32_t mem = 0;
+#pragma unroll
+      for (int i = 0; i < BR; ++i) {
+        const bool h = (v[i] >> bl_bit) & 1ull;
+        const uint32_t bal = __ballot_sync(FULL_MASK, h);
+        if (lane == 0) S.bl_cnt[i * NW + warp] = __popc(bal);
+        mem |= h ? (1u << i) : 0u;
+      }
+      __syncthreads();
+      const uint32_t c = lane < BR * NW ? S.bl_cnt[lane] : 0u;
+      uint32_t inc = c;
+#pragma unroll
+      for (int o = 1; o < BR * NW; o <<= 1) {
+        const uint32_t t2 = __shfl_up_sync(FULL_MASK, inc, o);
+        if (lane >= o) inc += t2;
+      }
+      const int tot = (int)__shfl_sync(FULL_MASK, inc, BR * NW - 1);
+      const uint32_t ex = inc - c;
+#pragma unroll
+      for (int i = 0; i < BR; ++i) {
+        const bool h = (mem >> i) & 1u;
+        const uint32_t bal = __ballot_sync(FULL_MASK, h);
+        const uint32_t off = __shfl_sync(FULL_MASK, ex, i * NW + warp);
+        if (h) {
+          const int rank = got + (int)(off + __popc(bal & lanemask_lt()));
+          if (rank < n) {
+            uint32_t m = (uint32_t)v[i];
+            if (m >= cpar.n_payload) {
+              raise_fault(fs, FAULT_MEMBER);
+              m = 0;
+            }
+            S.m[k][rank] = m;
+            bulk_g2s(&S.pl[k][rank], payload + m, 64, &S.bar[k]);
+            if (rank == n - 1) S.bl_next = bl_cur + (uint32_t)(i * CT + tid) + 1u;
+          }
+        }
+      }
+      if (got + tot >= n) {
+        __syncthreads();  // bl_next
+        bl_cur = S.bl_next;
+        got = n;
+      } else {
+        got += tot;
+        bl_cur += (uint32_t)(BR * CT);
+        if (bl_cur >= bl_end) {  // the list ran out before the tile's count: fill the
+          if (tid == 0) raise_fault(fs, FAULT_LIST);  // stage with record 0 (no hang)
+          for (int r = got + tid; r < n; r += CT) {
+            S.m[k][r] = 0;
+            bulk_g2s(&S.pl[k][r], payload, 64, &S.bar[k]);
+          }
+          got = n;
+        }
+      }
+      __syncthreads();  // bl_cnt reused
+    }
+    // every thread stores the (identical) new position, so its own next read
+    // sees it even when no barrier separates two refills
+    S.bl_cur = bl_cur;
+  };
+
   auto issue = [&](uint32_t bb, int k) {  // stage members [bb, bb+256) into buffer k
     const int n = (int)min((uint32_t)CB, e - bb);
     if (tid == 0) mbar_expect_tx(&S.bar[k], (uint32_t)n * REC);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (!EXACT && PH != 0 && S.bl_on) {
+      issue_block(n, k);
+      return;
+    }
 #pragma unroll
     for (int h = 0; h < CB / CT; ++h) {
       const int j = tid + h * CT;
@@ -860,6 +963,10 @@ static void launch_comp(const Work &w, FrameState *fs, int32_t W, int32_t H,
   cp.n_list = (uint32_t)std::min<int64_t>(2 * w.P_cap, 0xffffffffll);
   cp.n_payload = (uint32_t)w.M_cap;
   cp.n_maxw = n_maxw;
+  const uint32_t nb = (uint32_t)block_count(tiles_x, tiles_y);
+  cp.blist = PH ? w.pairs[PH - 1] : nullptr;
+  cp.bl_start = w.bl_start + (PH == 2 ? nb + 1 : 0);
+  cp.bl_len = w.bl_len + (PH == 2 ? nb : 0);
   k_composite<EXACT, MODE, PH><<<T, CC<EXACT, PH>::CT, sm, s>>>(
       w.list, PH == 2 ? w.tile_start_b : w.tile_start, PH == 2 ? w.tile_order_b : w.tile_order,
       w.payload, w.precise, fs, cp, out.image_dev, out.visible_dev, out.maxw_dev);

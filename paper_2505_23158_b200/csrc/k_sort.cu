@@ -420,8 +420,9 @@ __global__ void k_depth_rank(const uint32_t *val, uint32_t *vrank, uint32_t cap,
 }
 
 __global__ void k_list_verify(const uint32_t *list, const uint32_t *tile_start, uint32_t T,
-                              const uint32_t *vrank, uint32_t cap, FrameState *fs) {
+                              const uint32_t *vrank, uint32_t cap, FrameState *fs, int second) {
   if (fs->stats.overflow) return;  // a discarded attempt: no lists
+  if (second ? fs->scan_b : fs->scan_a) return;  // block lists: no per-tile lists
   const uint32_t n = fs->n_pairs;
   for (uint32_t t = blockIdx.x; t < T; t += gridDim.x) {
     const uint32_t s = tile_start[t], e = tile_start[t + 1];
@@ -442,7 +443,8 @@ void launch_list_verify(const Work &w, FrameState *fs, uint32_t T, bool second,
   if (!second)
     k_depth_rank<<<296, 256, 0, s>>>(w.val_depth[0], w.vrank, (uint32_t)w.M_cap, fs);
   k_list_verify<<<std::min<uint32_t>(T, 148 * 8), 128, 0, s>>>(
-      w.list, second ? w.tile_start_b : w.tile_start, T, w.vrank, (uint32_t)w.M_cap, fs);
+      w.list, second ? w.tile_start_b : w.tile_start, T, w.vrank, (uint32_t)w.M_cap, fs,
+      second ? 1 : 0);
 }
 #endif
 

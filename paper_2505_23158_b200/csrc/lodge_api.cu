@@ -126,7 +126,7 @@ static int ensure_tiles(lodge_ctx *c, int32_t W, int32_t H) {
   Work &w = c->w;
   if (need > c->tiles_cap || !w.tile_diff) {
     void *old[] = {w.tile_diff, w.tile_start, w.tile_order, w.tile_diff_a, w.count_all,
-                   w.tile_start_b, w.tile_order_b, w.alive, w.sat};
+                   w.tile_start_b, w.tile_order_b, w.alive, w.sat, w.bl_start, w.bl_len};
     for (void *p : old) cudaFree(p);
     c->tiles_cap = 0;
     CK(cudaMalloc(&w.tile_diff, 4 * need));
@@ -140,7 +140,14 @@ static int ensure_tiles(lodge_ctx *c, int32_t W, int32_t H) {
     CK(cudaMalloc(&w.tile_order_b, 4 * need));
     CK(cudaMalloc(&w.alive, 4 * (need / 32 + 1)));
     CK(cudaMalloc(&w.sat, 4 * need));
+    // block lists: capacity offsets and lengths per phase (blocks <= tiles)
+    CK(cudaMalloc(&w.bl_start, 4 * 2 * need));
+    CK(cudaMalloc(&w.bl_len, 4 * 2 * need));
     c->tiles_cap = need;
+  }
+  {  // block-list look-back: BL_CHMAX status words per block
+    const int rc = ensure_status(c, (int64_t)block_count((int32_t)tx, (int32_t)ty) * BL_CHMAX + 64);
+    if (rc) return rc;
   }
   const int64_t px = (int64_t)W * H;
   if (px > c->pixels_cap || !w.state) {
@@ -530,10 +537,11 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
     launch_dup_emit(w, c->fs, tiles_x, s, true); ++nl;
     DSYNC("launch_dup_emit");
     c->mark(6);
-    // sorted pairs (n_sort_a of them), or -- a first phase of few large
-    // splats -- the lists scanned from their rectangles; both leave w.list
+    // per-tile lists from the sorted pairs (n_sort_a of them), or -- a first
+    // phase of few large splats -- block lists (k_block_lists); each launch
+    // does nothing in the other mode
     launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s, TK_TILE0, &c->fs->n_sort_a);
-    launch_list_scan(w, c->fs, tiles_x, tiles_y, s); ++nl;
+    launch_block_lists(w, c->fs, tiles_x, tiles_y, 1, s); ++nl;
 #ifdef LODGE_VERIFY
     launch_list_verify(w, c->fs, (uint32_t)(tiles_x * tiles_y), false, s);
 #endif
@@ -553,7 +561,8 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
                    U_cap, s, slab_geom, slab_sh);
     DSYNC("launch_payload (second phase)");
     nl += 4;
-    launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s, TK_TILEB0);
+    launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s, TK_TILEB0, &c->fs->n_sort_b);
+    launch_block_lists(w, c->fs, tiles_x, tiles_y, 2, s); ++nl;
 #ifdef LODGE_VERIFY
     launch_list_verify(w, c->fs, (uint32_t)(tiles_x * tiles_y), true, s);
 #endif
