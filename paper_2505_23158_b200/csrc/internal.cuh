@@ -62,7 +62,14 @@ enum Ticket {
 // Block lists: blocks of BLK_W x BLK_H tiles (tile bit (y % BLK_H) * BLK_W +
 // x % BLK_W of an entry's mask), scanned in chunks of BL_CHUNK splats, at
 // most BL_CHMAX chunks (a phase uses block lists only below that many splats).
-constexpr int BLK_W = 8, BLK_H = 4;
+#ifndef LODGE_BLK_W
+#define LODGE_BLK_W 8
+#endif
+#ifndef LODGE_BLK_H
+#define LODGE_BLK_H 4
+#endif
+constexpr int BLK_W = LODGE_BLK_W, BLK_H = LODGE_BLK_H;
+static_assert(BLK_W * BLK_H <= 32 && BLK_W <= 16, "tile masks fit 32 bits");
 constexpr int BL_CHUNK = 1024;
 constexpr int BL_CHMAX = 64;
 __host__ __device__ inline int32_t block_count(int32_t tiles_x, int32_t tiles_y) {

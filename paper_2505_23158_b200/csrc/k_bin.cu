@@ -209,8 +209,12 @@ __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t *dif
   // a first phase of few splats with many tiles each (near, large splats)
   // keeps block lists (k_block_lists) instead of emitting and sorting P_A pairs
   const uint32_t S = fs->split_S;
+#ifdef LODGE_NO_BLOCK_LISTS
+  const bool scan = false;
+#else
   const bool scan = diff_a && n_pairs > 0 && S <= (uint32_t)(BL_CHUNK * BL_CHMAX) &&
                     (uint64_t)s_tot >= (uint64_t)LODGE_SCAN_MIN_TILES * S;
+#endif
   if (scan) block_offsets([&](int t) { return at(lc, t); }, tiles_x, tiles_y, bl_start, s_sum);
   if (tid == 0) {
     fs->stats.P = P;
@@ -242,7 +246,13 @@ constexpr int BL_THREADS = 256;
 constexpr int BL_WARPS = BL_THREADS / 32;
 constexpr int BL_R = BL_CHUNK / BL_THREADS;
 static_assert(BL_R * BL_WARPS == 32, "one warp scans the chunk's (item, warp) counts");
-static_assert(BLK_W * BLK_H == 32, "32-bit tile masks");
+// mask of column 0 in every row of a block (a row's column bits times this
+// replicate it down the rows)
+__host__ __device__ constexpr uint32_t blk_rep() {
+  uint32_t r = 0;
+  for (int y = 0; y < BLK_H; ++y) r |= 1u << (BLK_W * y);
+  return r;
+}
 
 template <int PH>
 __global__ void __launch_bounds__(BL_THREADS) k_block_lists(const Work w, FrameState *fs,
@@ -294,10 +304,10 @@ __global__ void __launch_bounds__(BL_THREADS) k_block_lists(const Work w, FrameS
       if (x0 <= bx1 && x1 >= bx0 && y0 <= by1 && y1 >= by0) {
         const uint32_t cx0 = max(x0, bx0) - bx0, cx1 = min(x1, bx1) - bx0;
         const uint32_t cy0 = max(y0, by0) - by0, cy1 = min(y1, by1) - by0;
-        const uint32_t row = (2u << cx1) - (1u << cx0);  // columns cx0..cx1 (cx1 <= 7)
+        const uint32_t row = (2u << cx1) - (1u << cx0);  // columns cx0..cx1
         const uint32_t rows = (uint32_t)((2ull << (BLK_W * cy1 + BLK_W - 1)) -
-                                         (1ull << (BLK_W * cy0)));  // bytes cy0..cy1
-        m = (row * 0x01010101u) & rows & keep;
+                                         (1ull << (BLK_W * cy0)));  // rows cy0..cy1
+        m = (row * blk_rep()) & rows & keep;
       }
       mask[i] = m;
       const uint32_t bal = __ballot_sync(FULL_MASK, m != 0u);

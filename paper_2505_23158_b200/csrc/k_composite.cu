@@ -192,6 +192,33 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
+// Member staging.  cp.async (LDGSTS) 16-byte copies, four per 64 B record,
+// issued by consecutive lanes, completion tracked per thread on the stage's
+// mbarrier (cp.async.mbarrier.arrive.noinc: the barrier counts one arrival
+// per thread).  A per-thread cp.async.bulk of each record needs uniform
+// operands, and ptxas issues it lane by lane in an elect loop (~8
+// instructions per lane and record: 0.5k per warp and batch, ~7% of the
+// compositor's instructions at config 3); LODGE_COMP_TMA keeps that form.
+__device__ __forceinline__ void cp16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_arrive(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar))
+               : "memory");
+}
+// the c-th 16-byte chunk of member m's staged record(s) into stage slot j
+template <bool EXACT, typename Sm>
+__device__ __forceinline__ void stage_chunk(Sm &S, int k, int j, int c, uint32_t m,
+                                            const Payload *payload, const Precise *precise) {
+  if (EXACT && c >= 4)
+    cp16(reinterpret_cast<char *>(&S.pr[k][j]) + 16 * (c - 4),
+         reinterpret_cast<const char *>(precise + m) + 16 * (c - 4));
+  else
+    cp16(reinterpret_cast<char *>(&S.pl[k][j]) + 16 * c,
+         reinterpret_cast<const char *>(payload + m) + 16 * c);
+}
+
 template <bool EXACT, int PH = 0>
 struct CompSmem {
   static constexpr int CB = CC<EXACT, PH>::CB;
@@ -203,9 +230,8 @@ struct CompSmem {
   uint8_t wlist[CC<EXACT, PH>::NW * CB];
   uint64_t bar[2];
   uint32_t mt;  // end of the members the tile iterated (max over warps)
-  uint32_t bl_cnt[32];  // block-list refill: members per (round item, warp)
-  uint32_t bl_next;     // block-list entry after the batch's last member
-  uint32_t bl_on, bl_cur, bl_end, bl_bit;  // block-list walk (CTA-uniform, kept out of registers)
+  uint32_t bl_mask[32];  // block-list refill: member ballots per (round item, warp), 2 rounds
+  uint32_t bl_on, bl_cur, bl_end, bl_bit, bl_par;  // block-list walk (CTA-uniform, not in registers)
 };
 
 struct CompParams {
@@ -292,8 +318,13 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
     if (px < cpar.W && py0 + 2 * p < cpar.H) alive |= 1u << p;
 
   if (tid == 0) {
+#ifdef LODGE_COMP_TMA
     mbar_init(&S.bar[0], 1);
     mbar_init(&S.bar[1], 1);
+#else
+    mbar_init(&S.bar[0], CT);  // one cp.async arrival per thread and stage
+    mbar_init(&S.bar[1], CT);
+#endif
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     S.mt = s;
   }
@@ -314,17 +345,21 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
       S.bl_cur = c0;
       S.bl_end = c0 + min(cpar.bl_len[bi], cpar.bl_start[bi + 1] - c0);
       S.bl_bit = 32u + (ty % BLK_H) * BLK_W + tx % BLK_W;
+      S.bl_par = 0u;
     }
   }
   __syncthreads();
   // stage the tile's next n members from the block list into buffer k:
-  // rounds of BR entries per thread, members ranked in list order by
-  // ballots and a scan of the (item, warp) counts
+  // rounds of BR entries per thread; each warp publishes its member ballot
+  // per round item (double-buffered by round parity, so one barrier per
+  // round), every thread ranks its members from the scanned ballot counts
+  // and finds the entry after the batch's last member itself
   auto issue_block = [&](int n, int k) {
     constexpr int BR = 4;
     constexpr int NW = CC<EXACT, PH>::NW;
-    static_assert(BR * NW <= 32, "one warp scans the round's counts");
-    uint32_t bl_cur = S.bl_cur;
+    constexpr int NQ = BR * NW;  // (item, warp) slots of a round, item-major
+    static_assert(NQ <= 16, "two rounds of slots in bl_mask");
+    uint32_t bl_cur = S.bl_cur, par = S.bl_par;
     const uint32_t bl_end = S.bl_end, bl_bit = S.bl_bit;
     int got = 0;
     while (got < n) {
@@ -339,18 +374,22 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
       for (int i = 0; i < BR; ++i) {
         const bool h = (v[i] >> bl_bit) & 1ull;
         const uint32_t bal = __ballot_sync(FULL_MASK, h);
-        if (lane == 0) S.bl_cnt[i * NW + warp] = __popc(bal);
+        if (lane == 0) S.bl_mask[par * 16 + i * NW + warp] = bal;
         mem |= h ? (1u << i) : 0u;
       }
       __syncthreads();
-      const uint32_t c = lane < BR * NW ? S.bl_cnt[lane] : 0u;
+#ifdef LODGE_COUNTERS
+      if (tid == 0) atomicAdd(&fs->counters[6], 1ull);
+#endif
+      const uint32_t mk = lane < NQ ? S.bl_mask[par * 16 + lane] : 0u;
+      const uint32_t c = __popc(mk);
       uint32_t inc = c;
 #pragma unroll
-      for (int o = 1; o < BR * NW; o <<= 1) {
+      for (int o = 1; o < NQ; o <<= 1) {
         const uint32_t t2 = __shfl_up_sync(FULL_MASK, inc, o);
         if (lane >= o) inc += t2;
       }
-      const int tot = (int)__shfl_sync(FULL_MASK, inc, BR * NW - 1);
+      const int tot = (int)__shfl_sync(FULL_MASK, inc, NQ - 1);
       const uint32_t ex = inc - c;
 #pragma unroll
       for (int i = 0; i < BR; ++i) {
@@ -366,14 +405,25 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
               m = 0;
             }
             S.m[k][rank] = m;
+#ifdef LODGE_COMP_TMA
             bulk_g2s(&S.pl[k][rank], payload + m, 64, &S.bar[k]);
-            if (rank == n - 1) S.bl_next = bl_cur + (uint32_t)(i * CT + tid) + 1u;
+#else
+#pragma unroll
+            for (int c = 0; c < 4; ++c) stage_chunk<EXACT>(S, k, rank, c, m, payload, precise);
+#endif
           }
         }
       }
       if (got + tot >= n) {
-        __syncthreads();  // bl_next
-        bl_cur = S.bl_next;
+        // the member of rank n - 1: slot q (item q / NW, warp q % NW), its
+        // (need - ex_q)-th set bit
+        const uint32_t need = (uint32_t)(n - 1 - got);
+        const uint32_t qm = __ballot_sync(FULL_MASK, lane < NQ && ex <= need && need < ex + c);
+        const int q = __ffs(qm) - 1;
+        const uint32_t mq = __shfl_sync(FULL_MASK, mk, q);
+        const uint32_t eq = __shfl_sync(FULL_MASK, ex, q);
+        const uint32_t bitpos = __fns(mq, 0, (int)(need - eq) + 1);
+        bl_cur += (uint32_t)((q / NW) * CT + (q % NW) * 32) + bitpos + 1u;
         got = n;
       } else {
         got += tot;
@@ -382,20 +432,26 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
           if (tid == 0) raise_fault(fs, FAULT_LIST);  // stage with record 0 (no hang)
           for (int r = got + tid; r < n; r += CT) {
             S.m[k][r] = 0;
+#ifdef LODGE_COMP_TMA
             bulk_g2s(&S.pl[k][r], payload, 64, &S.bar[k]);
+#else
+            for (int c = 0; c < 4; ++c) stage_chunk<EXACT>(S, k, r, c, 0u, payload, precise);
+#endif
           }
           got = n;
         }
       }
-      __syncthreads();  // bl_cnt reused
+      par ^= 1u;
     }
-    // every thread stores the (identical) new position, so its own next read
+    // every thread stores the (identical) walk state, so its own next read
     // sees it even when no barrier separates two refills
     S.bl_cur = bl_cur;
+    S.bl_par = par;
   };
 
-  auto issue = [&](uint32_t bb, int k) {  // stage members [bb, bb+256) into buffer k
+  auto issue = [&](uint32_t bb, int k) {  // stage members [bb, bb+CB) into buffer k
     const int n = (int)min((uint32_t)CB, e - bb);
+#ifdef LODGE_COMP_TMA
     if (tid == 0) mbar_expect_tx(&S.bar[k], (uint32_t)n * REC);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (!EXACT && PH != 0 && S.bl_on) {
@@ -416,6 +472,29 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
         if (EXACT) bulk_g2s(&S.pr[k][j], precise + m, 64, &S.bar[k]);
       }
     }
+#else
+    if (!EXACT && PH != 0 && S.bl_on) {
+      issue_block(n, k);
+    } else {
+      // chunk q: member q / CPM, 16-byte piece q % CPM (consecutive lanes
+      // copy one record's consecutive pieces)
+      constexpr int CPM = (int)(REC / 16);
+#pragma unroll
+      for (int h = 0; h < CB * CPM / CT; ++h) {
+        const int q = tid + h * CT, j = q / CPM, c = q % CPM;
+        if (j < n) {
+          uint32_t m = list[bb + j];
+          if (m >= cpar.n_payload) {
+            if (c == 0) raise_fault(fs, FAULT_MEMBER);
+            m = 0;
+          }
+          if (c == 0) S.m[k][j] = m;
+          stage_chunk<EXACT>(S, k, j, c, m, payload, precise);
+        }
+      }
+    }
+    cp_arrive(&S.bar[k]);  // completes when this thread's copies land
+#endif
   };
 
   PxF<PX> Tu, cru, cgu, cbu;                           // FAST (pixel pairs for FFMA2)
@@ -893,7 +972,7 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
   atomicAdd(&fs->counters[3], c_px);  // pixel evaluations inside the cut-off
   if (tid == 0) {
     atomicMax(&fs->counters[5], c_batch);
-    if (c_batch > 16) atomicAdd(&fs->counters[6], 1ull);
+    // counters[6]: block-list refill rounds (issue_block)
   }
 #endif
   {  // members iterated (SURVEY.md 8d m_t): the whole list while a pixel is
