@@ -861,7 +861,9 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
       // ak: every member of the group is flagged all-keep for this warp's
       // block: no guard band, no keep test beyond T >= t_min
       constexpr int G = LODGE_COMP_GROUP;
-      auto group = [&](const int (&js)[G], const bool AK) {
+      // returns false (nothing blended) when a pixel of the warp falls in a
+      // member's guard band: the caller then takes the members one by one
+      auto group = [&](const int (&js)[G], const bool AK) -> bool {
         static_assert(PX % 2 == 0, "pixel pairs");
         PxF<PX> q[G];
         float4 mm[G], cn[G];
@@ -869,11 +871,7 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
 #pragma unroll
         for (int u = 0; u < G; ++u)
           near |= quad2(PL[js[u]], q[u], mm[u], cn[u], !AK);
-        if (!AK && __any_sync(FULL_MASK, near)) {
-#pragma unroll
-          for (int u = 0; u < G; ++u) one(js[u]);
-          return;
-        }
+        if (!AK && __any_sync(FULL_MASK, near)) return false;
 #ifdef LODGE_COUNTERS
         c_iter += G;
 #endif
@@ -908,26 +906,30 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
 #pragma unroll
         for (int u = 0; u < G; ++u) c_hit += __any_sync(FULL_MASK, wm[u] > 0.f) ? 1 : 0;
 #endif
+        return true;
       };
+      // groups of G members; a member is taken alone (one, a single call
+      // site: the kernel's code stays small) at the list's tail and when its
+      // group meets the guard band -- the next group then starts after it
       int i = 0;
-      for (; i + G <= cnt; i += G) {
+      while (i < cnt) {
         if (!__any_sync(FULL_MASK, live_any())) break;
-        int js[G];
-        uint32_t allk = 0x80;
+        if (i + G <= cnt) {
+          int js[G];
+          uint32_t allk = 0x80;
 #pragma unroll
-        for (int u = 0; u < G; ++u) {
-          const uint32_t ent = lds_u8(wl_sa + (uint32_t)(i + u));
-          js[u] = (int)(ent & 0x7f);
-          allk &= ent;
+          for (int u = 0; u < G; ++u) {
+            const uint32_t ent = lds_u8(wl_sa + (uint32_t)(i + u));
+            js[u] = (int)(ent & 0x7f);
+            allk &= ent;
+          }
+          if (allk ? group(js, true) : group(js, false)) {
+            i += G;
+            continue;
+          }
         }
-        if (allk) group(js, true);
-        else group(js, false);
-      }
-      if (i + G > cnt) {  // the tail (the loop did not stop on dead pixels)
-        for (; i < cnt; ++i) {
-          if (!__any_sync(FULL_MASK, live_any())) break;
-          one(lds_u8(wl_sa + (uint32_t)i) & 0x7f);
-        }
+        one(lds_u8(wl_sa + (uint32_t)i) & 0x7f);
+        ++i;
       }
       done_i = i;
     }
