@@ -545,11 +545,14 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
 #endif
   uint32_t phase0 = 0u, phase1 = 0u;
 
-  if (s < e) issue(s, 0);
   int k = 0;
   for (uint32_t b = s; b < e; b += CB, k ^= 1) {
     const int n = (int)min((uint32_t)CB, e - b);
-    if (b + CB < e) issue(b + CB, k ^ 1);  // next batch in flight while this one composites
+    // the first pass stages batches 0 and 1, later ones the next batch (in
+    // flight while this one composites); one call site keeps the code small
+#pragma unroll 1
+    for (uint32_t bi = (b == s ? s : b + CB); bi <= b + CB && bi < e; bi += CB)
+      issue(bi, (int)(((bi - s) / CB) & 1u));
     if (EXACT && b > s && ((b - s) & 1023u) == 0) {
       // block boundary of the reference's 1024-member cumprod
 #pragma unroll
