@@ -149,6 +149,22 @@ __device__ __forceinline__ F2 f2_mul(F2 a, F2 b) {
 }
 __device__ __forceinline__ F2 f2b(float v) { return F2{v, v}; }
 
+// 1.0f when T >= t_min (and qs > hi), else 0.0f (PTX set: FSET.BF)
+__device__ __forceinline__ float keep_f(float T, float tmin) {
+  float d;
+  asm("set.ge.f32.f32 %0, %1, %2;" : "=f"(d) : "f"(T), "f"(tmin));
+  return d;
+}
+__device__ __forceinline__ float keep_f(float T, float tmin, float qs, float hi) {
+  float d;
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.ge.f32 p, %1, %2;\n\t"
+      "set.gt.and.f32.f32 %0, %3, %4, p;\n\t}"
+      : "=f"(d)
+      : "f"(T), "f"(tmin), "f"(qs), "f"(hi));
+  return d;
+}
+
 // Per-thread pixel values, addressable as scalars (s[p]) or pixel pairs
 // (v[h] = pixels 2h, 2h + 1).
 template <int PX>
@@ -501,12 +517,14 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
   double tr[EXACT ? PX : 1], cp[EXACT ? PX : 1];      // EXACT transmittance
   double ir[EXACT ? PX : 1], ig[EXACT ? PX : 1], ib[EXACT ? PX : 1];
   double br[EXACT ? PX : 1], bg[EXACT ? PX : 1], bb[EXACT ? PX : 1];
-  int32_t vis[PX];
+  int32_t vis[PX];   // EXACT visible counts
+  PxF<PX> vf;         // FAST visible counts, as floats (FADD2 with the 0/1 keep factors)
 #pragma unroll
   for (int p = 0; p < PX; ++p) {
     Tu.s[p] = 1.f;
     cru.s[p] = cgu.s[p] = cbu.s[p] = 0.f;
     vis[p] = 0;
+    vf.s[p] = 0.f;
   }
   if (EXACT) {
 #pragma unroll
@@ -515,12 +533,13 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
       ir[p] = ig[p] = ib[p] = br[p] = bg[p] = bb[p] = 0.0;
     }
   }
-  // FAST tracks liveness in T itself (T >= t_min); out-of-image pixels never live
+  // FAST tracks liveness in T itself (T >= t_min); out-of-image pixels hold
+  // T = 0: never live, and their blend factors T * a stay 0
   if (!EXACT) {
 #pragma unroll
     for (int p = 0; p < PX; ++p) {
       if (!((alive >> p) & 1u)) {
-        Tu.s[p] = -INFINITY;
+        Tu.s[p] = 0.f;
       } else if (PH == 2) {  // resume the first phase's state
         const size_t pix = (size_t)(py0 + 2 * p) * cpar.W + px;
         const float4 st = cpar.state[pix];
@@ -528,7 +547,7 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
         cru.s[p] = st.y;
         cgu.s[p] = st.z;
         cbu.s[p] = st.w;
-        vis[p] = visible[pix];
+        vf.s[p] = (float)visible[pix];  // < 2^24: exact
       }
     }
   }
@@ -754,8 +773,8 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
               "setp.ge.f32 k, %2, %3;\n\t"
               "mul.rn.f32 %0, %2, %4;\n\t"
               "selp.f32 %0, %0, 0f00000000, k;\n\t"
-              "@k add.s32 %1, %1, 1;\n\t}"
-              : "=f"(w), "+r"(vis[p])
+              "@k add.rn.f32 %1, %1, 0f3F800000;\n\t}"
+              : "=f"(w), "+f"(vf.s[p])
               : "f"(Tu.s[p]), "f"(cpar.tmin_f), "f"(a));
         } else {
           asm("{\n\t.reg .pred k;\n\t"
@@ -763,8 +782,8 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
               "setp.gt.and.f32 k, %3, %5, k;\n\t"
               "mul.rn.f32 %0, %2, %6;\n\t"
               "selp.f32 %0, %0, 0f00000000, k;\n\t"
-              "@k add.s32 %1, %1, 1;\n\t}"
-              : "=f"(w), "+r"(vis[p])
+              "@k add.rn.f32 %1, %1, 0f3F800000;\n\t}"
+              : "=f"(w), "+f"(vf.s[p])
               : "f"(Tu.s[p]), "f"(qs), "f"(cpar.tmin_f), "f"(hi), "f"(a));
         }
         if (need_image) {
@@ -779,17 +798,23 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
 #endif
       };
       // the blend step for pixels 2h and 2h + 1 (the same operations as
-      // step, paired: FMUL2 / FFMA2 / FADD2 with the keep selection per lane)
+      // step, paired): the keep decisions as 0/1 factors (PTX set.f32:
+      // FSET, one ALU op per pixel), w = (T * a) * k -- bitwise the selected
+      // T * a or +0, T * a being finite and >= 0 -- and the visible counts
+      // += k, all as FMUL2 / FADD2 on the FMA pipe
       auto step2 = [&](int h, F2 qs, float hi, F2 a, const float4 &c, float &wmax,
                        const bool all_keep) {
         const int p0 = 2 * h, p1 = 2 * h + 1;
-        const bool k0 = Tu.s[p0] >= cpar.tmin_f && (all_keep || qs.x > hi);
-        const bool k1 = Tu.s[p1] >= cpar.tmin_f && (all_keep || qs.y > hi);
-        F2 w = f2_mul(Tu.v[h], a);
-        w.x = k0 ? w.x : 0.f;
-        w.y = k1 ? w.y : 0.f;
-        vis[p0] += k0 ? 1 : 0;
-        vis[p1] += k1 ? 1 : 0;
+        F2 kf;
+        if (all_keep) {
+          kf.x = keep_f(Tu.s[p0], cpar.tmin_f);
+          kf.y = keep_f(Tu.s[p1], cpar.tmin_f);
+        } else {
+          kf.x = keep_f(Tu.s[p0], cpar.tmin_f, qs.x, hi);
+          kf.y = keep_f(Tu.s[p1], cpar.tmin_f, qs.y, hi);
+        }
+        const F2 w = f2_mul(f2_mul(Tu.v[h], a), kf);
+        vf.v[h] = f2_add(vf.v[h], kf);
         if (need_image) {
           cru.v[h] = f2_fma(w, f2b(c.x), cru.v[h]);
           cgu.v[h] = f2_fma(w, f2b(c.y), cgu.v[h]);
@@ -846,7 +871,7 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
               cbu.s[p] = fmaf(w, c.z, cbu.s[p]);
             }
             Tu.s[p] -= w;
-            if (kp[p]) ++vis[p];
+            if (kp[p]) vf.s[p] += 1.f;
             wmax = fmaxf(wmax, w);
 #ifdef LODGE_COUNTERS
             c_px += kp[p] ? 1 : 0;
@@ -997,7 +1022,7 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
     const int py = py0 + 2 * p;
     if (!(px < cpar.W && py < cpar.H)) continue;
     const size_t pix = (size_t)py * cpar.W + px;
-    if (visible) visible[pix] = vis[p];
+    if (visible) visible[pix] = EXACT ? vis[p] : (int32_t)vf.s[p];
     if (PH == 1 && resume) {
       cpar.state[pix] = make_float4(Tu.s[p], cru.s[p], cgu.s[p], cbu.s[p]);
       continue;
