@@ -69,7 +69,7 @@ def parse():
                     help="full residency layout: flat level arrays, or chunk slabs (every "
                          "chunk's records contiguous in set order; paper_2505_23158_b200."
                          "device.SlabStore)")
-    ap.add_argument("--phase-budget", type=int, default=1280,
+    ap.add_argument("--phase-budget", type=int, default=2048,
                     help="FAST frames: first-phase pairs per tile of the two depth phases "
                          "(lodge_set_phase_budget); 0 = one pass over the full lists")
     ap.add_argument("--exact-steps", type=int, default=2,

@@ -57,7 +57,7 @@ class Renderer:
 
     def __init__(self, levels: Sequence, plan, device=None, storage: str = "fp32",
                  precision: str = "fast", raster_cfg: RasterConfig = RasterConfig(),
-                 n_streams: int = 1, full_lists: bool = False, phase_budget: int = 1280):
+                 n_streams: int = 1, full_lists: bool = False, phase_budget: int = 2048):
         self.ctx = context(device)
         self.device = self.ctx.device
         if n_streams < 1:
