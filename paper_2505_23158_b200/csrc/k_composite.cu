@@ -242,7 +242,7 @@ struct CompSmem {
   Precise pr[EXACT ? 2 : 1][EXACT ? CB : 1];  // EXACT: fp64 records
   uint32_t m[2][CB];                           // member splat ids (guard re-check)
   unsigned long long maxw[EXACT ? CB : 1];
-  uint32_t maxw32[CB];
+  uint32_t maxw32[CC<EXACT, PH>::NW][CB];  // FAST: per warp (each member once per warp and batch)
   uint8_t wlist[CC<EXACT, PH>::NW * CB];
   uint64_t bar[2];
   uint32_t mt;  // end of the members the tile iterated (max over warps)
@@ -608,7 +608,8 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
             half = INFINITY;
           }
           reinterpret_cast<float4 *>(&pj.mx)[0] = make_float4(mxl, myl, mid, half);
-          S.maxw32[j] = 0u;
+#pragma unroll
+          for (int w2 = 0; w2 < CC<EXACT, PH>::NW; ++w2) S.maxw32[w2][j] = 0u;
         } else {
           S.maxw[j] = 0ull;
         }
@@ -746,15 +747,17 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
         return need_image ? *reinterpret_cast<const float4 *>(&pj.r)
                           : make_float4(0.f, 0.f, 0.f, 0.f);
       };
-      // lane 0 maxes a member's warp-wide weight into its staged slot: one
-      // predicated shared reduction, no branch around it
-      const uint32_t maxw_sa = smem_addr(&S.maxw32[0]);
+      // lane 0 stores a member's warp-wide weight into the warp's own slot
+      // (a member comes once per warp and batch: a plain predicated store;
+      // ptxas branches around predicated shared atomics), the warps' slots
+      // are maxed when the batch is flushed
+      const uint32_t maxw_sa = smem_addr(&S.maxw32[warp][0]);
       auto record = [&](int j, unsigned wb) {
         asm volatile("{\n\t.reg .pred p;\n\t"
-                     "setp.ne.u32 p, %1, 0;\n\t"
-                     "setp.eq.and.u32 p, %2, 0, p;\n\t"
-                     "@p red.shared.max.u32 [%0], %1;\n\t}"
-                     :: "r"(maxw_sa + 4u * (uint32_t)j), "r"(wb), "r"(lane));
+                     "setp.eq.u32 p, %2, 0;\n\t"
+                     "@p st.shared.u32 [%0], %1;\n\t}"
+                     :: "r"(maxw_sa + 4u * (uint32_t)j), "r"(wb), "r"(lane)
+                     : "memory");
       };
       auto finish = [&](int j, float wmax) {
 #ifdef LODGE_COUNTERS
@@ -976,8 +979,11 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
           }
           if (EXACT) {
             if (S.maxw[j]) atomicMax(reinterpret_cast<unsigned long long *>(maxw) + src, S.maxw[j]);
-          } else if (S.maxw32[j]) {
-            atomicMax(reinterpret_cast<unsigned int *>(maxw) + src, S.maxw32[j]);
+          } else {
+            uint32_t mw = S.maxw32[0][j];
+#pragma unroll
+            for (int w2 = 1; w2 < CC<EXACT, PH>::NW; ++w2) mw = max(mw, S.maxw32[w2][j]);
+            if (mw) atomicMax(reinterpret_cast<unsigned int *>(maxw) + src, mw);
           }
         }
       }
