@@ -371,10 +371,11 @@ int launch_project_compat(const lodge_level &level, const int64_t *idx, int64_t 
 void launch_import_batch(const lodge_batch &b, int64_t M, const Work &w, FrameState *fs,
                          const lodge_camera *cam_dev, const lodge_raster_params &rp,
                          int32_t exact, cudaStream_t s);
-// Depth sort of the frame's inputs.  compacted: the projection left the M
-// survivors as (32-bit key, input index) in depth_keys_compact(w) and
-// val_depth[0] (any order); otherwise key_depth[0] holds fs->n_sort u64 keys
-// by position (~0: culled, dropped by the first pass), values the positions.
+// Depth sort of the frame's inputs into val_depth[0] (input indices in depth
+// order).  compacted: the projection left the M survivors as (32-bit key,
+// input index) in depth_keys_compact(w) and val_depth[1] (any order);
+// otherwise key_depth[0] holds fs->n_sort u64 keys by position (~0: culled,
+// dropped by the first pass) and val_depth[1] the positions.
 void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
                        cudaStream_t s, bool compacted = false);
 void launch_depth_sort64(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,

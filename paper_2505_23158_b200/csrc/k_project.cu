@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLeve
     for (uint32_t i = lane; i < wc; i += 32) {
       if (b0 + i < (uint32_t)w.M_cap) {
         ckey[b0 + i] = s_ck[wid][i];
-        w.val_depth[0][b0 + i] = s_cg[wid][i];
+        w.val_depth[1][b0 + i] = s_cg[wid][i];
       } else {
         raise_fault(fs, FAULT_SCATTER);
       }
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLeve
     const bool keep = valid && p.ok;
 #ifdef LODGE_DEPTH64  // the 64-bit sort reads every input's key by position
     if (valid) {
-      w.val_depth[0][g] = g;
+      w.val_depth[1][g] = g;
       if (!keep) w.key_depth[0][g] = ~0ull;
     }
     if (keep) atomicAdd(&fs->stats.M, 1u);
@@ -810,7 +810,7 @@ __global__ void __launch_bounds__(256) k_import_batch(lodge_batch b, int64_t M, 
   // source-index order via the values; the batch's src order is ascending
   // for project_scene outputs, otherwise the host pre-sorts (see raster.py).
   w.key_depth[0][m] = (uint64_t)__double_as_longlong(b.depth_dev[m]);
-  w.val_depth[0][m] = (uint32_t)m;
+  w.val_depth[1][m] = (uint32_t)m;  // the depth sort's input values
   if (m == 0) {
     fs->stats.M = (uint32_t)M;
     fs->n_sort = (uint32_t)M;

@@ -199,82 +199,39 @@ __global__ void __launch_bounds__(256) k_depth_hist32(const uint64_t *__restrict
 }
 
 // Tie repair after the 32-bit passes: every run of equal 32-bit keys is in
-// input order (the passes are stable); re-order it by (fp64 key, index).
-// Runs of up to TIE_SHORT members are sorted by the thread that owns the run
-// start; longer ones (only adversarial inputs: > 32 depths within one fp32
-// ulp) by the whole CTA through `scratch`, by rank counting.
-constexpr int TIE_SHORT = 32;
-constexpr int TIE_SEG = 1024;  // run starts examined per CTA step
+// input order (the passes are stable) and must be ordered by (fp64 key,
+// index).  One thread per element: an element without an equal neighbour
+// is copied; an element of a run finds the run's bounds and its rank in it
+// by (full key, index) and is written at run start + rank.  All elements
+// are independent (no thread walks a run alone), so the kernel's latency is
+// a few dependent loads; a run of n costs O(n^2) loads in all, which only
+// adversarial inputs make large (> 32 depths inside one fp32 ulp).
+// vin -> vout, both M long.
 __global__ void __launch_bounds__(256) k_depth_ties(const uint32_t *__restrict__ k32,
-                                                    uint32_t *val,
+                                                    const uint32_t *__restrict__ vin,
                                                     const uint64_t *__restrict__ full,
-                                                    uint32_t *scratch, FrameState *fs) {
-  __shared__ uint32_t s_long[TIE_SEG / (TIE_SHORT + 1) + 1];
-  __shared__ uint32_t s_nlong, s_end;
+                                                    uint32_t *__restrict__ vout,
+                                                    FrameState *fs) {
   const uint32_t M = fs->stats.M;
-  const int tid = threadIdx.x;
-  for (uint32_t seg = blockIdx.x * TIE_SEG; seg < M; seg += gridDim.x * TIE_SEG) {
-    if (tid == 0) s_nlong = 0;
-    __syncthreads();
-    const uint32_t segend = min(seg + (uint32_t)TIE_SEG, M);
-    for (uint32_t i = seg + tid; i < segend; i += blockDim.x) {
-      const uint32_t k = k32[i];
-      if (i + 1 >= M || k32[i + 1] != k) continue;  // no tie follows
-      if (i > 0 && k32[i - 1] == k) continue;       // not a run start
-      uint32_t e = i + 2;
-      while (e < M && e - i <= (uint32_t)TIE_SHORT && k32[e] == k) ++e;
-      if (e - i > (uint32_t)TIE_SHORT) {
-        s_long[atomicAdd(&s_nlong, 1u)] = i;
-        continue;
-      }
-      const uint32_t n = e - i;
-      uint32_t g[TIE_SHORT];
-      uint64_t f[TIE_SHORT];
-      for (uint32_t j = 0; j < n; ++j) {  // insertion sort by (full key, index)
-        const uint32_t gj = val[i + j];
-        const uint64_t fj = full[gj];
-        uint32_t q = j;
-        while (q > 0 && (f[q - 1] > fj || (f[q - 1] == fj && g[q - 1] > gj))) {
-          f[q] = f[q - 1];
-          g[q] = g[q - 1];
-          --q;
-        }
-        f[q] = fj;
-        g[q] = gj;
-      }
-      for (uint32_t j = 0; j < n; ++j) val[i + j] = g[j];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < M; i += gridDim.x * blockDim.x) {
+    const uint32_t k = k32[i];
+    const uint32_t gi = vin[i];
+    const bool l = i > 0 && k32[i - 1] == k, r = i + 1 < M && k32[i + 1] == k;
+    if (!l && !r) {
+      vout[i] = gi;
+      continue;
     }
-    __syncthreads();
-    const uint32_t nlong = s_nlong;
-    for (uint32_t r = 0; r < nlong; ++r) {
-      const uint32_t i0 = s_long[r];
-      const uint32_t k = k32[i0];
-      if (tid == 0) s_end = M;
-      __syncthreads();
-      for (uint32_t b = i0 + TIE_SHORT; b < M; b += blockDim.x) {  // run end
-        const uint32_t idx = b + tid;
-        if (idx < M && k32[idx] != k) atomicMin(&s_end, idx);
-        if (__syncthreads_or(s_end < M)) break;
-      }
-      const uint32_t n = s_end - i0;
-      for (uint32_t j = tid; j < n; j += blockDim.x) {
-        const uint32_t gj = val[i0 + j];
-        const uint64_t fj = full[gj];
-        uint32_t rank = 0;
-        for (uint32_t q = 0; q < n; ++q) {
-          const uint32_t gq = val[i0 + q];
-          const uint64_t fq = full[gq];
-          rank += (fq < fj || (fq == fj && gq < gj)) ? 1u : 0u;
-        }
-        scratch[i0 + rank] = gj;
-      }
-      __syncthreads();
-      for (uint32_t j = tid; j < n; j += blockDim.x) val[i0 + j] = scratch[i0 + j];
-      __syncthreads();
+    uint32_t s = i, e = i + 1;
+    while (s > 0 && k32[s - 1] == k) --s;
+    while (e < M && k32[e] == k) ++e;
+    const uint64_t fi = full[gi];
+    uint32_t rank = 0;
+    for (uint32_t j = s; j < e; ++j) {
+      const uint32_t gj = vin[j];
+      const uint64_t fj = full[gj];
+      rank += (fj < fi || (fj == fi && gj < gi)) ? 1u : 0u;
     }
-    // every thread has read s_nlong before the next segment resets it (a
-    // thread reading the reset value would skip the barriers above)
-    __syncthreads();
+    vout[s + rank] = gi;
   }
 }
 
@@ -455,7 +412,9 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
                        cudaStream_t s, bool compacted) {
   if (M_cap <= 0) return;
 #ifdef LODGE_DEPTH64
-  // opt-in: the eight 64-bit passes (0.17 vs 0.12 ms per config-3 frame)
+  // opt-in: the eight 64-bit passes (0.17 vs 0.12 ms per config-3 frame),
+  // which take their input values in val_depth[0]
+  cudaMemcpyAsync(w.val_depth[0], w.val_depth[1], 4 * (size_t)M_cap, cudaMemcpyDeviceToDevice, s);
   launch_depth_sort64(w, fs, M_cap, launches, s);
   return;
 #endif
@@ -484,32 +443,32 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
                                                     LODGE_PERSIST ? resident : 0x7fffffff);
   // keys 0: u64 (or the compacted k32[1]) -> k32[0], 1: k32[0] -> k32[1],
   // 2: k32[1] -> k32[0], 3: k32[0] -> k32[1]
+  // values (input in val_depth[1]): [1] -> [0] -> [1] -> [0] -> [1], then
+  // the tie repair [1] -> [0]
   if (compacted)
-    k_depth_pass<false><<<grid, OS_THREADS, sm, s>>>(nullptr, k32[1], k32[0], w.val_depth[0],
-                                                     w.val_depth[1], &fs->stats.M, 0,
+    k_depth_pass<false><<<grid, OS_THREADS, sm, s>>>(nullptr, k32[1], k32[0], w.val_depth[1],
+                                                     w.val_depth[0], &fs->stats.M, 0,
                                                      fs->off_depth[0], w.status, fs, TK_DEPTH0);
   else
     k_depth_pass<true><<<grid, OS_THREADS, sm, s>>>(w.key_depth[0], nullptr, k32[0],
-                                                    w.val_depth[0], w.val_depth[1], &fs->n_sort,
+                                                    w.val_depth[1], w.val_depth[0], &fs->n_sort,
                                                     0, fs->off_depth[0], w.status, fs, TK_DEPTH0);
 #ifdef LODGE_VERIFY
-  k_pass_verify<<<296, 256, 0, s>>>(k32[0], w.val_depth[1], w.key_depth[0], &fs->stats.M, 0, 0,
+  k_pass_verify<<<296, 256, 0, s>>>(k32[0], w.val_depth[0], w.key_depth[0], &fs->stats.M, 0, 0,
                                     fs);
 #endif
   for (int p = 1; p < 4; ++p) {
-    const int a = p & 1;  // values: [1] -> [0] -> [1] -> [0]
+    const int a = p & 1;  // keys: k32[a ^ 1] -> k32[a]; values: [a ^ 1] -> [a]
     k_depth_pass<false><<<grid, OS_THREADS, sm, s>>>(
-        nullptr, k32[a ^ 1], k32[a], w.val_depth[a], w.val_depth[a ^ 1], &fs->stats.M, 8 * p,
+        nullptr, k32[a ^ 1], k32[a], w.val_depth[a ^ 1], w.val_depth[a], &fs->stats.M, 8 * p,
         fs->off_depth[p], w.status, fs, TK_DEPTH0 + p);
 #ifdef LODGE_VERIFY
-    k_pass_verify<<<296, 256, 0, s>>>(k32[a], w.val_depth[a ^ 1], w.key_depth[0], &fs->stats.M,
+    k_pass_verify<<<296, 256, 0, s>>>(k32[a], w.val_depth[a], w.key_depth[0], &fs->stats.M,
                                       8 * p, p, fs);
 #endif
   }
-  const unsigned tgrid = (unsigned)std::min<int64_t>((M_cap + TIE_SEG - 1) / TIE_SEG, 148 * 16);
-#ifndef LODGE_NO_TIES
-  k_depth_ties<<<tgrid, 256, 0, s>>>(k32[1], w.val_depth[0], w.key_depth[0], w.val_depth[1], fs);
-#endif
+  const unsigned tgrid = (unsigned)std::min<int64_t>((M_cap + 255) / 256, 148 * 8);
+  k_depth_ties<<<tgrid, 256, 0, s>>>(k32[1], w.val_depth[1], w.key_depth[0], w.val_depth[0], fs);
 #ifdef LODGE_VERIFY
   k_depth_verify<<<296, 256, 0, s>>>(k32[1], w.val_depth[0], w.key_depth[0], fs);
 #endif
@@ -553,7 +512,7 @@ __global__ void k_debug_sort_out(const uint64_t *k0, const uint32_t *v0, FrameSt
 
 void launch_debug_depth_sort(const Work &w, FrameState *fs, const uint64_t *keys, uint32_t n,
                              uint64_t *ko, uint32_t *vo, uint32_t *m_out, cudaStream_t s) {
-  k_debug_sort_in<<<296, 256, 0, s>>>(keys, n, w.key_depth[0], w.val_depth[0], fs);
+  k_debug_sort_in<<<296, 256, 0, s>>>(keys, n, w.key_depth[0], w.val_depth[1], fs);
   int32_t nl = 0;
   launch_depth_sort(w, fs, n, &nl, s);
   k_debug_sort_out<<<296, 256, 0, s>>>(w.key_depth[0], w.val_depth[0], fs, ko, vo, m_out);
