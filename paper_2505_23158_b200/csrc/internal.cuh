@@ -283,15 +283,31 @@ __device__ __forceinline__ void warp_add_shared(int32_t *base, int32_t idx, int3
 }
 
 // The same update into a CTA-private difference array in shared memory.
+// Corners in the last column or row (x1 + 1 == tiles_x, y1 + 1 == tiles_y)
+// only feed cells beyond the tile grid, which the integration never reads:
+// they are skipped (the right and bottom border clips are the frequent
+// shared corners).  Per-lane shared atomics: the hardware resolves the
+// lanes that meet on a corner cheaper than a __match_any_sync aggregation
+// (projection 0.123 -> 0.117 ms at config 3); LODGE_DIFF_MATCH keeps that.
 __device__ __forceinline__ void add_tile_diff_shared(int32_t *diff, uint64_t rc, int32_t tiles_x,
-                                                     bool valid) {
+                                                     int32_t tiles_y, bool valid) {
   const int32_t x0 = (int32_t)(rc & 0xffff), x1 = (int32_t)((rc >> 16) & 0xffff);
   const int32_t y0 = (int32_t)((rc >> 32) & 0xffff), y1 = (int32_t)(rc >> 48);
   const int32_t stride = tiles_x + 1;
+  const bool xr = x1 + 1 < tiles_x, yb = y1 + 1 < tiles_y;
+#ifndef LODGE_DIFF_MATCH
+  if (valid) {
+    atomicAdd(diff + y0 * stride + x0, 1);
+    if (xr) atomicAdd(diff + y0 * stride + x1 + 1, -1);
+    if (yb) atomicAdd(diff + (y1 + 1) * stride + x0, -1);
+    if (xr && yb) atomicAdd(diff + (y1 + 1) * stride + x1 + 1, 1);
+  }
+#else
   warp_add_shared(diff, valid ? y0 * stride + x0 : -1, 1);
-  warp_add_shared(diff, valid ? y0 * stride + x1 + 1 : -1, -1);
-  warp_add_shared(diff, valid ? (y1 + 1) * stride + x0 : -1, -1);
-  warp_add_shared(diff, valid ? (y1 + 1) * stride + x1 + 1 : -1, 1);
+  warp_add_shared(diff, valid && xr ? y0 * stride + x1 + 1 : -1, -1);
+  warp_add_shared(diff, valid && yb ? (y1 + 1) * stride + x0 : -1, -1);
+  warp_add_shared(diff, valid && xr && yb ? (y1 + 1) * stride + x1 + 1 : -1, 1);
+#endif
 }
 
 // 2-D difference-array update for a tile rectangle (whole warp; valid flag).

@@ -488,15 +488,14 @@ __device__ __forceinline__ void stage_frame_ctx(FrameCtx &F, const ProjLevels &l
 // and record index for the colour.  Shared by the projection and the
 // payload kernel, so both evaluate the identical fp64 projection (DISPATCH:
 // drop the exact-zero camera terms, project_any; the fields are the same).
+// (gidx, tag: the slot's union entry.)
 template <typename GT, typename ST, bool DISPATCH = true>
-__device__ __forceinline__ Proj slot_project(const ProjLevels &lv, const Work &w,
-                                             const FrameCtx &F, const lodge_raster_params &rp,
-                                             int l, uint32_t slot, double v[12],
-                                             const ST *&sp, uint32_t &gidx) {
+__device__ __forceinline__ Proj slot_project_at(const ProjLevels &lv, const FrameCtx &F,
+                                                const lodge_raster_params &rp, int l,
+                                                uint32_t gidx, uint8_t tag, double v[12],
+                                                const ST *&sp) {
   const GT *gp = reinterpret_cast<const GT *>(lv.geom[l]);
   sp = reinterpret_cast<const ST *>(lv.sh[l]);
-  gidx = w.union_idx[slot];
-  const uint8_t tag = w.union_tag[slot];
   const double mod = (tag == 3) ? 1.0 : (tag == 1 ? F.t : 1.0 - F.t);
   if (lv.slab_geom) {  // tag 3 / 1: the primary chunk's slab, 2: the other's
     const int32_t e = ((tag == 2) ? F.o : F.f) * lv.L + l;
@@ -507,6 +506,14 @@ __device__ __forceinline__ Proj slot_project(const ProjLevels &lv, const Work &w
   if (lv.qnorm[l]) normalize_rot(v);
   return DISPATCH ? project_any(v, F.cam, rp, mod, true, F.wpat)
                   : project_core<W_FULL>(v, F.cam, rp, mod, true);
+}
+template <typename GT, typename ST, bool DISPATCH = true>
+__device__ __forceinline__ Proj slot_project(const ProjLevels &lv, const Work &w,
+                                             const FrameCtx &F, const lodge_raster_params &rp,
+                                             int l, uint32_t slot, double v[12],
+                                             const ST *&sp, uint32_t &gidx) {
+  gidx = w.union_idx[slot];
+  return slot_project_at<GT, ST, DISPATCH>(lv, F, rp, l, gidx, w.union_tag[slot], v, sp);
 }
 
 // K2, geometry only.  Outputs are written at the dense concatenated input
@@ -572,8 +579,9 @@ __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLeve
   for (uint32_t base = blockIdx.x * blockDim.x; base < nslots; base += gridDim.x * blockDim.x) {
     const uint32_t slot = base + threadIdx.x;
     // map slot -> level
-    int l = 0;
-    while (l + 1 < lv.L && slot >= lv.slot_base[l + 1]) ++l;
+    int l = 0;  // the levels' slot ranges are consecutive: count the starts passed
+#pragma unroll
+    for (int k = 1; k < LODGE_MAX_LEVELS; ++k) l += (k < lv.L && slot >= lv.slot_base[k]) ? 1 : 0;
     const uint32_t pos = slot - lv.slot_base[l];
     const bool valid = slot < nslots && pos < F.used[l];
     const uint32_t g = F.cat[l] + pos;
@@ -604,7 +612,7 @@ __global__ void __launch_bounds__(256, LODGE_PROJ_MINB) k_project_frame(ProjLeve
     }
     wc += __popc(kb);
     const uint64_t rc = keep ? tile_rect(p.mx, p.my, p.ex, p.ey, tiles_x, tiles_y) : 0ull;
-    if (priv) add_tile_diff_shared(s_diff, rc, tiles_x, keep);
+    if (priv) add_tile_diff_shared(s_diff, rc, tiles_x, tiles_y, keep);
     else add_tile_diff(w.tile_diff, rc, tiles_x, keep);
     if (keep) {  // the full key (tie repair) and the rectangle, by input index
       w.key_depth[0][g] = (uint64_t)__double_as_longlong(p.z);
