@@ -401,8 +401,8 @@ void launch_debug_depth_sort(const Work &w, FrameState *fs, const uint64_t *keys
 void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32_t tiles_x,
                        int32_t tiles_y, cudaStream_t s, bool two_phase = false);
 // two-phase frames: first-phase pair budget of the counting pass
-void launch_dup_count(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_cap,
-                      uint32_t budget, cudaStream_t s);
+void launch_dup_count(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
+                      int64_t M_cap, uint32_t budget, cudaStream_t s);
 void launch_dup_emit(const Work &w, FrameState *fs, int32_t tiles_x, cudaStream_t s,
                      bool first_phase);
 void launch_setup_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,

@@ -468,7 +468,13 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
                                                            const uint64_t *__restrict__ rect,
                                                            Work w, FrameState *fs,
                                                            uint32_t budget, int32_t tiles_x,
-                                                           uint32_t chunk_cap) {
+                                                           uint32_t chunk_cap, int32_t tiles_y,
+                                                           int32_t diff_smem) {
+  // first phase: the CTAs holding first-phase splats add their rectangles to
+  // a CTA-private difference array (dynamic shared memory, when it fits),
+  // flushed once -- the few CTAs at the front of the depth order otherwise
+  // serialise on global atomics at the shared border corners
+  extern __shared__ int32_t s_da[];
   constexpr int IT = COUNT_ITEMS;  // consecutive depth-order splats per thread
   constexpr int TK = SECOND ? TK_DUPB : TK_DUP;
   __shared__ uint32_t s_w[DUP_THREADS / 32], s_z[DUP_THREADS / 32];
@@ -563,6 +569,12 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
     if (lane == 0) s_zbase = pre;
   }
   __syncthreads();
+  const int32_t nd = (tiles_x + 1) * (tiles_y + 1);
+  const bool fa = !SECOND && budget && diff_smem && s_base < budget;  // CTA-uniform
+  if (fa) {
+    for (int32_t q = tid; q < nd; q += DUP_THREADS) s_da[q] = 0;
+    __syncthreads();
+  }
   uint32_t off = s_base + s_w[warp] + inc - cnt;
   uint32_t k = SECOND ? s_zbase + s_z[warp] + zinc - nz : 0u;  // owner index
 #pragma unroll
@@ -597,7 +609,8 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
     }
     if (!SECOND && budget) {  // whole warp: the difference-array update is collective
       const bool first = valid && off < budget;
-      add_tile_diff(w.tile_diff_a, rc[i], tiles_x, first);
+      if (fa) add_tile_diff_shared(s_da, rc[i], tiles_x, tiles_y, first);
+      else add_tile_diff(w.tile_diff_a, rc[i], tiles_x, first);
       if (first && (off + c[i] >= budget || r == n - 1)) {
         fs->split_S = r + 1;
         fs->stats.M_first = r + 1;
@@ -607,6 +620,13 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
     if (valid) {
       off += c[i];
       if (SECOND && c[i]) ++k;
+    }
+  }
+  if (fa) {
+    __syncthreads();
+    for (int32_t q = tid; q < nd; q += DUP_THREADS) {
+      const int32_t v = s_da[q];
+      if (v) atomicAdd(w.tile_diff_a + q, v);
     }
   }
 }
@@ -744,13 +764,21 @@ void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32
 
 static uint32_t chunk_cap(const Work &w) { return (uint32_t)(w.P_cap / EMIT_CHUNK + 4); }
 
-void launch_dup_count(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_cap,
-                      uint32_t budget, cudaStream_t s) {
+constexpr size_t DUP_DIFF_SMEM_MAX = 64 * 1024;  // CTA-private first-phase difference array
+void launch_dup_count(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
+                      int64_t M_cap, uint32_t budget, cudaStream_t s) {
   if (M_cap <= 0) return;
   const unsigned grid =
       (unsigned)((M_cap + DUP_THREADS * COUNT_ITEMS - 1) / (DUP_THREADS * COUNT_ITEMS));
-  k_dup_count<false><<<grid, DUP_THREADS, 0, s>>>(w.val_depth[0], w.rect, w, fs, budget, tiles_x,
-                                                  chunk_cap(w));
+  const size_t sm = (size_t)(tiles_x + 1) * (tiles_y + 1) * 4;
+  const bool priv = budget && sm <= DUP_DIFF_SMEM_MAX;
+  static PerDevice attr;
+  if (priv && sm > 48 * 1024 && (int64_t)sm > attr()) {
+    cudaFuncSetAttribute(k_dup_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr() = (int64_t)sm;
+  }
+  k_dup_count<false><<<grid, DUP_THREADS, priv ? sm : 0, s>>>(
+      w.val_depth[0], w.rect, w, fs, budget, tiles_x, chunk_cap(w), tiles_y, priv ? 1 : 0);
 }
 
 // Resident CTAs of a kernel on this device (persistent grids).
@@ -779,7 +807,7 @@ void launch_dup_emit(const Work &w, FrameState *fs, int32_t tiles_x, cudaStream_
 void launch_duplicate(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_cap,
                       cudaStream_t s) {
   if (M_cap <= 0) return;
-  launch_dup_count(w, fs, tiles_x, M_cap, 0u, s);
+  launch_dup_count(w, fs, tiles_x, 0, M_cap, 0u, s);  // one pass: no first-phase array
   launch_dup_emit(w, fs, tiles_x, s, false);
 }
 
@@ -812,7 +840,7 @@ void launch_enum_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles
   const unsigned grid =
       (unsigned)((M_cap + DUP_THREADS * COUNT_ITEMS - 1) / (DUP_THREADS * COUNT_ITEMS));
   k_dup_count<true><<<grid, DUP_THREADS, 0, s>>>(w.val_depth[0], w.rect, w, fs, 0u, tiles_x,
-                                                 chunk_cap(w));
+                                                 chunk_cap(w), tiles_y, 0);
   static PerDevice res;
   constexpr size_t sm = sizeof(EmitSmem<EB_CHUNK>);
   if (!res()) {

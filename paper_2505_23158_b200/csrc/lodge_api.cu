@@ -524,7 +524,7 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
     // tiles that still have live pixels then receive the rest of their pairs
     const uint32_t budget = (uint32_t)std::min<int64_t>(
         (int64_t)c->phase_budget * tiles_x * tiles_y, 0x7fffffff);
-    launch_dup_count(w, c->fs, tiles_x, U_cap, budget, s);
+    launch_dup_count(w, c->fs, tiles_x, tiles_y, U_cap, budget, s);
     DSYNC("launch_dup_count");
     // compositing records of the first phase's splats only
     launch_payload(levels, ls, w, c->fs, cam_dev, rp, shade, w.val_depth[0], &c->fs->split_S,
