@@ -136,8 +136,8 @@ typedef struct {
   uint32_t P;            /* tile-splat pairs */
   uint32_t overflow;     /* 1 if P exceeded the pair capacity */
   uint32_t guard_hits;   /* FAST: pixel-splat decisions re-checked in fp64 */
-  uint32_t P_first;      /* pairs sorted in the first (or only) depth phase */
-  uint32_t P_second;     /* pairs sorted in the second phase (two-phase frames) */
+  uint32_t P_first;      /* pairs of the first (or only) depth phase's lists */
+  uint32_t P_second;     /* pairs of the second phase's lists (two-phase frames) */
   uint32_t fault;        /* nonzero: a device-side bounds check fired (one bit per
                             site, internal.cuh FAULT_*); the frame's outputs are invalid */
   uint32_t M_first;      /* two-phase frames: splats of the first phase */
@@ -145,6 +145,8 @@ typedef struct {
   uint32_t comp_members; /* compositing work: sum over tiles (and phases) of the list
                             members a tile iterates before all its pixels have
                             T < t_min, or its whole list (SURVEY.md 8d m_t) */
+  uint32_t block_lists;  /* two-phase frames: bit 0 (1) the first phase, bit 1 (2) the
+                            second kept block lists instead of sorted per-tile lists */
 } lodge_frame_stats;
 
 /* ---- context ---------------------------------------------------------- */

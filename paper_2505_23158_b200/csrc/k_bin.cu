@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t *dif
     fs->stats.P_first = s_tot;
     fs->scan_a = scan ? 1u : 0u;
     fs->n_sort_a = scan ? 0u : n_pairs;
+    fs->stats.block_lists = scan ? 1u : 0u;
   }
 }
 
@@ -605,6 +606,7 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
         const bool sb = fs->scan_a && nq <= (uint32_t)(BL_CHUNK * BL_CHMAX);
         fs->scan_b = sb ? 1u : 0u;
         fs->n_sort_b = sb ? 0u : fs->n_pairs;
+        if (sb) fs->stats.block_lists |= 2u;
       }
     }
     if (!SECOND && budget) {  // whole warp: the difference-array update is collective

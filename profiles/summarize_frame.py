@@ -30,6 +30,8 @@ STAGE_OF = [
     ("k_depth_pass", "depth_sort"), ("k_depth_ties", "depth_sort"),
     ("k_dup_count<0>", "tile_setup"), ("k_payload", "tile_setup"), ("k_tile_setup", "tile_setup"),
     ("k_dup_emit", "duplicate"),
+    ("k_block_lists<1>", "tile_sort"),
+    ("k_block_lists<2>", "second_phase"),
     ("k_composite<0, 3, 1>", "composite"),
     ("k_setup_b", "second_phase"), ("k_dup_count<1>", "second_phase"),
     ("k_emit_b", "second_phase"),
