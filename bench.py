@@ -641,6 +641,12 @@ def run_lodge(args):
         img8_host = torch.empty((B, H, W, 3), dtype=torch.uint8).pin_memory()
         st_host = torch.empty((B, STATS_BYTES), dtype=torch.uint8).pin_memory()
         cams_host = cams.cpu()
+        # read-backs on one copy stream per slot: a frame's D2H copy overlaps
+        # the next frames of its slot; frame buffer j is re-rendered only
+        # after its previous copy completed
+        copy_s = [torch.cuda.Stream(device=dev) for _ in range(S)]
+        ready = [torch.cuda.Event() for _ in range(B)]
+        drained = [torch.cuda.Event() for _ in range(B)]
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -660,17 +666,22 @@ def run_lodge(args):
             for q in range(S):
                 r.stream_of(q).wait_stream(cur)
             for j, v in enumerate(blk):
-                do_render(r, cam_dev[par][j], frames[j], j % S, v)
-                r.to_srgb8(frames[j], img8[j], slot=j % S)
-                # each frame's read-back on its own stream, so it overlaps the
-                # frames still rendering instead of gating the next step
-                with torch.cuda.stream(r.stream_of(j % S)):
+                q = j % S
+                if si >= 1:  # frame buffer j: its previous read-back is done
+                    r.stream_of(q).wait_event(drained[j])
+                do_render(r, cam_dev[par][j], frames[j], q, v)
+                r.to_srgb8(frames[j], img8[j], slot=q)
+                ready[j].record(r.stream_of(q))
+                with torch.cuda.stream(copy_s[q]):
+                    copy_s[q].wait_event(ready[j])
                     img8_host[j].copy_(img8[j], non_blocking=True)
                     st_host[j].copy_(frames[j].stats, non_blocking=True)
+                    drained[j].record(copy_s[q])
             for q in range(S):
                 used[par][q].record(r.stream_of(q))
         for q in range(S):
             cur.wait_stream(r.stream_of(q))
+            cur.wait_stream(copy_s[q])
         f1.record(cur)
         torch.cuda.synchronize()
         ems = shard.max_over_ranks(f0.elapsed_time(f1), dev)
