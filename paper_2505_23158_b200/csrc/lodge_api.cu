@@ -547,7 +547,9 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
 #endif
     DSYNC("launch_tile_sort");
     c->mark(7);
+#ifndef LODGE_DEBUG_SKIP_COMPOSITE  // diagnostic builds: the frame without its compositing
     launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, (uint32_t)U_cap, s, 1);
+#endif
     ++nl;
     DSYNC("launch_composite");
     DSYNC_L(2, "segment: count .. first-phase composite");
@@ -568,7 +570,9 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
 #endif
     DSYNC("launch_tile_sort (second phase)");
     c->mark(9);
+#ifndef LODGE_DEBUG_SKIP_COMPOSITE
     launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, (uint32_t)U_cap, s, 2);
+#endif
     ++nl;
     DSYNC("launch_composite (second phase)");
     DSYNC_L(2, "segment: second phase");
