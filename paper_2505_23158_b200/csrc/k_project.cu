@@ -99,11 +99,21 @@ __device__ __forceinline__ bool all_finite9(const double c[9]) {
   return ok;
 }
 
+// The camera's clamp limits on x/z, y/z (src/raster.py:230-231), per
+// camera: computed once per CTA in the frame kernels (the same fp64
+// expression, so the same bits).
+struct CamLims {
+  double x, y;
+};
+__host__ __device__ inline CamLims cam_lims(const lodge_camera &cam) {
+  return CamLims{1.3 * 0.5 * (double)cam.w / cam.fx, 1.3 * 0.5 * (double)cam.h / cam.fy};
+}
+
 // v: [mean3, scale3, rot4 wxyz, opacity, fv]
 template <int WM = W_FULL>
 __device__ __forceinline__ Proj project_core(const double v[12], const lodge_camera &cam,
                                              const lodge_raster_params &rp, double mod,
-                                             bool has_mod) {
+                                             bool has_mod, const CamLims &lim) {
   Proj p;
   p.ok = false;
   const double *W = cam.R;
@@ -173,8 +183,7 @@ __device__ __forceinline__ Proj project_core(const double v[12], const lodge_cam
         cc[3 * i + l] = acc;
       }
   }
-  const double lim_x = 1.3 * 0.5 * (double)cam.w / fx;
-  const double lim_y = 1.3 * 0.5 * (double)cam.h / fy;
+  const double lim_x = lim.x, lim_y = lim.y;
   double tx = x / z, ty = y / z;
   tx = tx < -lim_x ? -lim_x : (tx > lim_x ? lim_x : tx);
   ty = ty < -lim_y ? -lim_y : (ty > lim_y ? lim_y : ty);
@@ -231,10 +240,10 @@ __device__ __forceinline__ Proj project_core(const double v[12], const lodge_cam
 // project_core for the camera's rotation zero pattern (uniform per camera).
 __device__ __forceinline__ Proj project_any(const double v[12], const lodge_camera &cam,
                                             const lodge_raster_params &rp, double mod,
-                                            bool has_mod, int wpat) {
-  if (wpat == W_IDENT) return project_core<W_IDENT>(v, cam, rp, mod, has_mod);
-  if (wpat == W_YAW) return project_core<W_YAW>(v, cam, rp, mod, has_mod);
-  return project_core<W_FULL>(v, cam, rp, mod, has_mod);
+                                            bool has_mod, int wpat, const CamLims &lim) {
+  if (wpat == W_IDENT) return project_core<W_IDENT>(v, cam, rp, mod, has_mod, lim);
+  if (wpat == W_YAW) return project_core<W_YAW>(v, cam, rp, mod, has_mod, lim);
+  return project_core<W_FULL>(v, cam, rp, mod, has_mod, lim);
 }
 
 // Coefficients of one record, (3, (DEG+1)^2), loaded with 16-byte vector
@@ -461,6 +470,7 @@ struct FrameCtx {
   double t;
   int32_t f, o;
   int32_t wpat;  // camera rotation zero pattern (project_any)
+  CamLims lim;   // the camera's x/z, y/z clamp limits
   uint32_t used[LODGE_MAX_LEVELS], cat[LODGE_MAX_LEVELS];
 };
 
@@ -470,6 +480,7 @@ __device__ __forceinline__ void stage_frame_ctx(FrameCtx &F, const ProjLevels &l
   if (threadIdx.x == 0) {
     F.cam = *cam_p;
     F.wpat = camera_wpattern(F.cam);
+    F.lim = cam_lims(F.cam);
     F.t = fs->stats.t;
     F.f = fs->stats.f;
     F.o = fs->stats.o < 0 ? fs->stats.f : fs->stats.o;
@@ -504,8 +515,8 @@ __device__ __forceinline__ Proj slot_project_at(const ProjLevels &lv, const Fram
   }
   load_geom<GT>(gp + (size_t)gidx * 12, v);
   if (lv.qnorm[l]) normalize_rot(v);
-  return DISPATCH ? project_any(v, F.cam, rp, mod, true, F.wpat)
-                  : project_core<W_FULL>(v, F.cam, rp, mod, true);
+  return DISPATCH ? project_any(v, F.cam, rp, mod, true, F.wpat, F.lim)
+                  : project_core<W_FULL>(v, F.cam, rp, mod, true, F.lim);
 }
 template <typename GT, typename ST, bool DISPATCH = true>
 __device__ __forceinline__ Proj slot_project(const ProjLevels &lv, const Work &w,
@@ -702,7 +713,8 @@ __global__ void __launch_bounds__(256) k_project_compat(const GT *geom, const ST
     g = idx ? idx[e] : e;
     load_geom<GT>(geom + (size_t)g * 12, v);
     if (qnorm) normalize_rot(v);
-    p = project_any(v, cam, rp, mod ? mod[e] : 1.0, mod != nullptr, camera_wpattern(cam));
+    p = project_any(v, cam, rp, mod ? mod[e] : 1.0, mod != nullptr, camera_wpattern(cam),
+                    cam_lims(cam));
   }
   const int64_t m = compact_slot(e < n && p.ok, w.status, fs->epoch + TK_COMPACT, part, s_warp,
                                  &s_base);
@@ -758,7 +770,7 @@ __global__ void __launch_bounds__(256) k_cover_keys(const GT *geom, const int64_
     const int64_t g = idx ? idx[e] : e;
     load_geom<GT>(geom + (size_t)g * 12, v);
     if (qnorm) normalize_rot(v);
-    p = project_any(v, cam, rp, 1.0, false, camera_wpattern(cam));
+    p = project_any(v, cam, rp, 1.0, false, camera_wpattern(cam), cam_lims(cam));
   }
   const int64_t m = compact_slot(e < n && p.ok, w.status, fs->epoch + TK_COMPACT, part, s_warp,
                                  &s_base);

@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(OS_THREADS, VALS ? LODGE_OS_VMINB
   Smem &S = *reinterpret_cast<Smem *>(smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t n = *n_ptr;
+  if (n == 0) return;  // e.g. a phase that kept block lists: no ticket traffic
   // persistent CTAs: partitions in ticket order until the keys run out
   for (;;) {
   if (tid == 0) S.misc[0] = atomicAdd(&fs->tickets[tk], 1u);
