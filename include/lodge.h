@@ -163,6 +163,16 @@ int lodge_reserve(lodge_ctx *ctx, int64_t max_splats, int64_t max_pairs);
  * composite the rest of their pairs.  Outputs are bitwise those of one pass.
  * 0 disables (every frame one pass); default 2048. */
 int lodge_set_phase_budget(lodge_ctx *ctx, int32_t pairs_per_tile);
+/* Block lists: a depth phase of few large splats keeps, per
+ * block of 8 x 4 tiles, its depth-ordered splats with tile masks instead of
+ * emitting and sorting its pairs.  AUTO decides per frame on the device
+ * (<= 64k splats averaging >= 64 tiles); FORCE uses them whenever the phase
+ * has <= 64k splats (second phase: owners); OFF never.  Outputs are the same
+ * in every mode; lodge_frame_stats.block_lists reports the choice. */
+#define LODGE_BLOCK_LISTS_AUTO 0
+#define LODGE_BLOCK_LISTS_OFF 1
+#define LODGE_BLOCK_LISTS_FORCE 2
+int lodge_set_block_lists(lodge_ctx *ctx, int32_t mode);
 int lodge_set_precision(lodge_ctx *ctx, int32_t precision);
 
 /* ---- chunk selection: nearest_two_chunks + blend_factor ---------------

@@ -399,7 +399,8 @@ void launch_depth_sort64(const Work &w, FrameState *fs, int64_t M_cap, int32_t *
 void launch_debug_depth_sort(const Work &w, FrameState *fs, const uint64_t *keys, uint32_t n,
                              uint64_t *ko, uint32_t *vo, uint32_t *m_out, cudaStream_t s);
 void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32_t tiles_x,
-                       int32_t tiles_y, cudaStream_t s, bool two_phase = false);
+                       int32_t tiles_y, cudaStream_t s, bool two_phase = false,
+                       int32_t bl_mode = LODGE_BLOCK_LISTS_AUTO);
 // two-phase frames: first-phase pair budget of the counting pass
 void launch_dup_count(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
                       int64_t M_cap, uint32_t budget, cudaStream_t s);

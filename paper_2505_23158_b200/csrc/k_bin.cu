@@ -164,7 +164,8 @@ __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t *dif
                                                      int32_t *tile_count, uint32_t *count_all,
                                                      uint32_t *alive, uint32_t *tile_start,
                                                      uint32_t *tile_order, FrameState *fs,
-                                                     int64_t P_cap, uint32_t *bl_start) {
+                                                     int64_t P_cap, uint32_t *bl_start,
+                                                     int32_t bl_mode) {
   extern __shared__ int32_t sd[];  // (tx+1)*(ty+1), twice with diff_a
   __shared__ uint32_t h0[256], h1[256];
   __shared__ uint32_t s_sum[1024];
@@ -213,7 +214,9 @@ __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t *dif
   const bool scan = false;
 #else
   const bool scan = diff_a && n_pairs > 0 && S <= (uint32_t)(BL_CHUNK * BL_CHMAX) &&
-                    (uint64_t)s_tot >= (uint64_t)LODGE_SCAN_MIN_TILES * S;
+                    bl_mode != LODGE_BLOCK_LISTS_OFF &&
+                    (bl_mode == LODGE_BLOCK_LISTS_FORCE ||
+                     (uint64_t)s_tot >= (uint64_t)LODGE_SCAN_MIN_TILES * S);
 #endif
   if (scan) block_offsets([&](int t) { return at(lc, t); }, tiles_x, tiles_y, bl_start, s_sum);
   if (tid == 0) {
@@ -750,7 +753,7 @@ __global__ void __launch_bounds__(DUP_THREADS) k_emit_b(const uint32_t *__restri
 }
 
 void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32_t tiles_x,
-                       int32_t tiles_y, cudaStream_t s, bool two_phase) {
+                       int32_t tiles_y, cudaStream_t s, bool two_phase, int32_t bl_mode) {
   const size_t nd = (size_t)(tiles_x + 1) * (tiles_y + 1) * 4;
   const size_t sm = two_phase ? 2 * nd : nd;
   static PerDevice attr;
@@ -761,7 +764,7 @@ void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32
   k_tile_setup<<<1, 1024, sm, s>>>(w.tile_diff, two_phase ? w.tile_diff_a : nullptr, tiles_x,
                                    tiles_y, tile_count, two_phase ? w.count_all : nullptr,
                                    two_phase ? w.alive : nullptr, w.tile_start, w.tile_order, fs,
-                                   w.P_cap, w.bl_start);
+                                   w.P_cap, w.bl_start, bl_mode);
 }
 
 static uint32_t chunk_cap(const Work &w) { return (uint32_t)(w.P_cap / EMIT_CHUNK + 4); }

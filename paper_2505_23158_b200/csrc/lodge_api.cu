@@ -39,6 +39,7 @@ struct lodge_ctx {
   int64_t tiles_cap = 0;  // capacity of tile_start (T+1) and diff
   int64_t pixels_cap = 0;  // capacity of the two-phase pixel state
   int32_t phase_budget = 2048;  // first-phase pairs per tile of two-phase frames (0: one pass)
+  int32_t block_lists = LODGE_BLOCK_LISTS_AUTO;  // lodge_set_block_lists
   int debug_sync = 0;  // LODGE_DEBUG_SYNC=1: check after every stage; 2: after each segment
   int32_t launches = 0;
   LevelSlots last_slots{};  // slot layout of the last union
@@ -266,6 +267,14 @@ int lodge_set_phase_budget(lodge_ctx *c, int32_t pairs_per_tile) {
   if (!c) return set_err(LODGE_ERR_BAD_ARG, "ctx is NULL");
   if (pairs_per_tile < 0) return set_err(LODGE_ERR_BAD_ARG, "phase budget must be >= 0");
   c->phase_budget = pairs_per_tile;
+  return 0;
+}
+
+int lodge_set_block_lists(lodge_ctx *c, int32_t mode) {
+  if (!c) return set_err(LODGE_ERR_BAD_ARG, "ctx is NULL");
+  if (mode < LODGE_BLOCK_LISTS_AUTO || mode > LODGE_BLOCK_LISTS_FORCE)
+    return set_err(LODGE_ERR_BAD_ARG, "block-list mode must be AUTO, OFF or FORCE");
+  c->block_lists = mode;
   return 0;
 }
 
@@ -530,7 +539,7 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
     launch_payload(levels, ls, w, c->fs, cam_dev, rp, shade, w.val_depth[0], &c->fs->split_S,
                    U_cap, s, slab_geom, slab_sh); ++nl;
     DSYNC("launch_payload");
-    launch_tile_setup(w, c->fs, out->tile_count_dev, tiles_x, tiles_y, s, true);
+    launch_tile_setup(w, c->fs, out->tile_count_dev, tiles_x, tiles_y, s, true, c->block_lists);
     DSYNC("launch_tile_setup");
     nl += 2;
     c->mark(5);

@@ -44,6 +44,9 @@ class Frame:
         return N.FrameStats.from_buffer_copy(raw)
 
 
+BLOCK_LIST_MODES = {"auto": 0, "off": 1, "force": 2}  # lodge.h LODGE_BLOCK_LISTS_*
+
+
 class Renderer:
     """n_streams > 1 keeps that many frames in flight: each slot owns a
     liblodge context (workspace + frame state) and a CUDA stream, so the
@@ -53,11 +56,14 @@ class Renderer:
     FAST frames composite in two depth phases (lodge_set_phase_budget:
     phase_budget first-phase pairs per tile, 0 = one pass); full_lists=True
     keeps one pass so the sorted per-tile lists stay inspectable
-    (lodge_frame_lists).  The outputs are the same either way."""
+    (lodge_frame_lists).  block_lists ("auto", "off", "force";
+    lodge_set_block_lists) chooses how a phase of few large splats builds
+    its lists.  The outputs are the same either way."""
 
     def __init__(self, levels: Sequence, plan, device=None, storage: str = "fp32",
                  precision: str = "fast", raster_cfg: RasterConfig = RasterConfig(),
-                 n_streams: int = 1, full_lists: bool = False, phase_budget: int = 2048):
+                 n_streams: int = 1, full_lists: bool = False, phase_budget: int = 2048,
+                 block_lists: str = "auto"):
         self.ctx = context(device)
         self.device = self.ctx.device
         if n_streams < 1:
@@ -84,6 +90,9 @@ class Renderer:
         if phase_budget < 0:
             raise ValueError("phase_budget must be >= 0")
         self.phase_budget = int(phase_budget)
+        if block_lists not in BLOCK_LIST_MODES:
+            raise ValueError("block_lists must be 'auto', 'off' or 'force'")
+        self.block_lists = BLOCK_LIST_MODES[block_lists]
         self.cfg = raster_cfg
         self._rp = params_struct(raster_cfg)
         lod_cap = sum(l.n for l in self.levels)
@@ -107,6 +116,7 @@ class Renderer:
             with torch.cuda.stream(s):
                 p = ctx.bind(self.precision)
         N.check(N.lib().lodge_set_phase_budget(p, self.phase_budget), "lodge_set_phase_budget")
+        N.check(N.lib().lodge_set_block_lists(p, self.block_lists), "lodge_set_block_lists")
         return p
 
     def reserve(self, max_pairs: int):
