@@ -394,9 +394,6 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
         mem |= h ? (1u << i) : 0u;
       }
       __syncthreads();
-#ifdef LODGE_COUNTERS
-      if (tid == 0) atomicAdd(&fs->counters[6], 1ull);
-#endif
       const uint32_t mk = lane < NQ ? S.bl_mask[par * 16 + lane] : 0u;
       const uint32_t c = __popc(mk);
       uint32_t inc = c;
@@ -561,6 +558,7 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
   uint32_t guard = 0;
 #ifdef LODGE_COUNTERS
   unsigned long long c_list = 0, c_iter = 0, c_hit = 0, c_px = 0, c_batch = 0;
+  unsigned long long c_akg = 0, c_nakg = 0;  // groups taken all-keep / with the band tests
 #endif
   uint32_t phase0 = 0u, phase1 = 0u;
 
@@ -905,6 +903,8 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
         if (!AK && __any_sync(FULL_MASK, near)) return false;
 #ifdef LODGE_COUNTERS
         c_iter += G;
+        if (AK) ++c_akg;
+        else ++c_nakg;
 #endif
         PxF<PX> a[G];
 #pragma unroll
@@ -1004,12 +1004,11 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
     atomicAdd(&fs->counters[1], c_iter);
     atomicAdd(&fs->counters[2], c_hit);
     atomicAdd(&fs->counters[4], c_batch);
+    atomicAdd(&fs->counters[5], c_akg);
+    atomicAdd(&fs->counters[6], c_nakg);
   }
   atomicAdd(&fs->counters[3], c_px);  // pixel evaluations inside the cut-off
-  if (tid == 0) {
-    atomicMax(&fs->counters[5], c_batch);
-    // counters[6]: block-list refill rounds (issue_block)
-  }
+  // counters[5] / [6]: all-keep / band-tested groups (per warp)
 #endif
   {  // members iterated (SURVEY.md 8d m_t): the whole list while a pixel is
      // still alive, else the furthest member a warp blended before its pixels

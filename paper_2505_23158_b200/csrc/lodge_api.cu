@@ -579,7 +579,7 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
 #endif
     DSYNC("launch_tile_sort (second phase)");
     c->mark(9);
-#ifndef LODGE_DEBUG_SKIP_COMPOSITE
+#if !defined(LODGE_DEBUG_SKIP_COMPOSITE) && !defined(LODGE_DEBUG_SKIP_COMPOSITE_B)
     launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, (uint32_t)U_cap, s, 2);
 #endif
     ++nl;
