@@ -6,7 +6,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <cstddef>
+#include <cmath>
 #include <string>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -40,6 +42,7 @@ struct lodge_ctx {
   int64_t pixels_cap = 0;  // capacity of the two-phase pixel state
   int32_t phase_budget = 2048;  // first-phase pairs per tile of two-phase frames (0: one pass)
   int32_t block_lists = LODGE_BLOCK_LISTS_AUTO;  // lodge_set_block_lists
+  float *srgb_thr = nullptr;  // lodge_to_srgb8's level thresholds on this device
   int debug_sync = 0;  // LODGE_DEBUG_SYNC=1: check after every stage; 2: after each segment
   int32_t launches = 0;
   LevelSlots last_slots{};  // slot layout of the last union
@@ -249,7 +252,7 @@ void lodge_destroy(lodge_ctx *c) {
                   w.status, w.union_idx, w.union_tag, c->fs, c->cam_dev, w.rect_sorted,
                   w.splat_off, w.chunk_first, w.tile_order, w.tile_diff_a, w.count_all,
                   w.tile_start_b, w.tile_order_b, w.alive, w.sat, w.state, w.vrank,
-                  c->edges_dev};
+                  w.bl_start, w.bl_len, c->edges_dev, c->srgb_thr};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c->cam_host) cudaFreeHost(c->cam_host);
@@ -751,18 +754,96 @@ int lodge_profile_read(lodge_ctx *c, double *stage_ms, int32_t *frames) {
   return 0;
 }
 
-__global__ void k_srgb8(const float *img, int64_t n, uint8_t *out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 3 * n) return;
-  const double x = fmin(fmax((double)img[i], 0.0), 1.0);
-  const double e = x <= 0.0031308 ? 12.92 * x : 1.055 * pow(x, 1.0 / 2.4) - 0.055;
-  out[i] = (uint8_t)rint(e * 255.0);  // np.round: half to even
+// 8-bit sRGB (the reference's to_uint8, src/images.py:10-17: clip, the
+// piecewise curve in fp64, np.round) is a non-decreasing step function of
+// the fp32 input with 255 steps.  Its thresholds -- the smallest fp32 x with
+// to_uint8(x) >= k, k = 1..255 -- are found once per process by bisection
+// over fp32 bit patterns with the reference's own fp64 formula on the host
+// (libm pow, as NumPy's power), and each pixel is a binary search over them:
+// no fp64 pow per channel.  NaN and x <= 0 give 0, x >= 1 gives 255, as
+// clip does.
+static int srgb_level(float xf) {
+  const double x = std::fmin(std::fmax((double)xf, 0.0), 1.0);
+  double e;
+  if (x <= 0.0031308) {
+    e = 12.92 * x;
+  } else {
+    volatile double a = 1.055 * std::pow(x, 1.0 / 2.4);  // no contraction with the - 0.055
+    e = a - 0.055;
+  }
+  volatile double y = e * 255.0;
+  return (int)std::nearbyint(y);  // round half to even, as np.round
+}
+
+static std::vector<float> make_srgb_thresholds() {
+  std::vector<float> t(256);
+  {
+    t[0] = -INFINITY;
+    for (int k = 1; k < 256; ++k) {
+      uint32_t lo = 0u, hi = 0x3f800000u;  // f(+0) = 0 < k <= 255 = f(1)
+      while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        float xm;
+        std::memcpy(&xm, &mid, 4);
+        if (srgb_level(xm) >= k) hi = mid;
+        else lo = mid + 1;
+      }
+      std::memcpy(&t[k], &lo, 4);
+    }
+  }
+  return t;
+}
+static const float *srgb_thresholds() {
+  static const std::vector<float> t = make_srgb_thresholds();  // thread-safe, once
+  return t.data();
+}
+
+__global__ void __launch_bounds__(256) k_srgb8(const float *__restrict__ img, int64_t n,
+                                               const float *__restrict__ thr,
+                                               uint8_t *__restrict__ out) {
+  __shared__ float t[256];
+  t[threadIdx.x] = thr[threadIdx.x];
+  __syncthreads();
+  const int64_t total = 3 * n;
+  for (int64_t i0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); i0 < total;
+       i0 += 4 * (int64_t)gridDim.x * blockDim.x) {
+    float x[4];
+    const bool full = i0 + 4 <= total && (reinterpret_cast<uintptr_t>(img + i0) & 15) == 0;
+    if (full) {
+      const float4 v = *reinterpret_cast<const float4 *>(img + i0);
+      x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) x[q] = i0 + q < total ? img[i0 + q] : 0.f;
+    }
+    uint32_t packed = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int k = 0;  // the number of thresholds <= x
+#pragma unroll
+      for (int st = 128; st >= 1; st >>= 1) k += (x[q] >= t[k + st]) ? st : 0;
+      packed |= (uint32_t)k << (8 * q);
+    }
+    if (full && (reinterpret_cast<uintptr_t>(out + i0) & 3) == 0) {
+      *reinterpret_cast<uint32_t *>(out + i0) = packed;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (i0 + q < total) out[i0 + q] = (uint8_t)(packed >> (8 * q));
+    }
+  }
 }
 
 int lodge_to_srgb8(lodge_ctx *c, const float *img, int64_t n, uint8_t *out) {
   if (!c || !img || !out) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
   if (n <= 0) return 0;
-  k_srgb8<<<(unsigned)((3 * n + 255) / 256), 256, 0, c->stream>>>(img, n, out);
+  if (!c->srgb_thr) {  // the per-device copy of the thresholds, once per context
+    CK(cudaMalloc(&c->srgb_thr, 256 * sizeof(float)));
+    CK(cudaMemcpy(c->srgb_thr, srgb_thresholds(), 256 * sizeof(float), cudaMemcpyHostToDevice));
+  }
+  const int64_t quads = (3 * n + 3) / 4;
+  const unsigned grid = (unsigned)std::min<int64_t>((quads + 255) / 256, 148 * 16);
+  k_srgb8<<<grid, 256, 0, c->stream>>>(img, n, c->srgb_thr, out);
   return check_launch("lodge_to_srgb8");
 }
 
