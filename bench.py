@@ -444,22 +444,29 @@ def run_lodge(args):
     pairs = ({v: host_pair(cfg.centers, sweep[v].position) for v in flat}
              if store is not None else None)
 
-    def do_render(rr, cam_row, frame, slot, v):
-        """One frame of args.mode (the CLI's render modes, src/cli.py:219-243)."""
+    def do_render(rr, cam_row, frame, slot, v, srgb8=None):
+        """One frame of args.mode (the CLI's render modes, src/cli.py:219-243).
+        srgb8: the 8-bit sRGB image written by the compositor itself (the
+        float image is then not stored); else the float image."""
+        kw = {} if srgb8 is None else {"srgb8_out": srgb8, "float_image": False}
         if store is not None:  # chunk pair decided on the host, slabs made resident
             f, o, t = pairs[v]
             if args.mode == "chunks":
                 o, t = None, 1.0
             st = rr.stream_of(slot)
             store.require([f, o], st)
-            rr.render(cam_row, frame, pair=(f, o), t=t, slot=slot)
+            rr.render(cam_row, frame, pair=(f, o), t=t, slot=slot, **kw)
             store.release([f, o], st)
         elif args.mode == "blend":
-            rr.render(cam_row, frame, slot=slot)
+            rr.render(cam_row, frame, slot=slot, **kw)
         elif args.mode == "chunks":
-            rr.render(cam_row, frame, pair=(near[v], None), slot=slot)
+            rr.render(cam_row, frame, pair=(near[v], None), slot=slot, **kw)
         else:
-            rr.render_lod(cam_row, frame, bounds, full=args.mode == "full", slot=slot)
+            if srgb8 is not None:  # render_lod has no 8-bit output: convert
+                rr.render_lod(cam_row, frame, bounds, full=args.mode == "full", slot=slot)
+                rr.to_srgb8(frame, srgb8, slot=slot)
+            else:
+                rr.render_lod(cam_row, frame, bounds, full=args.mode == "full", slot=slot)
 
     def read_stats(t):
         raw = t.cpu().numpy()
@@ -669,8 +676,7 @@ def run_lodge(args):
                 q = j % S
                 if si >= 1:  # frame buffer j: its previous read-back is done
                     r.stream_of(q).wait_event(drained[j])
-                do_render(r, cam_dev[par][j], frames[j], q, v)
-                r.to_srgb8(frames[j], img8[j], slot=q)
+                do_render(r, cam_dev[par][j], frames[j], q, v, srgb8=img8[j])
                 ready[j].record(r.stream_of(q))
                 with torch.cuda.stream(copy_s[q]):
                     copy_s[q].wait_event(ready[j])
@@ -688,7 +694,8 @@ def run_lodge(args):
         e2e = {"value": total_frames / (ems / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": int(B * cams.shape[1]),
                "d2h_bytes_per_step": int(B * (H * W * 3 + STATS_BYTES)),
-               "path": "Renderer.render + to_srgb8 (8-bit sRGB like splatlod render), pinned "
+               "path": "Renderer.render(srgb8_out=...): the compositor writes the 8-bit sRGB "
+                       "image (byte for byte to_srgb8, like splatlod render's to_uint8); pinned "
                        "host camera upload and image/stats read-back every step"}
 
     # ---- gather per-rank metrics and the timed view ids over NCCL ----------

@@ -123,6 +123,10 @@ typedef struct {
   int32_t *tile_count_dev;
   int32_t *visible_dev;
   void *maxw_dev;
+  /* optional (FAST only): the 8-bit sRGB image (h, w, 3) the compositor
+   * writes as it finishes each pixel -- byte for byte lodge_to_srgb8 of the
+   * float image, which image_dev may then leave out (NULL) */
+  uint8_t *srgb8_dev;
 } lodge_frame_out;
 
 /* Per-frame scalars written by the device (lodge_render_frame /

@@ -62,7 +62,8 @@ class Chunks(C.Structure):
 
 class FrameOut(C.Structure):
     _fields_ = [("image_dev", C.c_void_p), ("tile_count_dev", C.c_void_p),
-                ("visible_dev", C.c_void_p), ("maxw_dev", C.c_void_p)]
+                ("visible_dev", C.c_void_p), ("maxw_dev", C.c_void_p),
+                ("srgb8_dev", C.c_void_p)]
 
 
 class FrameStats(C.Structure):

@@ -128,6 +128,7 @@ struct Work {
   uint32_t *union_idx;      // slots
   uint8_t *union_tag;       // slots
   uint32_t *vrank;          // LODGE_VERIFY builds: depth rank of each input (M_cap)
+  float *srgb_thr;          // 256 level thresholds of the reference's to_uint8 (lodge_to_srgb8)
   uint32_t *bl_start;       // 2 x (blocks + 1): per phase, block-list capacity offsets
   uint32_t *bl_len;         // 2 x blocks: per phase, block-list lengths
   int64_t M_cap, P_cap, status_cap, slot_cap;

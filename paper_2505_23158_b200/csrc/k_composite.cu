@@ -264,6 +264,10 @@ struct CompParams {
   // lists, their capacity offsets and lengths (k_block_lists)
   const uint64_t *blist;
   const uint32_t *bl_start, *bl_len;
+  // FAST: optional 8-bit sRGB output (lodge_frame_out.srgb8_dev) and the
+  // level thresholds of lodge_to_srgb8
+  uint8_t *srgb8;
+  const float *srgb_thr;
 };
 
 // MODE < 0: need_image / record_max from cpar.flags at run time (EXACT);
@@ -1022,12 +1026,33 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
     resume = __syncthreads_count(live_any()) > 0 && cpar.count_all[t] > e - s;
     if (resume && tid == 0) atomicOr(&cpar.alive[t >> 5], 1u << (t & 31));
   }
+  // 8-bit sRGB of the final pixels (FAST): the level thresholds in the
+  // staging buffers, free after the batch loop (no copies in flight)
+  const bool srgb = !EXACT && need_image && cpar.srgb8 != nullptr && !(PH == 1 && resume);
+  float *thr = reinterpret_cast<float *>(&S.pl[0][0]);
+  if (!EXACT && need_image && cpar.srgb8 != nullptr) {  // CTA-uniform
+    __syncthreads();
+    for (int i = tid; i < 256; i += CT) thr[i] = cpar.srgb_thr[i];
+    __syncthreads();
+  }
+  auto level = [&](float v) -> uint32_t {  // the number of thresholds <= v
+    uint32_t k = 0;
+#pragma unroll
+    for (int st = 128; st >= 1; st >>= 1) k += (v >= thr[k + st]) ? st : 0;
+    return k;
+  };
 #pragma unroll
   for (int p = 0; p < PX; ++p) {
     const int py = py0 + 2 * p;
     if (!(px < cpar.W && py < cpar.H)) continue;
     const size_t pix = (size_t)py * cpar.W + px;
     if (visible) visible[pix] = EXACT ? vis[p] : (int32_t)vf.s[p];
+    if (srgb) {  // byte for byte lodge_to_srgb8 of the clipped float image
+      uint8_t *o8 = cpar.srgb8 + 3 * pix;
+      o8[0] = (uint8_t)level(fminf(fmaxf(cru.s[p], 0.f), 1.f));
+      o8[1] = (uint8_t)level(fminf(fmaxf(cgu.s[p], 0.f), 1.f));
+      o8[2] = (uint8_t)level(fminf(fmaxf(cbu.s[p], 0.f), 1.f));
+    }
     if (PH == 1 && resume) {
       cpar.state[pix] = make_float4(Tu.s[p], cru.s[p], cgu.s[p], cbu.s[p]);
       continue;
@@ -1081,6 +1106,8 @@ static void launch_comp(const Work &w, FrameState *fs, int32_t W, int32_t H,
   cp.blist = PH ? w.pairs[PH - 1] : nullptr;
   cp.bl_start = w.bl_start + (PH == 2 ? nb + 1 : 0);
   cp.bl_len = w.bl_len + (PH == 2 ? nb : 0);
+  cp.srgb8 = EXACT ? nullptr : reinterpret_cast<uint8_t *>(out.srgb8_dev);
+  cp.srgb_thr = w.srgb_thr;
   k_composite<EXACT, MODE, PH><<<T, CC<EXACT, PH>::CT, sm, s>>>(
       w.list, PH == 2 ? w.tile_start_b : w.tile_start, PH == 2 ? w.tile_order_b : w.tile_order,
       w.payload, w.precise, fs, cp, out.image_dev, out.visible_dev, out.maxw_dev);

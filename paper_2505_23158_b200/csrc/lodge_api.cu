@@ -29,6 +29,53 @@ static int set_err(int code, const std::string &msg) {
                      std::string(#call) + ": " + cudaGetErrorString(_e));         \
   } while (0)
 
+namespace {
+// 8-bit sRGB (the reference's to_uint8, src/images.py:10-17: clip, the
+// piecewise curve in fp64, np.round) is a non-decreasing step function of
+// the fp32 input with 255 steps.  Its thresholds -- the smallest fp32 x with
+// to_uint8(x) >= k, k = 1..255 -- are found once per process by bisection
+// over fp32 bit patterns with the reference's own fp64 formula on the host
+// (libm pow, as NumPy's power), and each pixel is a binary search over them:
+// no fp64 pow per channel.  NaN and x <= 0 give 0, x >= 1 gives 255, as
+// clip does.
+static int srgb_level(float xf) {
+  const double x = std::fmin(std::fmax((double)xf, 0.0), 1.0);
+  double e;
+  if (x <= 0.0031308) {
+    e = 12.92 * x;
+  } else {
+    volatile double a = 1.055 * std::pow(x, 1.0 / 2.4);  // no contraction with the - 0.055
+    e = a - 0.055;
+  }
+  volatile double y = e * 255.0;
+  return (int)std::nearbyint(y);  // round half to even, as np.round
+}
+
+static std::vector<float> make_srgb_thresholds() {
+  std::vector<float> t(256);
+  {
+    t[0] = -INFINITY;
+    for (int k = 1; k < 256; ++k) {
+      uint32_t lo = 0u, hi = 0x3f800000u;  // f(+0) = 0 < k <= 255 = f(1)
+      while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        float xm;
+        std::memcpy(&xm, &mid, 4);
+        if (srgb_level(xm) >= k) hi = mid;
+        else lo = mid + 1;
+      }
+      std::memcpy(&t[k], &lo, 4);
+    }
+  }
+  return t;
+}
+static const float *srgb_thresholds() {
+  static const std::vector<float> t = make_srgb_thresholds();  // thread-safe, once
+  return t.data();
+}
+
+}  // namespace
+
 struct lodge_ctx {
   int device = 0;
   cudaStream_t stream = 0;
@@ -42,7 +89,6 @@ struct lodge_ctx {
   int64_t pixels_cap = 0;  // capacity of the two-phase pixel state
   int32_t phase_budget = 2048;  // first-phase pairs per tile of two-phase frames (0: one pass)
   int32_t block_lists = LODGE_BLOCK_LISTS_AUTO;  // lodge_set_block_lists
-  float *srgb_thr = nullptr;  // lodge_to_srgb8's level thresholds on this device
   int debug_sync = 0;  // LODGE_DEBUG_SYNC=1: check after every stage; 2: after each segment
   int32_t launches = 0;
   LevelSlots last_slots{};  // slot layout of the last union
@@ -163,6 +209,24 @@ static int ensure_tiles(lodge_ctx *c, int32_t W, int32_t H) {
   return 0;
 }
 
+// the per-device copy of the sRGB level thresholds, once per context
+static int ensure_srgb(lodge_ctx *c) {
+  if (c->w.srgb_thr) return 0;
+  CK(cudaMalloc(&c->w.srgb_thr, 256 * sizeof(float)));
+  CK(cudaMemcpy(c->w.srgb_thr, srgb_thresholds(), 256 * sizeof(float), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+// a frame's optional 8-bit sRGB output: FAST frames with the image flag
+static int check_srgb_out(lodge_ctx *c, int32_t flags, const lodge_frame_out *out) {
+  if (!out->srgb8_dev) return 0;
+  if (c->precision != LODGE_PREC_FAST)
+    return set_err(LODGE_ERR_BAD_ARG, "8-bit sRGB output needs FAST precision");
+  if (!(flags & LODGE_NEED_IMAGE))
+    return set_err(LODGE_ERR_BAD_ARG, "8-bit sRGB output needs LODGE_NEED_IMAGE");
+  return ensure_srgb(c);
+}
+
 static int ensure_slots(lodge_ctx *c, int64_t need) {
   Work &w = c->w;
   if (need <= w.slot_cap && w.union_idx) return 0;
@@ -252,7 +316,7 @@ void lodge_destroy(lodge_ctx *c) {
                   w.status, w.union_idx, w.union_tag, c->fs, c->cam_dev, w.rect_sorted,
                   w.splat_off, w.chunk_first, w.tile_order, w.tile_diff_a, w.count_all,
                   w.tile_start_b, w.tile_order_b, w.alive, w.sat, w.state, w.vrank,
-                  w.bl_start, w.bl_len, c->edges_dev, c->srgb_thr};
+                  w.bl_start, w.bl_len, w.srgb_thr, c->edges_dev};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c->cam_host) cudaFreeHost(c->cam_host);
@@ -391,6 +455,7 @@ int lodge_rasterize(lodge_ctx *c, const lodge_batch *b, int64_t M, int64_t n_inp
   if (rc) return rc;
   if (M < 0 || M > 0x3fffffff || n_inputs < M) return set_err(LODGE_ERR_BAD_ARG, "bad batch size");
   CK(cudaSetDevice(c->device));
+  if ((rc = check_srgb_out(c, flags, out))) return rc;
   cudaStream_t s = c->stream;
   const int32_t tiles_x = (cam->w + 15) / 16, tiles_y = (cam->h + 15) / 16;
   const int32_t T = tiles_x * tiles_y;
@@ -515,6 +580,10 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
   const bool exact = c->precision == LODGE_PREC_EXACT;
   const int64_t U_cap = ls.slot_base[ls.n_levels];
   const int32_t tiles_x = (W + 15) / 16, tiles_y = (H + 15) / 16;
+  {
+    const int rc0 = check_srgb_out(c, flags, out);
+    if (rc0) return rc0;
+  }
   c->mark(2);
   if ((flags & LODGE_RECORD_MAX) && !(flags & LODGE_ACCUMULATE_MAX) && out->maxw_dev)
     CK(cudaMemsetAsync(out->maxw_dev, 0, (exact ? 8 : 4) * (size_t)U_cap, s));
@@ -754,50 +823,6 @@ int lodge_profile_read(lodge_ctx *c, double *stage_ms, int32_t *frames) {
   return 0;
 }
 
-// 8-bit sRGB (the reference's to_uint8, src/images.py:10-17: clip, the
-// piecewise curve in fp64, np.round) is a non-decreasing step function of
-// the fp32 input with 255 steps.  Its thresholds -- the smallest fp32 x with
-// to_uint8(x) >= k, k = 1..255 -- are found once per process by bisection
-// over fp32 bit patterns with the reference's own fp64 formula on the host
-// (libm pow, as NumPy's power), and each pixel is a binary search over them:
-// no fp64 pow per channel.  NaN and x <= 0 give 0, x >= 1 gives 255, as
-// clip does.
-static int srgb_level(float xf) {
-  const double x = std::fmin(std::fmax((double)xf, 0.0), 1.0);
-  double e;
-  if (x <= 0.0031308) {
-    e = 12.92 * x;
-  } else {
-    volatile double a = 1.055 * std::pow(x, 1.0 / 2.4);  // no contraction with the - 0.055
-    e = a - 0.055;
-  }
-  volatile double y = e * 255.0;
-  return (int)std::nearbyint(y);  // round half to even, as np.round
-}
-
-static std::vector<float> make_srgb_thresholds() {
-  std::vector<float> t(256);
-  {
-    t[0] = -INFINITY;
-    for (int k = 1; k < 256; ++k) {
-      uint32_t lo = 0u, hi = 0x3f800000u;  // f(+0) = 0 < k <= 255 = f(1)
-      while (lo < hi) {
-        const uint32_t mid = lo + (hi - lo) / 2;
-        float xm;
-        std::memcpy(&xm, &mid, 4);
-        if (srgb_level(xm) >= k) hi = mid;
-        else lo = mid + 1;
-      }
-      std::memcpy(&t[k], &lo, 4);
-    }
-  }
-  return t;
-}
-static const float *srgb_thresholds() {
-  static const std::vector<float> t = make_srgb_thresholds();  // thread-safe, once
-  return t.data();
-}
-
 __global__ void __launch_bounds__(256) k_srgb8(const float *__restrict__ img, int64_t n,
                                                const float *__restrict__ thr,
                                                uint8_t *__restrict__ out) {
@@ -837,13 +862,11 @@ __global__ void __launch_bounds__(256) k_srgb8(const float *__restrict__ img, in
 int lodge_to_srgb8(lodge_ctx *c, const float *img, int64_t n, uint8_t *out) {
   if (!c || !img || !out) return set_err(LODGE_ERR_BAD_ARG, "NULL argument");
   if (n <= 0) return 0;
-  if (!c->srgb_thr) {  // the per-device copy of the thresholds, once per context
-    CK(cudaMalloc(&c->srgb_thr, 256 * sizeof(float)));
-    CK(cudaMemcpy(c->srgb_thr, srgb_thresholds(), 256 * sizeof(float), cudaMemcpyHostToDevice));
-  }
+  int rc = ensure_srgb(c);
+  if (rc) return rc;
   const int64_t quads = (3 * n + 3) / 4;
   const unsigned grid = (unsigned)std::min<int64_t>((quads + 255) / 256, 148 * 16);
-  k_srgb8<<<grid, 256, 0, c->stream>>>(img, n, c->srgb_thr, out);
+  k_srgb8<<<grid, 256, 0, c->stream>>>(img, n, c->w.srgb_thr, out);
   return check_launch("lodge_to_srgb8");
 }
 

@@ -176,14 +176,24 @@ class Renderer:
 
     def render(self, cam_row: torch.Tensor, frame: Frame, pair=None, t: float = None,
                need_image: bool = True, record_max: bool = True, slot: int = 0,
-               accumulate_max: bool = False) -> Frame:
+               accumulate_max: bool = False, srgb8_out: torch.Tensor = None,
+               float_image: bool = True) -> Frame:
         """Enqueue one frame on slot `slot`'s stream (the current stream for a
         single-slot renderer).  cam_row: one row of upload_cameras().
         pair=None: nearest two chunks chosen on device.  accumulate_max: max
         this frame's per-input weights into frame.maxw instead of resetting it
-        (a device-side max over views, src/lod.py:95-131)."""
+        (a device-side max over views, src/lod.py:95-131).  srgb8_out: a
+        (h, w, 3) uint8 device tensor the compositor fills with the 8-bit
+        sRGB image as it finishes each pixel (FAST; byte for byte to_srgb8 of
+        the float image, which float_image=False then skips writing)."""
         out = N.FrameOut()
-        out.image_dev = frame.image.data_ptr() if (need_image and frame.image is not None) else None
+        out.image_dev = (frame.image.data_ptr()
+                         if (need_image and float_image and frame.image is not None) else None)
+        if srgb8_out is not None:
+            if (srgb8_out.dtype != torch.uint8 or not srgb8_out.is_contiguous()
+                    or srgb8_out.numel() != 3 * frame.width * frame.height):
+                raise ValueError("srgb8_out must be a contiguous uint8 (h, w, 3) tensor")
+            out.srgb8_dev = srgb8_out.data_ptr()
         out.tile_count_dev = frame.tile_count.data_ptr()
         out.visible_dev = frame.visible.data_ptr()
         out.maxw_dev = frame.maxw.data_ptr() if (record_max and frame.maxw is not None) else None

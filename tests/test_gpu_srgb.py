@@ -59,3 +59,36 @@ def test_srgb8_tails_and_alignment(ctx, n, offset):
     rng = np.random.default_rng(n + offset)
     x = rng.uniform(-0.05, 1.05, 3 * n).astype(np.float32)
     assert np.array_equal(srgb8(ctx, x, offset), to_uint8(x))
+
+
+@pytest.mark.parametrize("budget", [0, 300, 2048])
+@pytest.mark.parametrize("res", [(1920, 1080), (1277, 719)])
+def test_render_srgb8_out_equals_to_srgb8(budget, res):
+    """Renderer.render(srgb8_out=...) -- the compositor's own 8-bit output,
+    one pass and two phases -- equals to_srgb8 of the float image."""
+    from fixtures import scenes
+    import paper_2505_23158_b200 as L
+    from paper_2505_23158_b200.device import DeviceLevel, DevicePlan
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    cfg = scenes.build("street1080")
+    dev = torch.device("cuda", 0)
+    levels = [DeviceLevel.from_tensors(torch.from_numpy(g).to(dev), torch.from_numpy(s).to(dev),
+                                       cfg.degree) for g, s, _ in cfg.levels]
+    plan = DevicePlan.from_arrays(cfg.centers, cfg.offsets, cfg.data, cfg.L, dev)
+    r = L.Renderer(levels, plan, storage="fp32", precision="fast", phase_budget=budget)
+    w, h = res
+    for z in (8.0, 60.0):
+        cam = scenes.camera(z, width=w, height=h, focal=scenes.FOCAL * w / 1920)
+        cams = r.upload_cameras([cam])
+        fr = r.alloc_frame(w, h)
+        r.reserve(64 << 20)
+        r.render(cams[0], fr)
+        ref = torch.empty((h, w, 3), dtype=torch.uint8, device=dev)
+        r.to_srgb8(fr, ref)
+        got = torch.zeros((h, w, 3), dtype=torch.uint8, device=dev)
+        fr2 = r.alloc_frame(w, h)
+        r.render(cams[0], fr2, srgb8_out=got, float_image=False)
+        torch.cuda.synchronize()
+        assert torch.equal(got, ref)
+        assert fr2.read_stats().fault == 0
