@@ -422,7 +422,8 @@ void launch_block_lists(const Work &w, FrameState *fs, int32_t tiles_x, int32_t 
                         int phase, cudaStream_t s);
 #ifdef LODGE_VERIFY
 // debug builds: order check of the per-tile lists of the last tile sort
-void launch_list_verify(const Work &w, FrameState *fs, uint32_t T, bool second, cudaStream_t s);
+void launch_list_verify(const Work &w, FrameState *fs, uint32_t T, bool second, cudaStream_t s,
+                        int32_t tiles_x = 0, int32_t tiles_y = 0);
 #endif
 // phase 0: one pass over the full lists; 1 / 2: the two depth phases of a
 // FAST frame (1 saves the state of unfinished tiles, 2 resumes them).

@@ -395,14 +395,84 @@ __global__ void k_list_verify(const uint32_t *list, const uint32_t *tile_start, 
   }
 }
 
+// Debug check of a phase's block lists: per block, the
+// length within the capacity, every entry an input with a nonzero mask of
+// the block's tiles (alive tiles in phase 2), depth ranks strictly
+// increasing, and for every tile of the block the number of entries with
+// its bit equal to the tile's list count.
+__device__ void k_block_list_verify_body(const uint64_t *blist, const uint32_t *bl_start,
+                                         const uint32_t *bl_len, const uint32_t *tile_start,
+                                         const uint32_t *alive, int32_t tiles_x,
+                                         int32_t tiles_y, const uint32_t *vrank, uint32_t cap,
+                                         FrameState *fs) {
+  if (fs->stats.overflow) return;
+  const uint32_t nbx = (tiles_x + BLK_W - 1) / BLK_W, nb = block_count(tiles_x, tiles_y);
+  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const uint32_t s = bl_start[b], capb = bl_start[b + 1] - s;
+    if (capb == 0) continue;  // no pairs of the phase: the block was skipped
+    const uint32_t len = bl_len[b];
+    if (len > capb) {
+      if (threadIdx.x == 0) raise_fault(fs, FAULT_LISTORD);
+      continue;
+    }
+    const uint32_t bx0 = (b % nbx) * BLK_W, by0 = (b / nbx) * BLK_H;
+    uint32_t valid = 0;  // the block's tiles inside the frame (and alive in phase 2)
+    for (int q = 0; q < BLK_W * BLK_H; ++q) {
+      const uint32_t x = bx0 + q % BLK_W, y = by0 + q / BLK_W;
+      if (x >= (uint32_t)tiles_x || y >= (uint32_t)tiles_y) continue;
+      const uint32_t t = y * tiles_x + x;
+      if (!alive || ((alive[t >> 5] >> (t & 31)) & 1u)) valid |= 1u << q;
+    }
+    for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) {
+      const uint64_t e = blist[s + i];
+      const uint32_t m = (uint32_t)(e >> 32), id = (uint32_t)e;
+      bool ok = m != 0u && (m & ~valid) == 0u && id < cap;
+      if (ok && i + 1 < len) {
+        const uint32_t id2 = (uint32_t)blist[s + i + 1];
+        ok = id2 < cap && vrank[id] < vrank[id2];
+      }
+      if (!ok) raise_fault(fs, FAULT_LISTORD);
+    }
+    for (int q = threadIdx.x; q < BLK_W * BLK_H; q += blockDim.x) {
+      if (!((valid >> q) & 1u)) continue;
+      const uint32_t t = (by0 + q / BLK_W) * tiles_x + bx0 + q % BLK_W;
+      uint32_t c = 0;
+      for (uint32_t i = 0; i < len; ++i) c += (uint32_t)(blist[s + i] >> (32 + q)) & 1u;
+      if (c != tile_start[t + 1] - tile_start[t]) raise_fault(fs, FAULT_LISTORD);
+    }
+  }
+}
+
+// the phase's block-list check, when the phase kept block lists (a device
+// flag: the kernel body runs only then)
+template <int SECOND>
+__global__ void k_block_list_verify_if(const Work w, int32_t tiles_x, int32_t tiles_y,
+                                       FrameState *fs) {
+  if (!(SECOND ? fs->scan_b : fs->scan_a)) return;
+  const uint32_t nb = (uint32_t)block_count(tiles_x, tiles_y);
+  k_block_list_verify_body(w.pairs[SECOND], w.bl_start + (SECOND ? nb + 1 : 0),
+                           w.bl_len + (SECOND ? nb : 0),
+                           SECOND ? w.tile_start_b : w.tile_start, SECOND ? w.alive : nullptr,
+                           tiles_x, tiles_y, w.vrank, (uint32_t)w.M_cap, fs);
+}
+
 void launch_list_verify(const Work &w, FrameState *fs, uint32_t T, bool second,
-                        cudaStream_t s) {
+                        cudaStream_t s, int32_t tiles_x, int32_t tiles_y) {
   if (!w.vrank) return;
   if (!second)
     k_depth_rank<<<296, 256, 0, s>>>(w.val_depth[0], w.vrank, (uint32_t)w.M_cap, fs);
   k_list_verify<<<std::min<uint32_t>(T, 148 * 8), 128, 0, s>>>(
       w.list, second ? w.tile_start_b : w.tile_start, T, w.vrank, (uint32_t)w.M_cap, fs,
       second ? 1 : 0);
+  if (tiles_x > 0) {  // two-phase frames: the phase's block lists, when it kept them
+    const uint32_t nb = (uint32_t)block_count(tiles_x, tiles_y);
+    if (second)
+      k_block_list_verify_if<1><<<std::min<uint32_t>(nb, 148 * 4), 128, 0, s>>>(
+          w, tiles_x, tiles_y, fs);
+    else
+      k_block_list_verify_if<0><<<std::min<uint32_t>(nb, 148 * 4), 128, 0, s>>>(
+          w, tiles_x, tiles_y, fs);
+  }
 }
 #endif
 

@@ -624,7 +624,7 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
     launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s, TK_TILE0, &c->fs->n_sort_a);
     launch_block_lists(w, c->fs, tiles_x, tiles_y, 1, s); ++nl;
 #ifdef LODGE_VERIFY
-    launch_list_verify(w, c->fs, (uint32_t)(tiles_x * tiles_y), false, s);
+    launch_list_verify(w, c->fs, (uint32_t)(tiles_x * tiles_y), false, s, tiles_x, tiles_y);
 #endif
     DSYNC("launch_tile_sort");
     c->mark(7);
@@ -647,7 +647,7 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
     launch_tile_sort(w, c->fs, tiles_x, tiles_y, &nl, s, TK_TILEB0, &c->fs->n_sort_b);
     launch_block_lists(w, c->fs, tiles_x, tiles_y, 2, s); ++nl;
 #ifdef LODGE_VERIFY
-    launch_list_verify(w, c->fs, (uint32_t)(tiles_x * tiles_y), true, s);
+    launch_list_verify(w, c->fs, (uint32_t)(tiles_x * tiles_y), true, s, tiles_x, tiles_y);
 #endif
     DSYNC("launch_tile_sort (second phase)");
     c->mark(9);

@@ -14,7 +14,8 @@ fails these stresses within seconds (profiles/r02_stress.md).
   frame's outputs (image, per_pixel_visible, per_tile_count, max weights)
   bit-identical to the same view rendered serially on one stream, and -- in
   a LODGE_VERIFY build, in a subprocess -- the device order checks of the
-  depth sort, every staged onesweep partition and every per-tile list silent.
+  depth sort, every staged onesweep partition, every per-tile list and
+  every block list (order, masks, per-tile counts) silent.
 """
 
 import json
