@@ -635,6 +635,7 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
     DSYNC("launch_composite");
     DSYNC_L(2, "segment: count .. first-phase composite");
     c->mark(8);
+#ifndef LODGE_DEBUG_SKIP_PHASE2  // diagnostic builds: the frame without its second phase
     launch_setup_b(w, c->fs, tiles_x, tiles_y, s);
     DSYNC("launch_setup_b");
     launch_enum_b(w, c->fs, tiles_x, tiles_y, U_cap, s);
@@ -655,6 +656,9 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
     launch_composite(w, c->fs, cam_dev, W, H, rp, flags, exact, *out, (uint32_t)U_cap, s, 2);
 #endif
     ++nl;
+#else
+    c->mark(9);
+#endif
     DSYNC("launch_composite (second phase)");
     DSYNC_L(2, "segment: second phase");
     c->mark(10);
