@@ -6,7 +6,9 @@
 // Counts come from a 2-D difference array filled by K2 (four atomics per
 // splat instead of one per pair), integrated here; the duplication kernel
 // uses a single-pass look-back scan and block-cooperative emission so one
-// huge splat (all 8160 tiles at 1080p) does not serialise a thread.
+// huge splat (all 8160 tiles at 1080p) does not serialise a thread.  A
+// depth phase of few large splats keeps per-block lists instead of pairs
+// (k_block_lists).
 #include <algorithm>
 
 #include "emit.cuh"

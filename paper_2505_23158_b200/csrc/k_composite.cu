@@ -3,20 +3,23 @@
 //
 // One CTA per 16x16 tile (heaviest tiles first).  FAST: 64 threads, 4 pixels
 // per thread, each warp owning a 16x8 pixel block; EXACT: 128 threads, 2
-// pixels per thread, 16x4 blocks.  The tile's sorted member list is consumed
-// in batches (128 members FAST, 256 EXACT) through a two-stage TMA pipeline:
-// for batch b+1 each thread issues cp.async.bulk copies of its members' 64 B
-// payloads (plus the 64 B fp64 records in EXACT mode) into the idle
-// shared-memory stage, completing on that stage's mbarrier, while the warps
-// composite batch b.  After a stage lands each member's mean is converted
-// once to tile-local fp32 in place.  Each warp then compacts (ballots) the
-// members whose ellipse can reach one of its pixel centres -- the extremum of
-// the quadratic form over the block's centre rectangle against the member's
+// pixels per thread, 16x4 blocks.  The tile's member list -- its sorted
+// per-tile list, or its members extracted from its block's list (DESIGN.md
+// 3.4) -- is consumed in batches (128 members FAST, 256 EXACT) through a
+// two-stage pipeline: for batch b+1 the threads issue 16-byte cp.async
+// copies of the members' 64 B payloads (plus the 64 B fp64 records in EXACT
+// mode) into the idle shared-memory stage, each thread arriving on that
+// stage's mbarrier when its copies land, while the warps composite batch b.
+// After a stage lands each member's mean is converted once to tile-local
+// fp32 in place.  Each warp then compacts (ballots) the members whose
+// ellipse can reach one of its pixel centres -- the extremum of the
+// quadratic form over the block's centre rectangle against the member's
 // cut-off -- and walks only those, in list order.  Warp votes stop a warp
 // when all its pixels have T < t_min and the CTA when all pixels have (the
 // reference's per-block break is the same per-pixel rule).  Per-member max
-// weights reduce in-warp with redux.sync, per CTA with shared-memory atomics,
-// then one global atomicMax on the float bits per member and batch.
+// weights reduce in-warp with redux.sync into per-warp shared slots, maxed
+// per batch, then one global atomicMax on the float bits per member and
+// batch.  An optional 8-bit sRGB image is written with the final pixels.
 //
 // FAST: fp32 FMA/MUFU.  Both skip tests of src/raster.py:356 are folded into
 // one per-splat cut-off on the quadratic form, stored with the conic in
