@@ -35,6 +35,7 @@ struct FrameState {
   // order with their tile masks; the compositor walks them instead of sorted
   // per-tile lists
   uint32_t scan_a, scan_b;            // phase 1 / phase 2 uses block lists
+  uint32_t bl_nlive[2];               // per phase: blocks with pairs (entries of bl_live)
   uint32_t n_sort_a, n_sort_b;        // pairs emitted and sorted per phase (0 with block lists)
   uint32_t fault_sticky;              // OR of every frame's stats.fault (lodge_fault_flags)
   // union reuse (lodge_chunks.uid): the pair and sizes of the union held in
@@ -131,6 +132,7 @@ struct Work {
   float *srgb_thr;          // 256 level thresholds of the reference's to_uint8 (lodge_to_srgb8)
   uint32_t *bl_start;       // 2 x (blocks + 1): per phase, block-list capacity offsets
   uint32_t *bl_len;         // 2 x blocks: per phase, block-list lengths
+  uint32_t *bl_live;        // 2 x blocks: per phase, the blocks with pairs (any order)
   int64_t M_cap, P_cap, status_cap, slot_cap;
 };
 

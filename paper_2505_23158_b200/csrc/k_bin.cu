@@ -125,12 +125,17 @@ __device__ __forceinline__ void integrate_diff(int32_t *sd, int32_t tiles_x, int
 // per-tile counts cnt(t) of block b's tiles, out[nb] = the total.  A block's
 // list holds the splats that meet it, each covering >= 1 of its tiles, so its
 // length is at most its tiles' count sum.
+// The blocks with pairs go to live[] (any order), their number to *nlive:
+// the block-list kernel takes work items over those only.
 template <typename CountFn>
 __device__ void block_offsets(CountFn cnt, int32_t tiles_x, int32_t tiles_y, uint32_t *out,
-                              uint32_t *s_sum) {
+                              uint32_t *s_sum, uint32_t *live, uint32_t *nlive) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int nbx = (tiles_x + BLK_W - 1) / BLK_W, nb = block_count(tiles_x, tiles_y);
   const int per = (nb + nt - 1) / nt, b0 = tid * per, b1 = min(nb, b0 + per);
+  __shared__ uint32_t s_nlive;
+  if (tid == 0) s_nlive = 0;
+  __syncthreads();
   uint32_t loc = 0;
   for (int b = b0; b < b1; ++b) {
     const int x0 = (b % nbx) * BLK_W, y0 = (b / nbx) * BLK_H;
@@ -139,6 +144,7 @@ __device__ void block_offsets(CountFn cnt, int32_t tiles_x, int32_t tiles_y, uin
       for (int x = x0; x < min(x0 + BLK_W, tiles_x); ++x) sum += cnt(y * tiles_x + x);
     out[b] = loc;
     loc += sum;
+    if (sum) live[atomicAdd(&s_nlive, 1u)] = (uint32_t)b;
   }
   __syncthreads();
   s_sum[tid] = loc;
@@ -152,6 +158,7 @@ __device__ void block_offsets(CountFn cnt, int32_t tiles_x, int32_t tiles_y, uin
   const uint32_t base = tid ? s_sum[tid - 1] : 0u;
   for (int b = b0; b < b1; ++b) out[b] += base;
   if (tid == nt - 1) out[nb] = s_sum[nt - 1];
+  if (tid == 0) *nlive = s_nlive;
   __syncthreads();
 }
 
@@ -167,7 +174,7 @@ __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t *dif
                                                      uint32_t *alive, uint32_t *tile_start,
                                                      uint32_t *tile_order, FrameState *fs,
                                                      int64_t P_cap, uint32_t *bl_start,
-                                                     int32_t bl_mode) {
+                                                     int32_t bl_mode, uint32_t *bl_live) {
   extern __shared__ int32_t sd[];  // (tx+1)*(ty+1), twice with diff_a
   __shared__ uint32_t h0[256], h1[256];
   __shared__ uint32_t s_sum[1024];
@@ -220,7 +227,9 @@ __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t *dif
                     (bl_mode == LODGE_BLOCK_LISTS_FORCE ||
                      (uint64_t)s_tot >= (uint64_t)LODGE_SCAN_MIN_TILES * S);
 #endif
-  if (scan) block_offsets([&](int t) { return at(lc, t); }, tiles_x, tiles_y, bl_start, s_sum);
+  if (scan)
+    block_offsets([&](int t) { return at(lc, t); }, tiles_x, tiles_y, bl_start, s_sum, bl_live,
+                  &fs->bl_nlive[0]);
   if (tid == 0) {
     fs->stats.P = P;
     fs->stats.overflow = (int64_t)P > P_cap ? 1u : 0u;
@@ -269,6 +278,9 @@ __global__ void __launch_bounds__(BL_THREADS) k_block_lists(const Work w, FrameS
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt = (1u << lane) - 1u;
   const uint32_t nbx = (tiles_x + BLK_W - 1) / BLK_W, nb = block_count(tiles_x, tiles_y);
+  const uint32_t nlive = fs->bl_nlive[PH - 1];  // blocks with pairs in this phase
+  const uint32_t *live = w.bl_live + (PH == 1 ? 0 : nb);
+  if (nlive == 0) return;
   const uint32_t n = PH == 1 ? fs->split_S : fs->n_owners_b;
   const uint32_t nch = (n + BL_CHUNK - 1) / BL_CHUNK;
   const uint64_t *__restrict__ rect = PH == 1 ? w.rect_sorted : w.rect;
@@ -282,10 +294,9 @@ __global__ void __launch_bounds__(BL_THREADS) k_block_lists(const Work w, FrameS
     __syncthreads();
     const uint32_t item = s_tk;
     __syncthreads();  // every thread has the ticket before the next is drawn
-    const uint32_t c = item / nb, b = item % nb;
+    const uint32_t c = item / nlive, b = live[item % nlive];
     if (c >= nch || c >= (uint32_t)BL_CHMAX) break;
     const uint32_t cap0 = bl_start[b], cap1 = bl_start[b + 1];
-    if (cap1 == cap0) continue;  // no pairs of this phase in the block: no members
     const uint32_t bx0 = (b % nbx) * BLK_W, by0 = (b / nbx) * BLK_H;
     const uint32_t bx1 = min(bx0 + BLK_W, (uint32_t)tiles_x) - 1,
                    by1 = min(by0 + BLK_H, (uint32_t)tiles_y) - 1;
@@ -367,7 +378,7 @@ __global__ void __launch_bounds__(1024) k_setup_b(const uint32_t *__restrict__ a
                                                   int32_t tiles_x, int32_t tiles_y,
                                                   uint32_t *tile_start, uint32_t *tile_order,
                                                   uint32_t *sat, FrameState *fs,
-                                                  uint32_t *bl_start) {
+                                                  uint32_t *bl_start, uint32_t *bl_live) {
   extern __shared__ int32_t ss[];  // (tx+1)*(ty+1) summed-area table
   __shared__ uint32_t h0[256], h1[256];
   __shared__ uint32_t s_sum[1024];
@@ -434,7 +445,7 @@ __global__ void __launch_bounds__(1024) k_setup_b(const uint32_t *__restrict__ a
   __syncthreads();
   // phase-2 block lists follow the first phase's choice (k_dup_count<true>
   // confirms it once the owners are counted)
-  if (fs->scan_a) block_offsets(cnt, tiles_x, tiles_y, bl_start, s_sum);
+  if (fs->scan_a) block_offsets(cnt, tiles_x, tiles_y, bl_start, s_sum, bl_live, &fs->bl_nlive[1]);
   if (tid == 0) {
     fs->n_alive = s_nz;
     fs->n_pairs = fs->stats.overflow ? 0u : s_tot;
@@ -766,7 +777,7 @@ void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32
   k_tile_setup<<<1, 1024, sm, s>>>(w.tile_diff, two_phase ? w.tile_diff_a : nullptr, tiles_x,
                                    tiles_y, tile_count, two_phase ? w.count_all : nullptr,
                                    two_phase ? w.alive : nullptr, w.tile_start, w.tile_order, fs,
-                                   w.P_cap, w.bl_start, bl_mode);
+                                   w.P_cap, w.bl_start, bl_mode, w.bl_live);
 }
 
 static uint32_t chunk_cap(const Work &w) { return (uint32_t)(w.P_cap / EMIT_CHUNK + 4); }
@@ -838,7 +849,8 @@ void launch_setup_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tile
   }
   k_setup_b<<<1, 1024, sm, s>>>(w.alive, w.count_all, w.tile_start, tiles_x, tiles_y,
                                 w.tile_start_b, w.tile_order_b, w.sat, fs,
-                                w.bl_start + block_count(tiles_x, tiles_y) + 1);
+                                w.bl_start + block_count(tiles_x, tiles_y) + 1,
+                                w.bl_live + block_count(tiles_x, tiles_y));
 }
 
 void launch_enum_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,

@@ -176,7 +176,8 @@ static int ensure_tiles(lodge_ctx *c, int32_t W, int32_t H) {
   Work &w = c->w;
   if (need > c->tiles_cap || !w.tile_diff) {
     void *old[] = {w.tile_diff, w.tile_start, w.tile_order, w.tile_diff_a, w.count_all,
-                   w.tile_start_b, w.tile_order_b, w.alive, w.sat, w.bl_start, w.bl_len};
+                   w.tile_start_b, w.tile_order_b, w.alive, w.sat, w.bl_start, w.bl_len,
+                   w.bl_live};
     for (void *p : old) cudaFree(p);
     c->tiles_cap = 0;
     CK(cudaMalloc(&w.tile_diff, 4 * need));
@@ -193,6 +194,7 @@ static int ensure_tiles(lodge_ctx *c, int32_t W, int32_t H) {
     // block lists: capacity offsets and lengths per phase (blocks <= tiles)
     CK(cudaMalloc(&w.bl_start, 4 * 2 * need));
     CK(cudaMalloc(&w.bl_len, 4 * 2 * need));
+    CK(cudaMalloc(&w.bl_live, 4 * 2 * need));
     c->tiles_cap = need;
   }
   {  // block-list look-back: BL_CHMAX status words per block
@@ -316,7 +318,7 @@ void lodge_destroy(lodge_ctx *c) {
                   w.status, w.union_idx, w.union_tag, c->fs, c->cam_dev, w.rect_sorted,
                   w.splat_off, w.chunk_first, w.tile_order, w.tile_diff_a, w.count_all,
                   w.tile_start_b, w.tile_order_b, w.alive, w.sat, w.state, w.vrank,
-                  w.bl_start, w.bl_len, w.srgb_thr, c->edges_dev};
+                  w.bl_start, w.bl_len, w.bl_live, w.srgb_thr, c->edges_dev};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c->cam_host) cudaFreeHost(c->cam_host);
