@@ -385,65 +385,72 @@ __global__ void __launch_bounds__(UN_THREADS) k_band_select(BandArgs a, FrameSta
                                                            uint64_t *lb_status,
                                                            uint32_t *union_idx,
                                                            uint8_t *union_tag) {
-  __shared__ uint32_t s_w[UN_THREADS / 32];
+  // item-major: item it of lane l in warp w is input part*UN_TILE +
+  // it*UN_THREADS + w*32 + l, so each load instruction of a warp reads 32
+  // consecutive records (coalesced); kept inputs are ranked over (item,
+  // warp, lane) -- index order -- by ballots and a scan of the per-(item,
+  // warp) counts
+  constexpr int NW = UN_THREADS / 32;
+  static_assert(UN_ITEMS * NW <= 64, "two (item, warp) counts per lane");
+  __shared__ uint32_t s_c[UN_ITEMS * NW];
   __shared__ uint32_t s_tk;
   const uint32_t g = take_ticket(&fs->tickets[TK_UNION0], &s_tk);
   int l = 0;
   while (l + 1 < a.L && g >= a.part_base[l + 1]) ++l;
   const uint32_t part = g - a.part_base[l];
   const int64_t n = a.n[l];
-  const int64_t i0 = (int64_t)part * UN_TILE + (int64_t)threadIdx.x * UN_ITEMS;
+  const int64_t i0 = (int64_t)part * UN_TILE;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double px = pos[0], py = pos[1], pz = pos[2];
-  uint32_t kmask = 0;
+  uint32_t bal[UN_ITEMS];
 #pragma unroll
   for (int it = 0; it < UN_ITEMS; ++it) {
-    const int64_t i = i0 + it;
+    const int64_t i = i0 + it * UN_THREADS + tid;
+    bool keep = false;
     if (i < n) {
       double mx, my, mz;
       if (a.geom32) {
-        const float *r = reinterpret_cast<const float *>(a.geom[l]) + i * 12;
-        mx = r[0]; my = r[1]; mz = r[2];
+        const float4 r = *reinterpret_cast<const float4 *>(
+            reinterpret_cast<const float *>(a.geom[l]) + i * 12);  // 48 B records: 16-B aligned
+        mx = r.x; my = r.y; mz = r.z;
       } else {
         const double *r = reinterpret_cast<const double *>(a.geom[l]) + i * 12;
-        mx = r[0]; my = r[1]; mz = r[2];
+        const double2 r01 = *reinterpret_cast<const double2 *>(r);
+        mx = r01.x; my = r01.y; mz = r[2];
       }
       const double dx = mx - px, dy = my - py, dz = mz - pz;
       const double d = sqrt((dx * dx + dy * dy) + dz * dz);
-      if (d >= a.lo[l] && d < a.hi[l]) kmask |= 1u << it;
+      keep = d >= a.lo[l] && d < a.hi[l];
     }
+    bal[it] = __ballot_sync(FULL_MASK, keep);
+    if (lane == 0) s_c[it * NW + warp] = __popc(bal[it]);
   }
-  const uint32_t kc = __popc(kmask);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t inc = kc;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
-    if (lane >= o) inc += t;
-  }
-  if (lane == 31) s_w[warp] = inc;
   __syncthreads();
-  if (warp == 0) {
-    const uint32_t wv = lane < UN_THREADS / 32 ? s_w[lane] : 0u;
-    uint32_t wi = wv;
+  if (warp == 0) {  // exclusive offsets over (item, warp), then the level's look-back
+    const uint32_t c0 = 2 * lane < UN_ITEMS * NW ? s_c[2 * lane] : 0u;
+    const uint32_t c1 = 2 * lane + 1 < UN_ITEMS * NW ? s_c[2 * lane + 1] : 0u;
+    const uint32_t v = c0 + c1;
+    uint32_t inc = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(FULL_MASK, wi, o);
-      if (lane >= o) wi += t;
+      const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
+      if (lane >= o) inc += t;
     }
-    const uint32_t total = __shfl_sync(FULL_MASK, wi, UN_THREADS / 32 - 1);
+    const uint32_t total = __shfl_sync(FULL_MASK, inc, 31);
     const uint32_t pre = lookback_warp(lb_status + a.part_base[l], part, total,
                                        fs->epoch + TK_UNION0);
-    if (lane < UN_THREADS / 32) s_w[lane] = pre + wi - wv;
+    if (2 * lane < UN_ITEMS * NW) s_c[2 * lane] = pre + inc - v;
+    if (2 * lane + 1 < UN_ITEMS * NW) s_c[2 * lane + 1] = pre + inc - v + c0;
     if (lane == 0 && (int64_t)(part + 1) * UN_TILE >= n) fs->stats.U_level[l] = pre + total;
   }
   __syncthreads();
-  uint32_t m = a.slot_base[l] + s_w[warp] + inc - kc;
+  const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
   for (int it = 0; it < UN_ITEMS; ++it) {
-    if ((kmask >> it) & 1u) {
-      union_idx[m] = (uint32_t)(i0 + it);
+    if ((bal[it] >> lane) & 1u) {
+      const uint32_t m = a.slot_base[l] + s_c[it * NW + warp] + __popc(bal[it] & lt);
+      union_idx[m] = (uint32_t)(i0 + it * UN_THREADS + tid);
       union_tag[m] = 3;
-      ++m;
     }
   }
 }
