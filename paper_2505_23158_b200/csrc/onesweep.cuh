@@ -158,7 +158,10 @@ __device__ __forceinline__ void onesweep_partition(OSmem<ITEMS, VALS, KI, (1 << 
       st_store(st + dg, st_pack(epoch, ST_PREFIX, tot));
     } else {
       st_store(st + dg, st_pack(epoch, ST_AGG, tot));
-      constexpr int LB = 8;  // partitions read per round trip
+#ifndef LODGE_OS_LB
+#define LODGE_OS_LB 8
+#endif
+      constexpr int LB = LODGE_OS_LB;  // partitions read per round trip
       int64_t q = (int64_t)part - 1;
       bool done = false;
       while (!done) {
