@@ -644,16 +644,19 @@ def run_lodge(args):
         # per parity and slot: the renders that read cam_dev[parity] are done
         # (the upload two steps later must not overwrite a camera in use)
         used = [[torch.cuda.Event() for _ in range(S)] for _ in range(2)]
-        img8 = torch.empty((B, H, W, 3), dtype=torch.uint8, device=dev)
-        img8_host = torch.empty((B, H, W, 3), dtype=torch.uint8).pin_memory()
-        st_host = torch.empty((B, STATS_BYTES), dtype=torch.uint8).pin_memory()
+        # frame and 8-bit image buffers double-buffered by step parity, so a
+        # buffer's read-back has a whole step to finish before it is reused
+        frames2 = [frames, [r.alloc_frame(W, H) for _ in range(B)]]
+        img8 = torch.empty((2, B, H, W, 3), dtype=torch.uint8, device=dev)
+        img8_host = torch.empty((2, B, H, W, 3), dtype=torch.uint8).pin_memory()
+        st_host = torch.empty((2, B, STATS_BYTES), dtype=torch.uint8).pin_memory()
         cams_host = cams.cpu()
         # read-backs on one copy stream per slot: a frame's D2H copy overlaps
-        # the next frames of its slot; frame buffer j is re-rendered only
+        # the next frames of its slot; a frame buffer is re-rendered only
         # after its previous copy completed
         copy_s = [torch.cuda.Stream(device=dev) for _ in range(S)]
-        ready = [torch.cuda.Event() for _ in range(B)]
-        drained = [torch.cuda.Event() for _ in range(B)]
+        ready = [[torch.cuda.Event() for _ in range(B)] for _ in range(2)]
+        drained = [[torch.cuda.Event() for _ in range(B)] for _ in range(2)]
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -674,15 +677,16 @@ def run_lodge(args):
                 r.stream_of(q).wait_stream(cur)
             for j, v in enumerate(blk):
                 q = j % S
-                if si >= 1:  # frame buffer j: its previous read-back is done
-                    r.stream_of(q).wait_event(drained[j])
-                do_render(r, cam_dev[par][j], frames[j], q, v, srgb8=img8[j])
-                ready[j].record(r.stream_of(q))
+                fr = frames2[par][j]
+                if si >= 2:  # this buffer's read-back two steps ago is done
+                    r.stream_of(q).wait_event(drained[par][j])
+                do_render(r, cam_dev[par][j], fr, q, v, srgb8=img8[par, j])
+                ready[par][j].record(r.stream_of(q))
                 with torch.cuda.stream(copy_s[q]):
-                    copy_s[q].wait_event(ready[j])
-                    img8_host[j].copy_(img8[j], non_blocking=True)
-                    st_host[j].copy_(frames[j].stats, non_blocking=True)
-                    drained[j].record(copy_s[q])
+                    copy_s[q].wait_event(ready[par][j])
+                    img8_host[par, j].copy_(img8[par, j], non_blocking=True)
+                    st_host[par, j].copy_(fr.stats, non_blocking=True)
+                    drained[par][j].record(copy_s[q])
             for q in range(S):
                 used[par][q].record(r.stream_of(q))
         for q in range(S):
