@@ -36,6 +36,13 @@ struct FrameState {
   // per-tile lists
   uint32_t scan_a, scan_b;            // phase 1 / phase 2 uses block lists
   uint32_t bl_nlive[2];               // per phase: blocks with pairs (entries of bl_live)
+  // two-phase frames sort only what they composite: the
+  // candidates of the first phase and the owners of the second
+  uint32_t n_cand;                    // first-phase candidates (depth bins <= sel_B)
+  uint32_t sel_B;                     // last candidate depth bin
+  uint32_t n_ocand;                   // second-phase owners found by the filter
+  uint32_t p1_g;                      // the last first-phase splat (input index) ...
+  uint64_t p1_key;                    // ... and its fp64 depth key
   uint32_t n_sort_a, n_sort_b;        // pairs emitted and sorted per phase (0 with block lists)
   uint32_t fault_sticky;              // OR of every frame's stats.fault (lodge_fault_flags)
   // union reuse (lodge_chunks.uid): the pair and sizes of the union held in
@@ -58,6 +65,7 @@ enum Ticket {
   TK_TILEB0 = 22,  //               tile passes (.. TK_TILEB0 + 1)
   TK_BLA = 24,     // block lists, phase 1
   TK_BLB = 25,     // block lists, phase 2
+  TK_OSORT0 = 26,  // second-phase owner sort passes (.. TK_OSORT0 + 3)
 };
 
 // Block lists: blocks of BLK_W x BLK_H tiles (tile bit (y % BLK_H) * BLK_W +
@@ -133,6 +141,9 @@ struct Work {
   uint32_t *bl_start;       // 2 x (blocks + 1): per phase, block-list capacity offsets
   uint32_t *bl_len;         // 2 x blocks: per phase, block-list lengths
   uint32_t *bl_live;        // 2 x blocks: per phase, the blocks with pairs (any order)
+  uint32_t *sel_hist;       // SEL_BINS: pair counts per depth bin (zero between frames)
+  uint32_t *sel_keys, *sel_vals;  // M_cap each: candidates / owners to sort (any order)
+  uint32_t *sort_scr[4];    // M_cap each: subset-sort ping-pong (keys 0, 1; values 0, 1)
   int64_t M_cap, P_cap, status_cap, slot_cap;
 };
 
@@ -397,6 +408,23 @@ void launch_import_batch(const lodge_batch &b, int64_t M, const Work &w, FrameSt
 // dropped by the first pass) and val_depth[1] the positions.
 void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
                        cudaStream_t s, bool compacted = false);
+// The same sort of *n_ptr (32-bit key, input index) pairs from kin / vin
+// (any order) into vout (input indices in (fp64 depth, index) order), with
+// explicit ping-pong buffers and ticket slots tk0 .. tk0 + 3.
+void launch_subset_sort(const Work &w, FrameState *fs, int64_t cap, const uint32_t *n_ptr,
+                        const uint32_t *kin, const uint32_t *vin, uint32_t *ks0, uint32_t *ks1,
+                        uint32_t *vs0, uint32_t *vs1, uint32_t *vout, int tk0,
+                        int32_t *launches, cudaStream_t s);
+// Two-phase frames: the first-phase candidates -- the survivors in the depth
+// bins whose preceding bins hold fewer than `budget` pairs -- into sel_keys /
+// sel_vals (n_cand of them); and, after the first phase, the second-phase
+// owners (survivors after the first phase that meet an alive tile).
+constexpr int SEL_SHIFT = 20;                // depth bins: the top 12 bits of the 32-bit key
+constexpr int SEL_BINS = 1 << (32 - SEL_SHIFT);  // (an eighth of an octave each)
+void launch_depth_select(const Work &w, FrameState *fs, int64_t M_cap, uint32_t budget,
+                         cudaStream_t s);
+void launch_owner_filter(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_cap,
+                         cudaStream_t s);
 void launch_depth_sort64(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
                          cudaStream_t s);
 void launch_debug_depth_sort(const Work &w, FrameState *fs, const uint64_t *keys, uint32_t n,
@@ -406,7 +434,8 @@ void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32
                        int32_t bl_mode = LODGE_BLOCK_LISTS_AUTO);
 // two-phase frames: first-phase pair budget of the counting pass
 void launch_dup_count(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
-                      int64_t M_cap, uint32_t budget, cudaStream_t s);
+                      int64_t M_cap, uint32_t budget, cudaStream_t s,
+                      const uint32_t *n_ptr = nullptr /* &fs->stats.M */);
 void launch_dup_emit(const Work &w, FrameState *fs, int32_t tiles_x, cudaStream_t s,
                      bool first_phase);
 void launch_setup_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,

@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(1024) k_tile_setup(int32_t *diff, int32_t *dif
 // the tile's list of the emission + stable tile sort (reference
 // src/raster.py:401-425), which the compositor extracts as it goes.
 // Phase 1: the depth-ordered splats [0, split_S) (rect_sorted, val_depth[0]);
-// phase 2: the owners of k_dup_count<true> (rect, val_depth[1]), their
+// phase 2: the owners of k_dup_count<true> (rect_sorted, val_depth[1]), their
 // rectangles clipped to the alive tiles (the phase-2 members of an alive
 // tile are unchanged by the clip).  Work items are (chunk of BL_CHUNK
 // splats, block) in ticket order, chunk-major; a chunk's offset in its
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(BL_THREADS) k_block_lists(const Work w, FrameS
   if (nlive == 0) return;
   const uint32_t n = PH == 1 ? fs->split_S : fs->n_owners_b;
   const uint32_t nch = (n + BL_CHUNK - 1) / BL_CHUNK;
-  const uint64_t *__restrict__ rect = PH == 1 ? w.rect_sorted : w.rect;
+  const uint64_t *__restrict__ rect = w.rect_sorted;  // depth order (phase 2: the owners, clipped)
   const uint32_t *__restrict__ ids = PH == 1 ? w.val_depth[0] : w.val_depth[1];
   const uint32_t *bl_start = w.bl_start + (PH == 1 ? 0 : nb + 1);
   uint32_t *bl_len = w.bl_len + (PH == 1 ? 0 : nb);
@@ -474,19 +474,21 @@ __device__ __forceinline__ bool rect_alive(const uint32_t *__restrict__ sat, uin
 // splat's pair range the splat that owns it (the emission CTAs' splitters).
 // Two-phase frames: budget > 0 makes the splats whose pairs start before it
 // the first phase (their rectangles go to the tile_diff_a difference array;
-// split_S and P_A record the split).  SECOND: the enumeration of the second
-// phase over splats [split_S, M) -- only the splats that meet an alive tile,
-// their rectangles clipped to the alive tiles' bounding box, compacted in
-// depth order (a second look-back) into the owner list the emission reads:
-// rectangles in w.rect, ids in w.val_depth[1] (both dead by then), pair
-// offsets and splitters over that list.
+// split_S and P_A record the split; the splats are the depth-sorted
+// first-phase candidates, *n_ptr of them).  SECOND: the second phase's
+// owners -- the depth-sorted output of launch_owner_filter, which kept the
+// later splats that meet an alive tile -- with their rectangles clipped to
+// the alive tiles' bounding box (into rect_sorted), pair offsets and
+// splitters over that list (the same clip and alive test re-run: every
+// owner passes, so the compaction is the identity).
 template <bool SECOND>
 __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__restrict__ order,
                                                            const uint64_t *__restrict__ rect,
                                                            Work w, FrameState *fs,
                                                            uint32_t budget, int32_t tiles_x,
                                                            uint32_t chunk_cap, int32_t tiles_y,
-                                                           int32_t diff_smem) {
+                                                           int32_t diff_smem,
+                                                           const uint32_t *n_ptr) {
   // first phase: the CTAs holding first-phase splats add their rectangles to
   // a CTA-private difference array (dynamic shared memory, when it fits),
   // flushed once -- the few CTAs at the front of the depth order otherwise
@@ -500,17 +502,12 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
   if (tid == 0) s_part = atomicAdd(&fs->tickets[TK], 1u);
   __syncthreads();
   const uint32_t part = s_part;
-  const uint32_t S = SECOND ? fs->split_S : 0u;
-  const uint32_t M = fs->stats.overflow ? S : fs->stats.M;
-  const uint32_t n = M - S;
+  const uint32_t n = SECOND ? (fs->stats.overflow ? 0u : fs->n_ocand) : *n_ptr;
   const uint32_t r0 = part * (DUP_THREADS * IT) + tid * IT;
   if (part * (DUP_THREADS * IT) >= n) return;
   uint32_t c[IT];
   uint64_t rc[IT];
-  if (SECOND) {
-#pragma unroll
-    for (int i = 0; i < IT; ++i) rc[i] = (r0 + i < n) ? w.rect_sorted[S + r0 + i] : 0ull;
-  } else {
+  {
     uint32_t m[IT];
     if (r0 + IT <= n) {  // order is 16-byte aligned and r0 a multiple of IT
 #pragma unroll
@@ -603,10 +600,7 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
     const uint32_t q = SECOND ? k : r;
     if (own) {
       w.splat_off[q] = off;
-      if (SECOND) {
-        w.rect[q] = rc[i];
-        w.val_depth[1][q] = order[S + r];
-      }
+      if (SECOND) w.rect_sorted[q] = rc[i];  // (order is already the owner list)
       for (uint32_t kk = (off + EMIT_CHUNK - 1) / EMIT_CHUNK;
            kk * EMIT_CHUNK < off + c[i] && kk < chunk_cap; ++kk)
         w.chunk_first[kk] = q;
@@ -633,6 +627,9 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
         fs->split_S = r + 1;
         fs->stats.M_first = r + 1;
         fs->P_A = off + c[i];
+        const uint32_t g = order[r];  // the last first-phase splat (launch_owner_filter)
+        fs->p1_g = g;
+        fs->p1_key = w.key_depth[0][g];
       }
     }
     if (valid) {
@@ -712,9 +709,9 @@ __global__ void __launch_bounds__(DUP_THREADS) k_emit_b(const uint32_t *__restri
   const uint32_t j1 = min(j0 + (uint32_t)EB_CHUNK, Pe);
   uint32_t r0, r1;
   emit_owners(w, j0, j1, Pe, n, r0, r1);
-  Work wb = w;  // the compacted owner list of k_dup_count<true>
-  wb.rect_sorted = w.rect;
-  emit_stage(E, w.val_depth[1], wb, j0, j1, r0, r1, fs);  // ends with a barrier
+  // the owner list of k_dup_count<true>: ids in val_depth[1], clipped
+  // rectangles in rect_sorted
+  emit_stage(E, w.val_depth[1], w, j0, j1, r0, r1, fs);  // ends with a barrier
   uint64_t key[EB_ITEMS];
   uint32_t keep = 0;
 #pragma unroll
@@ -765,6 +762,181 @@ __global__ void __launch_bounds__(DUP_THREADS) k_emit_b(const uint32_t *__restri
   }
 }
 
+// ---- two-phase frames: sort only what is composited ------
+// The first phase is the depth-order prefix of the survivors whose pair
+// ranges start before `budget`; a survivor in depth bin b (the top 16 bits of
+// its 32-bit key, monotone in the depth) starts at or after the pairs of all
+// earlier bins, so only the bins whose preceding bins hold fewer than
+// `budget` pairs can contribute: those survivors are the candidates, sorted
+// and counted instead of all M.  The second phase's owners are found among
+// the survivors after the first phase's last splat directly (the alive-tile
+// test of k_dup_count<true>), then sorted.
+constexpr int SEL_ITEMS = 8;  // survivors per thread and CTA step (compaction kernels)
+
+// pairs per depth bin: a CTA-private histogram in shared memory, flushed
+// once (global atomics on the few bins that hold most survivors serialised)
+__global__ void __launch_bounds__(256) k_sel_hist(const Work w, const FrameState *fs) {
+  __shared__ uint32_t h[SEL_BINS];
+  for (int i = threadIdx.x; i < SEL_BINS; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const uint32_t M = fs->stats.M;
+  const uint32_t *__restrict__ keys = depth_keys_compact(w);
+  const uint32_t *__restrict__ ids = w.val_depth[1];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < M; i += gridDim.x * blockDim.x) {
+    const uint64_t rc = w.rect[ids[i]];
+    const uint32_t x0 = rc & 0xffff, x1 = (rc >> 16) & 0xffff, y0 = (rc >> 32) & 0xffff,
+                   y1 = rc >> 48;
+    atomicAdd(&h[keys[i] >> SEL_SHIFT], (x1 - x0 + 1) * (y1 - y0 + 1));
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < SEL_BINS; i += blockDim.x)
+    if (h[i]) atomicAdd(&w.sel_hist[i], h[i]);
+}
+
+// one CTA: the last bin whose preceding bins hold fewer than `budget` pairs
+// (every bin when the total stays below it); the bins are re-zeroed
+__global__ void __launch_bounds__(1024) k_sel_scan(const Work w, FrameState *fs,
+                                                   uint32_t budget) {
+  constexpr int PER = SEL_BINS / 1024;
+  static_assert(PER % 4 == 0, "vector loads of the bins");
+  __shared__ uint32_t s_sum[1024];
+  __shared__ uint32_t s_B;
+  const int tid = threadIdx.x;
+  uint32_t *h = w.sel_hist + tid * PER;
+  uint32_t v[PER];
+  uint32_t loc = 0;
+#pragma unroll
+  for (int q = 0; q < PER / 4; ++q) {
+    const uint4 u = reinterpret_cast<const uint4 *>(h)[q];
+    v[4 * q] = u.x; v[4 * q + 1] = u.y; v[4 * q + 2] = u.z; v[4 * q + 3] = u.w;
+    loc += (u.x + u.y) + (u.z + u.w);
+    reinterpret_cast<uint4 *>(h)[q] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  if (tid == 0) s_B = 0;
+  s_sum[tid] = loc;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const uint32_t t = tid >= o ? s_sum[tid - o] : 0u;
+    __syncthreads();
+    s_sum[tid] += t;
+    __syncthreads();
+  }
+  uint32_t cum = tid ? s_sum[tid - 1] : 0u;  // pairs of the bins before this thread's
+  int last = -1;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    if (cum < budget) last = tid * PER + q;
+    cum += v[q];
+  }
+  if (last >= 0) atomicMax(&s_B, (uint32_t)last);
+  __syncthreads();
+  if (tid == 0) fs->sel_B = s_B;
+}
+
+// CTA-aggregated append of the flagged survivors (32-bit key, input index)
+// into sel_keys / sel_vals at *count (the order is free: they are sorted)
+template <typename Keep>
+__device__ __forceinline__ void sel_compact(const Work &w, uint32_t M, uint32_t *count,
+                                            Keep keep) {
+  __shared__ uint32_t s_w[8], s_base;
+  const uint32_t *__restrict__ keys = depth_keys_compact(w);
+  const uint32_t *__restrict__ ids = w.val_depth[1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr uint32_t STEP = 256 * SEL_ITEMS;
+  for (uint32_t b = blockIdx.x * STEP; b < M; b += gridDim.x * STEP) {
+    uint32_t k[SEL_ITEMS], g[SEL_ITEMS], m = 0;
+#pragma unroll
+    for (int it = 0; it < SEL_ITEMS; ++it) {
+      const uint32_t i = b + it * 256 + tid;
+      k[it] = i < M ? keys[i] : 0u;
+      g[it] = i < M ? ids[i] : 0u;
+      if (i < M && keep(k[it], g[it])) m |= 1u << it;
+    }
+    const uint32_t cnt = __popc(m);
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t tot = 0;
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t v = s_w[q];
+        s_w[q] = tot;
+        tot += v;
+      }
+      s_base = tot ? atomicAdd(count, tot) : 0u;
+    }
+    __syncthreads();
+    uint32_t at = s_base + s_w[warp] + inc - cnt;
+#pragma unroll
+    for (int it = 0; it < SEL_ITEMS; ++it)
+      if ((m >> it) & 1u) {
+        if (at < (uint32_t)w.M_cap) {
+          w.sel_keys[at] = k[it];
+          w.sel_vals[at] = g[it];
+        }
+        ++at;
+      }
+    __syncthreads();  // s_w / s_base reused
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sel_compact(const Work w, FrameState *fs) {
+  const uint32_t B = fs->sel_B;
+  sel_compact(w, fs->stats.M, &fs->n_cand,
+              [&](uint32_t k, uint32_t) { return (k >> SEL_SHIFT) <= B; });
+}
+
+// the second phase's owners: survivors after the first phase's last splat in
+// (fp64 depth, index) order whose rectangle, clipped to the alive tiles'
+// bounding box, contains an alive tile
+__global__ void __launch_bounds__(256) k_owner_filter(const Work w, FrameState *fs,
+                                                      int32_t tiles_x) {
+  if (fs->stats.overflow) return;
+  const uint32_t S = fs->split_S;
+  const uint64_t bkey = fs->p1_key;
+  const uint32_t bg = fs->p1_g;
+  const uint32_t ax0 = fs->alive_box[0], ax1 = fs->alive_box[1], ay0 = fs->alive_box[2],
+                 ay1 = fs->alive_box[3];
+  sel_compact(w, fs->stats.M, &fs->n_ocand, [&](uint32_t, uint32_t g) {
+    if (S > 0) {
+      const uint64_t fk = w.key_depth[0][g];
+      if (fk < bkey || (fk == bkey && g <= bg)) return false;  // a first-phase splat
+    }
+    const uint64_t rc = w.rect[g];
+    const uint32_t x0 = max((uint32_t)(rc & 0xffff), ax0), x1 = min((uint32_t)((rc >> 16) & 0xffff), ax1);
+    const uint32_t y0 = max((uint32_t)((rc >> 32) & 0xffff), ay0), y1 = min((uint32_t)(rc >> 48), ay1);
+    if (x0 > x1 || y0 > y1) return false;
+    const uint64_t cr = (uint64_t)x0 | ((uint64_t)x1 << 16) | ((uint64_t)y0 << 32) |
+                        ((uint64_t)y1 << 48);
+    return rect_alive(w.sat, cr, tiles_x);
+  });
+}
+
+static unsigned sel_grid(int64_t M_cap) {
+  return (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>((M_cap + 256 * SEL_ITEMS - 1) / (256 * SEL_ITEMS), 148 * 8));
+}
+
+void launch_depth_select(const Work &w, FrameState *fs, int64_t M_cap, uint32_t budget,
+                         cudaStream_t s) {
+  if (M_cap <= 0) return;
+  const unsigned hgrid = (unsigned)std::min<int64_t>((M_cap + 4095) / 4096, 148 * 2);
+  k_sel_hist<<<hgrid, 256, 0, s>>>(w, fs);
+  k_sel_scan<<<1, 1024, 0, s>>>(w, fs, budget);
+  k_sel_compact<<<sel_grid(M_cap), 256, 0, s>>>(w, fs);
+}
+
+void launch_owner_filter(const Work &w, FrameState *fs, int32_t tiles_x, int64_t M_cap,
+                         cudaStream_t s) {
+  if (M_cap <= 0) return;
+  k_owner_filter<<<sel_grid(M_cap), 256, 0, s>>>(w, fs, tiles_x);
+}
+
 void launch_tile_setup(const Work &w, FrameState *fs, int32_t *tile_count, int32_t tiles_x,
                        int32_t tiles_y, cudaStream_t s, bool two_phase, int32_t bl_mode) {
   const size_t nd = (size_t)(tiles_x + 1) * (tiles_y + 1) * 4;
@@ -784,7 +956,7 @@ static uint32_t chunk_cap(const Work &w) { return (uint32_t)(w.P_cap / EMIT_CHUN
 
 constexpr size_t DUP_DIFF_SMEM_MAX = 64 * 1024;  // CTA-private first-phase difference array
 void launch_dup_count(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles_y,
-                      int64_t M_cap, uint32_t budget, cudaStream_t s) {
+                      int64_t M_cap, uint32_t budget, cudaStream_t s, const uint32_t *n_ptr) {
   if (M_cap <= 0) return;
   const unsigned grid =
       (unsigned)((M_cap + DUP_THREADS * COUNT_ITEMS - 1) / (DUP_THREADS * COUNT_ITEMS));
@@ -796,7 +968,8 @@ void launch_dup_count(const Work &w, FrameState *fs, int32_t tiles_x, int32_t ti
     attr() = (int64_t)sm;
   }
   k_dup_count<false><<<grid, DUP_THREADS, priv ? sm : 0, s>>>(
-      w.val_depth[0], w.rect, w, fs, budget, tiles_x, chunk_cap(w), tiles_y, priv ? 1 : 0);
+      w.val_depth[0], w.rect, w, fs, budget, tiles_x, chunk_cap(w), tiles_y, priv ? 1 : 0,
+      n_ptr ? n_ptr : &fs->stats.M);
 }
 
 // Resident CTAs of a kernel on this device (persistent grids).
@@ -858,8 +1031,9 @@ void launch_enum_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles
   if (M_cap <= 0) return;
   const unsigned grid =
       (unsigned)((M_cap + DUP_THREADS * COUNT_ITEMS - 1) / (DUP_THREADS * COUNT_ITEMS));
-  k_dup_count<true><<<grid, DUP_THREADS, 0, s>>>(w.val_depth[0], w.rect, w, fs, 0u, tiles_x,
-                                                 chunk_cap(w), tiles_y, 0);
+  // the owners, depth-sorted by launch_owner_filter + launch_subset_sort
+  k_dup_count<true><<<grid, DUP_THREADS, 0, s>>>(w.val_depth[1], w.rect, w, fs, 0u, tiles_x,
+                                                 chunk_cap(w), tiles_y, 0, nullptr);
   static PerDevice res;
   constexpr size_t sm = sizeof(EmitSmem<EB_CHUNK>);
   if (!res()) {

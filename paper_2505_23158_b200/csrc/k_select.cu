@@ -532,6 +532,8 @@ __global__ void k_begin_frame(FrameState *fs) {
     fs->P_A = 0;
     fs->n_alive = 0;
     fs->n_owners_b = 0;
+    fs->n_cand = fs->n_ocand = 0;
+    fs->sel_B = 0;
     fs->scan_a = fs->scan_b = 0;
     fs->n_sort_a = fs->n_sort_b = 0;
     fs->stats.f = -1;  // set by k_select_frame on the chunk paths

@@ -175,11 +175,11 @@ __global__ void __launch_bounds__(OS_THREADS, LODGE_OS_VMINB)
 template <bool COMPACT>
 __global__ void __launch_bounds__(256) k_depth_hist32(const uint64_t *__restrict__ keys,
                                                      const uint32_t *__restrict__ keys32,
-                                                     FrameState *fs) {
+                                                     const uint32_t *n_ptr, FrameState *fs) {
   __shared__ uint32_t h[4][256];
   for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
   __syncthreads();
-  const uint32_t n = COMPACT ? fs->stats.M : fs->n_sort;
+  const uint32_t n = COMPACT ? *n_ptr : fs->n_sort;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     uint32_t k32;
     if (COMPACT) {
@@ -212,8 +212,8 @@ __global__ void __launch_bounds__(256) k_depth_ties(const uint32_t *__restrict__
                                                     const uint32_t *__restrict__ vin,
                                                     const uint64_t *__restrict__ full,
                                                     uint32_t *__restrict__ vout,
-                                                    FrameState *fs) {
-  const uint32_t M = fs->stats.M;
+                                                    const uint32_t *n_ptr) {
+  const uint32_t M = *n_ptr;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < M; i += gridDim.x * blockDim.x) {
     const uint32_t k = k32[i];
     const uint32_t gi = vin[i];
@@ -339,8 +339,8 @@ __global__ void k_pass_verify(const uint32_t *kout, const uint32_t *vout, const 
 // Debug check of the frame depth order: keys non-decreasing, every value an
 // input whose own key is the sorted key.
 __global__ void k_depth_verify(const uint32_t *k32, const uint32_t *val, const uint64_t *full,
-                               FrameState *fs) {
-  const uint32_t M = fs->stats.M, U = fs->n_sort;
+                               const uint32_t *n_ptr, FrameState *fs) {
+  const uint32_t M = *n_ptr, U = fs->n_sort;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < M; i += gridDim.x * blockDim.x) {
     const uint32_t g = val[i];
     bool ok = g < U && depth_key32(full[g]) == k32[i];
@@ -368,8 +368,8 @@ __global__ void k_depth_verify64(const uint64_t *k, const uint32_t *val, FrameSt
 // depth)) restricted to the tile, src/raster.py:401-423), and the list
 // ranges must lie inside the sorted pairs.
 __global__ void k_depth_rank(const uint32_t *val, uint32_t *vrank, uint32_t cap,
-                             FrameState *fs) {
-  const uint32_t M = fs->stats.M;
+                             const uint32_t *n_ptr, FrameState *fs) {
+  const uint32_t M = *n_ptr;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < M; i += gridDim.x * blockDim.x) {
     const uint32_t g = val[i];
     if (g < cap) vrank[g] = i;
@@ -459,8 +459,14 @@ __global__ void k_block_list_verify_if(const Work w, int32_t tiles_x, int32_t ti
 void launch_list_verify(const Work &w, FrameState *fs, uint32_t T, bool second,
                         cudaStream_t s, int32_t tiles_x, int32_t tiles_y) {
   if (!w.vrank) return;
+  // depth ranks of the phase's members: the first phase's (or the one
+  // pass's) sorted survivors, the second phase's sorted owners
   if (!second)
-    k_depth_rank<<<296, 256, 0, s>>>(w.val_depth[0], w.vrank, (uint32_t)w.M_cap, fs);
+    k_depth_rank<<<296, 256, 0, s>>>(w.val_depth[0], w.vrank, (uint32_t)w.M_cap,
+                                     tiles_x > 0 ? &fs->n_cand : &fs->stats.M, fs);
+  else
+    k_depth_rank<<<296, 256, 0, s>>>(w.val_depth[1], w.vrank, (uint32_t)w.M_cap,
+                                     &fs->n_owners_b, fs);
   k_list_verify<<<std::min<uint32_t>(T, 148 * 8), 128, 0, s>>>(
       w.list, second ? w.tile_start_b : w.tile_start, T, w.vrank, (uint32_t)w.M_cap, fs,
       second ? 1 : 0);
@@ -479,25 +485,15 @@ void launch_list_verify(const Work &w, FrameState *fs, uint32_t T, bool second,
 // Frames: four passes over 32-bit keys (u32 ping-pong in the two halves of
 // key_depth[1]; key_depth[0] keeps the full keys by input index for the tie
 // repair), sorted input indices in val_depth[0].
-void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
-                       cudaStream_t s, bool compacted) {
-  if (M_cap <= 0) return;
-#ifdef LODGE_DEPTH64
-  // opt-in: the eight 64-bit passes (0.17 vs 0.12 ms per config-3 frame),
-  // which take their input values in val_depth[0]
-  cudaMemcpyAsync(w.val_depth[0], w.val_depth[1], 4 * (size_t)M_cap, cudaMemcpyDeviceToDevice, s);
-  launch_depth_sort64(w, fs, M_cap, launches, s);
-  return;
-#endif
-  int hist_blocks = (int)((M_cap + 1023) / 1024);
-  if (hist_blocks > 148 * 4) hist_blocks = 148 * 4;
-  uint32_t *k32[2] = {depth_keys32(w, 0), depth_keys32(w, 1)};
-  if (compacted) {
-    hist_blocks = std::max(1, hist_blocks / 2);  // 4 B per key instead of 8
-    k_depth_hist32<true><<<hist_blocks, 256, 0, s>>>(nullptr, k32[1], fs);
-  } else {
-    k_depth_hist32<false><<<hist_blocks, 256, 0, s>>>(w.key_depth[0], nullptr, fs);
-  }
+void launch_subset_sort(const Work &w, FrameState *fs, int64_t cap, const uint32_t *n_ptr,
+                        const uint32_t *kin, const uint32_t *vin, uint32_t *ks0, uint32_t *ks1,
+                        uint32_t *vs0, uint32_t *vs1, uint32_t *vout, int tk0,
+                        int32_t *launches, cudaStream_t s) {
+  if (cap <= 0) return;
+  cudaMemsetAsync(fs->hist_depth, 0, sizeof(uint32_t) * 4 * 256, s);  // (a frame may sort twice)
+  int hist_blocks = (int)((cap + 2047) / 2048);
+  if (hist_blocks > 148 * 2) hist_blocks = 148 * 2;
+  k_depth_hist32<true><<<hist_blocks, 256, 0, s>>>(nullptr, kin, n_ptr, fs);
   k_depth_scan<<<1, 256, 0, s>>>(fs);
   *launches += 2;
   constexpr int64_t TILE = (int64_t)OS_THREADS * LODGE_OS_ITEMS_D;
@@ -509,21 +505,69 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
                          (int)sm);
     res() = resident_grid(k_depth_pass<true>, OS_THREADS, sm, 1 << 30);
   }
-  const int64_t resident = res();
+  const unsigned grid = (unsigned)std::min<int64_t>((cap + TILE - 1) / TILE,
+                                                    LODGE_PERSIST ? res() : 0x7fffffff);
+  // keys kin -> ks0 -> ks1 -> ks0 -> ks1, values vin -> vs0 -> vs1 -> vs0 -> vs1,
+  // then the tie repair vs1 -> vout
+  const uint32_t *ki[4] = {kin, ks0, ks1, ks0};
+  uint32_t *ko[4] = {ks0, ks1, ks0, ks1};
+  const uint32_t *vi[4] = {vin, vs0, vs1, vs0};
+  uint32_t *vo[4] = {vs0, vs1, vs0, vs1};
+  for (int p = 0; p < 4; ++p) {
+    k_depth_pass<false><<<grid, OS_THREADS, sm, s>>>(nullptr, ki[p], ko[p], vi[p], vo[p], n_ptr,
+                                                     8 * p, fs->off_depth[p], w.status, fs,
+                                                     tk0 + p);
+#ifdef LODGE_VERIFY
+    k_pass_verify<<<296, 256, 0, s>>>(ko[p], vo[p], w.key_depth[0], n_ptr, 8 * p, p, fs);
+#endif
+  }
+  const unsigned tgrid = (unsigned)std::min<int64_t>((cap + 255) / 256, 148 * 8);
+  k_depth_ties<<<tgrid, 256, 0, s>>>(ks1, vs1, w.key_depth[0], vout, n_ptr);
+#ifdef LODGE_VERIFY
+  k_depth_verify<<<296, 256, 0, s>>>(ks1, vout, w.key_depth[0], n_ptr, fs);
+#endif
+  *launches += 5;
+}
+
+// Frames: four passes over 32-bit keys (u32 ping-pong in the two halves of
+// key_depth[1]; key_depth[0] keeps the full keys by input index for the tie
+// repair), sorted input indices in val_depth[0].
+void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *launches,
+                       cudaStream_t s, bool compacted) {
+  if (M_cap <= 0) return;
+#ifdef LODGE_DEPTH64
+  // opt-in: the eight 64-bit passes (0.17 vs 0.12 ms per config-3 frame),
+  // which take their input values in val_depth[0]
+  cudaMemcpyAsync(w.val_depth[0], w.val_depth[1], 4 * (size_t)M_cap, cudaMemcpyDeviceToDevice, s);
+  launch_depth_sort64(w, fs, M_cap, launches, s);
+  return;
+#endif
+  uint32_t *k32[2] = {depth_keys32(w, 0), depth_keys32(w, 1)};
+  if (compacted) {  // the projection's compacted survivors (keys in k32[1], values val_depth[1])
+    launch_subset_sort(w, fs, M_cap, &fs->stats.M, k32[1], w.val_depth[1], k32[0], k32[1],
+                       w.val_depth[0], w.val_depth[1], w.val_depth[0], TK_DEPTH0, launches, s);
+    return;
+  }
+  int hist_blocks = (int)((M_cap + 1023) / 1024);
+  if (hist_blocks > 148 * 4) hist_blocks = 148 * 4;
+  k_depth_hist32<false><<<hist_blocks, 256, 0, s>>>(w.key_depth[0], nullptr, nullptr, fs);
+  k_depth_scan<<<1, 256, 0, s>>>(fs);
+  *launches += 2;
+  constexpr int64_t TILE = (int64_t)OS_THREADS * LODGE_OS_ITEMS_D;
+  const size_t sm = sizeof(OSmem<LODGE_OS_ITEMS_D, true, uint32_t, 256>);
+  static PerDevice res;
+  if (!res()) {
+    cudaFuncSetAttribute(k_depth_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_depth_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    res() = resident_grid(k_depth_pass<true>, OS_THREADS, sm, 1 << 30);
+  }
   const unsigned grid = (unsigned)std::min<int64_t>((M_cap + TILE - 1) / TILE,
-                                                    LODGE_PERSIST ? resident : 0x7fffffff);
-  // keys 0: u64 (or the compacted k32[1]) -> k32[0], 1: k32[0] -> k32[1],
-  // 2: k32[1] -> k32[0], 3: k32[0] -> k32[1]
-  // values (input in val_depth[1]): [1] -> [0] -> [1] -> [0] -> [1], then
-  // the tie repair [1] -> [0]
-  if (compacted)
-    k_depth_pass<false><<<grid, OS_THREADS, sm, s>>>(nullptr, k32[1], k32[0], w.val_depth[1],
-                                                     w.val_depth[0], &fs->stats.M, 0,
-                                                     fs->off_depth[0], w.status, fs, TK_DEPTH0);
-  else
-    k_depth_pass<true><<<grid, OS_THREADS, sm, s>>>(w.key_depth[0], nullptr, k32[0],
-                                                    w.val_depth[1], w.val_depth[0], &fs->n_sort,
-                                                    0, fs->off_depth[0], w.status, fs, TK_DEPTH0);
+                                                    LODGE_PERSIST ? res() : 0x7fffffff);
+  // keys 0: u64 -> k32[0], then as launch_subset_sort; values from val_depth[1]
+  k_depth_pass<true><<<grid, OS_THREADS, sm, s>>>(w.key_depth[0], nullptr, k32[0],
+                                                  w.val_depth[1], w.val_depth[0], &fs->n_sort,
+                                                  0, fs->off_depth[0], w.status, fs, TK_DEPTH0);
 #ifdef LODGE_VERIFY
   k_pass_verify<<<296, 256, 0, s>>>(k32[0], w.val_depth[0], w.key_depth[0], &fs->stats.M, 0, 0,
                                     fs);
@@ -539,9 +583,10 @@ void launch_depth_sort(const Work &w, FrameState *fs, int64_t M_cap, int32_t *la
 #endif
   }
   const unsigned tgrid = (unsigned)std::min<int64_t>((M_cap + 255) / 256, 148 * 8);
-  k_depth_ties<<<tgrid, 256, 0, s>>>(k32[1], w.val_depth[1], w.key_depth[0], w.val_depth[0], fs);
+  k_depth_ties<<<tgrid, 256, 0, s>>>(k32[1], w.val_depth[1], w.key_depth[0], w.val_depth[0],
+                                     &fs->stats.M);
 #ifdef LODGE_VERIFY
-  k_depth_verify<<<296, 256, 0, s>>>(k32[1], w.val_depth[0], w.key_depth[0], fs);
+  k_depth_verify<<<296, 256, 0, s>>>(k32[1], w.val_depth[0], w.key_depth[0], &fs->stats.M, fs);
 #endif
   *launches += 5;
 }

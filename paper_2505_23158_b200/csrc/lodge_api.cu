@@ -116,6 +116,10 @@ static int ensure_M(lodge_ctx *c, int64_t need) {
   int64_t ncap = std::max<int64_t>(std::max<int64_t>(need, w.M_cap + w.M_cap / 2), 4096);
   cudaFree(w.key_depth[0]); cudaFree(w.key_depth[1]);
   cudaFree(w.val_depth[0]); cudaFree(w.val_depth[1]);
+  cudaFree(w.sel_keys); cudaFree(w.sel_vals);
+  for (int q = 0; q < 4; ++q) cudaFree(w.sort_scr[q]);
+  w.sel_keys = w.sel_vals = nullptr;
+  for (int q = 0; q < 4; ++q) w.sort_scr[q] = nullptr;
   cudaFree(w.rect); cudaFree(w.payload); cudaFree(w.precise);
   cudaFree(w.rect_sorted); cudaFree(w.splat_off); cudaFree(w.vrank);
   w.vrank = nullptr;
@@ -126,6 +130,13 @@ static int ensure_M(lodge_ctx *c, int64_t need) {
   CK(cudaMalloc(&w.key_depth[1], 8 * ncap));
   CK(cudaMalloc(&w.val_depth[0], 4 * ncap));
   CK(cudaMalloc(&w.val_depth[1], 4 * ncap));
+  CK(cudaMalloc(&w.sel_keys, 4 * ncap));
+  CK(cudaMalloc(&w.sel_vals, 4 * ncap));
+  for (int q = 0; q < 4; ++q) CK(cudaMalloc(&w.sort_scr[q], 4 * ncap));
+  if (!w.sel_hist) {
+    CK(cudaMalloc(&w.sel_hist, 4 * (size_t)SEL_BINS));
+    CK(cudaMemset(w.sel_hist, 0, 4 * (size_t)SEL_BINS));  // re-zeroed by k_sel_scan
+  }
   CK(cudaMalloc(&w.rect, 8 * ncap));
   CK(cudaMalloc(&w.payload, sizeof(Payload) * ncap));
   CK(cudaMalloc(&w.precise, sizeof(Precise) * ncap));
@@ -318,7 +329,9 @@ void lodge_destroy(lodge_ctx *c) {
                   w.status, w.union_idx, w.union_tag, c->fs, c->cam_dev, w.rect_sorted,
                   w.splat_off, w.chunk_first, w.tile_order, w.tile_diff_a, w.count_all,
                   w.tile_start_b, w.tile_order_b, w.alive, w.sat, w.state, w.vrank,
-                  w.bl_start, w.bl_len, w.bl_live, w.srgb_thr, c->edges_dev};
+                  w.bl_start, w.bl_len, w.bl_live, w.srgb_thr, w.sel_hist, w.sel_keys,
+                  w.sel_vals, w.sort_scr[0], w.sort_scr[1], w.sort_scr[2], w.sort_scr[3],
+                  c->edges_dev};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c->cam_host) cudaFreeHost(c->cam_host);
@@ -597,17 +610,27 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
   ++nl;
   DSYNC("launch_project_frame");
   c->mark(3);
-  launch_depth_sort(w, c->fs, U_cap, &nl, s, true);
+  const bool two = two_phase(c, W, H, flags, out);
+  const uint32_t budget =
+      (uint32_t)std::min<int64_t>((int64_t)c->phase_budget * tiles_x * tiles_y, 0x7fffffff);
+  if (two) {
+    // two-phase frames sort only the first phase's candidates
+    launch_depth_select(w, c->fs, U_cap, budget, s);
+    launch_subset_sort(w, c->fs, U_cap, &c->fs->n_cand, w.sel_keys, w.sel_vals, w.sort_scr[0],
+                       w.sort_scr[1], w.sort_scr[2], w.sort_scr[3], w.val_depth[0], TK_DEPTH0,
+                       &nl, s);
+    nl += 3;
+  } else {
+    launch_depth_sort(w, c->fs, U_cap, &nl, s, true);
+  }
   DSYNC("launch_depth_sort");
   DSYNC_L(2, "segment: select .. depth sort");
   c->mark(4);
-  if (two_phase(c, W, H, flags, out)) {
+  if (two) {
     // FAST frames in two depth phases: the splats whose pairs
     // start within the budget are binned, sorted and composited first; the
     // tiles that still have live pixels then receive the rest of their pairs
-    const uint32_t budget = (uint32_t)std::min<int64_t>(
-        (int64_t)c->phase_budget * tiles_x * tiles_y, 0x7fffffff);
-    launch_dup_count(w, c->fs, tiles_x, tiles_y, U_cap, budget, s);
+    launch_dup_count(w, c->fs, tiles_x, tiles_y, U_cap, budget, s, &c->fs->n_cand);
     DSYNC("launch_dup_count");
     // compositing records of the first phase's splats only
     launch_payload(levels, ls, w, c->fs, cam_dev, rp, shade, w.val_depth[0], &c->fs->split_S,
@@ -640,6 +663,13 @@ static int render_tail(lodge_ctx *c, const lodge_level *levels, const LevelSlots
 #ifndef LODGE_DEBUG_SKIP_PHASE2  // diagnostic builds: the frame without its second phase
     launch_setup_b(w, c->fs, tiles_x, tiles_y, s);
     DSYNC("launch_setup_b");
+    // the later splats that meet an alive tile, in depth order
+    launch_owner_filter(w, c->fs, tiles_x, U_cap, s);
+    launch_subset_sort(w, c->fs, U_cap, &c->fs->n_ocand, w.sel_keys, w.sel_vals, w.sort_scr[0],
+                       w.sort_scr[1], w.sort_scr[2], w.sort_scr[3], w.val_depth[1], TK_OSORT0,
+                       &nl, s);
+    ++nl;
+    DSYNC("launch_owner_filter + sort");
     launch_enum_b(w, c->fs, tiles_x, tiles_y, U_cap, s);
     DSYNC("launch_enum_b");
     // ... and of the later splats that meet an unfinished tile
