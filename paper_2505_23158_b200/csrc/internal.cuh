@@ -42,6 +42,7 @@ struct FrameState {
   uint32_t sel_B;                     // last candidate depth bin
   uint32_t n_ocand;                   // second-phase owners found by the filter
   uint32_t p1_g;                      // the last first-phase splat (input index) ...
+  uint32_t p1_k32;                    // ... its 32-bit depth key ...
   uint64_t p1_key;                    // ... and its fp64 depth key
   uint32_t n_sort_a, n_sort_b;        // pairs emitted and sorted per phase (0 with block lists)
   uint32_t fault_sticky;              // OR of every frame's stats.fault (lodge_fault_flags)

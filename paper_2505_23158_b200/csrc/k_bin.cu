@@ -499,10 +499,13 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
   __shared__ uint32_t s_w[DUP_THREADS / 32], s_z[DUP_THREADS / 32];
   __shared__ uint32_t s_part, s_base, s_zbase;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t n = SECOND ? (fs->stats.overflow ? 0u : fs->n_ocand) : *n_ptr;
+  // the grid is sized for the capacity: CTAs beyond the partitions leave
+  // before drawing a ticket (the others draw 0 .. partitions - 1)
+  if ((uint64_t)blockIdx.x * (DUP_THREADS * IT) >= n) return;
   if (tid == 0) s_part = atomicAdd(&fs->tickets[TK], 1u);
   __syncthreads();
   const uint32_t part = s_part;
-  const uint32_t n = SECOND ? (fs->stats.overflow ? 0u : fs->n_ocand) : *n_ptr;
   const uint32_t r0 = part * (DUP_THREADS * IT) + tid * IT;
   if (part * (DUP_THREADS * IT) >= n) return;
   uint32_t c[IT];
@@ -628,8 +631,10 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
         fs->stats.M_first = r + 1;
         fs->P_A = off + c[i];
         const uint32_t g = order[r];  // the last first-phase splat (launch_owner_filter)
+        const uint64_t fk = w.key_depth[0][g];
         fs->p1_g = g;
-        fs->p1_key = w.key_depth[0][g];
+        fs->p1_key = fk;
+        fs->p1_k32 = __float_as_uint(__double2float_rz(__longlong_as_double((long long)fk)));
       }
     }
     if (valid) {
@@ -899,13 +904,16 @@ __global__ void __launch_bounds__(256) k_owner_filter(const Work w, FrameState *
   if (fs->stats.overflow) return;
   const uint32_t S = fs->split_S;
   const uint64_t bkey = fs->p1_key;
-  const uint32_t bg = fs->p1_g;
+  const uint32_t bg = fs->p1_g, bk32 = fs->p1_k32;
   const uint32_t ax0 = fs->alive_box[0], ax1 = fs->alive_box[1], ay0 = fs->alive_box[2],
                  ay1 = fs->alive_box[3];
-  sel_compact(w, fs->stats.M, &fs->n_ocand, [&](uint32_t, uint32_t g) {
-    if (S > 0) {
-      const uint64_t fk = w.key_depth[0][g];
-      if (fk < bkey || (fk == bkey && g <= bg)) return false;  // a first-phase splat
+  sel_compact(w, fs->stats.M, &fs->n_ocand, [&](uint32_t k32, uint32_t g) {
+    if (S > 0) {  // the 32-bit key is monotone in the fp64 one: the full key only on a tie
+      if (k32 < bk32) return false;  // a first-phase splat
+      if (k32 == bk32) {
+        const uint64_t fk = w.key_depth[0][g];
+        if (fk < bkey || (fk == bkey && g <= bg)) return false;
+      }
     }
     const uint64_t rc = w.rect[g];
     const uint32_t x0 = max((uint32_t)(rc & 0xffff), ax0), x1 = min((uint32_t)((rc >> 16) & 0xffff), ax1);

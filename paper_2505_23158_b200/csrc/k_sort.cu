@@ -65,7 +65,9 @@ __global__ void __launch_bounds__(OS_THREADS, VALS ? LODGE_OS_VMINB
   Smem &S = *reinterpret_cast<Smem *>(smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t n = *n_ptr;
-  if (n == 0) return;  // e.g. a phase that kept block lists: no ticket traffic
+  // e.g. a phase that kept block lists: no ticket traffic; and CTAs beyond
+  // the partitions of a small sort leave before drawing one
+  if ((uint64_t)blockIdx.x * OS_TILE >= n) return;
   // persistent CTAs: partitions in ticket order until the keys run out
   for (;;) {
   if (tid == 0) S.misc[0] = atomicAdd(&fs->tickets[tk], 1u);
@@ -137,6 +139,7 @@ __global__ void __launch_bounds__(OS_THREADS, LODGE_OS_VMINB)
   Smem &S = *reinterpret_cast<Smem *>(smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t n = *n_ptr;
+  if ((uint64_t)blockIdx.x * TILE >= n) return;  // beyond the partitions (small sorts)
   for (;;) {  // persistent CTAs, partitions in ticket order
   if (tid == 0) S.misc[0] = atomicAdd(&fs->tickets[tk], 1u);
   __syncthreads();
