@@ -125,7 +125,10 @@ __device__ __forceinline__ uint32_t depth_key32(uint64_t k) {
 
 // One pass over 32-bit depth keys; FIRST reads the u64 keys the projection
 // wrote (at the concatenated input index), maps them and drops the culled.
-template <bool FIRST>
+#ifndef LODGE_OS_ITEMS_SUB
+#define LODGE_OS_ITEMS_SUB 8  // keys per thread of the subset sorts (few partitions: latency)
+#endif
+template <bool FIRST, int IT = LODGE_OS_ITEMS_D>
 __global__ void __launch_bounds__(OS_THREADS, LODGE_OS_VMINB)
     k_depth_pass(const uint64_t *__restrict__ kin64, const uint32_t *__restrict__ kin32,
                  uint32_t *__restrict__ kout, const uint32_t *__restrict__ vin,
@@ -133,7 +136,6 @@ __global__ void __launch_bounds__(OS_THREADS, LODGE_OS_VMINB)
                  const uint32_t *__restrict__ digit_off, uint64_t *status, FrameState *fs,
                  int tk) {
   extern __shared__ __align__(16) uint8_t smem[];
-  constexpr int IT = LODGE_OS_ITEMS_D;
   constexpr uint32_t TILE = OS_THREADS * IT;
   using Smem = OSmem<IT, true, uint32_t, 256>;
   Smem &S = *reinterpret_cast<Smem *>(smem);
@@ -488,25 +490,24 @@ void launch_list_verify(const Work &w, FrameState *fs, uint32_t T, bool second,
 // Frames: four passes over 32-bit keys (u32 ping-pong in the two halves of
 // key_depth[1]; key_depth[0] keeps the full keys by input index for the tie
 // repair), sorted input indices in val_depth[0].
-void launch_subset_sort(const Work &w, FrameState *fs, int64_t cap, const uint32_t *n_ptr,
+template <int IT>
+static void subset_sort(const Work &w, FrameState *fs, int64_t cap, const uint32_t *n_ptr,
                         const uint32_t *kin, const uint32_t *vin, uint32_t *ks0, uint32_t *ks1,
                         uint32_t *vs0, uint32_t *vs1, uint32_t *vout, int tk0,
                         int32_t *launches, cudaStream_t s) {
-  if (cap <= 0) return;
   cudaMemsetAsync(fs->hist_depth, 0, sizeof(uint32_t) * 4 * 256, s);  // (a frame may sort twice)
   int hist_blocks = (int)((cap + 2047) / 2048);
   if (hist_blocks > 148 * 2) hist_blocks = 148 * 2;
   k_depth_hist32<true><<<hist_blocks, 256, 0, s>>>(nullptr, kin, n_ptr, fs);
   k_depth_scan<<<1, 256, 0, s>>>(fs);
   *launches += 2;
-  constexpr int64_t TILE = (int64_t)OS_THREADS * LODGE_OS_ITEMS_D;
-  const size_t sm = sizeof(OSmem<LODGE_OS_ITEMS_D, true, uint32_t, 256>);
+  constexpr int64_t TILE = (int64_t)OS_THREADS * IT;
+  const size_t sm = sizeof(OSmem<IT, true, uint32_t, 256>);
   static PerDevice res;
   if (!res()) {
-    cudaFuncSetAttribute(k_depth_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k_depth_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_depth_pass<false, IT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
-    res() = resident_grid(k_depth_pass<true>, OS_THREADS, sm, 1 << 30);
+    res() = resident_grid(k_depth_pass<false, IT>, OS_THREADS, sm, 1 << 30);
   }
   const unsigned grid = (unsigned)std::min<int64_t>((cap + TILE - 1) / TILE,
                                                     LODGE_PERSIST ? res() : 0x7fffffff);
@@ -517,9 +518,9 @@ void launch_subset_sort(const Work &w, FrameState *fs, int64_t cap, const uint32
   const uint32_t *vi[4] = {vin, vs0, vs1, vs0};
   uint32_t *vo[4] = {vs0, vs1, vs0, vs1};
   for (int p = 0; p < 4; ++p) {
-    k_depth_pass<false><<<grid, OS_THREADS, sm, s>>>(nullptr, ki[p], ko[p], vi[p], vo[p], n_ptr,
-                                                     8 * p, fs->off_depth[p], w.status, fs,
-                                                     tk0 + p);
+    k_depth_pass<false, IT><<<grid, OS_THREADS, sm, s>>>(nullptr, ki[p], ko[p], vi[p], vo[p],
+                                                         n_ptr, 8 * p, fs->off_depth[p],
+                                                         w.status, fs, tk0 + p);
 #ifdef LODGE_VERIFY
     k_pass_verify<<<296, 256, 0, s>>>(ko[p], vo[p], w.key_depth[0], n_ptr, 8 * p, p, fs);
 #endif
@@ -530,6 +531,21 @@ void launch_subset_sort(const Work &w, FrameState *fs, int64_t cap, const uint32
   k_depth_verify<<<296, 256, 0, s>>>(ks1, vout, w.key_depth[0], n_ptr, fs);
 #endif
   *launches += 5;
+}
+
+void launch_subset_sort(const Work &w, FrameState *fs, int64_t cap, const uint32_t *n_ptr,
+                        const uint32_t *kin, const uint32_t *vin, uint32_t *ks0, uint32_t *ks1,
+                        uint32_t *vs0, uint32_t *vs1, uint32_t *vout, int tk0,
+                        int32_t *launches, cudaStream_t s) {
+  if (cap <= 0) return;
+  // all survivors of a one-pass frame: the large-partition passes; a two-phase
+  // frame's candidates and owners (a few partitions): small ones
+  if (n_ptr == &fs->stats.M)
+    subset_sort<LODGE_OS_ITEMS_D>(w, fs, cap, n_ptr, kin, vin, ks0, ks1, vs0, vs1, vout, tk0,
+                                  launches, s);
+  else
+    subset_sort<LODGE_OS_ITEMS_SUB>(w, fs, cap, n_ptr, kin, vin, ks0, ks1, vs0, vs1, vout, tk0,
+                                    launches, s);
 }
 
 // Frames: four passes over 32-bit keys (u32 ping-pong in the two halves of
