@@ -195,12 +195,14 @@ class Clocks:
 # algorithmic bytes per stage
 # ---------------------------------------------------------------------------
 def stage_bytes(U, AB, M, P, W, H, sh_terms, geom_bytes=48, sh_elem=4, P1=None, P2=0.0,
-                M1=None, M2=0.0, bl1=0.0, bl2=0.0):
+                M1=None, M2=0.0, bl1=0.0, bl2=0.0, C=None):
     """Algorithmic bytes per frame of each stage.
-    Two-phase frames (P1 = pairs of the first depth phase < P): tile_setup is
-    the counting pass, duplicate / tile_sort / composite the first phase,
-    second_phase the enumeration, compaction and sort (or block lists) of the
-    P2 pairs the unfinished tiles still need, composite_b their compositing.
+    Two-phase frames (P1 = pairs of the first depth phase < P): the depth
+    stage selects and sorts the C first-phase candidates,
+    tile_setup is their counting pass, duplicate / tile_sort / composite the
+    first phase, second_phase the owner filter over the survivors, the owner
+    sort and the lists (sorted pairs or block lists) of the P2 pairs the
+    unfinished tiles still need, composite_b their compositing.
     bl1 / bl2: the fraction of frames whose first / second phase kept block
     lists (stats.block_lists): no pairs emitted or sorted; the block-list
     pass reads each splat's rectangle and id (12 B) and writes at least one
@@ -209,30 +211,36 @@ def stage_bytes(U, AB, M, P, W, H, sh_terms, geom_bytes=48, sh_elem=4, P1=None, 
     two = P1 is not None and (P1 < P or P2 > 0)
     P1 = P if P1 is None else P1
     M1 = M if (M1 is None or not two) else M1
-    count = M * (4.0 + 8.0 + 8.0 + 4.0)  # order + rect in, rect + offset out
+    C = M if (C is None or not two) else C
+    # a sort of n (32-bit key, index) pairs: histogram read, four passes
+    # reading and writing key + index, the tie repair reading keys and
+    # indices and writing indices
+    sort = lambda n: n * 4.0 + 4 * n * 16.0 + n * 12.0  # noqa: E731
+    count = C * (4.0 + 8.0 + 8.0 + 4.0)  # order + rect in, rect + offset out
     # k_payload: id, geometry and SH in, payload + fp64 record out, per
     # composited splat
     payload = 4.0 + 8.0 + geom_bytes + sh_b + 128.0
     blk = lambda m: m * (12.0 + 8.0)  # noqa: E731
+    # candidate selection: the histogram reads key, index and rectangle of
+    # every survivor, the compaction key and index and writes the candidates
+    select = (M * 16.0 + M * 8.0 + C * 8.0) if two else 0.0
     return {
         "select": 0.0,
         "union": 4.0 * AB + 5.0 * U,
         # geometry only: union slot + record in; per survivor the full key and
         # rectangle by index and the compacted (32-bit key, index) out
         "project": U * (5.0 + geom_bytes) + M * 24.0,
-        # histogram of the M compacted keys, four passes reading and writing
-        # M x (key + index), the tie repair reading keys and indices, writing
-        # indices
-        "depth_sort": M * 4.0 + 4 * M * 16.0 + M * 12.0,
+        "depth_sort": select + sort(C),
         "tile_setup": (count if two else 0.0) + M1 * payload,
         "duplicate": (1.0 - bl1) * P1 * 8.0 if two else M * 12.0 + P * 8.0,
         # pass 1 reads u64 pairs, writes packed u32; pass 2 reads and writes u32
         "tile_sort": (1.0 - bl1) * (8.0 + 4.0 + 4.0 + 4.0) * P1 + bl1 * blk(M1),
         "composite": P1 * 4.0 + M1 * 64.0 + W * H * 16.0 + U * 4.0,
-        # owner scan over the later splats' rectangles, their compositing
-        # records, the emitted pairs (8 B) and their two tile passes (20 B)
-        "second_phase": (M * 8.0 + M2 * payload + (1.0 - bl2) * P2 * (8.0 + 20.0)
-                         + bl2 * blk(M2)) if two else 0.0,
+        # owner filter (key, index, rectangle per survivor; owners out), the
+        # owner sort, the owners' counting pass and compositing records, the
+        # emitted pairs (8 B) and their two tile passes (20 B) or block lists
+        "second_phase": (M * 16.0 + M2 * 8.0 + sort(M2) + M2 * 24.0 + M2 * payload
+                         + (1.0 - bl2) * P2 * (8.0 + 20.0) + bl2 * blk(M2)) if two else 0.0,
         "composite_b": (P2 * 4.0 + M2 * 64.0) if two else 0.0,
     }
 
@@ -559,8 +567,9 @@ def run_lodge(args):
     M1, M2 = mean(lambda s: s.M_first), mean(lambda s: s.M_second)
     bl1 = mean(lambda s: s.block_lists & 1)
     bl2 = mean(lambda s: (s.block_lists >> 1) & 1)
+    Cs = mean(lambda s: s.sorted_first)
     sb = stage_bytes(U, AB, M, P, W, H, (cfg.degree + 1) ** 2, P1=P1, P2=P2, M1=M1, M2=M2,
-                     bl1=bl1, bl2=bl2)
+                     bl1=bl1, bl2=bl2, C=Cs)
     peak, peak_kind = load_peaks()
     stages = {}
     for i, name in enumerate(N.STAGES):
@@ -786,6 +795,7 @@ def run_lodge(args):
                     "mean_P_phase": [round(P1), round(P2)],
                     "mean_M_composited": [round(M1), round(M2)],
                     "block_list_frames": [round(bl1, 3), round(bl2, 3)],
+                    "mean_sorted": [round(Cs), round(M2)],
                     "levels": cfg.n_gaussians(), "chunks": cfg.K,
                     "pairs_per_s": P * value, "gaussians_per_s": U * value,
                     "overflow_frames": overflow_all, "fault_frames": faults_all,

@@ -151,6 +151,9 @@ typedef struct {
                             T < t_min, or its whole list (SURVEY.md 8d m_t) */
   uint32_t block_lists;  /* two-phase frames: bit 0 (1) the first phase, bit 1 (2) the
                             second kept block lists instead of sorted per-tile lists */
+  uint32_t sorted_first; /* survivors depth-sorted for the first (or only) phase: M in
+                            one pass, the first-phase candidates in two phases (the
+                            second phase sorts its M_second owners) */
 } lodge_frame_stats;
 
 /* ---- context ---------------------------------------------------------- */

@@ -72,7 +72,8 @@ class FrameStats(C.Structure):
                 ("P", C.c_uint32), ("overflow", C.c_uint32), ("guard_hits", C.c_uint32),
                 ("P_first", C.c_uint32), ("P_second", C.c_uint32), ("fault", C.c_uint32),
                 ("M_first", C.c_uint32), ("M_second", C.c_uint32),
-                ("comp_members", C.c_uint32), ("block_lists", C.c_uint32)]
+                ("comp_members", C.c_uint32), ("block_lists", C.c_uint32),
+                ("sorted_first", C.c_uint32)]
 
 
 class Batch(C.Structure):

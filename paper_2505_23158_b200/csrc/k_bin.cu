@@ -611,6 +611,7 @@ __global__ void __launch_bounds__(DUP_THREADS) k_dup_count(const uint32_t *__res
     if (valid && r == n - 1) {  // totals: owners and pairs
       const uint32_t nq = SECOND ? k + (c[i] ? 1u : 0u) : n;
       w.splat_off[nq] = off + c[i];
+      if (!SECOND) fs->stats.sorted_first = n;
       if (SECOND) {
         fs->n_owners_b = nq;
         fs->stats.M_second = nq;

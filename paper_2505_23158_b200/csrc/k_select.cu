@@ -528,6 +528,7 @@ __global__ void k_begin_frame(FrameState *fs) {
     fs->stats.M_second = 0;
     fs->stats.comp_members = 0;
     fs->stats.block_lists = 0;
+    fs->stats.sorted_first = 0;
     fs->split_S = 0;
     fs->P_A = 0;
     fs->n_alive = 0;
