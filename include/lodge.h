@@ -173,8 +173,8 @@ int lodge_set_phase_budget(lodge_ctx *ctx, int32_t pairs_per_tile);
 /* Block lists: a depth phase of few large splats keeps, per
  * block of 8 x 4 tiles, its depth-ordered splats with tile masks instead of
  * emitting and sorting its pairs.  AUTO decides per frame on the device
- * (<= 64k splats averaging >= 64 tiles); FORCE uses them whenever the phase
- * has <= 64k splats (second phase: owners); OFF never.  Outputs are the same
+ * (<= 128k splats averaging >= 64 tiles); FORCE uses them whenever the phase
+ * has <= 128k splats (second phase: owners); OFF never.  Outputs are the same
  * in every mode; lodge_frame_stats.block_lists reports the choice. */
 #define LODGE_BLOCK_LISTS_AUTO 0
 #define LODGE_BLOCK_LISTS_OFF 1

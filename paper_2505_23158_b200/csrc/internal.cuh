@@ -81,7 +81,10 @@ enum Ticket {
 constexpr int BLK_W = LODGE_BLK_W, BLK_H = LODGE_BLK_H;
 static_assert(BLK_W * BLK_H <= 32 && BLK_W <= 16, "tile masks fit 32 bits");
 constexpr int BL_CHUNK = 1024;
-constexpr int BL_CHMAX = 64;
+#ifndef LODGE_BL_CHMAX
+#define LODGE_BL_CHMAX 128
+#endif
+constexpr int BL_CHMAX = LODGE_BL_CHMAX;
 __host__ __device__ inline int32_t block_count(int32_t tiles_x, int32_t tiles_y) {
   return ((tiles_x + BLK_W - 1) / BLK_W) * ((tiles_y + BLK_H - 1) / BLK_H);
 }
