@@ -2,7 +2,7 @@
 compositor's block walk in csrc/k_composite.cu) give bitwise the outputs of
 sorted per-tile lists -- image, per_pixel_visible, per_tile_count, max
 weights, P and M.  lodge_set_block_lists FORCE takes them for every phase
-that fits (<= 64k splats) whatever the splat sizes, OFF never: the street
+that fits (<= 128k splats) whatever the splat sizes, OFF never: the street
 sweep at 1080p for budgets from one pair per tile to more than P, an odd
 resolution (partial blocks on the right and bottom edges), a frame smaller
 than one block, LOD and full modes, and frames in flight.  The one-pass
@@ -54,9 +54,9 @@ def test_forced_block_lists_equal_sorted_lists(street, budget, z):
     assert_same(outputs(fro, sto), ref)
     assert stf.fault == 0 and sto.fault == 0
     assert sto.block_lists == 0
-    if stf.M_first <= 65536 and stf.P_first > 0:
+    if stf.M_first <= 131072 and stf.P_first > 0:
         assert stf.block_lists & 1  # the first phase took block lists
-    if stf.M_second and stf.M_second <= 65536:
+    if stf.M_second and stf.M_second <= 131072:
         assert stf.block_lists & 2
 
 
