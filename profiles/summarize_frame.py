@@ -23,11 +23,11 @@ from summarize_ncu import launches  # noqa: E402
 
 STAGE_OF = [
     ("k_begin_frame", "select"), ("k_select_frame", "select"),
+    ("k_sel_hist", "depth_sort"), ("k_sel_scan", "depth_sort"), ("k_sel_compact", "depth_sort"),
+    ("k_owner_filter", "second_phase"),
     ("k_union_check", "union"), ("k_union_split", "union"), ("k_union_merge", "union"),
     ("k_union_sizes", "union"),
     ("k_project_frame", "project"),
-    ("k_depth_hist", "depth_sort"), ("k_depth_scan", "depth_sort"),
-    ("k_depth_pass", "depth_sort"), ("k_depth_ties", "depth_sort"),
     ("k_dup_count<0>", "tile_setup"), ("k_payload", "tile_setup"), ("k_tile_setup", "tile_setup"),
     ("k_dup_emit", "duplicate"),
     ("k_block_lists<1>", "tile_sort"),
@@ -39,7 +39,16 @@ STAGE_OF = [
 ]
 
 
+SORT_KERNELS = ("k_depth_hist", "k_depth_scan", "k_depth_pass", "k_depth_ties")
+
+
 def stage_of(name, state):
+    # two-phase frames sort twice: the first-phase candidates (depth_sort)
+    # and, after k_owner_filter, the second-phase owners (second_phase)
+    if any(k in name for k in SORT_KERNELS):
+        return "second_phase" if state.get("owners") else "depth_sort"
+    if "k_owner_filter" in name:
+        state["owners"] = True
     if "k_onesweep" in name:
         state["tile_passes"] += 1
         return "tile_sort" if state["tile_passes"] <= 2 else "second_phase"
@@ -59,7 +68,7 @@ def main():
     ap.add_argument("--table")
     a = ap.parse_args()
     ls = launches(a.rep)
-    state = {"tile_passes": 0, "payloads": 0}
+    state = {"tile_passes": 0, "payloads": 0, "owners": False}
     per = {}
     rows = []
     for l in ls:
