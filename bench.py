@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--views-per-step", type=int, default=BLOCK)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--streams", type=int, default=4,
+    ap.add_argument("--streams", type=int, default=8,
                     help="frames in flight per GPU (one liblodge context + stream each)")
     ap.add_argument("--cpu-views", type=int, default=1, help="views in the CPU baseline sample")
     ap.add_argument("--residency", default="full", choices=["full", "stream"],
@@ -69,7 +69,7 @@ def parse():
                     help="full residency layout: flat level arrays, or chunk slabs (every "
                          "chunk's records contiguous in set order; paper_2505_23158_b200."
                          "device.SlabStore)")
-    ap.add_argument("--phase-budget", type=int, default=2048,
+    ap.add_argument("--phase-budget", type=int, default=1536,
                     help="FAST frames: first-phase pairs per tile of the two depth phases "
                          "(lodge_set_phase_budget); 0 = one pass over the full lists")
     ap.add_argument("--exact-steps", type=int, default=2,

@@ -168,7 +168,7 @@ int lodge_reserve(lodge_ctx *ctx, int64_t max_splats, int64_t max_pairs);
  * start within pairs_per_tile * T of the pair sequence are binned, sorted and
  * composited first; only the tiles left with live pixels receive, sort and
  * composite the rest of their pairs.  Outputs are bitwise those of one pass.
- * 0 disables (every frame one pass); default 2048. */
+ * 0 disables (every frame one pass); default 1536. */
 int lodge_set_phase_budget(lodge_ctx *ctx, int32_t pairs_per_tile);
 /* Block lists: a depth phase of few large splats keeps, per
  * block of 8 x 4 tiles, its depth-ordered splats with tile masks instead of

@@ -87,7 +87,7 @@ struct lodge_ctx {
   Work w{};
   int64_t tiles_cap = 0;  // capacity of tile_start (T+1) and diff
   int64_t pixels_cap = 0;  // capacity of the two-phase pixel state
-  int32_t phase_budget = 2048;  // first-phase pairs per tile of two-phase frames (0: one pass)
+  int32_t phase_budget = 1536;  // first-phase pairs per tile of two-phase frames (0: one pass)
   int32_t block_lists = LODGE_BLOCK_LISTS_AUTO;  // lodge_set_block_lists
   int debug_sync = 0;  // LODGE_DEBUG_SYNC=1: check after every stage; 2: after each segment
   int32_t launches = 0;

@@ -62,7 +62,7 @@ class Renderer:
 
     def __init__(self, levels: Sequence, plan, device=None, storage: str = "fp32",
                  precision: str = "fast", raster_cfg: RasterConfig = RasterConfig(),
-                 n_streams: int = 1, full_lists: bool = False, phase_budget: int = 2048,
+                 n_streams: int = 1, full_lists: bool = False, phase_budget: int = 1536,
                  block_lists: str = "auto"):
         self.ctx = context(device)
         self.device = self.ctx.device

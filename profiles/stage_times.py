@@ -21,7 +21,7 @@ def main():
     ap.add_argument("--config", default="config3")
     ap.add_argument("--frames", type=int, default=64)
     ap.add_argument("--store", default="flat", choices=["flat", "slab"])
-    ap.add_argument("--phase-budget", type=int, default=2048)
+    ap.add_argument("--phase-budget", type=int, default=1536)
     a = ap.parse_args()
     import torch
 

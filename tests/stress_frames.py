@@ -31,7 +31,7 @@ FAULT_BITS = {1: "owners", 2: "compact", 4: "scatter", 8: "list", 16: "tile", 32
               64: "depth_order", 128: "member", 256: "src", 512: "list_order"}
 
 
-def run(config="config3", streams=4, frames=432, reps=1, phase_budget=2048, views=4096,
+def run(config="config3", streams=4, frames=432, reps=1, phase_budget=1536, views=4096,
         seed_views=0, cfg=None):
     import numpy as np
     import torch
@@ -124,7 +124,7 @@ def main():
     ap.add_argument("--streams", type=int, default=4)
     ap.add_argument("--frames", type=int, default=432)
     ap.add_argument("--reps", type=int, default=1)
-    ap.add_argument("--phase-budget", type=int, default=2048)
+    ap.add_argument("--phase-budget", type=int, default=1536)
     ap.add_argument("--seed", type=int, default=0)
     a = ap.parse_args()
     res = run(a.config, a.streams, a.frames, a.reps, a.phase_budget, seed_views=a.seed)

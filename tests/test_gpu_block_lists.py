@@ -42,7 +42,7 @@ def renderer(street, mode, budget, **kw):
                       block_lists=mode, **kw)
 
 
-@pytest.mark.parametrize("budget", [1, 40, 300, 2048, 1 << 20])
+@pytest.mark.parametrize("budget", [1, 40, 300, 1536, 2048, 1 << 20])
 @pytest.mark.parametrize("z", [6.0, 47.0, 118.0])
 def test_forced_block_lists_equal_sorted_lists(street, budget, z):
     cfg, levels, plan, one = street

@@ -45,7 +45,7 @@ def assert_same(a, b):
         assert np.array_equal(a[k], b[k]), k
 
 
-@pytest.mark.parametrize("budget", [1, 40, 300, 1280, 2048, 1 << 20])
+@pytest.mark.parametrize("budget", [1, 40, 300, 1280, 1536, 2048, 1 << 20])
 @pytest.mark.parametrize("z", [6.0, 47.0, 118.0])
 def test_two_phase_equals_one_pass(street, budget, z):
     cfg, levels, plan, one = street
