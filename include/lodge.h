@@ -170,6 +170,11 @@ int lodge_reserve(lodge_ctx *ctx, int64_t max_splats, int64_t max_pairs);
  * composite the rest of their pairs.  Outputs are bitwise those of one pass.
  * 0 disables (every frame one pass); default 1536. */
 int lodge_set_phase_budget(lodge_ctx *ctx, int32_t pairs_per_tile);
+/* Frames in flight on several contexts: the projection's and
+ * the record gather's persistent grids use at most ctas_per_sm CTAs per SM
+ * (0: their single-frame default, 3 and 4), leaving room on every SM for the
+ * other contexts' kernels.  Outputs are the same for every value. */
+int lodge_set_grid_share(lodge_ctx *ctx, int32_t ctas_per_sm);
 /* Block lists: a depth phase of few large splats keeps, per
  * block of 8 x 4 tiles, its depth-ordered splats with tile masks instead of
  * emitting and sorting its pairs.  AUTO decides per frame on the device

@@ -87,6 +87,7 @@ EXPORTS = {
     "lodge_create": ([C.c_int32, C.POINTER(C.c_void_p)], C.c_int),
     "lodge_set_phase_budget": ([C.c_void_p, C.c_int32], C.c_int),
     "lodge_set_block_lists": ([C.c_void_p, C.c_int32], C.c_int),
+    "lodge_set_grid_share": ([C.c_void_p, C.c_int32], C.c_int),
     "lodge_fault_flags": ([C.c_void_p, C.POINTER(C.c_uint32)], C.c_int),
     "lodge_destroy": ([C.c_void_p], None),
     "lodge_last_error": ([], C.c_char_p),

@@ -69,6 +69,13 @@ enum Ticket {
   TK_OSORT0 = 26,  // second-phase owner sort passes (.. TK_OSORT0 + 3)
 };
 
+// Persistent (ticketed) grids: at most this many CTAs per SM, below the
+// occupancy limit, so the frames in flight on other streams keep room on
+// every SM
+#ifndef LODGE_PERSIST_PER
+#define LODGE_PERSIST_PER 64
+#endif
+
 // Block lists: blocks of BLK_W x BLK_H tiles (tile bit (y % BLK_H) * BLK_W +
 // x % BLK_W of an entry's mask), scanned in chunks of BL_CHUNK splats, at
 // most BL_CHMAX chunks (a phase uses block lists only below that many splats).
@@ -116,6 +123,7 @@ static_assert(sizeof(Precise) == 64, "precise record must be 64 B");
 
 // Workspace pointers handed to kernels.
 struct Work {
+  int32_t grid_share = 0;   // lodge_set_grid_share: persistent CTAs per SM (0: default)
   uint64_t *key_depth[2];   // M_cap each (ping-pong)
   uint32_t *val_depth[2];   // M_cap each
   uint64_t *rect;           // M_cap packed x0|x1<<16|y0<<32|y1<<48

@@ -988,6 +988,7 @@ static int64_t resident_ctas(K kernel, int threads) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, 0);
+  per = std::min(per, LODGE_PERSIST_PER);
   return (int64_t)std::max(per, 1) * std::max(sms, 1);
 }
 
@@ -1051,6 +1052,7 @@ void launch_enum_b(const Work &w, FrameState *fs, int32_t tiles_x, int32_t tiles
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_emit_b, DUP_THREADS, sm);
+    per = std::min(per, LODGE_PERSIST_PER);
     res() = (int64_t)std::max(per, 1) * std::max(sms, 1);
   }
   const int64_t resident = res();

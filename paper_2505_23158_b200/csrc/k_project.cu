@@ -856,7 +856,8 @@ template <typename GT, typename ST>
 static void launch_pf(ProjLevels lv, const Work &w, FrameState *fs,
                       const lodge_camera *cam, const lodge_raster_params &rp, uint32_t nslots,
                       int32_t tiles_x, int32_t tiles_y, cudaStream_t s) {
-  const uint32_t want = (nslots + 255) / 256, cap = LODGE_PROJ_MINB * (uint32_t)sm_count();
+  const uint32_t per = w.grid_share > 0 ? std::min(w.grid_share, LODGE_PROJ_MINB) : LODGE_PROJ_MINB;
+  const uint32_t want = (nslots + 255) / 256, cap = per * (uint32_t)sm_count();
   const int64_t bytes = 4ll * (tiles_x + 1) * (tiles_y + 1);
   lv.diff_in_smem = bytes <= PROJ_DIFF_SMEM_MAX ? 1 : 0;
   const size_t sm = lv.diff_in_smem ? (size_t)bytes : 0;
@@ -874,7 +875,8 @@ template <typename GT, typename ST>
 static void launch_pl(const ProjLevels &lv, const Work &w, FrameState *fs,
                       const lodge_camera *cam, const lodge_raster_params &rp, int32_t shade,
                       const uint32_t *ids, const uint32_t *n_ptr, int64_t n_cap, cudaStream_t s) {
-  const int64_t want = (n_cap + 255) / 256, cap = 4 * (int64_t)sm_count();
+  const int64_t per = w.grid_share > 0 ? std::min(w.grid_share, 4) : 4;  // CTAs per SM
+  const int64_t want = (n_cap + 255) / 256, cap = per * (int64_t)sm_count();
   k_payload<GT, ST><<<(unsigned)std::max<int64_t>(1, std::min(want, cap)), 256, 0, s>>>(
       lv, w, fs, cam, rp, shade, ids, n_ptr);
 }

@@ -286,6 +286,7 @@ static unsigned resident_grid(K kernel, int threads, size_t smem, int64_t need) 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+  per = std::min(per, LODGE_PERSIST_PER);
   const int64_t r = (int64_t)std::max(per, 1) * std::max(sms, 1);
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, r));
 }

@@ -352,6 +352,13 @@ int lodge_set_phase_budget(lodge_ctx *c, int32_t pairs_per_tile) {
   return 0;
 }
 
+int lodge_set_grid_share(lodge_ctx *c, int32_t ctas_per_sm) {
+  if (!c) return set_err(LODGE_ERR_BAD_ARG, "ctx is NULL");
+  if (ctas_per_sm < 0) return set_err(LODGE_ERR_BAD_ARG, "CTAs per SM must be >= 0");
+  c->w.grid_share = ctas_per_sm;
+  return 0;
+}
+
 int lodge_set_block_lists(lodge_ctx *c, int32_t mode) {
   if (!c) return set_err(LODGE_ERR_BAD_ARG, "ctx is NULL");
   if (mode < LODGE_BLOCK_LISTS_AUTO || mode > LODGE_BLOCK_LISTS_FORCE)

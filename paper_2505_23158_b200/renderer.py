@@ -58,12 +58,15 @@ class Renderer:
     keeps one pass so the sorted per-tile lists stay inspectable
     (lodge_frame_lists).  block_lists ("auto", "off", "force";
     lodge_set_block_lists) chooses how a phase of few large splats builds
-    its lists.  The outputs are the same either way."""
+    its lists.  grid_share (lodge_set_grid_share; default 1 CTA per SM with
+    several slots, 0 = the single-frame grids otherwise) caps the
+    projection's persistent grids so frames in flight share the SMs.  The
+    outputs are the same either way."""
 
     def __init__(self, levels: Sequence, plan, device=None, storage: str = "fp32",
                  precision: str = "fast", raster_cfg: RasterConfig = RasterConfig(),
                  n_streams: int = 1, full_lists: bool = False, phase_budget: int = 1536,
-                 block_lists: str = "auto"):
+                 block_lists: str = "auto", grid_share: int = None):
         self.ctx = context(device)
         self.device = self.ctx.device
         if n_streams < 1:
@@ -93,6 +96,13 @@ class Renderer:
         if block_lists not in BLOCK_LIST_MODES:
             raise ValueError("block_lists must be 'auto', 'off' or 'force'")
         self.block_lists = BLOCK_LIST_MODES[block_lists]
+        # frames in flight: the projection's persistent grids leave room on
+        # every SM for the other slots' kernels (lodge_set_grid_share)
+        if grid_share is None:
+            grid_share = 1 if n_streams > 1 else 0
+        if grid_share < 0:
+            raise ValueError("grid_share must be >= 0")
+        self.grid_share = int(grid_share)
         self.cfg = raster_cfg
         self._rp = params_struct(raster_cfg)
         lod_cap = sum(l.n for l in self.levels)
@@ -117,6 +127,7 @@ class Renderer:
                 p = ctx.bind(self.precision)
         N.check(N.lib().lodge_set_phase_budget(p, self.phase_budget), "lodge_set_phase_budget")
         N.check(N.lib().lodge_set_block_lists(p, self.block_lists), "lodge_set_block_lists")
+        N.check(N.lib().lodge_set_grid_share(p, self.grid_share), "lodge_set_grid_share")
         return p
 
     def reserve(self, max_pairs: int):

@@ -103,3 +103,25 @@ def test_forced_block_lists_frames_in_flight(street):
 def test_block_list_mode_is_validated(street):
     with pytest.raises(ValueError):
         renderer(street, "sometimes", 300)
+
+
+@pytest.mark.parametrize("share", [1, 2, 7])
+@pytest.mark.parametrize("z", [6.0, 47.0])
+def test_grid_share_same_outputs(street, share, z):
+    """lodge_set_grid_share caps the projection's and the record gather's
+    persistent grids (frames in flight); the outputs do not depend on it."""
+    cfg, levels, plan, one = street
+    cam = scenes.camera(z)
+    ref = outputs(*one.render_camera(cam))
+    base = renderer(street, "auto", 1536)
+    assert base.grid_share == 0
+    fr0, st0 = base.render_camera(cam)
+    fr, st = renderer(street, "auto", 1536, grid_share=share).render_camera(cam)
+    assert_same(outputs(fr, st), outputs(fr0, st0))
+    assert_same(outputs(fr, st), ref)
+    assert st.fault == 0
+
+
+def test_grid_share_rejects_negative(street):
+    with pytest.raises(ValueError):
+        renderer(street, "auto", 1536, grid_share=-1)

@@ -74,3 +74,6 @@ def test_c_abi_argument_checks(L):
         N.check(lib.lodge_asset_split(ctx.bind(), None, 0, 7, None, None, C.byref(bad)),
                 "lodge_asset_split")
     assert "sh degree" in lib.lodge_last_error().decode()
+    with pytest.raises(ValueError, match="CTAs per SM must be >= 0"):
+        N.check(lib.lodge_set_grid_share(ctx.bind(), -1), "lodge_set_grid_share")
+    N.check(lib.lodge_set_grid_share(ctx.bind(), 0), "lodge_set_grid_share")
