@@ -540,8 +540,11 @@ def run_lodge(args):
 
     # ---- per-stage times: the timed views re-rendered serially on one
     # stream (with frames in flight a stage's events would also span the
-    # other streams' kernels)
+    # other streams' kernels), with the single-frame persistent grids
+    # (grid_share 0: a frame alone on the GPU)
     n_stage = min(n_timed, 64)
+    share = r.grid_share
+    r.grid_share = 0
     r.profile(True, n_stage)
     k = 0
     for blk in timed:
@@ -552,8 +555,9 @@ def run_lodge(args):
     torch.cuda.synchronize()
     stage_ms, nprof_frames = r.profile_read()
     r.profile(False)
+    r.grid_share = share
     stage_timing = (f"events around each stage, {nprof_frames} of the timed views re-rendered "
-                    "serially on one stream after the timed region")
+                    "serially on one stream after the timed region, single-frame grids")
 
     # ---- per-stage roofline ----------------------------------------------
     mean = lambda f: float(np.mean([f(s) for s in stats]))  # noqa: E731
