@@ -124,8 +124,10 @@ typedef struct {
   int32_t *visible_dev;
   void *maxw_dev;
   /* optional (FAST only): the 8-bit sRGB image (h, w, 3) the compositor
-   * writes as it finishes each pixel -- byte for byte lodge_to_srgb8 of the
-   * float image, which image_dev may then leave out (NULL) */
+   * writes as it finishes each tile -- byte for byte lodge_to_srgb8 of the
+   * float image, which image_dev may then leave out (NULL).  Device memory
+   * or pinned (mapped) host memory: zero-copy read-back, in 16-byte row
+   * segments when w is a multiple of 16 and the pointer 16-byte aligned */
   uint8_t *srgb8_dev;
 } lodge_frame_out;
 

@@ -273,6 +273,40 @@ struct CompParams {
   const float *srgb_thr;
 };
 
+// The number of level thresholds <= v (lodge_to_srgb8's binary search over
+// the 255 thresholds in shared memory).
+__device__ __forceinline__ uint32_t srgb_level(const float *thr, float v) {
+  uint32_t k = 0;
+#pragma unroll
+  for (int st = 128; st >= 1; st >>= 1) k += (v >= thr[k + st]) ? st : 0;
+  return k;
+}
+
+// A finished tile's 8-bit sRGB image as 16-byte row segments (48 B per tile
+// row; the caller checks the alignment): whole sectors, so a destination in
+// pinned host memory (zero-copy read-back) takes full PCIe writes.  Kept out
+// of line: the compositor's walk compiles as without it.  Every thread of
+// the CTA calls it (one barrier).
+template <int PX, int CT>
+__device__ __noinline__ void srgb_tile_rows(PxF<PX> r, PxF<PX> g, PxF<PX> b, const float *thr,
+                                            uint8_t *t8, int lx, int ly0, int tx, int ty,
+                                            uint8_t *out, int32_t W, int32_t H) {
+#pragma unroll
+  for (int p = 0; p < PX; ++p) {
+    uint8_t *o8 = t8 + 3 * ((ly0 + 2 * p) * 16 + lx);
+    o8[0] = (uint8_t)srgb_level(thr, fminf(fmaxf(r.s[p], 0.f), 1.f));
+    o8[1] = (uint8_t)srgb_level(thr, fminf(fmaxf(g.s[p], 0.f), 1.f));
+    o8[2] = (uint8_t)srgb_level(thr, fminf(fmaxf(b.s[p], 0.f), 1.f));
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < 48; q += CT) {
+    const int row = q / 3, part = q - 3 * row, py = ty * 16 + row;
+    if (py < H)
+      *reinterpret_cast<uint4 *>(out + 3 * ((size_t)py * W + tx * 16) + 16 * part) =
+          *reinterpret_cast<const uint4 *>(t8 + 48 * row + 16 * part);
+  }
+}
+
 // MODE < 0: need_image / record_max from cpar.flags at run time (EXACT);
 // otherwise bit 0 = image, bit 1 = max weights, fixed at compile time (FAST:
 // no per-member branches on either)
@@ -1044,13 +1078,23 @@ __global__ void __launch_bounds__(CC<EXACT, PH>::CT,
     for (int st = 128; st >= 1; st >>= 1) k += (v >= thr[k + st]) ? st : 0;
     return k;
   };
+  // the 8-bit tile goes out as 16-byte row segments when the frame width
+  // keeps them aligned (srgb_tile_rows)
+#ifndef LODGE_SRGB_ROWS
+#define LODGE_SRGB_ROWS 1
+#endif
+  const bool srgb_rows = LODGE_SRGB_ROWS && srgb && (cpar.W & 15) == 0 &&
+                         (reinterpret_cast<uintptr_t>(cpar.srgb8) & 15) == 0;
+  if (srgb_rows)  // CTA-uniform
+    srgb_tile_rows<PX, CT>(cru, cgu, cbu, thr, reinterpret_cast<uint8_t *>(&S.pl[1][0]), lx, ly0,
+                           tx, ty, cpar.srgb8, cpar.W, cpar.H);
 #pragma unroll
   for (int p = 0; p < PX; ++p) {
     const int py = py0 + 2 * p;
     if (!(px < cpar.W && py < cpar.H)) continue;
     const size_t pix = (size_t)py * cpar.W + px;
     if (visible) visible[pix] = EXACT ? vis[p] : (int32_t)vf.s[p];
-    if (srgb) {  // byte for byte lodge_to_srgb8 of the clipped float image
+    if (srgb && !srgb_rows) {  // byte for byte lodge_to_srgb8 of the clipped float image
       uint8_t *o8 = cpar.srgb8 + 3 * pix;
       o8[0] = (uint8_t)level(fminf(fmaxf(cru.s[p], 0.f), 1.f));
       o8[1] = (uint8_t)level(fminf(fmaxf(cgu.s[p], 0.f), 1.f));

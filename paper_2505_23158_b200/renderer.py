@@ -194,9 +194,12 @@ class Renderer:
         pair=None: nearest two chunks chosen on device.  accumulate_max: max
         this frame's per-input weights into frame.maxw instead of resetting it
         (a device-side max over views, src/lod.py:95-131).  srgb8_out: a
-        (h, w, 3) uint8 device tensor the compositor fills with the 8-bit
-        sRGB image as it finishes each pixel (FAST; byte for byte to_srgb8 of
-        the float image, which float_image=False then skips writing)."""
+        (h, w, 3) uint8 tensor the compositor fills with the 8-bit sRGB image
+        as it finishes each tile (FAST; byte for byte to_srgb8 of the float
+        image, which float_image=False then skips writing) -- on the device,
+        or in pinned host memory (zero-copy: the image reaches the host as
+        the compositor writes it, in 16-byte row segments when the width is
+        a multiple of 16)."""
         out = N.FrameOut()
         out.image_dev = (frame.image.data_ptr()
                          if (need_image and float_image and frame.image is not None) else None)
@@ -204,6 +207,8 @@ class Renderer:
             if (srgb8_out.dtype != torch.uint8 or not srgb8_out.is_contiguous()
                     or srgb8_out.numel() != 3 * frame.width * frame.height):
                 raise ValueError("srgb8_out must be a contiguous uint8 (h, w, 3) tensor")
+            if not (srgb8_out.is_cuda or srgb8_out.is_pinned()):
+                raise ValueError("srgb8_out must be a device tensor or pinned host memory")
             out.srgb8_dev = srgb8_out.data_ptr()
         out.tile_count_dev = frame.tile_count.data_ptr()
         out.visible_dev = frame.visible.data_ptr()

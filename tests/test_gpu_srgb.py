@@ -92,3 +92,16 @@ def test_render_srgb8_out_equals_to_srgb8(budget, res):
         torch.cuda.synchronize()
         assert torch.equal(got, ref)
         assert fr2.read_stats().fault == 0
+        # zero-copy into pinned host memory (16-byte row segments at width
+        # 1920, bytes at 1277), and a device buffer off 16-byte alignment
+        host = torch.zeros((h, w, 3), dtype=torch.uint8).pin_memory()
+        r.render(cams[0], fr2, srgb8_out=host, float_image=False)
+        torch.cuda.synchronize()
+        assert torch.equal(host, ref.cpu())
+        raw = torch.zeros(h * w * 3 + 1, dtype=torch.uint8, device=dev)
+        odd = raw[1:].view(h, w, 3)
+        r.render(cams[0], fr2, srgb8_out=odd, float_image=False)
+        torch.cuda.synchronize()
+        assert torch.equal(odd, ref)
+        with pytest.raises(ValueError, match="pinned host memory"):
+            r.render(cams[0], fr2, srgb8_out=torch.zeros((h, w, 3), dtype=torch.uint8))
