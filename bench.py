@@ -663,6 +663,12 @@ def run_lodge(args):
         # frame and 8-bit image buffers double-buffered by step parity, so a
         # buffer's read-back has a whole step to finish before it is reused
         frames2 = [frames, [r.alloc_frame(W, H) for _ in range(B)]]
+        # LOD / full modes convert with a separate full-grid kernel
+        # (render_lod has no 8-bit output): writing over PCIe from it would
+        # hold every SM for the transfer, so those modes convert into HBM
+        # and read back with the copy engine
+        direct = args.mode in ("blend", "chunks")
+        img8 = None if direct else torch.empty((2, B, H, W, 3), dtype=torch.uint8, device=dev)
         img8_host = torch.empty((2, B, H, W, 3), dtype=torch.uint8).pin_memory()
         st_host = torch.empty((2, B, STATS_BYTES), dtype=torch.uint8).pin_memory()
         cams_host = cams.cpu()
@@ -695,10 +701,13 @@ def run_lodge(args):
                 fr = frames2[par][j]
                 if si >= 2:  # this buffer's read-back two steps ago is done
                     r.stream_of(q).wait_event(drained[par][j])
-                do_render(r, cam_dev[par][j], fr, q, v, srgb8=img8_host[par, j])
+                do_render(r, cam_dev[par][j], fr, q, v,
+                          srgb8=img8_host[par, j] if direct else img8[par, j])
                 ready[par][j].record(r.stream_of(q))
                 with torch.cuda.stream(copy_s[q]):
                     copy_s[q].wait_event(ready[par][j])
+                    if not direct:
+                        img8_host[par, j].copy_(img8[par, j], non_blocking=True)
                     st_host[par, j].copy_(fr.stats, non_blocking=True)
                     drained[par][j].record(copy_s[q])
             for q in range(S):
@@ -720,11 +729,14 @@ def run_lodge(args):
                "host_image_check": host_ok,
                "h2d_bytes_per_step": int(B * cams.shape[1]),
                "d2h_bytes_per_step": int(B * (H * W * 3 + STATS_BYTES)),
-               "path": "Renderer.render(srgb8_out=<pinned host tensor>): the compositor writes "
-                       "the 8-bit sRGB image (byte for byte to_srgb8, like splatlod render's "
-                       "to_uint8) straight into pinned host memory (zero-copy D2H over PCIe); "
-                       "pinned host camera upload (H2D copy) and stats read-back (D2H copy) "
-                       "every step"}
+               "path": ("Renderer.render(srgb8_out=<pinned host tensor>): the compositor writes "
+                        "the 8-bit sRGB image (byte for byte to_srgb8, like splatlod render's "
+                        "to_uint8) straight into pinned host memory (zero-copy D2H over PCIe)"
+                        if direct else
+                        "Renderer.render_lod + to_srgb8 into HBM (byte for byte like splatlod "
+                        "render's to_uint8), D2H copy of the 8-bit image")
+                       + "; pinned host camera upload (H2D copy) and stats read-back (D2H copy) "
+                         "every step"}
         if not host_ok:
             e2e["invalid"] = "the host image differs from a device re-render of the same view"
             print("[bench] e2e host image check FAILED", file=sys.stderr)
